@@ -1,0 +1,195 @@
+/*
+ * kr_engine.h — C ABI of the B200 gradient oracle (libkrcuda.so).
+ *
+ * Drop-in replacement for the reference's gradient boundary
+ *   class GradientEngine { Vec Ax(x2); Vec ATx(x1); int64 flops(); }
+ *   (/root/reference/proj/include/kronriver/solver.hpp:21-27)
+ * implemented there by FactoredEngine (solver.hpp:30-40) over
+ *   matvec          (engine.hpp:58-93)   y = (Ahat + U M^-1 V^T) x
+ *   matvecTranspose (engine.hpp:96-133)  x = (Ahat + U M^-1 V^T)^T y
+ * and of the solver step that drives it, dcfrSolve (solver.hpp:343-404)
+ * with bestResponseValue / exploitability (solver.hpp:292-331).
+ *
+ * Plain pointers and sizes only; no exceptions cross the ABI.  Status codes
+ * mirror the reference's error taxonomy (errors.hpp:11-58).  There is no CPU
+ * fallback: creating an engine without a CUDA device fails with KR_NO_DEVICE.
+ */
+#ifndef KR_ENGINE_H
+#define KR_ENGINE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:22-58 codes, plus two device-side codes. */
+enum kr_status {
+  KR_OK = 0,
+  KR_INVALID_INPUT = 1,      /* InvalidInputError  "INVALID_INPUT"      */
+  KR_PARSE = 2,              /* ParseError         "PARSE"              */
+  KR_IO = 3,                 /* IoError            "IO"                 */
+  KR_GUARD_EXCEEDED = 4,     /* GuardError         "GUARD_EXCEEDED"     */
+  KR_DEGENERATE_BELIEFS = 5, /* DegenerateBeliefsError                  */
+  KR_CONTRACT = 6,           /* ContractError      "CONTRACT"           */
+  KR_CUDA = 7,               /* CUDA runtime failure                    */
+  KR_NO_DEVICE = 8           /* no CUDA device: no CPU fallback exists  */
+};
+
+typedef struct kr_engine kr_engine;
+typedef struct kr_solver kr_solver;
+
+/* One compressed factor in the reference's storage order
+ * (Eigen::SparseMatrix compressed arrays, linalg.hpp:12-16):
+ * outer[outer_size+1], inner[nnz], val[nnz]; inner indices ascending. */
+typedef struct {
+  int64_t outer_size;
+  const int64_t* outer;
+  const int32_t* inner;
+  const double* val;
+} kr_compressed;
+
+/* Sparsification (sparsify.hpp:110-121): A = Ahat + U M^-1 V^T. */
+typedef struct {
+  int64_t rows, cols, k;
+  kr_compressed ahat; /* CSR rows x cols   */
+  kr_compressed u;    /* CSR rows x k      */
+  kr_compressed m;    /* CSC k x k, unit lower triangular */
+  kr_compressed v;    /* CSC cols x k      */
+  /* Optional layout hint: sequences per hand of the row / column player
+   * (KronPayoff::flat, kron.hpp:124-126).  0 = unknown. */
+  int32_t n1, n2;
+} kr_factors;
+
+/* Engine flags. */
+#define KR_FLAG_DEFAULT 0u
+
+/* Create an engine for one Sparsification on CUDA device `device`.
+ * Replaces FactoredEngine(const Sparsification&) (solver.hpp:32); the
+ * factors are copied to HBM, so the caller may free them afterwards. */
+int kr_engine_create(const kr_factors* f, int device, uint32_t flags, kr_engine** out);
+
+/* Block-diagonal engine over `nboards` independent Sparsifications (the
+ * chance/board dimension of a turn endgame):
+ * x and y are the per-board vectors concatenated in board order. */
+int kr_engine_create_boards(const kr_factors* boards, int nboards, int device, uint32_t flags,
+                            kr_engine** out);
+
+int kr_engine_destroy(kr_engine* e);
+
+/* rows, cols, k, nnz(ahat), nnz(u), nnz(m), nnz(v), identity(M) */
+int kr_engine_dims(const kr_engine* e, int64_t out[8]);
+
+/* GradientEngine::Ax (solver.hpp:24, engine.hpp:58): y[rows] = A x[cols].
+ * HOST buffers (pinned buffers from kr_host_alloc transfer fastest).
+ * KR_INVALID_INPUT on a size mismatch (engine.hpp:59-61), KR_CONTRACT when M
+ * is not unit lower triangular (engine.hpp:35-36). */
+int kr_engine_ax(kr_engine* e, const double* x, int64_t nx, double* y, int64_t ny);
+
+/* GradientEngine::ATx (solver.hpp:25, engine.hpp:96): x[cols] = A^T y[rows]. */
+int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t nx);
+
+/* Device-pointer variants, enqueued on `stream` (NULL = the engine's own
+ * stream); asynchronous with respect to the host. */
+int kr_engine_ax_device(kr_engine* e, const double* x_dev, double* y_dev, void* stream);
+int kr_engine_atx_device(kr_engine* e, const double* y_dev, double* x_dev, void* stream);
+
+/* GradientEngine::flops() (solver.hpp:26, 35): cumulative multiply-adds,
+ * counted with the reference rule nnz(V)+nnz(U)+nnz(Ahat)+[M!=I](nnz(M)-k)
+ * per product (engine.hpp:72,77,90-91,110-131). */
+int64_t kr_engine_flops(const kr_engine* e);
+/* multiply-adds of the last product (GradientWorkspace::flops) */
+int64_t kr_engine_last_flops(const kr_engine* e);
+
+/* The engine's CUDA stream (cudaStream_t) and device. */
+void* kr_engine_stream(const kr_engine* e);
+int kr_engine_device(const kr_engine* e);
+
+/* Kernel launches issued by this engine since creation (both directions). */
+int64_t kr_engine_launches(const kr_engine* e);
+
+/* Pinned host memory for the host-buffer entry points. */
+void* kr_host_alloc(int64_t bytes);
+void kr_host_free(void* p);
+
+/* Last error message of the calling thread, and its status code. */
+const char* kr_last_error(int* code);
+
+/* Number of CUDA devices visible (0 on a machine without a GPU). */
+int kr_device_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Solver step on the device: DCFR with alternating updates
+ * (solver.hpp:343-404), regret matching (166-194), sequence form (197-218),
+ * regret sweep (222-260), discounting (262-264), averaging (381-387), and
+ * best response / exploitability at checkpoints (292-331).
+ * ------------------------------------------------------------------------- */
+
+/* Treeplex of one player (skeleton.hpp:89-126): that player's decision nodes
+ * in preorder.  node i has parent sequence node_parent_seq[i] (0 = empty
+ * sequence) and actions action_seq[node_action_ptr[i] .. node_action_ptr[i+1])
+ * (1-based sequence ids, skeleton.hpp:84). */
+typedef struct {
+  int32_t n_seq;
+  int32_t n_nodes;
+  const int32_t* node_parent_seq;
+  const int32_t* node_action_ptr;
+  const int32_t* action_seq;
+} kr_treeplex;
+
+/* DcfrParams (solver.hpp:101-109). */
+typedef struct {
+  double alpha, beta, gamma;
+  int32_t max_iters;
+  double target_exploitability;
+  int32_t checkpoint_every;
+} kr_dcfr_params;
+
+/* Caller-owned result buffers (DcfrResult, solver.hpp:133-140).  trace_* hold
+ * up to trace_cap checkpoints; per-board arrays hold trace_cap*nboards values
+ * (checkpoint-major) when non-NULL.  avg1/avg2 receive the final average
+ * sequence-form strategies when non-NULL. */
+typedef struct {
+  int32_t iterations;
+  double exploitability;
+  int64_t gradient_flops;
+  int32_t trace_len;
+  int32_t trace_cap;
+  int32_t* trace_iter;
+  double* trace_expl;
+  double* trace_br1;        /* summed over boards */
+  double* trace_br2;
+  double* trace_board_br1;  /* [trace_cap * nboards] or NULL */
+  double* trace_board_br2;
+  double* avg1;             /* [rows] or NULL */
+  double* avg2;             /* [cols] or NULL */
+  double seconds;           /* device time of the whole solve (CUDA events) */
+} kr_dcfr_result;
+
+/* Bind a solver to an engine.  hands1[b], hands2[b]: hand counts of board b
+ * (rows = sum hands1[b] * p1->n_seq, cols = sum hands2[b] * p2->n_seq);
+ * pot = 2 * potContribution (solver.hpp:329).  The engine must outlive the
+ * solver. */
+int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2, int nboards,
+                     const int32_t* hands1, const int32_t* hands2, double pot, kr_solver** out);
+int kr_solver_destroy(kr_solver* s);
+
+/* dcfrSolve.  exploitability = sum_b (br1_b + br2_b) / 2 / pot / nboards
+ * (the chance root picks a board uniformly; nboards = 1 is the reference). */
+int kr_solver_run(kr_solver* s, const kr_dcfr_params* p, kr_dcfr_result* r);
+
+/* bestResponseValue (solver.hpp:292-321) against a HOST opponent strategy;
+ * value summed over boards (per-board values in board_values if non-NULL).
+ * KR_INVALID_INPUT on a malformed strategy (validateSequenceStrategy,
+ * solver.hpp:266-286). */
+int kr_solver_best_response(kr_solver* s, int player, const double* opp, int64_t n, double* value,
+                            double* board_values);
+
+/* Kernel launches issued by the solver (its own kernels, not the engine's). */
+int64_t kr_solver_launches(const kr_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KR_ENGINE_H */

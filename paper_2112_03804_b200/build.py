@@ -1,0 +1,77 @@
+"""Build the native libraries in-tree (they travel to the GPU box with the repo).
+
+libkrcuda.so  — CUDA kernels + the kr_* C ABI (include/kr_engine.h), sm_100a.
+libkrhost.so  — C++ host side: instance loader, payoff assembly, sparsifier,
+                bundle I/O (include/kr_host.h).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2112_03804_b200")
+LIBDIR = os.path.join(PKG, "lib")
+CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu")]
+HOST_SRC = [os.path.join(PKG, "csrc", "host", f) for f in ("kr_host.cpp",)]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+NVCC_FLAGS = [
+    "-O3", "-std=c++17",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-lineinfo",
+    # bitwise parity with the reference's x86-64 build: never contract a*b+c
+    "-fmad=false",
+    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-I", os.path.join(ROOT, "include"),
+    "-I", os.path.join(PKG, "csrc", "cuda"),
+]
+
+CXX_FLAGS = ["-std=c++20", "-O3", "-ffp-contract=off", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc", "host")]
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    deps = list(sources)
+    for d in (os.path.join(ROOT, "include"), os.path.join(PKG, "csrc", "cuda"), os.path.join(PKG, "csrc", "host")):
+        if os.path.isdir(d):
+            deps += [os.path.join(d, f) for f in os.listdir(d)]
+    return any(os.path.getmtime(s) > t for s in deps if os.path.exists(s))
+
+
+def build_cuda(force=False, verbose=False):
+    os.makedirs(LIBDIR, exist_ok=True)
+    out = os.path.join(LIBDIR, "libkrcuda.so")
+    srcs = [s for s in CUDA_SRC if os.path.exists(s)]
+    if force or _stale(out, srcs):
+        cmd = [NVCC, *NVCC_FLAGS, "-o", out, *srcs]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return out
+
+
+def build_host(force=False, verbose=False):
+    os.makedirs(LIBDIR, exist_ok=True)
+    out = os.path.join(LIBDIR, "libkrhost.so")
+    srcs = [s for s in HOST_SRC if os.path.exists(s)]
+    if not srcs:
+        return None
+    if force or _stale(out, srcs):
+        cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-o", out, *srcs]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return out
+
+
+def build_all(force=False, verbose=False):
+    return build_host(force, verbose), build_cuda(force, verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose=True)

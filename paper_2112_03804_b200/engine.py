@@ -1,0 +1,117 @@
+"""CudaEngine: the reference's GradientEngine boundary on the B200.
+
+Mirrors kronriver::FactoredEngine (solver.hpp:30-40):
+    Ax(x2)  -> A x2     (matvec, engine.hpp:58-93)
+    ATx(x1) -> A^T x1   (matvecTranspose, engine.hpp:96-133)
+    flops() -> cumulative multiply-adds (engine.hpp:16-17)
+through the C ABI of libkrcuda.so.  Errors carry the reference codes
+(InvalidInputError for size mismatches, ContractError for a bad M).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+def _factor_struct(sp, keep):
+    f = sp.factors() if hasattr(sp, "factors") else sp
+    get = (lambda k: f[k]) if isinstance(f, dict) else (lambda k: getattr(f, k))
+    rows, cols, k = int(getattr(sp, "rows", None) or get("rows")), int(getattr(sp, "cols", None) or get("cols")), \
+        int(getattr(sp, "k", None) if getattr(sp, "k", None) is not None else get("k"))
+    n1 = int(getattr(sp, "n1", 0) or (f.get("n1", 0) if isinstance(f, dict) else 0))
+    n2 = int(getattr(sp, "n2", 0) or (f.get("n2", 0) if isinstance(f, dict) else 0))
+    parts = [N.compressed(*get(name), keep) for name in ("ahat", "u", "m", "v")]
+    return N.kr_factors(rows, cols, k, *parts, n1, n2)
+
+
+class CudaEngine:
+    """GradientEngine whose products run as sm_100a kernels in HBM.
+
+    `factors` is one Sparsification-like object (attributes rows/cols/k and a
+    factors() mapping name -> (outer, inner, val) in the reference storage
+    order), or a list of them for a block-diagonal multi-board engine.
+    """
+
+    def __init__(self, factors, device=0, flags=0):
+        L = N.cuda()
+        keep = []
+        boards = factors if isinstance(factors, (list, tuple)) else [factors]
+        arr = (N.kr_factors * len(boards))(*[_factor_struct(b, keep) for b in boards])
+        h = C.c_void_p()
+        N.check(L.kr_engine_create_boards(arr, len(boards), device, flags, C.byref(h)))
+        self._h = h
+        dims = np.zeros(8, np.int64)
+        N.check(L.kr_engine_dims(self._h, N.ptr(dims)))
+        self.rows, self.cols, self.k = int(dims[0]), int(dims[1]), int(dims[2])
+        self.nnz = {"ahat": int(dims[3]), "u": int(dims[4]), "m": int(dims[5]), "v": int(dims[6])}
+        self.m_identity = bool(dims[7])
+        self.device = device
+        self.nboards = len(boards)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            N.cuda().kr_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- GradientEngine (solver.hpp:21-27) --------------------------------
+    def Ax(self, x2):
+        x = np.ascontiguousarray(x2, np.float64)
+        y = np.empty(self.rows)
+        N.check(N.cuda().kr_engine_ax(self._h, N.ptr(x), len(x), N.ptr(y), len(y)))
+        return y
+
+    def ATx(self, x1):
+        y = np.ascontiguousarray(x1, np.float64)
+        x = np.empty(self.cols)
+        N.check(N.cuda().kr_engine_atx(self._h, N.ptr(y), len(y), N.ptr(x), len(x)))
+        return x
+
+    def flops(self):
+        return int(N.cuda().kr_engine_flops(self._h))
+
+    def last_flops(self):
+        return int(N.cuda().kr_engine_last_flops(self._h))
+
+    def launches(self):
+        return int(N.cuda().kr_engine_launches(self._h))
+
+    def flops_per_product(self):
+        nz = self.nnz
+        return nz["v"] + nz["u"] + nz["ahat"] + (0 if self.m_identity else nz["m"] - self.k)
+
+    def bytes_per_product(self):
+        """Algorithmic HBM bytes of one product (BASELINE.md §2 formula):
+        fp64 values + int32 indices + int32 outer pointers of Ahat, U, V (and
+        M's off-diagonals when M != I), plus reading x and writing y."""
+        nz = self.nnz
+        b = 12 * nz["ahat"] + 4 * (self.rows + 1) + 12 * nz["u"] + 4 * (self.rows + 1) \
+            + 12 * nz["v"] + 4 * (self.k + 1) + 8 * (self.rows + self.cols)
+        if not self.m_identity:
+            b += 12 * (nz["m"] - self.k) + 4 * (self.k + 1)
+        return b
+
+    # -- device-pointer variants (torch tensors on the engine's device) ----
+    @property
+    def stream(self):
+        return N.cuda().kr_engine_stream(self._h)
+
+    def ax_device(self, x_ptr, y_ptr, stream=None):
+        N.check(N.cuda().kr_engine_ax_device(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                             C.c_void_p(stream) if stream else None))
+
+    def atx_device(self, y_ptr, x_ptr, stream=None):
+        N.check(N.cuda().kr_engine_atx_device(self._h, C.c_void_p(y_ptr), C.c_void_p(x_ptr),
+                                              C.c_void_p(stream) if stream else None))
