@@ -42,17 +42,22 @@ int guarded(F&& f) {
     }
 }
 
-// One row-ordered compressed matrix in HBM.  Row r's entries are summed in
-// storage order by exactly one thread (the reference's accumulation order),
-// and `blk` partitions rows into thread blocks of <= kRowsPerBlock rows and
-// roughly kNnzPerBlock entries.
-struct DevRows {
-    int64_t nrows = 0, nnz = 0;
-    int64_t* rowptr = nullptr;
-    int32_t* col = nullptr;
+__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// SELL-32-sigma matrix in HBM (sliced ELLPACK, Kreutzer et al.): output rows
+// are taken in windows of kSigma, sorted by length inside the window, and cut
+// into slices of 32 rows.  Entry j of the row held by lane l of slice s lives
+// at slice_ptr[s] + 32*j + l, so a warp streams 32 rows with coalesced loads
+// while every row is still folded by ONE lane in its storage order — the
+// reference's accumulation order (engine.hpp:67-70, 82-88, 104-108, 118-129).
+constexpr int kSigma = 1024;
+struct DevSell {
+    int64_t nrows = 0, nslices = 0, nnz = 0, padded = 0;
+    int64_t* slice_ptr = nullptr;  // nslices + 1
+    int32_t* lane_row = nullptr;   // nslices * 32; -1 = unused lane
+    int32_t* lane_len = nullptr;   // nslices * 32
+    int32_t* col = nullptr;        // padded entries
     double* val = nullptr;
-    int32_t* blk = nullptr;
-    int32_t nblk = 0;
 };
 
 template <class T>
@@ -76,27 +81,34 @@ struct kr_engine {
     // level-scheduled, 3 not unit lower triangular (products fail CONTRACT).
     int mkind = 0;
     std::string mfail;
-    krb::DevRows VT;  // rows of V^T (= V's CSC columns): t = V^T x            engine.hpp:65-72
-    krb::DevRows UA;  // row i = [U row i | Ahat row i] over [z | x]            engine.hpp:81-89
-    krb::DevRows UT;  // rows of U^T: s = U^T y                                 engine.hpp:103-110
-    krb::DevRows AV;  // row c = [Ahat^T row c | V row c] over [y | z]          engine.hpp:117-130
-    // chains (mkind 1): elements in solve order; mul = M(row, previous row)
+    // Internal layouts: the k coordinates are relabelled chain-major (mkind
+    // 1) so every chain is a contiguous range, and V^T x gathers from a
+    // sequence-major copy of x (x'[s*M2 + J] = x[J*n2 + s]) when n2 is known.
+    bool xseq = false;
+    int64_t M2 = 0;  // hands of the column player over all boards
+    krb::DevSell VT;  // t = V^T x'                     engine.hpp:65-72
+    krb::DevSell UA;  // y = [U | Ahat] [z ; x]         engine.hpp:81-89
+    krb::DevSell UT;  // s = U^T y                      engine.hpp:103-110
+    krb::DevSell AV;  // x = [Ahat^T | V] [y ; z]       engine.hpp:117-130
+    // chains (mkind 1): chain c = positions [chain_ptr[c], chain_ptr[c+1]);
+    // chain_mul[p] = M(p, p-1) in the relabelled space; chain_neg1[c] = all -1.
     int64_t nchains = 0;
     int64_t* chain_ptr = nullptr;
-    int32_t* chain_idx = nullptr;
     double* chain_mul = nullptr;
+    uint8_t* chain_neg1 = nullptr;
     // levels (mkind 2): forward uses strict-lower CSR(M), backward CSC(M)
     std::vector<int64_t> lvl_fwd_ptr, lvl_bwd_ptr;  // host: level boundaries
     int32_t* lvl_fwd_rows = nullptr;
     int32_t* lvl_bwd_cols = nullptr;
-    int64_t* mr_ptr = nullptr;  // CSR strictly lower
+    int64_t* mr_ptr = nullptr;
     int32_t* mr_col = nullptr;
     double* mr_val = nullptr;
-    int64_t* mc_ptr = nullptr;  // CSC strictly lower
+    int64_t* mc_ptr = nullptr;
     int32_t* mc_row = nullptr;
     double* mc_val = nullptr;
     // scratch
     double* d_tz = nullptr;  // k: t, then z in place (GradientWorkspace::y/z)
+    double* d_xp = nullptr;  // cols: sequence-major copy of x
     double* d_in = nullptr;  // staging for host-buffer calls
     double* d_out = nullptr;
     int64_t flops_total = 0, flops_last = 0, launches = 0;
@@ -104,7 +116,7 @@ struct kr_engine {
 };
 
 namespace krb {
-// Enqueue the products on `s` (device pointers); return KR status.
+// Enqueue the products on `s` (device pointers).
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s);
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s);
 }  // namespace krb

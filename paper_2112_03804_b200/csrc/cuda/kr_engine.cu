@@ -2,31 +2,32 @@
 // A = Ahat + U M^-1 V^T (arXiv 2112.03804; reference engine.hpp:58-133).
 //
 // Design:
-//  * Every product is "ordered": each output row is accumulated by ONE thread
+//  * Every product is "ordered": each output row is accumulated by ONE lane
 //    in the reference's storage order (engine.hpp:67-70, 82-88, 104-108,
 //    118-129), so results are bitwise equal to the reference (compiled with
 //    -fmad=false: no contraction, as in the reference's x86-64 build).
-//  * The scatter loops of matvecTranspose become gathers over precomputed
-//    transposed layouts built once at create time (no atomics, deterministic).
-//  * Ax = [V^T x] -> [M solve] -> [[U|Ahat] over [z|x]]; the U and Ahat rows
-//    are merged so one pass reproduces the single accumulator of
-//    engine.hpp:83-89.  ATx = [U^T y] -> [M^T solve] -> [[Ahat^T|V] over [y|z]].
-//  * SpMV kernel: row blocks of <= 256 rows and ~4K entries; each tile of
-//    column indices and values is streamed with coalesced loads, the products
-//    are staged in shared memory, then each thread folds its own row's
-//    products in order.  Technique B's M is a set of chains (segmented
-//    recurrences over strength-sorted hands), solved one chain per thread.
+//  * matvecTranspose's scatters become gathers over transposed layouts built
+//    once at create time (no atomics, deterministic).
+//  * Ax  = [V^T x'] -> [M solve] -> [[U|Ahat] over [z|x]]   (3 launches + x')
+//    ATx = [U^T y]  -> [M^T solve] -> [[Ahat^T|V] over [y|z]]  (3 launches)
+//    U and Ahat rows are merged so one pass reproduces the single accumulator
+//    of engine.hpp:83-89 (and likewise engine.hpp:117-130).
+//  * Matrices are stored SELL-32-sigma (kr_common.cuh): one warp streams 32
+//    rows with coalesced 128/256-byte loads, no shared memory, no barriers.
+//  * Technique B's M is a set of chains over strength-sorted hands; k is
+//    relabelled chain-major so each chain is contiguous, and one warp walks
+//    a chain with a shuffle-fed serial recurrence (the exact reference
+//    recurrence z_r = t_r - M(r,p) z_p, engine.hpp:38-39).
 #include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <thread>
 
 #include "kr_common.cuh"
 
 namespace krb {
-
-__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
 namespace {
 thread_local int g_code = 0;
@@ -40,129 +41,143 @@ void set_error(int code, const std::string& msg) {
 
 namespace {
 
-constexpr int kThreads = 256;        // threads per SpMV block == max rows per block
-constexpr int kTile = 2048;          // entries staged per tile (16 KB of products)
-constexpr int kPer = kTile / kThreads;
-constexpr int64_t kNnzPerBlock = 4096;
+constexpr int kWarpsPerBlock = 4;
 
 // ------------------------------------------------------------- kernels ----
 
-// y[r] = sum over row r of val * src[col], in storage order.  src is the
-// concatenation [xa (split entries) | xb] when TWO is set.
+// y[row] = sum_j val * src[col] over the row's entries in storage order;
+// src = [xa (split entries) | xb] when TWO.
 template <bool TWO>
-__global__ void __launch_bounds__(kThreads) k_ordered_spmv(const int64_t* __restrict__ rowptr,
-                                                           const int32_t* __restrict__ col,
-                                                           const double* __restrict__ val,
-                                                           const int32_t* __restrict__ blk,
-                                                           const double* __restrict__ xa,
-                                                           const double* __restrict__ xb, int32_t split,
-                                                           double* __restrict__ y) {
-    __shared__ double P[kTile];
-    const int32_t r0 = blk[blockIdx.x], r1 = blk[blockIdx.x + 1];
-    const int64_t e0 = rowptr[r0], e1 = rowptr[r1];
-    const int tid = threadIdx.x;
-    const int32_t r = r0 + tid;
-    int64_t rs = 0, re = 0;
-    if (r < r1) {
-        rs = rowptr[r];
-        re = rowptr[r + 1];
-    }
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_sell_spmv(const int64_t* __restrict__ slice_ptr, const int32_t* __restrict__ lane_row,
+                const int32_t* __restrict__ lane_len, const int32_t* __restrict__ col,
+                const double* __restrict__ val, int64_t nslices, const double* __restrict__ xa,
+                const double* __restrict__ xb, int32_t split, double* __restrict__ y) {
+    const int64_t s = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s >= nslices) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t base = slice_ptr[s] + lane;
+    const int32_t len = lane_len[s * 32 + lane];
+    const int32_t row = lane_row[s * 32 + lane];
     double acc = 0.0;
-    for (int64_t t0 = e0; t0 < e1; t0 += kTile) {
-        const int n = int(lmin(kTile, e1 - t0));
-        int32_t cc[kPer];
-        double vv[kPer];
+    int32_t j = 0;
+    for (; j + 4 <= len; j += 4) {
+        int32_t c[4];
+        double v[4], x[4];
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int q = tid + u * kThreads;
-            if (q < n) {
-                cc[u] = __ldcs(col + t0 + q);
-                vv[u] = __ldcs(val + t0 + q);
-            }
+        for (int u = 0; u < 4; ++u) {
+            c[u] = __ldcs(col + base + int64_t(j + u) * 32);
+            v[u] = __ldcs(val + base + int64_t(j + u) * 32);
         }
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int q = tid + u * kThreads;
-            if (q < n) {
-                double xv;
-                if (TWO) xv = cc[u] < split ? __ldg(xa + cc[u]) : __ldg(xb + (cc[u] - split));
-                else xv = __ldg(xa + cc[u]);
-                P[q] = vv[u] * xv;
-            }
+        for (int u = 0; u < 4; ++u) {
+            if (TWO) x[u] = c[u] < split ? __ldg(xa + c[u]) : __ldg(xb + (c[u] - split));
+            else x[u] = __ldg(xa + c[u]);
         }
-        __syncthreads();
-        const int64_t s = max(rs, t0), en = min(re, t0 + n);
-        for (int64_t e = s; e < en; ++e) acc += P[e - t0];
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += v[u] * x[u];
     }
-    if (r < r1) y[r] = acc;
+    for (; j < len; ++j) {
+        const int32_t c = __ldcs(col + base + int64_t(j) * 32);
+        const double v = __ldcs(val + base + int64_t(j) * 32);
+        double x;
+        if (TWO) x = c < split ? __ldg(xa + c) : __ldg(xb + (c - split));
+        else x = __ldg(xa + c);
+        acc += v * x;
+    }
+    if (row >= 0) y[row] = acc;
+}
+
+// x'[s*M2 + J] = x[J*n2 + s]: the sequence-major copy V^T x gathers from.
+__global__ void k_seq_major(const double* __restrict__ x, int64_t M2, int32_t n2, double* __restrict__ xp) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= M2 * n2) return;
+    const int64_t J = q / n2;
+    const int32_t s = int32_t(q - J * n2);
+    xp[int64_t(s) * M2 + J] = x[q];
 }
 
 // Forward solve M z = t along chains (engine.hpp:31-41 restricted to <=1
-// off-diagonal per row/column): z_r = t_r - M(r,p) z_p, skipped when z_p == 0.
-__global__ void k_chain_forward(const int64_t* __restrict__ cptr, const int32_t* __restrict__ cidx,
-                                const double* __restrict__ cmul, int64_t nchains, double* __restrict__ z) {
-    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// off-diagonal per row/column), one warp per chain.  Lanes stage 32
+// consecutive elements; every lane then replays the serial recurrence
+//   z_p = (z_{p-1} != 0) ? t_p - M(p,p-1) z_{p-1} : t_p
+// from shuffles (for M(p,p-1) == -1 this is exactly t_p + z_{p-1}).
+__global__ void k_chain_forward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
+                                const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
+    const int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (c >= nchains) return;
+    const int lane = threadIdx.x & 31;
     const int64_t a = cptr[c], b = cptr[c + 1];
+    const bool allneg = neg1[c] != 0;
     double prev = 0.0;
-    for (int64_t k0 = a; k0 < b; k0 += 8) {
-        const int n = int(lmin(8, b - k0));
-        int32_t rr[8];
-        double mm[8], tt[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < n) {
-                rr[u] = cidx[k0 + u];
-                mm[u] = cmul[k0 + u];
+    for (int64_t k0 = a; k0 < b; k0 += 32) {
+        const int n = int(lmin(32, b - k0));
+        const double tv = lane < n ? z[k0 + lane] : 0.0;
+        const double mv = (!allneg && lane < n) ? cmul[k0 + lane] : 0.0;
+        double mine = 0.0;
+        if (allneg) {
+#pragma unroll 8
+            for (int j = 0; j < n; ++j) {
+                const double tj = __shfl_sync(0xffffffffu, tv, j);
+                const double zj = (k0 + j == a) ? tj : tj + prev;
+                if (lane == j) mine = zj;
+                prev = zj;
             }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < n) tt[u] = z[rr[u]];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < n) {
-                double zr = tt[u];
-                if (k0 + u != a && prev != 0.0) zr = tt[u] - mm[u] * prev;
-                z[rr[u]] = zr;
-                prev = zr;
+        } else {
+#pragma unroll 8
+            for (int j = 0; j < n; ++j) {
+                const double tj = __shfl_sync(0xffffffffu, tv, j);
+                const double mj = __shfl_sync(0xffffffffu, mv, j);
+                const double zj = (k0 + j == a || prev == 0.0) ? tj : tj - mj * prev;
+                if (lane == j) mine = zj;
+                prev = zj;
             }
+        }
+        if (lane < n) z[k0 + lane] = mine;
     }
 }
 
-// Backward solve M^T z = s along chains (engine.hpp:44-54): visiting each
-// chain in reverse, z_r = s_r - (0 + M(next, r) z_next).
-__global__ void k_chain_backward(const int64_t* __restrict__ cptr, const int32_t* __restrict__ cidx,
-                                 const double* __restrict__ cmul, int64_t nchains, double* __restrict__ z) {
-    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// Backward solve M^T z = s along chains (engine.hpp:44-54), one warp per
+// chain walked in reverse: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
+__global__ void k_chain_backward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
+                                 const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
+    const int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (c >= nchains) return;
+    const int lane = threadIdx.x & 31;
     const int64_t a = cptr[c], b = cptr[c + 1];
+    const bool allneg = neg1[c] != 0;
     double next = 0.0, mulNext = 0.0;
     bool have = false;
-    for (int64_t k1 = b; k1 > a; k1 -= 8) {
-        const int n = int(lmin(8, k1 - a));
-        int32_t rr[8];
-        double mm[8], ss[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < n) {
-                rr[u] = cidx[k1 - 1 - u];
-                mm[u] = cmul[k1 - 1 - u];
-            }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < n) ss[u] = z[rr[u]];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < n) {
-                double acc = 0.0;
-                if (have) acc += mulNext * next;
-                const double zr = ss[u] - acc;
-                z[rr[u]] = zr;
-                next = zr;
-                mulNext = mm[u];
+    for (int64_t k1 = b; k1 > a; k1 -= 32) {
+        const int n = int(lmin(32, k1 - a));
+        const int64_t k0 = k1 - n;
+        const double sv = lane < n ? z[k0 + lane] : 0.0;
+        const double mv = lane < n ? cmul[k0 + lane] : 0.0;
+        double mine = 0.0;
+        if (allneg) {
+#pragma unroll 8
+            for (int j = n - 1; j >= 0; --j) {
+                const double sj = __shfl_sync(0xffffffffu, sv, j);
+                const double zj = have ? sj + next : sj;
+                if (lane == j) mine = zj;
+                next = zj;
                 have = true;
             }
+        } else {
+#pragma unroll 8
+            for (int j = n - 1; j >= 0; --j) {
+                const double sj = __shfl_sync(0xffffffffu, sv, j);
+                const double mj = __shfl_sync(0xffffffffu, mv, j);
+                double acc = 0.0;
+                if (have) acc += mulNext * next;
+                const double zj = sj - acc;
+                if (lane == j) mine = zj;
+                next = zj;
+                mulNext = mj;
+                have = true;
+            }
+        }
+        if (lane < n) z[k0 + lane] = mine;
     }
 }
 
@@ -196,11 +211,117 @@ __global__ void k_level_backward(const int32_t* __restrict__ cols, int64_t n, co
 
 // ------------------------------------------------------- host building ----
 
-struct HostRows {  // row-ordered matrix under construction (one board)
-    std::vector<int64_t> ptr;
+struct HostRows {  // one board's matrix in OUTPUT-row order, final indices
+    std::vector<int64_t> ptr{0};
+    std::vector<int32_t> col;
+    std::vector<double> val;
+    void push(int32_t c, double v) {
+        col.push_back(c);
+        val.push_back(v);
+    }
+    void endRow() { ptr.push_back(int64_t(col.size())); }
+    int64_t rows() const { return int64_t(ptr.size()) - 1; }
+};
+
+struct HostSell {
+    std::vector<int64_t> sptr;  // relative slice starts (no terminal entry)
+    std::vector<int32_t> lrow, llen;
     std::vector<int32_t> col;
     std::vector<double> val;
 };
+
+// Sizes of the SELL layout of a matrix with the given row lengths.
+void sell_sizes(const std::vector<int64_t>& len, int64_t& slices, int64_t& padded) {
+    const int64_t n = int64_t(len.size());
+    slices = 0;
+    padded = 0;
+    std::vector<int64_t> w;
+    for (int64_t w0 = 0; w0 < n; w0 += kSigma) {
+        const int64_t w1 = std::min<int64_t>(n, w0 + kSigma);
+        w.assign(len.begin() + w0, len.begin() + w1);
+        std::sort(w.begin(), w.end(), std::greater<int64_t>());
+        for (size_t s0 = 0; s0 < w.size(); s0 += 32) {
+            padded += 32 * w[s0];
+            ++slices;
+        }
+    }
+}
+
+void to_sell(const HostRows& h, int64_t rowBase, HostSell& out) {
+    const int64_t n = h.rows();
+    out = HostSell{};
+    std::vector<int64_t> idx;
+    int64_t cur = 0;
+    for (int64_t w0 = 0; w0 < n; w0 += kSigma) {
+        const int64_t w1 = std::min<int64_t>(n, w0 + kSigma);
+        idx.resize(size_t(w1 - w0));
+        std::iota(idx.begin(), idx.end(), w0);
+        std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+            return h.ptr[a + 1] - h.ptr[a] > h.ptr[b + 1] - h.ptr[b];
+        });
+        for (size_t s0 = 0; s0 < idx.size(); s0 += 32) {
+            const int64_t width = h.ptr[idx[s0] + 1] - h.ptr[idx[s0]];
+            out.sptr.push_back(cur);
+            const size_t at = out.col.size();
+            out.col.resize(at + size_t(32 * width), 0);
+            out.val.resize(at + size_t(32 * width), 0.0);
+            for (int l = 0; l < 32; ++l) {
+                const size_t q = s0 + size_t(l);
+                if (q < idx.size()) {
+                    const int64_t r = idx[q];
+                    const int64_t len = h.ptr[r + 1] - h.ptr[r];
+                    out.lrow.push_back(int32_t(rowBase + r));
+                    out.llen.push_back(int32_t(len));
+                    for (int64_t j = 0; j < len; ++j) {
+                        out.col[at + size_t(32 * j + l)] = h.col[size_t(h.ptr[r] + j)];
+                        out.val[at + size_t(32 * j + l)] = h.val[size_t(h.ptr[r] + j)];
+                    }
+                } else {
+                    out.lrow.push_back(-1);
+                    out.llen.push_back(0);
+                }
+            }
+            cur += 32 * width;
+        }
+    }
+}
+
+void alloc_sell(krb::DevSell& d, int64_t nrows, int64_t nslices, int64_t nnz, int64_t padded) {
+    d.nrows = nrows;
+    d.nslices = nslices;
+    d.nnz = nnz;
+    d.padded = padded;
+    d.slice_ptr = dev_alloc<int64_t>(nslices + 1);
+    d.lane_row = dev_alloc<int32_t>(std::max<int64_t>(32 * nslices, 1));
+    d.lane_len = dev_alloc<int32_t>(std::max<int64_t>(32 * nslices, 1));
+    d.col = dev_alloc<int32_t>(std::max<int64_t>(padded, 1));
+    d.val = dev_alloc<double>(std::max<int64_t>(padded, 1));
+    KR_CK(cudaMemcpy(d.slice_ptr + nslices, &padded, 8, cudaMemcpyHostToDevice));
+}
+
+void upload_sell(const HostSell& h, int64_t sliceBase, int64_t entryBase, krb::DevSell& d, cudaStream_t s) {
+    const int64_t ns = int64_t(h.sptr.size());
+    if (ns == 0) return;
+    std::vector<int64_t> p(h.sptr);
+    for (auto& x : p) x += entryBase;
+    KR_CK(cudaMemcpyAsync(d.slice_ptr + sliceBase, p.data(), 8 * size_t(ns), cudaMemcpyHostToDevice, s));
+    KR_CK(cudaMemcpyAsync(d.lane_row + 32 * sliceBase, h.lrow.data(), 4 * h.lrow.size(), cudaMemcpyHostToDevice, s));
+    KR_CK(cudaMemcpyAsync(d.lane_len + 32 * sliceBase, h.llen.data(), 4 * h.llen.size(), cudaMemcpyHostToDevice, s));
+    if (!h.col.empty()) {
+        KR_CK(cudaMemcpyAsync(d.col + entryBase, h.col.data(), 4 * h.col.size(), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.val + entryBase, h.val.data(), 8 * h.val.size(), cudaMemcpyHostToDevice, s));
+    }
+    KR_CK(cudaStreamSynchronize(s));
+}
+
+void free_sell(krb::DevSell& d) {
+    cudaFree(d.slice_ptr);
+    cudaFree(d.lane_row);
+    cudaFree(d.lane_len);
+    cudaFree(d.col);
+    cudaFree(d.val);
+    d = krb::DevSell{};
+}
 
 // Stable counting-sort transpose of a compressed matrix: rows of the result
 // list the original outer index in ascending order (== the reference's
@@ -222,27 +343,9 @@ void transpose_into(int64_t outerN, int64_t innerN, const int64_t* outer, const 
         }
 }
 
-void partition_rows(const std::vector<int64_t>& ptr, int32_t rowOff, std::vector<int32_t>& blk) {
-    const int64_t n = int64_t(ptr.size()) - 1;
-    int64_t r = 0;
-    while (r < n) {
-        const int64_t start = r;
-        int64_t nnz = 0;
-        while (r < n && r - start < kThreads) {
-            const int64_t len = ptr[r + 1] - ptr[r];
-            if (r > start && nnz + len > kNnzPerBlock) break;
-            nnz += len;
-            ++r;
-        }
-        blk.push_back(int32_t(rowOff + start));
-    }
-}
-
 void check_compressed(const kr_compressed& c, int64_t outerN, int64_t innerN, const char* name) {
-    if (c.outer_size != outerN)
-        throw Fail{KR_CONTRACT, std::string(name) + " dimensions do not match Ahat/M"};
-    if (outerN > 0 && (!c.outer)) throw Fail{KR_INVALID_INPUT, std::string(name) + ": null outer array"};
-    if (outerN == 0 && !c.outer) return;
+    if (c.outer_size != outerN) throw Fail{KR_CONTRACT, std::string(name) + " dimensions do not match Ahat/M"};
+    if (!c.outer) throw Fail{KR_INVALID_INPUT, std::string(name) + ": null outer array"};
     if (c.outer[0] != 0) throw Fail{KR_INVALID_INPUT, std::string(name) + ": outer[0] must be 0"};
     for (int64_t o = 0; o < outerN; ++o)
         if (c.outer[o + 1] < c.outer[o]) throw Fail{KR_INVALID_INPUT, std::string(name) + ": outer not monotone"};
@@ -276,59 +379,138 @@ int classify_m(const kr_compressed& m, int64_t k, std::string& why) {
 }
 
 struct BoardPlan {
-    const kr_factors* f;
-    int64_t rowOff, colOff, kOff;
-    int64_t nnzVT, nnzUA, nnzUT, nnzAV;  // offsets into the combined arrays
-    int mkind;
+    const kr_factors* f = nullptr;
+    int64_t rowOff = 0, colOff = 0, kOff = 0;
+    int mkind = 0;
     std::string why;
+    // chain-major relabelling of this board's k coordinates (local)
+    std::vector<int32_t> pos;     // t -> position
+    std::vector<int32_t> at;      // position -> t
+    std::vector<int64_t> chains;  // local chain starts (+ terminal)
+    std::vector<double> mul;      // per position: M(p, p-1)
+    // SELL sizes and offsets in the combined arrays
+    int64_t sl[4] = {0, 0, 0, 0}, pad[4] = {0, 0, 0, 0}, slOff[4] = {0, 0, 0, 0}, padOff[4] = {0, 0, 0, 0};
 };
 
-void upload_rows(const HostRows& h, int64_t rowBase, int64_t nnzBase, krb::DevRows& d, cudaStream_t s) {
-    const int64_t n = int64_t(h.ptr.size()) - 1;
-    std::vector<int64_t> p(h.ptr.begin(), h.ptr.end() - 1);
-    for (auto& x : p) x += nnzBase;
-    if (n > 0) KR_CK(cudaMemcpyAsync(d.rowptr + rowBase, p.data(), 8 * size_t(n), cudaMemcpyHostToDevice, s));
-    if (!h.col.empty()) {
-        KR_CK(cudaMemcpyAsync(d.col + nnzBase, h.col.data(), 4 * h.col.size(), cudaMemcpyHostToDevice, s));
-        KR_CK(cudaMemcpyAsync(d.val + nnzBase, h.val.data(), 8 * h.val.size(), cudaMemcpyHostToDevice, s));
+void build_chain_order(BoardPlan& p, bool chainMode) {
+    const kr_factors& f = *p.f;
+    const int64_t k = f.k;
+    p.pos.assign(static_cast<size_t>(k), 0);
+    p.at.clear();
+    p.chains.assign(1, 0);
+    p.mul.clear();
+    if (!chainMode) {
+        for (int64_t t = 0; t < k; ++t) {
+            p.pos[t] = int32_t(t);
+            p.at.push_back(int32_t(t));
+        }
+        return;
     }
-    KR_CK(cudaStreamSynchronize(s));
+    std::vector<int64_t> nxt(static_cast<size_t>(k), -1);
+    std::vector<double> mulOf(static_cast<size_t>(k), 0.0);
+    std::vector<char> hasPrev(static_cast<size_t>(k), 0);
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t q = f.m.outer[j] + 1; q < f.m.outer[j + 1]; ++q) {
+            nxt[j] = f.m.inner[q];
+            mulOf[size_t(f.m.inner[q])] = f.m.val[q];
+            hasPrev[size_t(f.m.inner[q])] = 1;
+        }
+    for (int64_t j = 0; j < k; ++j) {
+        if (hasPrev[j]) continue;
+        for (int64_t r = j; r >= 0; r = nxt[r]) {
+            p.pos[r] = int32_t(p.at.size());
+            p.at.push_back(int32_t(r));
+            p.mul.push_back(mulOf[r]);
+        }
+        p.chains.push_back(int64_t(p.at.size()));
+    }
 }
 
-void alloc_rows(krb::DevRows& d, int64_t nrows, int64_t nnz) {
-    d.nrows = nrows;
-    d.nnz = nnz;
-    d.rowptr = dev_alloc<int64_t>(nrows + 1);
-    d.col = dev_alloc<int32_t>(std::max<int64_t>(nnz, 1));
-    d.val = dev_alloc<double>(std::max<int64_t>(nnz, 1));
-    KR_CK(cudaMemcpy(d.rowptr + nrows, &nnz, 8, cudaMemcpyHostToDevice));
+// The four matrices of one board in output-row order with final indices.
+//  which 0: VT (rows = positions), 1: UA (rows = Ahat rows), 2: UT (rows =
+//  positions), 3: AV (rows = Ahat cols).
+void board_rows(const BoardPlan& p, int which, int64_t R, int64_t K, bool xseq, int64_t M2, int32_t n2,
+                HostRows& h) {
+    const kr_factors& f = *p.f;
+    h = HostRows{};
+    auto xcol = [&](int64_t c) -> int32_t {  // global x index -> gather index
+        const int64_t g = p.colOff + c;
+        return xseq ? int32_t((g % n2) * M2 + g / n2) : int32_t(g);
+    };
+    auto kcol = [&](int64_t t) -> int32_t { return int32_t(p.kOff + p.pos[size_t(t)]); };
+    if (which == 0) {
+        for (int64_t q = 0; q < f.k; ++q) {
+            const int64_t t = p.at[size_t(q)];
+            for (int64_t e = f.v.outer[t]; e < f.v.outer[t + 1]; ++e) h.push(xcol(f.v.inner[e]), f.v.val[e]);
+            h.endRow();
+        }
+    } else if (which == 1) {
+        for (int64_t i = 0; i < f.rows; ++i) {
+            for (int64_t e = f.u.outer[i]; e < f.u.outer[i + 1]; ++e) h.push(kcol(f.u.inner[e]), f.u.val[e]);
+            for (int64_t e = f.ahat.outer[i]; e < f.ahat.outer[i + 1]; ++e)
+                h.push(int32_t(K + p.colOff + f.ahat.inner[e]), f.ahat.val[e]);
+            h.endRow();
+        }
+    } else if (which == 2) {
+        std::vector<int64_t> tp;
+        std::vector<int32_t> ti;
+        std::vector<double> tv;
+        transpose_into(f.rows, f.k, f.u.outer, f.u.inner, f.u.val, tp, ti, tv);
+        for (int64_t q = 0; q < f.k; ++q) {
+            const int64_t t = p.at[size_t(q)];
+            for (int64_t e = tp[t]; e < tp[t + 1]; ++e) h.push(int32_t(p.rowOff + ti[e]), tv[e]);
+            h.endRow();
+        }
+    } else {
+        std::vector<int64_t> ap, vp;
+        std::vector<int32_t> ai, vi;
+        std::vector<double> av, vv;
+        transpose_into(f.rows, f.cols, f.ahat.outer, f.ahat.inner, f.ahat.val, ap, ai, av);
+        transpose_into(f.k, f.cols, f.v.outer, f.v.inner, f.v.val, vp, vi, vv);
+        h.col.reserve(ai.size() + vi.size());
+        h.val.reserve(ai.size() + vi.size());
+        for (int64_t c = 0; c < f.cols; ++c) {
+            for (int64_t e = ap[c]; e < ap[c + 1]; ++e) h.push(int32_t(p.rowOff + ai[e]), av[e]);
+            for (int64_t e = vp[c]; e < vp[c + 1]; ++e) h.push(int32_t(R + kcol(vi[e])), vv[e]);
+            h.endRow();
+        }
+    }
 }
 
-void free_rows(krb::DevRows& d) {
-    cudaFree(d.rowptr);
-    cudaFree(d.col);
-    cudaFree(d.val);
-    cudaFree(d.blk);
-    d = krb::DevRows{};
-}
-
-void finish_blocks(krb::DevRows& d, std::vector<int32_t>& blk) {
-    blk.push_back(int32_t(d.nrows));
-    d.nblk = int32_t(blk.size()) - 1;
-    d.blk = dev_alloc<int32_t>(int64_t(blk.size()));
-    KR_CK(cudaMemcpy(d.blk, blk.data(), 4 * blk.size(), cudaMemcpyHostToDevice));
+// Row lengths of the four matrices (for the sizing pass).
+std::vector<int64_t> board_lengths(const BoardPlan& p, int which) {
+    const kr_factors& f = *p.f;
+    std::vector<int64_t> L;
+    if (which == 0) {
+        for (int64_t q = 0; q < f.k; ++q) {
+            const int64_t t = p.at[size_t(q)];
+            L.push_back(f.v.outer[t + 1] - f.v.outer[t]);
+        }
+    } else if (which == 1) {
+        for (int64_t i = 0; i < f.rows; ++i)
+            L.push_back(f.u.outer[i + 1] - f.u.outer[i] + f.ahat.outer[i + 1] - f.ahat.outer[i]);
+    } else if (which == 2) {
+        std::vector<int64_t> cnt(static_cast<size_t>(f.k), 0);
+        for (int64_t e = 0; e < f.u.outer[f.rows]; ++e) cnt[size_t(f.u.inner[e])]++;
+        for (int64_t q = 0; q < f.k; ++q) L.push_back(cnt[size_t(p.at[size_t(q)])]);
+    } else {
+        L.assign(static_cast<size_t>(f.cols), 0);
+        for (int64_t e = 0; e < f.ahat.outer[f.rows]; ++e) L[size_t(f.ahat.inner[e])]++;
+        for (int64_t e = 0; e < f.v.outer[f.k]; ++e) L[size_t(f.v.inner[e])]++;
+    }
+    return L;
 }
 
 void destroy_engine(kr_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
-    free_rows(e->VT);
-    free_rows(e->UA);
-    free_rows(e->UT);
-    free_rows(e->AV);
+    free_sell(e->VT);
+    free_sell(e->UA);
+    free_sell(e->UT);
+    free_sell(e->AV);
     cudaFree(e->chain_ptr);
-    cudaFree(e->chain_idx);
     cudaFree(e->chain_mul);
+    cudaFree(e->chain_neg1);
     cudaFree(e->lvl_fwd_rows);
     cudaFree(e->lvl_bwd_cols);
     cudaFree(e->mr_ptr);
@@ -338,10 +520,36 @@ void destroy_engine(kr_engine* e) {
     cudaFree(e->mc_row);
     cudaFree(e->mc_val);
     cudaFree(e->d_tz);
+    cudaFree(e->d_xp);
     cudaFree(e->d_in);
     cudaFree(e->d_out);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
+}
+
+template <class F>
+void parallel_boards(int nb, F&& body) {
+    std::atomic<int> next{0};
+    std::mutex mu;
+    Fail firstFail{KR_OK, ""};
+    auto worker = [&] {
+        try {
+            for (int b; (b = next.fetch_add(1)) < nb;) body(b);
+        } catch (const Fail& f) {
+            std::lock_guard<std::mutex> g(mu);
+            if (firstFail.code == KR_OK) firstFail = f;
+        } catch (const std::exception& x) {
+            std::lock_guard<std::mutex> g(mu);
+            if (firstFail.code == KR_OK) firstFail = Fail{KR_CUDA, x.what()};
+        }
+    };
+    int nth = int(std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u));
+    nth = std::min(nth, nb);
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    if (firstFail.code != KR_OK) throw firstFail;
 }
 
 kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t flags) {
@@ -356,7 +564,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
     KR_CK(cudaSetDevice(device));
 
     std::vector<BoardPlan> plan(static_cast<size_t>(nb));
-    int64_t R = 0, Cc = 0, K = 0, nVT = 0, nUA = 0, nUT = 0, nAV = 0, nM = 0;
+    int64_t R = 0, Cc = 0, K = 0, nA = 0, nU = 0, nV = 0, nM = 0;
     int32_t n1 = boards[0].n1, n2 = boards[0].n2;
     for (int b = 0; b < nb; ++b) {
         const kr_factors& f = boards[b];
@@ -366,28 +574,24 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         check_compressed(f.m, f.k, f.k, "M");
         check_compressed(f.v, f.k, f.cols, "V");
         if (f.n1 != n1 || f.n2 != n2) n1 = n2 = 0;
-        BoardPlan& p = plan[b];
+        BoardPlan& p = plan[size_t(b)];
         p.f = &f;
         p.rowOff = R;
         p.colOff = Cc;
         p.kOff = K;
-        p.nnzVT = nVT;
-        p.nnzUA = nUA;
-        p.nnzUT = nUT;
-        p.nnzAV = nAV;
-        const int64_t a = f.ahat.outer[f.rows], u = f.u.outer[f.rows], v = f.v.outer[f.k];
-        nVT += v;
-        nUA += u + a;
-        nUT += u;
-        nAV += a + v;
+        nA += f.ahat.outer[f.rows];
+        nU += f.u.outer[f.rows];
+        nV += f.v.outer[f.k];
         nM += f.m.outer[f.k];
         R += f.rows;
         Cc += f.cols;
         K += f.k;
         p.mkind = classify_m(f.m, f.k, p.why);
     }
-    if (R > INT32_MAX || Cc > INT32_MAX || K > INT32_MAX || R + K > INT32_MAX || Cc + K > INT32_MAX)
-        throw Fail{KR_INVALID_INPUT, "dimensions exceed 32-bit indices"};
+    if (R + K > INT32_MAX || Cc + K > INT32_MAX) throw Fail{KR_INVALID_INPUT, "dimensions exceed 32-bit indices"};
+    bool xseq = n2 > 0;
+    for (auto& p : plan)
+        if (xseq && (p.f->cols % n2 != 0)) xseq = false;
 
     kr_engine* e = new kr_engine();
     try {
@@ -396,172 +600,96 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         e->rows = R;
         e->cols = Cc;
         e->k = K;
-        e->nnzA = nUA - nUT;
-        e->nnzU = nUT;
-        e->nnzV = nVT;
+        e->nnzA = nA;
+        e->nnzU = nU;
+        e->nnzV = nV;
         e->nnzM = nM;
         e->n1 = n1;
         e->n2 = n2;
-        int worst = 0;
-        bool anyGeneral = false, allIdentity = true;
+        e->xseq = xseq;
+        e->M2 = xseq ? Cc / n2 : 0;
+        bool invalid = false, anyGeneral = false, allIdentity = true;
         for (auto& p : plan) {
-            if (p.mkind == 3 && worst != 3) {
-                worst = 3;
+            if (p.mkind == 3 && !invalid) {
+                invalid = true;
                 e->mfail = p.why;
             }
             if (p.mkind == 2) anyGeneral = true;
             if (p.mkind != 0) allIdentity = false;
         }
-        e->mkind = worst == 3 ? 3 : allIdentity ? 0 : anyGeneral ? 2 : 1;
+        e->mkind = invalid ? 3 : allIdentity ? 0 : anyGeneral ? 2 : 1;
         // flop rule (engine.hpp:72,77,90-91): the combined M is the identity
         // iff every board's is.
-        e->flops_per_product = e->nnzV + e->nnzU + e->nnzA + (e->mkind == 0 ? 0 : e->nnzM - K);
+        e->flops_per_product = nV + nU + nA + (e->mkind == 0 ? 0 : nM - K);
+        // Identity boards inside a chain engine are sets of singleton chains.
+        const bool chainMode = e->mkind == 1;
 
-        alloc_rows(e->VT, K, nVT);
-        alloc_rows(e->UA, R, nUA);
-        alloc_rows(e->UT, K, nUT);
-        alloc_rows(e->AV, Cc, nAV);
+        // pass 1: relabelling and SELL sizes
+        parallel_boards(nb, [&](int b) {
+            BoardPlan& p = plan[size_t(b)];
+            build_chain_order(p, chainMode);
+            for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), p.sl[w], p.pad[w]);
+        });
+        int64_t tsl[4] = {0, 0, 0, 0}, tpad[4] = {0, 0, 0, 0};
+        for (auto& p : plan)
+            for (int w = 0; w < 4; ++w) {
+                p.slOff[w] = tsl[w];
+                p.padOff[w] = tpad[w];
+                tsl[w] += p.sl[w];
+                tpad[w] += p.pad[w];
+            }
+        krb::DevSell* mats[4] = {&e->VT, &e->UA, &e->UT, &e->AV};
+        const int64_t nrowsOf[4] = {K, R, K, Cc};
+        const int64_t nnzOf[4] = {nV, nU + nA, nU, nA + nV};
+        for (int w = 0; w < 4; ++w) alloc_sell(*mats[w], nrowsOf[w], tsl[w], nnzOf[w], tpad[w]);
         e->d_tz = dev_alloc<double>(std::max<int64_t>(K, 1));
+        e->d_xp = dev_alloc<double>(std::max<int64_t>(Cc, 1));
         e->d_in = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
         e->d_out = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
 
-        std::vector<std::vector<int32_t>> bVT(static_cast<size_t>(nb)), bUA(static_cast<size_t>(nb)), bUT(static_cast<size_t>(nb)), bAV(static_cast<size_t>(nb));
-        std::atomic<int> next{0};
-        std::mutex mu;
-        Fail firstFail{KR_OK, ""};
-        auto worker = [&] {
-            try {
-                KR_CK(cudaSetDevice(device));
-                cudaStream_t s;
-                KR_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-                for (int b; (b = next.fetch_add(1)) < nb;) {
-                    const BoardPlan& p = plan[size_t(b)];
-                    const kr_factors& f = *p.f;
-                    HostRows h;
-                    // VT: V's CSC columns as rows, entries index x.
-                    h.ptr.assign(f.v.outer, f.v.outer + f.k + 1);
-                    const int64_t nv = f.v.outer[f.k];
-                    h.col.resize(size_t(nv));
-                    for (int64_t q = 0; q < nv; ++q) h.col[q] = int32_t(p.colOff + f.v.inner[q]);
-                    h.val.assign(f.v.val, f.v.val + nv);
-                    upload_rows(h, p.kOff, p.nnzVT, e->VT, s);
-                    partition_rows(h.ptr, int32_t(p.kOff), bVT[size_t(b)]);
-                    // UA: [U row | Ahat row] over [z (K) | x].
-                    h.ptr.assign(size_t(f.rows) + 1, 0);
-                    h.col.clear();
-                    h.val.clear();
-                    for (int64_t i = 0; i < f.rows; ++i) {
-                        for (int64_t q = f.u.outer[i]; q < f.u.outer[i + 1]; ++q) {
-                            h.col.push_back(int32_t(p.kOff + f.u.inner[q]));
-                            h.val.push_back(f.u.val[q]);
-                        }
-                        for (int64_t q = f.ahat.outer[i]; q < f.ahat.outer[i + 1]; ++q) {
-                            h.col.push_back(int32_t(K + p.colOff + f.ahat.inner[q]));
-                            h.val.push_back(f.ahat.val[q]);
-                        }
-                        h.ptr[size_t(i) + 1] = int64_t(h.col.size());
-                    }
-                    upload_rows(h, p.rowOff, p.nnzUA, e->UA, s);
-                    partition_rows(h.ptr, int32_t(p.rowOff), bUA[size_t(b)]);
-                    // UT: U^T rows, entries index y.
-                    std::vector<int64_t> tp;
-                    std::vector<int32_t> ti;
-                    std::vector<double> tv;
-                    transpose_into(f.rows, f.k, f.u.outer, f.u.inner, f.u.val, tp, ti, tv);
-                    for (auto& c : ti) c = int32_t(c + p.rowOff);
-                    h.ptr = std::move(tp);
-                    h.col = std::move(ti);
-                    h.val = std::move(tv);
-                    upload_rows(h, p.kOff, p.nnzUT, e->UT, s);
-                    partition_rows(h.ptr, int32_t(p.kOff), bUT[size_t(b)]);
-                    // AV: [Ahat^T row | V row] over [y (R) | z].
-                    std::vector<int64_t> ap, vp;
-                    std::vector<int32_t> ai, vi;
-                    std::vector<double> av, vv;
-                    transpose_into(f.rows, f.cols, f.ahat.outer, f.ahat.inner, f.ahat.val, ap, ai, av);
-                    transpose_into(f.k, f.cols, f.v.outer, f.v.inner, f.v.val, vp, vi, vv);
-                    h.ptr.assign(size_t(f.cols) + 1, 0);
-                    h.col.clear();
-                    h.val.clear();
-                    h.col.reserve(ai.size() + vi.size());
-                    h.val.reserve(ai.size() + vi.size());
-                    for (int64_t c = 0; c < f.cols; ++c) {
-                        for (int64_t q = ap[c]; q < ap[c + 1]; ++q) {
-                            h.col.push_back(int32_t(p.rowOff + ai[q]));
-                            h.val.push_back(av[q]);
-                        }
-                        for (int64_t q = vp[c]; q < vp[c + 1]; ++q) {
-                            h.col.push_back(int32_t(R + p.kOff + vi[q]));
-                            h.val.push_back(vv[q]);
-                        }
-                        h.ptr[size_t(c) + 1] = int64_t(h.col.size());
-                    }
-                    upload_rows(h, p.colOff, p.nnzAV, e->AV, s);
-                    partition_rows(h.ptr, int32_t(p.colOff), bAV[size_t(b)]);
-                }
-                cudaStreamDestroy(s);
-            } catch (const Fail& f) {
-                std::lock_guard<std::mutex> g(mu);
-                if (firstFail.code == KR_OK) firstFail = f;
-            } catch (const std::exception& x) {
-                std::lock_guard<std::mutex> g(mu);
-                if (firstFail.code == KR_OK) firstFail = Fail{KR_CUDA, x.what()};
+        // pass 2: build and upload each board's slices
+        parallel_boards(nb, [&](int b) {
+            KR_CK(cudaSetDevice(device));
+            cudaStream_t s;
+            KR_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            const BoardPlan& p = plan[size_t(b)];
+            const int64_t rowBase[4] = {p.kOff, p.rowOff, p.kOff, p.colOff};
+            HostRows h;
+            HostSell hs;
+            for (int w = 0; w < 4; ++w) {
+                board_rows(p, w, R, K, xseq, e->M2, n2, h);
+                to_sell(h, rowBase[w], hs);
+                if (int64_t(hs.sptr.size()) != p.sl[w] || int64_t(hs.col.size()) != p.pad[w])
+                    throw Fail{KR_CUDA, "internal: SELL sizing mismatch"};
+                upload_sell(hs, p.slOff[w], p.padOff[w], *mats[w], s);
             }
-        };
-        int nth = int(std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u));
-        nth = std::min(nth, nb);
-        std::vector<std::thread> pool;
-        for (int t = 1; t < nth; ++t) pool.emplace_back(worker);
-        worker();
-        for (auto& t : pool) t.join();
-        if (firstFail.code != KR_OK) throw firstFail;
+            cudaStreamDestroy(s);
+        });
 
-        auto cat = [&](std::vector<std::vector<int32_t>>& parts, krb::DevRows& d) {
-            std::vector<int32_t> all;
-            for (auto& v : parts) all.insert(all.end(), v.begin(), v.end());
-            finish_blocks(d, all);
-        };
-        cat(bVT, e->VT);
-        cat(bUA, e->UA);
-        cat(bUT, e->UT);
-        cat(bAV, e->AV);
-
-        // M solve structures (global indices).
-        if (e->mkind == 1) {
+        // M solve structures (global, relabelled indices).
+        if (chainMode) {
             std::vector<int64_t> cptr{0};
-            std::vector<int32_t> cidx;
-            std::vector<double> cmul;
+            std::vector<double> cmul(static_cast<size_t>(K), 0.0);
+            std::vector<uint8_t> neg;
             for (auto& p : plan) {
-                const kr_factors& f = *p.f;
-                std::vector<int64_t> nxt(static_cast<size_t>(f.k), -1);
-                std::vector<double> mul(static_cast<size_t>(f.k), 0.0);
-                std::vector<char> hasPrev(static_cast<size_t>(f.k), 0);
-                for (int64_t j = 0; j < f.k; ++j)
-                    for (int64_t q = f.m.outer[j] + 1; q < f.m.outer[j + 1]; ++q) {
-                        nxt[j] = f.m.inner[q];
-                        mul[size_t(f.m.inner[q])] = f.m.val[q];
-                        hasPrev[size_t(f.m.inner[q])] = 1;
+                for (size_t c = 0; c + 1 < p.chains.size(); ++c) {
+                    bool allneg = true;
+                    for (int64_t q = p.chains[c]; q < p.chains[c + 1]; ++q) {
+                        cmul[size_t(p.kOff + q)] = p.mul[size_t(q)];
+                        if (q > p.chains[c] && p.mul[size_t(q)] != -1.0) allneg = false;
                     }
-                for (int64_t j = 0; j < f.k; ++j) {
-                    if (hasPrev[j]) continue;
-                    for (int64_t r = j; r >= 0; r = nxt[r]) {
-                        cidx.push_back(int32_t(p.kOff + r));
-                        cmul.push_back(mul[r]);
-                    }
-                    cptr.push_back(int64_t(cidx.size()));
+                    cptr.push_back(p.kOff + p.chains[c + 1]);
+                    neg.push_back(allneg ? 1 : 0);
                 }
             }
-            e->nchains = int64_t(cptr.size()) - 1;
+            e->nchains = int64_t(neg.size());
             e->chain_ptr = dev_alloc<int64_t>(int64_t(cptr.size()));
-            e->chain_idx = dev_alloc<int32_t>(std::max<int64_t>(1, int64_t(cidx.size())));
-            e->chain_mul = dev_alloc<double>(std::max<int64_t>(1, int64_t(cmul.size())));
+            e->chain_mul = dev_alloc<double>(std::max<int64_t>(K, 1));
+            e->chain_neg1 = dev_alloc<uint8_t>(std::max<int64_t>(e->nchains, 1));
             KR_CK(cudaMemcpy(e->chain_ptr, cptr.data(), 8 * cptr.size(), cudaMemcpyHostToDevice));
-            if (!cidx.empty()) {
-                KR_CK(cudaMemcpy(e->chain_idx, cidx.data(), 4 * cidx.size(), cudaMemcpyHostToDevice));
-                KR_CK(cudaMemcpy(e->chain_mul, cmul.data(), 8 * cmul.size(), cudaMemcpyHostToDevice));
-            }
+            if (K) KR_CK(cudaMemcpy(e->chain_mul, cmul.data(), 8 * size_t(K), cudaMemcpyHostToDevice));
+            if (e->nchains) KR_CK(cudaMemcpy(e->chain_neg1, neg.data(), neg.size(), cudaMemcpyHostToDevice));
         } else if (e->mkind == 2) {
-            // strictly-lower parts, global indices; CSR via transpose of CSC
             std::vector<int64_t> cp{0};
             std::vector<int32_t> crow;
             std::vector<double> cval;
@@ -579,7 +707,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             std::vector<int32_t> rcol;
             std::vector<double> rval;
             transpose_into(K, K, cp.data(), crow.data(), cval.data(), rp, rcol, rval);
-            std::vector<int32_t> lf(static_cast<size_t>(K), 0), lb(size_t(K), 0);
+            std::vector<int32_t> lf(static_cast<size_t>(K), 0), lb(static_cast<size_t>(K), 0);
             int32_t maxf = 0, maxb = 0;
             for (int64_t r = 0; r < K; ++r) {
                 for (int64_t q = rp[r]; q < rp[r + 1]; ++q) lf[r] = std::max(lf[r], lf[rcol[q]] + 1);
@@ -628,20 +756,25 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
     return e;
 }
 
-void launch_spmv(kr_engine* e, const krb::DevRows& A, const double* xa, const double* xb, int64_t split,
-                 double* y, cudaStream_t s) {
-    if (A.nblk == 0) return;
-    if (xb) k_ordered_spmv<true><<<A.nblk, kThreads, 0, s>>>(A.rowptr, A.col, A.val, A.blk, xa, xb, int32_t(split), y);
-    else k_ordered_spmv<false><<<A.nblk, kThreads, 0, s>>>(A.rowptr, A.col, A.val, A.blk, xa, nullptr, 0, y);
+void launch_sell(kr_engine* e, const krb::DevSell& A, const double* xa, const double* xb, int64_t split, double* y,
+                 cudaStream_t s) {
+    if (A.nslices == 0) return;
+    const unsigned grid = unsigned((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if (xb)
+        k_sell_spmv<true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val,
+                                                               A.nslices, xa, xb, int32_t(split), y);
+    else
+        k_sell_spmv<false><<<grid, 32 * kWarpsPerBlock, 0, s>>>(A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val,
+                                                                A.nslices, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
     e->launches++;
 }
 
 void solve_forward(kr_engine* e, cudaStream_t s) {
     if (e->mkind == 1 && e->nchains > 0) {
-        const int nt = 128;
-        k_chain_forward<<<unsigned((e->nchains + nt - 1) / nt), nt, 0, s>>>(e->chain_ptr, e->chain_idx,
-                                                                          e->chain_mul, e->nchains, e->d_tz);
+        const int wpb = 4;
+        k_chain_forward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(e->chain_ptr, e->chain_mul,
+                                                                                  e->chain_neg1, e->nchains, e->d_tz);
         KR_CK_LAUNCH();
         e->launches++;
     } else if (e->mkind == 2) {
@@ -658,9 +791,9 @@ void solve_forward(kr_engine* e, cudaStream_t s) {
 
 void solve_backward(kr_engine* e, cudaStream_t s) {
     if (e->mkind == 1 && e->nchains > 0) {
-        const int nt = 128;
-        k_chain_backward<<<unsigned((e->nchains + nt - 1) / nt), nt, 0, s>>>(e->chain_ptr, e->chain_idx,
-                                                                           e->chain_mul, e->nchains, e->d_tz);
+        const int wpb = 4;
+        k_chain_backward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(e->chain_ptr, e->chain_mul,
+                                                                                   e->chain_neg1, e->nchains, e->d_tz);
         KR_CK_LAUNCH();
         e->launches++;
     } else if (e->mkind == 2) {
@@ -679,18 +812,25 @@ void solve_backward(kr_engine* e, cudaStream_t s) {
 
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) {
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    launch_spmv(e, e->VT, x, nullptr, 0, e->d_tz, s);    // t = V^T x       engine.hpp:65-72
-    solve_forward(e, s);                                 // z = M^-1 t      engine.hpp:74-78
-    launch_spmv(e, e->UA, e->d_tz, x, e->k, y, s);       // y = U z + Ahat x  engine.hpp:81-89
+    const double* xg = x;
+    if (e->xseq && e->cols > 0) {
+        k_seq_major<<<unsigned((e->cols + 255) / 256), 256, 0, s>>>(x, e->M2, e->n2, e->d_xp);
+        KR_CK_LAUNCH();
+        e->launches++;
+        xg = e->d_xp;
+    }
+    launch_sell(e, e->VT, xg, nullptr, 0, e->d_tz, s);  // t = V^T x            engine.hpp:65-72
+    solve_forward(e, s);                                // z = M^-1 t           engine.hpp:74-78
+    launch_sell(e, e->UA, e->d_tz, x, e->k, y, s);      // y = U z + Ahat x     engine.hpp:81-89
     e->flops_last = e->flops_per_product;
     e->flops_total += e->flops_last;
 }
 
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) {
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    launch_spmv(e, e->UT, y, nullptr, 0, e->d_tz, s);    // s = U^T y         engine.hpp:103-110
-    solve_backward(e, s);                                // z = M^-T s        engine.hpp:112-115
-    launch_spmv(e, e->AV, y, e->d_tz, e->rows, x, s);    // x = Ahat^T y + V z  engine.hpp:117-130
+    launch_sell(e, e->UT, y, nullptr, 0, e->d_tz, s);      // s = U^T y          engine.hpp:103-110
+    solve_backward(e, s);                                  // z = M^-T s         engine.hpp:112-115
+    launch_sell(e, e->AV, y, e->d_tz, e->rows, x, s);      // x = Ahat^T y + V z  engine.hpp:117-130
     e->flops_last = e->flops_per_product;
     e->flops_total += e->flops_last;
 }
@@ -749,8 +889,8 @@ int kr_engine_ax(kr_engine* e, const double* x, int64_t nx, double* y, int64_t n
             throw Fail{KR_INVALID_INPUT,
                        "matvec input has size " + std::to_string(nx) + ", expected " + std::to_string(e->cols)};
         if (ny != e->rows) throw Fail{KR_INVALID_INPUT, "matvec output has the wrong size"};
-        KR_CK(cudaSetDevice(e->device));
         if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
+        KR_CK(cudaSetDevice(e->device));
         KR_CK(cudaMemcpyAsync(e->d_in, x, 8 * size_t(nx), cudaMemcpyHostToDevice, e->stream));
         krb::engine_ax(e, e->d_in, e->d_out, e->stream);
         KR_CK(cudaMemcpyAsync(y, e->d_out, 8 * size_t(ny), cudaMemcpyDeviceToHost, e->stream));
@@ -765,8 +905,8 @@ int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t 
             throw Fail{KR_INVALID_INPUT,
                        "matvec input has size " + std::to_string(ny) + ", expected " + std::to_string(e->rows)};
         if (nx != e->cols) throw Fail{KR_INVALID_INPUT, "matvec output has the wrong size"};
-        KR_CK(cudaSetDevice(e->device));
         if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
+        KR_CK(cudaSetDevice(e->device));
         KR_CK(cudaMemcpyAsync(e->d_in, y, 8 * size_t(ny), cudaMemcpyHostToDevice, e->stream));
         krb::engine_atx(e, e->d_in, e->d_out, e->stream);
         KR_CK(cudaMemcpyAsync(x, e->d_out, 8 * size_t(nx), cudaMemcpyDeviceToHost, e->stream));

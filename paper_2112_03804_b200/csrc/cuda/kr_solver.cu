@@ -1,0 +1,545 @@
+// kr_solver.cu — DCFR solver step on the B200 (reference solver.hpp:145-414).
+//
+// One DCFR iteration (solver.hpp:365-388) becomes:
+//   g1 = A x2                      engine (kr_engine.cu)
+//   k_player_step(P1, g1)          fused: cfrSweep (222-260) -> sequenceForm
+//                                  (197-218) -> discount (262-264) ->
+//                                  avg = (avg + x) * shrink (381-387)
+//   g2 = A^T x1                    engine
+//   k_player_step(P2, -g2)         same, gradient negated (solver.hpp:370)
+// Fusing the discount and the averaging of player 1 into its own step is
+// exact: the reference touches rt1 / avg1 nowhere between sequenceForm(rt1)
+// and those updates.  Each thread owns one hand and replays the reference's
+// per-hand treeplex walks in the same order, so with bitwise-equal gradients
+// the regrets, strategies, averages and exploitability trace are bitwise
+// equal to the reference.  A block stages its hands' gradient / regret rows
+// in shared memory with coalesced loads (hand-major rows, as KronPayoff::flat
+// lays them out, kron.hpp:124-126) and walks them there.
+//
+// Scalars that need pow() (discount factors, shrink) are computed on the host
+// with std::pow exactly as the reference does and passed as kernel arguments.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "kr_common.cuh"
+
+struct kr_solver {
+    kr_engine* eng = nullptr;
+    int device = 0;
+    int nboards = 0;
+    int n[2] = {0, 0};
+    int nnodes[2] = {0, 0};
+    int maxActs = 0;
+    int64_t H[2] = {0, 0};
+    std::vector<int64_t> boardStart[2];  // host copy, hands prefix per board
+    double pot = 0;
+    int32_t* d_tree[2] = {nullptr, nullptr};  // [parent(nn) | aptr(nn+1) | aseq(na)]
+    int32_t treeLen[2] = {0, 0};
+    int64_t* d_bstart[2] = {nullptr, nullptr};
+    double* regret[2] = {nullptr, nullptr};
+    double* avg[2] = {nullptr, nullptr};
+    double* x[2] = {nullptr, nullptr};
+    double* g = nullptr;        // gradient scratch, max(rows, cols)
+    double* a[2] = {nullptr, nullptr};  // normalised averages at checkpoints
+    double* handval = nullptr;  // per-hand best-response values
+    double* boardval = nullptr; // per-board sums
+    int* d_flag = nullptr;
+    int nt[2] = {64, 64};       // hands per block of the step kernel
+    int64_t launches = 0;
+};
+
+namespace krb {
+namespace {
+
+constexpr int kMaxActions = 32;
+
+struct Tree {
+    const int32_t* parent;
+    const int32_t* aptr;
+    const int32_t* aseq;
+};
+
+__device__ __forceinline__ Tree tree_view(const int32_t* t, int nn) { return Tree{t, t + nn, t + 2 * nn + 1}; }
+
+// regretMatch (solver.hpp:166-194) on a strided shared-memory row.
+__device__ __forceinline__ void regret_match(const double* R, int stride, const int32_t* seqs, int count,
+                                             double* probs) {
+    double best = R[(seqs[0] - 1) * stride];
+    double maxAbs = fabs(best);
+    for (int a = 1; a < count; ++a) {
+        const double r = R[(seqs[a] - 1) * stride];
+        best = (best < r) ? r : best;  // std::max
+        const double ar = fabs(r);
+        maxAbs = (maxAbs < ar) ? ar : maxAbs;
+    }
+    const double tol = 1e-9 * (1 + maxAbs);
+    if (best > tol) {
+        double sumPos = 0;
+        for (int a = 0; a < count; ++a) {
+            const double r = R[(seqs[a] - 1) * stride];
+            if (r > 0) sumPos += r;
+        }
+        for (int a = 0; a < count; ++a) {
+            const double r = R[(seqs[a] - 1) * stride];
+            probs[a] = r > 0 ? r / sumPos : 0.0;
+        }
+        return;
+    }
+    int ties = 0;
+    for (int a = 0; a < count; ++a)
+        if (R[(seqs[a] - 1) * stride] >= best - tol) ++ties;
+    for (int a = 0; a < count; ++a) probs[a] = R[(seqs[a] - 1) * stride] >= best - tol ? 1.0 / ties : 0.0;
+}
+
+// mode 0: sequence form only (initial strategy, solver.hpp:363-364)
+// mode 1: full DCFR player step (sweep, sequence form, discount, average)
+__global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H, int nt,
+                              const double* __restrict__ g, int negate, double* __restrict__ regret,
+                              double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
+                              double shrink) {
+    extern __shared__ double sm[];
+    const int stride = nt + 1;
+    double* G = sm;                       // (n+1) x stride : gradient, then x
+    double* Rg = G + (n + 1) * stride;    // (n+1) x stride : regrets
+    double* V = Rg + (n + 1) * stride;    // (n+1) x stride : seqVal / reach
+    int32_t* T = reinterpret_cast<int32_t*>(V + (n + 1) * stride);
+    const int tl = 2 * nn + 1 + 0;  // parent + aptr
+    for (int q = threadIdx.x; q < tl; q += blockDim.x) T[q] = treeBuf[q];
+    const int64_t h0 = int64_t(blockIdx.x) * nt;
+    const int nh = int(lmin(nt, H - h0));
+    const int64_t e0 = h0 * n;
+    const int ne = nh * n;
+    // total actions = aptr[nn]
+    __syncthreads();
+    const int na = T[2 * nn];
+    for (int q = threadIdx.x; q < na; q += blockDim.x) T[tl + q] = treeBuf[tl + q];
+    for (int q = threadIdx.x; q < ne; q += blockDim.x) {
+        const int hh = q / n, s = q - hh * n;
+        Rg[s * stride + hh] = regret[e0 + q];
+        if (mode == 1) {
+            const double gv = g[e0 + q];
+            G[s * stride + hh] = negate ? -gv : gv;
+        }
+    }
+    __syncthreads();
+    const Tree tr = tree_view(T, nn);
+    const int t = threadIdx.x;
+    if (t < nh) {
+        double probs[kMaxActions];
+        int32_t seqs[kMaxActions];
+        double* R = Rg + t;
+        double* Gt = G + t;
+        double* Vt = V + t;
+        if (mode == 1) {
+            // cfrSweep (solver.hpp:227-245): bottom-up over the player's nodes
+            for (int s = 0; s <= n; ++s) Vt[s * stride] = 0.0;
+            for (int v = nn - 1; v >= 0; --v) {
+                const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
+                for (int a = 0; a < cnt; ++a) seqs[a] = tr.aseq[a0 + a];
+                regret_match(R, stride, seqs, cnt, probs);
+                double nodeVal = 0;
+                for (int a = 0; a < cnt; ++a) {
+                    const int sq = seqs[a];
+                    const double ev = Gt[(sq - 1) * stride] + Vt[sq * stride];
+                    Vt[sq * stride] = ev;
+                    nodeVal += probs[a] * ev;
+                }
+                for (int a = 0; a < cnt; ++a) {
+                    const int sq = seqs[a];
+                    R[(sq - 1) * stride] += Vt[sq * stride] - nodeVal;
+                }
+                Vt[tr.parent[v] * stride] += nodeVal;
+            }
+        }
+        // sequenceForm (solver.hpp:202-215): top-down reach, x into G
+        Vt[0] = 1.0;
+        for (int v = 0; v < nn; ++v) {
+            const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
+            for (int a = 0; a < cnt; ++a) seqs[a] = tr.aseq[a0 + a];
+            regret_match(R, stride, seqs, cnt, probs);
+            const double mass = Vt[tr.parent[v] * stride];
+            for (int a = 0; a < cnt; ++a) {
+                const double m = mass * probs[a];
+                Vt[seqs[a] * stride] = m;
+                Gt[(seqs[a] - 1) * stride] = m;
+            }
+        }
+        if (mode == 1)  // discount (solver.hpp:262-264)
+            for (int s = 0; s < n; ++s) {
+                const double r = R[s * stride];
+                R[s * stride] = r * (r > 0 ? pos : neg);
+            }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < ne; q += blockDim.x) {
+        const int hh = q / n, s = q - hh * n;
+        const double xv = G[s * stride + hh];
+        xout[e0 + q] = xv;
+        if (mode == 1) {
+            regret[e0 + q] = Rg[s * stride + hh];
+            avg[e0 + q] = (avg[e0 + q] + xv) * shrink;  // solver.hpp:382-386
+        }
+    }
+}
+
+__global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w, double* __restrict__ out) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q < n) out[q] = avg[q] / w;  // solver.hpp:390-391
+}
+
+// bestResponseValue per hand (solver.hpp:304-318): bottom-up max walk.
+__global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
+                                const double* __restrict__ g, int negate, double* __restrict__ handval) {
+    extern __shared__ int32_t Ts[];
+    const int tl = 2 * nn + 1;
+    for (int q = threadIdx.x; q < tl; q += blockDim.x) Ts[q] = treeBuf[q];
+    __syncthreads();
+    const int na = Ts[2 * nn];
+    for (int q = threadIdx.x; q < na; q += blockDim.x) Ts[tl + q] = treeBuf[tl + q];
+    double* seqVal = reinterpret_cast<double*>(Ts + ((tl + na + 1) & ~1));
+    __syncthreads();
+    const Tree tr = tree_view(Ts, nn);
+    const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (h >= H) return;
+    double* sv = seqVal + threadIdx.x;
+    const int st = blockDim.x;
+    for (int s = 0; s <= n; ++s) sv[s * st] = 0.0;
+    const double* gh = g + h * n;
+    for (int v = nn - 1; v >= 0; --v) {
+        double best = 0;
+        bool first = true;
+        for (int a = tr.aptr[v]; a < tr.aptr[v + 1]; ++a) {
+            const int sq = tr.aseq[a];
+            const double gv = negate ? -gh[sq - 1] : gh[sq - 1];
+            const double ev = gv + sv[sq * st];
+            if (first || ev > best) best = ev;
+            first = false;
+        }
+        sv[tr.parent[v] * st] += best;
+    }
+    handval[h] = sv[0];
+}
+
+// Per-board totals in ascending hand order (solver.hpp:318 `total += ...`).
+__global__ void k_board_sums(const double* __restrict__ handval, const int64_t* __restrict__ bstart, int nb,
+                             double* __restrict__ out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    double total = 0;
+    for (int64_t h = bstart[b]; h < bstart[b + 1]; ++h) total += handval[h];
+    out[b] = total;
+}
+
+// validateSequenceStrategy (solver.hpp:266-286): flag 1 = negative entry,
+// 2 = flow conservation violated.
+__global__ void k_validate(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
+                           const double* __restrict__ x, double tol, int* __restrict__ flag) {
+    const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (h >= H) return;
+    const Tree tr = tree_view(treeBuf, nn);
+    const double* xh = x + h * n;
+    for (int s = 0; s < n; ++s)
+        if (xh[s] < -tol) atomicOr(flag, 1);
+    for (int v = 0; v < nn; ++v) {
+        const int p = tr.parent[v];
+        const double parentMass = p == 0 ? 1.0 : xh[p - 1];
+        double sum = 0;
+        for (int a = tr.aptr[v]; a < tr.aptr[v + 1]; ++a) sum += xh[tr.aseq[a] - 1];
+        if (fabs(sum - parentMass) > tol * (1 + fabs(parentMass))) atomicOr(flag, 2);
+    }
+}
+
+size_t step_smem(int n, int nt, int nn, int na) {
+    return size_t(3) * size_t(n + 1) * size_t(nt + 1) * 8 + size_t(2 * nn + 1 + na) * 4 + 16;
+}
+
+void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
+                 cudaStream_t st) {
+    const int nt = s->nt[p];
+    const unsigned grid = unsigned((s->H[p] + nt - 1) / nt);
+    if (grid == 0) return;
+    const int na = s->treeLen[p] - (2 * s->nnodes[p] + 1);
+    const size_t smem = step_smem(s->n[p], nt, s->nnodes[p], na);
+    k_player_step<<<grid, nt, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->H[p], nt, g, negate,
+                                          s->regret[p], s->x[p], s->avg[p], pos, neg, shrink);
+    KR_CK_LAUNCH();
+    s->launches++;
+}
+
+// Best-response totals of `player` against device strategy `opp`; fills
+// per-board values (host) and returns their sum.
+void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<double>& boards, cudaStream_t st) {
+    kr_engine* e = s->eng;
+    if (player == 0) engine_ax(e, opp, s->g, st);
+    else engine_atx(e, opp, s->g, st);
+    const int nn = s->nnodes[player], n = s->n[player];
+    const int bt = 128;
+    const int na = s->treeLen[player] - (2 * nn + 1);
+    const size_t smem = size_t((2 * nn + 1 + na + 2) * 4) + size_t(n + 1) * bt * 8 + 16;
+    const unsigned grid = unsigned((s->H[player] + bt - 1) / bt);
+    if (grid) {
+        k_best_response<<<grid, bt, smem, st>>>(s->d_tree[player], nn, n, s->H[player], s->g, player == 1,
+                                                s->handval);
+        KR_CK_LAUNCH();
+        s->launches++;
+    }
+    k_board_sums<<<unsigned((s->nboards + 127) / 128), 128, 0, st>>>(s->handval, s->d_bstart[player], s->nboards,
+                                                                      s->boardval);
+    KR_CK_LAUNCH();
+    s->launches++;
+    boards.assign(size_t(s->nboards), 0.0);
+    KR_CK(cudaMemcpyAsync(boards.data(), s->boardval, 8 * size_t(s->nboards), cudaMemcpyDeviceToHost, st));
+    KR_CK(cudaStreamSynchronize(st));
+}
+
+void destroy_solver(kr_solver* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    for (int p = 0; p < 2; ++p) {
+        cudaFree(s->d_tree[p]);
+        cudaFree(s->d_bstart[p]);
+        cudaFree(s->regret[p]);
+        cudaFree(s->avg[p]);
+        cudaFree(s->x[p]);
+        cudaFree(s->a[p]);
+    }
+    cudaFree(s->g);
+    cudaFree(s->handval);
+    cudaFree(s->boardval);
+    cudaFree(s->d_flag);
+    delete s;
+}
+
+}  // namespace
+}  // namespace krb
+
+using krb::Fail;
+using krb::guarded;
+
+extern "C" {
+
+int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2, int nboards, const int32_t* hands1,
+                     const int32_t* hands2, double pot, kr_solver** out) {
+    return guarded([&] {
+        if (!e || !p1 || !p2 || !hands1 || !hands2 || !out || nboards < 1)
+            throw Fail{KR_INVALID_INPUT, "null argument to kr_solver_create"};
+        if (!(pot > 0)) throw Fail{KR_INVALID_INPUT, "pot must be positive"};
+        KR_CK(cudaSetDevice(e->device));
+        auto* s = new kr_solver();
+        try {
+            s->eng = e;
+            s->device = e->device;
+            s->nboards = nboards;
+            s->pot = pot;
+            const kr_treeplex* tp[2] = {p1, p2};
+            const int32_t* hands[2] = {hands1, hands2};
+            for (int p = 0; p < 2; ++p) {
+                const kr_treeplex& t = *tp[p];
+                if (t.n_seq < 1 || t.n_nodes < 1) throw Fail{KR_INVALID_INPUT, "empty treeplex"};
+                s->n[p] = t.n_seq;
+                s->nnodes[p] = t.n_nodes;
+                if (t.node_action_ptr[0] != 0) throw Fail{KR_INVALID_INPUT, "treeplex action_ptr[0] must be 0"};
+                const int na = t.node_action_ptr[t.n_nodes];
+                std::vector<char> seen(size_t(t.n_seq) + 1, 0);
+                for (int v = 0; v < t.n_nodes; ++v) {
+                    const int cnt = t.node_action_ptr[v + 1] - t.node_action_ptr[v];
+                    if (cnt < 1 || cnt > krb::kMaxActions)
+                        throw Fail{KR_INVALID_INPUT, "decision node action count out of range"};
+                    if (t.node_parent_seq[v] < 0 || t.node_parent_seq[v] > t.n_seq)
+                        throw Fail{KR_INVALID_INPUT, "parent sequence out of range"};
+                    s->maxActs = std::max(s->maxActs, cnt);
+                }
+                for (int a = 0; a < na; ++a) {
+                    const int sq = t.action_seq[a];
+                    if (sq < 1 || sq > t.n_seq || seen[size_t(sq)]) throw Fail{KR_INVALID_INPUT, "bad action sequence id"};
+                    seen[size_t(sq)] = 1;
+                }
+                std::vector<int32_t> buf;
+                buf.insert(buf.end(), t.node_parent_seq, t.node_parent_seq + t.n_nodes);
+                buf.insert(buf.end(), t.node_action_ptr, t.node_action_ptr + t.n_nodes + 1);
+                buf.insert(buf.end(), t.action_seq, t.action_seq + na);
+                s->treeLen[p] = int32_t(buf.size());
+                s->d_tree[p] = krb::dev_alloc<int32_t>(int64_t(buf.size()));
+                KR_CK(cudaMemcpy(s->d_tree[p], buf.data(), 4 * buf.size(), cudaMemcpyHostToDevice));
+                s->boardStart[p].assign(1, 0);
+                for (int b = 0; b < nboards; ++b) {
+                    if (hands[p][b] < 0) throw Fail{KR_INVALID_INPUT, "negative hand count"};
+                    s->boardStart[p].push_back(s->boardStart[p].back() + hands[p][b]);
+                }
+                s->H[p] = s->boardStart[p].back();
+                s->d_bstart[p] = krb::dev_alloc<int64_t>(nboards + 1);
+                KR_CK(cudaMemcpy(s->d_bstart[p], s->boardStart[p].data(), 8 * size_t(nboards + 1),
+                                 cudaMemcpyHostToDevice));
+                // hands per block: largest multiple of 32 (<= 64) that fits
+                int nt = 64;
+                while (nt > 32 && krb::step_smem(t.n_seq, nt, t.n_nodes, na) > 200 * 1024) nt -= 32;
+                if (krb::step_smem(t.n_seq, nt, t.n_nodes, na) > 220 * 1024)
+                    throw Fail{KR_INVALID_INPUT, "treeplex too large for the on-chip solver step"};
+                s->nt[p] = nt;
+                KR_CK(cudaFuncSetAttribute(krb::k_player_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(krb::step_smem(t.n_seq, nt, t.n_nodes, na))));
+                const int64_t len = s->H[p] * s->n[p];
+                s->regret[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
+                s->avg[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
+                s->x[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
+                s->a[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
+            }
+            if (s->H[0] * s->n[0] != e->rows || s->H[1] * s->n[1] != e->cols)
+                throw Fail{KR_INVALID_INPUT, "treeplex x hands does not match the engine dimensions"};
+            s->g = krb::dev_alloc<double>(std::max<int64_t>(std::max(e->rows, e->cols), 1));
+            s->handval = krb::dev_alloc<double>(std::max<int64_t>(std::max(s->H[0], s->H[1]), 1));
+            s->boardval = krb::dev_alloc<double>(nboards);
+            s->d_flag = krb::dev_alloc<int>(1);
+            const int bsm0 = int((2 * s->nnodes[0] + 1 + s->treeLen[0] + 4) * 4 + (s->n[0] + 1) * 128 * 8 + 16);
+            const int bsm1 = int((2 * s->nnodes[1] + 1 + s->treeLen[1] + 4) * 4 + (s->n[1] + 1) * 128 * 8 + 16);
+            KR_CK(cudaFuncSetAttribute(krb::k_best_response, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       std::max(bsm0, bsm1)));
+        } catch (...) {
+            krb::destroy_solver(s);
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int kr_solver_destroy(kr_solver* s) {
+    return guarded([&] { krb::destroy_solver(s); });
+}
+
+int64_t kr_solver_launches(const kr_solver* s) { return s ? s->launches : 0; }
+
+int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
+    return guarded([&] {
+        if (!s || !prm || !r) throw Fail{KR_INVALID_INPUT, "null argument to kr_solver_run"};
+        if (prm->max_iters < 1) throw Fail{KR_INVALID_INPUT, "iteration budget must be positive"};
+        if (prm->checkpoint_every < 1) throw Fail{KR_INVALID_INPUT, "checkpoint period must be positive"};
+        kr_engine* e = s->eng;
+        KR_CK(cudaSetDevice(s->device));
+        cudaStream_t st = e->stream;
+        for (int p = 0; p < 2; ++p) {
+            const int64_t len = s->H[p] * s->n[p];
+            KR_CK(cudaMemsetAsync(s->regret[p], 0, 8 * size_t(len), st));
+            KR_CK(cudaMemsetAsync(s->avg[p], 0, 8 * size_t(len), st));
+        }
+        cudaEvent_t ev0, ev1;
+        KR_CK(cudaEventCreate(&ev0));
+        KR_CK(cudaEventCreate(&ev1));
+        KR_CK(cudaEventRecord(ev0, st));
+        const int64_t flops0 = e->flops_total;
+        // x1, x2 = sequenceForm of zero regrets (solver.hpp:363-364)
+        krb::launch_step(s, 0, 0, nullptr, 0, 0, 0, 0, st);
+        krb::launch_step(s, 1, 0, nullptr, 0, 0, 0, 0, st);
+        double weightSum = 0;
+        r->trace_len = 0;
+        std::vector<double> b1, b2;
+        int t = 1;
+        for (; t <= prm->max_iters; ++t) {
+            const double ta = std::pow(double(t), prm->alpha), tb = std::pow(double(t), prm->beta);
+            const double pos = ta / (ta + 1), neg = tb / (tb + 1);
+            const double shrink = std::pow(double(t) / (t + 1), prm->gamma);
+            krb::engine_ax(e, s->x[1], s->g, st);                       // g1 = A x2
+            krb::launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st);   // P1 sweep/seqform/discount/avg
+            krb::engine_atx(e, s->x[0], s->g, st);                      // A^T x1
+            krb::launch_step(s, 1, 1, s->g, 1, pos, neg, shrink, st);   // P2 with g2 = -A^T x1
+            weightSum += 1;
+            weightSum *= shrink;
+            if (t % prm->checkpoint_every == 0 || t == prm->max_iters) {
+                for (int p = 0; p < 2; ++p) {
+                    const int64_t len = s->H[p] * s->n[p];
+                    if (len == 0) continue;
+                    krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, weightSum,
+                                                                                  s->a[p]);
+                    KR_CK_LAUNCH();
+                    s->launches++;
+                }
+                krb::best_response_dev(s, 0, s->a[1], b1, st);  // br1 vs avg2 (solver.hpp:327)
+                krb::best_response_dev(s, 1, s->a[0], b2, st);  // br2 vs avg1 (solver.hpp:328)
+                double br1 = 0, br2 = 0, expl;
+                for (int b = 0; b < s->nboards; ++b) {
+                    br1 += b1[size_t(b)];
+                    br2 += b2[size_t(b)];
+                }
+                if (s->nboards == 1) {
+                    expl = (b1[0] + b2[0]) / 2 / s->pot;  // solver.hpp:329-330
+                } else {
+                    expl = 0;
+                    for (int b = 0; b < s->nboards; ++b) expl += (b1[size_t(b)] + b2[size_t(b)]) / 2 / s->pot;
+                    expl /= s->nboards;
+                }
+                const int i = r->trace_len;
+                if (i < r->trace_cap) {
+                    if (r->trace_iter) r->trace_iter[i] = t;
+                    if (r->trace_expl) r->trace_expl[i] = expl;
+                    if (r->trace_br1) r->trace_br1[i] = br1;
+                    if (r->trace_br2) r->trace_br2[i] = br2;
+                    for (int b = 0; b < s->nboards; ++b) {
+                        if (r->trace_board_br1) r->trace_board_br1[size_t(i) * s->nboards + b] = b1[size_t(b)];
+                        if (r->trace_board_br2) r->trace_board_br2[size_t(i) * s->nboards + b] = b2[size_t(b)];
+                    }
+                }
+                r->trace_len = i + 1;
+                r->iterations = t;
+                r->exploitability = expl;
+                if (prm->target_exploitability > 0 && expl <= prm->target_exploitability) break;
+            }
+        }
+        KR_CK(cudaEventRecord(ev1, st));
+        KR_CK(cudaEventSynchronize(ev1));
+        float ms = 0;
+        KR_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        r->seconds = ms / 1e3;
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        // final averages (solver.hpp:400-401)
+        for (int p = 0; p < 2; ++p) {
+            double* dst = p == 0 ? r->avg1 : r->avg2;
+            const int64_t len = s->H[p] * s->n[p];
+            if (!dst || len == 0) continue;
+            krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, weightSum, s->a[p]);
+            KR_CK_LAUNCH();
+            s->launches++;
+            KR_CK(cudaMemcpyAsync(dst, s->a[p], 8 * size_t(len), cudaMemcpyDeviceToHost, st));
+        }
+        KR_CK(cudaStreamSynchronize(st));
+        r->gradient_flops = e->flops_total - flops0;
+    });
+}
+
+int kr_solver_best_response(kr_solver* s, int player, const double* opp, int64_t n, double* value,
+                            double* board_values) {
+    return guarded([&] {
+        if (!s || !opp || !value) throw Fail{KR_INVALID_INPUT, "null argument"};
+        if (player != 0 && player != 1) throw Fail{KR_INVALID_INPUT, "player must be 0 or 1"};
+        const int opp_p = 1 - player;
+        const int64_t len = s->H[opp_p] * s->n[opp_p];
+        if (n != len)
+            throw Fail{KR_INVALID_INPUT,
+                       "strategy vector has size " + std::to_string(n) + ", expected " + std::to_string(len)};
+        KR_CK(cudaSetDevice(s->device));
+        cudaStream_t st = s->eng->stream;
+        KR_CK(cudaMemcpyAsync(s->a[opp_p], opp, 8 * size_t(len), cudaMemcpyHostToDevice, st));
+        KR_CK(cudaMemsetAsync(s->d_flag, 0, 4, st));
+        if (s->H[opp_p]) {
+            krb::k_validate<<<unsigned((s->H[opp_p] + 127) / 128), 128, 0, st>>>(
+                s->d_tree[opp_p], s->nnodes[opp_p], s->n[opp_p], s->H[opp_p], s->a[opp_p], 1e-9, s->d_flag);
+            KR_CK_LAUNCH();
+            s->launches++;
+        }
+        int flag = 0;
+        KR_CK(cudaMemcpyAsync(&flag, s->d_flag, 4, cudaMemcpyDeviceToHost, st));
+        KR_CK(cudaStreamSynchronize(st));
+        if (flag & 1) throw Fail{KR_INVALID_INPUT, "strategy vector has negative entries"};
+        if (flag & 2) throw Fail{KR_INVALID_INPUT, "strategy violates flow conservation at a node"};
+        std::vector<double> b;
+        krb::best_response_dev(s, player, s->a[opp_p], b, st);
+        double total = 0;
+        for (int i = 0; i < s->nboards; ++i) {
+            total += b[size_t(i)];
+            if (board_values) board_values[i] = b[size_t(i)];
+        }
+        *value = total;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+"""Device DCFR solver (reference solver.hpp:145-414) through the kr_solver C ABI.
+
+CudaSolver binds a CudaEngine to the two players' treeplexes and runs
+dcfrSolve / bestResponseValue / exploitability on the B200.  Per-hand walks
+replay the reference's arithmetic order, so with the engine's ordered
+products the whole trace is bitwise equal to the reference's.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+
+@dataclass
+class Treeplex:
+    """One player's decision nodes in preorder (skeleton.hpp:89-126)."""
+    n_seq: int
+    parent: np.ndarray      # [nodes] parent sequence id (0 = empty sequence)
+    action_ptr: np.ndarray  # [nodes+1]
+    action_seq: np.ndarray  # [actions] 1-based sequence ids
+
+    @classmethod
+    def from_flat(cls, n_seq, flat):
+        """[parent, nActions, seq...] per node (oracle/product export format)."""
+        parent, ptr, seqs = [], [0], []
+        q = 0
+        flat = list(int(v) for v in flat)
+        while q < len(flat):
+            parent.append(flat[q])
+            cnt = flat[q + 1]
+            seqs.extend(flat[q + 2:q + 2 + cnt])
+            ptr.append(ptr[-1] + cnt)
+            q += 2 + cnt
+        return cls(n_seq, np.array(parent, np.int32), np.array(ptr, np.int32), np.array(seqs, np.int32))
+
+    def struct(self, keep):
+        arrs = [np.ascontiguousarray(a, np.int32) for a in (self.parent, self.action_ptr, self.action_seq)]
+        keep += arrs
+        return N.kr_treeplex(self.n_seq, len(self.parent), *(N.ptr(a) for a in arrs))
+
+
+@dataclass
+class DcfrParams:
+    """DcfrParams (solver.hpp:101-109)."""
+    alpha: float = 1.5
+    beta: float = 0.0
+    gamma: float = 2.0
+    max_iters: int = 1000
+    target_exploitability: float = 0.0
+    checkpoint_every: int = 50
+
+
+@dataclass
+class DcfrResult:
+    """DcfrResult (solver.hpp:133-140) plus per-board best-response values."""
+    iterations: int
+    exploitability: float
+    gradient_flops: int
+    trace_iter: np.ndarray
+    trace_expl: np.ndarray
+    trace_br1: np.ndarray
+    trace_br2: np.ndarray
+    board_br1: np.ndarray
+    board_br2: np.ndarray
+    avg1: np.ndarray
+    avg2: np.ndarray
+    seconds: float
+    launches: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class CudaSolver:
+    def __init__(self, engine, tree1: Treeplex, tree2: Treeplex, hands1, hands2, pot):
+        L = N.cuda()
+        keep = []
+        t1, t2 = tree1.struct(keep), tree2.struct(keep)
+        h1 = np.ascontiguousarray(np.atleast_1d(hands1), np.int32)
+        h2 = np.ascontiguousarray(np.atleast_1d(hands2), np.int32)
+        if len(h1) != len(h2):
+            raise N.InvalidInputError(1, "hand-count lists differ in length")
+        h = C.c_void_p()
+        N.check(L.kr_solver_create(engine.handle, C.byref(t1), C.byref(t2), len(h1), N.ptr(h1), N.ptr(h2),
+                                   C.c_double(pot), C.byref(h)))
+        self._h = h
+        self.engine = engine  # keep alive: the solver borrows the engine (solver.hpp:32 ownership rule)
+        self.nboards = len(h1)
+        self.rows, self.cols = engine.rows, engine.cols
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            N.cuda().kr_solver_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self):
+        return int(N.cuda().kr_solver_launches(self._h))
+
+    def run(self, params: DcfrParams = None, want_avg=True) -> DcfrResult:
+        p = params or DcfrParams()
+        cap = p.max_iters // p.checkpoint_every + 2
+        ti = np.zeros(cap, np.int32)
+        te, b1, b2 = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        bb1, bb2 = np.zeros(cap * self.nboards), np.zeros(cap * self.nboards)
+        a1 = np.zeros(self.rows) if want_avg else None
+        a2 = np.zeros(self.cols) if want_avg else None
+        prm = N.kr_dcfr_params(p.alpha, p.beta, p.gamma, p.max_iters, p.target_exploitability, p.checkpoint_every)
+        res = N.kr_dcfr_result(0, 0.0, 0, 0, cap, N.ptr(ti), N.ptr(te), N.ptr(b1), N.ptr(b2), N.ptr(bb1),
+                               N.ptr(bb2), N.ptr(a1), N.ptr(a2), 0.0)
+        launches0 = self.launches() + self.engine.launches()
+        N.check(N.cuda().kr_solver_run(self._h, C.byref(prm), C.byref(res)))
+        n = min(res.trace_len, cap)
+        return DcfrResult(res.iterations, res.exploitability, res.gradient_flops, ti[:n], te[:n], b1[:n], b2[:n],
+                          bb1[:n * self.nboards].reshape(n, self.nboards),
+                          bb2[:n * self.nboards].reshape(n, self.nboards), a1, a2, res.seconds,
+                          self.launches() + self.engine.launches() - launches0)
+
+    def best_response(self, player, opp, per_board=False):
+        """bestResponseValue (solver.hpp:292-321) against a host strategy."""
+        opp = np.ascontiguousarray(opp, np.float64)
+        v = C.c_double()
+        bv = np.zeros(self.nboards)
+        N.check(N.cuda().kr_solver_best_response(self._h, player, N.ptr(opp), len(opp), C.byref(v), N.ptr(bv)))
+        return (v.value, bv) if per_board else v.value
+
+    def exploitability(self, x1, x2):
+        """exploitability (solver.hpp:325-331) for a single board."""
+        br1 = self.best_response(0, x2)
+        br2 = self.best_response(1, x1)
+        return br1, br2

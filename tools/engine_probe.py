@@ -112,8 +112,60 @@ def main():
         co += Ib.cols
     print("config3 stacked bitwise:", good)
     ok &= good
+    ok &= solver_probe()
     print("ALL OK" if ok else "FAILURES")
     return 0 if ok else 1
+
+
+def solver_probe():
+    from paper_2112_03804_b200.solver import CudaSolver, DcfrParams, Treeplex
+    ok = True
+
+    def mk(I, sps, hands1, hands2):
+        eng = CudaEngine(sps)
+        t1 = Treeplex.from_flat(I.n1, I.treeplex(0))
+        t2 = Treeplex.from_flat(I.n2, I.treeplex(1))
+        return eng, CudaSolver(eng, t1, t2, hands1, hands2, 2 * 1875.0)
+
+    I = po.Instance.builtin("twenty_card")
+    S = I.sparsify("b", True)
+    eng, sol = mk(I, S, [I.m1], [I.m2])
+    r = sol.run(DcfrParams(max_iters=600))
+    o = po.dcfr(I, S, max_iters=600)
+    good = r.exploitability == o["exploitability"] and r.gradient_flops == o["gradient_flops"] == 67228200
+    good &= bits_equal(r.avg1, o["avg1"]) and bits_equal(r.avg2, o["avg2"])
+    print(f"twenty_card 600 it: gpu expl {r.exploitability!r} oracle {o['exploitability']!r} flops {r.gradient_flops}"
+          f" bitwise={good} ({r.seconds*1e3:.1f} ms, {r.launches} launches)")
+    ok &= good
+    r = sol.run(DcfrParams(max_iters=300, checkpoint_every=1))
+    o = po.dcfr(I, S, max_iters=300, checkpoint_every=1)
+    good = bits_equal(r.trace_expl, o["trace_expl"]) and bits_equal(r.trace_br1, o["trace_br1"])
+    print(f"twenty_card 300 it every-iteration trace bitwise={good}  ({r.seconds*1e3:.1f} ms)")
+    ok &= good
+    for nm in ("bluffing", "all_tie", "golden"):
+        Ib = po.Instance.builtin(nm)
+        Sb = Ib.sparsify("b", True)
+        e_b, s_b = mk(Ib, Sb, [Ib.m1], [Ib.m2])
+        s_b = CudaSolver(e_b, Treeplex.from_flat(Ib.n1, Ib.treeplex(0)), Treeplex.from_flat(Ib.n2, Ib.treeplex(1)),
+                         [Ib.m1], [Ib.m2], 20.0 if nm != "golden" else 3750.0)
+        r = s_b.run(DcfrParams(max_iters=400, checkpoint_every=1))
+        o = po.dcfr(Ib, Sb, max_iters=400, checkpoint_every=1)
+        good = bits_equal(r.trace_br1, o["trace_br1"]) and bits_equal(r.trace_br2, o["trace_br2"])
+        print(f"{nm} 400 it trace bitwise={good} final expl {r.exploitability!r} vs {o['exploitability']!r}")
+        ok &= good
+    I2 = po.Instance.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=3)
+    S2 = I2.sparsify("b", True)
+    e2, s2 = mk(I2, S2, [I2.m1], [I2.m2])
+    r = s2.run(DcfrParams(max_iters=60, checkpoint_every=10))
+    t = time.time()
+    o = po.dcfr(I2, S2, max_iters=60, checkpoint_every=10)
+    tcpu = time.time() - t
+    good = bits_equal(r.trace_br1, o["trace_br1"]) and bits_equal(r.trace_br2, o["trace_br2"])
+    print(f"config2 60 it (ckpt 10) trace bitwise={good} gpu {r.seconds*1e3:.1f} ms cpu {tcpu*1e3:.0f} ms")
+    ok &= good
+    r = s2.run(DcfrParams(max_iters=500, checkpoint_every=50))
+    print(f"config2 500 it: {500/r.seconds:.0f} it/s  expl {r.exploitability:.6g}")
+    return ok
 
 
 if __name__ == "__main__":
