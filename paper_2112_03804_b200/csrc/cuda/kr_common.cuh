@@ -50,7 +50,11 @@ __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return 
 // at slice_ptr[s] + 32*j + l, so a warp streams 32 rows with coalesced loads
 // while every row is still folded by ONE lane in its storage order — the
 // reference's accumulation order (engine.hpp:67-70, 82-88, 104-108, 118-129).
+// Rows longer than kLongRow entries are kept out of the slices and handled
+// by one thread block each (cooperative loads, ordered one-thread sum), so a
+// few very long rows cannot serialise a warp on memory latency.
 constexpr int kSigma = 1024;
+constexpr int kLongRow = 256;
 struct DevSell {
     int64_t nrows = 0, nslices = 0, nnz = 0, padded = 0;
     int64_t* slice_ptr = nullptr;  // nslices + 1
@@ -58,6 +62,12 @@ struct DevSell {
     int32_t* lane_len = nullptr;   // nslices * 32
     int32_t* col = nullptr;        // padded entries
     double* val = nullptr;
+    // long rows, plain CSR
+    int64_t nlong = 0, nnzLong = 0;
+    int64_t* long_ptr = nullptr;   // nlong + 1
+    int32_t* long_row = nullptr;   // output row of each long row
+    int32_t* long_col = nullptr;
+    double* long_val = nullptr;
 };
 
 template <class T>

@@ -45,45 +45,108 @@ constexpr int kWarpsPerBlock = 4;
 
 // ------------------------------------------------------------- kernels ----
 
+struct SellView {
+    const int64_t* slice_ptr;
+    const int32_t* lane_row;
+    const int32_t* lane_len;
+    const int32_t* col;
+    const double* val;
+    int64_t nslices;
+    const int64_t* long_ptr;
+    const int32_t* long_row;
+    const int32_t* long_col;
+    const double* long_val;
+    int64_t nlong;
+};
+
+constexpr int kLongTile = 1024;
+constexpr int kU = 8;  // entries per lane per pipeline stage
+
+template <bool TWO>
+__device__ __forceinline__ double gather(const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
+                                         int32_t c) {
+    if (TWO) return c < split ? __ldg(xa + c) : __ldg(xb + (c - split));
+    return __ldg(xa + c);
+}
+
 // y[row] = sum_j val * src[col] over the row's entries in storage order;
-// src = [xa (split entries) | xb] when TWO.
+// src = [xa (split entries) | xb] when TWO.  Blocks [0, nlong) each fold one
+// long row (all threads load and multiply a tile, thread 0 adds the tile's
+// products in order); the remaining blocks run four SELL slices each, one
+// per warp, with a two-stage register pipeline (loads of stage g+1 in flight
+// while stage g gathers and accumulates).
 template <bool TWO>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    k_sell_spmv(const int64_t* __restrict__ slice_ptr, const int32_t* __restrict__ lane_row,
-                const int32_t* __restrict__ lane_len, const int32_t* __restrict__ col,
-                const double* __restrict__ val, int64_t nslices, const double* __restrict__ xa,
-                const double* __restrict__ xb, int32_t split, double* __restrict__ y) {
-    const int64_t s = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (s >= nslices) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t base = slice_ptr[s] + lane;
-    const int32_t len = lane_len[s * 32 + lane];
-    const int32_t row = lane_row[s * 32 + lane];
-    double acc = 0.0;
-    int32_t j = 0;
-    for (; j + 4 <= len; j += 4) {
-        int32_t c[4];
-        double v[4], x[4];
+    k_spmv(SellView A, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
+           double* __restrict__ y) {
+    __shared__ double P[kLongTile];
+    if (blockIdx.x < A.nlong) {
+        const int64_t b = blockIdx.x;
+        const int64_t e0 = A.long_ptr[b], e1 = A.long_ptr[b + 1];
+        double acc = 0.0;
+        for (int64_t t0 = e0; t0 < e1; t0 += kLongTile) {
+            const int n = int(lmin(kLongTile, e1 - t0));
+            constexpr int per = kLongTile / (32 * kWarpsPerBlock);
+            int32_t c[per];
+            double v[per];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            c[u] = __ldcs(col + base + int64_t(j + u) * 32);
-            v[u] = __ldcs(val + base + int64_t(j + u) * 32);
+            for (int u = 0; u < per; ++u) {
+                const int q = threadIdx.x + u * 32 * kWarpsPerBlock;
+                if (q < n) {
+                    c[u] = __ldcs(A.long_col + t0 + q);
+                    v[u] = __ldcs(A.long_val + t0 + q);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < per; ++u) {
+                const int q = threadIdx.x + u * 32 * kWarpsPerBlock;
+                if (q < n) P[q] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int q = 0; q < n; ++q) acc += P[q];
+            __syncthreads();
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (TWO) x[u] = c[u] < split ? __ldg(xa + c[u]) : __ldg(xb + (c[u] - split));
-            else x[u] = __ldg(xa + c[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc += v[u] * x[u];
+        if (threadIdx.x == 0) y[A.long_row[b]] = acc;
+        return;
     }
-    for (; j < len; ++j) {
-        const int32_t c = __ldcs(col + base + int64_t(j) * 32);
-        const double v = __ldcs(val + base + int64_t(j) * 32);
-        double x;
-        if (TWO) x = c < split ? __ldg(xa + c) : __ldg(xb + (c - split));
-        else x = __ldg(xa + c);
-        acc += v * x;
+    const int64_t s = (int64_t(blockIdx.x) - A.nlong) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s >= A.nslices) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t base = A.slice_ptr[s] + lane;
+    const int32_t len = A.lane_len[s * 32 + lane];
+    const int32_t row = A.lane_row[s * 32 + lane];
+    double acc = 0.0;
+    int32_t c[kU];
+    double v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+        if (u < len) {
+            c[u] = __ldcs(A.col + base + int64_t(u) * 32);
+            v[u] = __ldcs(A.val + base + int64_t(u) * 32);
+        }
+    for (int32_t j = 0; j < len; j += kU) {
+        int32_t cn[kU];
+        double vn[kU], x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int32_t jj = j + kU + u;
+            if (jj < len) {
+                cn[u] = __ldcs(A.col + base + int64_t(jj) * 32);
+                vn[u] = __ldcs(A.val + base + int64_t(jj) * 32);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (j + u < len) x[u] = gather<TWO>(xa, xb, split, c[u]);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (j + u < len) acc += v[u] * x[u];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            c[u] = cn[u];
+            v[u] = vn[u];
+        }
     }
     if (row >= 0) y[row] = acc;
 }
@@ -228,17 +291,28 @@ struct HostSell {
     std::vector<int32_t> lrow, llen;
     std::vector<int32_t> col;
     std::vector<double> val;
+    std::vector<int64_t> lptr{0};  // long rows (relative CSR)
+    std::vector<int32_t> lgrow, lcol;
+    std::vector<double> lval;
 };
 
-// Sizes of the SELL layout of a matrix with the given row lengths.
-void sell_sizes(const std::vector<int64_t>& len, int64_t& slices, int64_t& padded) {
+// Sizes of the SELL layout (short rows) and of the long-row CSR.
+void sell_sizes(const std::vector<int64_t>& len, int64_t& slices, int64_t& padded, int64_t& nlong,
+                int64_t& nnzLong) {
     const int64_t n = int64_t(len.size());
-    slices = 0;
-    padded = 0;
+    slices = padded = nlong = nnzLong = 0;
     std::vector<int64_t> w;
     for (int64_t w0 = 0; w0 < n; w0 += kSigma) {
         const int64_t w1 = std::min<int64_t>(n, w0 + kSigma);
-        w.assign(len.begin() + w0, len.begin() + w1);
+        w.clear();
+        for (int64_t r = w0; r < w1; ++r) {
+            if (len[size_t(r)] > kLongRow) {
+                ++nlong;
+                nnzLong += len[size_t(r)];
+            } else {
+                w.push_back(len[size_t(r)]);
+            }
+        }
         std::sort(w.begin(), w.end(), std::greater<int64_t>());
         for (size_t s0 = 0; s0 < w.size(); s0 += 32) {
             padded += 32 * w[s0];
@@ -254,8 +328,18 @@ void to_sell(const HostRows& h, int64_t rowBase, HostSell& out) {
     int64_t cur = 0;
     for (int64_t w0 = 0; w0 < n; w0 += kSigma) {
         const int64_t w1 = std::min<int64_t>(n, w0 + kSigma);
-        idx.resize(size_t(w1 - w0));
-        std::iota(idx.begin(), idx.end(), w0);
+        idx.clear();
+        for (int64_t r = w0; r < w1; ++r) {
+            const int64_t len = h.ptr[r + 1] - h.ptr[r];
+            if (len > kLongRow) {
+                out.lgrow.push_back(int32_t(rowBase + r));
+                out.lcol.insert(out.lcol.end(), h.col.begin() + h.ptr[r], h.col.begin() + h.ptr[r + 1]);
+                out.lval.insert(out.lval.end(), h.val.begin() + h.ptr[r], h.val.begin() + h.ptr[r + 1]);
+                out.lptr.push_back(int64_t(out.lcol.size()));
+            } else {
+                idx.push_back(r);
+            }
+        }
         std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
             return h.ptr[a + 1] - h.ptr[a] > h.ptr[b + 1] - h.ptr[b];
         });
@@ -286,7 +370,15 @@ void to_sell(const HostRows& h, int64_t rowBase, HostSell& out) {
     }
 }
 
-void alloc_sell(krb::DevSell& d, int64_t nrows, int64_t nslices, int64_t nnz, int64_t padded) {
+void alloc_sell(krb::DevSell& d, int64_t nrows, int64_t nslices, int64_t nnz, int64_t padded, int64_t nlong,
+                int64_t nnzLong) {
+    d.nlong = nlong;
+    d.nnzLong = nnzLong;
+    d.long_ptr = dev_alloc<int64_t>(nlong + 1);
+    d.long_row = dev_alloc<int32_t>(std::max<int64_t>(nlong, 1));
+    d.long_col = dev_alloc<int32_t>(std::max<int64_t>(nnzLong, 1));
+    d.long_val = dev_alloc<double>(std::max<int64_t>(nnzLong, 1));
+    KR_CK(cudaMemcpy(d.long_ptr + nlong, &nnzLong, 8, cudaMemcpyHostToDevice));
     d.nrows = nrows;
     d.nslices = nslices;
     d.nnz = nnz;
@@ -299,7 +391,18 @@ void alloc_sell(krb::DevSell& d, int64_t nrows, int64_t nslices, int64_t nnz, in
     KR_CK(cudaMemcpy(d.slice_ptr + nslices, &padded, 8, cudaMemcpyHostToDevice));
 }
 
-void upload_sell(const HostSell& h, int64_t sliceBase, int64_t entryBase, krb::DevSell& d, cudaStream_t s) {
+void upload_sell(const HostSell& h, int64_t sliceBase, int64_t entryBase, int64_t longBase, int64_t longEntryBase,
+                 krb::DevSell& d, cudaStream_t s) {
+    const int64_t nl = int64_t(h.lgrow.size());
+    if (nl) {
+        std::vector<int64_t> lp(h.lptr.begin(), h.lptr.end() - 1);
+        for (auto& x : lp) x += longEntryBase;
+        KR_CK(cudaMemcpyAsync(d.long_ptr + longBase, lp.data(), 8 * size_t(nl), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.long_row + longBase, h.lgrow.data(), 4 * size_t(nl), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.long_col + longEntryBase, h.lcol.data(), 4 * h.lcol.size(), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.long_val + longEntryBase, h.lval.data(), 8 * h.lval.size(), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaStreamSynchronize(s));
+    }
     const int64_t ns = int64_t(h.sptr.size());
     if (ns == 0) return;
     std::vector<int64_t> p(h.sptr);
@@ -320,6 +423,10 @@ void free_sell(krb::DevSell& d) {
     cudaFree(d.lane_len);
     cudaFree(d.col);
     cudaFree(d.val);
+    cudaFree(d.long_ptr);
+    cudaFree(d.long_row);
+    cudaFree(d.long_col);
+    cudaFree(d.long_val);
     d = krb::DevSell{};
 }
 
@@ -390,6 +497,7 @@ struct BoardPlan {
     std::vector<double> mul;      // per position: M(p, p-1)
     // SELL sizes and offsets in the combined arrays
     int64_t sl[4] = {0, 0, 0, 0}, pad[4] = {0, 0, 0, 0}, slOff[4] = {0, 0, 0, 0}, padOff[4] = {0, 0, 0, 0};
+    int64_t nl[4] = {0, 0, 0, 0}, nlz[4] = {0, 0, 0, 0}, nlOff[4] = {0, 0, 0, 0}, nlzOff[4] = {0, 0, 0, 0};
 };
 
 void build_chain_order(BoardPlan& p, bool chainMode) {
@@ -628,20 +736,24 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         parallel_boards(nb, [&](int b) {
             BoardPlan& p = plan[size_t(b)];
             build_chain_order(p, chainMode);
-            for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), p.sl[w], p.pad[w]);
+            for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), p.sl[w], p.pad[w], p.nl[w], p.nlz[w]);
         });
-        int64_t tsl[4] = {0, 0, 0, 0}, tpad[4] = {0, 0, 0, 0};
+        int64_t tsl[4] = {0, 0, 0, 0}, tpad[4] = {0, 0, 0, 0}, tnl[4] = {0, 0, 0, 0}, tnlz[4] = {0, 0, 0, 0};
         for (auto& p : plan)
             for (int w = 0; w < 4; ++w) {
                 p.slOff[w] = tsl[w];
                 p.padOff[w] = tpad[w];
+                p.nlOff[w] = tnl[w];
+                p.nlzOff[w] = tnlz[w];
                 tsl[w] += p.sl[w];
                 tpad[w] += p.pad[w];
+                tnl[w] += p.nl[w];
+                tnlz[w] += p.nlz[w];
             }
         krb::DevSell* mats[4] = {&e->VT, &e->UA, &e->UT, &e->AV};
         const int64_t nrowsOf[4] = {K, R, K, Cc};
         const int64_t nnzOf[4] = {nV, nU + nA, nU, nA + nV};
-        for (int w = 0; w < 4; ++w) alloc_sell(*mats[w], nrowsOf[w], tsl[w], nnzOf[w], tpad[w]);
+        for (int w = 0; w < 4; ++w) alloc_sell(*mats[w], nrowsOf[w], tsl[w], nnzOf[w], tpad[w], tnl[w], tnlz[w]);
         e->d_tz = dev_alloc<double>(std::max<int64_t>(K, 1));
         e->d_xp = dev_alloc<double>(std::max<int64_t>(Cc, 1));
         e->d_in = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
@@ -659,9 +771,10 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             for (int w = 0; w < 4; ++w) {
                 board_rows(p, w, R, K, xseq, e->M2, n2, h);
                 to_sell(h, rowBase[w], hs);
-                if (int64_t(hs.sptr.size()) != p.sl[w] || int64_t(hs.col.size()) != p.pad[w])
+                if (int64_t(hs.sptr.size()) != p.sl[w] || int64_t(hs.col.size()) != p.pad[w] ||
+                    int64_t(hs.lgrow.size()) != p.nl[w] || int64_t(hs.lcol.size()) != p.nlz[w])
                     throw Fail{KR_CUDA, "internal: SELL sizing mismatch"};
-                upload_sell(hs, p.slOff[w], p.padOff[w], *mats[w], s);
+                upload_sell(hs, p.slOff[w], p.padOff[w], p.nlOff[w], p.nlzOff[w], *mats[w], s);
             }
             cudaStreamDestroy(s);
         });
@@ -758,14 +871,12 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
 
 void launch_sell(kr_engine* e, const krb::DevSell& A, const double* xa, const double* xb, int64_t split, double* y,
                  cudaStream_t s) {
-    if (A.nslices == 0) return;
-    const unsigned grid = unsigned((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    if (xb)
-        k_sell_spmv<true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val,
-                                                               A.nslices, xa, xb, int32_t(split), y);
-    else
-        k_sell_spmv<false><<<grid, 32 * kWarpsPerBlock, 0, s>>>(A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val,
-                                                                A.nslices, xa, nullptr, 0, y);
+    const int64_t blocks = A.nlong + (A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks == 0) return;
+    SellView v{A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val, A.nslices,
+               A.long_ptr, A.long_row, A.long_col, A.long_val, A.nlong};
+    if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
+    else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
     e->launches++;
 }
