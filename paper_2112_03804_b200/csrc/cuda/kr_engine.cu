@@ -20,6 +20,7 @@
 //    recurrence z_r = t_r - M(r,p) z_p, engine.hpp:38-39).
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -59,7 +60,7 @@ struct SellView {
     int64_t nlong;
 };
 
-constexpr int kLongTile = 1024;
+constexpr int kChunk = 256;  // long-row entries staged per warp
 constexpr int kU = 8;  // entries per lane per pipeline stage
 
 template <bool TWO>
@@ -70,49 +71,80 @@ __device__ __forceinline__ double gather(const double* __restrict__ xa, const do
 }
 
 // y[row] = sum_j val * src[col] over the row's entries in storage order;
-// src = [xa (split entries) | xb] when TWO.  Blocks [0, nlong) each fold one
-// long row (all threads load and multiply a tile, thread 0 adds the tile's
-// products in order); the remaining blocks run four SELL slices each, one
-// per warp, with a two-stage register pipeline (loads of stage g+1 in flight
-// while stage g gathers and accumulates).
+// src = [xa (split entries) | xb] when TWO.  The first blocks fold one long
+// row per warp (the 32 lanes load and multiply a chunk, lane 0 adds the
+// chunk's products in order while the next chunk's loads are in flight); the
+// remaining blocks run four SELL slices each, one per warp, with a two-stage
+// register pipeline (loads of stage g+1 in flight while stage g gathers and
+// accumulates).
 template <bool TWO>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     k_spmv(SellView A, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
            double* __restrict__ y) {
-    __shared__ double P[kLongTile];
-    if (blockIdx.x < A.nlong) {
-        const int64_t b = blockIdx.x;
-        const int64_t e0 = A.long_ptr[b], e1 = A.long_ptr[b + 1];
+    __shared__ double P[kWarpsPerBlock][kChunk];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t longBlocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blockIdx.x < longBlocks) {
+        const int64_t r = int64_t(blockIdx.x) * kWarpsPerBlock + w;
+        if (r >= A.nlong) return;
+        const int64_t e0 = A.long_ptr[r], e1 = A.long_ptr[r + 1];
         double acc = 0.0;
-        for (int64_t t0 = e0; t0 < e1; t0 += kLongTile) {
-            const int n = int(lmin(kLongTile, e1 - t0));
-            constexpr int per = kLongTile / (32 * kWarpsPerBlock);
+        constexpr int per = kChunk / 32;
+        double p[per];
+        // chunk 0 products
+        int n = int(lmin(kChunk, e1 - e0));
+        {
             int32_t c[per];
             double v[per];
 #pragma unroll
-            for (int u = 0; u < per; ++u) {
-                const int q = threadIdx.x + u * 32 * kWarpsPerBlock;
-                if (q < n) {
-                    c[u] = __ldcs(A.long_col + t0 + q);
-                    v[u] = __ldcs(A.long_val + t0 + q);
+            for (int u = 0; u < per; ++u)
+                if (u * 32 + lane < n) {
+                    c[u] = __ldcs(A.long_col + e0 + u * 32 + lane);
+                    v[u] = __ldcs(A.long_val + e0 + u * 32 + lane);
                 }
+#pragma unroll
+            for (int u = 0; u < per; ++u)
+                if (u * 32 + lane < n) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+        }
+        for (int64_t t0 = e0; t0 < e1; t0 += kChunk) {
+#pragma unroll
+            for (int u = 0; u < per; ++u)
+                if (u * 32 + lane < n) P[w][u * 32 + lane] = p[u];
+            __syncwarp();
+            // issue the next chunk's loads before lane 0 folds this one
+            const int64_t t1 = t0 + kChunk;
+            const int nn = int(lmin(kChunk, e1 - t1));
+            int32_t c[per];
+            double v[per];
+#pragma unroll
+            for (int u = 0; u < per; ++u)
+                if (u * 32 + lane < nn) {
+                    c[u] = __ldcs(A.long_col + t1 + u * 32 + lane);
+                    v[u] = __ldcs(A.long_val + t1 + u * 32 + lane);
+                }
+            if (lane == 0) {
+                int q = 0;
+                for (; q + 8 <= n; q += 8) {
+                    double t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t[u] = P[w][q + u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc += t[u];
+                }
+                for (; q < n; ++q) acc += P[w][q];
             }
 #pragma unroll
-            for (int u = 0; u < per; ++u) {
-                const int q = threadIdx.x + u * 32 * kWarpsPerBlock;
-                if (q < n) P[q] = v[u] * gather<TWO>(xa, xb, split, c[u]);
-            }
-            __syncthreads();
-            if (threadIdx.x == 0)
-                for (int q = 0; q < n; ++q) acc += P[q];
-            __syncthreads();
+            for (int u = 0; u < per; ++u)
+                if (u * 32 + lane < nn) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+            __syncwarp();
+            n = nn;
         }
-        if (threadIdx.x == 0) y[A.long_row[b]] = acc;
+        if (lane == 0) y[A.long_row[r]] = acc;
         return;
     }
-    const int64_t s = (int64_t(blockIdx.x) - A.nlong) * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int64_t s = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
     if (s >= A.nslices) return;
-    const int lane = threadIdx.x & 31;
     const int64_t base = A.slice_ptr[s] + lane;
     const int32_t len = A.lane_len[s * 32 + lane];
     const int32_t row = A.lane_row[s * 32 + lane];
@@ -160,87 +192,120 @@ __global__ void k_seq_major(const double* __restrict__ x, int64_t M2, int32_t n2
     xp[int64_t(s) * M2 + J] = x[q];
 }
 
+constexpr int kChainChunk = 512;
+
 // Forward solve M z = t along chains (engine.hpp:31-41 restricted to <=1
-// off-diagonal per row/column), one warp per chain.  Lanes stage 32
-// consecutive elements; every lane then replays the serial recurrence
+// off-diagonal per row/column), one warp per chain.  The warp stages a chunk
+// of the (contiguous, chain-major) chain in shared memory with coalesced
+// loads; lane 0 then runs the exact serial recurrence
 //   z_p = (z_{p-1} != 0) ? t_p - M(p,p-1) z_{p-1} : t_p
-// from shuffles (for M(p,p-1) == -1 this is exactly t_p + z_{p-1}).
-__global__ void k_chain_forward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
-                                const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
-    const int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+// (for M(p,p-1) == -1 this is exactly t_p + z_{p-1}), one dependent add per
+// element, and the warp stores the chunk back.
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_chain_forward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
+                    const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
+    __shared__ double T[kWarpsPerBlock][kChainChunk];
+    __shared__ double Mu[kWarpsPerBlock][kChainChunk];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = int64_t(blockIdx.x) * kWarpsPerBlock + w;
     if (c >= nchains) return;
-    const int lane = threadIdx.x & 31;
     const int64_t a = cptr[c], b = cptr[c + 1];
     const bool allneg = neg1[c] != 0;
     double prev = 0.0;
-    for (int64_t k0 = a; k0 < b; k0 += 32) {
-        const int n = int(lmin(32, b - k0));
-        const double tv = lane < n ? z[k0 + lane] : 0.0;
-        const double mv = (!allneg && lane < n) ? cmul[k0 + lane] : 0.0;
-        double mine = 0.0;
-        if (allneg) {
-#pragma unroll 8
-            for (int j = 0; j < n; ++j) {
-                const double tj = __shfl_sync(0xffffffffu, tv, j);
-                const double zj = (k0 + j == a) ? tj : tj + prev;
-                if (lane == j) mine = zj;
-                prev = zj;
-            }
-        } else {
-#pragma unroll 8
-            for (int j = 0; j < n; ++j) {
-                const double tj = __shfl_sync(0xffffffffu, tv, j);
-                const double mj = __shfl_sync(0xffffffffu, mv, j);
-                const double zj = (k0 + j == a || prev == 0.0) ? tj : tj - mj * prev;
-                if (lane == j) mine = zj;
-                prev = zj;
+    for (int64_t k0 = a; k0 < b; k0 += kChainChunk) {
+        const int n = int(lmin(kChainChunk, b - k0));
+        for (int q = lane; q < n; q += 32) {
+            T[w][q] = z[k0 + q];
+            if (!allneg) Mu[w][q] = cmul[k0 + q];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // batches of 8: shared-memory loads issued together, then the
+            // dependent recurrence, then the stores
+            for (int q0 = 0; q0 < n; q0 += 8) {
+                double t[8], m[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    t[u] = q0 + u < n ? T[w][q0 + u] : 0.0;
+                    m[u] = (!allneg && q0 + u < n) ? Mu[w][q0 + u] : -1.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q0 + u < n) {
+                        double zq = t[u];
+                        if (k0 + q0 + u != a) {
+                            if (allneg) zq = t[u] + prev;
+                            else if (prev != 0.0) zq = t[u] - m[u] * prev;
+                        }
+                        t[u] = zq;
+                        prev = zq;
+                    }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q0 + u < n) T[w][q0 + u] = t[u];
             }
         }
-        if (lane < n) z[k0 + lane] = mine;
+        __syncwarp();
+        for (int q = lane; q < n; q += 32) z[k0 + q] = T[w][q];
+        __syncwarp();
     }
 }
 
 // Backward solve M^T z = s along chains (engine.hpp:44-54), one warp per
-// chain walked in reverse: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
-__global__ void k_chain_backward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
-                                 const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
-    const int64_t c = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+// chain walked in reverse by lane 0: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_chain_backward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
+                     const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
+    __shared__ double T[kWarpsPerBlock][kChainChunk];
+    __shared__ double Mu[kWarpsPerBlock][kChainChunk];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = int64_t(blockIdx.x) * kWarpsPerBlock + w;
     if (c >= nchains) return;
-    const int lane = threadIdx.x & 31;
     const int64_t a = cptr[c], b = cptr[c + 1];
     const bool allneg = neg1[c] != 0;
     double next = 0.0, mulNext = 0.0;
     bool have = false;
-    for (int64_t k1 = b; k1 > a; k1 -= 32) {
-        const int n = int(lmin(32, k1 - a));
+    for (int64_t k1 = b; k1 > a; k1 -= kChainChunk) {
+        const int n = int(lmin(kChainChunk, k1 - a));
         const int64_t k0 = k1 - n;
-        const double sv = lane < n ? z[k0 + lane] : 0.0;
-        const double mv = lane < n ? cmul[k0 + lane] : 0.0;
-        double mine = 0.0;
-        if (allneg) {
-#pragma unroll 8
-            for (int j = n - 1; j >= 0; --j) {
-                const double sj = __shfl_sync(0xffffffffu, sv, j);
-                const double zj = have ? sj + next : sj;
-                if (lane == j) mine = zj;
-                next = zj;
-                have = true;
-            }
-        } else {
-#pragma unroll 8
-            for (int j = n - 1; j >= 0; --j) {
-                const double sj = __shfl_sync(0xffffffffu, sv, j);
-                const double mj = __shfl_sync(0xffffffffu, mv, j);
-                double acc = 0.0;
-                if (have) acc += mulNext * next;
-                const double zj = sj - acc;
-                if (lane == j) mine = zj;
-                next = zj;
-                mulNext = mj;
-                have = true;
+        for (int q = lane; q < n; q += 32) {
+            T[w][q] = z[k0 + q];
+            if (!allneg) Mu[w][q] = cmul[k0 + q];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (int q1 = n; q1 > 0; q1 -= 8) {
+                double t[8], m[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int q = q1 - 1 - u;
+                    t[u] = q >= 0 ? T[w][q] : 0.0;
+                    m[u] = (!allneg && q >= 0) ? Mu[w][q] : -1.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q1 - 1 - u >= 0) {
+                        double zq;
+                        if (allneg) {
+                            zq = have ? t[u] + next : t[u];
+                        } else {
+                            double acc = 0.0;
+                            if (have) acc += mulNext * next;
+                            zq = t[u] - acc;
+                            mulNext = m[u];
+                        }
+                        t[u] = zq;
+                        next = zq;
+                        have = true;
+                    }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q1 - 1 - u >= 0) T[w][q1 - 1 - u] = t[u];
             }
         }
-        if (lane < n) z[k0 + lane] = mine;
+        __syncwarp();
+        for (int q = lane; q < n; q += 32) z[k0 + q] = T[w][q];
+        __syncwarp();
     }
 }
 
@@ -297,7 +362,7 @@ struct HostSell {
 };
 
 // Sizes of the SELL layout (short rows) and of the long-row CSR.
-void sell_sizes(const std::vector<int64_t>& len, int64_t& slices, int64_t& padded, int64_t& nlong,
+void sell_sizes(const std::vector<int64_t>& len, int64_t longRow, int64_t& slices, int64_t& padded, int64_t& nlong,
                 int64_t& nnzLong) {
     const int64_t n = int64_t(len.size());
     slices = padded = nlong = nnzLong = 0;
@@ -306,7 +371,7 @@ void sell_sizes(const std::vector<int64_t>& len, int64_t& slices, int64_t& padde
         const int64_t w1 = std::min<int64_t>(n, w0 + kSigma);
         w.clear();
         for (int64_t r = w0; r < w1; ++r) {
-            if (len[size_t(r)] > kLongRow) {
+            if (len[size_t(r)] > longRow) {
                 ++nlong;
                 nnzLong += len[size_t(r)];
             } else {
@@ -321,7 +386,7 @@ void sell_sizes(const std::vector<int64_t>& len, int64_t& slices, int64_t& padde
     }
 }
 
-void to_sell(const HostRows& h, int64_t rowBase, HostSell& out) {
+void to_sell(const HostRows& h, int64_t rowBase, int64_t longRow, HostSell& out) {
     const int64_t n = h.rows();
     out = HostSell{};
     std::vector<int64_t> idx;
@@ -331,7 +396,7 @@ void to_sell(const HostRows& h, int64_t rowBase, HostSell& out) {
         idx.clear();
         for (int64_t r = w0; r < w1; ++r) {
             const int64_t len = h.ptr[r + 1] - h.ptr[r];
-            if (len > kLongRow) {
+            if (len > longRow) {
                 out.lgrow.push_back(int32_t(rowBase + r));
                 out.lcol.insert(out.lcol.end(), h.col.begin() + h.ptr[r], h.col.begin() + h.ptr[r + 1]);
                 out.lval.insert(out.lval.end(), h.val.begin() + h.ptr[r], h.val.begin() + h.ptr[r + 1]);
@@ -731,12 +796,16 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         e->flops_per_product = nV + nU + nA + (e->mkind == 0 ? 0 : nM - K);
         // Identity boards inside a chain engine are sets of singleton chains.
         const bool chainMode = e->mkind == 1;
+        // Rows longer than longRow take the warp-per-row path (SELL measured
+        // faster for everything shorter, at config 2 and config 3 alike).
+        int64_t longRow = kLongRow;
+        if (const char* env = std::getenv("KR_LONG_ROW")) longRow = std::max<int64_t>(8, std::atoll(env));
 
         // pass 1: relabelling and SELL sizes
         parallel_boards(nb, [&](int b) {
             BoardPlan& p = plan[size_t(b)];
             build_chain_order(p, chainMode);
-            for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), p.sl[w], p.pad[w], p.nl[w], p.nlz[w]);
+            for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), longRow, p.sl[w], p.pad[w], p.nl[w], p.nlz[w]);
         });
         int64_t tsl[4] = {0, 0, 0, 0}, tpad[4] = {0, 0, 0, 0}, tnl[4] = {0, 0, 0, 0}, tnlz[4] = {0, 0, 0, 0};
         for (auto& p : plan)
@@ -770,7 +839,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             HostSell hs;
             for (int w = 0; w < 4; ++w) {
                 board_rows(p, w, R, K, xseq, e->M2, n2, h);
-                to_sell(h, rowBase[w], hs);
+                to_sell(h, rowBase[w], longRow, hs);
                 if (int64_t(hs.sptr.size()) != p.sl[w] || int64_t(hs.col.size()) != p.pad[w] ||
                     int64_t(hs.lgrow.size()) != p.nl[w] || int64_t(hs.lcol.size()) != p.nlz[w])
                     throw Fail{KR_CUDA, "internal: SELL sizing mismatch"};
@@ -871,7 +940,8 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
 
 void launch_sell(kr_engine* e, const krb::DevSell& A, const double* xa, const double* xb, int64_t split, double* y,
                  cudaStream_t s) {
-    const int64_t blocks = A.nlong + (A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int64_t blocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock +
+                           (A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return;
     SellView v{A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val, A.nslices,
                A.long_ptr, A.long_row, A.long_col, A.long_val, A.nlong};
@@ -883,7 +953,7 @@ void launch_sell(kr_engine* e, const krb::DevSell& A, const double* xa, const do
 
 void solve_forward(kr_engine* e, cudaStream_t s) {
     if (e->mkind == 1 && e->nchains > 0) {
-        const int wpb = 4;
+        const int wpb = kWarpsPerBlock;
         k_chain_forward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(e->chain_ptr, e->chain_mul,
                                                                                   e->chain_neg1, e->nchains, e->d_tz);
         KR_CK_LAUNCH();
@@ -902,7 +972,7 @@ void solve_forward(kr_engine* e, cudaStream_t s) {
 
 void solve_backward(kr_engine* e, cudaStream_t s) {
     if (e->mkind == 1 && e->nchains > 0) {
-        const int wpb = 4;
+        const int wpb = kWarpsPerBlock;
         k_chain_backward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(e->chain_ptr, e->chain_mul,
                                                                                    e->chain_neg1, e->nchains, e->d_tz);
         KR_CK_LAUNCH();
