@@ -202,6 +202,18 @@ void or_inst_FS(void* h, int which, int64_t* outer, int32_t* inner, double* val)
     std::memcpy(val, m.val.data(), m.val.size() * 8);
 }
 
+// sparsifyW (sparsify.hpp:68-103) on a dense row-major W: rank and the
+// nnz of What, U, V.
+int or_peel(const double* W, int rows, int cols, int maxIters, int64_t* out) {
+    return guarded([&] {
+        WFactorization wf = sparsifyW(std::vector<double>(W, W + size_t(rows) * cols), rows, cols, maxIters);
+        out[0] = wf.rank();
+        out[1] = wf.What.nnz();
+        out[2] = wf.U.nnz();
+        out[3] = wf.V.nnz();
+    });
+}
+
 int64_t or_dense_nnz(void* h) { return densePayoffNonzeros(static_cast<Inst*>(h)->kp); }
 int or_dense_expand(void* h, double guard, double* out) {
     return guarded([&] {

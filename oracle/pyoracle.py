@@ -289,6 +289,15 @@ def time_pairs_multi(sps, threads, reps):
     return lib().or_time_pairs_multi(arr, len(sps), threads, reps, C.byref(sink))
 
 
+def peel(W, max_iters=1000):
+    """sparsifyW (sparsify.hpp:68-103): (rank, nnz What, nnz U, nnz V)."""
+    W = np.ascontiguousarray(W, np.float64)
+    out = np.zeros(4, np.int64)
+    _check(lib().or_peel(W.ctypes.data_as(C.c_void_p), W.shape[0], W.shape[1], max_iters,
+                         out.ctypes.data_as(C.c_void_p)))
+    return tuple(int(v) for v in out)
+
+
 def best_response(inst, sp, player, opp):
     opp = np.ascontiguousarray(opp, np.float64)
     out = C.c_double()

@@ -16,6 +16,9 @@ LIBDIR = os.path.join(PKG, "lib")
 CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu")]
 HOST_SRC = [os.path.join(PKG, "csrc", "host", f) for f in ("kr_host.cpp",)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# the system g++ links libstdc++ dynamically (a statically linked libstdc++
+# inside a Python extension clashes with the process copy in iostreams)
+CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
@@ -23,6 +26,7 @@ NVCC_FLAGS = [
     "-lineinfo",
     # bitwise parity with the reference's x86-64 build: never contract a*b+c
     "-fmad=false",
+    "-ccbin", CXX,
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
     "-I", os.path.join(ROOT, "include"),
     "-I", os.path.join(PKG, "csrc", "cuda"),
@@ -62,7 +66,7 @@ def build_host(force=False, verbose=False):
     if not srcs:
         return None
     if force or _stale(out, srcs):
-        cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-o", out, *srcs]
+        cmd = [CXX, *CXX_FLAGS, "-o", out, *srcs]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
