@@ -106,7 +106,7 @@ class CudaSolver:
 
     def run(self, params: DcfrParams = None, want_avg=True) -> DcfrResult:
         p = params or DcfrParams()
-        cap = p.max_iters // p.checkpoint_every + 2
+        cap = max(p.max_iters, 0) // max(p.checkpoint_every, 1) + 2  # the C ABI validates the params
         ti = np.zeros(cap, np.int32)
         te, b1, b2 = np.zeros(cap), np.zeros(cap), np.zeros(cap)
         bb1, bb2 = np.zeros(cap * self.nboards), np.zeros(cap * self.nboards)
@@ -136,3 +136,18 @@ class CudaSolver:
         br1 = self.best_response(0, x2)
         br2 = self.best_response(1, x1)
         return br1, br2
+
+
+def solver_for(boards, device=0):
+    """Engine + solver over one or more (Instance, Factors) boards that share a
+    betting tree (product host objects, paper_2112_03804_b200.host)."""
+    from .engine import CudaEngine
+    insts = [b[0] for b in boards]
+    eng = CudaEngine([b[1] for b in boards], device=device)
+    i0 = insts[0]
+    return CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [i.m1 for i in insts], [i.m2 for i in insts], i0.pot)
+
+
+def dcfr_solve(instance, factors, params: DcfrParams = None, device=0) -> DcfrResult:
+    """dcfrSolve(kp, FactoredEngine(s), params) (solver.hpp:343-414) on the B200."""
+    return solver_for([(instance, factors)], device).run(params)
