@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 gradient oracle.
+
+Metric (BASELINE.json): payoff matvec pairs/s (fp64); solver iters/s is
+reported beside it.  A step is one matvec pair (A x and A^T y, engine.hpp:58
+and :96) over the whole workload:
+
+  config 3: turn Ks7d4c2h + each of the 48 river cards,
+  1,081 hands per side, 3-bet tree (n = 43 sequences), Technique B with
+  postprocessing, beliefs from seed 1000 + card id; ~3.0e8 stored nonzeros,
+  3.6 GB of factors streamed per product (>> the 126 MB L2, so no flush is
+  needed between steps).
+
+It is the largest single-GPU configuration of BASELINE.json and the instance
+the north star's roofline target names.  Factors are built by the product's
+C++ host side (libkrhost) and applied by the sm_100a kernels (libkrcuda).
+
+  python bench.py [--gpus N --steps K --warmup W]           product arm
+  python bench.py --impl reference [...]                    CPU reference arm
+
+Multi-GPU (torchrun, one process per GPU): boards are sharded contiguously
+(48/N per GPU), products need no communication, time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "payoff matvec pairs/s and solver iters/s (fp64) at 1/2/4/8 B200 vs CPU"
+TURN = "Ks7d4c2h"
+NBOARDS = 48
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["product", "reference"], default="product")
+    p.add_argument("--boards", type=int, default=NBOARDS)
+    p.add_argument("--solver-iters", type=int, default=100)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the bounded CPU sample")
+    return p.parse_args()
+
+
+def workload_config(nboards, world, extra=None):
+    cfg = {"workload": f"config3: turn {TURN} x {nboards} river boards, 1081 hands/side, 3-bet tree (n=43), "
+                       "Technique B postprocessed, fp64 factors", "boards": nboards, "hands_per_side": 1081,
+           "sequences": 43, "tree": "menus {0.5,1.0} all contexts, all-in, raise cap 3, stacks 18125, pot 1875",
+           "l2": "no flush: every product streams 3.6 GB of factors (>> 126 MB L2)",
+           "parallelism": f"boards sharded {nboards // world if nboards % world == 0 else 'uneven'} per GPU, "
+                          f"{world} GPU(s), no data-path collective"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# --------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_id):
+        self.dev = device_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", self.dev], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------ CPU side ----
+def oracle_boards(indices, threads):
+    """CPU oracle factors (oracle/, test infrastructure) for the given boards."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2112_03804_b200.host import turn_boards
+    specs = turn_boards(TURN, NBOARDS)
+
+    def one(b):
+        card, seed = specs[b]
+        inst = po.Instance.builtin("river_full", seed=seed, board=TURN + card, tree=3)
+        return inst.sparsify("b", True)
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(one, indices))
+
+
+def cpu_baseline(threads, budget_s):
+    """The reference engine (restated in oracle/: matvec / matvecTranspose,
+    engine.hpp:58-133, sequential per call) over a bounded sample of the
+    boards, one board per host thread; scaled to full-turn pairs/s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    nb = min(NBOARDS, threads)
+    sps = oracle_boards(range(nb), threads)
+    t1 = po.time_pairs_multi(sps, threads, 1)  # warm + estimate
+    reps = max(1, int(budget_s / max(t1, 1e-3)))
+    t = po.time_pairs_multi(sps, threads, reps)
+    board_pairs_per_s = nb * reps / t
+    return {"value": board_pairs_per_s / NBOARDS, "unit": "pairs/s", "cores": threads, "kind": "port",
+            "sample": f"{nb} of {NBOARDS} boards x {reps} matvec pairs each, one board per thread "
+                      f"({t:.1f} s); full-turn pairs/s = board-pairs/s / {NBOARDS}"}
+
+
+def run_reference(args):
+    """Reference arm: the reference's CPU implementation of the path (the
+    oracle's restatement; the reference itself needs Eigen3, absent here) on
+    all host threads, same metric and workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    threads = os.cpu_count() or 1
+    sps = oracle_boards(range(args.boards), threads)
+    t1 = po.time_pairs_multi(sps, threads, 1)
+    steps = args.steps
+    budget = 150.0
+    if t1 * (args.steps + args.warmup) > budget:
+        steps = max(3, int(budget / t1) - args.warmup)
+    for _ in range(args.warmup):
+        po.time_pairs_multi(sps, threads, 1)
+    total = 0.0
+    for _ in range(steps):
+        total += po.time_pairs_multi(sps, threads, 1)
+    value = steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.boards, 1, {"steps_requested": args.steps}),
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                             "sample": f"all {args.boards} boards per step, one board per thread at a time; "
+                                       "reference engine restated in oracle/ (Eigen3 absent: reference "
+                                       "unbuildable)"},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------- product (GPU) ----
+def run_product(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200 import host as H
+    from paper_2112_03804_b200.dist import DistributedDcfr, shard
+    from paper_2112_03804_b200.solver import CudaSolver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    mine = shard(args.boards, rank, world)
+    t0 = time.time()
+    boards = H.turn_instances(TURN, args.boards, indices=list(mine))
+    build_s = time.time() - t0
+    t0 = time.time()
+    eng = CudaEngine([f for _, f in boards], device=local)
+    create_s = time.time() - t0
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    x = torch.randn(eng.cols, dtype=torch.float64, device=dev, generator=g)
+    y = torch.randn(eng.rows, dtype=torch.float64, device=dev, generator=g)
+    ax = torch.empty(eng.rows, dtype=torch.float64, device=dev)
+    atx = torch.empty(eng.cols, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def pair():
+        eng.ax_device(x.data_ptr(), ax.data_ptr())
+        eng.atx_device(y.data_ptr(), atx.data_ptr())
+
+    for _ in range(max(args.warmup, 3)):
+        pair()
+    torch.cuda.synchronize(dev)
+    eng.kernel_times()  # reset counters
+    eng.set_timing(True)
+    launches0 = eng.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    sampler = ClockSampler(uuid if uuid.startswith("GPU-") else f"GPU-{uuid}")
+    barrier()
+    torch.cuda.synchronize(dev)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            pair()
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize(dev)
+    barrier()
+    ms_local = e0.elapsed_time(e1)
+    gpu_launches = int(sum_over_ranks(eng.launches() - launches0))
+    eng.set_timing(False)
+    ktimes = eng.kernel_times()
+    ms = max_over_ranks(ms_local)
+    pairs_per_s = args.steps / (ms / 1e3)
+
+    # ---- e2e: the C-ABI host-buffer calls, H2D + D2H inside the region ----
+    from paper_2112_03804_b200 import _native as N
+    L = N.cuda()
+    nx, ny = eng.cols, eng.rows
+    px, py = L.kr_host_alloc(8 * nx), L.kr_host_alloc(8 * ny)
+    pax, patx = L.kr_host_alloc(8 * ny), L.kr_host_alloc(8 * nx)
+    as_np = lambda p, n: np.ctypeslib.as_array((__import__("ctypes").c_double * n).from_address(p))  # noqa: E731
+    hx, hy, hax, hatx = as_np(px, nx), as_np(py, ny), as_np(pax, ny), as_np(patx, nx)
+    hx[:] = x.cpu().numpy()
+    hy[:] = y.cpu().numpy()
+    e2e_steps = max(5, min(args.steps, 50))
+    for _ in range(2):
+        N.check(L.kr_engine_ax(eng.handle, px, nx, pax, ny))
+        N.check(L.kr_engine_atx(eng.handle, py, ny, patx, nx))
+    barrier()
+    t_e2e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        N.check(L.kr_engine_ax(eng.handle, px, nx, pax, ny))
+        N.check(L.kr_engine_atx(eng.handle, py, ny, patx, nx))
+    e2e_s = max_over_ranks(time.perf_counter() - t_e2e0)
+    barrier()
+    check_ok = bool(np.array_equal(hax, ax.cpu().numpy()))
+    for p in (px, py, pax, patx):
+        L.kr_host_free(p)
+
+    # ---- solver iterations/s (DCFR, checkpointEvery = 50) ----------------
+    i0 = boards[0][0]
+    solver = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
+                        i0.pot)
+    drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=dev)
+    drv.run(max_iters=5, checkpoint_every=5)  # warm
+    barrier()
+    torch.cuda.synchronize(dev)
+    ts = time.perf_counter()
+    res = drv.run(max_iters=args.solver_iters, checkpoint_every=50)
+    torch.cuda.synchronize(dev)
+    solver_s = max_over_ranks(time.perf_counter() - ts)
+
+    if rank != 0:
+        return 0
+    peak, peak_src = measured_peak()
+    dominant = max(ktimes, key=lambda k: ktimes[k]["ms"])
+    kd = ktimes[dominant]
+    per_launch_ms = kd["ms"] / max(kd["launches"], 1)
+    achieved = kd["bytes_per_launch"] / (per_launch_ms / 1e3) / 1e9
+    kernels = {k: {"launches": v["launches"], "avg_us": 1e3 * v["ms"] / max(v["launches"], 1),
+                   "gb_per_s": v["bytes_per_launch"] / (v["ms"] / max(v["launches"], 1) / 1e3) / 1e9
+                   if v["launches"] else None, "bytes_per_launch": v["bytes_per_launch"],
+                   "share_of_step": v["ms"] / ms_local if ms_local else None} for k, v in ktimes.items()}
+    pair_bytes = 2 * eng.bytes_per_product()
+    line = {
+        "metric": METRIC, "value": pairs_per_s, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.boards, world, {
+            "nnz_stored": int(sum(f.size() for _, f in boards)) if world == 1 else None,
+            "algorithmic_bytes_per_pair": pair_bytes if world == 1 else None,
+            "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2)}),
+        "roofline": {"bound": "hbm", "kernel": f"k_spmv[{dominant}]", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                     "traffic": ncu_traffic(dominant),
+                     "whole_pair_gb_per_s": pair_bytes / (ms_local / args.steps / 1e3) / 1e9 if world == 1 else None},
+        "kernels": kernels,
+        "e2e": {"value": e2e_steps / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": 8 * (nx + ny),
+                "d2h_bytes_per_step": 8 * (nx + ny), "api": "kr_engine_ax / kr_engine_atx (host pinned buffers)",
+                "steps": e2e_steps, "matches_device_path": check_ok},
+        "solver_iters_per_s": args.solver_iters / solver_s,
+        "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"],
+                   "checkpoint_every": 50},
+        "gpu_launches": gpu_launches,
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_product(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

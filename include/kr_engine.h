@@ -188,6 +188,27 @@ int kr_solver_best_response(kr_solver* s, int player, const double* opp, int64_t
 /* Kernel launches issued by the solver (its own kernels, not the engine's). */
 int64_t kr_solver_launches(const kr_solver* s);
 
+/* Incremental form of kr_solver_run, for drivers that combine boards held by
+ * several ranks between checkpoints (one allreduce of the gap scalars per
+ * checkpoint).  begin: zero regrets/averages and form the
+ * uniform strategies (solver.hpp:348-364); iterate: n DCFR iterations
+ * (365-388); checkpoint: best-response values of the current average profile
+ * per board (389-392, 325-331); averages: the normalised average strategies
+ * (400-401). */
+int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma);
+int kr_solver_iterate(kr_solver* s, int n);
+int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2);
+int kr_solver_averages(kr_solver* s, double* avg1, double* avg2);
+int kr_solver_iteration(const kr_solver* s);
+
+/* Per-kernel CUDA-event timing of the engine's SpMV launches (off by
+ * default).  When enabled every SpMV launch is bracketed by events on the
+ * engine's stream; kr_engine_kernel_times returns, for the four matrices
+ * [V^T, U|Ahat, U^T, Ahat^T|V], the number of launches, their summed
+ * milliseconds and the algorithmic bytes of one launch. */
+int kr_engine_set_timing(kr_engine* e, int enabled);
+int kr_engine_kernel_times(kr_engine* e, int64_t launches[4], double ms[4], double bytes[4]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1471,6 +1471,60 @@ inline DcfrResult dcfrSolve(const KronPayoff& kp, const GradientEngine& eng, con
     return res;
 }
 
+// The loop body of dcfrSolve (solver.hpp:365-392) split into begin /
+// iterate / checkpoint so a multi-rank test driver can combine boards between
+// checkpoints; the arithmetic is the same statements in the same order.
+struct DcfrState {
+    const KronPayoff* kp;
+    const GradientEngine* eng;
+    DcfrParams p;
+    RegretTable rt1, rt2;
+    Vec x1, x2;
+    double weightSum = 0;
+    int t = 0;
+    DcfrState(const KronPayoff& k, const GradientEngine& e) : kp(&k), eng(&e) {}
+    void begin(const DcfrParams& params) {
+        p = params;
+        rt1.init(0, kp->n1, kp->handCount(0));
+        rt2.init(1, kp->n2, kp->handCount(1));
+        weightSum = 0;
+        t = 0;
+        x1 = sequenceForm(kp->skeleton, rt1);
+        x2 = sequenceForm(kp->skeleton, rt2);
+    }
+    void iterate(int n) {
+        const Skeleton& sk = kp->skeleton;
+        for (int q = 0; q < n; ++q) {
+            const int tt = ++t;
+            Vec g1 = eng->Ax(x2);
+            cfrSweep(sk, rt1, g1);
+            x1 = sequenceForm(sk, rt1);
+            Vec g2 = eng->ATx(x1);
+            for (double& v : g2) v = -v;
+            cfrSweep(sk, rt2, g2);
+            x2 = sequenceForm(sk, rt2);
+            double ta = std::pow(double(tt), p.alpha), tb = std::pow(double(tt), p.beta);
+            double pos = ta / (ta + 1), neg = tb / (tb + 1);
+            discount(rt1, pos, neg);
+            discount(rt2, pos, neg);
+            double shrink = std::pow(double(tt) / (tt + 1), p.gamma);
+            for (size_t e = 0; e < x1.size(); ++e) rt1.avg[e] += x1[e];
+            for (size_t e = 0; e < x2.size(); ++e) rt2.avg[e] += x2[e];
+            weightSum += 1;
+            for (double& v : rt1.avg) v *= shrink;
+            for (double& v : rt2.avg) v *= shrink;
+            weightSum *= shrink;
+        }
+    }
+    void checkpoint(double* br1, double* br2) const {
+        Vec a1(rt1.avg.size()), a2(rt2.avg.size());
+        for (size_t e = 0; e < a1.size(); ++e) a1[e] = rt1.avg[e] / weightSum;
+        for (size_t e = 0; e < a2.size(); ++e) a2[e] = rt2.avg[e] / weightSum;
+        *br1 = bestResponseValue(*kp, *eng, 0, a2);
+        *br2 = bestResponseValue(*kp, *eng, 1, a1);
+    }
+};
+
 // ------------------------------------------------------------- instances ---
 // instances.hpp:19-29
 inline BettingConfig referenceBettingConfig() {

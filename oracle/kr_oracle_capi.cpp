@@ -362,6 +362,34 @@ int or_best_response(void* h, void* sp, int player, const double* opp, double* o
     });
 }
 
+// Incremental DCFR over one board (test driver for the multi-rank path).
+struct DcfrHandle {
+    FactoredEngine eng;
+    DcfrState st;
+    DcfrHandle(const KronPayoff& kp, const Sparsification& s) : eng(s), st(kp, eng) {}
+};
+int or_dcfr_state_create(void* h, void* sp, void** out) {
+    return guarded([&] {
+        *out = new DcfrHandle(static_cast<Inst*>(h)->kp, static_cast<Sp*>(sp)->s);
+    });
+}
+void or_dcfr_state_free(void* s) { delete static_cast<DcfrHandle*>(s); }
+int or_dcfr_begin(void* s, double alpha, double beta, double gamma) {
+    return guarded([&] {
+        DcfrParams p;
+        p.alpha = alpha;
+        p.beta = beta;
+        p.gamma = gamma;
+        static_cast<DcfrHandle*>(s)->st.begin(p);
+    });
+}
+int or_dcfr_iterate(void* s, int n) {
+    return guarded([&] { static_cast<DcfrHandle*>(s)->st.iterate(n); });
+}
+int or_dcfr_checkpoint(void* s, double* br1, double* br2) {
+    return guarded([&] { static_cast<DcfrHandle*>(s)->st.checkpoint(br1, br2); });
+}
+
 // engine: 0 factored (sp), 1 reference block formula, 2 dense
 // trace arrays sized >= number of checkpoints.  Returns trace length in *ntrace.
 int or_dcfr(void* h, void* sp, int engineKind, double alpha, double beta, double gamma, int maxIters,

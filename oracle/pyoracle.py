@@ -305,6 +305,42 @@ def best_response(inst, sp, player, opp):
     return out.value
 
 
+class DcfrBoards:
+    """Incremental oracle DCFR over independent boards (same interface as the
+    product's CudaSolver begin/iterate/checkpoint; multi-rank test stand-in)."""
+
+    def __init__(self, pairs):
+        self.pairs = pairs  # keep (Instance, Sparsification) alive
+        self.nboards = len(pairs)
+        self.hs = []
+        for inst, sp in pairs:
+            out = C.c_void_p()
+            _check(lib().or_dcfr_state_create(inst.h, sp.h, C.byref(out)))
+            self.hs.append(out)
+
+    def __del__(self):
+        if _LIB is not None:
+            for h in getattr(self, "hs", []):
+                _LIB.or_dcfr_state_free(h)
+            self.hs = []
+
+    def begin(self, alpha=1.5, beta=0.0, gamma=2.0):
+        for h in self.hs:
+            _check(lib().or_dcfr_begin(h, C.c_double(alpha), C.c_double(beta), C.c_double(gamma)))
+
+    def iterate(self, n):
+        for h in self.hs:
+            _check(lib().or_dcfr_iterate(h, int(n)))
+
+    def checkpoint(self):
+        b1, b2 = np.zeros(self.nboards), np.zeros(self.nboards)
+        for i, h in enumerate(self.hs):
+            x, y = C.c_double(), C.c_double()
+            _check(lib().or_dcfr_checkpoint(h, C.byref(x), C.byref(y)))
+            b1[i], b2[i] = x.value, y.value
+        return b1, b2
+
+
 def dcfr(inst, sp=None, engine="factored", alpha=1.5, beta=0.0, gamma=2.0, max_iters=1000, target=0.0,
          checkpoint_every=50):
     """dcfrSolve (solver.hpp:343-404).  Returns a dict with the trace."""

@@ -90,7 +90,8 @@ CUDA_SYMBOLS = [
     "kr_engine_atx", "kr_engine_ax_device", "kr_engine_atx_device", "kr_engine_flops", "kr_engine_last_flops",
     "kr_engine_stream", "kr_engine_device", "kr_engine_launches", "kr_host_alloc", "kr_host_free", "kr_last_error",
     "kr_device_count", "kr_solver_create", "kr_solver_destroy", "kr_solver_run", "kr_solver_best_response",
-    "kr_solver_launches",
+    "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
+    "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times",
 ]
 
 
@@ -135,6 +136,13 @@ def cuda():
                                                   C.POINTER(C.c_double), C.c_void_p]
             L.kr_solver_launches.restype = C.c_int64
             L.kr_solver_launches.argtypes = [C.c_void_p]
+            L.kr_solver_begin.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
+            L.kr_solver_iterate.argtypes = [C.c_void_p, C.c_int]
+            L.kr_solver_checkpoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.kr_solver_averages.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.kr_solver_iteration.argtypes = [C.c_void_p]
+        L.kr_engine_set_timing.argtypes = [C.c_void_p, C.c_int]
+        L.kr_engine_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _CUDA = L
     return _CUDA
 

@@ -123,6 +123,16 @@ struct kr_engine {
     double* d_out = nullptr;
     int64_t flops_total = 0, flops_last = 0, launches = 0;
     int64_t flops_per_product = 0;
+    // optional per-kernel event timing (kr_engine_set_timing)
+    bool timing = false;
+    struct Pending {
+        int which;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> eventPool;
+    int64_t tLaunches[4] = {0, 0, 0, 0};
+    double tMs[4] = {0, 0, 0, 0};
 };
 
 namespace krb {

@@ -696,6 +696,11 @@ void destroy_engine(kr_engine* e) {
     cudaFree(e->d_xp);
     cudaFree(e->d_in);
     cudaFree(e->d_out);
+    for (auto& p : e->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto ev : e->eventPool) cudaEventDestroy(ev);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -938,17 +943,53 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
     return e;
 }
 
-void launch_sell(kr_engine* e, const krb::DevSell& A, const double* xa, const double* xb, int64_t split, double* y,
-                 cudaStream_t s) {
+cudaEvent_t pool_event(kr_engine* e) {
+    if (!e->eventPool.empty()) {
+        cudaEvent_t ev = e->eventPool.back();
+        e->eventPool.pop_back();
+        return ev;
+    }
+    cudaEvent_t ev;
+    KR_CK(cudaEventCreate(&ev));
+    return ev;
+}
+
+void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* xa, const double* xb, int64_t split,
+                 double* y, cudaStream_t s) {
     const int64_t blocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock +
                            (A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return;
     SellView v{A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val, A.nslices,
                A.long_ptr, A.long_row, A.long_col, A.long_val, A.nlong};
+    kr_engine::Pending pend{which, nullptr, nullptr};
+    if (e->timing) {
+        pend.a = pool_event(e);
+        pend.b = pool_event(e);
+        KR_CK(cudaEventRecord(pend.a, s));
+    }
     if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
     else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
+    if (e->timing) {
+        KR_CK(cudaEventRecord(pend.b, s));
+        e->pending.push_back(pend);
+    }
     e->launches++;
+}
+
+// Algorithmic bytes of one launch of matrix `which`: fp64
+// values + int32 indices of the factor entries it streams, int32 outer
+// pointers of each merged factor, the input vector(s) read once and the
+// output written once; the intermediates t / z are excluded, as in the
+// per-matvec formula of BASELINE.md §2.
+double launch_bytes(const kr_engine* e, int which) {
+    const double R = double(e->rows), Cc = double(e->cols), K = double(e->k);
+    switch (which) {
+        case 0: return 12.0 * double(e->nnzV) + 4.0 * (K + 1) + 8.0 * Cc;
+        case 1: return 12.0 * double(e->nnzU + e->nnzA) + 8.0 * (R + 1) + 8.0 * Cc + 8.0 * R;
+        case 2: return 12.0 * double(e->nnzU) + 4.0 * (K + 1) + 8.0 * R;
+        default: return 12.0 * double(e->nnzA + e->nnzV) + 8.0 * (Cc + 1) + 8.0 * R + 8.0 * Cc;
+    }
 }
 
 void solve_forward(kr_engine* e, cudaStream_t s) {
@@ -1000,18 +1041,18 @@ void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) {
         e->launches++;
         xg = e->d_xp;
     }
-    launch_sell(e, e->VT, xg, nullptr, 0, e->d_tz, s);  // t = V^T x            engine.hpp:65-72
-    solve_forward(e, s);                                // z = M^-1 t           engine.hpp:74-78
-    launch_sell(e, e->UA, e->d_tz, x, e->k, y, s);      // y = U z + Ahat x     engine.hpp:81-89
+    launch_sell(e, 0, e->VT, xg, nullptr, 0, e->d_tz, s);  // t = V^T x          engine.hpp:65-72
+    solve_forward(e, s);                                   // z = M^-1 t         engine.hpp:74-78
+    launch_sell(e, 1, e->UA, e->d_tz, x, e->k, y, s);      // y = U z + Ahat x   engine.hpp:81-89
     e->flops_last = e->flops_per_product;
     e->flops_total += e->flops_last;
 }
 
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) {
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    launch_sell(e, e->UT, y, nullptr, 0, e->d_tz, s);      // s = U^T y          engine.hpp:103-110
-    solve_backward(e, s);                                  // z = M^-T s         engine.hpp:112-115
-    launch_sell(e, e->AV, y, e->d_tz, e->rows, x, s);      // x = Ahat^T y + V z  engine.hpp:117-130
+    launch_sell(e, 2, e->UT, y, nullptr, 0, e->d_tz, s);      // s = U^T y         engine.hpp:103-110
+    solve_backward(e, s);                                     // z = M^-T s        engine.hpp:112-115
+    launch_sell(e, 3, e->AV, y, e->d_tz, e->rows, x, s);      // x = Ahat^T y + V z  engine.hpp:117-130
     e->flops_last = e->flops_per_product;
     e->flops_total += e->flops_last;
 }
@@ -1108,6 +1149,37 @@ int kr_engine_atx_device(kr_engine* e, const double* y, double* x, void* stream)
         if (!e || !x || !y) throw Fail{KR_INVALID_INPUT, "null argument"};
         KR_CK(cudaSetDevice(e->device));
         krb::engine_atx(e, y, x, stream ? static_cast<cudaStream_t>(stream) : e->stream);
+    });
+}
+
+int kr_engine_set_timing(kr_engine* e, int enabled) {
+    return guarded([&] {
+        if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
+        e->timing = enabled != 0;
+    });
+}
+
+int kr_engine_kernel_times(kr_engine* e, int64_t launches[4], double ms[4], double bytes[4]) {
+    return guarded([&] {
+        if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
+        KR_CK(cudaSetDevice(e->device));
+        for (auto& p : e->pending) {
+            KR_CK(cudaEventSynchronize(p.b));
+            float t = 0;
+            KR_CK(cudaEventElapsedTime(&t, p.a, p.b));
+            e->tLaunches[p.which]++;
+            e->tMs[p.which] += double(t);
+            e->eventPool.push_back(p.a);
+            e->eventPool.push_back(p.b);
+        }
+        e->pending.clear();
+        for (int w = 0; w < 4; ++w) {
+            if (launches) launches[w] = e->tLaunches[w];
+            if (ms) ms[w] = e->tMs[w];
+            if (bytes) bytes[w] = krb::launch_bytes(e, w);
+            e->tLaunches[w] = 0;
+            e->tMs[w] = 0;
+        }
     });
 }
 

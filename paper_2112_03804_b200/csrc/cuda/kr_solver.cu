@@ -47,6 +47,11 @@ struct kr_solver {
     int* d_flag = nullptr;
     int nt[2] = {64, 64};       // hands per block of the step kernel
     int64_t launches = 0;
+    // incremental state (kr_solver_begin / iterate / checkpoint)
+    bool begun = false;
+    double alpha = 1.5, beta = 0.0, gamma = 2.0;
+    int t = 0;                  // iterations completed
+    double weightSum = 0;       // solver.hpp:354, 384-387
 };
 
 namespace krb {
@@ -409,6 +414,94 @@ int kr_solver_destroy(kr_solver* s) {
 
 int64_t kr_solver_launches(const kr_solver* s) { return s ? s->launches : 0; }
 
+namespace {
+void normalise_averages(kr_solver* s, cudaStream_t st) {
+    for (int p = 0; p < 2; ++p) {
+        const int64_t len = s->H[p] * s->n[p];
+        if (len == 0) continue;
+        krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, s->weightSum, s->a[p]);
+        KR_CK_LAUNCH();
+        s->launches++;
+    }
+}
+}  // namespace
+
+int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma) {
+    return guarded([&] {
+        if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
+        KR_CK(cudaSetDevice(s->device));
+        cudaStream_t st = s->eng->stream;
+        for (int p = 0; p < 2; ++p) {
+            const int64_t len = s->H[p] * s->n[p];
+            KR_CK(cudaMemsetAsync(s->regret[p], 0, 8 * size_t(len), st));
+            KR_CK(cudaMemsetAsync(s->avg[p], 0, 8 * size_t(len), st));
+        }
+        // x1, x2 = sequenceForm of zero regrets (solver.hpp:363-364)
+        krb::launch_step(s, 0, 0, nullptr, 0, 0, 0, 0, st);
+        krb::launch_step(s, 1, 0, nullptr, 0, 0, 0, 0, st);
+        s->alpha = alpha;
+        s->beta = beta;
+        s->gamma = gamma;
+        s->t = 0;
+        s->weightSum = 0;
+        s->begun = true;
+    });
+}
+
+int kr_solver_iterate(kr_solver* s, int n) {
+    return guarded([&] {
+        if (!s || !s->begun) throw Fail{KR_INVALID_INPUT, "kr_solver_begin must precede kr_solver_iterate"};
+        if (n < 0) throw Fail{KR_INVALID_INPUT, "negative iteration count"};
+        KR_CK(cudaSetDevice(s->device));
+        kr_engine* e = s->eng;
+        cudaStream_t st = e->stream;
+        for (int q = 0; q < n; ++q) {
+            const int t = ++s->t;  // solver.hpp:365-388
+            const double ta = std::pow(double(t), s->alpha), tb = std::pow(double(t), s->beta);
+            const double pos = ta / (ta + 1), neg = tb / (tb + 1);
+            const double shrink = std::pow(double(t) / (t + 1), s->gamma);
+            krb::engine_ax(e, s->x[1], s->g, st);                      // g1 = A x2
+            krb::launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st);  // P1 sweep/seqform/discount/avg
+            krb::engine_atx(e, s->x[0], s->g, st);                     // A^T x1
+            krb::launch_step(s, 1, 1, s->g, 1, pos, neg, shrink, st);  // P2 with g2 = -A^T x1
+            s->weightSum += 1;
+            s->weightSum *= shrink;
+        }
+    });
+}
+
+int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2) {
+    return guarded([&] {
+        if (!s || !s->begun || s->t < 1) throw Fail{KR_INVALID_INPUT, "no iterations to checkpoint"};
+        if (!board_br1 || !board_br2) throw Fail{KR_INVALID_INPUT, "null output arrays"};
+        KR_CK(cudaSetDevice(s->device));
+        cudaStream_t st = s->eng->stream;
+        normalise_averages(s, st);                            // solver.hpp:390-391
+        std::vector<double> b1, b2;
+        krb::best_response_dev(s, 0, s->a[1], b1, st);        // br1 vs avg2 (solver.hpp:327)
+        krb::best_response_dev(s, 1, s->a[0], b2, st);        // br2 vs avg1 (solver.hpp:328)
+        std::memcpy(board_br1, b1.data(), 8 * b1.size());
+        std::memcpy(board_br2, b2.data(), 8 * b2.size());
+    });
+}
+
+int kr_solver_averages(kr_solver* s, double* avg1, double* avg2) {
+    return guarded([&] {
+        if (!s || !s->begun || s->t < 1) throw Fail{KR_INVALID_INPUT, "no iterations to average"};
+        KR_CK(cudaSetDevice(s->device));
+        cudaStream_t st = s->eng->stream;
+        normalise_averages(s, st);                            // solver.hpp:400-401
+        for (int p = 0; p < 2; ++p) {
+            double* dst = p == 0 ? avg1 : avg2;
+            const int64_t len = s->H[p] * s->n[p];
+            if (dst && len) KR_CK(cudaMemcpyAsync(dst, s->a[p], 8 * size_t(len), cudaMemcpyDeviceToHost, st));
+        }
+        KR_CK(cudaStreamSynchronize(st));
+    });
+}
+
+int kr_solver_iteration(const kr_solver* s) { return s ? s->t : -1; }
+
 int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
     return guarded([&] {
         if (!s || !prm || !r) throw Fail{KR_INVALID_INPUT, "null argument to kr_solver_run"};
@@ -417,72 +510,52 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
         kr_engine* e = s->eng;
         KR_CK(cudaSetDevice(s->device));
         cudaStream_t st = e->stream;
-        for (int p = 0; p < 2; ++p) {
-            const int64_t len = s->H[p] * s->n[p];
-            KR_CK(cudaMemsetAsync(s->regret[p], 0, 8 * size_t(len), st));
-            KR_CK(cudaMemsetAsync(s->avg[p], 0, 8 * size_t(len), st));
-        }
         cudaEvent_t ev0, ev1;
         KR_CK(cudaEventCreate(&ev0));
         KR_CK(cudaEventCreate(&ev1));
         KR_CK(cudaEventRecord(ev0, st));
         const int64_t flops0 = e->flops_total;
-        // x1, x2 = sequenceForm of zero regrets (solver.hpp:363-364)
-        krb::launch_step(s, 0, 0, nullptr, 0, 0, 0, 0, st);
-        krb::launch_step(s, 1, 0, nullptr, 0, 0, 0, 0, st);
-        double weightSum = 0;
-        r->trace_len = 0;
-        std::vector<double> b1, b2;
-        int t = 1;
-        for (; t <= prm->max_iters; ++t) {
-            const double ta = std::pow(double(t), prm->alpha), tb = std::pow(double(t), prm->beta);
-            const double pos = ta / (ta + 1), neg = tb / (tb + 1);
-            const double shrink = std::pow(double(t) / (t + 1), prm->gamma);
-            krb::engine_ax(e, s->x[1], s->g, st);                       // g1 = A x2
-            krb::launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st);   // P1 sweep/seqform/discount/avg
-            krb::engine_atx(e, s->x[0], s->g, st);                      // A^T x1
-            krb::launch_step(s, 1, 1, s->g, 1, pos, neg, shrink, st);   // P2 with g2 = -A^T x1
-            weightSum += 1;
-            weightSum *= shrink;
-            if (t % prm->checkpoint_every == 0 || t == prm->max_iters) {
-                for (int p = 0; p < 2; ++p) {
-                    const int64_t len = s->H[p] * s->n[p];
-                    if (len == 0) continue;
-                    krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, weightSum,
-                                                                                  s->a[p]);
-                    KR_CK_LAUNCH();
-                    s->launches++;
-                }
-                krb::best_response_dev(s, 0, s->a[1], b1, st);  // br1 vs avg2 (solver.hpp:327)
-                krb::best_response_dev(s, 1, s->a[0], b2, st);  // br2 vs avg1 (solver.hpp:328)
-                double br1 = 0, br2 = 0, expl;
-                for (int b = 0; b < s->nboards; ++b) {
-                    br1 += b1[size_t(b)];
-                    br2 += b2[size_t(b)];
-                }
-                if (s->nboards == 1) {
-                    expl = (b1[0] + b2[0]) / 2 / s->pot;  // solver.hpp:329-330
-                } else {
-                    expl = 0;
-                    for (int b = 0; b < s->nboards; ++b) expl += (b1[size_t(b)] + b2[size_t(b)]) / 2 / s->pot;
-                    expl /= s->nboards;
-                }
-                const int i = r->trace_len;
-                if (i < r->trace_cap) {
-                    if (r->trace_iter) r->trace_iter[i] = t;
-                    if (r->trace_expl) r->trace_expl[i] = expl;
-                    if (r->trace_br1) r->trace_br1[i] = br1;
-                    if (r->trace_br2) r->trace_br2[i] = br2;
-                    for (int b = 0; b < s->nboards; ++b) {
-                        if (r->trace_board_br1) r->trace_board_br1[size_t(i) * s->nboards + b] = b1[size_t(b)];
-                        if (r->trace_board_br2) r->trace_board_br2[size_t(i) * s->nboards + b] = b2[size_t(b)];
-                    }
-                }
-                r->trace_len = i + 1;
-                r->iterations = t;
-                r->exploitability = expl;
-                if (prm->target_exploitability > 0 && expl <= prm->target_exploitability) break;
+        auto ck = [](int rc) {
+            if (rc != KR_OK) {
+                int code = 0;
+                throw Fail{rc, kr_last_error(&code)};
             }
+        };
+        ck(kr_solver_begin(s, prm->alpha, prm->beta, prm->gamma));
+        r->trace_len = 0;
+        std::vector<double> b1(size_t(s->nboards)), b2(size_t(s->nboards));
+        while (s->t < prm->max_iters) {
+            // run to the next checkpoint (t % every == 0 or t == maxIters)
+            const int next = std::min(prm->max_iters, (s->t / prm->checkpoint_every + 1) * prm->checkpoint_every);
+            ck(kr_solver_iterate(s, next - s->t));
+            ck(kr_solver_checkpoint(s, b1.data(), b2.data()));
+            double br1 = 0, br2 = 0, expl;
+            for (int b = 0; b < s->nboards; ++b) {
+                br1 += b1[size_t(b)];
+                br2 += b2[size_t(b)];
+            }
+            if (s->nboards == 1) {
+                expl = (b1[0] + b2[0]) / 2 / s->pot;  // solver.hpp:329-330
+            } else {
+                expl = 0;
+                for (int b = 0; b < s->nboards; ++b) expl += (b1[size_t(b)] + b2[size_t(b)]) / 2 / s->pot;
+                expl /= s->nboards;
+            }
+            const int i = r->trace_len;
+            if (i < r->trace_cap) {
+                if (r->trace_iter) r->trace_iter[i] = s->t;
+                if (r->trace_expl) r->trace_expl[i] = expl;
+                if (r->trace_br1) r->trace_br1[i] = br1;
+                if (r->trace_br2) r->trace_br2[i] = br2;
+                for (int b = 0; b < s->nboards; ++b) {
+                    if (r->trace_board_br1) r->trace_board_br1[size_t(i) * s->nboards + b] = b1[size_t(b)];
+                    if (r->trace_board_br2) r->trace_board_br2[size_t(i) * s->nboards + b] = b2[size_t(b)];
+                }
+            }
+            r->trace_len = i + 1;
+            r->iterations = s->t;
+            r->exploitability = expl;
+            if (prm->target_exploitability > 0 && expl <= prm->target_exploitability) break;
         }
         KR_CK(cudaEventRecord(ev1, st));
         KR_CK(cudaEventSynchronize(ev1));
@@ -491,17 +564,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
         r->seconds = ms / 1e3;
         cudaEventDestroy(ev0);
         cudaEventDestroy(ev1);
-        // final averages (solver.hpp:400-401)
-        for (int p = 0; p < 2; ++p) {
-            double* dst = p == 0 ? r->avg1 : r->avg2;
-            const int64_t len = s->H[p] * s->n[p];
-            if (!dst || len == 0) continue;
-            krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, weightSum, s->a[p]);
-            KR_CK_LAUNCH();
-            s->launches++;
-            KR_CK(cudaMemcpyAsync(dst, s->a[p], 8 * size_t(len), cudaMemcpyDeviceToHost, st));
-        }
-        KR_CK(cudaStreamSynchronize(st));
+        if (r->avg1 || r->avg2) ck(kr_solver_averages(s, r->avg1, r->avg2));
         r->gradient_flops = e->flops_total - flops0;
     });
 }

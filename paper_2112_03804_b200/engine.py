@@ -103,6 +103,21 @@ class CudaEngine:
             b += 12 * (nz["m"] - self.k) + 4 * (self.k + 1)
         return b
 
+    # -- per-kernel event timing (kr_engine_set_timing) -------------------
+    KERNELS = ("VT", "UA", "UT", "AV")  # V^T x | [U|Ahat][z;x] | U^T y | [Ahat^T|V][y;z]
+
+    def set_timing(self, enabled=True):
+        N.check(N.cuda().kr_engine_set_timing(self._h, int(enabled)))
+
+    def kernel_times(self):
+        """Per SpMV matrix since the last call: launches, total ms, algorithmic
+        bytes of one launch."""
+        n = np.zeros(4, np.int64)
+        ms, by = np.zeros(4), np.zeros(4)
+        N.check(N.cuda().kr_engine_kernel_times(self._h, N.ptr(n), N.ptr(ms), N.ptr(by)))
+        return {k: {"launches": int(n[i]), "ms": float(ms[i]), "bytes_per_launch": float(by[i])}
+                for i, k in enumerate(self.KERNELS)}
+
     # -- device-pointer variants (torch tensors on the engine's device) ----
     @property
     def stream(self):

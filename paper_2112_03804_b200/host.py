@@ -230,11 +230,14 @@ def turn_boards(turn="Ks7d4c2h", nboards=48, tree=3, seed_base=1000):
     return [(c, seed_base + ranks.index(c[0]) * 4 + suits.index(c[1])) for c in cards]
 
 
-def turn_instances(turn="Ks7d4c2h", nboards=48, tree=3, threads=None):
+def turn_instances(turn="Ks7d4c2h", nboards=48, tree=3, threads=None, indices=None):
     """Build the turn's river instances (and B-post factors) in parallel threads
-    (libkrhost releases the GIL inside each ctypes call)."""
+    (libkrhost releases the GIL inside each ctypes call).  `indices` selects a
+    subset of the boards (a rank's shard)."""
     from concurrent.futures import ThreadPoolExecutor
     specs = turn_boards(turn, nboards, tree)
+    if indices is not None:
+        specs = [specs[i] for i in indices]
 
     def one(spec):
         card, seed = spec

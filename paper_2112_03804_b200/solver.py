@@ -123,6 +123,29 @@ class CudaSolver:
                           bb2[:n * self.nboards].reshape(n, self.nboards), a1, a2, res.seconds,
                           self.launches() + self.engine.launches() - launches0)
 
+    # -- incremental interface (multi-rank drivers, dist.py) ----------------
+    def begin(self, params: DcfrParams = None):
+        p = params or DcfrParams()
+        N.check(N.cuda().kr_solver_begin(self._h, p.alpha, p.beta, p.gamma))
+
+    def iterate(self, n):
+        N.check(N.cuda().kr_solver_iterate(self._h, int(n)))
+
+    def checkpoint(self):
+        """Per-board best-response values (br1, br2) of the current averages."""
+        b1, b2 = np.zeros(self.nboards), np.zeros(self.nboards)
+        N.check(N.cuda().kr_solver_checkpoint(self._h, N.ptr(b1), N.ptr(b2)))
+        return b1, b2
+
+    def averages(self):
+        a1, a2 = np.zeros(self.rows), np.zeros(self.cols)
+        N.check(N.cuda().kr_solver_averages(self._h, N.ptr(a1), N.ptr(a2)))
+        return a1, a2
+
+    @property
+    def iteration(self):
+        return int(N.cuda().kr_solver_iteration(self._h))
+
     def best_response(self, player, opp, per_board=False):
         """bestResponseValue (solver.hpp:292-321) against a host strategy."""
         opp = np.ascontiguousarray(opp, np.float64)
