@@ -100,10 +100,15 @@ struct kr_engine {
     krb::DevSell UA;  // y = [U | Ahat] [z ; x]         engine.hpp:81-89
     krb::DevSell UT;  // s = U^T y                      engine.hpp:103-110
     krb::DevSell AV;  // x = [Ahat^T | V] [y ; z]       engine.hpp:117-130
-    // chains (mkind 1): chain c = positions [chain_ptr[c], chain_ptr[c+1]);
-    // chain_mul[p] = M(p, p-1) in the relabelled space; chain_neg1[c] = all -1.
-    int64_t nchains = 0;
+    // chains (mkind 1), chain-sliced: slice s holds 32 chains, element j of
+    // lane l's chain at position chain_ptr[s] + 32 j + l (j < chain_len);
+    // chain_mul[p] = M(t, previous t of the chain); chain_neg1 = all -1.
+    int64_t kpad = 0;       // internal k positions (>= k; padding never touched)
+    int64_t nchains = 0;    // number of chain slices
+    bool chain_tma = true;  // TMA bulk-copy pipeline (else register pipeline)
+    int chain_withmul = 0;  // some chain has a multiplier other than -1
     int64_t* chain_ptr = nullptr;
+    int32_t* chain_len = nullptr;
     double* chain_mul = nullptr;
     uint8_t* chain_neg1 = nullptr;
     // levels (mkind 2): forward uses strict-lower CSR(M), backward CSC(M)

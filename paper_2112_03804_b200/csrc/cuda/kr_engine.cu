@@ -192,120 +192,279 @@ __global__ void k_seq_major(const double* __restrict__ x, int64_t M2, int32_t n2
     xp[int64_t(s) * M2 + J] = x[q];
 }
 
-constexpr int kChainChunk = 512;
+constexpr int kChainU = 8;  // chain elements per lane per pipeline stage
 
-// Forward solve M z = t along chains (engine.hpp:31-41 restricted to <=1
-// off-diagonal per row/column), one warp per chain.  The warp stages a chunk
-// of the (contiguous, chain-major) chain in shared memory with coalesced
-// loads; lane 0 then runs the exact serial recurrence
-//   z_p = (z_{p-1} != 0) ? t_p - M(p,p-1) z_{p-1} : t_p
-// (for M(p,p-1) == -1 this is exactly t_p + z_{p-1}), one dependent add per
-// element, and the warp stores the chunk back.
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    k_chain_forward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
-                    const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
-    __shared__ double T[kWarpsPerBlock][kChainChunk];
-    __shared__ double Mu[kWarpsPerBlock][kChainChunk];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t c = int64_t(blockIdx.x) * kWarpsPerBlock + w;
-    if (c >= nchains) return;
-    const int64_t a = cptr[c], b = cptr[c + 1];
-    const bool allneg = neg1[c] != 0;
-    double prev = 0.0;
-    for (int64_t k0 = a; k0 < b; k0 += kChainChunk) {
-        const int n = int(lmin(kChainChunk, b - k0));
-        for (int q = lane; q < n; q += 32) {
-            T[w][q] = z[k0 + q];
-            if (!allneg) Mu[w][q] = cmul[k0 + q];
+// ---- TMA bulk-copy pipeline for the chain solves -------------------------
+// A chain slice is contiguous: row j (element j of its 32 chains) is 256
+// bytes.  One warp per slice streams chunks of kChunkRows rows into a
+// kStages-deep shared-memory ring with cp.async.bulk (TMA, completion on an
+// mbarrier), so ~kStages*kChunkRows rows are in flight while each lane runs
+// its chain's serial recurrence out of shared memory.
+constexpr int kChunkRows = 32;  // rows per stage (8 KB)
+constexpr int kStages = 8;      // 256 rows (64 KB) in flight per slice
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Chain solve over one slice per block (32 threads).  dir = +1 forward
+// (engine.hpp:31-41), -1 backward (engine.hpp:44-54); same recurrences as
+// the register kernels above.
+// Dynamic shared memory: kStages chunks of t (and of the multipliers when
+// the engine has any chain whose multipliers are not all -1: withMul).
+template <int DIR>
+__global__ void __launch_bounds__(32)
+    k_chain_tma(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int withMul,
+                double* __restrict__ z) {
+    extern __shared__ __align__(128) double dsm[];
+    __shared__ __align__(8) uint64_t bar[kStages];
+    double(*Tb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm);
+    double(*Mb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm + kStages * kChunkRows * 32);
+    const int lane = threadIdx.x;
+    const int64_t s = blockIdx.x;
+    const int64_t b0 = sbase[s];
+    const int32_t width = int32_t((sbase[s + 1] - b0) / 32);
+    const int32_t len = slen[s * 32 + lane];
+    const bool allneg = neg1[s * 32 + lane] != 0;
+    const bool needMul = withMul && __any_sync(0xffffffffu, !allneg);
+    const int nChunks = (width + kChunkRows - 1) / kChunkRows;
+    if (lane == 0)
+        for (int q = 0; q < kStages; ++q) mbar_init(&bar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    // chunk c covers rows [r0, r0 + n); forward chunks ascend, backward descend
+    auto chunk_rows = [&](int c, int32_t& r0, int32_t& n) {
+        if (DIR > 0) {
+            r0 = c * kChunkRows;
+            n = min(kChunkRows, width - r0);
+        } else {
+            const int32_t r1 = width - c * kChunkRows;
+            r0 = max(0, r1 - kChunkRows);
+            n = r1 - r0;
         }
-        __syncwarp();
-        if (lane == 0) {
-            // batches of 8: shared-memory loads issued together, then the
-            // dependent recurrence, then the stores
+    };
+    auto issue = [&](int c) {
+        if (lane == 0 && c < nChunks) {
+            int32_t r0, n;
+            chunk_rows(c, r0, n);
+            const int st = c % kStages;
+            const uint32_t bytes = uint32_t(n) * 32 * 8;
+            mbar_expect_tx(&bar[st], needMul ? 2 * bytes : bytes);
+            bulk_g2s(Tb[st], z + b0 + int64_t(r0) * 32, bytes, &bar[st]);
+            if (needMul) bulk_g2s(Mb[st], cmul + b0 + int64_t(r0) * 32, bytes, &bar[st]);
+        }
+    };
+    for (int c = 0; c < kStages - 1; ++c) issue(c);
+    double carry = 0.0, mulNext = 0.0;
+    for (int c = 0; c < nChunks; ++c) {
+        issue(c + kStages - 1);
+        const int st = c % kStages;
+        mbar_wait(&bar[st], uint32_t((c / kStages) & 1));
+        int32_t r0, n;
+        chunk_rows(c, r0, n);
+        const double* T = Tb[st];
+        const double* Mu = Mb[st];
+        double* zc = z + b0 + lane;
+        // Branch-free batches of 8: the shared-memory loads of a batch are
+        // issued together; each element costs one dependent DADD (+ select).
+        // Rows past n or past the lane's chain length are computed and
+        // discarded (predicated store, carry kept).
+        if (!needMul) {  // every multiplier is -1: z_p = t_p + z_{p-1}
             for (int q0 = 0; q0 < n; q0 += 8) {
-                double t[8], m[8];
+                double t[8];
+                if (DIR > 0) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    t[u] = q0 + u < n ? T[w][q0 + u] : 0.0;
-                    m[u] = (!allneg && q0 + u < n) ? Mu[w][q0 + u] : -1.0;
-                }
+                    for (int u = 0; u < 8; ++u) t[u] = T[(q0 + u) * 32 + lane];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (q0 + u < n) {
-                        double zq = t[u];
-                        if (k0 + q0 + u != a) {
-                            if (allneg) zq = t[u] + prev;
-                            else if (prev != 0.0) zq = t[u] - m[u] * prev;
-                        }
-                        t[u] = zq;
-                        prev = zq;
+                    for (int u = 0; u < 8; ++u) {
+                        const int32_t j = r0 + q0 + u;
+                        const double zq = j == 0 ? t[u] : t[u] + carry;
+                        const bool ok = q0 + u < n && j < len;
+                        if (ok) zc[int64_t(j) * 32] = zq;
+                        carry = ok ? zq : carry;
                     }
+                } else {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (q0 + u < n) T[w][q0 + u] = t[u];
+                    for (int u = 0; u < 8; ++u) t[u] = T[(n - 1 - q0 - u >= 0 ? n - 1 - q0 - u : 0) * 32 + lane];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int32_t q = n - 1 - q0 - u;
+                        const int32_t j = r0 + q;
+                        const double zq = j == len - 1 ? t[u] : t[u] + carry;
+                        const bool ok = q >= 0 && j < len;
+                        if (ok) zc[int64_t(j) * 32] = zq;
+                        carry = ok ? zq : carry;
+                    }
+                }
+            }
+        } else if (DIR > 0) {
+            for (int q = 0; q < n; ++q) {
+                const int32_t j = r0 + q;
+                if (j < len) {
+                    const double tq = T[q * 32 + lane];
+                    double zq = tq;
+                    if (j != 0) {
+                        if (allneg) zq = tq + carry;
+                        else if (carry != 0.0) zq = tq - Mu[q * 32 + lane] * carry;
+                    }
+                    zc[int64_t(j) * 32] = zq;
+                    carry = zq;
+                }
+            }
+        } else {
+            for (int q = n - 1; q >= 0; --q) {
+                const int32_t j = r0 + q;
+                if (j < len) {
+                    const double tq = T[q * 32 + lane];
+                    double zq;
+                    if (allneg) {
+                        zq = j != len - 1 ? tq + carry : tq;
+                    } else {
+                        double acc = 0.0;
+                        if (j != len - 1) acc += mulNext * carry;
+                        zq = tq - acc;
+                        mulNext = Mu[q * 32 + lane];
+                    }
+                    zc[int64_t(j) * 32] = zq;
+                    carry = zq;
+                }
             }
         }
+        // all lanes are done reading this stage before TMA refills it
         __syncwarp();
-        for (int q = lane; q < n; q += 32) z[k0 + q] = T[w][q];
-        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
 }
 
-// Backward solve M^T z = s along chains (engine.hpp:44-54), one warp per
-// chain walked in reverse by lane 0: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
+// Forward solve M z = t along chains (engine.hpp:31-41 restricted to <=1
+// off-diagonal per row/column).  Chain-sliced layout: a warp owns 32 chains,
+// lane l walks chain l whose element j sits at base + 32 j + l, so every
+// load and store is coalesced across the warp and each lane runs the exact
+// serial recurrence of its chain from registers:
+//   z_p = (z_{p-1} != 0) ? t_p - M(p,p-1) z_{p-1} : t_p
+// (for M(p,p-1) == -1 this is bitwise t_p + z_{p-1}: one dependent add).
+// The next stage's loads are issued before the current stage's adds.
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    k_chain_backward(const int64_t* __restrict__ cptr, const double* __restrict__ cmul,
-                     const uint8_t* __restrict__ neg1, int64_t nchains, double* __restrict__ z) {
-    __shared__ double T[kWarpsPerBlock][kChainChunk];
-    __shared__ double Mu[kWarpsPerBlock][kChainChunk];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t c = int64_t(blockIdx.x) * kWarpsPerBlock + w;
-    if (c >= nchains) return;
-    const int64_t a = cptr[c], b = cptr[c + 1];
-    const bool allneg = neg1[c] != 0;
-    double next = 0.0, mulNext = 0.0;
-    bool have = false;
-    for (int64_t k1 = b; k1 > a; k1 -= kChainChunk) {
-        const int n = int(lmin(kChainChunk, k1 - a));
-        const int64_t k0 = k1 - n;
-        for (int q = lane; q < n; q += 32) {
-            T[w][q] = z[k0 + q];
-            if (!allneg) Mu[w][q] = cmul[k0 + q];
+    k_chain_forward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                    const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t nslices,
+                    double* __restrict__ z) {
+    const int64_t s = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s >= nslices) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t len = slen[s * 32 + lane];
+    const bool allneg = neg1[s * 32 + lane] != 0;
+    double* zc = z + sbase[s] + lane;
+    const double* mc = cmul + sbase[s] + lane;
+    double prev = 0.0;
+    double t[kChainU], m[kChainU];
+#pragma unroll
+    for (int u = 0; u < kChainU; ++u) {
+        t[u] = u < len ? zc[int64_t(u) * 32] : 0.0;
+        m[u] = (!allneg && u < len) ? mc[int64_t(u) * 32] : -1.0;
+    }
+    for (int32_t j0 = 0; j0 < len; j0 += kChainU) {
+        double tn[kChainU], mn[kChainU];
+#pragma unroll
+        for (int u = 0; u < kChainU; ++u) {
+            const int32_t j = j0 + kChainU + u;
+            tn[u] = j < len ? zc[int64_t(j) * 32] : 0.0;
+            mn[u] = (!allneg && j < len) ? mc[int64_t(j) * 32] : -1.0;
         }
-        __syncwarp();
-        if (lane == 0) {
-            for (int q1 = n; q1 > 0; q1 -= 8) {
-                double t[8], m[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int q = q1 - 1 - u;
-                    t[u] = q >= 0 ? T[w][q] : 0.0;
-                    m[u] = (!allneg && q >= 0) ? Mu[w][q] : -1.0;
+        for (int u = 0; u < kChainU; ++u) {
+            const int32_t j = j0 + u;
+            if (j < len) {
+                double zq = t[u];
+                if (j != 0) {
+                    if (allneg) zq = t[u] + prev;
+                    else if (prev != 0.0) zq = t[u] - m[u] * prev;
                 }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (q1 - 1 - u >= 0) {
-                        double zq;
-                        if (allneg) {
-                            zq = have ? t[u] + next : t[u];
-                        } else {
-                            double acc = 0.0;
-                            if (have) acc += mulNext * next;
-                            zq = t[u] - acc;
-                            mulNext = m[u];
-                        }
-                        t[u] = zq;
-                        next = zq;
-                        have = true;
-                    }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (q1 - 1 - u >= 0) T[w][q1 - 1 - u] = t[u];
+                zc[int64_t(j) * 32] = zq;
+                prev = zq;
             }
         }
-        __syncwarp();
-        for (int q = lane; q < n; q += 32) z[k0 + q] = T[w][q];
-        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kChainU; ++u) {
+            t[u] = tn[u];
+            m[u] = mn[u];
+        }
+    }
+}
+
+// Backward solve M^T z = s along chains (engine.hpp:44-54), same layout,
+// each lane walking its chain in reverse: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_chain_backward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t nslices,
+                     double* __restrict__ z) {
+    const int64_t s = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s >= nslices) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t len = slen[s * 32 + lane];
+    const bool allneg = neg1[s * 32 + lane] != 0;
+    double* zc = z + sbase[s] + lane;
+    const double* mc = cmul + sbase[s] + lane;
+    double next = 0.0, mulNext = 0.0;
+    double t[kChainU], m[kChainU];
+#pragma unroll
+    for (int u = 0; u < kChainU; ++u) {
+        const int32_t j = len - 1 - u;
+        t[u] = j >= 0 ? zc[int64_t(j) * 32] : 0.0;
+        m[u] = (!allneg && j >= 0) ? mc[int64_t(j) * 32] : -1.0;
+    }
+    for (int32_t j1 = len - 1; j1 >= 0; j1 -= kChainU) {
+        double tn[kChainU], mn[kChainU];
+#pragma unroll
+        for (int u = 0; u < kChainU; ++u) {
+            const int32_t j = j1 - kChainU - u;
+            tn[u] = j >= 0 ? zc[int64_t(j) * 32] : 0.0;
+            mn[u] = (!allneg && j >= 0) ? mc[int64_t(j) * 32] : -1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kChainU; ++u) {
+            const int32_t j = j1 - u;
+            if (j >= 0) {
+                double zq;
+                if (allneg) {
+                    zq = j != len - 1 ? t[u] + next : t[u];
+                } else {
+                    double acc = 0.0;
+                    if (j != len - 1) acc += mulNext * next;
+                    zq = t[u] - acc;
+                    mulNext = m[u];
+                }
+                zc[int64_t(j) * 32] = zq;
+                next = zq;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kChainU; ++u) {
+            t[u] = tn[u];
+            m[u] = mn[u];
+        }
     }
 }
 
@@ -339,10 +498,11 @@ __global__ void k_level_backward(const int32_t* __restrict__ cols, int64_t n, co
 
 // ------------------------------------------------------- host building ----
 
-struct HostRows {  // one board's matrix in OUTPUT-row order, final indices
+struct HostRows {  // one board's matrix in processing order, final indices
     std::vector<int64_t> ptr{0};
     std::vector<int32_t> col;
     std::vector<double> val;
+    std::vector<int32_t> outRow;  // output row of each row (empty: rowBase + r)
     void push(int32_t c, double v) {
         col.push_back(c);
         val.push_back(v);
@@ -397,7 +557,7 @@ void to_sell(const HostRows& h, int64_t rowBase, int64_t longRow, HostSell& out)
         for (int64_t r = w0; r < w1; ++r) {
             const int64_t len = h.ptr[r + 1] - h.ptr[r];
             if (len > longRow) {
-                out.lgrow.push_back(int32_t(rowBase + r));
+                out.lgrow.push_back(h.outRow.empty() ? int32_t(rowBase + r) : h.outRow[size_t(r)]);
                 out.lcol.insert(out.lcol.end(), h.col.begin() + h.ptr[r], h.col.begin() + h.ptr[r + 1]);
                 out.lval.insert(out.lval.end(), h.val.begin() + h.ptr[r], h.val.begin() + h.ptr[r + 1]);
                 out.lptr.push_back(int64_t(out.lcol.size()));
@@ -419,7 +579,7 @@ void to_sell(const HostRows& h, int64_t rowBase, int64_t longRow, HostSell& out)
                 if (q < idx.size()) {
                     const int64_t r = idx[q];
                     const int64_t len = h.ptr[r + 1] - h.ptr[r];
-                    out.lrow.push_back(int32_t(rowBase + r));
+                    out.lrow.push_back(h.outRow.empty() ? int32_t(rowBase + r) : h.outRow[size_t(r)]);
                     out.llen.push_back(int32_t(len));
                     for (int64_t j = 0; j < len; ++j) {
                         out.col[at + size_t(32 * j + l)] = h.col[size_t(h.ptr[r] + j)];
@@ -555,11 +715,16 @@ struct BoardPlan {
     int64_t rowOff = 0, colOff = 0, kOff = 0;
     int mkind = 0;
     std::string why;
-    // chain-major relabelling of this board's k coordinates (local)
-    std::vector<int32_t> pos;     // t -> position
-    std::vector<int32_t> at;      // position -> t
-    std::vector<int64_t> chains;  // local chain starts (+ terminal)
-    std::vector<double> mul;      // per position: M(p, p-1)
+    // chain-sliced relabelling of this board's k coordinates (local): chains
+    // sorted by length are cut into slices of 32; element j of the chain in
+    // lane l of slice s sits at position sbase[s] + 32 j + l.
+    int64_t kpad = 0;              // positions incl. padding (>= k)
+    std::vector<int32_t> pos;      // t -> position
+    std::vector<int32_t> at;       // position -> t, -1 = padding
+    std::vector<double> mul;       // per position: M(t, previous t in chain)
+    std::vector<int64_t> sbase;    // per slice
+    std::vector<int32_t> slen;     // per slice lane: chain length
+    std::vector<uint8_t> sneg;     // per slice lane: all multipliers are -1
     // SELL sizes and offsets in the combined arrays
     int64_t sl[4] = {0, 0, 0, 0}, pad[4] = {0, 0, 0, 0}, slOff[4] = {0, 0, 0, 0}, padOff[4] = {0, 0, 0, 0};
     int64_t nl[4] = {0, 0, 0, 0}, nlz[4] = {0, 0, 0, 0}, nlOff[4] = {0, 0, 0, 0}, nlzOff[4] = {0, 0, 0, 0};
@@ -570,13 +735,16 @@ void build_chain_order(BoardPlan& p, bool chainMode) {
     const int64_t k = f.k;
     p.pos.assign(static_cast<size_t>(k), 0);
     p.at.clear();
-    p.chains.assign(1, 0);
     p.mul.clear();
+    p.sbase.clear();
+    p.slen.clear();
+    p.sneg.clear();
     if (!chainMode) {
         for (int64_t t = 0; t < k; ++t) {
             p.pos[t] = int32_t(t);
             p.at.push_back(int32_t(t));
         }
+        p.kpad = k;
         return;
     }
     std::vector<int64_t> nxt(static_cast<size_t>(k), -1);
@@ -588,20 +756,65 @@ void build_chain_order(BoardPlan& p, bool chainMode) {
             mulOf[size_t(f.m.inner[q])] = f.m.val[q];
             hasPrev[size_t(f.m.inner[q])] = 1;
         }
+    std::vector<std::vector<int32_t>> chains;
     for (int64_t j = 0; j < k; ++j) {
         if (hasPrev[j]) continue;
-        for (int64_t r = j; r >= 0; r = nxt[r]) {
-            p.pos[r] = int32_t(p.at.size());
-            p.at.push_back(int32_t(r));
-            p.mul.push_back(mulOf[r]);
-        }
-        p.chains.push_back(int64_t(p.at.size()));
+        chains.emplace_back();
+        for (int64_t r = j; r >= 0; r = nxt[r]) chains.back().push_back(int32_t(r));
     }
+    std::stable_sort(chains.begin(), chains.end(),
+                     [](const std::vector<int32_t>& a, const std::vector<int32_t>& b) { return a.size() > b.size(); });
+    int64_t cur = 0;
+    for (size_t s0 = 0; s0 < chains.size(); s0 += 32) {
+        const int64_t width = int64_t(chains[s0].size());
+        p.sbase.push_back(cur);
+        p.at.resize(size_t(cur + 32 * width), -1);
+        p.mul.resize(size_t(cur + 32 * width), 0.0);
+        for (int l = 0; l < 32; ++l) {
+            const size_t c = s0 + size_t(l);
+            if (c >= chains.size()) {
+                p.slen.push_back(0);
+                p.sneg.push_back(1);
+                continue;
+            }
+            bool neg = true;
+            for (size_t j = 0; j < chains[c].size(); ++j) {
+                const int32_t t = chains[c][j];
+                const int64_t q = cur + 32 * int64_t(j) + l;
+                p.pos[size_t(t)] = int32_t(q);
+                p.at[size_t(q)] = t;
+                p.mul[size_t(q)] = mulOf[size_t(t)];
+                if (j > 0 && mulOf[size_t(t)] != -1.0) neg = false;
+            }
+            p.slen.push_back(int32_t(chains[c].size()));
+            p.sneg.push_back(neg ? 1 : 0);
+        }
+        cur += 32 * width;
+    }
+    p.kpad = cur;
 }
 
-// The four matrices of one board in output-row order with final indices.
-//  which 0: VT (rows = positions), 1: UA (rows = Ahat rows), 2: UT (rows =
-//  positions), 3: AV (rows = Ahat cols).
+// Real k positions of a board in chain-major order (chain by chain, element
+// by element): the order V^T and U^T rows are processed in, which keeps the
+// rows of one window on one showdown sequence (one stripe of x') while the
+// results land at their chain-sliced positions.
+std::vector<int64_t> k_order(const BoardPlan& p) {
+    std::vector<int64_t> out;
+    out.reserve(size_t(p.f->k));
+    if (p.sbase.empty()) {
+        for (int64_t q = 0; q < p.kpad; ++q)
+            if (p.at[size_t(q)] >= 0) out.push_back(q);
+        return out;
+    }
+    for (size_t s = 0; s < p.sbase.size(); ++s)
+        for (int l = 0; l < 32; ++l)
+            for (int32_t j = 0; j < p.slen[s * 32 + size_t(l)]; ++j) out.push_back(p.sbase[s] + 32 * int64_t(j) + l);
+    return out;
+}
+
+// The four matrices of one board in processing order with final indices.
+//  which 0: VT (rows = k positions), 1: UA (rows = Ahat rows), 2: UT (rows =
+//  k positions), 3: AV (rows = Ahat cols).
 void board_rows(const BoardPlan& p, int which, int64_t R, int64_t K, bool xseq, int64_t M2, int32_t n2,
                 HostRows& h) {
     const kr_factors& f = *p.f;
@@ -612,10 +825,11 @@ void board_rows(const BoardPlan& p, int which, int64_t R, int64_t K, bool xseq, 
     };
     auto kcol = [&](int64_t t) -> int32_t { return int32_t(p.kOff + p.pos[size_t(t)]); };
     if (which == 0) {
-        for (int64_t q = 0; q < f.k; ++q) {
+        for (int64_t q : k_order(p)) {
             const int64_t t = p.at[size_t(q)];
             for (int64_t e = f.v.outer[t]; e < f.v.outer[t + 1]; ++e) h.push(xcol(f.v.inner[e]), f.v.val[e]);
             h.endRow();
+            h.outRow.push_back(int32_t(p.kOff + q));
         }
     } else if (which == 1) {
         for (int64_t i = 0; i < f.rows; ++i) {
@@ -629,10 +843,11 @@ void board_rows(const BoardPlan& p, int which, int64_t R, int64_t K, bool xseq, 
         std::vector<int32_t> ti;
         std::vector<double> tv;
         transpose_into(f.rows, f.k, f.u.outer, f.u.inner, f.u.val, tp, ti, tv);
-        for (int64_t q = 0; q < f.k; ++q) {
+        for (int64_t q : k_order(p)) {
             const int64_t t = p.at[size_t(q)];
             for (int64_t e = tp[t]; e < tp[t + 1]; ++e) h.push(int32_t(p.rowOff + ti[e]), tv[e]);
             h.endRow();
+            h.outRow.push_back(int32_t(p.kOff + q));
         }
     } else {
         std::vector<int64_t> ap, vp;
@@ -655,7 +870,7 @@ std::vector<int64_t> board_lengths(const BoardPlan& p, int which) {
     const kr_factors& f = *p.f;
     std::vector<int64_t> L;
     if (which == 0) {
-        for (int64_t q = 0; q < f.k; ++q) {
+        for (int64_t q : k_order(p)) {
             const int64_t t = p.at[size_t(q)];
             L.push_back(f.v.outer[t + 1] - f.v.outer[t]);
         }
@@ -665,7 +880,7 @@ std::vector<int64_t> board_lengths(const BoardPlan& p, int which) {
     } else if (which == 2) {
         std::vector<int64_t> cnt(static_cast<size_t>(f.k), 0);
         for (int64_t e = 0; e < f.u.outer[f.rows]; ++e) cnt[size_t(f.u.inner[e])]++;
-        for (int64_t q = 0; q < f.k; ++q) L.push_back(cnt[size_t(p.at[size_t(q)])]);
+        for (int64_t q : k_order(p)) L.push_back(cnt[size_t(p.at[size_t(q)])]);
     } else {
         L.assign(static_cast<size_t>(f.cols), 0);
         for (int64_t e = 0; e < f.ahat.outer[f.rows]; ++e) L[size_t(f.ahat.inner[e])]++;
@@ -682,6 +897,7 @@ void destroy_engine(kr_engine* e) {
     free_sell(e->UT);
     free_sell(e->AV);
     cudaFree(e->chain_ptr);
+    cudaFree(e->chain_len);
     cudaFree(e->chain_mul);
     cudaFree(e->chain_neg1);
     cudaFree(e->lvl_fwd_rows);
@@ -812,6 +1028,15 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             build_chain_order(p, chainMode);
             for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), longRow, p.sl[w], p.pad[w], p.nl[w], p.nlz[w]);
         });
+        // internal k space: each board's chain-sliced positions, in board order
+        int64_t Kp = 0;
+        for (auto& p : plan) {
+            p.kOff = Kp;
+            Kp += p.kpad;
+        }
+        if (R + Kp > INT32_MAX || Cc + Kp > INT32_MAX)
+            throw Fail{KR_INVALID_INPUT, "dimensions exceed 32-bit indices"};
+        e->kpad = Kp;
         int64_t tsl[4] = {0, 0, 0, 0}, tpad[4] = {0, 0, 0, 0}, tnl[4] = {0, 0, 0, 0}, tnlz[4] = {0, 0, 0, 0};
         for (auto& p : plan)
             for (int w = 0; w < 4; ++w) {
@@ -825,10 +1050,10 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
                 tnlz[w] += p.nlz[w];
             }
         krb::DevSell* mats[4] = {&e->VT, &e->UA, &e->UT, &e->AV};
-        const int64_t nrowsOf[4] = {K, R, K, Cc};
+        const int64_t nrowsOf[4] = {Kp, R, Kp, Cc};
         const int64_t nnzOf[4] = {nV, nU + nA, nU, nA + nV};
         for (int w = 0; w < 4; ++w) alloc_sell(*mats[w], nrowsOf[w], tsl[w], nnzOf[w], tpad[w], tnl[w], tnlz[w]);
-        e->d_tz = dev_alloc<double>(std::max<int64_t>(K, 1));
+        e->d_tz = dev_alloc<double>(std::max<int64_t>(Kp, 1));
         e->d_xp = dev_alloc<double>(std::max<int64_t>(Cc, 1));
         e->d_in = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
         e->d_out = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
@@ -843,7 +1068,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             HostRows h;
             HostSell hs;
             for (int w = 0; w < 4; ++w) {
-                board_rows(p, w, R, K, xseq, e->M2, n2, h);
+                board_rows(p, w, R, Kp, xseq, e->M2, n2, h);
                 to_sell(h, rowBase[w], longRow, hs);
                 if (int64_t(hs.sptr.size()) != p.sl[w] || int64_t(hs.col.size()) != p.pad[w] ||
                     int64_t(hs.lgrow.size()) != p.nl[w] || int64_t(hs.lcol.size()) != p.nlz[w])
@@ -855,27 +1080,33 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
 
         // M solve structures (global, relabelled indices).
         if (chainMode) {
-            std::vector<int64_t> cptr{0};
-            std::vector<double> cmul(static_cast<size_t>(K), 0.0);
-            std::vector<uint8_t> neg;
+            std::vector<int64_t> sbase;
+            std::vector<int32_t> slen;
+            std::vector<uint8_t> sneg;
+            std::vector<double> cmul(static_cast<size_t>(Kp), 0.0);
             for (auto& p : plan) {
-                for (size_t c = 0; c + 1 < p.chains.size(); ++c) {
-                    bool allneg = true;
-                    for (int64_t q = p.chains[c]; q < p.chains[c + 1]; ++q) {
-                        cmul[size_t(p.kOff + q)] = p.mul[size_t(q)];
-                        if (q > p.chains[c] && p.mul[size_t(q)] != -1.0) allneg = false;
-                    }
-                    cptr.push_back(p.kOff + p.chains[c + 1]);
-                    neg.push_back(allneg ? 1 : 0);
-                }
+                for (int64_t b0 : p.sbase) sbase.push_back(p.kOff + b0);
+                slen.insert(slen.end(), p.slen.begin(), p.slen.end());
+                sneg.insert(sneg.end(), p.sneg.begin(), p.sneg.end());
+                std::copy(p.mul.begin(), p.mul.end(), cmul.begin() + p.kOff);
             }
-            e->nchains = int64_t(neg.size());
-            e->chain_ptr = dev_alloc<int64_t>(int64_t(cptr.size()));
-            e->chain_mul = dev_alloc<double>(std::max<int64_t>(K, 1));
-            e->chain_neg1 = dev_alloc<uint8_t>(std::max<int64_t>(e->nchains, 1));
-            KR_CK(cudaMemcpy(e->chain_ptr, cptr.data(), 8 * cptr.size(), cudaMemcpyHostToDevice));
-            if (K) KR_CK(cudaMemcpy(e->chain_mul, cmul.data(), 8 * size_t(K), cudaMemcpyHostToDevice));
-            if (e->nchains) KR_CK(cudaMemcpy(e->chain_neg1, neg.data(), neg.size(), cudaMemcpyHostToDevice));
+            e->nchains = int64_t(sbase.size());  // chain slices (32 chains each)
+            sbase.push_back(Kp);                 // terminal: slice s spans [sbase[s], sbase[s+1])
+            for (uint8_t v : sneg) e->chain_withmul |= v == 0;
+            if (const char* env = std::getenv("KR_CHAIN")) e->chain_tma = std::string(env) != "reg";
+            e->chain_ptr = dev_alloc<int64_t>(e->nchains + 1);
+            e->chain_len = dev_alloc<int32_t>(std::max<int64_t>(32 * e->nchains, 1));
+            e->chain_neg1 = dev_alloc<uint8_t>(std::max<int64_t>(32 * e->nchains, 1));
+            e->chain_mul = dev_alloc<double>(std::max<int64_t>(Kp, 1));
+            const int smem = int(size_t(kStages) * kChunkRows * 32 * sizeof(double) * 2);
+            KR_CK(cudaFuncSetAttribute(k_chain_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            KR_CK(cudaFuncSetAttribute(k_chain_tma<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            if (e->nchains) {
+                KR_CK(cudaMemcpy(e->chain_ptr, sbase.data(), 8 * sbase.size(), cudaMemcpyHostToDevice));
+                KR_CK(cudaMemcpy(e->chain_len, slen.data(), 4 * slen.size(), cudaMemcpyHostToDevice));
+                KR_CK(cudaMemcpy(e->chain_neg1, sneg.data(), sneg.size(), cudaMemcpyHostToDevice));
+            }
+            if (Kp) KR_CK(cudaMemcpy(e->chain_mul, cmul.data(), 8 * size_t(Kp), cudaMemcpyHostToDevice));
         } else if (e->mkind == 2) {
             std::vector<int64_t> cp{0};
             std::vector<int32_t> crow;
@@ -992,11 +1223,20 @@ double launch_bytes(const kr_engine* e, int which) {
     }
 }
 
+size_t chain_smem(const kr_engine* e) {
+    return size_t(kStages) * kChunkRows * 32 * sizeof(double) * (e->chain_withmul ? 2 : 1);
+}
+
 void solve_forward(kr_engine* e, cudaStream_t s) {
     if (e->mkind == 1 && e->nchains > 0) {
-        const int wpb = kWarpsPerBlock;
-        k_chain_forward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(e->chain_ptr, e->chain_mul,
-                                                                                  e->chain_neg1, e->nchains, e->d_tz);
+        if (e->chain_tma) {
+            k_chain_tma<1><<<unsigned(e->nchains), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
+                                                                         e->chain_neg1, e->chain_withmul, e->d_tz);
+        } else {
+            const int wpb = kWarpsPerBlock;
+            k_chain_forward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, e->nchains, e->d_tz);
+        }
         KR_CK_LAUNCH();
         e->launches++;
     } else if (e->mkind == 2) {
@@ -1013,9 +1253,14 @@ void solve_forward(kr_engine* e, cudaStream_t s) {
 
 void solve_backward(kr_engine* e, cudaStream_t s) {
     if (e->mkind == 1 && e->nchains > 0) {
-        const int wpb = kWarpsPerBlock;
-        k_chain_backward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(e->chain_ptr, e->chain_mul,
-                                                                                   e->chain_neg1, e->nchains, e->d_tz);
+        if (e->chain_tma) {
+            k_chain_tma<-1><<<unsigned(e->nchains), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
+                                                                          e->chain_neg1, e->chain_withmul, e->d_tz);
+        } else {
+            const int wpb = kWarpsPerBlock;
+            k_chain_backward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, e->nchains, e->d_tz);
+        }
         KR_CK_LAUNCH();
         e->launches++;
     } else if (e->mkind == 2) {
@@ -1043,7 +1288,7 @@ void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) {
     }
     launch_sell(e, 0, e->VT, xg, nullptr, 0, e->d_tz, s);  // t = V^T x          engine.hpp:65-72
     solve_forward(e, s);                                   // z = M^-1 t         engine.hpp:74-78
-    launch_sell(e, 1, e->UA, e->d_tz, x, e->k, y, s);      // y = U z + Ahat x   engine.hpp:81-89
+    launch_sell(e, 1, e->UA, e->d_tz, x, e->kpad, y, s);   // y = U z + Ahat x   engine.hpp:81-89
     e->flops_last = e->flops_per_product;
     e->flops_total += e->flops_last;
 }
