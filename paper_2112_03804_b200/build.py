@@ -73,8 +73,24 @@ def build_host(force=False, verbose=False):
     return out
 
 
+def build_cli(force=False, verbose=False):
+    """krb200: the C++ CLI (tools/krb200_cli.cpp) over both C ABIs."""
+    src = os.path.join(ROOT, "tools", "krb200_cli.cpp")
+    out = os.path.join(LIBDIR, "krb200")
+    deps = [src, os.path.join(LIBDIR, "libkrhost.so"), os.path.join(LIBDIR, "libkrcuda.so")]
+    if force or _stale(out, deps):
+        cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), "-o", out, src,
+               "-L", LIBDIR, "-lkrhost", "-lkrcuda", "-Wl,-rpath,$ORIGIN", "-ldl", "-lpthread", "-lrt"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return out
+
+
 def build_all(force=False, verbose=False):
-    return build_host(force, verbose), build_cuda(force, verbose)
+    out = build_host(force, verbose), build_cuda(force, verbose)
+    build_cli(force, verbose)
+    return out
 
 
 if __name__ == "__main__":
