@@ -67,9 +67,17 @@ struct Tree {
 
 __device__ __forceinline__ Tree tree_view(const int32_t* t, int nn) { return Tree{t, t + nn, t + 2 * nn + 1}; }
 
-// regretMatch (solver.hpp:166-194) on a strided shared-memory row.
-__device__ __forceinline__ void regret_match(const double* R, int stride, const int32_t* seqs, int count,
-                                             double* probs) {
+// regretMatch (solver.hpp:166-194), split so no per-action array is needed:
+// rm_stats scans a node's regrets once; rm_prob then yields probs[a] from the
+// action's regret with the same expressions (r / sumPos, 1.0 / ties).
+struct RmStats {
+    bool positive;
+    double sumPos;  // when positive
+    double cut;     // best - tol, when not positive
+    double uniform; // 1.0 / ties, when not positive
+};
+
+__device__ __forceinline__ RmStats rm_stats(const double* R, int stride, const int32_t* seqs, int count) {
     double best = R[(seqs[0] - 1) * stride];
     double maxAbs = fabs(best);
     for (int a = 1; a < count; ++a) {
@@ -79,22 +87,28 @@ __device__ __forceinline__ void regret_match(const double* R, int stride, const 
         maxAbs = (maxAbs < ar) ? ar : maxAbs;
     }
     const double tol = 1e-9 * (1 + maxAbs);
-    if (best > tol) {
-        double sumPos = 0;
+    RmStats st;
+    st.positive = best > tol;
+    st.sumPos = 0;
+    st.cut = best - tol;
+    st.uniform = 0;
+    if (st.positive) {
         for (int a = 0; a < count; ++a) {
             const double r = R[(seqs[a] - 1) * stride];
-            if (r > 0) sumPos += r;
+            if (r > 0) st.sumPos += r;
         }
-        for (int a = 0; a < count; ++a) {
-            const double r = R[(seqs[a] - 1) * stride];
-            probs[a] = r > 0 ? r / sumPos : 0.0;
-        }
-        return;
+    } else {
+        int ties = 0;
+        for (int a = 0; a < count; ++a)
+            if (R[(seqs[a] - 1) * stride] >= st.cut) ++ties;
+        st.uniform = 1.0 / ties;
     }
-    int ties = 0;
-    for (int a = 0; a < count; ++a)
-        if (R[(seqs[a] - 1) * stride] >= best - tol) ++ties;
-    for (int a = 0; a < count; ++a) probs[a] = R[(seqs[a] - 1) * stride] >= best - tol ? 1.0 / ties : 0.0;
+    return st;
+}
+
+__device__ __forceinline__ double rm_prob(const RmStats& st, double r) {
+    if (st.positive) return r > 0 ? r / st.sumPos : 0.0;
+    return r >= st.cut ? st.uniform : 0.0;
 }
 
 // mode 0: sequence form only (initial strategy, solver.hpp:363-364)
@@ -103,52 +117,62 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
                               const double* __restrict__ g, int negate, double* __restrict__ regret,
                               double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
                               double shrink) {
+    // Shared memory per hand: its regret row and its seqVal / reach row
+    // (strided so consecutive threads hit consecutive banks).  The gradient
+    // row is read straight from global memory (each element once); the
+    // sequence-form strategy is the reach row itself (x[s-1] = reach[s]).
     extern __shared__ double sm[];
     const int stride = nt + 1;
-    double* G = sm;                       // (n+1) x stride : gradient, then x
-    double* Rg = G + (n + 1) * stride;    // (n+1) x stride : regrets
-    double* V = Rg + (n + 1) * stride;    // (n+1) x stride : seqVal / reach
+    double* Rg = sm;                      // n x stride     : regrets
+    double* V = Rg + n * stride;          // (n+1) x stride : seqVal / reach
     int32_t* T = reinterpret_cast<int32_t*>(V + (n + 1) * stride);
-    const int tl = 2 * nn + 1 + 0;  // parent + aptr
+    const int tl = 2 * nn + 1;  // parent + aptr
     for (int q = threadIdx.x; q < tl; q += blockDim.x) T[q] = treeBuf[q];
     const int64_t h0 = int64_t(blockIdx.x) * nt;
     const int nh = int(lmin(nt, H - h0));
     const int64_t e0 = h0 * n;
     const int ne = nh * n;
-    // total actions = aptr[nn]
     __syncthreads();
-    const int na = T[2 * nn];
+    const int na = T[2 * nn];  // aptr[nn]
     for (int q = threadIdx.x; q < na; q += blockDim.x) T[tl + q] = treeBuf[tl + q];
-    for (int q = threadIdx.x; q < ne; q += blockDim.x) {
-        const int hh = q / n, s = q - hh * n;
-        Rg[s * stride + hh] = regret[e0 + q];
-        if (mode == 1) {
-            const double gv = g[e0 + q];
-            G[s * stride + hh] = negate ? -gv : gv;
+    // coalesced loads, 8 in flight per thread
+    for (int q0 = threadIdx.x; q0 < ne; q0 += 8 * blockDim.x) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * blockDim.x;
+            v[u] = q < ne ? regret[e0 + q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * blockDim.x;
+            if (q < ne) {
+                const int hh = q / n, s = q - hh * n;
+                Rg[s * stride + hh] = v[u];
+            }
         }
     }
     __syncthreads();
     const Tree tr = tree_view(T, nn);
     const int t = threadIdx.x;
     if (t < nh) {
-        double probs[kMaxActions];
-        int32_t seqs[kMaxActions];
         double* R = Rg + t;
-        double* Gt = G + t;
         double* Vt = V + t;
+        const double* gh = g + (h0 + t) * n;
         if (mode == 1) {
             // cfrSweep (solver.hpp:227-245): bottom-up over the player's nodes
             for (int s = 0; s <= n; ++s) Vt[s * stride] = 0.0;
             for (int v = nn - 1; v >= 0; --v) {
                 const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
-                for (int a = 0; a < cnt; ++a) seqs[a] = tr.aseq[a0 + a];
-                regret_match(R, stride, seqs, cnt, probs);
+                const int32_t* seqs = tr.aseq + a0;
+                const RmStats st = rm_stats(R, stride, seqs, cnt);
                 double nodeVal = 0;
                 for (int a = 0; a < cnt; ++a) {
                     const int sq = seqs[a];
-                    const double ev = Gt[(sq - 1) * stride] + Vt[sq * stride];
+                    const double gv = negate ? -__ldg(gh + sq - 1) : __ldg(gh + sq - 1);
+                    const double ev = gv + Vt[sq * stride];
                     Vt[sq * stride] = ev;
-                    nodeVal += probs[a] * ev;
+                    nodeVal += rm_prob(st, R[(sq - 1) * stride]) * ev;
                 }
                 for (int a = 0; a < cnt; ++a) {
                     const int sq = seqs[a];
@@ -157,17 +181,16 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
                 Vt[tr.parent[v] * stride] += nodeVal;
             }
         }
-        // sequenceForm (solver.hpp:202-215): top-down reach, x into G
+        // sequenceForm (solver.hpp:202-215): top-down reach
         Vt[0] = 1.0;
         for (int v = 0; v < nn; ++v) {
             const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
-            for (int a = 0; a < cnt; ++a) seqs[a] = tr.aseq[a0 + a];
-            regret_match(R, stride, seqs, cnt, probs);
+            const int32_t* seqs = tr.aseq + a0;
+            const RmStats st = rm_stats(R, stride, seqs, cnt);
             const double mass = Vt[tr.parent[v] * stride];
             for (int a = 0; a < cnt; ++a) {
-                const double m = mass * probs[a];
-                Vt[seqs[a] * stride] = m;
-                Gt[(seqs[a] - 1) * stride] = m;
+                const int sq = seqs[a];
+                Vt[sq * stride] = mass * rm_prob(st, R[(sq - 1) * stride]);
             }
         }
         if (mode == 1)  // discount (solver.hpp:262-264)
@@ -177,13 +200,27 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
             }
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < ne; q += blockDim.x) {
-        const int hh = q / n, s = q - hh * n;
-        const double xv = G[s * stride + hh];
-        xout[e0 + q] = xv;
+    for (int q0 = threadIdx.x; q0 < ne; q0 += 8 * blockDim.x) {
+        double a[8];
         if (mode == 1) {
-            regret[e0 + q] = Rg[s * stride + hh];
-            avg[e0 + q] = (avg[e0 + q] + xv) * shrink;  // solver.hpp:382-386
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * blockDim.x;
+                a[u] = q < ne ? avg[e0 + q] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * blockDim.x;
+            if (q < ne) {
+                const int hh = q / n, s = q - hh * n;
+                const double xv = V[(s + 1) * stride + hh];
+                xout[e0 + q] = xv;
+                if (mode == 1) {
+                    regret[e0 + q] = Rg[s * stride + hh];
+                    avg[e0 + q] = (a[u] + xv) * shrink;  // solver.hpp:382-386
+                }
+            }
         }
     }
 }
@@ -227,13 +264,34 @@ __global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int
 }
 
 // Per-board totals in ascending hand order (solver.hpp:318 `total += ...`).
-__global__ void k_board_sums(const double* __restrict__ handval, const int64_t* __restrict__ bstart, int nb,
-                             double* __restrict__ out) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+// One block per board: the block stages chunks of the board's hand values in
+// shared memory with coalesced loads; thread 0 adds them in hand order.
+constexpr int kSumChunk = 2048;
+__global__ void __launch_bounds__(256) k_board_sums(const double* __restrict__ handval,
+                                                    const int64_t* __restrict__ bstart, int nb,
+                                                    double* __restrict__ out) {
+    __shared__ double buf[kSumChunk];
+    const int b = blockIdx.x;
     if (b >= nb) return;
     double total = 0;
-    for (int64_t h = bstart[b]; h < bstart[b + 1]; ++h) total += handval[h];
-    out[b] = total;
+    for (int64_t h0 = bstart[b]; h0 < bstart[b + 1]; h0 += kSumChunk) {
+        const int n = int(lmin(kSumChunk, bstart[b + 1] - h0));
+        for (int q = threadIdx.x; q < n; q += blockDim.x) buf[q] = handval[h0 + q];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int q = 0;
+            for (; q + 8 <= n; q += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = buf[q + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) total += v[u];
+            }
+            for (; q < n; ++q) total += buf[q];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[b] = total;
 }
 
 // validateSequenceStrategy (solver.hpp:266-286): flag 1 = negative entry,
@@ -256,7 +314,7 @@ __global__ void k_validate(const int32_t* __restrict__ treeBuf, int nn, int n, i
 }
 
 size_t step_smem(int n, int nt, int nn, int na) {
-    return size_t(3) * size_t(n + 1) * size_t(nt + 1) * 8 + size_t(2 * nn + 1 + na) * 4 + 16;
+    return size_t(2 * n + 1) * size_t(nt + 1) * 8 + size_t(2 * nn + 1 + na) * 4 + 16;
 }
 
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
@@ -289,8 +347,7 @@ void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<
         KR_CK_LAUNCH();
         s->launches++;
     }
-    k_board_sums<<<unsigned((s->nboards + 127) / 128), 128, 0, st>>>(s->handval, s->d_bstart[player], s->nboards,
-                                                                      s->boardval);
+    k_board_sums<<<unsigned(s->nboards), 256, 0, st>>>(s->handval, s->d_bstart[player], s->nboards, s->boardval);
     KR_CK_LAUNCH();
     s->launches++;
     boards.assign(size_t(s->nboards), 0.0);

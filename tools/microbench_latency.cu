@@ -27,6 +27,10 @@ __global__ void chain(double* out, double a, double b, int n, long long* cyc) {
         for (int i = 0; i < n; ++i) x = sm[i & 1023] + x;
     if (OP == 6)  // recurrence with a compare/select like the chain solve
         for (int i = 0; i < n; ++i) x = (x != 0.0) ? sm[i & 1023] - (-1.0) * x : sm[i & 1023];
+    if (OP == 7)  // IEEE fp64 division (regret matching r / sumPos)
+        for (int i = 0; i < n; ++i) x = y / x;
+    if (OP == 8)  // global load chain (L2 latency)
+        for (int i = 0; i < n; ++i) x = out[(long long)(x) & 1] + 1e-300;
     long long t1 = clock64();
     out[0] = x + xf + double(xi);
     cyc[0] = t1 - t0;
@@ -37,9 +41,9 @@ int main() {
     long long* cyc;
     cudaMalloc(&out, 8);
     cudaMallocManaged(&cyc, 8);
-    const char* names[] = {"DADD", "DMUL", "DFMA", "FADD", "IADD64", "LDS+DADD", "LDS+DMUL+DADD+select"};
+    const char* names[] = {"DADD", "DMUL", "DFMA", "FADD", "IADD64", "LDS+DADD", "LDS+DMUL+DADD+select", "DDIV", "LDG chain"};
     const int n = 100000;
-    for (int op = 0; op < 7; ++op) {
+    for (int op = 0; op < 9; ++op) {
         for (int rep = 0; rep < 2; ++rep) {
             switch (op) {
                 case 0: chain<0><<<1, 1>>>(out, 1.0, 1e-9, n, cyc); break;
@@ -49,6 +53,8 @@ int main() {
                 case 4: chain<4><<<1, 1>>>(out, 1.0, 3, n, cyc); break;
                 case 5: chain<5><<<1, 1>>>(out, 1.0, 1e-9, n, cyc); break;
                 case 6: chain<6><<<1, 1>>>(out, 1.0, 1e-9, n, cyc); break;
+                case 7: chain<7><<<1, 1>>>(out, 1.5, 1.25, n, cyc); break;
+                case 8: chain<8><<<1, 1>>>(out, 0.0, 1.0, n, cyc); break;
             }
             cudaDeviceSynchronize();
         }
