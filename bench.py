@@ -229,10 +229,20 @@ def run_product(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NCCL over NVLink between the GPUs of the node; KR_DIST_BACKEND=gloo
+    # runs the same multi-rank logic with host collectives (used to smoke the
+    # torchrun path on a one-GPU box: ranks share cuda:0, no kernel waits on
+    # another rank).
+    backend = os.environ.get("KR_DIST_BACKEND", "nccl")
+    local = min(local, torch.cuda.device_count() - 1)
+    coll_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -243,14 +253,14 @@ def run_product(args):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -329,7 +339,7 @@ def run_product(args):
     i0 = boards[0][0]
     solver = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
                         i0.pot)
-    drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=dev)
+    drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=coll_dev)
     drv.run(max_iters=5, checkpoint_every=5)  # warm
     barrier()
     torch.cuda.synchronize(dev)
@@ -360,7 +370,7 @@ def run_product(args):
             "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2)}),
         "roofline": {"bound": "hbm", "kernel": f"k_spmv[{dominant}]", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-                     "traffic": ncu_traffic(dominant),
+                     "traffic": ncu_traffic(dominant) if world == 1 and args.boards == NBOARDS else None,
                      "whole_pair_gb_per_s": pair_bytes / (ms_local / args.steps / 1e3) / 1e9 if world == 1 else None},
         "kernels": kernels,
         "e2e": {"value": e2e_steps / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": 8 * (nx + ny),

@@ -162,12 +162,37 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
         if (mode == 1) {
             // cfrSweep (solver.hpp:227-245): bottom-up over the player's nodes
             for (int s = 0; s <= n; ++s) Vt[s * stride] = 0.0;
+            // the gradient entries of node v-1 are loaded while node v is
+            // processed (up to kPre actions per node in registers)
+            constexpr int kPre = 8;
+            double gnext[kPre];
+            auto prefetch = [&](int v, double* dst) {
+                if (v < 0) return;
+                const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
+#pragma unroll
+                for (int u = 0; u < kPre; ++u)
+                    if (u < cnt) dst[u] = __ldg(gh + tr.aseq[a0 + u] - 1);
+            };
+            prefetch(nn - 1, gnext);
             for (int v = nn - 1; v >= 0; --v) {
                 const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
                 const int32_t* seqs = tr.aseq + a0;
+                double gcur[kPre];
+#pragma unroll
+                for (int u = 0; u < kPre; ++u) gcur[u] = gnext[u];
+                prefetch(v - 1, gnext);
                 const RmStats st = rm_stats(R, stride, seqs, cnt);
                 double nodeVal = 0;
-                for (int a = 0; a < cnt; ++a) {
+#pragma unroll
+                for (int a = 0; a < kPre; ++a)
+                    if (a < cnt) {
+                        const int sq = seqs[a];
+                        const double gv = negate ? -gcur[a] : gcur[a];
+                        const double ev = gv + Vt[sq * stride];
+                        Vt[sq * stride] = ev;
+                        nodeVal += rm_prob(st, R[(sq - 1) * stride]) * ev;
+                    }
+                for (int a = kPre; a < cnt; ++a) {
                     const int sq = seqs[a];
                     const double gv = negate ? -__ldg(gh + sq - 1) : __ldg(gh + sq - 1);
                     const double ev = gv + Vt[sq * stride];
