@@ -87,6 +87,10 @@ int or_builtin(const char* name, uint64_t seed, int hands, int shared, const cha
                     for (int s = 0; s < 2; ++s) deck.cards.emplace_back(r, s);
             }
             BettingConfig cfg = tree == 3 ? threeBetConfig() : referenceBettingConfig();
+            if (tree == 91) {  // menus {0.33, 0.75, 1.5}, raise cap 3
+                cfg = threeBetConfig();
+                for (int x = 0; x < kBetContexts; ++x) cfg.menu1[x] = cfg.menu2[x] = {0.33, 0.75, 1.5};
+            }
             h->inst = fullRangeRiver(Board::fromCode(board), deck, seed, cfg);
         } else throw InvalidInputError("unknown builtin '" + n + "'");
         h->kp = assemble(h->inst);

@@ -1427,8 +1427,16 @@ int krh_instance_builtin(const char* name, uint64_t seed, int hands, int shared,
             for (int q = 0; q < shared; ++q) (void)krh::randomSmallInstance(rng, hands);
             in = krh::randomSmallInstance(rng, hands);
         } else if (n == "bench") in = krh::benchInstance(seed, hands, shared);
-        else if (n == "river_full")
-            in = krh::fullRangeRiver(board, deck, seed, tree == 3 ? krh::threeBetConfig() : krh::referenceBettingConfig());
+        else if (n == "river_full") {
+            krh::BettingConfig cfg = krh::referenceBettingConfig();
+            if (tree == 3) cfg = krh::threeBetConfig();
+            if (tree == 91) {  // menus {0.33, 0.75, 1.5}, raise cap 3 -> n = 91
+                cfg = krh::threeBetConfig();
+                for (int p = 0; p < 2; ++p)
+                    for (auto& m : cfg.menu[p]) m = {0.33, 0.75, 1.5};
+            }
+            in = krh::fullRangeRiver(board, deck, seed, cfg);
+        }
         else throw krh::Error{krh::INVALID_INPUT, "unknown built-in instance '" + n + "'"};
         *out = new krh_instance{std::move(in)};
     });
