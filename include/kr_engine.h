@@ -64,6 +64,30 @@ typedef struct {
 /* Engine flags. */
 #define KR_FLAG_DEFAULT 0u
 
+/* One river board in Kronecker form (kron.hpp:104-132): the payoff block of
+ * hand pair (i, j) is pi_ij (F + W_ij S) with pi_ij = lambda1_i lambda2_j
+ * [hands disjoint] and W_ij = sign(key1_i - key2_j).  Hands of each player are
+ * strength-sorted ascending (kron.hpp:74-83); cards are ids 0..51. */
+typedef struct {
+  int32_t m1, m2, n1, n2;
+  const uint32_t* key1;   /* [m1] packed strength keys (cards.hpp:167-194) */
+  const uint32_t* key2;   /* [m2] */
+  const uint8_t* cards1;  /* [2*m1] */
+  const uint8_t* cards2;  /* [2*m2] */
+  const double* lambda1;  /* [m1] mu1 / sqrt(beta) (kron.hpp:163)  */
+  const double* lambda2;  /* [m2] */
+  kr_compressed F;        /* CSR n1 x n2 fold payments (skeleton.hpp:332-349) */
+  kr_compressed S;        /* CSR n1 x n2 showdown stakes */
+} kr_kron_board;
+
+/* Implicit Kronecker engine (the "showdown/fold factors as segmented prefix
+ * scans with card-removal corrections" of the north star; SURVEY.md 8(f)
+ * row 1).  Same products as kr_engine_ax / kr_engine_atx with nothing
+ * materialised: per board it streams x and y (~0.8 MB) instead of the
+ * factors (~76 MB).  Results equal referenceMatvec(T) (kron.hpp:211-254) up
+ * to rounding (summation order differs); flops() counts its multiply-adds. */
+int kr_engine_create_kron(const kr_kron_board* boards, int nboards, int device, uint32_t flags, kr_engine** out);
+
 /* Create an engine for one Sparsification on CUDA device `device`.
  * Replaces FactoredEngine(const Sparsification&) (solver.hpp:32); the
  * factors are copied to HBM, so the caller may free them afterwards. */

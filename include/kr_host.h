@@ -55,6 +55,8 @@ int krh_instance_vectors(const krh_instance* h, double* mu1, double* mu2, double
 int krh_instance_treeplex(const krh_instance* h, int player, int32_t* parent, int32_t* action_ptr,
                           int32_t* action_seq);
 int64_t krh_dense_nnz(const krh_instance* h);
+/* Kronecker view for kr_engine_create_kron (pointers valid while h lives). */
+int krh_instance_kron_view(const krh_instance* h, kr_kron_board* out);
 
 /* technique 0 = A (rectangle peel, peel_iters), 1 = B.  post != 0 applies
  * postprocess (Technique B post is built in closed form, bit-identical to

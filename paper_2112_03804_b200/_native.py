@@ -66,6 +66,12 @@ class kr_factors(C.Structure):
                 ("n2", C.c_int32)]
 
 
+class kr_kron_board(C.Structure):
+    _fields_ = [("m1", C.c_int32), ("m2", C.c_int32), ("n1", C.c_int32), ("n2", C.c_int32), ("key1", C.c_void_p),
+                ("key2", C.c_void_p), ("cards1", C.c_void_p), ("cards2", C.c_void_p), ("lambda1", C.c_void_p),
+                ("lambda2", C.c_void_p), ("F", kr_compressed), ("S", kr_compressed)]
+
+
 class kr_treeplex(C.Structure):
     _fields_ = [("n_seq", C.c_int32), ("n_nodes", C.c_int32), ("node_parent_seq", C.c_void_p),
                 ("node_action_ptr", C.c_void_p), ("action_seq", C.c_void_p)]
@@ -91,7 +97,7 @@ CUDA_SYMBOLS = [
     "kr_engine_stream", "kr_engine_device", "kr_engine_launches", "kr_host_alloc", "kr_host_free", "kr_last_error",
     "kr_device_count", "kr_solver_create", "kr_solver_destroy", "kr_solver_run", "kr_solver_best_response",
     "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
-    "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times",
+    "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times", "kr_engine_create_kron",
 ]
 
 
@@ -127,6 +133,8 @@ def cuda():
         L.kr_engine_create.argtypes = [C.POINTER(kr_factors), C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]
         L.kr_engine_create_boards.argtypes = [C.POINTER(kr_factors), C.c_int, C.c_int, C.c_uint32,
                                               C.POINTER(C.c_void_p)]
+        L.kr_engine_create_kron.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.c_int, C.c_uint32,
+                                            C.POINTER(C.c_void_p)]
         if hasattr(L, "kr_solver_create"):
             L.kr_solver_create.argtypes = [C.c_void_p, C.POINTER(kr_treeplex), C.POINTER(kr_treeplex), C.c_int,
                                            C.c_void_p, C.c_void_p, C.c_double, C.POINTER(C.c_void_p)]

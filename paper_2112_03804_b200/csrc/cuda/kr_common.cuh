@@ -77,6 +77,10 @@ T* dev_alloc(int64_t n) {
     return p;
 }
 
+struct KronState;  // implicit Kronecker engine (kr_kron.cu)
+void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s);
+void kron_destroy(KronState* k);
+
 }  // namespace krb
 
 // Engine state (opaque to C callers).
@@ -138,6 +142,8 @@ struct kr_engine {
     std::vector<cudaEvent_t> eventPool;
     int64_t tLaunches[4] = {0, 0, 0, 0};
     double tMs[4] = {0, 0, 0, 0};
+    // implicit Kronecker mode (kr_engine_create_kron): no factors at all
+    krb::KronState* kron = nullptr;
 };
 
 namespace krb {

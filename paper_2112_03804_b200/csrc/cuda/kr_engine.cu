@@ -892,6 +892,7 @@ std::vector<int64_t> board_lengths(const BoardPlan& p, int which) {
 void destroy_engine(kr_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
+    kron_destroy(e->kron);
     free_sell(e->VT);
     free_sell(e->UA);
     free_sell(e->UT);
@@ -1278,6 +1279,7 @@ void solve_backward(kr_engine* e, cudaStream_t s) {
 }  // namespace
 
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) {
+    if (e->kron) return kron_product(e, 0, x, y, s);
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
     const double* xg = x;
     if (e->xseq && e->cols > 0) {
@@ -1294,6 +1296,7 @@ void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) {
 }
 
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) {
+    if (e->kron) return kron_product(e, 1, y, x, s);
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
     launch_sell(e, 2, e->UT, y, nullptr, 0, e->d_tz, s);      // s = U^T y         engine.hpp:103-110
     solve_backward(e, s);                                     // z = M^-T s        engine.hpp:112-115

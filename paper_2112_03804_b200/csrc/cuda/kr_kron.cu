@@ -1,0 +1,474 @@
+// kr_kron.cu — the implicit Kronecker engine.
+//
+// The payoff of one river board is A = Σ_ij π_ij (F + W_ij S) ⊗ e_i e_jᵀ with
+// π_ij = λ1_i λ2_j [hands i, j disjoint] and W_ij = sign(key1_i − key2_j)
+// (kron.hpp:104-132; referenceMatvec / referenceMatvecT, kron.hpp:211-254).
+// Nothing of A is materialised.  For an output hand i on side O (player 1
+// for A x, player 2 for Aᵀ y), summing over the hands j of side Σ:
+//
+//   out[i·n_O + a] = λ_O(i) · ( Σ_{j disj i} WF_j[a]  +  σ Σ_{j disj i} W_ij WS_j[a] )
+//   WF_j[a] = λ_Σ(j) (F_d v_j)[a],   WS_j[a] = λ_Σ(j) (S_d v_j)[a]
+//
+// with F_d = F (A x) or Fᵀ (Aᵀ y), σ = +1 (A x) or −1 (Aᵀ y).  Hands of each
+// side are strength-sorted ascending, so "key_j < key_i" is a prefix of the
+// summing side: the W-weighted sum is (prefix below) − (suffix above), and
+// the disjointness constraint is inclusion–exclusion over the two cards of i
+// (all − hands holding c1 − hands holding c2 + the hand holding both), each
+// card list again strength-sorted so its part is a prefix of the list.
+//
+// One fused kernel per product, one CTA per (sequence a, board b); every
+// intermediate lives in shared memory (≈ 5 m_Σ doubles, ≤ 54 KB):
+//   1. wf[j], ws[j] for every summing hand j (gathers of v, L2-resident)
+//   2. ps = exclusive prefix of ws, TF = Σ wf, TS = Σ ws (block scan), and
+//      for each of the 52 cards the prefix of ws and the sum of wf over the
+//      hands holding it (one warp per card, shuffle scans)
+//   3. every output hand i of the board: out = λ_O (TF − CF[c1] − CF[c2]
+//      + wf[dup] + σ (lower − upper)), lookups from a per-hand table
+// so HBM sees only v, the output, and the small per-board tables.  The
+// lookups (key ranks lt / le, their per-card-list counterparts, the
+// duplicate-hand index) depend only on the keys and are built once on the
+// host at create time.  Results equal referenceMatvec(T) up to rounding
+// (different summation order): tests hold them to 1e-12 normwise.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kr_common.cuh"
+
+namespace krb {
+
+namespace {
+
+constexpr int kCards = 52;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// Lookup table of one output hand (positions inside the board's shared
+// arrays; card-list positions already include the list's own offset).
+struct alignas(16) OutHand {
+    int32_t lt, le, dup, cards;      // cards = c1 | c2 << 8
+    int32_t p1lt, p1le, p1end, p2lt;
+    int32_t p2le, p2end, pad0, pad1;
+};
+
+// Device view of one direction (0: A x, 1: Aᵀ y).
+struct KronDir {
+    int nO = 0, nS = 0, nb = 0, sign = 1;
+    int64_t mO = 0, mS = 0;
+    int maxMS = 0;
+    int64_t* sumOff = nullptr;    // [nb+1] global summing-hand offsets
+    int64_t* outOff = nullptr;    // [nb+1] global output-hand offsets
+    double* lamS = nullptr;       // [mS]
+    double* lamO = nullptr;       // [mO]
+    int64_t* fptr = nullptr;      // [nb*(nO+1)] global positions into fcol/fval
+    int32_t* fcol = nullptr;
+    double* fval = nullptr;
+    int64_t* sptr = nullptr;
+    int32_t* scol = nullptr;
+    double* sval = nullptr;
+    int32_t* listPtr = nullptr;   // [nb*53] offsets in the board's card-list space
+    int64_t* listBase = nullptr;  // [nb] base of the board's lists in listHands
+    int32_t* listHands = nullptr; // local summing-hand ids, list-major, ascending
+    OutHand* otab = nullptr;      // [mO]
+    int64_t flops = 0;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+size_t fused_smem(int maxMS) { return sizeof(double) * (5 * size_t(maxMS) + 1 + 2 * kCards); }
+
+__global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, const double* __restrict__ in,
+                                                         double* __restrict__ out) {
+    extern __shared__ double sm[];
+    __shared__ double warpTot[kWarps], warpF[kWarps];
+    const int a = blockIdx.x, b = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t sBase = d.sumOff[b];
+    const int mSb = int(d.sumOff[b + 1] - sBase);
+    double* wf = sm;                  // [mSb]
+    double* ws = wf + mSb;            // [mSb]
+    double* ps = ws + mSb;            // [mSb + 1]
+    double* cps = ps + mSb + 1;       // [2 mSb + 52]
+    double* cf = cps + 2 * mSb + kCards;  // [52]
+
+    // 1. weights of every summing hand for sequence a
+    {
+        const int64_t* fp = d.fptr + int64_t(b) * (d.nO + 1) + a;
+        const int64_t* sp = d.sptr + int64_t(b) * (d.nO + 1) + a;
+        const int64_t f0 = fp[0], f1 = fp[1], s0 = sp[0], s1 = sp[1];
+        const int nS = d.nS;
+        for (int j = tid; j < mSb; j += kThreads) {
+            const double* v = in + (sBase + j) * int64_t(nS);
+            double f = 0.0, s = 0.0;
+            for (int64_t e = f0; e < f1; ++e) f += __ldg(d.fval + e) * __ldg(v + __ldg(d.fcol + e));
+            for (int64_t e = s0; e < s1; ++e) s += __ldg(d.sval + e) * __ldg(v + __ldg(d.scol + e));
+            const double lam = __ldg(d.lamS + sBase + j);
+            wf[j] = lam * f;
+            ws[j] = lam * s;
+        }
+    }
+    __syncthreads();
+
+    // 2a. ps = exclusive prefix of ws; totals TS (ps[mSb]) and TF
+    {
+        const int chunk = (mSb + kThreads - 1) / kThreads;
+        const int j0 = min(mSb, tid * chunk), j1 = min(mSb, j0 + chunk);
+        double loc = 0.0, locF = 0.0;
+        for (int j = j0; j < j1; ++j) {
+            loc += ws[j];
+            locF += wf[j];
+        }
+        const double incl = warp_incl_scan(loc, lane);
+        const double fsum = warp_sum(locF);
+        if (lane == 31) warpTot[warp] = incl;
+        if (lane == 0) warpF[warp] = fsum;
+        __syncthreads();
+        double run = incl - loc;
+        for (int w = 0; w < warp; ++w) run += warpTot[w];
+        for (int j = j0; j < j1; ++j) {
+            ps[j] = run;
+            run += ws[j];
+        }
+        if (tid == kThreads - 1) ps[mSb] = run;
+    }
+    // 2b. per card: prefix of ws over the hands holding it, and Σ wf
+    {
+        const int32_t* lp = d.listPtr + int64_t(b) * (kCards + 1);
+        const int32_t* hands = d.listHands + d.listBase[b];
+        for (int c = warp; c < kCards; c += kWarps) {
+            const int p0 = lp[c], p1 = lp[c + 1];
+            double* o = cps + p0 + c;
+            double runC = 0.0, runF = 0.0;
+            for (int p = p0; p < p1; p += 32) {
+                const bool ok = p + lane < p1;
+                const int h = ok ? __ldg(hands + p + lane) : 0;
+                const double v = ok ? ws[h] : 0.0;
+                const double u = ok ? wf[h] : 0.0;
+                const double inc = warp_incl_scan(v, lane);
+                if (ok) o[p - p0 + lane] = runC + inc - v;
+                runC += __shfl_sync(0xffffffffu, inc, 31);
+                runF += warp_sum(u);
+            }
+            if (lane == 0) {
+                o[p1 - p0] = runC;
+                cf[c] = runF;
+            }
+        }
+    }
+    __syncthreads();
+
+    // 3. outputs of every hand of the board for sequence a
+    double TF = 0.0;
+    for (int w = 0; w < kWarps; ++w) TF += warpF[w];
+    const double TS = ps[mSb];
+    const int64_t oBase = d.outOff[b];
+    const int mOb = int(d.outOff[b + 1] - oBase);
+    const double sg = double(d.sign);
+    for (int i = tid; i < mOb; i += kThreads) {
+        const OutHand t = d.otab[oBase + i];
+        const int c1 = t.cards & 0xff, c2 = t.cards >> 8;
+        double fpart = TF - cf[c1] - cf[c2];
+        if (t.dup >= 0) fpart += wf[t.dup];
+        const double lower = ps[t.lt] - cps[t.p1lt] - cps[t.p2lt];
+        const double upper = (TS - ps[t.le]) - (cps[t.p1end] - cps[t.p1le]) - (cps[t.p2end] - cps[t.p2le]);
+        out[(oBase + i) * d.nO + a] = __ldg(d.lamO + oBase + i) * (fpart + sg * (lower - upper));
+    }
+}
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+    T* p = dev_alloc<T>(int64_t(v.size()));
+    if (!v.empty()) KR_CK(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return p;
+}
+
+void check_csr(const kr_compressed& m, int rows, int cols, const char* name) {
+    if (m.outer_size != rows || !m.outer) throw Fail{KR_INVALID_INPUT, std::string(name) + ": wrong outer size"};
+    if (m.outer[0] != 0) throw Fail{KR_INVALID_INPUT, std::string(name) + ": outer[0] != 0"};
+    for (int r = 0; r < rows; ++r)
+        if (m.outer[r + 1] < m.outer[r]) throw Fail{KR_INVALID_INPUT, std::string(name) + ": outer not monotone"};
+    const int64_t nnz = m.outer[rows];
+    if (nnz > 0 && (!m.inner || !m.val)) throw Fail{KR_INVALID_INPUT, std::string(name) + ": null arrays"};
+    for (int64_t e = 0; e < nnz; ++e) {
+        if (m.inner[e] < 0 || m.inner[e] >= cols)
+            throw Fail{KR_INVALID_INPUT, std::string(name) + ": column index out of range"};
+        if (!std::isfinite(m.val[e])) throw Fail{KR_INVALID_INPUT, std::string(name) + ": non-finite value"};
+    }
+}
+
+struct HostCsr {
+    std::vector<int64_t> ptr;
+    std::vector<int32_t> col;
+    std::vector<double> val;
+};
+
+// F (n1 x n2) as given, or its transpose (stable counting sort: columns of
+// each transposed row ascending).
+HostCsr csr_dir(const kr_compressed& m, int n1, int n2, bool transpose) {
+    HostCsr h;
+    const int64_t nnz = m.outer[n1];
+    if (!transpose) {
+        h.ptr.assign(m.outer, m.outer + n1 + 1);
+        h.col.assign(m.inner, m.inner + nnz);
+        h.val.assign(m.val, m.val + nnz);
+        return h;
+    }
+    h.ptr.assign(static_cast<size_t>(n2) + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e) h.ptr[size_t(m.inner[e]) + 1]++;
+    for (int c = 0; c < n2; ++c) h.ptr[size_t(c) + 1] += h.ptr[size_t(c)];
+    h.col.resize(static_cast<size_t>(nnz));
+    h.val.resize(static_cast<size_t>(nnz));
+    std::vector<int64_t> pos(h.ptr.begin(), h.ptr.end() - 1);
+    for (int r = 0; r < n1; ++r)
+        for (int64_t e = m.outer[r]; e < m.outer[r + 1]; ++e) {
+            const int64_t q = pos[size_t(m.inner[e])]++;
+            h.col[size_t(q)] = r;
+            h.val[size_t(q)] = m.val[e];
+        }
+    return h;
+}
+
+struct Side {
+    int m;
+    const uint32_t* key;
+    const uint8_t* cards;
+    const double* lam;
+};
+
+void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
+    const int O = dir == 0 ? 0 : 1;
+    d.nb = nb;
+    d.sign = dir == 0 ? 1 : -1;
+    d.nO = O == 0 ? boards[0].n1 : boards[0].n2;
+    d.nS = O == 0 ? boards[0].n2 : boards[0].n1;
+    const size_t NB = static_cast<size_t>(nb);
+    std::vector<int64_t> sumOff(NB + 1, 0), outOff(NB + 1, 0), listBase(NB);
+    std::vector<int32_t> listPtr, listHands;
+    std::vector<OutHand> otab;
+    std::vector<double> lamS, lamO;
+    std::vector<int64_t> fptr, sptr;
+    std::vector<int32_t> fcol, scol;
+    std::vector<double> fval, sval;
+    int64_t nnzFS = 0;
+    d.maxMS = 0;
+    for (int b = 0; b < nb; ++b) {
+        const kr_kron_board& B = boards[b];
+        const Side sO = O == 0 ? Side{B.m1, B.key1, B.cards1, B.lambda1} : Side{B.m2, B.key2, B.cards2, B.lambda2};
+        const Side sS = O == 0 ? Side{B.m2, B.key2, B.cards2, B.lambda2} : Side{B.m1, B.key1, B.cards1, B.lambda1};
+        const int mS = sS.m;
+        d.maxMS = std::max(d.maxMS, mS);
+        sumOff[size_t(b) + 1] = sumOff[size_t(b)] + mS;
+        outOff[size_t(b) + 1] = outOff[size_t(b)] + sO.m;
+        lamS.insert(lamS.end(), sS.lam, sS.lam + mS);
+        lamO.insert(lamO.end(), sO.lam, sO.lam + sO.m);
+        // F_d / S_d of this board, positions global
+        const HostCsr F = csr_dir(B.F, B.n1, B.n2, O == 1), S = csr_dir(B.S, B.n1, B.n2, O == 1);
+        for (int a = 0; a <= d.nO; ++a) {
+            fptr.push_back(int64_t(fcol.size()) + F.ptr[size_t(a)]);
+            sptr.push_back(int64_t(scol.size()) + S.ptr[size_t(a)]);
+        }
+        nnzFS += int64_t(F.col.size() + S.col.size()) * mS;
+        fcol.insert(fcol.end(), F.col.begin(), F.col.end());
+        fval.insert(fval.end(), F.val.begin(), F.val.end());
+        scol.insert(scol.end(), S.col.begin(), S.col.end());
+        sval.insert(sval.end(), S.val.begin(), S.val.end());
+        // card lists of the summing side (hands ascending = keys ascending)
+        std::vector<int32_t> cnt(kCards + 1, 0);
+        for (int j = 0; j < mS; ++j)
+            for (int s = 0; s < 2; ++s) cnt[size_t(sS.cards[2 * j + s]) + 1]++;
+        for (int c = 0; c < kCards; ++c) cnt[size_t(c) + 1] += cnt[size_t(c)];
+        listBase[size_t(b)] = int64_t(listHands.size());
+        listPtr.insert(listPtr.end(), cnt.begin(), cnt.end());
+        std::vector<int32_t> lh(static_cast<size_t>(2 * mS));
+        {
+            std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+            for (int j = 0; j < mS; ++j)
+                for (int s = 0; s < 2; ++s) lh[size_t(pos[size_t(sS.cards[2 * j + s])]++)] = j;
+        }
+        listHands.insert(listHands.end(), lh.begin(), lh.end());
+        // output-side lookups
+        const uint32_t* kS = sS.key;
+        for (int i = 0; i < sO.m; ++i) {
+            const uint32_t k = sO.key[i];
+            const int c1 = sO.cards[2 * i], c2 = sO.cards[2 * i + 1];
+            OutHand t{};
+            t.lt = int32_t(std::lower_bound(kS, kS + mS, k) - kS);
+            t.le = int32_t(std::upper_bound(kS, kS + mS, k) - kS);
+            t.dup = -1;
+            t.cards = c1 | (c2 << 8);
+            for (int s = 0; s < 2; ++s) {
+                const int c = s == 0 ? c1 : c2;
+                const int p0 = cnt[size_t(c)], p1 = cnt[size_t(c) + 1];
+                auto keyAt = [&](int p) { return kS[lh[size_t(p)]]; };
+                int lo = p0, hi = p1;  // first list position with key >= k
+                while (lo < hi) {
+                    const int mid = (lo + hi) / 2;
+                    if (keyAt(mid) < k) lo = mid + 1; else hi = mid;
+                }
+                int lo2 = lo, hi2 = p1;  // first with key > k
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) / 2;
+                    if (keyAt(mid) <= k) lo2 = mid + 1; else hi2 = mid;
+                }
+                // list c starts at p0 + c in the board's CPS array
+                if (s == 0) {
+                    t.p1lt = lo + c;
+                    t.p1le = lo2 + c;
+                    t.p1end = p1 + c;
+                } else {
+                    t.p2lt = lo + c;
+                    t.p2le = lo2 + c;
+                    t.p2end = p1 + c;
+                }
+                if (s == 0)
+                    for (int p = p0; p < p1; ++p) {
+                        const int j = lh[size_t(p)];
+                        const int d1 = sS.cards[2 * j], d2 = sS.cards[2 * j + 1];
+                        if ((d1 == c1 && d2 == c2) || (d1 == c2 && d2 == c1)) t.dup = j;
+                    }
+            }
+            otab.push_back(t);
+        }
+    }
+    d.mO = outOff[NB];
+    d.mS = sumOff[NB];
+    // weights (2 flops per F/S entry per summing hand), scans (6 per summing
+    // hand and sequence), combine (14 per output)
+    d.flops = 2 * int64_t(nnzFS) + 6 * int64_t(d.nO) * d.mS + 14 * d.mO * d.nO;
+    d.sumOff = upload(sumOff);
+    d.outOff = upload(outOff);
+    d.lamS = upload(lamS);
+    d.lamO = upload(lamO);
+    d.fptr = upload(fptr);
+    d.fcol = upload(fcol);
+    d.fval = upload(fval);
+    d.sptr = upload(sptr);
+    d.scol = upload(scol);
+    d.sval = upload(sval);
+    d.listPtr = upload(listPtr);
+    d.listBase = upload(listBase);
+    d.listHands = upload(listHands);
+    d.otab = upload(otab);
+}
+
+void free_dir(KronDir& d) {
+    void* ps[] = {d.sumOff, d.outOff, d.lamS, d.lamO, d.fptr, d.fcol, d.fval, d.sptr, d.scol, d.sval,
+                  d.listPtr, d.listBase, d.listHands, d.otab};
+    for (void* p : ps) cudaFree(p);
+    d = KronDir{};
+}
+
+void validate_board(const kr_kron_board& B, const kr_kron_board& B0, int b) {
+    const std::string at = "board " + std::to_string(b) + ": ";
+    if (B.m1 < 0 || B.m2 < 0) throw Fail{KR_INVALID_INPUT, at + "negative hand count"};
+    if (B.n1 < 1 || B.n2 < 1) throw Fail{KR_INVALID_INPUT, at + "empty sequence space"};
+    if (B.n1 != B0.n1 || B.n2 != B0.n2) throw Fail{KR_INVALID_INPUT, at + "boards must share one betting tree"};
+    check_csr(B.F, B.n1, B.n2, "F");
+    check_csr(B.S, B.n1, B.n2, "S");
+    const Side sides[2] = {{B.m1, B.key1, B.cards1, B.lambda1}, {B.m2, B.key2, B.cards2, B.lambda2}};
+    for (const Side& s : sides) {
+        if (s.m > 0 && (!s.key || !s.cards || !s.lam)) throw Fail{KR_INVALID_INPUT, at + "null hand arrays"};
+        for (int i = 0; i < s.m; ++i) {
+            if (i > 0 && s.key[i] < s.key[i - 1])
+                throw Fail{KR_INVALID_INPUT, at + "hands must be strength-sorted ascending (kron.hpp:74-83)"};
+            const int c1 = s.cards[2 * i], c2 = s.cards[2 * i + 1];
+            if (c1 >= kCards || c2 >= kCards || c1 == c2) throw Fail{KR_INVALID_INPUT, at + "bad hand cards"};
+            if (!std::isfinite(s.lam[i])) throw Fail{KR_INVALID_INPUT, at + "non-finite lambda"};
+        }
+    }
+}
+
+}  // namespace
+
+struct KronState {
+    KronDir dir[2];
+    size_t smem[2] = {0, 0};
+};
+
+void kron_destroy(KronState* k) {
+    if (!k) return;
+    free_dir(k->dir[0]);
+    free_dir(k->dir[1]);
+    delete k;
+}
+
+void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
+    KronState* k = e->kron;
+    KronDir& d = k->dir[dir];
+    if (d.mO * d.nO == 0) return;
+    k_kron_fused<<<dim3(unsigned(d.nO), unsigned(d.nb)), kThreads, k->smem[dir], s>>>(d, in, out);
+    KR_CK_LAUNCH();
+    e->launches++;
+    e->flops_last = d.flops;
+    e->flops_total += d.flops;
+}
+
+kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, uint32_t flags) {
+    (void)flags;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw Fail{KR_NO_DEVICE, "no CUDA device available (the engine has no CPU fallback)"};
+    }
+    if (device < 0 || device >= ndev) throw Fail{KR_INVALID_INPUT, "device index out of range"};
+    if (!boards || nb < 1) throw Fail{KR_INVALID_INPUT, "at least one board is required"};
+    int64_t R = 0, C = 0;
+    for (int b = 0; b < nb; ++b) {
+        validate_board(boards[b], boards[0], b);
+        R += int64_t(boards[b].m1) * boards[b].n1;
+        C += int64_t(boards[b].m2) * boards[b].n2;
+    }
+    if (R > INT32_MAX || C > INT32_MAX) throw Fail{KR_INVALID_INPUT, "dimensions exceed 32-bit indices"};
+    KR_CK(cudaSetDevice(device));
+    kr_engine* e = new kr_engine();
+    try {
+        e->device = device;
+        KR_CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->rows = R;
+        e->cols = C;
+        e->n1 = boards[0].n1;
+        e->n2 = boards[0].n2;
+        e->kron = new KronState();
+        size_t smMax = 0;
+        for (int dir = 0; dir < 2; ++dir) {
+            build_dir(e->kron->dir[dir], boards, nb, dir);
+            e->kron->smem[dir] = fused_smem(e->kron->dir[dir].maxMS);
+            smMax = std::max(smMax, e->kron->smem[dir]);
+        }
+        if (smMax > 227 * 1024) throw Fail{KR_INVALID_INPUT, "board has too many hands for the implicit engine"};
+        KR_CK(cudaFuncSetAttribute(k_kron_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smMax)));
+        e->flops_per_product = e->kron->dir[0].flops;
+        e->d_in = dev_alloc<double>(std::max(R, C));
+        e->d_out = dev_alloc<double>(std::max(R, C));
+        KR_CK(cudaDeviceSynchronize());
+    } catch (...) {
+        kr_engine_destroy(e);
+        throw;
+    }
+    return e;
+}
+
+}  // namespace krb
+
+extern "C" int kr_engine_create_kron(const kr_kron_board* boards, int nboards, int device, uint32_t flags,
+                                     kr_engine** out) {
+    return krb::guarded([&] {
+        if (!out) throw krb::Fail{KR_INVALID_INPUT, "null output handle"};
+        *out = krb::create_kron_engine(boards, nboards, device, flags);
+    });
+}

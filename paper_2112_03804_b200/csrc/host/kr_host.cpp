@@ -1376,6 +1376,7 @@ Factors readBundle(const std::string& dir) {  // bundle_io.hpp:57-94
 // ==================================================================== C ABI
 struct krh_instance {
     krh::Instance in;
+    std::vector<uint8_t> cards[2];  // card ids per hand, filled by krh_instance_kron_view
 };
 struct krh_factors {
     krh::Factors f;
@@ -1496,6 +1497,35 @@ int krh_instance_treeplex(const krh_instance* h, int player, int32_t* parent, in
 }
 
 int64_t krh_dense_nnz(const krh_instance* h) { return krh::densePayoffNonzeros(h->in); }
+
+int krh_instance_kron_view(const krh_instance* h, kr_kron_board* out) {
+    return guard([&] {
+        const auto& in = h->in;
+        auto& cards = const_cast<krh_instance*>(h)->cards;
+        for (int p = 0; p < 2; ++p) {
+            cards[p].clear();
+            for (const auto& hd : in.hands[p]) {
+                cards[p].push_back(hd.hi);
+                cards[p].push_back(hd.lo);
+            }
+        }
+        auto view = [](const krh::Compressed& m) {
+            return kr_compressed{m.outerSize(), m.outer.data(), m.inner.data(), m.val.data()};
+        };
+        out->m1 = in.m(0);
+        out->m2 = in.m(1);
+        out->n1 = in.n(0);
+        out->n2 = in.n(1);
+        out->key1 = in.key[0].data();
+        out->key2 = in.key[1].data();
+        out->cards1 = cards[0].data();
+        out->cards2 = cards[1].data();
+        out->lambda1 = in.lambda[0].data();
+        out->lambda2 = in.lambda[1].data();
+        out->F = view(in.F);
+        out->S = view(in.S);
+    });
+}
 
 int krh_sparsify(const krh_instance* h, int technique, int post, int peel_iters, krh_factors** out) {
     return guard([&] {

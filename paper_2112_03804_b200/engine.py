@@ -42,14 +42,35 @@ class CudaEngine:
         arr = (N.kr_factors * len(boards))(*[_factor_struct(b, keep) for b in boards])
         h = C.c_void_p()
         N.check(L.kr_engine_create_boards(arr, len(boards), device, flags, C.byref(h)))
+        self._attach(h, device, len(boards))
+
+    @classmethod
+    def kron(cls, instances, device=0, flags=0):
+        """Implicit Kronecker engine (kr_engine_create_kron): the same products
+        computed from each board's F, S, strength keys, cards and lambdas with
+        nothing materialised.  `instances` is one
+        host.Instance or a list of them sharing one betting tree."""
+        L = N.cuda()
+        insts = instances if isinstance(instances, (list, tuple)) else [instances]
+        arr = (N.kr_kron_board * len(insts))(*[i.kron_view() for i in insts])
+        h = C.c_void_p()
+        N.check(L.kr_engine_create_kron(arr, len(insts), device, flags, C.byref(h)))
+        self = cls.__new__(cls)
+        self._attach(h, device, len(insts))
+        self.implicit = True
+        return self
+
+    implicit = False
+
+    def _attach(self, h, device, nboards):
         self._h = h
         dims = np.zeros(8, np.int64)
-        N.check(L.kr_engine_dims(self._h, N.ptr(dims)))
+        N.check(N.cuda().kr_engine_dims(self._h, N.ptr(dims)))
         self.rows, self.cols, self.k = int(dims[0]), int(dims[1]), int(dims[2])
         self.nnz = {"ahat": int(dims[3]), "u": int(dims[4]), "m": int(dims[5]), "v": int(dims[6])}
         self.m_identity = bool(dims[7])
         self.device = device
-        self.nboards = len(boards)
+        self.nboards = nboards
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -95,7 +116,10 @@ class CudaEngine:
     def bytes_per_product(self):
         """Algorithmic HBM bytes of one product (BASELINE.md §2 formula):
         fp64 values + int32 indices + int32 outer pointers of Ahat, U, V (and
-        M's off-diagonals when M != I), plus reading x and writing y."""
+        M's off-diagonals when M != I), plus reading x and writing y.  The
+        implicit engine materialises nothing: reading x and writing y."""
+        if self.implicit:
+            return 8 * (self.rows + self.cols)
         nz = self.nnz
         b = 12 * nz["ahat"] + 4 * (self.rows + 1) + 12 * nz["u"] + 4 * (self.rows + 1) \
             + 12 * nz["v"] + 4 * (self.k + 1) + 8 * (self.rows + self.cols)

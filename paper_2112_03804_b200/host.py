@@ -26,6 +26,7 @@ HOST_SYMBOLS = [
     "krh_instance_pot", "krh_instance_hands", "krh_instance_vectors", "krh_instance_treeplex", "krh_dense_nnz",
     "krh_sparsify", "krh_postprocess", "krh_factors_from_arrays", "krh_factors_free", "krh_factors_dims",
     "krh_factors_view", "krh_factors_validate", "krh_bundle_write", "krh_bundle_read", "krh_last_error",
+    "krh_instance_kron_view",
 ]
 
 
@@ -55,6 +56,7 @@ def host():
         L.krh_instance_hands.argtypes = [C.c_void_p, C.c_int, C.c_char_p]
         L.krh_instance_vectors.argtypes = [C.c_void_p] + [C.c_void_p] * 4
         L.krh_instance_treeplex.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.krh_instance_kron_view.argtypes = [C.c_void_p, C.POINTER(N.kr_kron_board)]
         L.krh_sparsify.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.krh_postprocess.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
         L.krh_factors_from_arrays.argtypes = [C.POINTER(N.kr_factors), C.c_int, C.c_int, C.POINTER(C.c_void_p)]
@@ -121,6 +123,12 @@ class Instance:
         aseq = np.zeros(max(acts, 1), np.int32)
         _check(host().krh_instance_treeplex(self._h, player, N.ptr(parent), N.ptr(aptr), N.ptr(aseq)))
         return Treeplex(self.n1 if player == 0 else self.n2, parent, aptr, aseq[:acts])
+
+    def kron_view(self):
+        """kr_kron_board for kr_engine_create_kron (valid while self lives)."""
+        v = N.kr_kron_board()
+        _check(host().krh_instance_kron_view(self._h, C.byref(v)))
+        return v
 
     def dense_nnz(self):
         """densePayoffNonzeros (kron.hpp:198-207)."""

@@ -161,12 +161,15 @@ class CudaSolver:
         return br1, br2
 
 
-def solver_for(boards, device=0):
+def solver_for(boards, device=0, implicit=False):
     """Engine + solver over one or more (Instance, Factors) boards that share a
-    betting tree (product host objects, paper_2112_03804_b200.host)."""
+    betting tree (product host objects, paper_2112_03804_b200.host).  With
+    implicit=True the gradient runs on the implicit Kronecker engine
+    (CudaEngine.kron) and the factors are not needed (entries may be bare
+    Instances)."""
     from .engine import CudaEngine
-    insts = [b[0] for b in boards]
-    eng = CudaEngine([b[1] for b in boards], device=device)
+    insts = [b[0] if isinstance(b, (tuple, list)) else b for b in boards]
+    eng = CudaEngine.kron(insts, device=device) if implicit else CudaEngine([b[1] for b in boards], device=device)
     i0 = insts[0]
     return CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [i.m1 for i in insts], [i.m2 for i in insts], i0.pot)
 
