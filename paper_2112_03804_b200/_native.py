@@ -102,7 +102,9 @@ CUDA_SYMBOLS = [
 
 
 def cuda_lib_path():
-    return os.path.join(_build.LIBDIR, "libkrcuda.so")
+    # KR_CUDA_LIB_VARIANT=name loads lib/libkrcuda_<name>.so (A/B kernel timing)
+    v = os.environ.get("KR_CUDA_LIB_VARIANT")
+    return os.path.join(_build.LIBDIR, f"libkrcuda_{v}.so" if v else "libkrcuda.so")
 
 
 def cuda():

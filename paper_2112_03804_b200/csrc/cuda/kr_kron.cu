@@ -17,13 +17,13 @@
 // card list again strength-sorted so its part is a prefix of the list.
 //
 // One fused kernel per product, one CTA per (sequence a, board b); every
-// intermediate lives in shared memory (≈ 5 m_Σ doubles, ≤ 54 KB):
+// intermediate lives in shared memory (≈ 5 m_Σ doubles + 2 m_Σ ints):
 //   1. wf[j], ws[j] for every summing hand j (gathers of v, L2-resident)
-//   2. ps = exclusive prefix of ws, TF = Σ wf, TS = Σ ws (block scan), and
-//      for each of the 52 cards the prefix of ws and the sum of wf over the
-//      hands holding it (one warp per card, shuffle scans)
+//   2. one block scan giving the prefix of ws in strength order, the prefix
+//      of ws inside each of the 52 card lists, TF = Σ wf and the per-card
+//      sums CF[c] of wf (see k_kron_fused)
 //   3. every output hand i of the board: out = λ_O (TF − CF[c1] − CF[c2]
-//      + wf[dup] + σ (lower − upper)), lookups from a per-hand table
+//      + wf[dup] + σ (lower − upper)), lookups from a 16-byte per-hand table
 // so HBM sees only v, the output, and the small per-board tables.  The
 // lookups (key ranks lt / le, their per-card-list counterparts, the
 // duplicate-hand index) depend only on the keys and are built once on the
@@ -45,13 +45,16 @@ constexpr int kCards = 52;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-// Lookup table of one output hand (positions inside the board's shared
-// arrays; card-list positions already include the list's own offset).
-struct alignas(16) OutHand {
-    int32_t lt, le, dup, cards;      // cards = c1 | c2 << 8
-    int32_t p1lt, p1le, p1end, p2lt;
-    int32_t p2le, p2end, pad0, pad1;
-};
+// Lookup table of one output hand, packed in 16 bytes (positions in the
+// kernel's virtual prefix array; list starts and ends come from the staged
+// list pointers):
+//   x = lt | le << 16          (ranks of the hand's key on the summing side)
+//   y = (dup + 1) | c1 << 16 | c2 << 24
+//   z = p1lt | p1le << 16      (m + the same ranks inside the list of c1)
+//   w = p2lt | p2le << 16      (m + ... inside the list of c2)
+// Hands per side per board are at most C(52,2) = 1326, so 3 m < 2^16.
+constexpr int kMaxHands = 1536;            // = kPer * kThreads
+constexpr int kPer = kMaxHands / kThreads; // hands per thread per board
 
 // Device view of one direction (0: A x, 1: Aᵀ y).
 struct KronDir {
@@ -71,15 +74,9 @@ struct KronDir {
     int32_t* listPtr = nullptr;   // [nb*53] offsets in the board's card-list space
     int64_t* listBase = nullptr;  // [nb] base of the board's lists in listHands
     int32_t* listHands = nullptr; // local summing-hand ids, list-major, ascending
-    OutHand* otab = nullptr;      // [mO]
+    int4* otab = nullptr;         // [mO] packed lookups
     int64_t flops = 0;
 };
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 #pragma unroll
@@ -90,103 +87,174 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
-size_t fused_smem(int maxMS) { return sizeof(double) * (5 * size_t(maxMS) + 1 + 2 * kCards); }
+// Dynamic shared memory for a board of maxMS summing hands: wf, ws (m each),
+// the virtual prefix P (3 m + 1), the list-boundary prefixes of wf (56),
+// then the list hands (2 m int32) and list pointers (56 int32).  (Staging the
+// output table too, and looping over several sequences per CTA, was measured
+// slower: the larger footprint halves the resident CTAs per SM.)
+size_t fused_smem(int maxMS) {
+    return sizeof(double) * (5 * size_t(maxMS) + 1 + 56) + sizeof(int32_t) * (2 * size_t(maxMS) + 56);
+}
 
+// One CTA per (sequence a, board b); see the file header for the algebra.
+//
+// The prefix sums run over one virtual array of 3 m entries: the m values
+// ws[j] (strength order), then the 2 m values ws[h] of the 52 card lists laid
+// end to end.  Its exclusive prefix P gives ps = P[0..m] directly and every
+// per-card prefix as a difference P[m + pos] − P[m + start(c)], so a single
+// block scan replaces 53 segmented ones.  The same scan carries wf, whose
+// prefix is only kept at the 53 list boundaries (QB): TF = QB[0] and the
+// per-card sums CF[c] = QB[c+1] − QB[c].
 __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, const double* __restrict__ in,
                                                          double* __restrict__ out) {
     extern __shared__ double sm[];
-    __shared__ double warpTot[kWarps], warpF[kWarps];
+    __shared__ double warpV[kWarps], warpW[kWarps];
     const int a = blockIdx.x, b = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t sBase = d.sumOff[b];
     const int mSb = int(d.sumOff[b + 1] - sBase);
-    double* wf = sm;                  // [mSb]
-    double* ws = wf + mSb;            // [mSb]
-    double* ps = ws + mSb;            // [mSb + 1]
-    double* cps = ps + mSb + 1;       // [2 mSb + 52]
-    double* cf = cps + 2 * mSb + kCards;  // [52]
+    const int N = 3 * mSb;
+    double* wf = sm;             // [mSb]
+    double* ws = wf + mSb;       // [mSb]
+    double* P = ws + mSb;        // [N + 1]
+    double* QB = P + N + 1;      // [53]
+    int32_t* lhand = reinterpret_cast<int32_t*>(QB + 56);  // [2 mSb]
+    int32_t* lptr = lhand + 2 * mSb;                       // [53]
 
-    // 1. weights of every summing hand for sequence a
+    // 1. weights of every summing hand for sequence a: the few F/S entries of
+    // row a are uniform across the CTA, so each thread issues the gathers of
+    // all its kPer hands back to back.  The card lists are staged meanwhile.
     {
+        const int32_t* lb = d.listPtr + int64_t(b) * (kCards + 1);
+        if (tid <= kCards) lptr[tid] = __ldg(lb + tid);
+        const int32_t* hands = d.listHands + d.listBase[b];
+#pragma unroll
+        for (int q = 0; q < 2 * kPer; ++q)
+            if (tid + q * kThreads < 2 * mSb) lhand[tid + q * kThreads] = __ldg(hands + tid + q * kThreads);
+
         const int64_t* fp = d.fptr + int64_t(b) * (d.nO + 1) + a;
         const int64_t* sp = d.sptr + int64_t(b) * (d.nO + 1) + a;
         const int64_t f0 = fp[0], f1 = fp[1], s0 = sp[0], s1 = sp[1];
-        const int nS = d.nS;
-        for (int j = tid; j < mSb; j += kThreads) {
-            const double* v = in + (sBase + j) * int64_t(nS);
-            double f = 0.0, s = 0.0;
-            for (int64_t e = f0; e < f1; ++e) f += __ldg(d.fval + e) * __ldg(v + __ldg(d.fcol + e));
-            for (int64_t e = s0; e < s1; ++e) s += __ldg(d.sval + e) * __ldg(v + __ldg(d.scol + e));
-            const double lam = __ldg(d.lamS + sBase + j);
-            wf[j] = lam * f;
-            ws[j] = lam * s;
+        const int64_t nS = d.nS;
+        const double* v0 = in + (sBase + tid) * nS;
+        const int64_t step = int64_t(kThreads) * nS;
+        double f[kPer], s[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) f[q] = s[q] = 0.0;
+        for (int64_t e = f0; e < f1; ++e) {
+            const double val = __ldg(d.fval + e);
+            const double* vc = v0 + __ldg(d.fcol + e);
+#pragma unroll
+            for (int q = 0; q < kPer; ++q)
+                if (tid + q * kThreads < mSb) f[q] += val * __ldg(vc + q * step);
+        }
+        for (int64_t e = s0; e < s1; ++e) {
+            const double val = __ldg(d.sval + e);
+            const double* vc = v0 + __ldg(d.scol + e);
+#pragma unroll
+            for (int q = 0; q < kPer; ++q)
+                if (tid + q * kThreads < mSb) s[q] += val * __ldg(vc + q * step);
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int j = tid + q * kThreads;
+            if (j < mSb) {
+                const double lam = __ldg(d.lamS + sBase + j);
+                wf[j] = lam * f[q];
+                ws[j] = lam * s[q];
+            }
         }
     }
     __syncthreads();
 
-    // 2a. ps = exclusive prefix of ws; totals TS (ps[mSb]) and TF
-    {
-        const int chunk = (mSb + kThreads - 1) / kThreads;
-        const int j0 = min(mSb, tid * chunk), j1 = min(mSb, j0 + chunk);
-        double loc = 0.0, locF = 0.0;
-        for (int j = j0; j < j1; ++j) {
-            loc += ws[j];
-            locF += wf[j];
-        }
-        const double incl = warp_incl_scan(loc, lane);
-        const double fsum = warp_sum(locF);
-        if (lane == 31) warpTot[warp] = incl;
-        if (lane == 0) warpF[warp] = fsum;
-        __syncthreads();
-        double run = incl - loc;
-        for (int w = 0; w < warp; ++w) run += warpTot[w];
-        for (int j = j0; j < j1; ++j) {
-            ps[j] = run;
-            run += ws[j];
-        }
-        if (tid == kThreads - 1) ps[mSb] = run;
+    // 2. one block scan over the virtual array (contiguous chunk per thread)
+    const int chunk = (N + kThreads - 1) / kThreads;
+    const int j0 = min(N, tid * chunk), j1 = min(N, j0 + chunk);
+    double sv = 0.0, sw = 0.0;
+#pragma unroll 4
+    for (int p = j0; p < j1; ++p) {
+        const int h = p < mSb ? p : lhand[p - mSb];
+        const double v = ws[h];
+        P[p] = v;  // staged; replaced by its prefix below
+        sv += v;
+        sw += wf[h];
     }
-    // 2b. per card: prefix of ws over the hands holding it, and Σ wf
-    {
-        const int32_t* lp = d.listPtr + int64_t(b) * (kCards + 1);
-        const int32_t* hands = d.listHands + d.listBase[b];
-        for (int c = warp; c < kCards; c += kWarps) {
-            const int p0 = lp[c], p1 = lp[c + 1];
-            double* o = cps + p0 + c;
-            double runC = 0.0, runF = 0.0;
-            for (int p = p0; p < p1; p += 32) {
-                const bool ok = p + lane < p1;
-                const int h = ok ? __ldg(hands + p + lane) : 0;
-                const double v = ok ? ws[h] : 0.0;
-                const double u = ok ? wf[h] : 0.0;
-                const double inc = warp_incl_scan(v, lane);
-                if (ok) o[p - p0 + lane] = runC + inc - v;
-                runC += __shfl_sync(0xffffffffu, inc, 31);
-                runF += warp_sum(u);
-            }
-            if (lane == 0) {
-                o[p1 - p0] = runC;
-                cf[c] = runF;
-            }
+    const double iv = warp_incl_scan(sv, lane);
+    const double iw = warp_incl_scan(sw, lane);
+    if (lane == 31) {
+        warpV[warp] = iv;
+        warpW[warp] = iw;
+    }
+    // output tables are independent of the scan: load them before the barrier
+    const int64_t oBase = d.outOff[b];
+    const int mOb = int(d.outOff[b + 1] - oBase);
+    int4 tb[kPer];
+    double lo[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int i = tid + q * kThreads;
+        if (i < mOb) {
+            tb[q] = __ldg(d.otab + oBase + i);
+            lo[q] = __ldg(d.lamO + oBase + i);
         }
     }
+    __syncthreads();
+    double run = iv - sv, runQ = iw - sw;
+    for (int w = 0; w < warp; ++w) {
+        run += warpV[w];
+        runQ += warpW[w];
+    }
+    {
+        // wf prefix at the list boundaries inside [j0, j1): B_c = mSb + lptr[c]
+        int nc = 0;
+        {
+            int hi = kCards + 1;  // first c with mSb + lptr[c] >= j0
+            while (nc < hi) {
+                const int mid = (nc + hi) >> 1;
+                if (mSb + lptr[mid] < j0) nc = mid + 1; else hi = mid;
+            }
+        }
+        int p = j0;
+        for (; nc <= kCards; ++nc) {
+            const int B = mSb + lptr[nc];
+            if (B >= j1) break;
+            for (; p < B; ++p) runQ += wf[p < mSb ? p : lhand[p - mSb]];
+            QB[nc] = runQ;
+        }
+        if (tid == kThreads - 1) {
+            for (; p < j1; ++p) runQ += wf[p < mSb ? p : lhand[p - mSb]];
+            for (; nc <= kCards; ++nc) QB[nc] = runQ;  // lists ending at N
+        }
+    }
+#pragma unroll 4
+    for (int p = j0; p < j1; ++p) {
+        const double v = P[p];
+        P[p] = run;
+        run += v;
+    }
+    if (tid == kThreads - 1) P[N] = run;
     __syncthreads();
 
     // 3. outputs of every hand of the board for sequence a
-    double TF = 0.0;
-    for (int w = 0; w < kWarps; ++w) TF += warpF[w];
-    const double TS = ps[mSb];
-    const int64_t oBase = d.outOff[b];
-    const int mOb = int(d.outOff[b + 1] - oBase);
+    const double TF = QB[0];
+    const double TS = P[mSb];
     const double sg = double(d.sign);
-    for (int i = tid; i < mOb; i += kThreads) {
-        const OutHand t = d.otab[oBase + i];
-        const int c1 = t.cards & 0xff, c2 = t.cards >> 8;
-        double fpart = TF - cf[c1] - cf[c2];
-        if (t.dup >= 0) fpart += wf[t.dup];
-        const double lower = ps[t.lt] - cps[t.p1lt] - cps[t.p2lt];
-        const double upper = (TS - ps[t.le]) - (cps[t.p1end] - cps[t.p1le]) - (cps[t.p2end] - cps[t.p2le]);
-        out[(oBase + i) * d.nO + a] = __ldg(d.lamO + oBase + i) * (fpart + sg * (lower - upper));
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int i = tid + q * kThreads;
+        if (i < mOb) {
+            const int4 t = tb[q];
+            const int lt = t.x & 0xffff, le = t.x >> 16;
+            const int dup = (t.y & 0xffff) - 1, c1 = (t.y >> 16) & 0xff, c2 = t.y >> 24;
+            const int p1lt = t.z & 0xffff, p1le = t.z >> 16, p2lt = t.w & 0xffff, p2le = t.w >> 16;
+            const int B1 = mSb + lptr[c1], E1 = mSb + lptr[c1 + 1];
+            const int B2 = mSb + lptr[c2], E2 = mSb + lptr[c2 + 1];
+            double fpart = TF - (QB[c1 + 1] - QB[c1]) - (QB[c2 + 1] - QB[c2]);
+            if (dup >= 0) fpart += wf[dup];
+            const double lower = P[lt] - (P[p1lt] - P[B1]) - (P[p2lt] - P[B2]);
+            const double upper = (TS - P[le]) - (P[E1] - P[p1le]) - (P[E2] - P[p2le]);
+            out[(oBase + i) * d.nO + a] = lo[q] * (fpart + sg * (lower - upper));
+        }
     }
 }
 
@@ -259,7 +327,7 @@ void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
     const size_t NB = static_cast<size_t>(nb);
     std::vector<int64_t> sumOff(NB + 1, 0), outOff(NB + 1, 0), listBase(NB);
     std::vector<int32_t> listPtr, listHands;
-    std::vector<OutHand> otab;
+    std::vector<int4> otab;
     std::vector<double> lamS, lamO;
     std::vector<int64_t> fptr, sptr;
     std::vector<int32_t> fcol, scol;
@@ -271,6 +339,8 @@ void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
         const Side sO = O == 0 ? Side{B.m1, B.key1, B.cards1, B.lambda1} : Side{B.m2, B.key2, B.cards2, B.lambda2};
         const Side sS = O == 0 ? Side{B.m2, B.key2, B.cards2, B.lambda2} : Side{B.m1, B.key1, B.cards1, B.lambda1};
         const int mS = sS.m;
+        if (mS > kMaxHands || sO.m > kMaxHands)
+            throw Fail{KR_INVALID_INPUT, "more than 1536 hands on one side of a board"};
         d.maxMS = std::max(d.maxMS, mS);
         sumOff[size_t(b) + 1] = sumOff[size_t(b)] + mS;
         outOff[size_t(b) + 1] = outOff[size_t(b)] + sO.m;
@@ -306,11 +376,9 @@ void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
         for (int i = 0; i < sO.m; ++i) {
             const uint32_t k = sO.key[i];
             const int c1 = sO.cards[2 * i], c2 = sO.cards[2 * i + 1];
-            OutHand t{};
-            t.lt = int32_t(std::lower_bound(kS, kS + mS, k) - kS);
-            t.le = int32_t(std::upper_bound(kS, kS + mS, k) - kS);
-            t.dup = -1;
-            t.cards = c1 | (c2 << 8);
+            int32_t lt = int32_t(std::lower_bound(kS, kS + mS, k) - kS);
+            int32_t le = int32_t(std::upper_bound(kS, kS + mS, k) - kS);
+            int32_t dup = -1, plt[2], ple[2];
             for (int s = 0; s < 2; ++s) {
                 const int c = s == 0 ? c1 : c2;
                 const int p0 = cnt[size_t(c)], p1 = cnt[size_t(c) + 1];
@@ -325,23 +393,20 @@ void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
                     const int mid = (lo2 + hi2) / 2;
                     if (keyAt(mid) <= k) lo2 = mid + 1; else hi2 = mid;
                 }
-                // list c starts at p0 + c in the board's CPS array
-                if (s == 0) {
-                    t.p1lt = lo + c;
-                    t.p1le = lo2 + c;
-                    t.p1end = p1 + c;
-                } else {
-                    t.p2lt = lo + c;
-                    t.p2le = lo2 + c;
-                    t.p2end = p1 + c;
-                }
+                plt[s] = mS + lo;  // position in the kernel's virtual prefix array
+                ple[s] = mS + lo2;
                 if (s == 0)
                     for (int p = p0; p < p1; ++p) {
                         const int j = lh[size_t(p)];
                         const int d1 = sS.cards[2 * j], d2 = sS.cards[2 * j + 1];
-                        if ((d1 == c1 && d2 == c2) || (d1 == c2 && d2 == c1)) t.dup = j;
+                        if ((d1 == c1 && d2 == c2) || (d1 == c2 && d2 == c1)) dup = j;
                     }
             }
+            int4 t;
+            t.x = lt | (le << 16);
+            t.y = (dup + 1) | (c1 << 16) | (c2 << 24);
+            t.z = plt[0] | (ple[0] << 16);
+            t.w = plt[1] | (ple[1] << 16);
             otab.push_back(t);
         }
     }
@@ -446,8 +511,9 @@ kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, u
         e->kron = new KronState();
         size_t smMax = 0;
         for (int dir = 0; dir < 2; ++dir) {
-            build_dir(e->kron->dir[dir], boards, nb, dir);
-            e->kron->smem[dir] = fused_smem(e->kron->dir[dir].maxMS);
+            KronDir& d = e->kron->dir[dir];
+            build_dir(d, boards, nb, dir);
+            e->kron->smem[dir] = fused_smem(d.maxMS);
             smMax = std::max(smMax, e->kron->smem[dir]);
         }
         if (smMax > 227 * 1024) throw Fail{KR_INVALID_INPUT, "board has too many hands for the implicit engine"};

@@ -238,7 +238,7 @@ def turn_boards(turn="Ks7d4c2h", nboards=48, tree=3, seed_base=1000):
     return [(c, seed_base + ranks.index(c[0]) * 4 + suits.index(c[1])) for c in cards]
 
 
-def turn_instances(turn="Ks7d4c2h", nboards=48, tree=3, threads=None, indices=None):
+def turn_instances(turn="Ks7d4c2h", nboards=48, tree=3, threads=None, indices=None, factors=True):
     """Build the turn's river instances (and B-post factors) in parallel threads
     (libkrhost releases the GIL inside each ctypes call).  `indices` selects a
     subset of the boards (a rank's shard)."""
@@ -250,7 +250,7 @@ def turn_instances(turn="Ks7d4c2h", nboards=48, tree=3, threads=None, indices=No
     def one(spec):
         card, seed = spec
         inst = builtin("river_full", seed=seed, board=turn + card, tree=tree)
-        return inst, inst.sparsify("b", True)
+        return inst, (inst.sparsify("b", True) if factors else None)
 
     with ThreadPoolExecutor(max_workers=threads or min(16, os.cpu_count() or 1)) as ex:
         return list(ex.map(one, specs))
