@@ -348,6 +348,10 @@ def run_product(args):
     torch.cuda.synchronize(dev)
     solver_s = max_over_ranks(time.perf_counter() - ts)
 
+    # ---- implicit Kronecker engine (K7) -------------
+    implicit = run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
+                            sum_over_ranks)
+
     if rank != 0:
         return 0
     peak, peak_src = measured_peak()
@@ -381,6 +385,7 @@ def run_product(args):
                    "checkpoint_every": 50},
         "gpu_launches": gpu_launches,
         "clocks": sampler.summary(),
+        "implicit": implicit,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds)
@@ -388,6 +393,90 @@ def run_product(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
+                 sum_over_ranks):
+    """The same matvec pairs through the implicit Kronecker engine (nothing
+    materialised: strength-order and card-list prefix scans per board and
+    sequence, kr_kron.cu), on the same boards and inputs: device pairs/s,
+    host-buffer e2e pairs/s, agreement with the factored engine, and DCFR
+    iterations/s driven by it."""
+    import ctypes
+    import torch
+
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200 import _native as N
+    from paper_2112_03804_b200.dist import DistributedDcfr
+    from paper_2112_03804_b200.solver import CudaSolver
+
+    ek = CudaEngine.kron([b[0] for b in boards], device=local)
+    st = torch.cuda.ExternalStream(ek.stream, device=dev)
+    kax = torch.empty_like(ax)
+    katx = torch.empty(ek.cols, dtype=torch.float64, device=dev)
+
+    def pair():
+        ek.ax_device(x.data_ptr(), kax.data_ptr())
+        ek.atx_device(y.data_ptr(), katx.data_ptr())
+
+    for _ in range(max(args.warmup, 3)):
+        pair()
+    torch.cuda.synchronize(dev)
+    l0 = ek.launches()
+    steps = max(args.steps, 50)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(st)
+    for _ in range(steps):
+        pair()
+    e1.record(st)
+    e1.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = int(sum_over_ranks(ek.launches() - l0))
+    dif = float((kax - ax).abs().max().item() / (1.0 + ax.abs().max().item()))
+    dif = max_over_ranks(dif)
+
+    L = N.cuda()
+    nx, ny = ek.cols, ek.rows
+    px, py, pax, patx = (L.kr_host_alloc(8 * n) for n in (nx, ny, ny, nx))
+    as_np = lambda p, n: np.ctypeslib.as_array((ctypes.c_double * n).from_address(p))  # noqa: E731
+    as_np(px, nx)[:] = x.cpu().numpy()
+    as_np(py, ny)[:] = y.cpu().numpy()
+    for _ in range(2):
+        N.check(L.kr_engine_ax(ek.handle, px, nx, pax, ny))
+        N.check(L.kr_engine_atx(ek.handle, py, ny, patx, nx))
+    e2e_steps = 50
+    barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        N.check(L.kr_engine_ax(ek.handle, px, nx, pax, ny))
+        N.check(L.kr_engine_atx(ek.handle, py, ny, patx, nx))
+    e2e_s = max_over_ranks(time.perf_counter() - t)
+    for p in (px, py, pax, patx):
+        L.kr_host_free(p)
+
+    i0 = boards[0][0]
+    solver = CudaSolver(ek, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
+                        i0.pot)
+    drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=coll_dev)
+    drv.run(max_iters=5, checkpoint_every=5)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ts = time.perf_counter()
+    res = drv.run(max_iters=args.solver_iters, checkpoint_every=50)
+    torch.cuda.synchronize(dev)
+    solver_s = max_over_ranks(time.perf_counter() - ts)
+    out = {"engine": "kr_engine_create_kron (k_kron_fused: one CTA per board and sequence)",
+           "pairs_per_s": steps / (ms / 1e3), "us_per_pair": 1e3 * ms / steps, "steps": steps,
+           "gpu_launches": launches, "normwise_diff_vs_factored": dif, "tolerance": 1e-12,
+           "e2e": {"value": e2e_steps / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": 8 * (nx + ny),
+                   "d2h_bytes_per_step": 8 * (nx + ny), "api": "kr_engine_ax / kr_engine_atx (host pinned buffers)"},
+           "solver_iters_per_s": args.solver_iters / solver_s,
+           "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"]}}
+    solver.close()
+    ek.close()
+    return out
 
 
 def main():

@@ -61,8 +61,13 @@ typedef struct {
   int32_t n1, n2;
 } kr_factors;
 
-/* Engine flags. */
+/* Engine flags.  Host-buffer calls (kr_engine_ax / kr_engine_atx) on a
+ * multi-board engine pipeline over up to four board groups, overlapping the
+ * host<->device copies of one group with the kernels of another;
+ * KR_FLAG_SINGLE_PART disables that (one copy, kernels, one copy; the
+ * environment variable KR_GROUPS=<n> sets the group count). */
 #define KR_FLAG_DEFAULT 0u
+#define KR_FLAG_SINGLE_PART 1u
 
 /* One river board in Kronecker form (kron.hpp:104-132): the payoff block of
  * hand pair (i, j) is pi_ij (F + W_ij S) with pi_ij = lambda1_i lambda2_j

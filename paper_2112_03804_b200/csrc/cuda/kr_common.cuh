@@ -78,7 +78,10 @@ T* dev_alloc(int64_t n) {
 }
 
 struct KronState;  // implicit Kronecker engine (kr_kron.cu)
-void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s);
+// Boards [b0, b1) of direction dir (0: A x, 1: Aᵀ y); b1 < 0 = all boards.
+void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0 = 0, int b1 = -1);
+int64_t kron_flops(const kr_engine* e, int dir);
+int kron_boards(const kr_engine* e);
 void kron_destroy(KronState* k);
 
 }  // namespace krb
@@ -144,10 +147,22 @@ struct kr_engine {
     double tMs[4] = {0, 0, 0, 0};
     // implicit Kronecker mode (kr_engine_create_kron): no factors at all
     krb::KronState* kron = nullptr;
+    // Board groups.  Host-buffer calls pipeline over them: input copies,
+    // per-group kernels and output copies run concurrently (copyIn / stream /
+    // copyOut).  grpBoard: board ranges; grpRow / grpCol: row / column
+    // offsets; bSl / bNl: first slice / long row of each board per matrix.
+    std::vector<int64_t> grpRow{0}, grpCol{0};
+    std::vector<int64_t> bSl[4], bNl[4];
+    std::vector<int32_t> grpBoard{0};
+    cudaStream_t copyIn = nullptr, copyOut = nullptr;
+    std::vector<cudaEvent_t> evIn, evOut;
+    int ngroups() const { return int(grpRow.size()) - 1; }
 };
 
 namespace krb {
 // Enqueue the products on `s` (device pointers).
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s);
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s);
+// Copy streams and events for the pipelined host-buffer calls (>= 2 groups).
+void engine_make_pipeline(kr_engine* e);
 }  // namespace krb

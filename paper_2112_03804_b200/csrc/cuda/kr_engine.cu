@@ -184,9 +184,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 }
 
 // x'[s*M2 + J] = x[J*n2 + s]: the sequence-major copy V^T x gathers from.
-__global__ void k_seq_major(const double* __restrict__ x, int64_t M2, int32_t n2, double* __restrict__ xp) {
-    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= M2 * n2) return;
+__global__ void k_seq_major(const double* __restrict__ x, int64_t M2, int32_t n2, double* __restrict__ xp,
+                            int64_t q0, int64_t q1) {
+    const int64_t q = q0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= q1) return;
     const int64_t J = q / n2;
     const int32_t s = int32_t(q - J * n2);
     xp[int64_t(s) * M2 + J] = x[q];
@@ -892,6 +893,10 @@ std::vector<int64_t> board_lengths(const BoardPlan& p, int which) {
 void destroy_engine(kr_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
+    for (cudaEvent_t ev : e->evIn) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->evOut) cudaEventDestroy(ev);
+    if (e->copyIn) cudaStreamDestroy(e->copyIn);
+    if (e->copyOut) cudaStreamDestroy(e->copyOut);
     kron_destroy(e->kron);
     free_sell(e->VT);
     free_sell(e->UA);
@@ -947,8 +952,10 @@ void parallel_boards(int nb, F&& body) {
     if (firstFail.code != KR_OK) throw firstFail;
 }
 
+int group_count(int nb, uint32_t flags);
+void make_pipeline(kr_engine* e);
+
 kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t flags) {
-    (void)flags;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -1167,12 +1174,53 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
                 KR_CK(cudaMemcpy(e->mc_val, cval.data(), 8 * size_t(no), cudaMemcpyHostToDevice));
             }
         }
+        for (int w = 0; w < 4; ++w) {
+            e->bSl[w].clear();
+            e->bNl[w].clear();
+            for (auto& p : plan) {
+                e->bSl[w].push_back(p.slOff[w]);
+                e->bNl[w].push_back(p.nlOff[w]);
+            }
+            e->bSl[w].push_back(tsl[w]);
+            e->bNl[w].push_back(tnl[w]);
+        }
+        const int G = group_count(nb, flags);
+        for (int g = 0; g < G; ++g) {
+            const int g1 = int(int64_t(nb) * (g + 1) / G);
+            e->grpBoard.push_back(g1);
+            e->grpRow.push_back(g1 < nb ? plan[size_t(g1)].rowOff : R);
+            e->grpCol.push_back(g1 < nb ? plan[size_t(g1)].colOff : Cc);
+        }
+        make_pipeline(e);
         KR_CK(cudaDeviceSynchronize());
     } catch (...) {
         destroy_engine(e);
         throw;
     }
     return e;
+}
+
+// Host-call pipeline resources: two copy streams and one event pair per group.
+void make_pipeline(kr_engine* e) {
+    const int G = e->ngroups();
+    if (G < 2) return;
+    KR_CK(cudaStreamCreateWithFlags(&e->copyIn, cudaStreamNonBlocking));
+    KR_CK(cudaStreamCreateWithFlags(&e->copyOut, cudaStreamNonBlocking));
+    e->evIn.resize(size_t(G));
+    e->evOut.resize(size_t(G));
+    for (int g = 0; g < G; ++g) {
+        KR_CK(cudaEventCreateWithFlags(&e->evIn[size_t(g)], cudaEventDisableTiming));
+        KR_CK(cudaEventCreateWithFlags(&e->evOut[size_t(g)], cudaEventDisableTiming));
+    }
+}
+
+// Board groups of the pipelined host-buffer calls: up to four contiguous
+// board ranges (KR_FLAG_SINGLE_PART: one; KR_GROUPS overrides the count).
+int group_count(int nb, uint32_t flags) {
+    if (flags & KR_FLAG_SINGLE_PART) return 1;
+    int G = 4;
+    if (const char* env = std::getenv("KR_GROUPS")) G = std::atoi(env);
+    return std::max(1, std::min(G, nb));
 }
 
 cudaEvent_t pool_event(kr_engine* e) {
@@ -1186,15 +1234,25 @@ cudaEvent_t pool_event(kr_engine* e) {
     return ev;
 }
 
+// Boards [b0, b1) only when b1 >= 0 (a board's slices and long rows are
+// contiguous: SELL windows never straddle boards); untimed.
 void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* xa, const double* xb, int64_t split,
-                 double* y, cudaStream_t s) {
-    const int64_t blocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock +
-                           (A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
+                 double* y, cudaStream_t s, int b0 = 0, int b1 = -1) {
+    int64_t s0 = 0, s1 = A.nslices, l0 = 0, l1 = A.nlong;
+    if (b1 >= 0) {
+        s0 = e->bSl[which][size_t(b0)];
+        s1 = e->bSl[which][size_t(b1)];
+        l0 = e->bNl[which][size_t(b0)];
+        l1 = e->bNl[which][size_t(b1)];
+    }
+    const int64_t blocks = (l1 - l0 + kWarpsPerBlock - 1) / kWarpsPerBlock +
+                           (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return;
-    SellView v{A.slice_ptr, A.lane_row, A.lane_len, A.col, A.val, A.nslices,
-               A.long_ptr, A.long_row, A.long_col, A.long_val, A.nlong};
+    SellView v{A.slice_ptr + s0, A.lane_row + 32 * s0, A.lane_len + 32 * s0, A.col, A.val, s1 - s0,
+               A.long_ptr + l0, A.long_row + l0, A.long_col, A.long_val, l1 - l0};
+    const bool timed = e->timing && b1 < 0;
     kr_engine::Pending pend{which, nullptr, nullptr};
-    if (e->timing) {
+    if (timed) {
         pend.a = pool_event(e);
         pend.b = pool_event(e);
         KR_CK(cudaEventRecord(pend.a, s));
@@ -1202,7 +1260,7 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
     if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
     else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
-    if (e->timing) {
+    if (timed) {
         KR_CK(cudaEventRecord(pend.b, s));
         e->pending.push_back(pend);
     }
@@ -1278,31 +1336,119 @@ void solve_backward(kr_engine* e, cudaStream_t s) {
 
 }  // namespace
 
-void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) {
-    if (e->kron) return kron_product(e, 0, x, y, s);
-    if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    const double* xg = x;
-    if (e->xseq && e->cols > 0) {
-        k_seq_major<<<unsigned((e->cols + 255) / 256), 256, 0, s>>>(x, e->M2, e->n2, e->d_xp);
-        KR_CK_LAUNCH();
-        e->launches++;
-        xg = e->d_xp;
+// One board group's product (monolithic engine: the only group), no flop
+// accounting.  Pointers address the whole vectors.
+void engine_make_pipeline(kr_engine* e) { make_pipeline(e); }
+
+namespace {
+
+// The product as first stage (per board group: the input-side kernels),
+// middle (the M solve, all groups) and last stage (per group: the kernel
+// writing the output).  Pointers address the whole vectors.
+void seq_major(kr_engine* e, const double* x, int64_t c0, int64_t c1, cudaStream_t s) {
+    if (c1 <= c0) return;
+    k_seq_major<<<unsigned((c1 - c0 + 255) / 256), 256, 0, s>>>(x, e->M2, e->n2, e->d_xp, c0, c1);
+    KR_CK_LAUNCH();
+    e->launches++;
+}
+
+void first_stage(kr_engine* e, int dir, const double* in, cudaStream_t s, int g = -1) {
+    if (e->kron) return;
+    const int b0 = g < 0 ? 0 : e->grpBoard[size_t(g)], b1 = g < 0 ? -1 : e->grpBoard[size_t(g) + 1];
+    if (dir == 0) {
+        const double* xg = in;
+        if (e->xseq && e->cols > 0) {
+            seq_major(e, in, g < 0 ? 0 : e->grpCol[size_t(g)], g < 0 ? e->cols : e->grpCol[size_t(g) + 1], s);
+            xg = e->d_xp;
+        }
+        launch_sell(e, 0, e->VT, xg, nullptr, 0, e->d_tz, s, b0, b1);      // t = V^T x    engine.hpp:65-72
+    } else {
+        launch_sell(e, 2, e->UT, in, nullptr, 0, e->d_tz, s, b0, b1);      // s = U^T y    engine.hpp:103-110
     }
-    launch_sell(e, 0, e->VT, xg, nullptr, 0, e->d_tz, s);  // t = V^T x          engine.hpp:65-72
-    solve_forward(e, s);                                   // z = M^-1 t         engine.hpp:74-78
-    launch_sell(e, 1, e->UA, e->d_tz, x, e->kpad, y, s);   // y = U z + Ahat x   engine.hpp:81-89
-    e->flops_last = e->flops_per_product;
+}
+
+void middle(kr_engine* e, int dir, cudaStream_t s) {
+    if (e->kron) return;
+    if (dir == 0) solve_forward(e, s);   // z = M^-1 t    engine.hpp:74-78
+    else solve_backward(e, s);           // z = M^-T s    engine.hpp:112-115
+}
+
+void last_stage(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int g = -1) {
+    const int b0 = g < 0 ? 0 : e->grpBoard[size_t(g)], b1 = g < 0 ? -1 : e->grpBoard[size_t(g) + 1];
+    if (e->kron) return kron_product(e, dir, in, out, s, b0, b1);
+    if (dir == 0) launch_sell(e, 1, e->UA, e->d_tz, in, e->kpad, out, s, b0, b1);   // y = U z + Ahat x
+    else launch_sell(e, 3, e->AV, in, e->d_tz, e->rows, out, s, b0, b1);           // x = Ahat^T y + V z
+}
+
+void account(kr_engine* e, int dir) {
+    e->flops_last = e->kron ? kron_flops(e, dir) : e->flops_per_product;
     e->flops_total += e->flops_last;
 }
 
-void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) {
-    if (e->kron) return kron_product(e, 1, y, x, s);
+}  // namespace
+
+void engine_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    launch_sell(e, 2, e->UT, y, nullptr, 0, e->d_tz, s);      // s = U^T y         engine.hpp:103-110
-    solve_backward(e, s);                                     // z = M^-T s        engine.hpp:112-115
-    launch_sell(e, 3, e->AV, y, e->d_tz, e->rows, x, s);      // x = Ahat^T y + V z  engine.hpp:117-130
-    e->flops_last = e->flops_per_product;
-    e->flops_total += e->flops_last;
+    first_stage(e, dir, in, s);
+    middle(e, dir, s);
+    last_stage(e, dir, in, out, s);
+    account(e, dir);
+}
+
+void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) { engine_product(e, 0, x, y, s); }
+void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) { engine_product(e, 1, y, x, s); }
+
+// Host-buffer product (the reference's synchronous Ax / ATx).  With several
+// board groups the input copy of group g overlaps the first-stage kernels of
+// the groups already copied, and the output copy of group g overlaps the
+// last-stage kernels of the groups after it (copyIn / stream / copyOut).
+void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double* hout, int64_t nout) {
+    const int64_t wantIn = dir == 0 ? e->cols : e->rows, wantOut = dir == 0 ? e->rows : e->cols;
+    if (nin != wantIn)
+        throw Fail{KR_INVALID_INPUT,
+                   "matvec input has size " + std::to_string(nin) + ", expected " + std::to_string(wantIn)};
+    if (nout != wantOut) throw Fail{KR_INVALID_INPUT, "matvec output has the wrong size"};
+    if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
+    KR_CK(cudaSetDevice(e->device));
+    const int G = e->ngroups();
+    if (G < 2) {
+        KR_CK(cudaMemcpyAsync(e->d_in, hin, 8 * size_t(nin), cudaMemcpyHostToDevice, e->stream));
+        engine_product(e, dir, e->d_in, e->d_out, e->stream);
+        KR_CK(cudaMemcpyAsync(hout, e->d_out, 8 * size_t(nout), cudaMemcpyDeviceToHost, e->stream));
+        KR_CK(cudaStreamSynchronize(e->stream));
+        return;
+    }
+    const std::vector<int64_t>& io = dir == 0 ? e->grpCol : e->grpRow;
+    const std::vector<int64_t>& oo = dir == 0 ? e->grpRow : e->grpCol;
+    auto copy_out = [&](int g) {
+        KR_CK(cudaEventRecord(e->evOut[size_t(g)], e->stream));
+        KR_CK(cudaStreamWaitEvent(e->copyOut, e->evOut[size_t(g)], 0));
+        const size_t a = size_t(oo[size_t(g)]), n = size_t(oo[size_t(g) + 1]) - a;
+        KR_CK(cudaMemcpyAsync(hout + a, e->d_out + a, 8 * n, cudaMemcpyDeviceToHost, e->copyOut));
+    };
+    for (int g = 0; g < G; ++g) {
+        const size_t a = size_t(io[size_t(g)]), n = size_t(io[size_t(g) + 1]) - a;
+        KR_CK(cudaMemcpyAsync(e->d_in + a, hin + a, 8 * n, cudaMemcpyHostToDevice, e->copyIn));
+        KR_CK(cudaEventRecord(e->evIn[size_t(g)], e->copyIn));
+    }
+    const bool fused = e->kron != nullptr;  // no middle stage: one kernel per group
+    for (int g = 0; g < G; ++g) {
+        KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
+        first_stage(e, dir, e->d_in, e->stream, g);
+        if (fused) {
+            last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
+            copy_out(g);
+        }
+    }
+    if (!fused) {
+        middle(e, dir, e->stream);
+        for (int g = 0; g < G; ++g) {
+            last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
+            copy_out(g);
+        }
+    }
+    KR_CK(cudaStreamSynchronize(e->copyOut));
+    account(e, dir);
 }
 
 }  // namespace krb
@@ -1355,32 +1501,14 @@ int kr_engine_dims(const kr_engine* e, int64_t out[8]) {
 int kr_engine_ax(kr_engine* e, const double* x, int64_t nx, double* y, int64_t ny) {
     return guarded([&] {
         if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
-        if (nx != e->cols)
-            throw Fail{KR_INVALID_INPUT,
-                       "matvec input has size " + std::to_string(nx) + ", expected " + std::to_string(e->cols)};
-        if (ny != e->rows) throw Fail{KR_INVALID_INPUT, "matvec output has the wrong size"};
-        if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-        KR_CK(cudaSetDevice(e->device));
-        KR_CK(cudaMemcpyAsync(e->d_in, x, 8 * size_t(nx), cudaMemcpyHostToDevice, e->stream));
-        krb::engine_ax(e, e->d_in, e->d_out, e->stream);
-        KR_CK(cudaMemcpyAsync(y, e->d_out, 8 * size_t(ny), cudaMemcpyDeviceToHost, e->stream));
-        KR_CK(cudaStreamSynchronize(e->stream));
+        krb::host_product(e, 0, x, nx, y, ny);
     });
 }
 
 int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t nx) {
     return guarded([&] {
         if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
-        if (ny != e->rows)
-            throw Fail{KR_INVALID_INPUT,
-                       "matvec input has size " + std::to_string(ny) + ", expected " + std::to_string(e->rows)};
-        if (nx != e->cols) throw Fail{KR_INVALID_INPUT, "matvec output has the wrong size"};
-        if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-        KR_CK(cudaSetDevice(e->device));
-        KR_CK(cudaMemcpyAsync(e->d_in, y, 8 * size_t(ny), cudaMemcpyHostToDevice, e->stream));
-        krb::engine_atx(e, e->d_in, e->d_out, e->stream);
-        KR_CK(cudaMemcpyAsync(x, e->d_out, 8 * size_t(nx), cudaMemcpyDeviceToHost, e->stream));
-        KR_CK(cudaStreamSynchronize(e->stream));
+        krb::host_product(e, 1, y, ny, x, nx);
     });
 }
 

@@ -31,6 +31,7 @@
 // (different summation order): tests hold them to 1e-12 normwise.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -105,11 +106,11 @@ size_t fused_smem(int maxMS) {
 // block scan replaces 53 segmented ones.  The same scan carries wf, whose
 // prefix is only kept at the 53 list boundaries (QB): TF = QB[0] and the
 // per-card sums CF[c] = QB[c+1] − QB[c].
-__global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, const double* __restrict__ in,
+__global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
                                                          double* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double warpV[kWarps], warpW[kWarps];
-    const int a = blockIdx.x, b = blockIdx.y;
+    const int a = blockIdx.x, b = b0 + int(blockIdx.y);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t sBase = d.sumOff[b];
     const int mSb = int(d.sumOff[b + 1] - sBase);
@@ -472,19 +473,20 @@ void kron_destroy(KronState* k) {
     delete k;
 }
 
-void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
+void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
     KronState* k = e->kron;
     KronDir& d = k->dir[dir];
-    if (d.mO * d.nO == 0) return;
-    k_kron_fused<<<dim3(unsigned(d.nO), unsigned(d.nb)), kThreads, k->smem[dir], s>>>(d, in, out);
+    if (b1 < 0) b1 = d.nb;
+    if (d.mO * d.nO == 0 || b1 <= b0) return;
+    k_kron_fused<<<dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads, k->smem[dir], s>>>(d, b0, in, out);
     KR_CK_LAUNCH();
     e->launches++;
-    e->flops_last = d.flops;
-    e->flops_total += d.flops;
 }
 
+int64_t kron_flops(const kr_engine* e, int dir) { return e->kron->dir[dir].flops; }
+int kron_boards(const kr_engine* e) { return e->kron->dir[0].nb; }
+
 kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, uint32_t flags) {
-    (void)flags;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -521,6 +523,24 @@ kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, u
         e->flops_per_product = e->kron->dir[0].flops;
         e->d_in = dev_alloc<double>(std::max(R, C));
         e->d_out = dev_alloc<double>(std::max(R, C));
+        // board groups for the pipelined host-buffer calls
+        // (eight: the kernel is short next to the copies, so finer groups
+        // shorten the unhidden first input copy and last output copy)
+        int G = 8;
+        if (const char* env = std::getenv("KR_GROUPS")) G = std::atoi(env);
+        G = (flags & KR_FLAG_SINGLE_PART) ? 1 : std::max(1, std::min(nb, G));
+        for (int g = 0; g < G; ++g) {
+            const int g0 = int(int64_t(nb) * g / G), g1 = int(int64_t(nb) * (g + 1) / G);
+            int64_t r = 0, c = 0;
+            for (int b = g0; b < g1; ++b) {
+                r += int64_t(boards[b].m1) * boards[b].n1;
+                c += int64_t(boards[b].m2) * boards[b].n2;
+            }
+            e->grpBoard.push_back(g1);
+            e->grpRow.push_back(e->grpRow.back() + r);
+            e->grpCol.push_back(e->grpCol.back() + c);
+        }
+        engine_make_pipeline(e);
         KR_CK(cudaDeviceSynchronize());
     } catch (...) {
         kr_engine_destroy(e);
