@@ -20,6 +20,7 @@
 // with std::pow exactly as the reference does and passed as kernel arguments.
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kr_common.cuh"
@@ -36,6 +37,9 @@ struct kr_solver {
     double pot = 0;
     int32_t* d_tree[2] = {nullptr, nullptr};  // [parent(nn) | aptr(nn+1) | aseq(na)]
     int32_t treeLen[2] = {0, 0};
+    int32_t na[2] = {0, 0};      // actions (entries of action_seq)
+    bool levelled[2] = {false, false};  // level tables appended (team step kernel)
+    int nlev[2] = {0, 0};
     int64_t* d_bstart[2] = {nullptr, nullptr};
     double* regret[2] = {nullptr, nullptr};
     double* avg[2] = {nullptr, nullptr};
@@ -80,24 +84,21 @@ struct RmStats {
 __device__ __forceinline__ RmStats rm_stats(const double* R, int stride, const int32_t* seqs, int count) {
     double best = R[(seqs[0] - 1) * stride];
     double maxAbs = fabs(best);
+    double sumPos = best > 0 ? 0.0 + best : 0.0;  // the same additions, in action order
     for (int a = 1; a < count; ++a) {
         const double r = R[(seqs[a] - 1) * stride];
         best = (best < r) ? r : best;  // std::max
         const double ar = fabs(r);
         maxAbs = (maxAbs < ar) ? ar : maxAbs;
+        if (r > 0) sumPos += r;
     }
     const double tol = 1e-9 * (1 + maxAbs);
     RmStats st;
     st.positive = best > tol;
-    st.sumPos = 0;
+    st.sumPos = sumPos;
     st.cut = best - tol;
     st.uniform = 0;
-    if (st.positive) {
-        for (int a = 0; a < count; ++a) {
-            const double r = R[(seqs[a] - 1) * stride];
-            if (r > 0) st.sumPos += r;
-        }
-    } else {
+    if (!st.positive) {
         int ties = 0;
         for (int a = 0; a < count; ++a)
             if (R[(seqs[a] - 1) * stride] >= st.cut) ++ties;
@@ -250,6 +251,167 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
     }
 }
 
+// The same player step with a team of kTeam lanes per hand: the treeplex is
+// walked level by level (its own-decision depth, 2-3 levels for river trees)
+// and the lanes of a team take the nodes of a level in parallel.  Bitwise
+// identical to k_player_step: every node performs the reference's per-node
+// arithmetic in the same order, and the bottom-up accumulation of child node
+// values into a sequence (Vt[parent] += nodeVal, solver.hpp:243, in
+// descending node order) is replaced by pulling the children's values in
+// that same descending order when the sequence's own node is processed.
+// Needs every node's parent sequence to belong to an earlier node (true for
+// the reference's skeleton); the host checks it and otherwise uses
+// k_player_step.  Level tables follow the base tree in treeBuf:
+//   nlev | levPtr[nlev+1] | levNodes[nn] | chPtr[n+2] | chNodes[...]
+// (chNodes: per sequence its child nodes, descending).
+constexpr int kTeam = 8;
+__global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __restrict__ treeBuf, int nn, int n,
+                                                     int na, int tlen, int64_t H, int hpb,
+                                                     const double* __restrict__ g, int negate,
+                                                     double* __restrict__ regret, double* __restrict__ xout,
+                                                     double* __restrict__ avg, double pos, double neg, double shrink) {
+    extern __shared__ double sm[];
+    const int stride = hpb + 1;
+    double* Rg = sm;                      // n x stride      regrets
+    double* V = Rg + n * stride;          // (n+1) x stride  gradient -> values -> probabilities -> reach
+    double* NV = V + (n + 1) * stride;    // nn x stride     node values
+    int32_t* T = reinterpret_cast<int32_t*>(NV + nn * stride);
+    for (int q = threadIdx.x; q < tlen; q += blockDim.x) T[q] = treeBuf[q];
+    const int64_t h0 = int64_t(blockIdx.x) * hpb;
+    const int nh = int(lmin(hpb, H - h0));
+    const int64_t e0 = h0 * n;
+    const int ne = nh * n;
+    // element q = hh * n + sq of the block's rows; the thread's position is
+    // advanced by blockDim.x without divisions
+    const int dh = int(blockDim.x) / n, ds = int(blockDim.x) - dh * n;
+    const int hh0 = int(threadIdx.x) / n, sq0 = int(threadIdx.x) - hh0 * n;
+    // coalesced staging: regrets, and (mode 1) the gradient rows into V[1..n]
+    {
+        int hh = hh0, sq = sq0;
+#pragma unroll 4
+        for (int q = threadIdx.x; q < ne; q += blockDim.x) {
+            Rg[sq * stride + hh] = regret[e0 + q];
+            if (mode == 1) V[(sq + 1) * stride + hh] = g[e0 + q];
+            hh += dh;
+            sq += ds;
+            if (sq >= n) {
+                sq -= n;
+                ++hh;
+            }
+        }
+    }
+    __syncthreads();
+    const Tree tr = tree_view(T, nn);
+    const int32_t* lv = T + 2 * nn + 1 + na;  // nlev, levPtr, levNodes, chPtr, chNodes, levSeqPtr, levSeq, seqPar
+    const int nlev = lv[0];
+    const int32_t* levPtr = lv + 1;
+    const int32_t* levNodes = levPtr + nlev + 1;
+    const int32_t* chPtr = levNodes + nn;
+    const int32_t* chNodes = chPtr + n + 2;
+    const int32_t* levSeqPtr = chNodes + chPtr[n + 1];
+    const int32_t* levSeq = levSeqPtr + nlev + 1;
+    const int32_t* seqPar = levSeq + n;  // parent sequence of each sequence's node (by sequence id - 1)
+    const int hand = threadIdx.x / kTeam, lane = threadIdx.x % kTeam;
+    const bool valid = hand < nh;
+    double* R = Rg + hand;
+    double* Vt = V + hand;
+    double* Nt = NV + hand;
+    if (mode == 1) {
+        // cfrSweep (solver.hpp:227-245), deepest level first.  Once a node's
+        // regrets are final its sequenceForm probabilities (solver.hpp:
+        // 202-215 reads exactly these regrets) replace the values in V.
+        for (int l = nlev - 1; l >= 0; --l) {
+            if (valid)
+                for (int k = levPtr[l] + lane; k < levPtr[l + 1]; k += kTeam) {
+                    const int v = levNodes[k];
+                    const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
+                    const int32_t* seqs = tr.aseq + a0;
+                    const RmStats st = rm_stats(R, stride, seqs, cnt);
+                    double nodeVal = 0;
+                    for (int a = 0; a < cnt; ++a) {
+                        const int sq = seqs[a];
+                        double cs = 0.0;  // Vt[sq] of the reference: children, descending
+                        for (int c = chPtr[sq]; c < chPtr[sq + 1]; ++c) cs += Nt[chNodes[c] * stride];
+                        const double gr = Vt[sq * stride];
+                        const double gv = negate ? -gr : gr;
+                        const double ev = gv + cs;
+                        Vt[sq * stride] = ev;
+                        nodeVal += rm_prob(st, R[(sq - 1) * stride]) * ev;
+                    }
+                    for (int a = 0; a < cnt; ++a) {
+                        const int sq = seqs[a];
+                        R[(sq - 1) * stride] += Vt[sq * stride] - nodeVal;
+                    }
+                    Nt[v * stride] = nodeVal;
+                    const RmStats st2 = rm_stats(R, stride, seqs, cnt);
+                    for (int a = 0; a < cnt; ++a) {
+                        const int sq = seqs[a];
+                        Vt[sq * stride] = rm_prob(st2, R[(sq - 1) * stride]);
+                    }
+                }
+            __syncwarp();
+        }
+        // sequenceForm: reach = mass * prob, root level first, lanes over sequences
+        if (valid && lane == 0) Vt[0] = 1.0;
+        __syncwarp();
+        for (int l = 0; l < nlev; ++l) {
+            if (valid)
+                for (int k = levSeqPtr[l] + lane; k < levSeqPtr[l + 1]; k += kTeam) {
+                    const int sq = levSeq[k];
+                    Vt[sq * stride] = Vt[seqPar[sq - 1] * stride] * Vt[sq * stride];
+                }
+            __syncwarp();
+        }
+        if (valid)  // discount (solver.hpp:262-264)
+            for (int q = lane; q < n; q += kTeam) {
+                const double r = R[q * stride];
+                R[q * stride] = r * (r > 0 ? pos : neg);
+            }
+    } else {
+        // sequenceForm only (initial strategy, solver.hpp:363-364)
+        if (valid && lane == 0) Vt[0] = 1.0;
+        __syncwarp();
+        for (int l = 0; l < nlev; ++l) {
+            if (valid)
+                for (int k = levPtr[l] + lane; k < levPtr[l + 1]; k += kTeam) {
+                    const int v = levNodes[k];
+                    const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
+                    const int32_t* seqs = tr.aseq + a0;
+                    const RmStats st = rm_stats(R, stride, seqs, cnt);
+                    const double mass = Vt[tr.parent[v] * stride];
+                    for (int a = 0; a < cnt; ++a) {
+                        const int sq = seqs[a];
+                        Vt[sq * stride] = mass * rm_prob(st, R[(sq - 1) * stride]);
+                    }
+                }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    {
+        int hh = hh0, sq = sq0;
+#pragma unroll 4
+        for (int q = threadIdx.x; q < ne; q += blockDim.x) {
+            const double xv = V[(sq + 1) * stride + hh];
+            xout[e0 + q] = xv;
+            if (mode == 1) {
+                regret[e0 + q] = Rg[sq * stride + hh];
+                avg[e0 + q] = (avg[e0 + q] + xv) * shrink;  // solver.hpp:382-386
+            }
+            hh += dh;
+            sq += ds;
+            if (sq >= n) {
+                sq -= n;
+                ++hh;
+            }
+        }
+    }
+}
+
+size_t team_smem(int n, int nn, int hpb, int tlen) {
+    return size_t(2 * n + 1 + nn) * size_t(hpb + 1) * 8 + size_t(tlen) * 4 + 16;
+}
+
 __global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w, double* __restrict__ out) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q < n) out[q] = avg[q] / w;  // solver.hpp:390-391
@@ -338,16 +500,81 @@ __global__ void k_validate(const int32_t* __restrict__ treeBuf, int nn, int n, i
     }
 }
 
+// Level tables for k_player_team (appended to the base tree buffer), when
+// every node's parent sequence belongs to an earlier node.
+void append_levels(const kr_treeplex& t, std::vector<int32_t>& buf, bool& ok, int& nlev) {
+    const int nn = t.n_nodes, n = t.n_seq;
+    std::vector<int32_t> owner(size_t(n) + 1, -1), lev(size_t(nn), 0);
+    for (int v = 0; v < nn; ++v)
+        for (int a = t.node_action_ptr[v]; a < t.node_action_ptr[v + 1]; ++a) owner[size_t(t.action_seq[a])] = v;
+    ok = true;
+    nlev = 0;
+    for (int v = 0; v < nn; ++v) {
+        const int ps = t.node_parent_seq[v];
+        if (ps == 0) lev[size_t(v)] = 0;
+        else if (owner[size_t(ps)] >= 0 && owner[size_t(ps)] < v) lev[size_t(v)] = lev[size_t(owner[size_t(ps)])] + 1;
+        else {
+            ok = false;
+            return;
+        }
+        nlev = std::max(nlev, lev[size_t(v)] + 1);
+    }
+    std::vector<int32_t> levPtr(size_t(nlev) + 1, 0), levNodes;
+    for (int v = 0; v < nn; ++v) levPtr[size_t(lev[size_t(v)]) + 1]++;
+    for (int l = 0; l < nlev; ++l) levPtr[size_t(l) + 1] += levPtr[size_t(l)];
+    for (int l = 0; l < nlev; ++l)
+        for (int v = 0; v < nn; ++v)
+            if (lev[size_t(v)] == l) levNodes.push_back(v);
+    std::vector<int32_t> chPtr(size_t(n) + 2, 0), chNodes;
+    for (int sq = 0; sq <= n; ++sq) {
+        chPtr[size_t(sq)] = int32_t(chNodes.size());
+        for (int v = nn - 1; v >= 0; --v)
+            if (t.node_parent_seq[v] == sq) chNodes.push_back(v);
+    }
+    chPtr[size_t(n) + 1] = int32_t(chNodes.size());
+    // sequences by level of their node, and each sequence's parent sequence
+    std::vector<int32_t> levSeqPtr(size_t(nlev) + 1, 0), levSeq, seqPar(size_t(n), 0);
+    for (int l = 0; l < nlev; ++l) {
+        for (int v : levNodes)
+            if (lev[size_t(v)] == l)
+                for (int a = t.node_action_ptr[v]; a < t.node_action_ptr[v + 1]; ++a) {
+                    levSeq.push_back(t.action_seq[a]);
+                    seqPar[size_t(t.action_seq[a]) - 1] = t.node_parent_seq[v];
+                }
+        levSeqPtr[size_t(l) + 1] = int32_t(levSeq.size());
+    }
+    buf.push_back(nlev);
+    buf.insert(buf.end(), levPtr.begin(), levPtr.end());
+    buf.insert(buf.end(), levNodes.begin(), levNodes.end());
+    buf.insert(buf.end(), chPtr.begin(), chPtr.end());
+    buf.insert(buf.end(), chNodes.begin(), chNodes.end());
+    buf.insert(buf.end(), levSeqPtr.begin(), levSeqPtr.end());
+    buf.insert(buf.end(), levSeq.begin(), levSeq.end());
+    buf.insert(buf.end(), seqPar.begin(), seqPar.end());
+}
+
 size_t step_smem(int n, int nt, int nn, int na) {
     return size_t(2 * n + 1) * size_t(nt + 1) * 8 + size_t(2 * nn + 1 + na) * 4 + 16;
 }
 
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
                  cudaStream_t st) {
+    if (s->levelled[p]) {
+        const int hpb = 256 / kTeam;
+        const unsigned grid = unsigned((s->H[p] + hpb - 1) / hpb);
+        if (grid == 0) return;
+        const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
+        k_player_team<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p],
+                                               s->H[p], hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg,
+                                               shrink);
+        KR_CK_LAUNCH();
+        s->launches++;
+        return;
+    }
     const int nt = s->nt[p];
     const unsigned grid = unsigned((s->H[p] + nt - 1) / nt);
     if (grid == 0) return;
-    const int na = s->treeLen[p] - (2 * s->nnodes[p] + 1);
+    const int na = s->na[p];
     const size_t smem = step_smem(s->n[p], nt, s->nnodes[p], na);
     k_player_step<<<grid, nt, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->H[p], nt, g, negate,
                                           s->regret[p], s->x[p], s->avg[p], pos, neg, shrink);
@@ -363,7 +590,7 @@ void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<
     else engine_atx(e, opp, s->g, st);
     const int nn = s->nnodes[player], n = s->n[player];
     const int bt = 128;
-    const int na = s->treeLen[player] - (2 * nn + 1);
+    const int na = s->na[player];
     const size_t smem = size_t((2 * nn + 1 + na + 2) * 4) + size_t(n + 1) * bt * 8 + 16;
     const unsigned grid = unsigned((s->H[player] + bt - 1) / bt);
     if (grid) {
@@ -446,6 +673,10 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 buf.insert(buf.end(), t.node_parent_seq, t.node_parent_seq + t.n_nodes);
                 buf.insert(buf.end(), t.node_action_ptr, t.node_action_ptr + t.n_nodes + 1);
                 buf.insert(buf.end(), t.action_seq, t.action_seq + na);
+                s->na[p] = na;
+                krb::append_levels(t, buf, s->levelled[p], s->nlev[p]);
+                if (const char* env = std::getenv("KR_STEP"))
+                    if (std::string(env) == "thread") s->levelled[p] = false;
                 s->treeLen[p] = int32_t(buf.size());
                 s->d_tree[p] = krb::dev_alloc<int32_t>(int64_t(buf.size()));
                 KR_CK(cudaMemcpy(s->d_tree[p], buf.data(), 4 * buf.size(), cudaMemcpyHostToDevice));
@@ -466,6 +697,13 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 s->nt[p] = nt;
                 KR_CK(cudaFuncSetAttribute(krb::k_player_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(krb::step_smem(t.n_seq, nt, t.n_nodes, na))));
+                if (s->levelled[p]) {
+                    const size_t tsm = krb::team_smem(t.n_seq, t.n_nodes, 256 / krb::kTeam, s->treeLen[p]);
+                    if (tsm > 220 * 1024) s->levelled[p] = false;
+                    else
+                        KR_CK(cudaFuncSetAttribute(krb::k_player_team, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(std::max(tsm, size_t(48 * 1024)))));
+                }
                 const int64_t len = s->H[p] * s->n[p];
                 s->regret[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
                 s->avg[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
