@@ -40,6 +40,7 @@ struct kr_solver {
     int32_t na[2] = {0, 0};      // actions (entries of action_seq)
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
+    int team = 4;                // lanes per hand in k_player_team (2, 4 or 8)
     int64_t* d_bstart[2] = {nullptr, nullptr};
     double* regret[2] = {nullptr, nullptr};
     double* avg[2] = {nullptr, nullptr};
@@ -264,7 +265,7 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
 // k_player_step.  Level tables follow the base tree in treeBuf:
 //   nlev | levPtr[nlev+1] | levNodes[nn] | chPtr[n+2] | chNodes[...]
 // (chNodes: per sequence its child nodes, descending).
-constexpr int kTeam = 8;
+template <int kTeam>
 __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __restrict__ treeBuf, int nn, int n,
                                                      int na, int tlen, int64_t H, int hpb,
                                                      const double* __restrict__ g, int negate,
@@ -560,13 +561,14 @@ size_t step_smem(int n, int nt, int nn, int na) {
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
                  cudaStream_t st) {
     if (s->levelled[p]) {
-        const int hpb = 256 / kTeam;
+        const int team = s->team;
+        const int hpb = 256 / team;
         const unsigned grid = unsigned((s->H[p] + hpb - 1) / hpb);
         if (grid == 0) return;
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
-        k_player_team<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p],
-                                               s->H[p], hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg,
-                                               shrink);
+        auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
+        kern<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
+                                      hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink);
         KR_CK_LAUNCH();
         s->launches++;
         return;
@@ -695,20 +697,36 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 if (krb::step_smem(t.n_seq, nt, t.n_nodes, na) > 220 * 1024)
                     throw Fail{KR_INVALID_INPUT, "treeplex too large for the on-chip solver step"};
                 s->nt[p] = nt;
-                KR_CK(cudaFuncSetAttribute(krb::k_player_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(krb::step_smem(t.n_seq, nt, t.n_nodes, na))));
+                if (const char* env = std::getenv("KR_TEAM")) {
+                    const int tm = std::atoi(env);
+                    s->team = tm == 2 || tm == 8 ? tm : 4;
+                }
                 if (s->levelled[p]) {
-                    const size_t tsm = krb::team_smem(t.n_seq, t.n_nodes, 256 / krb::kTeam, s->treeLen[p]);
+                    // the team size must fit the smem budget (hands per block = 256 / team)
+                    while (s->team < 8 && krb::team_smem(t.n_seq, t.n_nodes, 256 / s->team, s->treeLen[p]) > 200 * 1024)
+                        s->team *= 2;
+                    const size_t tsm = krb::team_smem(t.n_seq, t.n_nodes, 256 / s->team, s->treeLen[p]);
                     if (tsm > 220 * 1024) s->levelled[p] = false;
-                    else
-                        KR_CK(cudaFuncSetAttribute(krb::k_player_team, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(std::max(tsm, size_t(48 * 1024)))));
                 }
                 const int64_t len = s->H[p] * s->n[p];
                 s->regret[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
                 s->avg[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
                 s->x[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
                 s->a[p] = krb::dev_alloc<double>(std::max<int64_t>(len, 1));
+            }
+            {
+                size_t satt = 0;
+                for (int p = 0; p < 2; ++p)
+                    satt = std::max(satt, krb::step_smem(s->n[p], s->nt[p], s->nnodes[p], s->na[p]));
+                KR_CK(cudaFuncSetAttribute(krb::k_player_step, cudaFuncAttributeMaxDynamicSharedMemorySize, int(satt)));
+                // one attribute for both players (the final team size)
+                size_t att = 48 * 1024;
+                for (int p = 0; p < 2; ++p)
+                    if (s->levelled[p])
+                        att = std::max(att, krb::team_smem(s->n[p], s->nnodes[p], 256 / s->team, s->treeLen[p]));
+                KR_CK(cudaFuncSetAttribute(krb::k_player_team<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att)));
+                KR_CK(cudaFuncSetAttribute(krb::k_player_team<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att)));
+                KR_CK(cudaFuncSetAttribute(krb::k_player_team<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att)));
             }
             if (s->H[0] * s->n[0] != e->rows || s->H[1] * s->n[1] != e->cols)
                 throw Fail{KR_INVALID_INPUT, "treeplex x hands does not match the engine dimensions"};
