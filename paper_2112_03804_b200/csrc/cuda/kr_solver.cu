@@ -289,15 +289,26 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
     // coalesced staging: regrets, and (mode 1) the gradient rows into V[1..n]
     {
         int hh = hh0, sq = sq0;
-#pragma unroll 4
-        for (int q = threadIdx.x; q < ne; q += blockDim.x) {
-            Rg[sq * stride + hh] = regret[e0 + q];
-            if (mode == 1) V[(sq + 1) * stride + hh] = g[e0 + q];
-            hh += dh;
-            sq += ds;
-            if (sq >= n) {
-                sq -= n;
-                ++hh;
+        for (int q0 = threadIdx.x; q0 < ne; q0 += 4 * blockDim.x) {
+            double r[4], gv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // loads first: 4 (8) in flight
+                const int q = q0 + u * int(blockDim.x);
+                r[u] = q < ne ? regret[e0 + q] : 0.0;
+                gv[u] = (mode == 1 && q < ne) ? g[e0 + q] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (q0 + u * int(blockDim.x) < ne) {
+                    Rg[sq * stride + hh] = r[u];
+                    V[(sq + 1) * stride + hh] = gv[u];
+                }
+                hh += dh;
+                sq += ds;
+                if (sq >= n) {
+                    sq -= n;
+                    ++hh;
+                }
             }
         }
     }
@@ -391,19 +402,30 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
     __syncthreads();
     {
         int hh = hh0, sq = sq0;
-#pragma unroll 4
-        for (int q = threadIdx.x; q < ne; q += blockDim.x) {
-            const double xv = V[(sq + 1) * stride + hh];
-            xout[e0 + q] = xv;
-            if (mode == 1) {
-                regret[e0 + q] = Rg[sq * stride + hh];
-                avg[e0 + q] = (avg[e0 + q] + xv) * shrink;  // solver.hpp:382-386
+        for (int q0 = threadIdx.x; q0 < ne; q0 += 4 * blockDim.x) {
+            double a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * int(blockDim.x);
+                a[u] = (mode == 1 && q < ne) ? avg[e0 + q] : 0.0;
             }
-            hh += dh;
-            sq += ds;
-            if (sq >= n) {
-                sq -= n;
-                ++hh;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * int(blockDim.x);
+                if (q < ne) {
+                    const double xv = V[(sq + 1) * stride + hh];
+                    xout[e0 + q] = xv;
+                    if (mode == 1) {
+                        regret[e0 + q] = Rg[sq * stride + hh];
+                        avg[e0 + q] = (a[u] + xv) * shrink;  // solver.hpp:382-386
+                    }
+                }
+                hh += dh;
+                sq += ds;
+                if (sq >= n) {
+                    sq -= n;
+                    ++hh;
+                }
             }
         }
     }
