@@ -95,11 +95,12 @@ private:
     kr_engine* e_ = nullptr;
 };
 
-struct DcfrParams {  // solver.hpp:101-109
+struct DcfrParams {  // solver.hpp:101-109 (+ rule: KR_RULE_*, 0 = the reference's DCFR)
     double alpha = 1.5, beta = 0.0, gamma = 2.0;
     int maxIters = 1000;
     double targetExploitability = 0.0;
     int checkpointEvery = 50;
+    int rule = KR_RULE_DCFR;
 };
 
 struct TracePoint {
@@ -147,7 +148,7 @@ public:
         DcfrResult out;
         out.avg1.resize(size_t(rows_));
         out.avg2.resize(size_t(cols_));
-        kr_dcfr_params prm{p.alpha, p.beta, p.gamma, p.maxIters, p.targetExploitability, p.checkpointEvery};
+        kr_dcfr_params prm{p.alpha, p.beta, p.gamma, p.maxIters, p.targetExploitability, p.checkpointEvery, p.rule};
         kr_dcfr_result r{};
         r.trace_cap = cap;
         r.trace_iter = it.data();

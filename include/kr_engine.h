@@ -166,12 +166,25 @@ typedef struct {
   const int32_t* action_seq;
 } kr_treeplex;
 
-/* DcfrParams (solver.hpp:101-109). */
+/* DcfrParams (solver.hpp:101-109), plus the update rule (not in the
+ * reference, whose only solver is DCFR):
+ *   KR_RULE_DCFR  the reference's dcfrSolve (solver.hpp:343-404);
+ *   KR_RULE_CFRP  each player's regrets discounted right after its sweep and
+ *                 its strategy regret-matched on them; with alpha = +inf and
+ *                 beta = -inf that is CFR+ (R <- max(R + r, 0)), gamma = 1
+ *                 gives its linear averaging;
+ *   KR_RULE_PRMP  predictive regret matching+: as CFRP, strategy matched on
+ *                 R + r (the last instantaneous regret as the prediction).
+ * alpha / beta = +-inf use the limits 1 / 0 of t^e / (t^e + 1). */
+#define KR_RULE_DCFR 0
+#define KR_RULE_CFRP 1
+#define KR_RULE_PRMP 2
 typedef struct {
   double alpha, beta, gamma;
   int32_t max_iters;
   double target_exploitability;
   int32_t checkpoint_every;
+  int32_t rule; /* KR_RULE_* (0 = the reference's DCFR) */
 } kr_dcfr_params;
 
 /* Caller-owned result buffers (DcfrResult, solver.hpp:133-140).  trace_* hold
@@ -225,6 +238,10 @@ int64_t kr_solver_launches(const kr_solver* s);
  * per board (389-392, 325-331); averages: the normalised average strategies
  * (400-401). */
 int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma);
+/* Update rule (KR_RULE_*) of the following begin / iterate calls; rules other
+ * than DCFR need a treeplex whose parent sequences belong to earlier nodes
+ * (every reference skeleton), else KR_INVALID_INPUT. */
+int kr_solver_set_rule(kr_solver* s, int rule);
 int kr_solver_iterate(kr_solver* s, int n);
 int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2);
 int kr_solver_averages(kr_solver* s, double* avg1, double* avg2);

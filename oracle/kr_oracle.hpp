@@ -1239,7 +1239,23 @@ struct DcfrParams {
     double targetExploitability = 0.0;
     int checkpointEvery = 50;
     int threads = 1;
+    // Update rule (NOT in the reference, whose only solver is DCFR; SPEC.md:438
+    // lists CFR+ as a non-goal).  0 = DCFR as solver.hpp:343-404.  1 = CFR+
+    // style: each player's regrets are discounted right after its sweep and
+    // its strategy is regret-matched on the discounted regrets (with alpha =
+    // +inf, beta = -inf: R <- max(R + r, 0), i.e. regret matching+).  2 = PRM+
+    // (predictive): as 1, but the strategy is regret-matched on R + r, the
+    // last instantaneous regret serving as the prediction.
+    int rule = 0;
 };
+
+// t^e / (t^e + 1) (solver.hpp:378-379), extended to e = +-inf by its limit
+// (1 for +inf, 0 for -inf) where std::pow would give inf / inf.
+inline double discountFactor(int t, double e) {
+    if (std::isinf(e)) return e > 0 ? 1.0 : 0.0;
+    double te = std::pow(double(t), e);
+    return te / (te + 1);
+}
 struct TracePoint {
     int iteration = 0;
     double seconds = 0, exploitability = 0, br1 = 0, br2 = 0;
@@ -1293,8 +1309,9 @@ inline void regretMatch(const double* regrets, const std::vector<SkAction>& acts
     for (size_t a = 0; a < count; ++a) probs[a] = regrets[off + acts[a].seq - 1] >= best - tol ? 1.0 / ties : 0.0;
 }
 
-// solver.hpp:197-218
-inline Vec sequenceForm(const Skeleton& sk, const RegretTable& rt) {
+// solver.hpp:197-218, regret-matching `regrets` (the table's own by default)
+inline Vec sequenceForm(const Skeleton& sk, const RegretTable& rt, const Vec* regrets = nullptr) {
+    const Vec& R = regrets ? *regrets : rt.regret;
     Vec x(size_t(rt.handCount) * rt.n, 0.0);
     const auto& nodes = sk.playerNodes[rt.player];
     std::vector<double> reach(size_t(rt.n) + 1), probs;
@@ -1305,7 +1322,7 @@ inline Vec sequenceForm(const Skeleton& sk, const RegretTable& rt) {
             const SkNode& v = sk.nodes[idx];
             double mass = reach[v.parentSeq(rt.player)];
             probs.resize(v.actions.size());
-            regretMatch(rt.regret.data(), v.actions, off, probs.data());
+            regretMatch(R.data(), v.actions, off, probs.data());
             for (size_t a = 0; a < v.actions.size(); ++a) {
                 double m = mass * probs[a];
                 reach[v.actions[a].seq] = m;
@@ -1318,8 +1335,9 @@ inline Vec sequenceForm(const Skeleton& sk, const RegretTable& rt) {
 
 // solver.hpp:222-260 (single-threaded: the reference's partition is bitwise
 // neutral, test_solver.cpp:255-269)
-inline void cfrSweep(const Skeleton& sk, RegretTable& rt, const Vec& g) {
+inline void cfrSweep(const Skeleton& sk, RegretTable& rt, const Vec& g, Vec* inst = nullptr) {
     const auto& nodes = sk.playerNodes[rt.player];
+    if (inst) inst->assign(rt.regret.size(), 0.0);
     std::vector<double> seqVal(size_t(rt.n) + 1), probs;
     for (int h = 0; h < rt.handCount; ++h) {
         int off = h * rt.n;
@@ -1335,7 +1353,11 @@ inline void cfrSweep(const Skeleton& sk, RegretTable& rt, const Vec& g) {
                 seqVal[seq] = ev;
                 nodeVal += probs[a] * ev;
             }
-            for (const auto& act : v.actions) rt.regret[off + act.seq - 1] += seqVal[act.seq] - nodeVal;
+            for (const auto& act : v.actions) {
+                const double d = seqVal[act.seq] - nodeVal;
+                rt.regret[off + act.seq - 1] += d;
+                if (inst) (*inst)[off + act.seq - 1] = d;
+            }
             seqVal[v.parentSeq(rt.player)] += nodeVal;
         }
     }
@@ -1419,6 +1441,22 @@ inline Vec uniformStrategy(const KronPayoff& kp, int player) {
     return sequenceForm(kp.skeleton, rt);
 }
 
+// One player's half-iteration: sweep, then (rules 1, 2) the discount of its
+// own regrets, then its new strategy.  Rule 0 leaves the discount to the end
+// of the iteration, as solver.hpp:378-380 does.
+inline Vec playerUpdate(const Skeleton& sk, RegretTable& rt, const Vec& g, int rule, double pos, double neg) {
+    if (rule == 0) {
+        cfrSweep(sk, rt, g);
+        return sequenceForm(sk, rt);
+    }
+    Vec r;
+    cfrSweep(sk, rt, g, rule == 2 ? &r : nullptr);
+    discount(rt, pos, neg);
+    if (rule == 1) return sequenceForm(sk, rt);
+    for (size_t e = 0; e < r.size(); ++e) r[e] = rt.regret[e] + r[e];  // prediction: R + last regret
+    return sequenceForm(sk, rt, &r);
+}
+
 // solver.hpp:343-404
 inline DcfrResult dcfrSolve(const KronPayoff& kp, const GradientEngine& eng, const DcfrParams& params) {
     if (params.maxIters < 1) throw InvalidInputError("iteration budget must be positive");
@@ -1432,17 +1470,16 @@ inline DcfrResult dcfrSolve(const KronPayoff& kp, const GradientEngine& eng, con
     int64_t flops0 = eng.flops();
     Vec x1 = sequenceForm(sk, rt1), x2 = sequenceForm(sk, rt2);
     for (int t = 1; t <= params.maxIters; ++t) {
+        double pos = discountFactor(t, params.alpha), neg = discountFactor(t, params.beta);
         Vec g1 = eng.Ax(x2);
-        cfrSweep(sk, rt1, g1);
-        x1 = sequenceForm(sk, rt1);
+        x1 = playerUpdate(sk, rt1, g1, params.rule, pos, neg);
         Vec g2 = eng.ATx(x1);
         for (double& v : g2) v = -v;
-        cfrSweep(sk, rt2, g2);
-        x2 = sequenceForm(sk, rt2);
-        double ta = std::pow(double(t), params.alpha), tb = std::pow(double(t), params.beta);
-        double pos = ta / (ta + 1), neg = tb / (tb + 1);
-        discount(rt1, pos, neg);
-        discount(rt2, pos, neg);
+        x2 = playerUpdate(sk, rt2, g2, params.rule, pos, neg);
+        if (params.rule == 0) {
+            discount(rt1, pos, neg);
+            discount(rt2, pos, neg);
+        }
         double shrink = std::pow(double(t) / (t + 1), params.gamma);
         for (size_t e = 0; e < x1.size(); ++e) rt1.avg[e] += x1[e];
         for (size_t e = 0; e < x2.size(); ++e) rt2.avg[e] += x2[e];
@@ -1496,17 +1533,16 @@ struct DcfrState {
         const Skeleton& sk = kp->skeleton;
         for (int q = 0; q < n; ++q) {
             const int tt = ++t;
+            double pos = discountFactor(tt, p.alpha), neg = discountFactor(tt, p.beta);
             Vec g1 = eng->Ax(x2);
-            cfrSweep(sk, rt1, g1);
-            x1 = sequenceForm(sk, rt1);
+            x1 = playerUpdate(sk, rt1, g1, p.rule, pos, neg);
             Vec g2 = eng->ATx(x1);
             for (double& v : g2) v = -v;
-            cfrSweep(sk, rt2, g2);
-            x2 = sequenceForm(sk, rt2);
-            double ta = std::pow(double(tt), p.alpha), tb = std::pow(double(tt), p.beta);
-            double pos = ta / (ta + 1), neg = tb / (tb + 1);
-            discount(rt1, pos, neg);
-            discount(rt2, pos, neg);
+            x2 = playerUpdate(sk, rt2, g2, p.rule, pos, neg);
+            if (p.rule == 0) {
+                discount(rt1, pos, neg);
+                discount(rt2, pos, neg);
+            }
             double shrink = std::pow(double(tt) / (tt + 1), p.gamma);
             for (size_t e = 0; e < x1.size(); ++e) rt1.avg[e] += x1[e];
             for (size_t e = 0; e < x2.size(); ++e) rt2.avg[e] += x2[e];

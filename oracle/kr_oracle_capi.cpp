@@ -378,9 +378,10 @@ int or_dcfr_state_create(void* h, void* sp, void** out) {
     });
 }
 void or_dcfr_state_free(void* s) { delete static_cast<DcfrHandle*>(s); }
-int or_dcfr_begin(void* s, double alpha, double beta, double gamma) {
+int or_dcfr_begin(void* s, double alpha, double beta, double gamma, int rule) {
     return guarded([&] {
         DcfrParams p;
+        p.rule = rule;
         p.alpha = alpha;
         p.beta = beta;
         p.gamma = gamma;
@@ -399,10 +400,11 @@ int or_dcfr_checkpoint(void* s, double* br1, double* br2) {
 int or_dcfr(void* h, void* sp, int engineKind, double alpha, double beta, double gamma, int maxIters,
             double target, int checkpointEvery, int* iterations, double* expl, int64_t* flops, int* traceIter,
             double* traceExpl, double* traceBr1, double* traceBr2, int traceCap, int* ntrace, double* avg1,
-            double* avg2, double* seconds) {
+            double* avg2, double* seconds, int rule) {
     return guarded([&] {
         const auto& kp = static_cast<Inst*>(h)->kp;
         DcfrParams p;
+        p.rule = rule;
         p.alpha = alpha;
         p.beta = beta;
         p.gamma = gamma;

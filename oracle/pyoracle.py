@@ -324,9 +324,9 @@ class DcfrBoards:
                 _LIB.or_dcfr_state_free(h)
             self.hs = []
 
-    def begin(self, alpha=1.5, beta=0.0, gamma=2.0):
+    def begin(self, alpha=1.5, beta=0.0, gamma=2.0, rule=0):
         for h in self.hs:
-            _check(lib().or_dcfr_begin(h, C.c_double(alpha), C.c_double(beta), C.c_double(gamma)))
+            _check(lib().or_dcfr_begin(h, C.c_double(alpha), C.c_double(beta), C.c_double(gamma), int(rule)))
 
     def iterate(self, n):
         for h in self.hs:
@@ -342,7 +342,7 @@ class DcfrBoards:
 
 
 def dcfr(inst, sp=None, engine="factored", alpha=1.5, beta=0.0, gamma=2.0, max_iters=1000, target=0.0,
-         checkpoint_every=50):
+         checkpoint_every=50, rule=0):
     """dcfrSolve (solver.hpp:343-404).  Returns a dict with the trace."""
     kind = {"factored": 0, "reference": 1, "dense": 2}[engine]
     cap = max_iters // checkpoint_every + 2
@@ -354,7 +354,7 @@ def dcfr(inst, sp=None, engine="factored", alpha=1.5, beta=0.0, gamma=2.0, max_i
                          C.c_double(gamma), max_iters, C.c_double(target), checkpoint_every, C.byref(it),
                          C.byref(ex), C.byref(fl), ti.ctypes.data_as(C.c_void_p), te.ctypes.data_as(C.c_void_p),
                          tb1.ctypes.data_as(C.c_void_p), tb2.ctypes.data_as(C.c_void_p), cap, C.byref(nt),
-                         a1.ctypes.data_as(C.c_void_p), a2.ctypes.data_as(C.c_void_p), C.byref(sec)))
+                         a1.ctypes.data_as(C.c_void_p), a2.ctypes.data_as(C.c_void_p), C.byref(sec), int(rule)))
     n = min(nt.value, cap)
     return {"iterations": it.value, "exploitability": ex.value, "gradient_flops": fl.value,
             "trace_iter": ti[:n], "trace_expl": te[:n], "trace_br1": tb1[:n], "trace_br2": tb2[:n],

@@ -79,7 +79,7 @@ class kr_treeplex(C.Structure):
 
 class kr_dcfr_params(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("max_iters", C.c_int32),
-                ("target_exploitability", C.c_double), ("checkpoint_every", C.c_int32)]
+                ("target_exploitability", C.c_double), ("checkpoint_every", C.c_int32), ("rule", C.c_int32)]
 
 
 class kr_dcfr_result(C.Structure):
@@ -98,6 +98,7 @@ CUDA_SYMBOLS = [
     "kr_device_count", "kr_solver_create", "kr_solver_destroy", "kr_solver_run", "kr_solver_best_response",
     "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
     "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times", "kr_engine_create_kron",
+    "kr_solver_set_rule",
 ]
 
 
@@ -147,6 +148,7 @@ def cuda():
             L.kr_solver_launches.restype = C.c_int64
             L.kr_solver_launches.argtypes = [C.c_void_p]
             L.kr_solver_begin.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
+            L.kr_solver_set_rule.argtypes = [C.c_void_p, C.c_int]
             L.kr_solver_iterate.argtypes = [C.c_void_p, C.c_int]
             L.kr_solver_checkpoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
             L.kr_solver_averages.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]

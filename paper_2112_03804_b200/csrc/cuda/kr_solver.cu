@@ -41,6 +41,7 @@ struct kr_solver {
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
     int team = 4;                // lanes per hand in k_player_team (2, 4 or 8)
+    int rule = 0;                // KR_RULE_*
     int64_t* d_bstart[2] = {nullptr, nullptr};
     double* regret[2] = {nullptr, nullptr};
     double* avg[2] = {nullptr, nullptr};
@@ -270,7 +271,8 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                                                      int na, int tlen, int64_t H, int hpb,
                                                      const double* __restrict__ g, int negate,
                                                      double* __restrict__ regret, double* __restrict__ xout,
-                                                     double* __restrict__ avg, double pos, double neg, double shrink) {
+                                                     double* __restrict__ avg, double pos, double neg, double shrink,
+                                                     int rule) {
     extern __shared__ double sm[];
     const int stride = hpb + 1;
     double* Rg = sm;                      // n x stride      regrets
@@ -352,13 +354,33 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                     }
                     for (int a = 0; a < cnt; ++a) {
                         const int sq = seqs[a];
-                        R[(sq - 1) * stride] += Vt[sq * stride] - nodeVal;
+                        const double d = Vt[sq * stride] - nodeVal;  // instantaneous regret
+                        R[(sq - 1) * stride] += d;
+                        if (rule == 2) Vt[sq * stride] = d;
                     }
                     Nt[v * stride] = nodeVal;
-                    const RmStats st2 = rm_stats(R, stride, seqs, cnt);
-                    for (int a = 0; a < cnt; ++a) {
-                        const int sq = seqs[a];
-                        Vt[sq * stride] = rm_prob(st2, R[(sq - 1) * stride]);
+                    if (rule != 0)  // CFR+ / PRM+: discount before the strategy
+                        for (int a = 0; a < cnt; ++a) {
+                            double* rp = R + (seqs[a] - 1) * stride;
+                            const double r = *rp;
+                            *rp = r * (r > 0 ? pos : neg);
+                        }
+                    if (rule == 2) {  // PRM+: match R + d
+                        for (int a = 0; a < cnt; ++a) {
+                            const int sq = seqs[a];
+                            Vt[sq * stride] = R[(sq - 1) * stride] + Vt[sq * stride];
+                        }
+                        const RmStats st2 = rm_stats(Vt + stride, stride, seqs, cnt);
+                        for (int a = 0; a < cnt; ++a) {
+                            const int sq = seqs[a];
+                            Vt[sq * stride] = rm_prob(st2, Vt[sq * stride]);
+                        }
+                    } else {
+                        const RmStats st2 = rm_stats(R, stride, seqs, cnt);
+                        for (int a = 0; a < cnt; ++a) {
+                            const int sq = seqs[a];
+                            Vt[sq * stride] = rm_prob(st2, R[(sq - 1) * stride]);
+                        }
                     }
                 }
             __syncwarp();
@@ -374,7 +396,7 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                 }
             __syncwarp();
         }
-        if (valid)  // discount (solver.hpp:262-264)
+        if (valid && rule == 0)  // discount (solver.hpp:262-264)
             for (int q = lane; q < n; q += kTeam) {
                 const double r = R[q * stride];
                 R[q * stride] = r * (r > 0 ? pos : neg);
@@ -576,6 +598,14 @@ void append_levels(const kr_treeplex& t, std::vector<int32_t>& buf, bool& ok, in
     buf.insert(buf.end(), seqPar.begin(), seqPar.end());
 }
 
+// t^e / (t^e + 1) as the reference computes it (solver.hpp:378-379), with the
+// limits 1 / 0 for e = +-inf (where std::pow would give inf / inf).
+double discount_factor(int t, double e) {
+    if (std::isinf(e)) return e > 0 ? 1.0 : 0.0;
+    const double te = std::pow(double(t), e);
+    return te / (te + 1);
+}
+
 size_t step_smem(int n, int nt, int nn, int na) {
     return size_t(2 * n + 1) * size_t(nt + 1) * 8 + size_t(2 * nn + 1 + na) * 4 + 16;
 }
@@ -590,11 +620,12 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
         kern<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
-                                      hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink);
+                                      hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule);
         KR_CK_LAUNCH();
         s->launches++;
         return;
     }
+    if (s->rule != 0) throw Fail{KR_INVALID_INPUT, "update rule needs a reference-ordered treeplex"};
     const int nt = s->nt[p];
     const unsigned grid = unsigned((s->H[p] + nt - 1) / nt);
     if (grid == 0) return;
@@ -786,6 +817,16 @@ void normalise_averages(kr_solver* s, cudaStream_t st) {
 }
 }  // namespace
 
+int kr_solver_set_rule(kr_solver* s, int rule) {
+    return guarded([&] {
+        if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
+        if (rule < 0 || rule > 2) throw Fail{KR_INVALID_INPUT, "unknown update rule"};
+        if (rule != 0 && !(s->levelled[0] && s->levelled[1]))
+            throw Fail{KR_INVALID_INPUT, "update rule needs a reference-ordered treeplex"};
+        s->rule = rule;
+    });
+}
+
 int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma) {
     return guarded([&] {
         if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
@@ -817,8 +858,7 @@ int kr_solver_iterate(kr_solver* s, int n) {
         cudaStream_t st = e->stream;
         for (int q = 0; q < n; ++q) {
             const int t = ++s->t;  // solver.hpp:365-388
-            const double ta = std::pow(double(t), s->alpha), tb = std::pow(double(t), s->beta);
-            const double pos = ta / (ta + 1), neg = tb / (tb + 1);
+            const double pos = krb::discount_factor(t, s->alpha), neg = krb::discount_factor(t, s->beta);
             const double shrink = std::pow(double(t) / (t + 1), s->gamma);
             krb::engine_ax(e, s->x[1], s->g, st);                      // g1 = A x2
             krb::launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st);  // P1 sweep/seqform/discount/avg
@@ -881,6 +921,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
                 throw Fail{rc, kr_last_error(&code)};
             }
         };
+        ck(kr_solver_set_rule(s, prm->rule));
         ck(kr_solver_begin(s, prm->alpha, prm->beta, prm->gamma));
         r->trace_len = 0;
         std::vector<double> b1(size_t(s->nboards)), b2(size_t(s->nboards));

@@ -65,14 +65,14 @@ class DistributedDcfr:
         self.local, self.nboards, self.pot = local, nboards, pot
         self.rank, self.world, self.group, self.device = rank, world, group, device
 
-    def run(self, alpha=1.5, beta=0.0, gamma=2.0, max_iters=1000, target=0.0, checkpoint_every=50):
+    def run(self, alpha=1.5, beta=0.0, gamma=2.0, max_iters=1000, target=0.0, checkpoint_every=50, rule=0):
         if max_iters < 1 or checkpoint_every < 1:
             raise ValueError("iteration budget and checkpoint period must be positive")
-        try:
-            self.local.begin(alpha, beta, gamma)
-        except TypeError:  # CudaSolver.begin takes DcfrParams
-            from .solver import DcfrParams
-            self.local.begin(DcfrParams(alpha=alpha, beta=beta, gamma=gamma))
+        from .solver import CudaSolver, DcfrParams
+        if isinstance(self.local, CudaSolver):
+            self.local.begin(DcfrParams(alpha=alpha, beta=beta, gamma=gamma, rule=rule))
+        else:  # the oracle's DcfrBoards (CPU tests)
+            self.local.begin(alpha, beta, gamma, rule)
         t = 0
         trace = {"iter": [], "expl": [], "br1": [], "br2": []}
         while t < max_iters:

@@ -8,6 +8,7 @@ products the whole trace is bitwise equal to the reference's.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -43,15 +44,31 @@ class Treeplex:
         return N.kr_treeplex(self.n_seq, len(self.parent), *(N.ptr(a) for a in arrs))
 
 
+RULE_DCFR, RULE_CFRP, RULE_PRMP = 0, 1, 2
+
+
 @dataclass
 class DcfrParams:
-    """DcfrParams (solver.hpp:101-109)."""
+    """DcfrParams (solver.hpp:101-109) plus the update rule (kr_engine.h
+    KR_RULE_*): 0 is the reference's DCFR; CFR+ and PRM+ are presets beyond
+    the reference (its SPEC.md:438 lists CFR+ as a non-goal)."""
     alpha: float = 1.5
     beta: float = 0.0
     gamma: float = 2.0
     max_iters: int = 1000
     target_exploitability: float = 0.0
     checkpoint_every: int = 50
+    rule: int = RULE_DCFR
+
+    @classmethod
+    def cfr_plus(cls, **kw):
+        """CFR+: regret matching+ (R <- max(R + r, 0)), linear averaging."""
+        return cls(alpha=math.inf, beta=-math.inf, gamma=1.0, rule=RULE_CFRP, **kw)
+
+    @classmethod
+    def prm_plus(cls, **kw):
+        """Predictive regret matching+ (strategy from R + last regret), linear averaging."""
+        return cls(alpha=math.inf, beta=-math.inf, gamma=1.0, rule=RULE_PRMP, **kw)
 
 
 @dataclass
@@ -112,7 +129,8 @@ class CudaSolver:
         bb1, bb2 = np.zeros(cap * self.nboards), np.zeros(cap * self.nboards)
         a1 = np.zeros(self.rows) if want_avg else None
         a2 = np.zeros(self.cols) if want_avg else None
-        prm = N.kr_dcfr_params(p.alpha, p.beta, p.gamma, p.max_iters, p.target_exploitability, p.checkpoint_every)
+        prm = N.kr_dcfr_params(p.alpha, p.beta, p.gamma, p.max_iters, p.target_exploitability, p.checkpoint_every,
+                               p.rule)
         res = N.kr_dcfr_result(0, 0.0, 0, 0, cap, N.ptr(ti), N.ptr(te), N.ptr(b1), N.ptr(b2), N.ptr(bb1),
                                N.ptr(bb2), N.ptr(a1), N.ptr(a2), 0.0)
         launches0 = self.launches() + self.engine.launches()
@@ -126,6 +144,7 @@ class CudaSolver:
     # -- incremental interface (multi-rank drivers, dist.py) ----------------
     def begin(self, params: DcfrParams = None):
         p = params or DcfrParams()
+        N.check(N.cuda().kr_solver_set_rule(self._h, p.rule))
         N.check(N.cuda().kr_solver_begin(self._h, p.alpha, p.beta, p.gamma))
 
     def iterate(self, n):

@@ -68,7 +68,9 @@ def test_single_board_matches_reference_formula():
 
 
 @pytest.mark.parametrize("kw", [dict(max_iters=40, checkpoint_every=10),
-                                dict(max_iters=2000, checkpoint_every=5, target=0.02)])
+                                dict(max_iters=2000, checkpoint_every=5, target=0.02),
+                                dict(max_iters=40, checkpoint_every=10, alpha=float("inf"), beta=float("-inf"),
+                                     gamma=1.0, rule=1)])
 def test_two_ranks_match_one(kw):
     import pyoracle as po
     single = DistributedDcfr(po.DcfrBoards(boards(range(NBOARDS))), NBOARDS, POT).run(**kw)

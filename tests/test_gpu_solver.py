@@ -130,3 +130,29 @@ def test_solver_rejects_bad_parameters():
         s.run(DcfrParams(max_iters=0))
     with pytest.raises(InvalidInputError):
         s.run(DcfrParams(max_iters=10, checkpoint_every=0))
+
+
+@pytest.mark.parametrize("preset", ["cfr_plus", "prm_plus"])
+@pytest.mark.parametrize("name,kw,iters", [("twenty_card", {}, 400), ("golden", {}, 300), ("bluffing", {}, 300),
+                                           ("random_small", dict(seed=2), 200)])
+def test_rule_presets_bitwise(preset, name, kw, iters):
+    """CFR+ and PRM+ (beyond the reference: its only solver is DCFR) against
+    the oracle's restatement of the same rules, gap trajectory per iteration."""
+    p, o = both(name, **kw)
+    prm = getattr(DcfrParams, preset)(max_iters=iters, checkpoint_every=1)
+    r = dcfr_solve(p, p.sparsify("b", True), prm)
+    ro = po.dcfr(o, o.sparsify("b", True), alpha=prm.alpha, beta=prm.beta, gamma=prm.gamma, max_iters=iters,
+                 checkpoint_every=1, rule=prm.rule)
+    assert bits_equal(r.trace_br1, ro["trace_br1"]) and bits_equal(r.trace_br2, ro["trace_br2"])
+    assert bits_equal(r.avg1, ro["avg1"]) and bits_equal(r.avg2, ro["avg2"])
+    assert r.trace_expl[-1] <= r.trace_expl[0]
+
+
+def test_cfr_plus_config1_1000_iterations():
+    """BASELINE.json config 1's "1000 CFR+ iterations" on the parity game
+    (twenty_card plays the Leduc role): completes and converges."""
+    p = H.builtin("twenty_card")
+    r = dcfr_solve(p, p.sparsify("b", True), DcfrParams.cfr_plus(max_iters=1000, checkpoint_every=100))
+    assert r.iterations == 1000
+    assert r.exploitability < 1e-3
+    assert r.trace_expl[-1] < 0.2 * r.trace_expl[0]
