@@ -64,6 +64,10 @@ public:
     CudaEngine(const std::vector<kr_factors>& boards, int device = 0) {
         check(kr_engine_create_boards(boards.data(), int(boards.size()), device, 0, &e_));
     }
+    // The implicit Kronecker engine over KronPayoff pieces (kr_engine_create_kron).
+    explicit CudaEngine(const std::vector<kr_kron_board>& boards, int device = 0) {
+        check(kr_engine_create_kron(boards.data(), int(boards.size()), device, 0, &e_));
+    }
     ~CudaEngine() override {
         if (e_) kr_engine_destroy(e_);
     }

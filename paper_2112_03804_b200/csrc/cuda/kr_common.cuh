@@ -57,6 +57,7 @@ constexpr int kSigma = 1024;
 constexpr int kLongRow = 256;
 struct DevSell {
     int64_t nrows = 0, nslices = 0, nnz = 0, padded = 0;
+    int32_t maxLen = 0;            // longest row kept in the slices
     int64_t* slice_ptr = nullptr;  // nslices + 1
     int32_t* lane_row = nullptr;   // nslices * 32; -1 = unused lane
     int32_t* lane_len = nullptr;   // nslices * 32

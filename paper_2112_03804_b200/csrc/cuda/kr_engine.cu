@@ -77,8 +77,12 @@ __device__ __forceinline__ double gather(const double* __restrict__ xa, const do
 // remaining blocks run four SELL slices each, one per warp, with a two-stage
 // register pipeline (loads of stage g+1 in flight while stage g gathers and
 // accumulates).
-template <bool TWO>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+// KU / MINB: entries per lane per pipeline stage and minimum resident
+// blocks; matrices whose SELL rows hold at most one entry (U^T of Technique
+// B: one entry per k position) use <1, 8>, a lean variant with twice
+// the resident warps, since their cost is the per-row load latency.
+template <bool TWO, int KU = kU, int MINB = 1>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
     k_spmv(SellView A, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
            double* __restrict__ y) {
     __shared__ double P[kWarpsPerBlock][kChunk];
@@ -149,38 +153,54 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     const int32_t len = A.lane_len[s * 32 + lane];
     const int32_t row = A.lane_row[s * 32 + lane];
     double acc = 0.0;
-    int32_t c[kU];
-    double v[kU];
+    int32_t c[KU];
+    double v[KU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
+    for (int u = 0; u < KU; ++u)
         if (u < len) {
             c[u] = __ldcs(A.col + base + int64_t(u) * 32);
             v[u] = __ldcs(A.val + base + int64_t(u) * 32);
         }
-    for (int32_t j = 0; j < len; j += kU) {
-        int32_t cn[kU];
-        double vn[kU], x[kU];
+    for (int32_t j = 0; j < len; j += KU) {
+        int32_t cn[KU];
+        double vn[KU], x[KU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int32_t jj = j + kU + u;
+        for (int u = 0; u < KU; ++u) {
+            const int32_t jj = j + KU + u;
             if (jj < len) {
                 cn[u] = __ldcs(A.col + base + int64_t(jj) * 32);
                 vn[u] = __ldcs(A.val + base + int64_t(jj) * 32);
             }
         }
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
+        for (int u = 0; u < KU; ++u)
             if (j + u < len) x[u] = gather<TWO>(xa, xb, split, c[u]);
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
+        for (int u = 0; u < KU; ++u)
             if (j + u < len) acc += v[u] * x[u];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
+        for (int u = 0; u < KU; ++u) {
             c[u] = cn[u];
             v[u] = vn[u];
         }
     }
     if (row >= 0) y[row] = acc;
+}
+
+// x'[s*M2 + J] = x[J*n2 + s], tiled: a block stages the rows of 32 hands
+// (32 * n2 contiguous doubles) in shared memory and writes each sequence's 32
+// consecutive hands as one 256-byte segment.
+__global__ void __launch_bounds__(256) k_seq_major_tile(const double* __restrict__ x, int64_t M2, int32_t n2,
+                                                        double* __restrict__ xp, int64_t J0, int64_t J1) {
+    extern __shared__ double tile[];
+    const int64_t j0 = J0 + int64_t(blockIdx.x) * 32;
+    const int cnt = int(lmin(32, J1 - j0));
+    const double* src = x + j0 * n2;
+    for (int q = threadIdx.x; q < cnt * n2; q += blockDim.x) tile[q] = __ldcs(src + q);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    if (lane >= cnt) return;
+    for (int s = threadIdx.x >> 5; s < n2; s += blockDim.x >> 5) xp[int64_t(s) * M2 + j0 + lane] = tile[lane * n2 + s];
 }
 
 // x'[s*M2 + J] = x[J*n2 + s]: the sequence-major copy V^T x gathers from.
@@ -729,6 +749,7 @@ struct BoardPlan {
     // SELL sizes and offsets in the combined arrays
     int64_t sl[4] = {0, 0, 0, 0}, pad[4] = {0, 0, 0, 0}, slOff[4] = {0, 0, 0, 0}, padOff[4] = {0, 0, 0, 0};
     int64_t nl[4] = {0, 0, 0, 0}, nlz[4] = {0, 0, 0, 0}, nlOff[4] = {0, 0, 0, 0}, nlzOff[4] = {0, 0, 0, 0};
+    int32_t maxLen[4] = {0, 0, 0, 0};  // longest slice row per matrix
 };
 
 void build_chain_order(BoardPlan& p, bool chainMode) {
@@ -1082,6 +1103,9 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
                     int64_t(hs.lgrow.size()) != p.nl[w] || int64_t(hs.lcol.size()) != p.nlz[w])
                     throw Fail{KR_CUDA, "internal: SELL sizing mismatch"};
                 upload_sell(hs, p.slOff[w], p.padOff[w], p.nlOff[w], p.nlzOff[w], *mats[w], s);
+                int32_t ml = 0;
+                for (int32_t l : hs.llen) ml = std::max(ml, l);
+                plan[size_t(b)].maxLen[w] = ml;
             }
             cudaStreamDestroy(s);
         });
@@ -1174,6 +1198,8 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
                 KR_CK(cudaMemcpy(e->mc_val, cval.data(), 8 * size_t(no), cudaMemcpyHostToDevice));
             }
         }
+        for (int w = 0; w < 4; ++w)
+            for (auto& p : plan) mats[w]->maxLen = std::max(mats[w]->maxLen, p.maxLen[w]);
         for (int w = 0; w < 4; ++w) {
             e->bSl[w].clear();
             e->bNl[w].clear();
@@ -1258,6 +1284,8 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
         KR_CK(cudaEventRecord(pend.a, s));
     }
     if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
+    else if (A.maxLen <= 1 && !std::getenv("KR_NO_LEAN"))
+        k_spmv<false, 1, 8><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
     if (timed) {
@@ -1347,6 +1375,14 @@ namespace {
 // writing the output).  Pointers address the whole vectors.
 void seq_major(kr_engine* e, const double* x, int64_t c0, int64_t c1, cudaStream_t s) {
     if (c1 <= c0) return;
+    const size_t smem = size_t(32) * size_t(e->n2) * sizeof(double);
+    if (smem <= 48 * 1024 && c0 % e->n2 == 0 && c1 % e->n2 == 0) {
+        const int64_t J0 = c0 / e->n2, J1 = c1 / e->n2;
+        k_seq_major_tile<<<unsigned((J1 - J0 + 31) / 32), 256, smem, s>>>(x, e->M2, e->n2, e->d_xp, J0, J1);
+        KR_CK_LAUNCH();
+        e->launches++;
+        return;
+    }
     k_seq_major<<<unsigned((c1 - c0 + 255) / 256), 256, 0, s>>>(x, e->M2, e->n2, e->d_xp, c0, c1);
     KR_CK_LAUNCH();
     e->launches++;

@@ -58,3 +58,25 @@ def test_solve_reproduces_the_readme_line(twenty_card):
     r2 = run("solve", "--instance", inst, "--technique", "b", "--iters", "600", "--out", str(d / "run2"))
     assert r2.stdout.split()[1:4] == r.stdout.split()[1:4]
     assert (d / "run" / "trace.csv").read_text() == (d / "run2" / "trace.csv").read_text()
+
+
+def test_bad_engine_or_rule_exit_two(twenty_card):
+    d, inst = twenty_card
+    r = run("solve", "--instance", inst, "--engine", "dense", "--iters", "5", "--out", str(d / "bad"))
+    assert r.returncode == 2 and "INVALID_INPUT" in r.stderr
+    r = run("solve", "--instance", inst, "--rule", "mccfr", "--iters", "5", "--out", str(d / "bad"))
+    assert r.returncode == 2 and "INVALID_INPUT" in r.stderr
+
+
+@pytest.mark.gpu
+def test_solve_implicit_engine_and_cfr_plus(twenty_card):
+    """--engine implicit reproduces the README solve to the printed 12 digits
+    within 1e-7 relative; --rule cfr+ runs BASELINE config 1's 1000 CFR+ iterations."""
+    d, inst = twenty_card
+    r = run("solve", "--instance", inst, "--engine", "implicit", "--iters", "600", "--out", str(d / "imp"))
+    assert r.returncode == 0, r.stderr
+    expl = float(r.stdout.split("exploitability=")[1].split()[0])
+    assert abs(expl - 0.000189332132512) <= 1e-7 * 0.000189332132512
+    r = run("solve", "--instance", inst, "--rule", "cfr+", "--iters", "1000", "--out", str(d / "cfrp"))
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith("solve: iterations=1000 ") and "rule=cfr+" in r.stdout

@@ -5,10 +5,17 @@
 //   krb200 sparsify --instance F [--technique a|b] [--out DIR]
 //   krb200 solve    --instance F [--bundle DIR] [--technique a|b] [--iters N]
 //                   [--target-expl X] [--checkpoint-every N] [--out DIR]
+//                   [--engine factored|implicit] [--rule dcfr|cfr+|prm+]
+//
+// --engine implicit applies the payoff without factors (kr_engine_create_kron);
+// --rule selects the update rule (dcfr is the reference's; cfr+ and prm+ are
+// presets with alpha = +inf, beta = -inf, gamma = 1).
 //
 // Errors print `error code=... msg="..."` and exit 2, as the reference does
 // (main.cpp:420-426).
 #include <chrono>
+#include <cmath>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
@@ -21,7 +28,7 @@
 namespace {
 
 struct Options {
-    std::string cmd, instance, bundle, technique = "b", out = "out";
+    std::string cmd, instance, bundle, technique = "b", out = "out", engine = "factored", rule = "dcfr";
     int iters = 1000, checkpointEvery = 50;
     double targetExpl = 0;
 };
@@ -86,7 +93,12 @@ int runSparsify(const Options& o) {
 int runSolve(const Options& o) {
     Instance inst(o.instance);
     Factors f;
-    if (!o.bundle.empty()) {
+    if (o.engine != "factored" && o.engine != "implicit")
+        throw krb200::Error("INVALID_INPUT", "--engine must be factored or implicit");
+    if (o.rule != "dcfr" && o.rule != "cfr+" && o.rule != "prm+")
+        throw krb200::Error("INVALID_INPUT", "--rule must be dcfr, cfr+ or prm+");
+    if (o.engine == "implicit") {
+    } else if (!o.bundle.empty()) {
         hcheck(krh_bundle_read(o.bundle.c_str(), &f.h));
         int64_t d[9];
         f.dims(d);
@@ -95,10 +107,24 @@ int runSolve(const Options& o) {
     } else {
         hcheck(krh_sparsify(inst.h, o.technique == "a" ? 0 : 1, 1, 1000, &f.h));
     }
-    krb200::CudaEngine eng(f.view());
+    std::unique_ptr<krb200::CudaEngine> engp;
+    if (o.engine == "implicit") {
+        kr_kron_board kb;
+        hcheck(krh_instance_kron_view(inst.h, &kb));
+        engp = std::make_unique<krb200::CudaEngine>(std::vector<kr_kron_board>{kb});
+    } else {
+        engp = std::make_unique<krb200::CudaEngine>(f.view());
+    }
+    krb200::CudaEngine& eng = *engp;
     krb200::CudaSolver solver(eng, inst.treeplex(0), inst.treeplex(1), {int32_t(inst.d[0])}, {int32_t(inst.d[1])},
                               krh_instance_pot(inst.h));
     krb200::DcfrParams p;
+    if (o.rule != "dcfr") {
+        p.alpha = HUGE_VAL;
+        p.beta = -HUGE_VAL;
+        p.gamma = 1.0;
+        p.rule = o.rule == "cfr+" ? KR_RULE_CFRP : KR_RULE_PRMP;
+    }
     p.maxIters = o.iters;
     p.targetExploitability = o.targetExpl;
     p.checkpointEvery = o.checkpointEvery;
@@ -118,6 +144,8 @@ int runSolve(const Options& o) {
     }
     std::printf("solve: iterations=%d exploitability=%.12g gradient_flops=%lld trace=%s profile=%s\n", r.iterations,
                 r.exploitability, (long long)r.gradientFlops, trace.c_str(), profile.c_str());
+    if (o.engine != "factored" || o.rule != "dcfr")
+        std::printf("engine=%s rule=%s device_seconds=%.6f\n", o.engine.c_str(), o.rule.c_str(), r.deviceSeconds);
     return 0;
 }
 
@@ -139,6 +167,8 @@ int main(int argc, char** argv) {
         else if (k == "--iters") o.iters = std::atoi(v.c_str());
         else if (k == "--target-expl") o.targetExpl = std::atof(v.c_str());
         else if (k == "--checkpoint-every") o.checkpointEvery = std::atoi(v.c_str());
+        else if (k == "--engine") o.engine = v;
+        else if (k == "--rule") o.rule = v;
         else {
             std::fprintf(stderr, "unknown option %s\n", k.c_str());
             return 1;
