@@ -88,13 +88,14 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
-// Dynamic shared memory for a board of maxMS summing hands: wf, ws (m each),
-// the virtual prefix P (3 m + 1), the list-boundary prefixes of wf (56),
-// then the list hands (2 m int32) and list pointers (56 int32).  (Staging the
-// output table too, and looping over several sequences per CTA, was measured
-// slower: the larger footprint halves the resident CTAs per SM.)
+// Dynamic shared memory for a board of maxMS summing hands: (ws, wf) pairs
+// (2 m doubles), the virtual prefix P (3 m + 1), the list-boundary prefixes
+// of wf (56) and the per-card terms G, CF (2 x 56), then the list hands
+// (2 m int32) and list pointers (56 int32).  (Staging the output table too,
+// and looping over several sequences per CTA, was measured slower: the
+// larger footprint halves the resident CTAs per SM.)
 size_t fused_smem(int maxMS) {
-    return sizeof(double) * (5 * size_t(maxMS) + 1 + 56) + sizeof(int32_t) * (2 * size_t(maxMS) + 56);
+    return sizeof(double) * (5 * size_t(maxMS) + 1 + 3 * 56) + sizeof(int32_t) * (2 * size_t(maxMS) + 56);
 }
 
 // One CTA per (sequence a, board b); see the file header for the algebra.
@@ -105,7 +106,10 @@ size_t fused_smem(int maxMS) {
 // per-card prefix as a difference P[m + pos] − P[m + start(c)], so a single
 // block scan replaces 53 segmented ones.  The same scan carries wf, whose
 // prefix is only kept at the 53 list boundaries (QB): TF = QB[0] and the
-// per-card sums CF[c] = QB[c+1] − QB[c].
+// per-card sums CF[c] = QB[c+1] − QB[c].  With B_c / E_c the start / end of
+// card c's list in P, the W-weighted part of an output is
+//   lower − upper = (P[lt] + P[le] − TS) − (P[p1lt] + P[p1le])
+//                   − (P[p2lt] + P[p2le]) + G[c1] + G[c2],   G[c] = P[B_c] + P[E_c].
 __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
                                                          double* __restrict__ out) {
     extern __shared__ double sm[];
@@ -115,11 +119,12 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
     const int64_t sBase = d.sumOff[b];
     const int mSb = int(d.sumOff[b + 1] - sBase);
     const int N = 3 * mSb;
-    double* wf = sm;             // [mSb]
-    double* ws = wf + mSb;       // [mSb]
-    double* P = ws + mSb;        // [N + 1]
-    double* QB = P + N + 1;      // [53]
-    int32_t* lhand = reinterpret_cast<int32_t*>(QB + 56);  // [2 mSb]
+    double2* W = reinterpret_cast<double2*>(sm);  // [mSb] (ws, wf)
+    double* P = sm + 2 * mSb;                     // [N + 1]
+    double* QB = P + N + 1;                       // [53]
+    double* G = QB + 56;                          // [52]
+    double* CF = G + 56;                          // [52]
+    int32_t* lhand = reinterpret_cast<int32_t*>(CF + 56);  // [2 mSb]
     int32_t* lptr = lhand + 2 * mSb;                       // [53]
 
     // 1. weights of every summing hand for sequence a: the few F/S entries of
@@ -161,8 +166,7 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
             const int j = tid + q * kThreads;
             if (j < mSb) {
                 const double lam = __ldg(d.lamS + sBase + j);
-                wf[j] = lam * f[q];
-                ws[j] = lam * s[q];
+                W[j] = make_double2(lam * s[q], lam * f[q]);
             }
         }
     }
@@ -174,11 +178,10 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
     double sv = 0.0, sw = 0.0;
 #pragma unroll 4
     for (int p = j0; p < j1; ++p) {
-        const int h = p < mSb ? p : lhand[p - mSb];
-        const double v = ws[h];
-        P[p] = v;  // staged; replaced by its prefix below
-        sv += v;
-        sw += wf[h];
+        const double2 w = W[p < mSb ? p : lhand[p - mSb]];
+        P[p] = w.x;  // staged; replaced by its prefix below
+        sv += w.x;
+        sw += w.y;
     }
     const double iv = warp_incl_scan(sv, lane);
     const double iw = warp_incl_scan(sw, lane);
@@ -187,6 +190,8 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
         warpW[warp] = iw;
     }
     // output tables are independent of the scan: load them before the barrier
+    // (measured: loading them in step 3 instead frees registers for a fourth
+    // resident CTA but is 15% slower)
     const int64_t oBase = d.outOff[b];
     const int mOb = int(d.outOff[b + 1] - oBase);
     int4 tb[kPer];
@@ -219,11 +224,11 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
         for (; nc <= kCards; ++nc) {
             const int B = mSb + lptr[nc];
             if (B >= j1) break;
-            for (; p < B; ++p) runQ += wf[p < mSb ? p : lhand[p - mSb]];
+            for (; p < B; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
             QB[nc] = runQ;
         }
         if (tid == kThreads - 1) {
-            for (; p < j1; ++p) runQ += wf[p < mSb ? p : lhand[p - mSb]];
+            for (; p < j1; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
             for (; nc <= kCards; ++nc) QB[nc] = runQ;  // lists ending at N
         }
     }
@@ -234,6 +239,11 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
         run += v;
     }
     if (tid == kThreads - 1) P[N] = run;
+    __syncthreads();
+    if (tid < kCards) {  // per-card terms
+        G[tid] = P[mSb + lptr[tid]] + P[mSb + lptr[tid + 1]];
+        CF[tid] = QB[tid + 1] - QB[tid];
+    }
     __syncthreads();
 
     // 3. outputs of every hand of the board for sequence a
@@ -248,13 +258,10 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
             const int lt = t.x & 0xffff, le = t.x >> 16;
             const int dup = (t.y & 0xffff) - 1, c1 = (t.y >> 16) & 0xff, c2 = t.y >> 24;
             const int p1lt = t.z & 0xffff, p1le = t.z >> 16, p2lt = t.w & 0xffff, p2le = t.w >> 16;
-            const int B1 = mSb + lptr[c1], E1 = mSb + lptr[c1 + 1];
-            const int B2 = mSb + lptr[c2], E2 = mSb + lptr[c2 + 1];
-            double fpart = TF - (QB[c1 + 1] - QB[c1]) - (QB[c2 + 1] - QB[c2]);
-            if (dup >= 0) fpart += wf[dup];
-            const double lower = P[lt] - (P[p1lt] - P[B1]) - (P[p2lt] - P[B2]);
-            const double upper = (TS - P[le]) - (P[E1] - P[p1le]) - (P[E2] - P[p2le]);
-            out[(oBase + i) * d.nO + a] = lo[q] * (fpart + sg * (lower - upper));
+            double fpart = TF - CF[c1] - CF[c2];
+            if (dup >= 0) fpart += W[dup].y;
+            const double wsum = (P[lt] + P[le] - TS) - (P[p1lt] + P[p1le]) - (P[p2lt] + P[p2le]) + G[c1] + G[c2];
+            out[(oBase + i) * d.nO + a] = lo[q] * (fpart + sg * wsum);
         }
     }
 }
