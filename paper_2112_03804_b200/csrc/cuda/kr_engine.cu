@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(32)
         }
     };
     for (int c = 0; c < kStages - 1; ++c) issue(c);
-    double carry = 0.0, mulNext = 0.0;
+    double carry = needMul ? 0.0 : -0.0, mulNext = 0.0;
     for (int c = 0; c < nChunks; ++c) {
         issue(c + kStages - 1);
         const int st = c % kStages;
@@ -314,31 +314,58 @@ __global__ void __launch_bounds__(32)
         // Rows past n or past the lane's chain length are computed and
         // discarded (predicated store, carry kept).
         if (!needMul) {  // every multiplier is -1: z_p = t_p + z_{p-1}
-            for (int q0 = 0; q0 < n; q0 += 8) {
-                double t[8];
-                if (DIR > 0) {
+            // One dependent DADD per element and nothing else on the chain:
+            // the carry starts at -0.0, and t + (-0.0) == t for every t
+            // (including -0.0), so a chain's first element needs no special
+            // case; backward rows past the lane's chain end feed -0.0 instead
+            // of t, which keeps the carry at -0.0 until the chain starts.
+            // Forward rows past the chain end (and rows past the chunk, only
+            // in the last chunk) compute unused values.  The next batch's
+            // shared-memory loads are issued before this batch's adds.
+            const int nbat = (n + 7) / 8;
+            auto load = [&](int qb, double* dst) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) t[u] = T[(q0 + u) * 32 + lane];
+                for (int u = 0; u < 8; ++u) {
+                    const int q = DIR > 0 ? qb * 8 + u : n - 1 - (qb * 8 + u);
+                    dst[u] = T[(q >= 0 && q < n ? q : 0) * 32 + lane];
+                }
+            };
+            double t[8], tn[8];
+            load(0, t);
+            if (n == kChunkRows) {
+                // Full chunk: every row is inside the slice, so stores need no
+                // predicate -- rows past a lane's chain end are that lane's
+                // padding positions, which nothing reads (kpad >= k).
+                double* zr = zc + int64_t(r0) * 32;
+#pragma unroll
+                for (int qb = 0; qb < kChunkRows / 8; ++qb) {
+                    if (qb + 1 < kChunkRows / 8) load(qb + 1, tn);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        const int32_t j = r0 + q0 + u;
-                        const double zq = j == 0 ? t[u] : t[u] + carry;
-                        const bool ok = q0 + u < n && j < len;
-                        if (ok) zc[int64_t(j) * 32] = zq;
-                        carry = ok ? zq : carry;
+                        const int q = DIR > 0 ? qb * 8 + u : kChunkRows - 1 - (qb * 8 + u);
+                        const double tv = (DIR > 0 || r0 + q < len) ? t[u] : -0.0;
+                        const double zq = tv + carry;
+                        zr[q * 32] = zq;
+                        carry = zq;
                     }
-                } else {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) t[u] = T[(n - 1 - q0 - u >= 0 ? n - 1 - q0 - u : 0) * 32 + lane];
+                    for (int u = 0; u < 8; ++u) t[u] = tn[u];
+                }
+            } else {
+                for (int qb = 0; qb < nbat; ++qb) {
+                    if (qb + 1 < nbat) load(qb + 1, tn);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        const int32_t q = n - 1 - q0 - u;
+                        const int q = DIR > 0 ? qb * 8 + u : n - 1 - (qb * 8 + u);
                         const int32_t j = r0 + q;
-                        const double zq = j == len - 1 ? t[u] : t[u] + carry;
-                        const bool ok = q >= 0 && j < len;
-                        if (ok) zc[int64_t(j) * 32] = zq;
-                        carry = ok ? zq : carry;
+                        const bool live = j < len;
+                        const double tv = (DIR > 0 || live) ? t[u] : -0.0;
+                        const double zq = tv + carry;
+                        if (q >= 0 && q < n && live) zc[int64_t(j) * 32] = zq;
+                        carry = zq;
                     }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t[u] = tn[u];
                 }
             }
         } else if (DIR > 0) {
