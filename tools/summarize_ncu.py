@@ -42,6 +42,11 @@ def launches(path):
 def main():
     report, lcsv, tag = sys.argv[1:4]
     h, units, rows = raw(report)
+    # the capture may include the other kernels of a pair (seq_major, chain
+    # solves): the four SpMV launches, in pair order, are VT, UA, UT, AV
+    kn = h.index("Kernel Name")
+    others = [r for r in rows if "k_spmv" not in r[kn]]
+    rows = [r for r in rows if "k_spmv" in r[kn]]
     lines = [f"# ncu summary `{tag}`", "", f"report: `{os.path.basename(report)}` (ncu --set full, --clock-control none);"
              " launch list: `" + os.path.basename(lcsv) + "`", "", "## SpMV kernels (one matvec pair)", "",
              "| matrix | time us | dram read MB | dram write MB | dram % peak | L2 hit % | L1 hit % | warps active % | regs |",
@@ -64,6 +69,15 @@ def main():
                      f"{v['lts__t_sector_hit_rate.pct']:.1f} | {v['l1tex__t_sector_hit_rate.pct']:.1f} | "
                      f"{v['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f} | "
                      f"{v['launch__registers_per_thread']:.0f} |")
+    if others:
+        lines += ["", "Other kernels in the capture:", "", "| kernel | time us | dram read MB | dram write MB |",
+                  "|---|---|---|---|"]
+        for r in others:
+            def val(m):
+                i = h.index(m)
+                return float(r[i]) * SCALE.get(units[i], 1.0)
+            lines.append(f"| {r[kn].split('(')[0].split('::')[-1]} | {val('gpu__time_duration.sum') * 1e6:.1f} | "
+                         f"{val('dram__bytes_read.sum') / 1e6:.1f} | {val('dram__bytes_write.sum') / 1e6:.2f} |")
     ks = launches(lcsv)
     pair = ks[-7:]
     tot = sum(t for _, t in pair)

@@ -85,25 +85,37 @@ def main():
         t0 = time.time()
         eng = CudaEngine([f for _, f in boards])
         create_s = time.time() - t0
-        del boards
         pair_bytes = 2 * eng.bytes_per_product()
         est = pair_bytes / (PEAK * 1e9 * 0.8)
         reps = max(10, min(2000, int(2.0 / max(est, 1e-6))))
         t = time_pairs(eng, reps)
         gbs = pair_bytes / t / 1e9
+        eng.close()
+        torch.cuda.empty_cache()
+        # the same pairs through the implicit engine (K7, nothing materialised)
+        t0 = time.time()
+        ek = CudaEngine.kron([i for i, _ in boards])
+        kron_create_s = time.time() - t0
+        tk = time_pairs(ek, max(50, min(2000, int(0.5 / max(t / 8, 1e-6)))))
+        ek.close()
         row = {"point": name, "nnz": nnz, "bytes_per_pair": pair_bytes, "pairs_per_s": 1 / t,
                "us_per_pair": t * 1e6, "gb_per_s": gbs, "frac_of_measured_peak": gbs / PEAK,
-               "reps": reps, "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2)}
+               "reps": reps, "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2),
+               "implicit_us_per_pair": tk * 1e6, "implicit_pairs_per_s": 1 / tk,
+               "implicit_create_s": round(kron_create_s, 2)}
         rows.append(row)
         print(json.dumps(row), flush=True)
-        eng.close()
+        del boards
         torch.cuda.empty_cache()
     lines = [f"# Matvec bandwidth sweep ({tag}), one B200, fp64, Technique B postprocessed", "",
              f"Whole matvec pair (Ax + ATx); algorithmic bytes per BASELINE.md §2; peak {PEAK} GB/s (measured).", "",
-             "| point | stored nnz | MB / pair | us / pair | pairs/s | GB/s | % of peak |", "|---|---|---|---|---|---|---|"]
+             "The implicit columns time the same pairs through K7 (kr_engine_create_kron), which streams no factors.", "",
+             "| point | stored nnz | MB / pair | us / pair | pairs/s | GB/s | % of peak | K7 us / pair | K7 pairs/s |",
+             "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append(f"| {r['point']} | {r['nnz']:,} | {r['bytes_per_pair']/1e6:,.1f} | {r['us_per_pair']:,.1f} | "
-                     f"{r['pairs_per_s']:,.1f} | {r['gb_per_s']:,.0f} | {100*r['frac_of_measured_peak']:.1f} |")
+                     f"{r['pairs_per_s']:,.1f} | {r['gb_per_s']:,.0f} | {100*r['frac_of_measured_peak']:.1f} | "
+                     f"{r['implicit_us_per_pair']:,.1f} | {r['implicit_pairs_per_s']:,.0f} |")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_sweep.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
