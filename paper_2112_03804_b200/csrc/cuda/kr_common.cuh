@@ -114,6 +114,7 @@ struct kr_engine {
     int64_t kpad = 0;       // internal k positions (>= k; padding never touched)
     int64_t nchains = 0;    // number of chain slices
     bool chain_tma = true;  // TMA bulk-copy pipeline (else register pipeline)
+    bool lean = true;       // lean SELL variant for one-entry-row matrices (KR_NO_LEAN=1: off)
     int chain_withmul = 0;  // some chain has a multiplier other than -1
     int64_t* chain_ptr = nullptr;
     int32_t* chain_len = nullptr;

@@ -1237,6 +1237,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             e->bSl[w].push_back(tsl[w]);
             e->bNl[w].push_back(tnl[w]);
         }
+        e->lean = std::getenv("KR_NO_LEAN") == nullptr;
         const int G = group_count(nb, flags);
         for (int g = 0; g < G; ++g) {
             const int g1 = int(int64_t(nb) * (g + 1) / G);
@@ -1311,7 +1312,7 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
         KR_CK(cudaEventRecord(pend.a, s));
     }
     if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
-    else if (A.maxLen <= 1 && !std::getenv("KR_NO_LEAN"))
+    else if (A.maxLen <= 1 && e->lean)
         k_spmv<false, 1, 8><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
