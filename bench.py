@@ -164,6 +164,43 @@ def oracle_boards(indices, threads):
         return list(ex.map(one, indices))
 
 
+def config1_gpu():
+    """BASELINE config 1: the parity game (twenty_card plays the Leduc role,
+    SURVEY.md §7), Kronecker sparsification + 1000 CFR+ iterations in fp64,
+    checkpointEvery = 1 (the parity run), on the device."""
+    from paper_2112_03804_b200 import host as H
+    from paper_2112_03804_b200.solver import DcfrParams, solver_for
+    inst = H.builtin("twenty_card")
+    t0 = time.perf_counter()
+    f = inst.sparsify("b", True)
+    sparsify_s = time.perf_counter() - t0
+    sv = solver_for([(inst, f)])
+    prm = DcfrParams.cfr_plus(max_iters=1000, checkpoint_every=1)
+    sv.run(DcfrParams.cfr_plus(max_iters=5, checkpoint_every=1))  # warm
+    r = sv.run(prm)
+    return {"workload": "config1: twenty_card (Leduc role), Technique B post, 1000 CFR+ iterations, "
+                        "checkpointEvery=1", "iterations": r.iterations, "exploitability": r.exploitability,
+            "device_seconds": r.seconds, "iters_per_s": r.iterations / r.seconds if r.seconds else None,
+            "sparsify_s": sparsify_s, "alpha": "+inf", "beta": "-inf", "gamma": 1.0, "rule": "cfr+",
+            "_trace": r.trace_expl}
+
+
+def config1_cpu(gpu):
+    """The same 1000 CFR+ iterations on the oracle (CPU, one thread) and the
+    bitwise cross-check of the GPU trace against it."""
+    import math
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    o = po.Instance.builtin("twenty_card")
+    t0 = time.perf_counter()
+    r = po.dcfr(o, o.sparsify("b", True), alpha=math.inf, beta=-math.inf, gamma=1.0, max_iters=1000,
+                checkpoint_every=1, rule=1)
+    secs = time.perf_counter() - t0
+    same = bool(np.array_equal(np.asarray(gpu["_trace"]).view(np.int64), r["trace_expl"].view(np.int64)))
+    return {"seconds": secs, "iters_per_s": 1000 / secs, "cores": 1, "kind": "port",
+            "exploitability": r["exploitability"], "gpu_trace_bitwise_equal": same}
+
+
 def cpu_baseline(threads, budget_s):
     """The reference engine (restated in oracle/: matvec / matvecTranspose,
     engine.hpp:58-133, sequential per call) over a bounded sample of the
@@ -351,6 +388,7 @@ def run_product(args):
     # ---- implicit Kronecker engine (K7) -------------
     implicit = run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
                             sum_over_ranks)
+    config1 = config1_gpu() if rank == 0 else None
 
     if rank != 0:
         return 0
@@ -386,10 +424,12 @@ def run_product(args):
         "gpu_launches": gpu_launches,
         "clocks": sampler.summary(),
         "implicit": implicit,
+        "config1": {k: v for k, v in config1.items() if not k.startswith("_")},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds)
-    print(json.dumps(line), flush=True)
+        line["cpu_baseline"]["config1"] = config1_cpu(config1)
+    print(json.dumps(line, allow_nan=False), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -41,6 +41,13 @@ struct kr_solver {
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
     int team = 4;                // lanes per hand in k_player_team (2, 4 or 8)
+    // graph replay of whole iterations (kr_solver_run without early stop):
+    // per-iteration factors pos/neg/shrink and weightSum as device tables
+    // indexed by the device counter d_cnt[0] (iteration), d_cnt[1] = checkpoints
+    double* d_fac = nullptr;
+    double* d_ws = nullptr;
+    int* d_cnt = nullptr;
+    bool graphs = true;
     int rule = 0;                // KR_RULE_*
     int64_t* d_bstart[2] = {nullptr, nullptr};
     double* regret[2] = {nullptr, nullptr};
@@ -272,9 +279,16 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                                                      const double* __restrict__ g, int negate,
                                                      double* __restrict__ regret, double* __restrict__ xout,
                                                      double* __restrict__ avg, double pos, double neg, double shrink,
-                                                     int rule) {
+                                                     int rule, const double* __restrict__ fac,
+                                                     const int* __restrict__ dt) {
     extern __shared__ double sm[];
     const int stride = hpb + 1;
+    if (fac) {  // graph replay: this iteration's factors from the device table
+        const int t = *dt;
+        pos = fac[3 * t];
+        neg = fac[3 * t + 1];
+        shrink = fac[3 * t + 2];
+    }
     double* Rg = sm;                      // n x stride      regrets
     double* V = Rg + n * stride;          // (n+1) x stride  gradient -> values -> probabilities -> reach
     double* NV = V + (n + 1) * stride;    // nn x stride     node values
@@ -453,11 +467,16 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
     }
 }
 
+// Device-side counters of a replayed graph: c[which] += 1.
+__global__ void k_tick(int* c, int which) { c[which] += 1; }
+
 size_t team_smem(int n, int nn, int hpb, int tlen) {
     return size_t(2 * n + 1 + nn) * size_t(hpb + 1) * 8 + size_t(tlen) * 4 + 16;
 }
 
-__global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w, double* __restrict__ out) {
+__global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w, double* __restrict__ out,
+                            const double* __restrict__ wsArr, const int* __restrict__ dt) {
+    if (wsArr) w = wsArr[*dt];  // graph replay: weightSum of this iteration
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q < n) out[q] = avg[q] / w;  // solver.hpp:390-391
 }
@@ -501,8 +520,10 @@ __global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int
 constexpr int kSumChunk = 2048;
 __global__ void __launch_bounds__(256) k_board_sums(const double* __restrict__ handval,
                                                     const int64_t* __restrict__ bstart, int nb,
-                                                    double* __restrict__ out) {
+                                                    double* __restrict__ out, const int* __restrict__ slot,
+                                                    int64_t slotStride) {
     __shared__ double buf[kSumChunk];
+    if (slot) out += int64_t(*slot) * slotStride;  // graph replay: this checkpoint's slot
     const int b = blockIdx.x;
     if (b >= nb) return;
     double total = 0;
@@ -611,7 +632,7 @@ size_t step_smem(int n, int nt, int nn, int na) {
 }
 
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool dev = false) {
     if (s->levelled[p]) {
         const int team = s->team;
         const int hpb = 256 / team;
@@ -620,12 +641,14 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
         kern<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
-                                      hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule);
+                                      hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule,
+                                      dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr);
         KR_CK_LAUNCH();
         s->launches++;
         return;
     }
     if (s->rule != 0) throw Fail{KR_INVALID_INPUT, "update rule needs a reference-ordered treeplex"};
+    if (dev) throw Fail{KR_CUDA, "internal: graph replay needs the team step kernel"};
     const int nt = s->nt[p];
     const unsigned grid = unsigned((s->H[p] + nt - 1) / nt);
     if (grid == 0) return;
@@ -639,7 +662,10 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
 
 // Best-response totals of `player` against device strategy `opp`; fills
 // per-board values (host) and returns their sum.
-void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<double>& boards, cudaStream_t st) {
+// Per-board best-response totals of `player` against device strategy `opp`,
+// written to device memory `dst` (nboards values), nothing synchronised.
+void best_response_to(kr_solver* s, int player, const double* opp, double* dst, cudaStream_t st,
+                      const int* slot = nullptr, int64_t slotStride = 0) {
     kr_engine* e = s->eng;
     if (player == 0) engine_ax(e, opp, s->g, st);
     else engine_atx(e, opp, s->g, st);
@@ -654,9 +680,15 @@ void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<
         KR_CK_LAUNCH();
         s->launches++;
     }
-    k_board_sums<<<unsigned(s->nboards), 256, 0, st>>>(s->handval, s->d_bstart[player], s->nboards, s->boardval);
+    k_board_sums<<<unsigned(s->nboards), 256, 0, st>>>(s->handval, s->d_bstart[player], s->nboards, dst, slot,
+                                                        slotStride);
     KR_CK_LAUNCH();
     s->launches++;
+}
+
+// The same, copied to the host (synchronises the stream).
+void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<double>& boards, cudaStream_t st) {
+    best_response_to(s, player, opp, s->boardval, st);
     boards.assign(size_t(s->nboards), 0.0);
     KR_CK(cudaMemcpyAsync(boards.data(), s->boardval, 8 * size_t(s->nboards), cudaMemcpyDeviceToHost, st));
     KR_CK(cudaStreamSynchronize(st));
@@ -673,6 +705,9 @@ void destroy_solver(kr_solver* s) {
         cudaFree(s->x[p]);
         cudaFree(s->a[p]);
     }
+    cudaFree(s->d_fac);
+    cudaFree(s->d_ws);
+    cudaFree(s->d_cnt);
     cudaFree(s->g);
     cudaFree(s->handval);
     cudaFree(s->boardval);
@@ -806,14 +841,121 @@ int kr_solver_destroy(kr_solver* s) {
 int64_t kr_solver_launches(const kr_solver* s) { return s ? s->launches : 0; }
 
 namespace {
-void normalise_averages(kr_solver* s, cudaStream_t st) {
+void normalise_averages(kr_solver* s, cudaStream_t st, bool dev = false) {
     for (int p = 0; p < 2; ++p) {
         const int64_t len = s->H[p] * s->n[p];
         if (len == 0) continue;
-        krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, s->weightSum, s->a[p]);
+        krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, s->weightSum, s->a[p],
+                                                                      dev ? s->d_ws : nullptr,
+                                                                      dev ? s->d_cnt : nullptr);
         KR_CK_LAUNCH();
         s->launches++;
     }
+}
+}  // namespace
+
+namespace {
+// Iterations t = s->t+1 .. maxIters by replaying two captured CUDA graphs:
+// one DCFR iteration (tick, A x2, step 1, A^T x1, step 2) and the same plus
+// a checkpoint (normalise, two best responses into checkpoint slot d_cnt[1],
+// tick).  The per-iteration scalars come from device tables built here with
+// the host loop's exact expressions (kr_solver_iterate), so a replayed
+// iteration is bitwise the iteration kr_solver_iterate would launch.  The
+// engine's and solver's flop / launch counters advance per replay.
+void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<int>& at, cudaStream_t st) {
+    kr_engine* e = s->eng;
+    const int nb = s->nboards;
+    const int t0 = s->t;
+    std::vector<double> fac(size_t(3) * (maxIters + 1), 0.0), ws(size_t(maxIters) + 1, 0.0);
+    double w = s->weightSum;
+    ws[size_t(t0)] = w;
+    for (int t = t0 + 1; t <= maxIters; ++t) {
+        fac[3 * size_t(t)] = krb::discount_factor(t, s->alpha);
+        fac[3 * size_t(t) + 1] = krb::discount_factor(t, s->beta);
+        const double shrink = std::pow(double(t) / (t + 1), s->gamma);
+        fac[3 * size_t(t) + 2] = shrink;
+        w += 1;  // solver.hpp:384-387, as kr_solver_iterate
+        w *= shrink;
+        ws[size_t(t)] = w;
+    }
+    cudaFree(s->d_fac);
+    cudaFree(s->d_ws);
+    s->d_fac = s->d_ws = nullptr;
+    s->d_fac = krb::dev_alloc<double>(int64_t(fac.size()));
+    s->d_ws = krb::dev_alloc<double>(int64_t(ws.size()));
+    if (!s->d_cnt) s->d_cnt = krb::dev_alloc<int>(2);
+    KR_CK(cudaMemcpyAsync(s->d_fac, fac.data(), 8 * fac.size(), cudaMemcpyHostToDevice, st));
+    KR_CK(cudaMemcpyAsync(s->d_ws, ws.data(), 8 * ws.size(), cudaMemcpyHostToDevice, st));
+    const int cnt0[2] = {t0, 0};
+    KR_CK(cudaMemcpyAsync(s->d_cnt, cnt0, sizeof(cnt0), cudaMemcpyHostToDevice, st));
+    KR_CK(cudaStreamSynchronize(st));
+
+    const bool timing = e->timing;
+    e->timing = false;
+    struct Delta {
+        int64_t flops = 0, elaunch = 0, slaunch = 0;
+    };
+    auto capture = [&](bool withCk, cudaGraphExec_t& exec, Delta& d) {
+        const int64_t f0 = e->flops_total, el0 = e->launches, sl0 = s->launches;
+        cudaGraph_t g;
+        KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 0);
+            KR_CK_LAUNCH();
+            s->launches++;
+            krb::engine_ax(e, s->x[1], s->g, st);                                    // g1 = A x2
+            krb::launch_step(s, 0, 1, s->g, 0, 0.0, 0.0, 0.0, st, true);             // P1
+            krb::engine_atx(e, s->x[0], s->g, st);                                   // A^T x1
+            krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);             // P2
+            if (withCk) {
+                normalise_averages(s, st, true);                                     // solver.hpp:390-391
+                krb::best_response_to(s, 0, s->a[1], dck, st, s->d_cnt + 1, 2 * nb);
+                krb::best_response_to(s, 1, s->a[0], dck + nb, st, s->d_cnt + 1, 2 * nb);
+                krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 1);
+                KR_CK_LAUNCH();
+                s->launches++;
+            }
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            throw;
+        }
+        KR_CK(cudaStreamEndCapture(st, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        KR_CK(ie);
+        d.flops = e->flops_total - f0;
+        d.elaunch = e->launches - el0;
+        d.slaunch = s->launches - sl0;
+        e->flops_total = f0;
+        e->launches = el0;
+        s->launches = sl0;
+    };
+    cudaGraphExec_t gIt = nullptr, gCk = nullptr;
+    Delta dIt, dCk;
+    try {
+        capture(false, gIt, dIt);
+        capture(true, gCk, dCk);
+        for (int t = t0 + 1; t <= maxIters; ++t) {
+            const bool isCk = t % every == 0 || t == maxIters;
+            KR_CK(cudaGraphLaunch(isCk ? gCk : gIt, st));
+            const Delta& d = isCk ? dCk : dIt;
+            e->flops_total += d.flops;
+            e->launches += d.elaunch;
+            s->launches += d.slaunch;
+            if (isCk) at.push_back(t);
+        }
+        e->flops_last = e->kron ? krb::kron_flops(e, 1) : e->flops_per_product;
+    } catch (...) {
+        if (gIt) cudaGraphExecDestroy(gIt);
+        if (gCk) cudaGraphExecDestroy(gCk);
+        e->timing = timing;
+        throw;
+    }
+    cudaGraphExecDestroy(gIt);
+    cudaGraphExecDestroy(gCk);
+    e->timing = timing;
+    s->t = maxIters;
+    s->weightSum = ws[size_t(maxIters)];
 }
 }  // namespace
 
@@ -924,23 +1066,22 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
         ck(kr_solver_set_rule(s, prm->rule));
         ck(kr_solver_begin(s, prm->alpha, prm->beta, prm->gamma));
         r->trace_len = 0;
-        std::vector<double> b1(size_t(s->nboards)), b2(size_t(s->nboards));
-        while (s->t < prm->max_iters) {
-            // run to the next checkpoint (t % every == 0 or t == maxIters)
-            const int next = std::min(prm->max_iters, (s->t / prm->checkpoint_every + 1) * prm->checkpoint_every);
-            ck(kr_solver_iterate(s, next - s->t));
-            ck(kr_solver_checkpoint(s, b1.data(), b2.data()));
+        const int nb = s->nboards;
+        std::vector<double> b1(static_cast<size_t>(nb)), b2(static_cast<size_t>(nb));
+        // Record one checkpoint's per-board values (solver.hpp:389-392; the
+        // board-order sums are the chance-root average of SURVEY.md 8(d)).
+        auto record = [&](const double* v1, const double* v2) {
             double br1 = 0, br2 = 0, expl;
-            for (int b = 0; b < s->nboards; ++b) {
-                br1 += b1[size_t(b)];
-                br2 += b2[size_t(b)];
+            for (int b = 0; b < nb; ++b) {
+                br1 += v1[b];
+                br2 += v2[b];
             }
-            if (s->nboards == 1) {
-                expl = (b1[0] + b2[0]) / 2 / s->pot;  // solver.hpp:329-330
+            if (nb == 1) {
+                expl = (v1[0] + v2[0]) / 2 / s->pot;  // solver.hpp:329-330
             } else {
                 expl = 0;
-                for (int b = 0; b < s->nboards; ++b) expl += (b1[size_t(b)] + b2[size_t(b)]) / 2 / s->pot;
-                expl /= s->nboards;
+                for (int b = 0; b < nb; ++b) expl += (v1[b] + v2[b]) / 2 / s->pot;
+                expl /= nb;
             }
             const int i = r->trace_len;
             if (i < r->trace_cap) {
@@ -948,15 +1089,60 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
                 if (r->trace_expl) r->trace_expl[i] = expl;
                 if (r->trace_br1) r->trace_br1[i] = br1;
                 if (r->trace_br2) r->trace_br2[i] = br2;
-                for (int b = 0; b < s->nboards; ++b) {
-                    if (r->trace_board_br1) r->trace_board_br1[size_t(i) * s->nboards + b] = b1[size_t(b)];
-                    if (r->trace_board_br2) r->trace_board_br2[size_t(i) * s->nboards + b] = b2[size_t(b)];
+                for (int b = 0; b < nb; ++b) {
+                    if (r->trace_board_br1) r->trace_board_br1[size_t(i) * nb + b] = v1[b];
+                    if (r->trace_board_br2) r->trace_board_br2[size_t(i) * nb + b] = v2[b];
                 }
             }
             r->trace_len = i + 1;
             r->iterations = s->t;
             r->exploitability = expl;
-            if (prm->target_exploitability > 0 && expl <= prm->target_exploitability) break;
+            return expl;
+        };
+        if (prm->target_exploitability > 0) {
+            // early stop: every checkpoint's value is needed on the host at once
+            while (s->t < prm->max_iters) {
+                // run to the next checkpoint (t % every == 0 or t == maxIters)
+                const int next =
+                    std::min(prm->max_iters, (s->t / prm->checkpoint_every + 1) * prm->checkpoint_every);
+                ck(kr_solver_iterate(s, next - s->t));
+                ck(kr_solver_checkpoint(s, b1.data(), b2.data()));
+                if (record(b1.data(), b2.data()) <= prm->target_exploitability) break;
+            }
+        } else {
+            // no early stop: checkpoints write to a device buffer, read back once
+            const int nck = (prm->max_iters + prm->checkpoint_every - 1) / prm->checkpoint_every + 1;
+            double* dck = krb::dev_alloc<double>(int64_t(nck) * 2 * nb);
+            std::vector<int> at;
+            try {
+                if (s->graphs && s->levelled[0] && s->levelled[1] && !std::getenv("KR_NO_GRAPH")) {
+                    run_graphs(s, prm->max_iters, prm->checkpoint_every, dck, at, st);
+                } else {
+                    while (s->t < prm->max_iters) {
+                        const int next =
+                            std::min(prm->max_iters, (s->t / prm->checkpoint_every + 1) * prm->checkpoint_every);
+                        ck(kr_solver_iterate(s, next - s->t));
+                        double* slot = dck + size_t(at.size()) * 2 * nb;
+                        normalise_averages(s, st);                             // solver.hpp:390-391
+                        krb::best_response_to(s, 0, s->a[1], slot, st);       // br1 vs avg2
+                        krb::best_response_to(s, 1, s->a[0], slot + nb, st);  // br2 vs avg1
+                        at.push_back(s->t);
+                    }
+                }
+                std::vector<double> host(at.size() * 2 * size_t(nb));
+                KR_CK(cudaMemcpyAsync(host.data(), dck, 8 * host.size(), cudaMemcpyDeviceToHost, st));
+                KR_CK(cudaStreamSynchronize(st));
+                const int tEnd = s->t;
+                for (size_t c = 0; c < at.size(); ++c) {
+                    s->t = at[c];  // record() stamps the checkpoint's iteration
+                    record(host.data() + c * 2 * nb, host.data() + c * 2 * nb + nb);
+                }
+                s->t = tEnd;
+            } catch (...) {
+                cudaFree(dck);
+                throw;
+            }
+            cudaFree(dck);
         }
         KR_CK(cudaEventRecord(ev1, st));
         KR_CK(cudaEventSynchronize(ev1));
