@@ -67,6 +67,17 @@ def workload_config(nboards, world, extra=None):
     return cfg
 
 
+def _finite(obj):
+    """Strict JSON: non-finite floats become strings ("inf", "nan")."""
+    if isinstance(obj, float) and not np.isfinite(obj):
+        return str(obj)
+    if isinstance(obj, dict):
+        return {k: _finite(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_finite(v) for v in obj]
+    return obj
+
+
 # --------------------------------------------------------------- clocks ----
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -249,7 +260,7 @@ def run_reference(args):
                                        "reference engine restated in oracle/ (Eigen3 absent: reference "
                                        "unbuildable)"},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(_finite(line)), flush=True)
     return 0
 
 
@@ -429,7 +440,7 @@ def run_product(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds)
         line["cpu_baseline"]["config1"] = config1_cpu(config1)
-    print(json.dumps(line, allow_nan=False), flush=True)
+    print(json.dumps(_finite(line)), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
