@@ -10,7 +10,11 @@ import torch  # noqa: E402
 from paper_2112_03804_b200 import host as H  # noqa: E402
 from paper_2112_03804_b200.solver import DcfrParams, solver_for  # noqa: E402
 
-boards = H.turn_instances("Ks7d4c2h", 48, 3)
+if "--config2" in sys.argv:
+    inst = H.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=3)
+    boards = [(inst, inst.sparsify("b", True))]
+else:
+    boards = H.turn_instances("Ks7d4c2h", 48, 3)
 for implicit in (True, False):
     sv = solver_for(boards, implicit=implicit)
     sv.run(DcfrParams(max_iters=5, checkpoint_every=5))
