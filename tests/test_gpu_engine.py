@@ -165,3 +165,24 @@ def test_device_pointer_entry_points():
     eng.ax_device(x.data_ptr(), y.data_ptr())
     torch.cuda.ExternalStream(eng.stream).synchronize()
     assert bits_equal(y.cpu().numpy(), eng.Ax(x.cpu().numpy()))
+
+
+@pytest.mark.parametrize("groups", ["1", "2", "4"])
+def test_host_pipeline_groups_bitwise(groups, monkeypatch):
+    """kr_engine_ax / kr_engine_atx pipelined over board groups (first and
+    last SpMV launched per group range) give the bits of the oracle."""
+    monkeypatch.setenv("KR_GROUPS", groups)
+    ps = [H.builtin("river_full", seed=10 + k, board=b, deck=26, tree=3)
+          for k, b in enumerate(["Kc9d7c4d2c", "Ac8d6c3d2d", "QcJd9c5d3c", "Tc7d5c4d2c"])]
+    os_ = [po.Instance.builtin("river_full", seed=10 + k, board=b, deck=26, tree=3)
+           for k, b in enumerate(["Kc9d7c4d2c", "Ac8d6c3d2d", "QcJd9c5d3c", "Tc7d5c4d2c"])]
+    eng = CudaEngine([p.sparsify("b", True) for p in ps])
+    sps = [o.sparsify("b", True) for o in os_]
+    rng = np.random.default_rng(4)
+    x, y = rng.standard_normal(eng.cols), rng.standard_normal(eng.rows)
+    ax, aty = eng.Ax(x), eng.ATx(y)
+    cx = np.cumsum([0] + [p.cols for p in ps])
+    cy = np.cumsum([0] + [p.rows for p in ps])
+    ex = np.concatenate([sp.matvec(x[cx[b]:cx[b + 1]]) for b, sp in enumerate(sps)])
+    ey = np.concatenate([sp.matvec_t(y[cy[b]:cy[b + 1]]) for b, sp in enumerate(sps)])
+    assert bits_equal(ax, ex) and bits_equal(aty, ey)

@@ -129,3 +129,36 @@ def test_kron_solver_turn_boards():
     np.testing.assert_allclose(r_imp.board_br1[0], r_fac.board_br1[0], rtol=1e-5, atol=1e-12)
     np.testing.assert_allclose(r_imp.trace_expl[1], r_fac.trace_expl[1], rtol=5e-2)
     assert r_imp.trace_expl[1] < 0.5 * r_imp.trace_expl[0]
+
+
+def test_kron_mixed_hand_counts_match_factored():
+    """Boards with different hand counts in one engine (1081-hand and 210-hand
+    rivers sharing the 3-bet tree): every per-board offset of K7 is exercised."""
+    boards = [H.builtin("river_full", seed=4, board="Ks7d4c2h9s", tree=3),
+              H.builtin("river_full", seed=5, board="Kc9d7c4d2c", deck=26, tree=3),
+              H.builtin("river_full", seed=6, board="AhKhQh7c7d", tree=3)]
+    assert len({(b.n1, b.n2) for b in boards}) == 1 and len({b.m1 for b in boards}) == 2
+    fac = CudaEngine([b.sparsify("b", True) for b in boards])
+    imp = CudaEngine.kron(boards)
+    rng = np.random.default_rng(8)
+    x, y = rng.standard_normal(fac.cols), rng.standard_normal(fac.rows)
+    assert normwise(imp.Ax(x), fac.Ax(x)) <= TOL
+    assert normwise(imp.ATx(y), fac.ATx(y)) <= TOL
+
+
+@pytest.mark.parametrize("groups", ["1", "3"])
+def test_kron_host_pipeline_groups(groups, monkeypatch):
+    """Host-buffer calls pipelined over board groups (KR_GROUPS) give the
+    same bits as the device-pointer path."""
+    import torch
+    monkeypatch.setenv("KR_GROUPS", groups)
+    boards = [i for i, _ in H.turn_instances("Ks7d4c2h", nboards=5, tree=3, factors=False)]
+    eng = CudaEngine.kron(boards)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(eng.cols)
+    hx = eng.Ax(x)
+    dx = torch.tensor(x, device="cuda")
+    dy = torch.empty(eng.rows, dtype=torch.float64, device="cuda")
+    eng.ax_device(dx.data_ptr(), dy.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(hx, dy.cpu().numpy())
