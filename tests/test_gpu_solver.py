@@ -156,3 +156,12 @@ def test_cfr_plus_config1_1000_iterations():
     assert r.iterations == 1000
     assert r.exploitability < 1e-3
     assert r.trace_expl[-1] < 0.2 * r.trace_expl[0]
+
+
+@pytest.mark.parametrize("knob", [("KR_STEP", "thread"), ("KR_TEAM", "2"), ("KR_TEAM", "8"), ("KR_NO_GRAPH", "1"),
+                                  ("KR_CHAIN", "reg"), ("KR_NO_LEAN", "1")])
+def test_knobs_keep_the_bits(knob, monkeypatch):
+    """Every execution variant reproduces the oracle's gap
+    trajectory bitwise."""
+    monkeypatch.setenv(*knob)
+    gap_trajectory_case("golden", {}, "b", 200)
