@@ -158,7 +158,7 @@ def ncu_traffic(kernel):
 
 
 # ------------------------------------------------------------ CPU side ----
-def oracle_boards(indices, threads):
+def oracle_boards(indices, threads, with_instances=False):
     """CPU oracle factors (oracle/, test infrastructure) for the given boards."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
@@ -169,7 +169,7 @@ def oracle_boards(indices, threads):
     def one(b):
         card, seed = specs[b]
         inst = po.Instance.builtin("river_full", seed=seed, board=TURN + card, tree=3)
-        return inst.sparsify("b", True)
+        return (inst, inst.sparsify("b", True)) if with_instances else inst.sparsify("b", True)
 
     with ThreadPoolExecutor(max_workers=threads) as ex:
         return list(ex.map(one, indices))
@@ -219,14 +219,23 @@ def cpu_baseline(threads, budget_s):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     nb = min(NBOARDS, threads)
-    sps = oracle_boards(range(nb), threads)
+    pairs = oracle_boards(range(nb), threads, with_instances=True)
+    sps = [sp for _, sp in pairs]
     t1 = po.time_pairs_multi(sps, threads, 1)  # warm + estimate
     reps = max(1, int(budget_s / max(t1, 1e-3)))
     t = po.time_pairs_multi(sps, threads, reps)
     board_pairs_per_s = nb * reps / t
+    # DCFR iterations/s, same boards, one per thread
+    d1 = po.time_dcfr_multi(pairs, threads, 1)
+    iters = max(1, int(0.5 * budget_s / max(d1, 1e-3)))
+    d = po.time_dcfr_multi(pairs, threads, iters)
     return {"value": board_pairs_per_s / NBOARDS, "unit": "pairs/s", "cores": threads, "kind": "port",
             "sample": f"{nb} of {NBOARDS} boards x {reps} matvec pairs each, one board per thread "
-                      f"({t:.1f} s); full-turn pairs/s = board-pairs/s / {NBOARDS}"}
+                      f"({t:.1f} s); full-turn pairs/s = board-pairs/s / {NBOARDS}",
+            "solver_iters_per_s": nb * iters / d / NBOARDS,
+            "solver_sample": f"{nb} of {NBOARDS} boards x {iters} DCFR iterations each (default parameters, "
+                             f"no checkpoints), one board per thread ({d:.1f} s); full-turn it/s = "
+                             f"board-iterations/s / {NBOARDS}"}
 
 
 def run_reference(args):
@@ -239,7 +248,8 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     threads = os.cpu_count() or 1
-    sps = oracle_boards(range(args.boards), threads)
+    pairs = oracle_boards(range(args.boards), threads, with_instances=True)
+    sps = [sp for _, sp in pairs]
     t1 = po.time_pairs_multi(sps, threads, 1)
     steps = args.steps
     budget = 150.0
@@ -251,6 +261,10 @@ def run_reference(args):
     for _ in range(steps):
         total += po.time_pairs_multi(sps, threads, 1)
     value = steps / total
+    # DCFR iterations/s on the same game (all boards, one per thread), bounded
+    d1 = po.time_dcfr_multi(pairs, threads, 1)
+    it = max(1, min(20, int(30.0 / max(d1, 1e-3))))
+    solver_ips = it / po.time_dcfr_multi(pairs, threads, it)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -259,7 +273,10 @@ def run_reference(args):
                              "sample": f"all {args.boards} boards per step, one board per thread at a time; "
                                        "reference engine restated in oracle/ (Eigen3 absent: reference "
                                        "unbuildable)"},
-            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "solver_iters_per_s": solver_ips,
+            "solver_sample": f"all {args.boards} boards x {it} DCFR iterations (default parameters), one board "
+                             "per thread at a time"}
     print(json.dumps(_finite(line)), flush=True)
     return 0
 

@@ -339,6 +339,33 @@ double or_time_pairs_multi(void** sps, int count, int threads, int reps, double*
     }
     return sec;
 }
+// DCFR iterations (solver.hpp:365-388, default parameters) on `count`
+// independent boards, one board per host thread at a time: the CPU side of
+// the solver-iterations/s baseline.  Returns wall seconds.
+double or_time_dcfr_multi(void** insts, void** sps, int count, int threads, int iters, double* sink) {
+    std::vector<std::thread> pool;
+    std::vector<double> sinks(size_t(threads), 0.0);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int th = 0; th < threads; ++th)
+        pool.emplace_back([&, th] {
+            for (int b = th; b < count; b += threads) {
+                const auto& kp = static_cast<Inst*>(insts[b])->kp;
+                FactoredEngine eng(static_cast<Sp*>(sps[b])->s);
+                DcfrState st(kp, eng);
+                st.begin(DcfrParams{});
+                st.iterate(iters);
+                sinks[th] += st.x1.empty() ? 0.0 : st.x1[0];
+            }
+        });
+    for (auto& t : pool) t.join();
+    double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (sink) {
+        *sink = 0;
+        for (double v : sinks) *sink += v;
+    }
+    return sec;
+}
+
 int or_reference_matvec(void* h, const double* x, int64_t n, double* y) {
     return guarded([&] {
         Vec out = referenceMatvec(static_cast<Inst*>(h)->kp, Vec(x, x + n));

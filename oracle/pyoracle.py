@@ -289,6 +289,16 @@ def time_pairs_multi(sps, threads, reps):
     return lib().or_time_pairs_multi(arr, len(sps), threads, reps, C.byref(sink))
 
 
+def time_dcfr_multi(pairs, threads, iters):
+    """Wall seconds of `iters` DCFR iterations on each (Instance, Sparsification)
+    board, one board per thread at a time."""
+    ia = (C.c_void_p * len(pairs))(*[i.h.value for i, _ in pairs])
+    sa = (C.c_void_p * len(pairs))(*[s.h.value for _, s in pairs])
+    sink = C.c_double()
+    lib().or_time_dcfr_multi.restype = C.c_double
+    return lib().or_time_dcfr_multi(ia, sa, len(pairs), threads, iters, C.byref(sink))
+
+
 def peel(W, max_iters=1000):
     """sparsifyW (sparsify.hpp:68-103): (rank, nnz What, nnz U, nnz V)."""
     W = np.ascontiguousarray(W, np.float64)
