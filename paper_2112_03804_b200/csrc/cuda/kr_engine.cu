@@ -42,7 +42,10 @@ void set_error(int code, const std::string& msg) {
 
 namespace {
 
-constexpr int kWarpsPerBlock = 4;
+#ifndef KR_WARPS_PER_BLOCK
+#define KR_WARPS_PER_BLOCK 4
+#endif
+constexpr int kWarpsPerBlock = KR_WARPS_PER_BLOCK;  // SELL slices (warps) per block
 
 // ------------------------------------------------------------- kernels ----
 
@@ -61,7 +64,10 @@ struct SellView {
 };
 
 constexpr int kChunk = 256;  // long-row entries staged per warp
-constexpr int kU = 8;  // entries per lane per pipeline stage
+#ifndef KR_KU
+#define KR_KU 8
+#endif
+constexpr int kU = KR_KU;  // entries per lane per pipeline stage
 
 template <bool TWO>
 __device__ __forceinline__ double gather(const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
