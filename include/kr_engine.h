@@ -247,6 +247,24 @@ int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2);
 int kr_solver_averages(kr_solver* s, double* avg1, double* avg2);
 int kr_solver_iteration(const kr_solver* s);
 
+/* Turn endgames (a betting round above the river boards; beyond the
+ * reference).  The payoff is block diagonal: turnEng covers the
+ * turn block (m hands x the turn trees' sequences); riverEngs[t] covers
+ * continuation t's river block over all boards (board-major, each board's hand
+ * order).  mb[b] = river hands of board b; riverToTurn[r] = the turn hand of
+ * river hand r (board-major); sigma[2t + p] = player p's turn sequence leading
+ * to continuation t; riverTrees[2t + p] its river treeplex; pot = 2 x the
+ * turn contribution.  run: DCFR (rule KR_RULE_DCFR) with the turn treeplex
+ * composed as in DESIGN.md §4.8; avg1 / avg2 receive the full average
+ * strategies (turn block, then each continuation's river block). */
+typedef struct kr_turn_solver kr_turn_solver;
+int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs, const kr_treeplex* turnTrees,
+                          const kr_treeplex* riverTrees, int m, int nb, const int32_t* mb, const int32_t* riverToTurn,
+                          const int32_t* sigma, double pot, kr_turn_solver** out);
+int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* p, kr_dcfr_result* r);
+int kr_turn_solver_destroy(kr_turn_solver* s);
+int64_t kr_turn_solver_launches(const kr_turn_solver* s);
+
 /* Per-kernel CUDA-event timing of the engine's SpMV launches (off by
  * default).  When enabled every SpMV launch is bracketed by events on the
  * engine's stream; kr_engine_kernel_times returns, for the four matrices

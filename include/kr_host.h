@@ -41,6 +41,17 @@ int krh_instance_builtin(const char* name, uint64_t seed, int hands, int shared,
 
 void krh_instance_free(krh_instance* h);
 
+/* A river instance with explicit pieces (makeRiverInstance + assemble,
+ * kron.hpp:39-166): board = 5 card ids, deck 52 or 26, hands as card-id pairs
+ * with belief weights per player, and a betting configuration with one
+ * menu (pot fractions) for every context and both players (skeleton.hpp:44-78;
+ * stack per player, pot = each player's contribution, all-in flag, raise cap,
+ * raise_cap < 0 = none).  Used to build the river continuations of a turn
+ * endgame. */
+int krh_instance_custom(const int32_t board[5], int deck, const uint8_t* cards1, const double* w1, int m1,
+                        const uint8_t* cards2, const double* w2, int m2, double stack, double pot,
+                        const double* menu, int nmenu, int all_in, int raise_cap, krh_instance** out);
+
 /* m1 m2 n1 n2 rows cols nodes decisions1 decisions2 terminals folds
  * showdowns nnzF nnzS actions1 actions2 */
 int krh_instance_dims(const krh_instance* h, int64_t out[16]);

@@ -98,7 +98,8 @@ CUDA_SYMBOLS = [
     "kr_device_count", "kr_solver_create", "kr_solver_destroy", "kr_solver_run", "kr_solver_best_response",
     "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
     "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times", "kr_engine_create_kron",
-    "kr_solver_set_rule",
+    "kr_solver_set_rule", "kr_turn_solver_create", "kr_turn_solver_run", "kr_turn_solver_destroy",
+    "kr_turn_solver_launches",
 ]
 
 
@@ -153,6 +154,13 @@ def cuda():
             L.kr_solver_checkpoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
             L.kr_solver_averages.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
             L.kr_solver_iteration.argtypes = [C.c_void_p]
+        L.kr_turn_solver_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(kr_treeplex),
+                                            C.POINTER(kr_treeplex), C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_double, C.POINTER(C.c_void_p)]
+        L.kr_turn_solver_run.argtypes = [C.c_void_p, C.POINTER(kr_dcfr_params), C.POINTER(kr_dcfr_result)]
+        L.kr_turn_solver_destroy.argtypes = [C.c_void_p]
+        L.kr_turn_solver_launches.restype = C.c_int64
+        L.kr_turn_solver_launches.argtypes = [C.c_void_p]
         L.kr_engine_set_timing.argtypes = [C.c_void_p, C.c_int]
         L.kr_engine_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _CUDA = L

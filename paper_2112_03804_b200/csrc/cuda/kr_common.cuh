@@ -78,6 +78,17 @@ T* dev_alloc(int64_t n) {
     return p;
 }
 
+// Raise (never lower) a kernel's dynamic shared-memory limit: the attribute
+// belongs to the kernel, not to the engine or solver that launches it, so a
+// smaller later object must not shrink what an earlier one needs.
+template <class K>
+void raise_smem_limit(K kernel, size_t bytes) {
+    cudaFuncAttributes fa;
+    KR_CK(cudaFuncGetAttributes(&fa, kernel));
+    if (size_t(fa.maxDynamicSharedSizeBytes) < bytes)
+        KR_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
 struct KronState;  // implicit Kronecker engine (kr_kron.cu)
 // Boards [b0, b1) of direction dir (0: A x, 1: Aᵀ y); b1 < 0 = all boards.
 void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0 = 0, int b1 = -1);

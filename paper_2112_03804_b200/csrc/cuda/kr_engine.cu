@@ -1164,8 +1164,8 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             e->chain_neg1 = dev_alloc<uint8_t>(std::max<int64_t>(32 * e->nchains, 1));
             e->chain_mul = dev_alloc<double>(std::max<int64_t>(Kp, 1));
             const int smem = int(size_t(kStages) * kChunkRows * 32 * sizeof(double) * 2);
-            KR_CK(cudaFuncSetAttribute(k_chain_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            KR_CK(cudaFuncSetAttribute(k_chain_tma<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            raise_smem_limit(k_chain_tma<1>, size_t(smem));
+            raise_smem_limit(k_chain_tma<-1>, size_t(smem));
             if (e->nchains) {
                 KR_CK(cudaMemcpy(e->chain_ptr, sbase.data(), 8 * sbase.size(), cudaMemcpyHostToDevice));
                 KR_CK(cudaMemcpy(e->chain_len, slen.data(), 4 * slen.size(), cudaMemcpyHostToDevice));

@@ -526,7 +526,7 @@ kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, u
             smMax = std::max(smMax, e->kron->smem[dir]);
         }
         if (smMax > 227 * 1024) throw Fail{KR_INVALID_INPUT, "board has too many hands for the implicit engine"};
-        KR_CK(cudaFuncSetAttribute(k_kron_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smMax)));
+        raise_smem_limit(k_kron_fused, smMax);
         e->flops_per_product = e->kron->dir[0].flops;
         e->d_in = dev_alloc<double>(std::max(R, C));
         e->d_out = dev_alloc<double>(std::max(R, C));

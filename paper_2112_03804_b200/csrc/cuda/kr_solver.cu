@@ -280,7 +280,14 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                                                      double* __restrict__ regret, double* __restrict__ xout,
                                                      double* __restrict__ avg, double pos, double neg, double shrink,
                                                      int rule, const double* __restrict__ fac,
-                                                     const int* __restrict__ dt) {
+                                                     const int* __restrict__ dt, int noAvg = 0,
+                                                     double* __restrict__ rootOut = nullptr,
+                                                     const double* __restrict__ extra = nullptr) {
+    // noAvg: leave avg alone (river blocks of a turn game are averaged after
+    // their reach is scaled); rootOut: each hand's root value (the sum of its
+    // root nodes' values, descending node order: seqVal[0] of cfrSweep);
+    // extra: values added to each sequence after its children (the river
+    // subgames below a turn sequence).  Hand h, sequence s: extra[h*n + s-1].
     extern __shared__ double sm[];
     const int stride = hpb + 1;
     if (fac) {  // graph replay: this iteration's factors from the device table
@@ -360,6 +367,7 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                         const int sq = seqs[a];
                         double cs = 0.0;  // Vt[sq] of the reference: children, descending
                         for (int c = chPtr[sq]; c < chPtr[sq + 1]; ++c) cs += Nt[chNodes[c] * stride];
+                        if (extra) cs += extra[(h0 + hand) * n + sq - 1];
                         const double gr = Vt[sq * stride];
                         const double gv = negate ? -gr : gr;
                         const double ev = gv + cs;
@@ -398,6 +406,11 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                     }
                 }
             __syncwarp();
+        }
+        if (rootOut && valid && lane == 0) {  // seqVal[0]: root nodes, descending
+            double acc = 0.0;
+            for (int k = levPtr[1] - 1; k >= levPtr[0]; --k) acc += Nt[levNodes[k] * stride];
+            rootOut[h0 + hand] = acc;
         }
         // sequenceForm: reach = mass * prob, root level first, lanes over sequences
         if (valid && lane == 0) Vt[0] = 1.0;
@@ -443,7 +456,7 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int q = q0 + u * int(blockDim.x);
-                a[u] = (mode == 1 && q < ne) ? avg[e0 + q] : 0.0;
+                a[u] = (mode == 1 && !noAvg && q < ne) ? avg[e0 + q] : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -453,7 +466,7 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                     xout[e0 + q] = xv;
                     if (mode == 1) {
                         regret[e0 + q] = Rg[sq * stride + hh];
-                        avg[e0 + q] = (a[u] + xv) * shrink;  // solver.hpp:382-386
+                        if (!noAvg) avg[e0 + q] = (a[u] + xv) * shrink;  // solver.hpp:382-386
                     }
                 }
                 hh += dh;
@@ -483,7 +496,8 @@ __global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w,
 
 // bestResponseValue per hand (solver.hpp:304-318): bottom-up max walk.
 __global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
-                                const double* __restrict__ g, int negate, double* __restrict__ handval) {
+                                const double* __restrict__ g, int negate, double* __restrict__ handval,
+                                const double* __restrict__ extra = nullptr) {
     extern __shared__ int32_t Ts[];
     const int tl = 2 * nn + 1;
     for (int q = threadIdx.x; q < tl; q += blockDim.x) Ts[q] = treeBuf[q];
@@ -505,7 +519,8 @@ __global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int
         for (int a = tr.aptr[v]; a < tr.aptr[v + 1]; ++a) {
             const int sq = tr.aseq[a];
             const double gv = negate ? -gh[sq - 1] : gh[sq - 1];
-            const double ev = gv + sv[sq * st];
+            const double cs = extra ? sv[sq * st] + extra[h * n + sq - 1] : sv[sq * st];
+            const double ev = gv + cs;
             if (first || ev > best) best = ev;
             first = false;
         }
@@ -642,7 +657,7 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
         kern<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
                                       hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule,
-                                      dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr);
+                                      dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr);
         KR_CK_LAUNCH();
         s->launches++;
         return;
@@ -676,7 +691,7 @@ void best_response_to(kr_solver* s, int player, const double* opp, double* dst, 
     const unsigned grid = unsigned((s->H[player] + bt - 1) / bt);
     if (grid) {
         k_best_response<<<grid, bt, smem, st>>>(s->d_tree[player], nn, n, s->H[player], s->g, player == 1,
-                                                s->handval);
+                                                s->handval, nullptr);
         KR_CK_LAUNCH();
         s->launches++;
     }
@@ -806,15 +821,15 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 size_t satt = 0;
                 for (int p = 0; p < 2; ++p)
                     satt = std::max(satt, krb::step_smem(s->n[p], s->nt[p], s->nnodes[p], s->na[p]));
-                KR_CK(cudaFuncSetAttribute(krb::k_player_step, cudaFuncAttributeMaxDynamicSharedMemorySize, int(satt)));
+                krb::raise_smem_limit(krb::k_player_step, satt);
                 // one attribute for both players (the final team size)
                 size_t att = 48 * 1024;
                 for (int p = 0; p < 2; ++p)
                     if (s->levelled[p])
                         att = std::max(att, krb::team_smem(s->n[p], s->nnodes[p], 256 / s->team, s->treeLen[p]));
-                KR_CK(cudaFuncSetAttribute(krb::k_player_team<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att)));
-                KR_CK(cudaFuncSetAttribute(krb::k_player_team<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att)));
-                KR_CK(cudaFuncSetAttribute(krb::k_player_team<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att)));
+                krb::raise_smem_limit(krb::k_player_team<2>, att);
+                krb::raise_smem_limit(krb::k_player_team<4>, att);
+                krb::raise_smem_limit(krb::k_player_team<8>, att);
             }
             if (s->H[0] * s->n[0] != e->rows || s->H[1] * s->n[1] != e->cols)
                 throw Fail{KR_INVALID_INPUT, "treeplex x hands does not match the engine dimensions"};
@@ -824,8 +839,7 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
             s->d_flag = krb::dev_alloc<int>(1);
             const int bsm0 = int((2 * s->nnodes[0] + 1 + s->treeLen[0] + 4) * 4 + (s->n[0] + 1) * 128 * 8 + 16);
             const int bsm1 = int((2 * s->nnodes[1] + 1 + s->treeLen[1] + 4) * 4 + (s->n[1] + 1) * 128 * 8 + 16);
-            KR_CK(cudaFuncSetAttribute(krb::k_best_response, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       std::max(bsm0, bsm1)));
+            krb::raise_smem_limit(krb::k_best_response, size_t(std::max(bsm0, bsm1)));
         } catch (...) {
             krb::destroy_solver(s);
             throw;
@@ -1191,5 +1205,366 @@ int kr_solver_best_response(kr_solver* s, int player, const double* opp, int64_t
         *value = total;
     });
 }
+
+}  // extern "C"
+
+// ===================================================================== turn
+// Turn endgames (beyond the reference): a
+// turn betting tree whose continuations t lead into river subgames, one per
+// river card b.  The payoff is block diagonal (the turn fold block and, per
+// continuation, the river boards), so the gradient is one engine product per
+// block; turn and river couple only through the treeplex: river roots hang
+// under sigma_p(t).  One player's half-iteration (the CPU restatement is
+// oracle/turn_oracle.py):
+//   1. river team steps per continuation (regrets, mass-1 strategies, each
+//      river hand's root value; no averaging yet);
+//   2. root values summed over the boards in ascending order per turn hand,
+//      added to the turn sequence sigma_p(t) (k_turn_gather);
+//   3. the turn team step, whose sweep adds those sums after the children;
+//   4. river strategies scaled by the turn reach of sigma_p(t), then
+//      averaged (k_river_scale).
+// With the boards sharded over GPUs, step 2's per-turn-hand sums are the
+// place of the per-iteration allreduce of the north star.
+struct kr_turn_solver {
+    int device = 0;
+    kr_engine* turnEng = nullptr;
+    std::vector<kr_engine*> riverEng;
+    int T = 0, m = 0, nb = 0;
+    int64_t Hr = 0;                                // river hands over all boards
+    struct TreeDev {
+        int32_t* d = nullptr;
+        int len = 0, na = 0, nn = 0, n = 0;
+    };
+    TreeDev turnTree[2];
+    std::vector<TreeDev> riverTree[2];             // [p][t]
+    std::vector<int> sigma[2];                     // [p][t]
+    int64_t* d_boff = nullptr;                     // [nb+1] river-hand offsets per board
+    int32_t* d_r2t = nullptr;                      // [Hr] turn hand of each river hand
+    int32_t* d_t2r = nullptr;                      // [nb*m] river index of a turn hand, -1 = holds b
+    std::vector<int64_t> off[2];                   // vector offsets: [turn | t0 | t1 | ...]
+    double *regret[2] = {nullptr, nullptr}, *avg[2] = {nullptr, nullptr}, *x[2] = {nullptr, nullptr};
+    double *a[2] = {nullptr, nullptr};
+    double *g = nullptr, *root = nullptr, *extra = nullptr, *handval = nullptr, *bval = nullptr;
+    int64_t* d_one = nullptr;                      // {0, m}: one "board" of turn hands for k_board_sums
+    double pot = 0;
+    int64_t launches = 0;
+};
+
+namespace krb {
+namespace {
+
+__global__ void k_turn_gather(const double* __restrict__ root, const int32_t* __restrict__ t2r,
+                              const int64_t* __restrict__ boff, int nb, int m, int nt, int sigma,
+                              double* __restrict__ extra) {
+    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= m) return;
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        const int r = t2r[int64_t(b) * m + h];
+        if (r >= 0) acc += root[boff[b] + r];
+    }
+    extra[int64_t(h) * nt + sigma - 1] += acc;
+}
+
+__global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, const double* __restrict__ xturn,
+                              const int32_t* __restrict__ r2t, int64_t Hr, int nr, int nt, int sigma,
+                              double shrink, int doAvg) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= Hr * nr) return;
+    const int64_t r = q / nr;
+    const double xv = xturn[int64_t(r2t[r]) * nt + sigma - 1] * x[q];
+    x[q] = xv;
+    if (doAvg) avg[q] = (avg[q] + xv) * shrink;  // solver.hpp:382-386
+}
+
+kr_turn_solver::TreeDev make_tree(const kr_treeplex& t) {
+    if (t.n_seq < 1 || t.n_nodes < 1 || !t.node_parent_seq || !t.node_action_ptr || !t.action_seq)
+        throw Fail{KR_INVALID_INPUT, "empty treeplex"};
+    const int na = t.node_action_ptr[t.n_nodes];
+    std::vector<int32_t> buf;
+    buf.insert(buf.end(), t.node_parent_seq, t.node_parent_seq + t.n_nodes);
+    buf.insert(buf.end(), t.node_action_ptr, t.node_action_ptr + t.n_nodes + 1);
+    buf.insert(buf.end(), t.action_seq, t.action_seq + na);
+    bool ok = false;
+    int nlev = 0;
+    append_levels(t, buf, ok, nlev);
+    if (!ok) throw Fail{KR_INVALID_INPUT, "turn solver needs reference-ordered treeplexes"};
+    kr_turn_solver::TreeDev d;
+    d.len = int(buf.size());
+    d.na = na;
+    d.nn = t.n_nodes;
+    d.n = t.n_seq;
+    d.d = dev_alloc<int32_t>(d.len);
+    KR_CK(cudaMemcpy(d.d, buf.data(), 4 * buf.size(), cudaMemcpyHostToDevice));
+    return d;
+}
+
+constexpr int kTurnTeam = 4;
+
+void team_step(kr_turn_solver* s, const kr_turn_solver::TreeDev& T, int64_t H, int mode, const double* g, int negate,
+               double* regret, double* x, double* avg, double pos, double neg, double shrink, int noAvg,
+               double* rootOut, const double* extra, cudaStream_t st) {
+    const int hpb = 256 / kTurnTeam;
+    const unsigned grid = unsigned((H + hpb - 1) / hpb);
+    if (!grid) return;
+    const size_t smem = team_smem(T.n, T.nn, hpb, T.len);
+    k_player_team<kTurnTeam><<<grid, 256, smem, st>>>(mode, T.d, T.nn, T.n, T.na, T.len, H, hpb, g, negate, regret, x,
+                                                      avg, pos, neg, shrink, 0, nullptr, nullptr, noAvg, rootOut,
+                                                      extra);
+    KR_CK_LAUNCH();
+    s->launches++;
+}
+
+// Player p's half-iteration (mode 1) or initial strategy (mode 0).
+void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, double shrink, cudaStream_t st) {
+    const int nt = s->turnTree[p].n;
+    KR_CK(cudaMemsetAsync(s->extra, 0, 8 * size_t(s->m) * nt, st));
+    for (int t = 0; t < s->T; ++t) {
+        const int64_t o = s->off[p][size_t(t) + 1];
+        team_step(s, s->riverTree[p][size_t(t)], s->Hr, mode, s->g + o, p == 1, s->regret[p] + o, s->x[p] + o,
+                  s->avg[p] + o, pos, neg, shrink, 1, mode == 1 ? s->root : nullptr, nullptr, st);
+        if (mode == 1) {
+            k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root, s->d_t2r, s->d_boff, s->nb, s->m,
+                                                                         nt, s->sigma[p][size_t(t)], s->extra);
+            KR_CK_LAUNCH();
+            s->launches++;
+        }
+    }
+    team_step(s, s->turnTree[p], s->m, mode, s->g, p == 1, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, 0,
+              nullptr, mode == 1 ? s->extra : nullptr, st);
+    for (int t = 0; t < s->T; ++t) {
+        const int64_t o = s->off[p][size_t(t) + 1];
+        const int nr = s->riverTree[p][size_t(t)].n;
+        const int64_t n = s->Hr * nr;
+        k_river_scale<<<unsigned((n + 255) / 256), 256, 0, st>>>(s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr,
+                                                                  nr, nt, s->sigma[p][size_t(t)], shrink, mode == 1);
+        KR_CK_LAUNCH();
+        s->launches++;
+    }
+}
+
+void turn_gradient(kr_turn_solver* s, int p, const double* opp, double* g, cudaStream_t st) {
+    const int q = 1 - p;  // opponent's blocks are the inputs
+    if (p == 0) engine_ax(s->turnEng, opp, g, st);
+    else engine_atx(s->turnEng, opp, g, st);
+    for (int t = 0; t < s->T; ++t) {
+        const double* in = opp + s->off[q][size_t(t) + 1];
+        double* out = g + s->off[p][size_t(t) + 1];
+        if (p == 0) engine_ax(s->riverEng[size_t(t)], in, out, st);
+        else engine_atx(s->riverEng[size_t(t)], in, out, st);
+    }
+}
+
+// bestResponseValue of player p against the device strategy opp.
+double turn_br(kr_turn_solver* s, int p, const double* opp, cudaStream_t st) {
+    turn_gradient(s, p, opp, s->g, st);
+    const int nt = s->turnTree[p].n;
+    KR_CK(cudaMemsetAsync(s->extra, 0, 8 * size_t(s->m) * nt, st));
+    const int bt = 128;
+    auto br = [&](const kr_turn_solver::TreeDev& T, int64_t H, const double* g, double* out, const double* extra) {
+        const size_t smem = size_t((2 * T.nn + 1 + T.na + 2) * 4) + size_t(T.n + 1) * bt * 8 + 16;
+        k_best_response<<<unsigned((H + bt - 1) / bt), bt, smem, st>>>(T.d, T.nn, T.n, H, g, p == 1, out, extra);
+        KR_CK_LAUNCH();
+        s->launches++;
+    };
+    for (int t = 0; t < s->T; ++t) {
+        br(s->riverTree[p][size_t(t)], s->Hr, s->g + s->off[p][size_t(t) + 1], s->root, nullptr);
+        k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root, s->d_t2r, s->d_boff, s->nb, s->m, nt,
+                                                                     s->sigma[p][size_t(t)], s->extra);
+        KR_CK_LAUNCH();
+        s->launches++;
+    }
+    br(s->turnTree[p], s->m, s->g, s->handval, s->extra);
+    k_board_sums<<<1, 256, 0, st>>>(s->handval, s->d_one, 1, s->bval, nullptr, 0);
+    KR_CK_LAUNCH();
+    s->launches++;
+    double v = 0;
+    KR_CK(cudaMemcpyAsync(&v, s->bval, 8, cudaMemcpyDeviceToHost, st));
+    KR_CK(cudaStreamSynchronize(st));
+    return v;
+}
+
+void destroy_turn(kr_turn_solver* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    for (int p = 0; p < 2; ++p) {
+        cudaFree(s->turnTree[p].d);
+        for (auto& t : s->riverTree[p]) cudaFree(t.d);
+        cudaFree(s->regret[p]);
+        cudaFree(s->avg[p]);
+        cudaFree(s->x[p]);
+        cudaFree(s->a[p]);
+    }
+    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g, s->root, s->extra, s->handval, s->bval, s->d_one};
+    for (void* q : ps) cudaFree(q);
+    delete s;
+}
+
+}  // namespace
+}  // namespace krb
+
+extern "C" {
+
+int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs, const kr_treeplex* turnTrees,
+                          const kr_treeplex* riverTrees, int m, int nb, const int32_t* mb, const int32_t* riverToTurn,
+                          const int32_t* sigma, double pot, kr_turn_solver** out) {
+    return guarded([&] {
+        if (!turnEng || T < 1 || !riverEngs || !turnTrees || !riverTrees || m < 1 || nb < 1 || !mb || !riverToTurn ||
+            !sigma || !out)
+            throw Fail{KR_INVALID_INPUT, "bad arguments to kr_turn_solver_create"};
+        if (!(pot > 0)) throw Fail{KR_INVALID_INPUT, "pot must be positive"};
+        KR_CK(cudaSetDevice(turnEng->device));
+        auto* s = new kr_turn_solver();
+        try {
+            s->device = turnEng->device;
+            s->turnEng = turnEng;
+            s->T = T;
+            s->m = m;
+            s->nb = nb;
+            s->pot = pot;
+            std::vector<int64_t> boff{0};
+            for (int b = 0; b < nb; ++b) boff.push_back(boff.back() + mb[b]);
+            s->Hr = boff.back();
+            std::vector<int32_t> t2r(size_t(nb) * m, -1);
+            for (int b = 0; b < nb; ++b)
+                for (int64_t r = boff[size_t(b)]; r < boff[size_t(b) + 1]; ++r) {
+                    const int h = riverToTurn[r];
+                    if (h < 0 || h >= m) throw Fail{KR_INVALID_INPUT, "river hand maps outside the turn hands"};
+                    t2r[size_t(b) * m + size_t(h)] = int32_t(r - boff[size_t(b)]);
+                }
+            for (int p = 0; p < 2; ++p) {
+                s->turnTree[p] = krb::make_tree(turnTrees[p]);
+                s->off[p].assign(1, 0);
+                s->off[p].push_back(int64_t(m) * turnTrees[p].n_seq);
+                for (int t = 0; t < T; ++t) {
+                    const kr_treeplex& rt = riverTrees[2 * t + p];
+                    s->riverTree[p].push_back(krb::make_tree(rt));
+                    s->sigma[p].push_back(sigma[2 * t + p]);
+                    if (sigma[2 * t + p] < 1 || sigma[2 * t + p] > turnTrees[p].n_seq)
+                        throw Fail{KR_INVALID_INPUT, "continuation sequence out of range"};
+                    s->off[p].push_back(s->off[p].back() + s->Hr * rt.n_seq);
+                }
+            }
+            // the engines must cover exactly these blocks
+            if (turnEng->rows != s->off[0][1] || turnEng->cols != s->off[1][1])
+                throw Fail{KR_INVALID_INPUT, "turn engine does not match m x n_turn"};
+            for (int t = 0; t < T; ++t) {
+                kr_engine* e = riverEngs[t];
+                if (!e || e->device != s->device || e->rows != s->off[0][size_t(t) + 2] - s->off[0][size_t(t) + 1] ||
+                    e->cols != s->off[1][size_t(t) + 2] - s->off[1][size_t(t) + 1])
+                    throw Fail{KR_INVALID_INPUT, "river engine does not match its continuation block"};
+                s->riverEng.push_back(e);
+            }
+            // the team kernel's shared memory for the largest tree
+            size_t att = 48 * 1024;
+            for (int p = 0; p < 2; ++p) {
+                att = std::max(att, krb::team_smem(s->turnTree[p].n, s->turnTree[p].nn, 256 / krb::kTurnTeam,
+                                                   s->turnTree[p].len));
+                for (auto& rt : s->riverTree[p])
+                    att = std::max(att, krb::team_smem(rt.n, rt.nn, 256 / krb::kTurnTeam, rt.len));
+            }
+            if (att > 220 * 1024) throw Fail{KR_INVALID_INPUT, "treeplex too large for the on-chip solver step"};
+            krb::raise_smem_limit(krb::k_player_team<krb::kTurnTeam>, att);
+            s->d_boff = krb::dev_alloc<int64_t>(int64_t(boff.size()));
+            KR_CK(cudaMemcpy(s->d_boff, boff.data(), 8 * boff.size(), cudaMemcpyHostToDevice));
+            s->d_r2t = krb::dev_alloc<int32_t>(s->Hr);
+            KR_CK(cudaMemcpy(s->d_r2t, riverToTurn, 4 * size_t(s->Hr), cudaMemcpyHostToDevice));
+            s->d_t2r = krb::dev_alloc<int32_t>(int64_t(t2r.size()));
+            KR_CK(cudaMemcpy(s->d_t2r, t2r.data(), 4 * t2r.size(), cudaMemcpyHostToDevice));
+            for (int p = 0; p < 2; ++p) {
+                const int64_t len = s->off[p].back();
+                s->regret[p] = krb::dev_alloc<double>(len);
+                s->avg[p] = krb::dev_alloc<double>(len);
+                s->x[p] = krb::dev_alloc<double>(len);
+                s->a[p] = krb::dev_alloc<double>(len);
+            }
+            s->g = krb::dev_alloc<double>(std::max(s->off[0].back(), s->off[1].back()));
+            s->root = krb::dev_alloc<double>(s->Hr);
+            s->extra = krb::dev_alloc<double>(int64_t(m) * std::max(turnTrees[0].n_seq, turnTrees[1].n_seq));
+            s->handval = krb::dev_alloc<double>(std::max<int64_t>(m, s->Hr));
+            s->bval = krb::dev_alloc<double>(1);
+            const int64_t one[2] = {0, m};
+            s->d_one = krb::dev_alloc<int64_t>(2);
+            KR_CK(cudaMemcpy(s->d_one, one, 16, cudaMemcpyHostToDevice));
+            KR_CK(cudaDeviceSynchronize());
+        } catch (...) {
+            krb::destroy_turn(s);
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int kr_turn_solver_destroy(kr_turn_solver* s) {
+    return guarded([&] { krb::destroy_turn(s); });
+}
+
+int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
+    return guarded([&] {
+        if (!s || !prm || !r) throw Fail{KR_INVALID_INPUT, "null argument to kr_turn_solver_run"};
+        if (prm->max_iters < 1 || prm->checkpoint_every < 1)
+            throw Fail{KR_INVALID_INPUT, "iteration budget and checkpoint period must be positive"};
+        if (prm->rule != KR_RULE_DCFR) throw Fail{KR_INVALID_INPUT, "the turn solver runs DCFR"};
+        KR_CK(cudaSetDevice(s->device));
+        cudaStream_t st = s->turnEng->stream;
+        cudaEvent_t ev0, ev1;
+        KR_CK(cudaEventCreate(&ev0));
+        KR_CK(cudaEventCreate(&ev1));
+        KR_CK(cudaEventRecord(ev0, st));
+        for (int p = 0; p < 2; ++p) {
+            KR_CK(cudaMemsetAsync(s->regret[p], 0, 8 * size_t(s->off[p].back()), st));
+            KR_CK(cudaMemsetAsync(s->avg[p], 0, 8 * size_t(s->off[p].back()), st));
+        }
+        krb::turn_player(s, 0, 0, 0, 0, 0, st);  // sequenceForm of zero regrets (solver.hpp:363-364)
+        krb::turn_player(s, 1, 0, 0, 0, 0, st);
+        double ws = 0;
+        r->trace_len = 0;
+        for (int t = 1; t <= prm->max_iters; ++t) {
+            const double pos = krb::discount_factor(t, prm->alpha), neg = krb::discount_factor(t, prm->beta);
+            const double shrink = std::pow(double(t) / (t + 1), prm->gamma);
+            krb::turn_gradient(s, 0, s->x[1], s->g, st);        // g1 = A x2
+            krb::turn_player(s, 0, 1, pos, neg, shrink, st);
+            krb::turn_gradient(s, 1, s->x[0], s->g, st);        // A^T x1 (negated in the steps)
+            krb::turn_player(s, 1, 1, pos, neg, shrink, st);
+            ws += 1;
+            ws *= shrink;
+            if (t % prm->checkpoint_every == 0 || t == prm->max_iters) {
+                for (int p = 0; p < 2; ++p) {
+                    const int64_t len = s->off[p].back();
+                    krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, ws, s->a[p],
+                                                                                  nullptr, nullptr);
+                    KR_CK_LAUNCH();
+                }
+                const double br1 = krb::turn_br(s, 0, s->a[1], st), br2 = krb::turn_br(s, 1, s->a[0], st);
+                const double expl = (br1 + br2) / 2 / s->pot;
+                const int i = r->trace_len;
+                if (i < r->trace_cap) {
+                    if (r->trace_iter) r->trace_iter[i] = t;
+                    if (r->trace_expl) r->trace_expl[i] = expl;
+                    if (r->trace_br1) r->trace_br1[i] = br1;
+                    if (r->trace_br2) r->trace_br2[i] = br2;
+                }
+                r->trace_len = i + 1;
+                r->iterations = t;
+                r->exploitability = expl;
+                if (prm->target_exploitability > 0 && expl <= prm->target_exploitability) break;
+            }
+        }
+        KR_CK(cudaEventRecord(ev1, st));
+        KR_CK(cudaEventSynchronize(ev1));
+        float ms = 0;
+        KR_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        r->seconds = ms / 1e3;
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        for (int p = 0; p < 2; ++p) {
+            double* dst = p == 0 ? r->avg1 : r->avg2;
+            if (dst) KR_CK(cudaMemcpy(dst, s->a[p], 8 * size_t(s->off[p].back()), cudaMemcpyDeviceToHost));
+        }
+        r->gradient_flops = 0;
+    });
+}
+
+int64_t kr_turn_solver_launches(const kr_turn_solver* s) { return s ? s->launches : 0; }
 
 }  // extern "C"

@@ -1445,6 +1445,47 @@ int krh_instance_builtin(const char* name, uint64_t seed, int hands, int shared,
 
 void krh_instance_free(krh_instance* h) { delete h; }
 
+int krh_instance_custom(const int32_t board[5], int deck, const uint8_t* cards1, const double* w1, int m1,
+                        const uint8_t* cards2, const double* w2, int m2, double stack, double pot,
+                        const double* menu, int nmenu, int all_in, int raise_cap, krh_instance** out) {
+    return guard([&] {
+        if (!board || !out || m1 < 0 || m2 < 0 || nmenu < 0 || (nmenu && !menu))
+            throw krh::Error{krh::INVALID_INPUT, "bad arguments to krh_instance_custom"};
+        std::vector<int> dk;
+        if (deck == 26) {
+            for (int r = 0; r < 13; ++r)
+                for (int q = 0; q < 2; ++q) dk.push_back(r * 4 + q);
+        } else if (deck == 52) {
+            dk = krh::standardDeck();
+        } else {
+            throw krh::Error{krh::INVALID_INPUT, "deck must be 52 or 26"};
+        }
+        std::array<int, 5> bd{};
+        for (int i = 0; i < 5; ++i) {
+            if (board[i] < 0 || board[i] >= 52) throw krh::Error{krh::INVALID_INPUT, "board card out of range"};
+            bd[size_t(i)] = board[i];
+        }
+        auto hands = [](const uint8_t* c, int m) {
+            std::vector<krh::Hand> h;
+            for (int i = 0; i < m; ++i) {
+                if (c[2 * i] >= 52 || c[2 * i + 1] >= 52 || c[2 * i] == c[2 * i + 1])
+                    throw krh::Error{krh::INVALID_INPUT, "bad hand cards"};
+                h.push_back(krh::Hand::of(c[2 * i], c[2 * i + 1]));
+            }
+            return h;
+        };
+        krh::BettingConfig cfg;
+        cfg.stack1 = cfg.stack2 = stack;
+        cfg.pot = pot;
+        for (int p = 0; p < 2; ++p)
+            for (auto& m : cfg.menu[p]) m.assign(menu, menu + nmenu);
+        cfg.allIn = all_in != 0;
+        if (raise_cap >= 0) cfg.raiseCap = raise_cap;
+        *out = new krh_instance{krh::makeInstance(bd, dk, hands(cards1, m1), std::vector<double>(w1, w1 + m1),
+                                                  hands(cards2, m2), std::vector<double>(w2, w2 + m2), cfg)};
+    });
+}
+
 int krh_instance_dims(const krh_instance* h, int64_t out[16]) {
     return guard([&] {
         const auto& in = h->in;

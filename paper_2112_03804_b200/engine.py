@@ -50,13 +50,19 @@ class CudaEngine:
         computed from each board's F, S, strength keys, cards and lambdas with
         nothing materialised.  `instances` is one
         host.Instance or a list of them sharing one betting tree."""
-        L = N.cuda()
         insts = instances if isinstance(instances, (list, tuple)) else [instances]
-        arr = (N.kr_kron_board * len(insts))(*[i.kron_view() for i in insts])
+        return cls.from_kron_boards([i.kron_view() for i in insts], device, flags)
+
+    @classmethod
+    def from_kron_boards(cls, boards, device=0, flags=0):
+        """Implicit engine from kr_kron_board structs (the caller keeps the
+        arrays they point to alive until this returns: the engine copies)."""
+        L = N.cuda()
+        arr = (N.kr_kron_board * len(boards))(*boards)
         h = C.c_void_p()
-        N.check(L.kr_engine_create_kron(arr, len(insts), device, flags, C.byref(h)))
+        N.check(L.kr_engine_create_kron(arr, len(boards), device, flags, C.byref(h)))
         self = cls.__new__(cls)
-        self._attach(h, device, len(insts))
+        self._attach(h, device, len(boards))
         self.implicit = True
         return self
 

@@ -26,7 +26,7 @@ HOST_SYMBOLS = [
     "krh_instance_pot", "krh_instance_hands", "krh_instance_vectors", "krh_instance_treeplex", "krh_dense_nnz",
     "krh_sparsify", "krh_postprocess", "krh_factors_from_arrays", "krh_factors_free", "krh_factors_dims",
     "krh_factors_view", "krh_factors_validate", "krh_bundle_write", "krh_bundle_read", "krh_last_error",
-    "krh_instance_kron_view",
+    "krh_instance_kron_view", "krh_instance_custom",
 ]
 
 
@@ -57,6 +57,9 @@ def host():
         L.krh_instance_vectors.argtypes = [C.c_void_p] + [C.c_void_p] * 4
         L.krh_instance_treeplex.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         L.krh_instance_kron_view.argtypes = [C.c_void_p, C.POINTER(N.kr_kron_board)]
+        L.krh_instance_custom.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(C.c_void_p)]
         L.krh_sparsify.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.krh_postprocess.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
         L.krh_factors_from_arrays.argtypes = [C.POINTER(N.kr_factors), C.c_int, C.c_int, C.POINTER(C.c_void_p)]
@@ -219,6 +222,23 @@ class Factors:
 def builtin(name, seed=1, hands=0, shared=0, board="", deck=52, tree=1):
     out = C.c_void_p()
     _check(host().krh_instance_builtin(name.encode(), seed, hands, shared, board.encode(), deck, tree, C.byref(out)))
+    return Instance(out.value)
+
+
+def custom_instance(board, deck, cards1, w1, cards2, w2, stack, pot, menu, all_in=True, raise_cap=-1):
+    """krh_instance_custom: a river instance from explicit pieces.  board: 5
+    card ids; cards*: (m, 2) uint8 card ids; w*: belief weights; menu: pot
+    fractions used in every betting context by both players."""
+    b = np.ascontiguousarray(board, np.int32)
+    c1 = np.ascontiguousarray(cards1, np.uint8).reshape(-1, 2)
+    c2 = np.ascontiguousarray(cards2, np.uint8).reshape(-1, 2)
+    w1 = np.ascontiguousarray(w1, np.float64)
+    w2 = np.ascontiguousarray(w2, np.float64)
+    mn = np.ascontiguousarray(menu, np.float64)
+    out = C.c_void_p()
+    _check(host().krh_instance_custom(N.ptr(b), deck, N.ptr(c1), N.ptr(w1), len(c1), N.ptr(c2), N.ptr(w2), len(c2),
+                                      float(stack), float(pot), N.ptr(mn), len(mn), int(all_in), int(raise_cap),
+                                      C.byref(out)))
     return Instance(out.value)
 
 

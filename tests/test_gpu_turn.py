@@ -1,0 +1,58 @@
+"""Turn endgames on the B200 (kr_turn_solver, implicit Kronecker engines per
+block) against the CPU checker oracle/turn_oracle.py.
+
+Tolerances: the products differ from the checker's dense block formula only by
+summation order, so they are held to 1e-12 normwise.  The solver composes the
+same per-node arithmetic, so its best-response trace is held to 1e-9 relative
+over the first iterations (before DCFR's chaotic amplification of rounding,
+DESIGN.md §2, can act), and the solve must converge."""
+import numpy as np
+import pytest
+
+import turn_oracle as TO
+from paper_2112_03804_b200.turn import TurnGame, TurnSolver
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def game():
+    return TurnGame()
+
+
+def normwise(got, exp):
+    return np.abs(got - exp).max() / (1 + np.abs(exp).max())
+
+
+def test_turn_products_match_checker(game):
+    import torch
+    s = TurnSolver(game)
+    o = TO.TurnOracle(game)
+    rng = np.random.default_rng(5)
+    x2, y1 = rng.standard_normal(game.size[1]), rng.standard_normal(game.size[0])
+    got_ax = np.concatenate([s.turn_eng.Ax(x2[:game.off[1][0]])] +
+                            [e.Ax(x2[game.off[1][t]:game.off[1][t + 1]]) for t, e in enumerate(s.river_eng)])
+    got_atx = np.concatenate([s.turn_eng.ATx(y1[:game.off[0][0]])] +
+                             [e.ATx(y1[game.off[0][t]:game.off[0][t + 1]]) for t, e in enumerate(s.river_eng)])
+    assert normwise(got_ax, o.ax(x2)) <= 1e-12
+    assert normwise(got_atx, o.atx(y1)) <= 1e-12
+
+
+def test_turn_dcfr_matches_checker(game):
+    o = TO.TurnOracle(game)
+    trace, (a1, a2) = o.dcfr(6, checkpoint_every=1)
+    r = TurnSolver(game).run(max_iters=6, checkpoint_every=1, want_avg=True)
+    assert r["iterations"] == 6
+    ob1 = np.array([b for _, b, _, _ in trace])
+    ob2 = np.array([b for _, _, b, _ in trace])
+    np.testing.assert_allclose(r["trace_br1"], ob1, rtol=1e-9)
+    np.testing.assert_allclose(r["trace_br2"], ob2, rtol=1e-9)
+    np.testing.assert_allclose(r["trace_expl"], [e for *_, e in trace], rtol=1e-9)
+    assert normwise(r["avg1"], a1) <= 1e-9 and normwise(r["avg2"], a2) <= 1e-9
+
+
+def test_turn_dcfr_converges(game):
+    r = TurnSolver(game).run(max_iters=300, checkpoint_every=50)
+    e = r["trace_expl"]
+    assert len(e) == 6 and 0 < e[-1] < 0.05 * e[0]
+    assert np.all(np.diff(e) < 0)
