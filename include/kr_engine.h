@@ -264,6 +264,14 @@ int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs
 int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* p, kr_dcfr_result* r);
 int kr_turn_solver_destroy(kr_turn_solver* s);
 int64_t kr_turn_solver_launches(const kr_turn_solver* s);
+/* Board sharding over ranks: each rank's solver holds the turn block and its
+ * own boards.  fn(user) is called (stream synchronised) after the river steps
+ * of every half-iteration and of every best response, and must sum the turn
+ * values buffer `extra` (device, sizes[2] doubles, owned by the caller from
+ * now on) over the ranks in place: the one allreduce per half-iteration. */
+int kr_turn_solver_set_exchange(kr_turn_solver* s, void (*fn)(void*), void* user, double* extra);
+/* rows of player 1's vector, of player 2's, turn-values buffer length, river hands */
+int kr_turn_solver_sizes(const kr_turn_solver* s, int64_t out[4]);
 
 /* Per-kernel CUDA-event timing of the engine's SpMV launches (off by
  * default).  When enabled every SpMV launch is bracketed by events on the

@@ -99,7 +99,7 @@ CUDA_SYMBOLS = [
     "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
     "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times", "kr_engine_create_kron",
     "kr_solver_set_rule", "kr_turn_solver_create", "kr_turn_solver_run", "kr_turn_solver_destroy",
-    "kr_turn_solver_launches",
+    "kr_turn_solver_launches", "kr_turn_solver_set_exchange", "kr_turn_solver_sizes",
 ]
 
 
@@ -161,6 +161,8 @@ def cuda():
         L.kr_turn_solver_destroy.argtypes = [C.c_void_p]
         L.kr_turn_solver_launches.restype = C.c_int64
         L.kr_turn_solver_launches.argtypes = [C.c_void_p]
+        L.kr_turn_solver_set_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kr_turn_solver_sizes.argtypes = [C.c_void_p, C.c_void_p]
         L.kr_engine_set_timing.argtypes = [C.c_void_p, C.c_int]
         L.kr_engine_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _CUDA = L

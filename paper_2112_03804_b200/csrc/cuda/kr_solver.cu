@@ -1248,6 +1248,13 @@ struct kr_turn_solver {
     int64_t* d_one = nullptr;                      // {0, m}: one "board" of turn hands for k_board_sums
     double pot = 0;
     int64_t launches = 0;
+    // board sharding: after the river steps of a half-iteration (and of a
+    // best response) the per-turn-hand river values in `extra` cover this
+    // rank's boards only; exchange(user) must sum them over the ranks in place
+    // (the per-iteration allreduce), the stream having been synchronised.
+    void (*exchange)(void*) = nullptr;
+    void* user = nullptr;
+    bool ownExtra = true;
 };
 
 namespace krb {
@@ -1330,6 +1337,10 @@ void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, dou
             s->launches++;
         }
     }
+    if (mode == 1 && s->exchange) {
+        KR_CK(cudaStreamSynchronize(st));
+        s->exchange(s->user);
+    }
     team_step(s, s->turnTree[p], s->m, mode, s->g, p == 1, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, 0,
               nullptr, mode == 1 ? s->extra : nullptr, st);
     for (int t = 0; t < s->T; ++t) {
@@ -1374,6 +1385,10 @@ double turn_br(kr_turn_solver* s, int p, const double* opp, cudaStream_t st) {
         KR_CK_LAUNCH();
         s->launches++;
     }
+    if (s->exchange) {
+        KR_CK(cudaStreamSynchronize(st));
+        s->exchange(s->user);
+    }
     br(s->turnTree[p], s->m, s->g, s->handval, s->extra);
     k_board_sums<<<1, 256, 0, st>>>(s->handval, s->d_one, 1, s->bval, nullptr, 0);
     KR_CK_LAUNCH();
@@ -1395,8 +1410,9 @@ void destroy_turn(kr_turn_solver* s) {
         cudaFree(s->x[p]);
         cudaFree(s->a[p]);
     }
-    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g, s->root, s->extra, s->handval, s->bval, s->d_one};
+    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g, s->root, s->handval, s->bval, s->d_one};
     for (void* q : ps) cudaFree(q);
+    if (s->ownExtra) cudaFree(s->extra);
     delete s;
 }
 
@@ -1566,5 +1582,29 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
 }
 
 int64_t kr_turn_solver_launches(const kr_turn_solver* s) { return s ? s->launches : 0; }
+
+int kr_turn_solver_set_exchange(kr_turn_solver* s, void (*fn)(void*), void* user, double* extra) {
+    return guarded([&] {
+        if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
+        if (fn && !extra) throw Fail{KR_INVALID_INPUT, "an exchange needs the caller's turn-values buffer"};
+        if (extra) {
+            if (s->ownExtra) cudaFree(s->extra);
+            s->extra = extra;
+            s->ownExtra = false;
+        }
+        s->exchange = fn;
+        s->user = user;
+    });
+}
+
+int kr_turn_solver_sizes(const kr_turn_solver* s, int64_t out[4]) {
+    return guarded([&] {
+        if (!s || !out) throw Fail{KR_INVALID_INPUT, "null argument"};
+        out[0] = s->off[0].back();
+        out[1] = s->off[1].back();
+        out[2] = int64_t(s->m) * std::max(s->turnTree[0].n, s->turnTree[1].n);  // turn-values buffer
+        out[3] = s->Hr;
+    });
+}
 
 }  // extern "C"

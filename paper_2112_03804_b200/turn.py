@@ -51,11 +51,14 @@ class TurnGame:
     """Host-side description of a turn endgame (see the module docstring)."""
 
     def __init__(self, turn="Kc9d7c4d", deck=26, seed=1, stack=18125.0, pot=1875.0, turn_menu=(0.5,),
-                 turn_raise_cap=1, river_menu=(0.5, 1.0), river_raise_cap=1):
+                 turn_raise_cap=1, river_menu=(0.5, 1.0), river_raise_cap=1, boards=None):
+        """boards: indices of the river cards this object holds (a rank's
+        contiguous shard, dist.shard); default all."""
         self.deck = deck
         self.turn = [card_id(turn[i:i + 2]) for i in range(0, 8, 2)]
         cards = [c for c in deck_cards(deck) if c not in self.turn]
-        self.rivers = cards                                  # board cards b, ascending id
+        self.all_rivers = cards
+        self.rivers = cards if boards is None else [cards[i] for i in boards]  # board cards b, ascending id
         self.K = len(cards) - 4                              # river cards left given two hands
         self.hands = np.array([(max(a, b), min(a, b)) for a, b in itertools.combinations(cards, 2)], np.uint8)
         self.m = len(self.hands)
@@ -193,7 +196,11 @@ class TurnSolver:
     engines for the turn block and each continuation's river boards, the
     turn treeplex composed with the river treeplexes."""
 
-    def __init__(self, game: TurnGame, device=0):
+    def __init__(self, game: TurnGame, device=0, group=None):
+        """group: a torch.distributed process group over the ranks holding the
+        other board shards (each rank builds its TurnGame with boards=shard):
+        the per-turn-hand river values are all-reduced once per
+        half-iteration."""
         import ctypes as C
 
         from . import _native as N
@@ -220,12 +227,27 @@ class TurnSolver:
                                                len(game.rivers), N.ptr(mb), N.ptr(r2t), N.ptr(sig), 2 * game.pot,
                                                C.byref(h)))
         self._h = h
+        if group is not None:
+            import torch
+            import torch.distributed as dist
+            sz = np.zeros(4, np.int64)
+            N.check(N.cuda().kr_turn_solver_sizes(self._h, N.ptr(sz)))
+            self.extra = torch.zeros(int(sz[2]), dtype=torch.float64, device=torch.device("cuda", device))
+
+            def exchange(_user):
+                dist.all_reduce(self.extra, group=group)
+                torch.cuda.synchronize(self.extra.device)
+
+            self._cb = C.CFUNCTYPE(None, C.c_void_p)(exchange)
+            N.check(N.cuda().kr_turn_solver_set_exchange(self._h, C.cast(self._cb, C.c_void_p), None,
+                                                         C.c_void_p(self.extra.data_ptr())))
 
     def close(self):
         from . import _native as N
         if getattr(self, "_h", None) and self._h.value:
             N.cuda().kr_turn_solver_destroy(self._h)
             self._h = None
+        self.extra = None
 
     def __del__(self):
         try:

@@ -56,3 +56,37 @@ def test_turn_dcfr_converges(game):
     e = r["trace_expl"]
     assert len(e) == 6 and 0 < e[-1] < 0.05 * e[0]
     assert np.all(np.diff(e) < 0)
+
+
+def _rank(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+    from paper_2112_03804_b200.dist import shard
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = TurnGame(boards=list(shard(22, rank, world)))
+        r = TurnSolver(g, group=dist.group.WORLD).run(max_iters=6, checkpoint_every=1)
+        q.put((rank, r["trace_br1"].tolist(), r["trace_br2"].tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_turn_boards_sharded_over_two_ranks(game):
+    """Boards split over two ranks (one GPU, host collectives: no kernel waits
+    on another rank): one allreduce of the turn values per half-iteration
+    reproduces the single-rank trace (summation grouping differs: 1e-9)."""
+    import torch.multiprocessing as mp
+    ref = TurnSolver(game).run(max_iters=6, checkpoint_every=1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_rank, args=(r, 2, 29613, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, b1, b2 in out:
+        np.testing.assert_allclose(b1, ref["trace_br1"], rtol=1e-9)
+        np.testing.assert_allclose(b2, ref["trace_br2"], rtol=1e-9)
