@@ -175,6 +175,29 @@ def oracle_boards(indices, threads, with_instances=False):
         return list(ex.map(one, indices))
 
 
+def run_turn(rank, world, local, max_over_ranks, group):
+    """Turn endgame: the 52-card turn
+    Ks7d4c2h with a betting round (menus {0.5}, no raise) above its 48 river
+    boards (menus {0.5, 1.0}, one raise), 1,128 hands per side; boards sharded
+    over the ranks, one allreduce of the turn values per half-iteration."""
+    from paper_2112_03804_b200.dist import shard
+    from paper_2112_03804_b200.turn import TurnGame, TurnSolver
+    t0 = time.time()
+    g = TurnGame(turn=TURN, deck=52, boards=list(shard(NBOARDS, rank, world)))
+    s = TurnSolver(g, device=local, group=group if world > 1 else None)
+    setup = time.time() - t0
+    s.run(max_iters=3, checkpoint_every=3)  # warm
+    r = s.run(max_iters=200, checkpoint_every=50)
+    secs = max_over_ranks(r["seconds"])
+    return {"workload": f"turn {TURN}: betting round (menus {{0.5}}, no raise) above 48 river boards "
+                        "(menus {0.5, 1.0}, one raise), 1,128 hands per side, 3 continuations",
+            "sequences_per_player_this_rank": int(g.size[0]),
+            "iterations": r["iterations"], "device_seconds": secs, "iters_per_s": r["iterations"] / secs,
+            "exploitability": r["exploitability"], "setup_s": round(setup, 2),
+            "collective": "one allreduce (m x n_turn doubles) per half-iteration and per best response"
+            if world > 1 else "none (one GPU)"}
+
+
 def config1_gpu():
     """BASELINE config 1: the parity game (twenty_card plays the Leduc role,
     SURVEY.md §7), Kronecker sparsification + 1000 CFR+ iterations in fp64,
@@ -416,6 +439,7 @@ def run_product(args):
     # ---- implicit Kronecker engine (K7) -------------
     implicit = run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
                             sum_over_ranks)
+    turn = run_turn(rank, world, local, max_over_ranks, dist.group.WORLD if world > 1 else None)
     config1 = config1_gpu() if rank == 0 else None
 
     if rank != 0:
@@ -453,6 +477,7 @@ def run_product(args):
         "clocks": sampler.summary(),
         "implicit": implicit,
         "config1": {k: v for k, v in config1.items() if not k.startswith("_")},
+        "turn": turn,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds)
