@@ -93,6 +93,17 @@ typedef struct {
  * to rounding (summation order differs); flops() counts its multiply-adds. */
 int kr_engine_create_kron(const kr_kron_board* boards, int nboards, int device, uint32_t flags, kr_engine** out);
 
+/* Technique B with postprocessing (sparsify.hpp:246-406) built ON THE DEVICE
+ * from one board's KronPayoff pieces, bit-exact against
+ * the host builder, downloaded into host arrays in the reference's storage
+ * order (view: valid while f lives; usable with kr_engine_create).  seconds:
+ * device time of the build (CUDA events, downloads included). */
+typedef struct kr_devfactors kr_devfactors;
+int kr_factors_build_device(const kr_kron_board* b, int device, kr_devfactors** out);
+int kr_devfactors_view(const kr_devfactors* f, kr_factors* out);
+double kr_devfactors_seconds(const kr_devfactors* f);
+void kr_devfactors_free(kr_devfactors* f);
+
 /* Create an engine for one Sparsification on CUDA device `device`.
  * Replaces FactoredEngine(const Sparsification&) (solver.hpp:32); the
  * factors are copied to HBM, so the caller may free them afterwards. */

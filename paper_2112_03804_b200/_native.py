@@ -100,6 +100,7 @@ CUDA_SYMBOLS = [
     "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times", "kr_engine_create_kron",
     "kr_solver_set_rule", "kr_turn_solver_create", "kr_turn_solver_run", "kr_turn_solver_destroy",
     "kr_turn_solver_launches", "kr_turn_solver_set_exchange", "kr_turn_solver_sizes",
+    "kr_factors_build_device", "kr_devfactors_view", "kr_devfactors_seconds", "kr_devfactors_free",
 ]
 
 
@@ -163,6 +164,11 @@ def cuda():
         L.kr_turn_solver_launches.argtypes = [C.c_void_p]
         L.kr_turn_solver_set_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.kr_turn_solver_sizes.argtypes = [C.c_void_p, C.c_void_p]
+        L.kr_factors_build_device.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.POINTER(C.c_void_p)]
+        L.kr_devfactors_view.argtypes = [C.c_void_p, C.POINTER(kr_factors)]
+        L.kr_devfactors_seconds.restype = C.c_double
+        L.kr_devfactors_seconds.argtypes = [C.c_void_p]
+        L.kr_devfactors_free.argtypes = [C.c_void_p]
         L.kr_engine_set_timing.argtypes = [C.c_void_p, C.c_int]
         L.kr_engine_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _CUDA = L

@@ -133,6 +133,11 @@ class Instance:
         _check(host().krh_instance_kron_view(self._h, C.byref(v)))
         return v
 
+    def sparsify_device(self, device=0):
+        """Technique B with postprocessing built on the device
+        (kr_factors_build_device), bit-exact against sparsify("b", True)."""
+        return DeviceFactors(self, device)
+
     def dense_nnz(self):
         """densePayoffNonzeros (kron.hpp:198-207)."""
         return int(host().krh_dense_nnz(self._h))
@@ -217,6 +222,41 @@ class Factors:
         _check(host().krh_factors_from_arrays(C.byref(kf), 0 if technique == "a" else 1, int(postprocessed),
                                               C.byref(out)))
         return cls(out.value)
+
+
+class DeviceFactors:
+    """Factors built on the device (kr_factors_build_device), held as host
+    copies; the same interface as Factors for engines and comparisons."""
+
+    NAMES = Factors.NAMES
+
+    def __init__(self, inst, device=0):
+        v = inst.kron_view()
+        out = C.c_void_p()
+        N.check(N.cuda().kr_factors_build_device(C.byref(v), device, C.byref(out)))
+        self._h = out
+        fv = N.kr_factors()
+        N.check(N.cuda().kr_devfactors_view(self._h, C.byref(fv)))
+        self._v = fv
+        self.rows, self.cols, self.k = int(fv.rows), int(fv.cols), int(fv.k)
+        self.seconds = N.cuda().kr_devfactors_seconds(self._h)
+        self.nnz = {}
+        for n in self.NAMES:
+            c = getattr(fv, n)
+            self.nnz[n] = int(np.ctypeslib.as_array(C.cast(c.outer, C.POINTER(C.c_int64)), (c.outer_size + 1,))[-1])
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            N.cuda().kr_devfactors_free(self._h)
+            self._h = C.c_void_p()
+
+    def size(self):
+        return sum(self.nnz.values())
+
+    def view(self):
+        return self._v
+
+    factors = Factors.factors
 
 
 def builtin(name, seed=1, hands=0, shared=0, board="", deck=52, tree=1):
