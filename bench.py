@@ -45,7 +45,7 @@ NBOARDS = 48
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=800)  # ~1 s timed: several nvidia-smi clock samples
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["product", "reference"], default="product")
     p.add_argument("--boards", type=int, default=NBOARDS)
