@@ -12,7 +12,8 @@ are the river continuations t, each reached by one sequence pair (sigma1(t),
 sigma2(t)) with both players' contribution c_t (the S entry).  Continuation t
 deals the river card b uniformly among the cards not on the board and not in
 either hand (1/44 with the 52-card deck) and plays the river subgame built
-from (stack - (c_t - pot), c_t) with the river menus.
+from (stack - (c_t - pot), c_t) with the river menus; after an all-in call
+(no stack left) that subgame is a check-check showdown at stakes c_t.
 
 Payoff.  With pi_ij = lambda1_i lambda2_j [i, j disjoint]:
   turn block   A[(i, s1), (j, s2)] = pi_ij F_turn[s1, s2]
@@ -51,7 +52,7 @@ class TurnGame:
     """Host-side description of a turn endgame (see the module docstring)."""
 
     def __init__(self, turn="Kc9d7c4d", deck=26, seed=1, stack=18125.0, pot=1875.0, turn_menu=(0.5,),
-                 turn_raise_cap=1, river_menu=(0.5, 1.0), river_raise_cap=1, boards=None):
+                 turn_raise_cap=1, river_menu=(0.5, 1.0), river_raise_cap=1, boards=None, turn_all_in=False):
         """boards: indices of the river cards this object holds (a rank's
         contiguous shard, dist.shard); default all."""
         self.deck = deck
@@ -78,8 +79,8 @@ class TurnGame:
         h1 = free[0]
         h2 = next(h for h in free if not set(h.tolist()) & set(h1.tolist()))
         self.turn_inst = H.custom_instance(self.turn + [dummy], deck, np.array([h1], np.uint8), [1.0],
-                                           np.array([h2], np.uint8), [1.0], stack, pot, list(turn_menu), False,
-                                           turn_raise_cap)
+                                           np.array([h2], np.uint8), [1.0], stack, pot, list(turn_menu),
+                                           turn_all_in, turn_raise_cap)
         v = self.turn_inst.kron_view()
         self.n_turn = (v.n1, v.n2)
         self.F_turn = _csr(v.F, v.n2)
@@ -94,9 +95,13 @@ class TurnGame:
             for bi, b in enumerate(self.rivers):
                 keep = np.array([b not in h for h in self.hands])
                 idx = np.flatnonzero(keep)
+                left = stack - (c - pot)
+                if left > 0:
+                    cfg = (left, c, self.river_menu, True, river_raise_cap)
+                else:  # all-in on the turn: no river betting, a showdown at stakes c (check-check)
+                    cfg = (1.0, c, [], False, 0)
                 inst = H.custom_instance(self.turn + [b], deck, self.hands[idx], self.mu[0][idx], self.hands[idx],
-                                         self.mu[1][idx], stack - (c - pot), c, self.river_menu, True,
-                                         river_raise_cap)
+                                         self.mu[1][idx], *cfg)
                 if ti == 0:
                     code = {tuple(sorted(h)): i for i, h in enumerate(self.hands.tolist())}
                     self.order.append(np.array([code[tuple(sorted((card_id(s[:2]), card_id(s[2:]))))]

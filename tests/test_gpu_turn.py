@@ -90,3 +90,16 @@ def test_turn_boards_sharded_over_two_ranks(game):
     for rank, b1, b2 in out:
         np.testing.assert_allclose(b1, ref["trace_br1"], rtol=1e-9)
         np.testing.assert_allclose(b2, ref["trace_br2"], rtol=1e-9)
+
+
+def test_turn_with_raises_and_all_in():
+    """A richer turn tree (two bet sizes, a raise, all-in; 5 continuations, two
+    of them all-in calls whose river is a check-check showdown) matches the
+    checker's trace."""
+    g = TurnGame(turn_menu=(0.5, 1.0), turn_raise_cap=1, turn_all_in=True, stack=3000.0)
+    assert len(g.conts) == 5 and sorted(n[0] for n in g.n_river) == [1, 1, 4, 4, 7]
+    o = TO.TurnOracle(g)
+    trace, _ = o.dcfr(4, checkpoint_every=1)
+    r = TurnSolver(g).run(max_iters=4, checkpoint_every=1)
+    np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-9)
+    np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-9)

@@ -64,3 +64,12 @@ def test_composed_dcfr_converges(game):
     # the averages are sequence-form strategies: the turn block of each hand
     # sums to one over the root node's actions
     assert np.allclose(a1[:game.m * 4].reshape(game.m, 4)[:, :2].sum(axis=1), 1.0)
+
+
+def test_all_in_continuations_are_check_check_showdowns():
+    g = TurnGame(turn_menu=(0.5, 1.0), turn_raise_cap=1, turn_all_in=True, stack=3000.0)
+    allin = [t for t, (_, _, c) in enumerate(g.conts) if 3000.0 - (c - g.pot) <= 0]
+    assert allin and all(g.n_river[t] == (1, 1) for t in allin)
+    for t in allin:  # one forced check each, the showdown at the continuation's stakes
+        pc = g.kron_pieces(t)[0]
+        assert pc["S"].shape == (1, 1) and pc["S"][0, 0] == g.conts[t][2] and not pc["F"].any()
