@@ -103,3 +103,19 @@ def test_turn_with_raises_and_all_in():
     r = TurnSolver(g).run(max_iters=4, checkpoint_every=1)
     np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-9)
     np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-9)
+
+
+def test_52_card_turn_blocks_match_checker():
+    """The 52-card turn (1,128 hands) on a shard of 4 river boards: every
+    block's K7 product against the checker's block formula."""
+    g = TurnGame(turn="Ks7d4c2h", deck=52, boards=[0, 13, 30, 47])
+    assert g.m == 1128 and g.K == 44 and all(mb == 1081 for mb in g.mb)
+    s, o = TurnSolver(g), TO.TurnOracle(g)
+    rng = np.random.default_rng(9)
+    x2, y1 = rng.standard_normal(g.size[1]), rng.standard_normal(g.size[0])
+    got_ax = np.concatenate([s.turn_eng.Ax(x2[:g.off[1][0]])] +
+                            [e.Ax(x2[g.off[1][t]:g.off[1][t + 1]]) for t, e in enumerate(s.river_eng)])
+    got_atx = np.concatenate([s.turn_eng.ATx(y1[:g.off[0][0]])] +
+                             [e.ATx(y1[g.off[0][t]:g.off[0][t + 1]]) for t, e in enumerate(s.river_eng)])
+    assert normwise(got_ax, o.ax(x2)) <= 1e-12
+    assert normwise(got_atx, o.atx(y1)) <= 1e-12
