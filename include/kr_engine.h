@@ -104,6 +104,14 @@ int kr_devfactors_view(const kr_devfactors* f, kr_factors* out);
 double kr_devfactors_seconds(const kr_devfactors* f);
 void kr_devfactors_free(kr_devfactors* f);
 
+/* The factored engine (Technique B with postprocessing) built entirely on the
+ * device from the boards' KronPayoff pieces: factors generated row by row into
+ * the engine's layout, no factor arrays and no layout work on the host
+ * (SURVEY.md 8(f) row 3).  Products are bitwise those of kr_engine_create on
+ * the host builder's factors. */
+int kr_engine_create_device_b(const kr_kron_board* boards, int nboards, int device, uint32_t flags,
+                              kr_engine** out);
+
 /* Create an engine for one Sparsification on CUDA device `device`.
  * Replaces FactoredEngine(const Sparsification&) (solver.hpp:32); the
  * factors are copied to HBM, so the caller may free them afterwards. */

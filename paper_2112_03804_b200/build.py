@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2112_03804_b200")
 LIBDIR = os.path.join(PKG, "lib")
-CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu")]
+CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu")]
 HOST_SRC = [os.path.join(PKG, "csrc", "host", f) for f in ("kr_host.cpp",)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # the system g++ links libstdc++ dynamically (a statically linked libstdc++

@@ -178,4 +178,6 @@ void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s);
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s);
 // Copy streams and events for the pipelined host-buffer calls (>= 2 groups).
 void engine_make_pipeline(kr_engine* e);
+// Shared-memory limits of the chain-solve kernels (engines built elsewhere).
+void engine_chain_setup(kr_engine* e);
 }  // namespace krb

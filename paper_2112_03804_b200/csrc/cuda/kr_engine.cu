@@ -1402,6 +1402,12 @@ void solve_backward(kr_engine* e, cudaStream_t s) {
 // accounting.  Pointers address the whole vectors.
 void engine_make_pipeline(kr_engine* e) { make_pipeline(e); }
 
+void engine_chain_setup(kr_engine*) {
+    const size_t smem = size_t(kStages) * kChunkRows * 32 * sizeof(double) * 2;
+    raise_smem_limit(k_chain_tma<1>, smem);
+    raise_smem_limit(k_chain_tma<-1>, smem);
+}
+
 namespace {
 
 // The product as first stage (per board group: the input-side kernels),

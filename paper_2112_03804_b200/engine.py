@@ -66,6 +66,20 @@ class CudaEngine:
         self.implicit = True
         return self
 
+    @classmethod
+    def device_built(cls, instances, device=0, flags=0):
+        """The factored engine (Technique B post) built entirely on the device
+        from the instances' KronPayoff pieces (kr_engine_create_device_b):
+        bitwise the products of CudaEngine([inst.sparsify("b", True) ...])."""
+        L = N.cuda()
+        insts = instances if isinstance(instances, (list, tuple)) else [instances]
+        arr = (N.kr_kron_board * len(insts))(*[i.kron_view() for i in insts])
+        h = C.c_void_p()
+        N.check(L.kr_engine_create_device_b(arr, len(insts), device, flags, C.byref(h)))
+        self = cls.__new__(cls)
+        self._attach(h, device, len(insts))
+        return self
+
     implicit = False
 
     def _attach(self, h, device, nboards):

@@ -36,3 +36,40 @@ def test_device_factors_engine_products_bitwise():
     x, y = rng.standard_normal(p.cols), rng.standard_normal(p.rows)
     assert np.array_equal(e_host.Ax(x).view(np.int64), e_dev.Ax(x).view(np.int64))
     assert np.array_equal(e_host.ATx(y).view(np.int64), e_dev.ATx(y).view(np.int64))
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_device_built_engine_bitwise(name, kw):
+    """The engine laid out on the device (kr_engine_create_device_b) against
+    the engine built from the host builder's factors: identical products
+    bit for bit and the same flop count."""
+    p = H.builtin(name, **kw)
+    e_host, e_dev = CudaEngine(p.sparsify("b", True)), CudaEngine.device_built(p)
+    assert (e_dev.rows, e_dev.cols, e_dev.k) == (e_host.rows, e_host.cols, e_host.k)
+    assert e_dev.nnz == e_host.nnz
+    rng = np.random.default_rng(11)
+    for _ in range(2):
+        x, y = rng.standard_normal(p.cols), rng.standard_normal(p.rows)
+        assert np.array_equal(e_host.Ax(x).view(np.int64), e_dev.Ax(x).view(np.int64))
+        assert np.array_equal(e_host.ATx(y).view(np.int64), e_dev.ATx(y).view(np.int64))
+    assert e_host.last_flops() == e_dev.last_flops()
+
+
+def test_device_built_engine_multiboard_and_solver():
+    boards = H.turn_instances("Ks7d4c2h", nboards=5, tree=3)
+    mixed = [i for i, _ in boards] + [H.builtin("river_full", seed=5, board="Kc9d7c4d2c", deck=26, tree=3)]
+    e_host = CudaEngine([b.sparsify("b", True) for b in mixed])
+    e_dev = CudaEngine.device_built(mixed)
+    rng = np.random.default_rng(12)
+    x, y = rng.standard_normal(e_host.cols), rng.standard_normal(e_host.rows)
+    assert np.array_equal(e_host.Ax(x).view(np.int64), e_dev.Ax(x).view(np.int64))
+    assert np.array_equal(e_host.ATx(y).view(np.int64), e_dev.ATx(y).view(np.int64))
+    # a DCFR solve driven by the device-built engine is bitwise the host-built one
+    from paper_2112_03804_b200.solver import CudaSolver, DcfrParams
+    i0 = boards[0][0]
+    ins = [i for i, _ in boards]
+    runs = []
+    for eng in (CudaEngine([f for _, f in boards]), CudaEngine.device_built(ins)):
+        s = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [b.m1 for b in ins], [b.m2 for b in ins], i0.pot)
+        runs.append(s.run(DcfrParams(max_iters=20, checkpoint_every=5)))
+    assert np.array_equal(runs[0].trace_expl.view(np.int64), runs[1].trace_expl.view(np.int64))
