@@ -273,7 +273,7 @@ int kr_solver_iteration(const kr_solver* s);
  * order).  mb[b] = river hands of board b; riverToTurn[r] = the turn hand of
  * river hand r (board-major); sigma[2t + p] = player p's turn sequence leading
  * to continuation t; riverTrees[2t + p] its river treeplex; pot = 2 x the
- * turn contribution.  run: DCFR (rule KR_RULE_DCFR) with the turn treeplex
+ * turn contribution.  run: DCFR, CFR+ or PRM+ (kr_dcfr_params.rule) with the turn treeplex
  * composed as in DESIGN.md §4.8; avg1 / avg2 receive the full average
  * strategies (turn block, then each continuation's river block). */
 typedef struct kr_turn_solver kr_turn_solver;

@@ -71,8 +71,9 @@ def regret_match(R, seqs):  # solver.hpp:166-194
     return [1.0 / ties if v >= best - tol else 0.0 for v in r]
 
 
-def sweep(tree, R, g, extra=None):
-    """cfrSweep of one hand (solver.hpp:227-245); returns the root value."""
+def sweep(tree, R, g, extra=None, inst=None):
+    """cfrSweep of one hand (solver.hpp:227-245); returns the root value.
+    inst: receives each sequence's instantaneous regret (ev - nodeVal)."""
     sv = [0.0] * (tree.n + 1)
     for v in range(len(tree.parent) - 1, -1, -1):
         seqs = tree.acts[v]
@@ -86,9 +87,20 @@ def sweep(tree, R, g, extra=None):
             evs.append(ev)
             node += probs[a] * ev
         for s in seqs:
-            R[s - 1] += sv[s] - node
+            d = sv[s] - node
+            R[s - 1] += d
+            if inst is not None:
+                inst[s - 1] = d
         sv[tree.parent[v]] += node
     return sv[0]
+
+
+def factor(t, e):
+    """t^e / (t^e + 1), with the limits 1 / 0 at e = +-inf (kr_dcfr_params)."""
+    if np.isinf(e):
+        return 1.0 if e > 0 else 0.0
+    te = t ** e
+    return te / (te + 1)
 
 
 def seq_form(tree, R):
@@ -165,7 +177,20 @@ class TurnOracle:
                 lo = g.off[p][t] + (self.boff[b] + r) * n
                 yield b, r, slice(lo, lo + n)
 
-    def update(self, p, R, X, grad, mode1=True):
+    def _hand(self, tree, R, X, grad, sl, extra, rule, pos, neg):
+        """One hand's sweep and strategy under the update rule (the river
+        oracle's playerUpdate): 0 DCFR; 1 CFR+ (discount, then match the
+        discounted regrets); 2 PRM+ (match R + the last regret)."""
+        d = np.zeros(sl.stop - sl.start) if rule == 2 else None
+        Rs = R[sl]
+        root = sweep(tree, Rs, grad[sl], extra, d)
+        if rule != 0:
+            Rs *= np.where(Rs > 0, pos, neg)
+        R[sl] = Rs
+        X[sl] = seq_form(tree, Rs + d if rule == 2 else Rs)
+        return root
+
+    def update(self, p, R, X, grad, mode1=True, rule=0, pos=1.0, neg=0.0):
         """Regrets R and strategy X (full vectors) of player p from gradient
         grad (already negated for player 2); mode1=False: initial strategy."""
         g = self.g
@@ -174,11 +199,12 @@ class TurnOracle:
         for t in range(len(g.conts)):
             tree = self.tr[t][p]
             sigma = int(g.conts[t][p])
-            root = np.zeros(len(g.rivers) * 0 + sum(g.mb))
+            root = np.zeros(sum(g.mb))
             for b, r, sl in self._river_slices(p, t):
                 if mode1:
-                    root[self.boff[b] + r] = sweep(tree, R[sl], grad[sl])
-                X[sl] = seq_form(tree, R[sl])
+                    root[self.boff[b] + r] = self._hand(tree, R, X, grad, sl, None, rule, pos, neg)
+                else:
+                    X[sl] = seq_form(tree, R[sl])
             # sum over boards (ascending) per turn hand
             acc = np.zeros(g.m)
             for b in range(len(g.rivers)):
@@ -188,8 +214,9 @@ class TurnOracle:
         for h in range(g.m):
             sl = slice(h * nt, (h + 1) * nt)
             if mode1:
-                sweep(self.tt[p], R[sl], grad[sl], extra[sl])
-            X[sl] = seq_form(self.tt[p], R[sl])
+                self._hand(self.tt[p], R, X, grad, sl, extra[sl], rule, pos, neg)
+            else:
+                X[sl] = seq_form(self.tt[p], R[sl])
         # river strategies: turn reach of sigma_p(t) times the mass-1 form
         for t in range(len(g.conts)):
             sigma = int(g.conts[t][p])
@@ -215,7 +242,7 @@ class TurnOracle:
             total += br_walk(self.tt[p], grad[sl], extra[sl])
         return total
 
-    def dcfr(self, iters, alpha=1.5, beta=0.0, gamma=2.0, checkpoint_every=1):
+    def dcfr(self, iters, alpha=1.5, beta=0.0, gamma=2.0, checkpoint_every=1, rule=0):
         """dcfrSolve over the turn game; returns (trace of (br1, br2, expl), avgs)."""
         g = self.g
         R = [np.zeros(g.size[0]), np.zeros(g.size[1])]
@@ -227,13 +254,13 @@ class TurnOracle:
         trace = []
         pot = 2 * g.pot
         for t in range(1, iters + 1):
-            ta, tb = t ** alpha, t ** beta
-            pos, neg = ta / (ta + 1), tb / (tb + 1)
+            pos, neg = factor(t, alpha), factor(t, beta)
             shrink = (t / (t + 1)) ** gamma
-            self.update(0, R[0], X[0], self.ax(X[1]))
-            self.update(1, R[1], X[1], -self.atx(X[0]))
+            self.update(0, R[0], X[0], self.ax(X[1]), rule=rule, pos=pos, neg=neg)
+            self.update(1, R[1], X[1], -self.atx(X[0]), rule=rule, pos=pos, neg=neg)
             for p in range(2):
-                R[p] *= np.where(R[p] > 0, pos, neg)
+                if rule == 0:
+                    R[p] *= np.where(R[p] > 0, pos, neg)
                 A[p] = (A[p] + X[p]) * shrink
             ws = (ws + 1) * shrink
             if t % checkpoint_every == 0 or t == iters:

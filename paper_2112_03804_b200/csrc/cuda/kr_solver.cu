@@ -1248,6 +1248,7 @@ struct kr_turn_solver {
     int64_t* d_one = nullptr;                      // {0, m}: one "board" of turn hands for k_board_sums
     double pot = 0;
     int64_t launches = 0;
+    int rule = 0;  // KR_RULE_*
     // board sharding: after the river steps of a half-iteration (and of a
     // best response) the per-turn-hand river values in `extra` cover this
     // rank's boards only; exchange(user) must sum them over the ranks in place
@@ -1316,8 +1317,8 @@ void team_step(kr_turn_solver* s, const kr_turn_solver::TreeDev& T, int64_t H, i
     if (!grid) return;
     const size_t smem = team_smem(T.n, T.nn, hpb, T.len);
     k_player_team<kTurnTeam><<<grid, 256, smem, st>>>(mode, T.d, T.nn, T.n, T.na, T.len, H, hpb, g, negate, regret, x,
-                                                      avg, pos, neg, shrink, 0, nullptr, nullptr, noAvg, rootOut,
-                                                      extra);
+                                                      avg, pos, neg, shrink, s->rule, nullptr, nullptr, noAvg,
+                                                      rootOut, extra);
     KR_CK_LAUNCH();
     s->launches++;
 }
@@ -1520,7 +1521,8 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         if (!s || !prm || !r) throw Fail{KR_INVALID_INPUT, "null argument to kr_turn_solver_run"};
         if (prm->max_iters < 1 || prm->checkpoint_every < 1)
             throw Fail{KR_INVALID_INPUT, "iteration budget and checkpoint period must be positive"};
-        if (prm->rule != KR_RULE_DCFR) throw Fail{KR_INVALID_INPUT, "the turn solver runs DCFR"};
+        if (prm->rule < KR_RULE_DCFR || prm->rule > KR_RULE_PRMP) throw Fail{KR_INVALID_INPUT, "unknown update rule"};
+        s->rule = prm->rule;
         KR_CK(cudaSetDevice(s->device));
         cudaStream_t st = s->turnEng->stream;
         cudaEvent_t ev0, ev1;

@@ -260,7 +260,7 @@ class TurnSolver:
         except Exception:
             pass
 
-    def run(self, max_iters=100, checkpoint_every=10, alpha=1.5, beta=0.0, gamma=2.0, want_avg=False):
+    def run(self, max_iters=100, checkpoint_every=10, alpha=1.5, beta=0.0, gamma=2.0, want_avg=False, rule=0):
         import ctypes as C
 
         from . import _native as N
@@ -269,7 +269,7 @@ class TurnSolver:
         te, b1, b2 = np.zeros(cap), np.zeros(cap), np.zeros(cap)
         a1 = np.zeros(self.game.size[0]) if want_avg else None
         a2 = np.zeros(self.game.size[1]) if want_avg else None
-        prm = N.kr_dcfr_params(alpha, beta, gamma, max_iters, 0.0, checkpoint_every, 0)
+        prm = N.kr_dcfr_params(alpha, beta, gamma, max_iters, 0.0, checkpoint_every, rule)
         res = N.kr_dcfr_result(0, 0.0, 0, 0, cap, N.ptr(ti), N.ptr(te), N.ptr(b1), N.ptr(b2), None, None,
                                N.ptr(a1), N.ptr(a2), 0.0)
         N.check(N.cuda().kr_turn_solver_run(self._h, C.byref(prm), C.byref(res)))

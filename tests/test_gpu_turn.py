@@ -51,6 +51,24 @@ def test_turn_dcfr_matches_checker(game):
     assert normwise(r["avg1"], a1) <= 1e-9 and normwise(r["avg2"], a2) <= 1e-9
 
 
+@pytest.mark.parametrize("rule", [1, 2], ids=["cfr+", "prm+"])
+def test_turn_rules_match_checker(game, rule):
+    """CFR+ / PRM+ (alpha = +inf, beta = -inf, gamma = 1) through the turn
+    solver: the team kernel's per-node discount and the PRM+ prediction compose
+    across the river and turn passes as the checker's per-hand update does."""
+    inf = float("inf")
+    o = TO.TurnOracle(game)
+    trace, (a1, a2) = o.dcfr(6, alpha=inf, beta=-inf, gamma=1.0, checkpoint_every=1, rule=rule)
+    r = TurnSolver(game).run(max_iters=6, checkpoint_every=1, alpha=inf, beta=-inf, gamma=1.0,
+                             want_avg=True, rule=rule)
+    np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-9)
+    np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-9)
+    assert normwise(r["avg1"], a1) <= 1e-9 and normwise(r["avg2"], a2) <= 1e-9
+    long = TurnSolver(game).run(max_iters=200, checkpoint_every=50, alpha=inf, beta=-inf, gamma=1.0, rule=rule)
+    e = long["trace_expl"]  # CFR+ / PRM+ on this game: ~13% of the start after 200
+    assert e[-1] < 0.25 * e[0] and np.all(np.diff(e) < 0)
+
+
 def test_turn_dcfr_converges(game):
     r = TurnSolver(game).run(max_iters=300, checkpoint_every=50)
     e = r["trace_expl"]

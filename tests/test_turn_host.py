@@ -73,3 +73,24 @@ def test_all_in_continuations_are_check_check_showdowns():
     for t in allin:  # one forced check each, the showdown at the continuation's stakes
         pc = g.kron_pieces(t)[0]
         assert pc["S"].shape == (1, 1) and pc["S"][0, 0] == g.conts[t][2] and not pc["F"].any()
+
+
+def test_checker_rules_keep_their_invariants(game):
+    """The checker's CFR+ update leaves every regret non-negative (beta = -inf
+    zeroes the negative part); PRM+ keeps the same regrets but plays the regret
+    match of R + the last instantaneous regret (from R = 0 the two coincide,
+    hence the random start)."""
+    o = TO.TurnOracle(game)
+    n1, n2 = game.size
+    X2 = np.zeros(n2)
+    o.update(1, np.zeros(n2), X2, None, mode1=False)
+    grad = o.ax(X2)
+    R0, X0 = np.random.default_rng(3).uniform(0, 50, n1), np.zeros(n1)
+    o.update(0, R0, X0, None, mode1=False)
+    R, X = R0.copy(), X0.copy()
+    o.update(0, R, X, grad, rule=1, pos=1.0, neg=0.0)
+    assert R.min() >= 0 and R.max() > 0
+    Rp, Xp = R0.copy(), X0.copy()
+    o.update(0, Rp, Xp, grad, rule=2, pos=1.0, neg=0.0)
+    np.testing.assert_array_equal(Rp, R)  # same discounted regrets ...
+    assert not np.allclose(Xp, X)  # ... different strategy (matches R + r)
