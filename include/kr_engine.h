@@ -142,6 +142,17 @@ int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t 
 int kr_engine_ax_device(kr_engine* e, const double* x_dev, double* y_dev, void* stream);
 int kr_engine_atx_device(kr_engine* e, const double* y_dev, double* x_dev, void* stream);
 
+/* Both products of one pair, ax_dev = A x_dev and atx_dev = A^T y_dev, in
+ * flight together: A^T y runs on an engine-owned side stream forked from
+ * `stream` and joined back into it, so the latency-bound stages of each
+ * direction (transposes, M solves, short SpMVs) overlap the other direction's
+ * bandwidth-bound SpMV.  Results are bitwise those of kr_engine_ax_device /
+ * kr_engine_atx_device (each direction has its own scratch).  x_dev must not
+ * alias atx_dev, nor y_dev ax_dev.  No reference counterpart: the reference
+ * calls Ax and ATx one after the other (GradientEngine, solver.hpp:21-27). */
+int kr_engine_pair_device(kr_engine* e, const double* x_dev, double* ax_dev, const double* y_dev, double* atx_dev,
+                          void* stream);
+
 /* GradientEngine::flops() (solver.hpp:26, 35): cumulative multiply-adds,
  * counted with the reference rule nnz(V)+nnz(U)+nnz(Ahat)+[M!=I](nnz(M)-k)
  * per product (engine.hpp:72,77,90-91,110-131). */

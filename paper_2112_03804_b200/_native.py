@@ -93,7 +93,7 @@ class kr_dcfr_result(C.Structure):
 # Every symbol include/kr_engine.h declares (checked by the CPU test suite).
 CUDA_SYMBOLS = [
     "kr_engine_create", "kr_engine_create_boards", "kr_engine_destroy", "kr_engine_dims", "kr_engine_ax",
-    "kr_engine_atx", "kr_engine_ax_device", "kr_engine_atx_device", "kr_engine_flops", "kr_engine_last_flops",
+    "kr_engine_atx", "kr_engine_ax_device", "kr_engine_atx_device", "kr_engine_pair_device", "kr_engine_flops", "kr_engine_last_flops",
     "kr_engine_stream", "kr_engine_device", "kr_engine_launches", "kr_host_alloc", "kr_host_free", "kr_last_error",
     "kr_device_count", "kr_solver_create", "kr_solver_destroy", "kr_solver_run", "kr_solver_best_response",
     "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
@@ -135,6 +135,7 @@ def cuda():
         L.kr_engine_atx.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
         L.kr_engine_ax_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.kr_engine_atx_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kr_engine_pair_device.argtypes = [C.c_void_p] * 6
         L.kr_engine_dims.argtypes = [C.c_void_p, C.c_void_p]
         L.kr_engine_create.argtypes = [C.POINTER(kr_factors), C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]
         L.kr_engine_create_boards.argtypes = [C.POINTER(kr_factors), C.c_int, C.c_int, C.c_uint32,

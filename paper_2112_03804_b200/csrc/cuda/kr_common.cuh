@@ -69,6 +69,10 @@ struct DevSell {
     int32_t* long_row = nullptr;   // output row of each long row
     int32_t* long_col = nullptr;
     double* long_val = nullptr;
+    // dispatch order (widest slices first): over all slices, and within each
+    // board group (entries relative to the group's first slice)
+    int32_t* order_all = nullptr;
+    int32_t* order_grp = nullptr;
 };
 
 template <class T>
@@ -128,6 +132,7 @@ struct kr_engine {
     bool lean = true;       // lean SELL variant for one-entry-row matrices (KR_NO_LEAN=1: off)
     int chain_withmul = 0;  // some chain has a multiplier other than -1
     int64_t* chain_ptr = nullptr;
+    std::vector<int64_t> bCh;  // host: first chain slice of each board (+ total)
     int32_t* chain_len = nullptr;
     double* chain_mul = nullptr;
     uint8_t* chain_neg1 = nullptr;
@@ -142,7 +147,8 @@ struct kr_engine {
     int32_t* mc_row = nullptr;
     double* mc_val = nullptr;
     // scratch
-    double* d_tz = nullptr;  // k: t, then z in place (GradientWorkspace::y/z)
+    double* d_tz = nullptr;   // k: t, then z in place (GradientWorkspace::y/z), A x
+    double* d_tz2 = nullptr;  // the same for A^T y, so the two may run concurrently
     double* d_xp = nullptr;  // cols: sequence-major copy of x
     double* d_in = nullptr;  // staging for host-buffer calls
     double* d_out = nullptr;
@@ -160,6 +166,7 @@ struct kr_engine {
     double tMs[4] = {0, 0, 0, 0};
     // implicit Kronecker mode (kr_engine_create_kron): no factors at all
     krb::KronState* kron = nullptr;
+    int pf = 0;  // SELL slice L2 prefetch distance in batches (KR_PF)
     // Board groups.  Host-buffer calls pipeline over them: input copies,
     // per-group kernels and output copies run concurrently (copyIn / stream /
     // copyOut).  grpBoard: board ranges; grpRow / grpCol: row / column
@@ -167,8 +174,11 @@ struct kr_engine {
     std::vector<int64_t> grpRow{0}, grpCol{0};
     std::vector<int64_t> bSl[4], bNl[4];
     std::vector<int32_t> grpBoard{0};
-    cudaStream_t copyIn = nullptr, copyOut = nullptr;
-    std::vector<cudaEvent_t> evIn, evOut;
+    cudaStream_t copyIn = nullptr, copyOut = nullptr, stage2 = nullptr;
+    std::vector<cudaEvent_t> evIn, evOut, evMid;
+    // kr_engine_pair_device: A^T y forks onto `side` (created on first use)
+    cudaStream_t side = nullptr;
+    cudaEvent_t evFork = nullptr, evJoin = nullptr;
     int ngroups() const { return int(grpRow.size()) - 1; }
 };
 

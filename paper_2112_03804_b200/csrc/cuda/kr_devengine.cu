@@ -694,6 +694,7 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
         {
             std::vector<int64_t> sbase;
             std::vector<int32_t> slen;
+            e->bCh.assign(1, 0);
             for (auto& H : bh) {
                 const BoardDev& B = H.dev;
                 for (int s = 0; s < (B.nS + 31) / 32; ++s) {
@@ -704,6 +705,7 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
                     sbase.push_back(B.kOff + B.SB + int64_t(s) * 32);
                     for (int l = 0; l < 32; ++l) slen.push_back(s * 32 + l < B.nF ? 1 : 0);
                 }
+                e->bCh.push_back(int64_t(sbase.size()));
             }
             e->nchains = int64_t(sbase.size());
             sbase.push_back(kpadTotal);
@@ -722,12 +724,14 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
         }
         e->d_tz = dev_alloc<double>(std::max<int64_t>(kpadTotal, 1));
         KR_CK(cudaMemset(e->d_tz, 0, 8 * size_t(std::max<int64_t>(kpadTotal, 1))));
+        e->d_tz2 = dev_alloc<double>(std::max<int64_t>(kpadTotal, 1));
+        KR_CK(cudaMemset(e->d_tz2, 0, 8 * size_t(std::max<int64_t>(kpadTotal, 1))));
         e->d_xp = dev_alloc<double>(std::max<int64_t>(colsTotal, 1));
         e->d_in = dev_alloc<double>(std::max<int64_t>(std::max(rowsTotal, colsTotal), 1));
         e->d_out = dev_alloc<double>(std::max<int64_t>(std::max(rowsTotal, colsTotal), 1));
         e->lean = std::getenv("KR_NO_LEAN") == nullptr;
         // board groups for the host-buffer pipeline
-        int G = (flags & KR_FLAG_SINGLE_PART) ? 1 : 4;
+        int G = (flags & KR_FLAG_SINGLE_PART) ? 1 : 6;  // as group_count (kr_engine.cu)
         if (const char* env = std::getenv("KR_GROUPS")) G = std::atoi(env);
         G = std::max(1, std::min(G, nb));
         for (int g = 0; g < G; ++g) {
@@ -736,6 +740,7 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
             e->grpRow.push_back(g1 < nb ? bh[size_t(g1)].dev.rowOff : rowsTotal);
             e->grpCol.push_back(g1 < nb ? bh[size_t(g1)].dev.colOff : colsTotal);
         }
+        if (const char* env = std::getenv("KR_PF")) e->pf = std::max(0, std::atoi(env));
         engine_make_pipeline(e);
         KR_CK(cudaDeviceSynchronize());
     } catch (...) {

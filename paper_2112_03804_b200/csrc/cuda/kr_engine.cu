@@ -61,7 +61,14 @@ struct SellView {
     const int32_t* long_col;
     const double* long_val;
     int64_t nlong;
+    const int32_t* order;  // slice dispatch order (nullptr: storage order)
+    int32_t pf;            // L2 prefetch distance of the slice rows, in batches of KU (0: none)
 };
+
+// One bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 constexpr int kChunk = 256;  // long-row entries staged per warp
 #ifndef KR_KU
@@ -153,11 +160,28 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
         if (lane == 0) y[A.long_row[r]] = acc;
         return;
     }
-    const int64_t s = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
-    if (s >= A.nslices) return;
-    const int64_t base = A.slice_ptr[s] + lane;
+    const int64_t si = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
+    if (si >= A.nslices) return;
+    // widest slices first: a slice's latency grows with its width, so the
+    // widest ones must not be the last dispatched (they would set the tail)
+    const int64_t s = A.order ? int64_t(A.order[si]) : si;
+    const int64_t sb = A.slice_ptr[s];
+    const int64_t base = sb + lane;
     const int32_t len = A.lane_len[s * 32 + lane];
     const int32_t row = A.lane_row[s * 32 + lane];
+    // Slice rows are contiguous (row r: 32 entries at sb + 32 r), so lane 0
+    // (the slice's longest row: rows are sorted by length) keeps the next
+    // pf batches of col / val streaming into L2 with one bulk prefetch per
+    // array; each batch's loads then wait on L2, not on HBM.
+    const int32_t pfRows = A.pf * KU;
+    auto prefetch = [&](int32_t r0, int32_t n) {
+        n = min(n, len - r0);
+        if (n > 0) {
+            prefetch_l2(A.col + sb + int64_t(r0) * 32, uint32_t(n) * 32u * 4u);
+            prefetch_l2(A.val + sb + int64_t(r0) * 32, uint32_t(n) * 32u * 8u);
+        }
+    };
+    if (lane == 0 && pfRows > 0) prefetch(KU, pfRows);
     double acc = 0.0;
     int32_t c[KU];
     double v[KU];
@@ -168,6 +192,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
             v[u] = __ldcs(A.val + base + int64_t(u) * 32);
         }
     for (int32_t j = 0; j < len; j += KU) {
+        if (lane == 0 && pfRows > 0) prefetch(j + KU + pfRows, KU);
         int32_t cn[KU];
         double vn[KU], x[KU];
 #pragma unroll
@@ -265,13 +290,13 @@ template <int DIR>
 __global__ void __launch_bounds__(32)
     k_chain_tma(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
                 const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int withMul,
-                double* __restrict__ z) {
+                double* __restrict__ z, int64_t s0) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ __align__(8) uint64_t bar[kStages];
     double(*Tb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm);
     double(*Mb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm + kStages * kChunkRows * 32);
     const int lane = threadIdx.x;
-    const int64_t s = blockIdx.x;
+    const int64_t s = s0 + blockIdx.x;
     const int64_t b0 = sbase[s];
     const int32_t width = int32_t((sbase[s + 1] - b0) / 32);
     const int32_t len = slen[s * 32 + lane];
@@ -423,10 +448,10 @@ __global__ void __launch_bounds__(32)
 // The next stage's loads are issued before the current stage's adds.
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     k_chain_forward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
-                    const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t nslices,
+                    const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
                     double* __restrict__ z) {
-    const int64_t s = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (s >= nslices) return;
+    const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s >= s1) return;
     const int lane = threadIdx.x & 31;
     const int32_t len = slen[s * 32 + lane];
     const bool allneg = neg1[s * 32 + lane] != 0;
@@ -472,10 +497,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 // each lane walking its chain in reverse: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     k_chain_backward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
-                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t nslices,
+                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
                      double* __restrict__ z) {
-    const int64_t s = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (s >= nslices) return;
+    const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s >= s1) return;
     const int lane = threadIdx.x & 31;
     const int32_t len = slen[s * 32 + lane];
     const bool allneg = neg1[s * 32 + lane] != 0;
@@ -706,6 +731,8 @@ void free_sell(krb::DevSell& d) {
     cudaFree(d.long_row);
     cudaFree(d.long_col);
     cudaFree(d.long_val);
+    cudaFree(d.order_all);
+    cudaFree(d.order_grp);
     d = krb::DevSell{};
 }
 
@@ -951,6 +978,11 @@ void destroy_engine(kr_engine* e) {
     for (cudaEvent_t ev : e->evOut) cudaEventDestroy(ev);
     if (e->copyIn) cudaStreamDestroy(e->copyIn);
     if (e->copyOut) cudaStreamDestroy(e->copyOut);
+    if (e->stage2) cudaStreamDestroy(e->stage2);
+    for (cudaEvent_t ev : e->evMid) cudaEventDestroy(ev);
+    if (e->side) cudaStreamDestroy(e->side);
+    if (e->evFork) cudaEventDestroy(e->evFork);
+    if (e->evJoin) cudaEventDestroy(e->evJoin);
     kron_destroy(e->kron);
     free_sell(e->VT);
     free_sell(e->UA);
@@ -969,6 +1001,7 @@ void destroy_engine(kr_engine* e) {
     cudaFree(e->mc_row);
     cudaFree(e->mc_val);
     cudaFree(e->d_tz);
+    cudaFree(e->d_tz2);
     cudaFree(e->d_xp);
     cudaFree(e->d_in);
     cudaFree(e->d_out);
@@ -1008,6 +1041,9 @@ void parallel_boards(int nb, F&& body) {
 
 int group_count(int nb, uint32_t flags);
 void make_pipeline(kr_engine* e);
+}  // namespace
+void set_carveout();
+namespace {
 
 kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t flags) {
     int ndev = 0;
@@ -1116,6 +1152,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         const int64_t nnzOf[4] = {nV, nU + nA, nU, nA + nV};
         for (int w = 0; w < 4; ++w) alloc_sell(*mats[w], nrowsOf[w], tsl[w], nnzOf[w], tpad[w], tnl[w], tnlz[w]);
         e->d_tz = dev_alloc<double>(std::max<int64_t>(Kp, 1));
+        e->d_tz2 = dev_alloc<double>(std::max<int64_t>(Kp, 1));
         e->d_xp = dev_alloc<double>(std::max<int64_t>(Cc, 1));
         e->d_in = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
         e->d_out = dev_alloc<double>(std::max<int64_t>(std::max(R, Cc), 1));
@@ -1149,8 +1186,10 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             std::vector<int32_t> slen;
             std::vector<uint8_t> sneg;
             std::vector<double> cmul(static_cast<size_t>(Kp), 0.0);
+            e->bCh.assign(1, 0);
             for (auto& p : plan) {
                 for (int64_t b0 : p.sbase) sbase.push_back(p.kOff + b0);
+                e->bCh.push_back(int64_t(sbase.size()));
                 slen.insert(slen.end(), p.slen.begin(), p.slen.end());
                 sneg.insert(sneg.end(), p.sneg.begin(), p.sneg.end());
                 std::copy(p.mul.begin(), p.mul.end(), cmul.begin() + p.kOff);
@@ -1244,6 +1283,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             e->bNl[w].push_back(tnl[w]);
         }
         e->lean = std::getenv("KR_NO_LEAN") == nullptr;
+        if (const char* env = std::getenv("KR_PF")) e->pf = std::max(0, std::atoi(env));
         const int G = group_count(nb, flags);
         for (int g = 0; g < G; ++g) {
             const int g1 = int(int64_t(nb) * (g + 1) / G);
@@ -1261,24 +1301,75 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
 }
 
 // Host-call pipeline resources: two copy streams and one event pair per group.
+// Slice dispatch orders (DevSell::order_all / order_grp): a stable sort by
+// width, widest first, within each board group (and over all slices with
+// KR_LPT_ALL).  A group's launch lasts only ~50 us, so a wide slice (~30 us of
+// dependent loads) dispatched late would set its length.  The whole-range
+// launches keep storage order: there the tail is amortised and the sorted
+// order measured 1-2% slower.  The sums are untouched (each row is still one
+// lane's sequential sum).  KR_LPT=0 keeps storage order everywhere.
+void build_orders(kr_engine* e) {
+    if (const char* env = std::getenv("KR_LPT"))
+        if (std::atoi(env) == 0) return;
+    krb::DevSell* mats[4] = {&e->VT, &e->UA, &e->UT, &e->AV};
+    const int G = e->ngroups();
+    for (int w = 0; w < 4; ++w) {
+        krb::DevSell& A = *mats[w];
+        if (A.nslices < 2) continue;
+        std::vector<int64_t> sp(size_t(A.nslices) + 1);
+        KR_CK(cudaMemcpy(sp.data(), A.slice_ptr, 8 * sp.size(), cudaMemcpyDeviceToHost));
+        auto sorted = [&](int64_t a, int64_t b) {  // slices [a, b), relative to a
+            std::vector<int32_t> o(size_t(b - a));
+            std::iota(o.begin(), o.end(), 0);
+            std::stable_sort(o.begin(), o.end(), [&](int32_t i, int32_t j) {
+                return sp[size_t(a + i) + 1] - sp[size_t(a + i)] > sp[size_t(a + j) + 1] - sp[size_t(a + j)];
+            });
+            return o;
+        };
+        if (std::getenv("KR_LPT_ALL")) {  // whole-range launches too (measured: -1-2%, off)
+            std::vector<int32_t> all = sorted(0, A.nslices);
+            A.order_all = dev_alloc<int32_t>(A.nslices);
+            KR_CK(cudaMemcpy(A.order_all, all.data(), 4 * all.size(), cudaMemcpyHostToDevice));
+        }
+        if (G >= 2 && int64_t(e->bSl[w].size()) > int64_t(e->grpBoard.back())) {
+            std::vector<int32_t> grp(size_t(A.nslices));
+            for (int g = 0; g < G; ++g) {
+                const int64_t a = e->bSl[w][size_t(e->grpBoard[size_t(g)])];
+                const int64_t b = e->bSl[w][size_t(e->grpBoard[size_t(g) + 1])];
+                std::vector<int32_t> o = sorted(a, b);
+                std::copy(o.begin(), o.end(), grp.begin() + a);
+            }
+            A.order_grp = dev_alloc<int32_t>(A.nslices);
+            KR_CK(cudaMemcpy(A.order_grp, grp.data(), 4 * grp.size(), cudaMemcpyHostToDevice));
+        }
+    }
+}
+
 void make_pipeline(kr_engine* e) {
+    set_carveout();
+    build_orders(e);
     const int G = e->ngroups();
     if (G < 2) return;
     KR_CK(cudaStreamCreateWithFlags(&e->copyIn, cudaStreamNonBlocking));
     KR_CK(cudaStreamCreateWithFlags(&e->copyOut, cudaStreamNonBlocking));
+    KR_CK(cudaStreamCreateWithFlags(&e->stage2, cudaStreamNonBlocking));
     e->evIn.resize(size_t(G));
     e->evOut.resize(size_t(G));
+    e->evMid.resize(size_t(G));
     for (int g = 0; g < G; ++g) {
         KR_CK(cudaEventCreateWithFlags(&e->evIn[size_t(g)], cudaEventDisableTiming));
         KR_CK(cudaEventCreateWithFlags(&e->evOut[size_t(g)], cudaEventDisableTiming));
+        KR_CK(cudaEventCreateWithFlags(&e->evMid[size_t(g)], cudaEventDisableTiming));
     }
 }
 
-// Board groups of the pipelined host-buffer calls: up to four contiguous
+// Board groups of the pipelined host-buffer calls: up to six contiguous
 // board ranges (KR_FLAG_SINGLE_PART: one; KR_GROUPS overrides the count).
+// Measured at config 3 (profiles/r01l_e2e_pipeline.md): 4 -> 6 groups +2-3%,
+// 8 and more lose to per-launch tails.
 int group_count(int nb, uint32_t flags) {
     if (flags & KR_FLAG_SINGLE_PART) return 1;
-    int G = 4;
+    int G = 6;
     if (const char* env = std::getenv("KR_GROUPS")) G = std::atoi(env);
     return std::max(1, std::min(G, nb));
 }
@@ -1308,8 +1399,9 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
     const int64_t blocks = (l1 - l0 + kWarpsPerBlock - 1) / kWarpsPerBlock +
                            (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return;
+    const int32_t* order = b1 < 0 ? A.order_all : A.order_grp ? A.order_grp + s0 : nullptr;
     SellView v{A.slice_ptr + s0, A.lane_row + 32 * s0, A.lane_len + 32 * s0, A.col, A.val, s1 - s0,
-               A.long_ptr + l0, A.long_row + l0, A.long_col, A.long_val, l1 - l0};
+               A.long_ptr + l0, A.long_row + l0, A.long_col, A.long_val, l1 - l0, order, e->pf};
     const bool timed = e->timing && b1 < 0;
     kr_engine::Pending pend{which, nullptr, nullptr};
     if (timed) {
@@ -1348,15 +1440,18 @@ size_t chain_smem(const kr_engine* e) {
     return size_t(kStages) * kChunkRows * 32 * sizeof(double) * (e->chain_withmul ? 2 : 1);
 }
 
-void solve_forward(kr_engine* e, cudaStream_t s) {
-    if (e->mkind == 1 && e->nchains > 0) {
+// Chain slices [c0, c1) (a board group's: slices are per board, in board
+// order, bCh), or all of them (c1 < 0).
+void solve_forward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1) {
+    if (c1 < 0) c1 = e->nchains;
+    if (e->mkind == 1 && c1 > c0) {
         if (e->chain_tma) {
-            k_chain_tma<1><<<unsigned(e->nchains), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
-                                                                         e->chain_neg1, e->chain_withmul, e->d_tz);
+            k_chain_tma<1><<<unsigned(c1 - c0), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
+                                                                      e->chain_neg1, e->chain_withmul, e->d_tz, c0);
         } else {
             const int wpb = kWarpsPerBlock;
-            k_chain_forward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
-                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, e->nchains, e->d_tz);
+            k_chain_forward<<<unsigned((c1 - c0 + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, c0, c1, e->d_tz);
         }
         KR_CK_LAUNCH();
         e->launches++;
@@ -1372,15 +1467,16 @@ void solve_forward(kr_engine* e, cudaStream_t s) {
     }
 }
 
-void solve_backward(kr_engine* e, cudaStream_t s) {
-    if (e->mkind == 1 && e->nchains > 0) {
+void solve_backward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1) {
+    if (c1 < 0) c1 = e->nchains;
+    if (e->mkind == 1 && c1 > c0) {
         if (e->chain_tma) {
-            k_chain_tma<-1><<<unsigned(e->nchains), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
-                                                                          e->chain_neg1, e->chain_withmul, e->d_tz);
+            k_chain_tma<-1><<<unsigned(c1 - c0), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
+                                                                       e->chain_neg1, e->chain_withmul, e->d_tz2, c0);
         } else {
             const int wpb = kWarpsPerBlock;
-            k_chain_backward<<<unsigned((e->nchains + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
-                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, e->nchains, e->d_tz);
+            k_chain_backward<<<unsigned((c1 - c0 + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, c0, c1, e->d_tz2);
         }
         KR_CK_LAUNCH();
         e->launches++;
@@ -1389,7 +1485,7 @@ void solve_backward(kr_engine* e, cudaStream_t s) {
             const int64_t a = e->lvl_bwd_ptr[l], n = e->lvl_bwd_ptr[l + 1] - a;
             if (n == 0) continue;
             k_level_backward<<<unsigned((n + 127) / 128), 128, 0, s>>>(e->lvl_bwd_cols + a, n, e->mc_ptr,
-                                                                       e->mc_row, e->mc_val, e->d_tz);
+                                                                       e->mc_row, e->mc_val, e->d_tz2);
             KR_CK_LAUNCH();
             e->launches++;
         }
@@ -1406,6 +1502,27 @@ void engine_chain_setup(kr_engine*) {
     const size_t smem = size_t(kStages) * kChunkRows * 32 * sizeof(double) * 2;
     raise_smem_limit(k_chain_tma<1>, smem);
     raise_smem_limit(k_chain_tma<-1>, smem);
+}
+
+// One preferred L1 / shared-memory split for every engine kernel (percent of
+// the maximum shared memory), so kernels of different stages resident on an
+// SM together never force it to drain and reconfigure (KR_CARVEOUT).
+void set_carveout() {
+    static const int pct = [] {
+        const char* env = std::getenv("KR_CARVEOUT");
+        return env ? std::atoi(env) : -1;
+    }();
+    static bool done = false;
+    if (done || pct < 0) return;
+    done = true;
+    auto set = [](const void* f) { KR_CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct)); };
+    set(reinterpret_cast<const void*>(k_spmv<true>));
+    set(reinterpret_cast<const void*>(k_spmv<false>));
+    set(reinterpret_cast<const void*>(k_spmv<false, 1, 8>));
+    set(reinterpret_cast<const void*>(k_seq_major_tile));
+    set(reinterpret_cast<const void*>(k_seq_major));
+    set(reinterpret_cast<const void*>(k_chain_tma<1>));
+    set(reinterpret_cast<const void*>(k_chain_tma<-1>));
 }
 
 namespace {
@@ -1439,21 +1556,23 @@ void first_stage(kr_engine* e, int dir, const double* in, cudaStream_t s, int g 
         }
         launch_sell(e, 0, e->VT, xg, nullptr, 0, e->d_tz, s, b0, b1);      // t = V^T x    engine.hpp:65-72
     } else {
-        launch_sell(e, 2, e->UT, in, nullptr, 0, e->d_tz, s, b0, b1);      // s = U^T y    engine.hpp:103-110
+        launch_sell(e, 2, e->UT, in, nullptr, 0, e->d_tz2, s, b0, b1);     // s = U^T y    engine.hpp:103-110
     }
 }
 
-void middle(kr_engine* e, int dir, cudaStream_t s) {
+void middle(kr_engine* e, int dir, cudaStream_t s, int g = -1) {
     if (e->kron) return;
-    if (dir == 0) solve_forward(e, s);   // z = M^-1 t    engine.hpp:74-78
-    else solve_backward(e, s);           // z = M^-T s    engine.hpp:112-115
+    const int64_t c0 = g < 0 ? 0 : e->bCh[size_t(e->grpBoard[size_t(g)])];
+    const int64_t c1 = g < 0 ? -1 : e->bCh[size_t(e->grpBoard[size_t(g) + 1])];
+    if (dir == 0) solve_forward(e, s, c0, c1);   // z = M^-1 t    engine.hpp:74-78
+    else solve_backward(e, s, c0, c1);           // z = M^-T s    engine.hpp:112-115
 }
 
 void last_stage(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int g = -1) {
     const int b0 = g < 0 ? 0 : e->grpBoard[size_t(g)], b1 = g < 0 ? -1 : e->grpBoard[size_t(g) + 1];
     if (e->kron) return kron_product(e, dir, in, out, s, b0, b1);
     if (dir == 0) launch_sell(e, 1, e->UA, e->d_tz, in, e->kpad, out, s, b0, b1);   // y = U z + Ahat x
-    else launch_sell(e, 3, e->AV, in, e->d_tz, e->rows, out, s, b0, b1);           // x = Ahat^T y + V z
+    else launch_sell(e, 3, e->AV, in, e->d_tz2, e->rows, out, s, b0, b1);          // x = Ahat^T y + V z
 }
 
 void account(kr_engine* e, int dir) {
@@ -1496,8 +1615,8 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
     }
     const std::vector<int64_t>& io = dir == 0 ? e->grpCol : e->grpRow;
     const std::vector<int64_t>& oo = dir == 0 ? e->grpRow : e->grpCol;
-    auto copy_out = [&](int g) {
-        KR_CK(cudaEventRecord(e->evOut[size_t(g)], e->stream));
+    auto copy_out = [&](int g, cudaStream_t from) {
+        KR_CK(cudaEventRecord(e->evOut[size_t(g)], from));
         KR_CK(cudaStreamWaitEvent(e->copyOut, e->evOut[size_t(g)], 0));
         const size_t a = size_t(oo[size_t(g)]), n = size_t(oo[size_t(g) + 1]) - a;
         KR_CK(cudaMemcpyAsync(hout + a, e->d_out + a, 8 * n, cudaMemcpyDeviceToHost, e->copyOut));
@@ -1507,20 +1626,40 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
         KR_CK(cudaMemcpyAsync(e->d_in + a, hin + a, 8 * n, cudaMemcpyHostToDevice, e->copyIn));
         KR_CK(cudaEventRecord(e->evIn[size_t(g)], e->copyIn));
     }
-    const bool fused = e->kron != nullptr;  // no middle stage: one kernel per group
-    for (int g = 0; g < G; ++g) {
-        KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
-        first_stage(e, dir, e->d_in, e->stream, g);
-        if (fused) {
+    // Every factor is block diagonal over boards, and so is M's chain solve
+    // (chain slices per board, bCh): with chains (or none) a group's whole
+    // product runs as soon as its input has arrived.  Its M solve and last
+    // SpMV run on stage2 while the next group's first SpMV streams on the
+    // main stream (the latency-bound solve hides under it, and each kernel's
+    // tail under the other's); its output copy follows on copyOut.  The
+    // level solve (mkind 2) spans boards, so there it waits for every
+    // group's first stage.
+    if (e->kron) {
+        for (int g = 0; g < G; ++g) {
+            KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
             last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
-            copy_out(g);
+            copy_out(g, e->stream);
         }
-    }
-    if (!fused) {
+    } else if (e->mkind == 0 ||
+               (e->mkind == 1 && int64_t(e->bCh.size()) == int64_t(e->grpBoard.back()) + 1)) {
+        for (int g = 0; g < G; ++g) {
+            KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
+            first_stage(e, dir, e->d_in, e->stream, g);
+            KR_CK(cudaEventRecord(e->evMid[size_t(g)], e->stream));
+            KR_CK(cudaStreamWaitEvent(e->stage2, e->evMid[size_t(g)], 0));
+            middle(e, dir, e->stage2, g);
+            last_stage(e, dir, e->d_in, e->d_out, e->stage2, g);
+            copy_out(g, e->stage2);
+        }
+    } else {
+        for (int g = 0; g < G; ++g) {
+            KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
+            first_stage(e, dir, e->d_in, e->stream, g);
+        }
         middle(e, dir, e->stream);
         for (int g = 0; g < G; ++g) {
             last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
-            copy_out(g);
+            copy_out(g, e->stream);
         }
     }
     KR_CK(cudaStreamSynchronize(e->copyOut));
@@ -1601,6 +1740,28 @@ int kr_engine_atx_device(kr_engine* e, const double* y, double* x, void* stream)
         if (!e || !x || !y) throw Fail{KR_INVALID_INPUT, "null argument"};
         KR_CK(cudaSetDevice(e->device));
         krb::engine_atx(e, y, x, stream ? static_cast<cudaStream_t>(stream) : e->stream);
+    });
+}
+
+int kr_engine_pair_device(kr_engine* e, const double* x, double* ax, const double* y, double* atx, void* stream) {
+    return guarded([&] {
+        if (!e || !x || !ax || !y || !atx) throw Fail{KR_INVALID_INPUT, "null argument"};
+        KR_CK(cudaSetDevice(e->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+        if (!e->side) {
+            // KR_PAIR_PRIORITY (measurement knob): the side stream's priority
+            const char* pr = std::getenv("KR_PAIR_PRIORITY");
+            KR_CK(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, pr ? std::atoi(pr) : 0));
+            KR_CK(cudaEventCreateWithFlags(&e->evFork, cudaEventDisableTiming));
+            KR_CK(cudaEventCreateWithFlags(&e->evJoin, cudaEventDisableTiming));
+        }
+        // A^T y on the side stream, A x on s; s then waits for both
+        KR_CK(cudaEventRecord(e->evFork, s));
+        KR_CK(cudaStreamWaitEvent(e->side, e->evFork, 0));
+        krb::engine_atx(e, y, atx, e->side);
+        krb::engine_ax(e, x, ax, s);
+        KR_CK(cudaEventRecord(e->evJoin, e->side));
+        KR_CK(cudaStreamWaitEvent(s, e->evJoin, 0));
     });
 }
 

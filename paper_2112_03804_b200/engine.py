@@ -174,3 +174,8 @@ class CudaEngine:
     def atx_device(self, y_ptr, x_ptr, stream=None):
         N.check(N.cuda().kr_engine_atx_device(self._h, C.c_void_p(y_ptr), C.c_void_p(x_ptr),
                                               C.c_void_p(stream) if stream else None))
+
+    def pair_device(self, x_ptr, ax_ptr, y_ptr, atx_ptr, stream=None):
+        """A x and A^T y in flight together (kr_engine_pair_device)."""
+        N.check(N.cuda().kr_engine_pair_device(self._h, C.c_void_p(x_ptr), C.c_void_p(ax_ptr), C.c_void_p(y_ptr),
+                                               C.c_void_p(atx_ptr), C.c_void_p(stream) if stream else None))

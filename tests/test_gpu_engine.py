@@ -167,11 +167,15 @@ def test_device_pointer_entry_points():
     assert bits_equal(y.cpu().numpy(), eng.Ax(x.cpu().numpy()))
 
 
-@pytest.mark.parametrize("groups", ["1", "2", "4"])
-def test_host_pipeline_groups_bitwise(groups, monkeypatch):
-    """kr_engine_ax / kr_engine_atx pipelined over board groups (first and
-    last SpMV launched per group range) give the bits of the oracle."""
+@pytest.mark.parametrize("groups,knob", [("1", None), ("2", None), ("3", None), ("4", None), ("4", ("KR_LPT", "0")),
+                                         ("3", ("KR_LPT_ALL", "1")), ("2", ("KR_PF", "2"))])
+def test_host_pipeline_groups_bitwise(groups, knob, monkeypatch):
+    """kr_engine_ax / kr_engine_atx pipelined over board groups (each group's
+    whole product on two streams, widest slices first) give the bits of the
+    oracle, under every dispatch-order and prefetch variant."""
     monkeypatch.setenv("KR_GROUPS", groups)
+    if knob:
+        monkeypatch.setenv(*knob)
     ps = [H.builtin("river_full", seed=10 + k, board=b, deck=26, tree=3)
           for k, b in enumerate(["Kc9d7c4d2c", "Ac8d6c3d2d", "QcJd9c5d3c", "Tc7d5c4d2c"])]
     os_ = [po.Instance.builtin("river_full", seed=10 + k, board=b, deck=26, tree=3)
@@ -186,3 +190,25 @@ def test_host_pipeline_groups_bitwise(groups, monkeypatch):
     ex = np.concatenate([sp.matvec(x[cx[b]:cx[b + 1]]) for b, sp in enumerate(sps)])
     ey = np.concatenate([sp.matvec_t(y[cy[b]:cy[b + 1]]) for b, sp in enumerate(sps)])
     assert bits_equal(ax, ex) and bits_equal(aty, ey)
+
+
+@pytest.mark.parametrize("kind", ["factored", "implicit"])
+def test_pair_device_is_bitwise_ax_then_atx(kind):
+    """kr_engine_pair_device (A^T y forked onto a side stream, own scratch)
+    gives the bits of kr_engine_ax_device then kr_engine_atx_device, also
+    when repeated back to back on the same buffers."""
+    import torch
+    boards = H.turn_instances(nboards=3, factors=kind == "factored")
+    eng = CudaEngine([f for _, f in boards]) if kind == "factored" else CudaEngine.kron([i for i, _ in boards])
+    x = torch.randn(eng.cols, dtype=torch.float64, device="cuda")
+    y = torch.randn(eng.rows, dtype=torch.float64, device="cuda")
+    ax, atx = torch.empty(eng.rows, dtype=torch.float64, device="cuda"), torch.empty(eng.cols, dtype=torch.float64,
+                                                                                     device="cuda")
+    ax2, atx2 = torch.empty_like(ax), torch.empty_like(atx)
+    torch.cuda.synchronize()
+    eng.ax_device(x.data_ptr(), ax.data_ptr())
+    eng.atx_device(y.data_ptr(), atx.data_ptr())
+    for _ in range(3):
+        eng.pair_device(x.data_ptr(), ax2.data_ptr(), y.data_ptr(), atx2.data_ptr())
+    torch.cuda.ExternalStream(eng.stream).synchronize()
+    assert torch.equal(ax, ax2) and torch.equal(atx, atx2)

@@ -57,7 +57,7 @@ def e2e_pairs(eng, reps):
 
 
 if __name__ == "__main__":
-    groups = [int(g) for g in sys.argv[1:]] or [1, 2, 4, 8]
+    groups = [int(g) for g in sys.argv[1:] if g.isdigit()] or [1, 2, 4, 8]
     boards = H.turn_instances("Ks7d4c2h", 48, 3)
     ref = None
     for G in groups:
@@ -69,7 +69,7 @@ if __name__ == "__main__":
         print(json.dumps({"engine": "factored", "groups": G, "device_pairs_s": d, "e2e_pairs_s": e,
                           "same_as_first": bool(np.array_equal(out, ref))}), flush=True)
         eng.close()
-    for G in groups:
+    for G in groups if "--factored" not in sys.argv else []:
         os.environ["KR_GROUPS"] = str(G)
         eng = CudaEngine.kron([i for i, _ in boards])
         d = device_pairs(eng, 300)

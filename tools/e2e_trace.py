@@ -33,3 +33,6 @@ for e in sorted(ev, key=lambda e: e.time_range.start):
     print(f"{(e.time_range.start - t0):9.1f} {(e.time_range.end - t0):9.1f}  {e.name[:60]}")
 cpu = [e for e in prof.events() if e.device_type.name == "CPU"]
 print("cpu span us", max(e.time_range.end for e in cpu) - min(e.time_range.start for e in cpu))
+if "--api" in sys.argv:  # runtime API calls on the host timeline (same origin)
+    for e in sorted((e for e in cpu if e.name.startswith("cuda")), key=lambda e: e.time_range.start):
+        print(f"API {(e.time_range.start - t0):9.1f} {(e.time_range.end - t0):9.1f}  {e.name[:40]}")
