@@ -57,6 +57,13 @@ struct kr_solver {
     double* a[2] = {nullptr, nullptr};  // normalised averages at checkpoints
     double* handval = nullptr;  // per-hand best-response values
     double* boardval = nullptr; // per-board sums
+    // player 2's checkpoint best response runs beside player 1's on `side`
+    // (own gradient / hand scratch; the engine's A^T y has its own scratch)
+    double* g2 = nullptr;
+    double* handval2 = nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t evFork = nullptr, evJoin = nullptr;
+    bool brSerial = false;      // KR_BR_SERIAL: one after the other on the solver stream
     int* d_flag = nullptr;
     int nt[2] = {64, 64};       // hands per block of the step kernel
     int64_t launches = 0;
@@ -680,25 +687,48 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
 // Per-board best-response totals of `player` against device strategy `opp`,
 // written to device memory `dst` (nboards values), nothing synchronised.
 void best_response_to(kr_solver* s, int player, const double* opp, double* dst, cudaStream_t st,
-                      const int* slot = nullptr, int64_t slotStride = 0) {
+                      const int* slot = nullptr, int64_t slotStride = 0, double* g = nullptr,
+                      double* handval = nullptr) {
     kr_engine* e = s->eng;
-    if (player == 0) engine_ax(e, opp, s->g, st);
-    else engine_atx(e, opp, s->g, st);
+    if (!g) g = s->g;
+    if (!handval) handval = s->handval;
+    if (player == 0) engine_ax(e, opp, g, st);
+    else engine_atx(e, opp, g, st);
     const int nn = s->nnodes[player], n = s->n[player];
     const int bt = 128;
     const int na = s->na[player];
     const size_t smem = size_t((2 * nn + 1 + na + 2) * 4) + size_t(n + 1) * bt * 8 + 16;
     const unsigned grid = unsigned((s->H[player] + bt - 1) / bt);
     if (grid) {
-        k_best_response<<<grid, bt, smem, st>>>(s->d_tree[player], nn, n, s->H[player], s->g, player == 1,
-                                                s->handval, nullptr);
+        k_best_response<<<grid, bt, smem, st>>>(s->d_tree[player], nn, n, s->H[player], g, player == 1, handval,
+                                                nullptr);
         KR_CK_LAUNCH();
         s->launches++;
     }
-    k_board_sums<<<unsigned(s->nboards), 256, 0, st>>>(s->handval, s->d_bstart[player], s->nboards, dst, slot,
+    k_board_sums<<<unsigned(s->nboards), 256, 0, st>>>(handval, s->d_bstart[player], s->nboards, dst, slot,
                                                         slotStride);
     KR_CK_LAUNCH();
     s->launches++;
+}
+
+// Both checkpoint best responses (br1 vs avg2 into dst0, br2 vs avg1 into
+// dst1): player 2's forks onto the solver's side stream and joins back, so
+// the two products and walks overlap (inside a graph capture they become
+// parallel branches).  Each has its own scratch, so the values are the bits
+// of the serial order.
+void best_responses(kr_solver* s, double* dst0, double* dst1, cudaStream_t st, const int* slot = nullptr,
+                    int64_t slotStride = 0) {
+    if (s->brSerial || !s->side) {
+        best_response_to(s, 0, s->a[1], dst0, st, slot, slotStride);
+        best_response_to(s, 1, s->a[0], dst1, st, slot, slotStride);
+        return;
+    }
+    KR_CK(cudaEventRecord(s->evFork, st));
+    KR_CK(cudaStreamWaitEvent(s->side, s->evFork, 0));
+    best_response_to(s, 1, s->a[0], dst1, s->side, slot, slotStride, s->g2, s->handval2);
+    best_response_to(s, 0, s->a[1], dst0, st, slot, slotStride);
+    KR_CK(cudaEventRecord(s->evJoin, s->side));
+    KR_CK(cudaStreamWaitEvent(st, s->evJoin, 0));
 }
 
 // The same, copied to the host (synchronises the stream).
@@ -726,6 +756,11 @@ void destroy_solver(kr_solver* s) {
     cudaFree(s->g);
     cudaFree(s->handval);
     cudaFree(s->boardval);
+    cudaFree(s->g2);
+    cudaFree(s->handval2);
+    if (s->side) cudaStreamDestroy(s->side);
+    if (s->evFork) cudaEventDestroy(s->evFork);
+    if (s->evJoin) cudaEventDestroy(s->evJoin);
     cudaFree(s->d_flag);
     delete s;
 }
@@ -835,7 +870,15 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 throw Fail{KR_INVALID_INPUT, "treeplex x hands does not match the engine dimensions"};
             s->g = krb::dev_alloc<double>(std::max<int64_t>(std::max(e->rows, e->cols), 1));
             s->handval = krb::dev_alloc<double>(std::max<int64_t>(std::max(s->H[0], s->H[1]), 1));
-            s->boardval = krb::dev_alloc<double>(nboards);
+            s->boardval = krb::dev_alloc<double>(2 * int64_t(nboards));
+            s->brSerial = std::getenv("KR_BR_SERIAL") != nullptr;
+            if (!s->brSerial) {
+                s->g2 = krb::dev_alloc<double>(std::max<int64_t>(std::max(e->rows, e->cols), 1));
+                s->handval2 = krb::dev_alloc<double>(std::max<int64_t>(std::max(s->H[0], s->H[1]), 1));
+                KR_CK(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+                KR_CK(cudaEventCreateWithFlags(&s->evFork, cudaEventDisableTiming));
+                KR_CK(cudaEventCreateWithFlags(&s->evJoin, cudaEventDisableTiming));
+            }
             s->d_flag = krb::dev_alloc<int>(1);
             const int bsm0 = int((2 * s->nnodes[0] + 1 + s->treeLen[0] + 4) * 4 + (s->n[0] + 1) * 128 * 8 + 16);
             const int bsm1 = int((2 * s->nnodes[1] + 1 + s->treeLen[1] + 4) * 4 + (s->n[1] + 1) * 128 * 8 + 16);
@@ -923,8 +966,7 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
             krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);             // P2
             if (withCk) {
                 normalise_averages(s, st, true);                                     // solver.hpp:390-391
-                krb::best_response_to(s, 0, s->a[1], dck, st, s->d_cnt + 1, 2 * nb);
-                krb::best_response_to(s, 1, s->a[0], dck + nb, st, s->d_cnt + 1, 2 * nb);
+                krb::best_responses(s, dck, dck + nb, st, s->d_cnt + 1, 2 * nb);
                 krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 1);
                 KR_CK_LAUNCH();
                 s->launches++;
@@ -1033,11 +1075,14 @@ int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2) {
         KR_CK(cudaSetDevice(s->device));
         cudaStream_t st = s->eng->stream;
         normalise_averages(s, st);                            // solver.hpp:390-391
-        std::vector<double> b1, b2;
-        krb::best_response_dev(s, 0, s->a[1], b1, st);        // br1 vs avg2 (solver.hpp:327)
-        krb::best_response_dev(s, 1, s->a[0], b2, st);        // br2 vs avg1 (solver.hpp:328)
-        std::memcpy(board_br1, b1.data(), 8 * b1.size());
-        std::memcpy(board_br2, b2.data(), 8 * b2.size());
+        const size_t nb = size_t(s->nboards);
+        // br1 vs avg2, br2 vs avg1 (solver.hpp:327-328), side by side
+        krb::best_responses(s, s->boardval, s->boardval + nb, st);
+        std::vector<double> b(2 * nb);
+        KR_CK(cudaMemcpyAsync(b.data(), s->boardval, 8 * b.size(), cudaMemcpyDeviceToHost, st));
+        KR_CK(cudaStreamSynchronize(st));
+        std::memcpy(board_br1, b.data(), 8 * nb);
+        std::memcpy(board_br2, b.data() + nb, 8 * nb);
     });
 }
 
@@ -1138,8 +1183,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
                         ck(kr_solver_iterate(s, next - s->t));
                         double* slot = dck + size_t(at.size()) * 2 * nb;
                         normalise_averages(s, st);                             // solver.hpp:390-391
-                        krb::best_response_to(s, 0, s->a[1], slot, st);       // br1 vs avg2
-                        krb::best_response_to(s, 1, s->a[0], slot + nb, st);  // br2 vs avg1
+                        krb::best_responses(s, slot, slot + nb, st);  // br1 vs avg2, br2 vs avg1
                         at.push_back(s->t);
                     }
                 }
