@@ -49,12 +49,24 @@ def test_products_bitwise(name, kw, tech, post):
     check_engine(eng, o.sparsify(tech, post), p.rows, p.cols, np.random.default_rng(17))
 
 
-def test_config2_products_bitwise():
+@pytest.mark.parametrize("board,v", [("Ks7d4c2h9s", 3390846), ("AhKhQh7c7d", 2049828)], ids=["dry", "wet"])
+def test_config2_products_bitwise(board, v):
+    """Config 2 on the dry board and the wet one SURVEY.md §8(d) also names."""
+    p = H.builtin("river_full", seed=1, board=board, tree=3)
+    o = po.Instance.builtin("river_full", seed=1, board=board, tree=3)
+    eng = CudaEngine(p.sparsify("b", True))
+    assert eng.nnz == {"ahat": 2754388, "u": 61617, "m": 62697, "v": v}
+    check_engine(eng, o.sparsify("b", True), p.rows, p.cols, np.random.default_rng(3), trials=2)
+
+
+def test_config2_technique_a_bitwise():
+    """Config 2 through Technique A (the peel hits its rank cap of 1000, so
+    U and V carry the low-rank term at full size)."""
     p = H.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=3)
     o = po.Instance.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=3)
-    eng = CudaEngine(p.sparsify("b", True))
-    assert eng.nnz == {"ahat": 2754388, "u": 61617, "m": 62697, "v": 3390846}
-    check_engine(eng, o.sparsify("b", True), p.rows, p.cols, np.random.default_rng(3), trials=2)
+    eng = CudaEngine(p.sparsify("a", True))
+    assert eng.nnz == {"ahat": 9666364, "u": 795578, "m": 29028, "v": 795578}
+    check_engine(eng, o.sparsify("a", True), p.rows, p.cols, np.random.default_rng(9), trials=1)
 
 
 def test_config4_technique_a_bitwise():

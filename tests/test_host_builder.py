@@ -66,13 +66,26 @@ def test_generic_postprocess_matches_closed_form():
         assert factors_equal(p.sparsify("a", False).postprocess().factors(), p.sparsify("a", True).factors())
 
 
-@pytest.mark.parametrize("board,deck,tech", [("Kc9d7c4d2c", 26, "b"), ("Kc9d7c4d2c", 26, "a"),
-                                             ("Ks7d4c2h9s", 52, "b")])
+# SURVEY.md §8(a) sizing table: (ahat, u, m, v) after postprocessing, dense nnz
+SIZES = {("Kc9d7c4d2c", 26, "b"): ((229320, 11970, 12179, 301071), 2045246),
+         ("Kc9d7c4d2c", 26, "a"): ((470455, 157057, 29028, 159957), 2045246),
+         ("Ks7d4c2h9s", 52, "b"): ((2754388, 61617, 62697, 3390846), 60755142),
+         ("AhKhQh7c7d", 52, "b"): ((2754388, 61617, 62697, 2049828), 53173092),
+         ("Ks7d4c2h9s", 52, "a"): ((9666364, 795578, 29028, 795578), 60755142)}  # rank 1000 (peel cap)
+
+
+@pytest.mark.parametrize("board,deck,tech", list(SIZES))
 def test_synthetic_configs_bit_exact(board, deck, tech):
+    """Configs 2 (dry and wet board) and 4: structure bit-exact against the
+    oracle, and the sizes of SURVEY.md §8(a)."""
     o = po.Instance.builtin("river_full", seed=1, board=board, deck=deck, tree=3)
     p = H.builtin("river_full", seed=1, board=board, deck=deck, tree=3)
     assert o.hands(0) == p.hands(0)
-    assert factors_equal(o.sparsify(tech, True).factors(), p.sparsify(tech, True).factors())
+    f = p.sparsify(tech, True).factors()
+    assert factors_equal(o.sparsify(tech, True).factors(), f)
+    nnz, dense = SIZES[(board, deck, tech)]
+    assert tuple(int(f[k][0][-1]) for k in ("ahat", "u", "m", "v")) == nnz
+    assert p.dense_nnz() == dense
 
 
 def test_json_loader_matches_constructors(instance_fixtures, tmp_path):
