@@ -219,6 +219,72 @@ def config1_gpu():
             "_trace": r.trace_expl}
 
 
+def config2_gpu(peak):
+    """BASELINE configs[1] (config 2): one river board Ks7d4c2h9s, 1,081 hands
+    per side, 3-bet tree, B-post (6.27e6 stored nonzeros, 76 MB per product).
+    Kernels this small are latency-bound, so besides the serial pair it
+    reports the concurrent pair (kr_engine_pair_device), K7 and the solver."""
+    import torch
+
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200 import host as H
+    from paper_2112_03804_b200.solver import DcfrParams, solver_for
+    inst = H.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=3)
+    f = inst.sparsify("b", True)
+    eng, ek = CudaEngine(f), CudaEngine.kron([inst])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device="cpu").manual_seed(2)
+    x = torch.randn(eng.cols, dtype=torch.float64, generator=g).to(dev)
+    y = torch.randn(eng.rows, dtype=torch.float64, generator=g).to(dev)
+    outs = [torch.empty(n, dtype=torch.float64, device=dev) for n in (eng.rows, eng.cols) * 3]
+
+    def timed(e, fn, reps=300):
+        st = torch.cuda.ExternalStream(e.stream)
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3
+
+    def serial():
+        eng.ax_device(x.data_ptr(), outs[0].data_ptr())
+        eng.atx_device(y.data_ptr(), outs[1].data_ptr())
+
+    def pair():
+        eng.pair_device(x.data_ptr(), outs[2].data_ptr(), y.data_ptr(), outs[3].data_ptr())
+
+    def kron():
+        ek.ax_device(x.data_ptr(), outs[4].data_ptr())
+        ek.atx_device(y.data_ptr(), outs[5].data_ptr())
+
+    us_serial, us_pair, us_k7 = timed(eng, serial), timed(eng, pair), timed(ek, kron)
+    torch.cuda.synchronize(dev)
+    bitwise = bool(torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3]))
+    k7_diff = max(float((outs[4] - outs[0]).abs().max() / (1 + outs[0].abs().max())),
+                  float((outs[5] - outs[1]).abs().max() / (1 + outs[1].abs().max())))
+    pair_bytes = 2 * eng.bytes_per_product()
+    solver = {}
+    for name, implicit in (("factored", False), ("implicit", True)):
+        sv = solver_for([(inst, f)], implicit=implicit)
+        sv.run(DcfrParams(max_iters=10, checkpoint_every=10))
+        r = sv.run(DcfrParams(max_iters=400, checkpoint_every=50), want_avg=False)
+        solver[name] = {"iters_per_s": 400 / r.seconds, "exploitability": r.exploitability}
+    return {"workload": "config2: river Ks7d4c2h9s, 1,081 hands per side, 3-bet tree (n=43), B-post",
+            "nnz_stored": int(f.size()), "algorithmic_bytes_per_pair": pair_bytes,
+            "us_per_pair": us_serial, "pairs_per_s": 1e6 / us_serial,
+            "whole_pair_frac_of_peak": pair_bytes / (us_serial / 1e6) / 1e9 / peak,
+            "concurrent_pair": {"api": "kr_engine_pair_device", "us_per_pair": us_pair,
+                                "pairs_per_s": 1e6 / us_pair, "bitwise_equal_to_serial": bitwise},
+            "implicit": {"us_per_pair": us_k7, "pairs_per_s": 1e6 / us_k7, "normwise_diff_vs_factored": k7_diff,
+                         "tolerance": 1e-12},
+            "solver_checkpoint_every_50": solver}
+
+
 def config1_cpu(gpu):
     """The same 1000 CFR+ iterations on the oracle (CPU, one thread) and the
     bitwise cross-check of the GPU trace against it."""
@@ -441,6 +507,7 @@ def run_product(args):
                             sum_over_ranks)
     turn = run_turn(rank, world, local, max_over_ranks, dist.group.WORLD if world > 1 else None)
     config1 = config1_gpu() if rank == 0 else None
+    config2 = config2_gpu(measured_peak()[0]) if rank == 0 else None
 
     if rank != 0:
         return 0
@@ -477,6 +544,7 @@ def run_product(args):
         "clocks": sampler.summary(),
         "implicit": implicit,
         "config1": {k: v for k, v in config1.items() if not k.startswith("_")},
+        "config2": config2,
         "turn": turn,
     }
     if world == 1 and not args.no_cpu_baseline:
