@@ -79,7 +79,10 @@ def main():
             lines.append(f"| {r[kn].split('(')[0].split('::')[-1]} | {val('gpu__time_duration.sum') * 1e6:.1f} | "
                          f"{val('dram__bytes_read.sum') / 1e6:.1f} | {val('dram__bytes_write.sum') / 1e6:.2f} |")
     ks = launches(lcsv)
-    pair = ks[-7:]
+    # the first whole-range pair: seq_major, VT, chain, UA, UT, chain^T, AV
+    first = next((i for i in range(len(ks) - 6) if ks[i][0].startswith("k_seq_major")
+                  and ks[i + 6][0].startswith("k_spmv")), max(0, len(ks) - 7))
+    pair = ks[first:first + 7]
     tot = sum(t for _, t in pair)
     lines += ["", "## One matvec pair, launch list (cold-cache, serialised: compare shares)", "",
               "| kernel | ns | share |", "|---|---|---|"]
