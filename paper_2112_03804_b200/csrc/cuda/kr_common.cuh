@@ -174,8 +174,8 @@ struct kr_engine {
     std::vector<int64_t> grpRow{0}, grpCol{0};
     std::vector<int64_t> bSl[4], bNl[4];
     std::vector<int32_t> grpBoard{0};
-    cudaStream_t copyIn = nullptr, copyOut = nullptr, stage2 = nullptr;
-    std::vector<cudaEvent_t> evIn, evOut, evMid;
+    cudaStream_t copyIn = nullptr, copyOut = nullptr, stage2 = nullptr, stage3 = nullptr;
+    std::vector<cudaEvent_t> evIn, evOut, evMid, evSolve;
     // kr_engine_pair_device: A^T y forks onto `side` (created on first use)
     cudaStream_t side = nullptr;
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
@@ -188,6 +188,7 @@ void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s);
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s);
 // Copy streams and events for the pipelined host-buffer calls (>= 2 groups).
 void engine_make_pipeline(kr_engine* e);
+std::vector<int> group_ends(int nb, uint32_t flags);
 // Shared-memory limits of the chain-solve kernels (engines built elsewhere).
 void engine_chain_setup(kr_engine* e);
 }  // namespace krb

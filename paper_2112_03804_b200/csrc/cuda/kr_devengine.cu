@@ -731,11 +731,7 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
         e->d_out = dev_alloc<double>(std::max<int64_t>(std::max(rowsTotal, colsTotal), 1));
         e->lean = std::getenv("KR_NO_LEAN") == nullptr;
         // board groups for the host-buffer pipeline
-        int G = (flags & KR_FLAG_SINGLE_PART) ? 1 : 6;  // as group_count (kr_engine.cu)
-        if (const char* env = std::getenv("KR_GROUPS")) G = std::atoi(env);
-        G = std::max(1, std::min(G, nb));
-        for (int g = 0; g < G; ++g) {
-            const int g1 = int(int64_t(nb) * (g + 1) / G);
+        for (int g1 : group_ends(nb, flags)) {
             e->grpBoard.push_back(g1);
             e->grpRow.push_back(g1 < nb ? bh[size_t(g1)].dev.rowOff : rowsTotal);
             e->grpCol.push_back(g1 < nb ? bh[size_t(g1)].dev.colOff : colsTotal);

@@ -979,7 +979,9 @@ void destroy_engine(kr_engine* e) {
     if (e->copyIn) cudaStreamDestroy(e->copyIn);
     if (e->copyOut) cudaStreamDestroy(e->copyOut);
     if (e->stage2) cudaStreamDestroy(e->stage2);
+    if (e->stage3) cudaStreamDestroy(e->stage3);
     for (cudaEvent_t ev : e->evMid) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->evSolve) cudaEventDestroy(ev);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->evFork) cudaEventDestroy(e->evFork);
     if (e->evJoin) cudaEventDestroy(e->evJoin);
@@ -1284,9 +1286,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         }
         e->lean = std::getenv("KR_NO_LEAN") == nullptr;
         if (const char* env = std::getenv("KR_PF")) e->pf = std::max(0, std::atoi(env));
-        const int G = group_count(nb, flags);
-        for (int g = 0; g < G; ++g) {
-            const int g1 = int(int64_t(nb) * (g + 1) / G);
+        for (int g1 : group_ends(nb, flags)) {
             e->grpBoard.push_back(g1);
             e->grpRow.push_back(g1 < nb ? plan[size_t(g1)].rowOff : R);
             e->grpCol.push_back(g1 < nb ? plan[size_t(g1)].colOff : Cc);
@@ -1353,13 +1353,17 @@ void make_pipeline(kr_engine* e) {
     KR_CK(cudaStreamCreateWithFlags(&e->copyIn, cudaStreamNonBlocking));
     KR_CK(cudaStreamCreateWithFlags(&e->copyOut, cudaStreamNonBlocking));
     KR_CK(cudaStreamCreateWithFlags(&e->stage2, cudaStreamNonBlocking));
+    const char* ps = std::getenv("KR_PIPE_STREAMS");
+    if (!(ps && std::atoi(ps) == 2)) KR_CK(cudaStreamCreateWithFlags(&e->stage3, cudaStreamNonBlocking));
     e->evIn.resize(size_t(G));
     e->evOut.resize(size_t(G));
     e->evMid.resize(size_t(G));
+    e->evSolve.resize(size_t(G));
     for (int g = 0; g < G; ++g) {
         KR_CK(cudaEventCreateWithFlags(&e->evIn[size_t(g)], cudaEventDisableTiming));
         KR_CK(cudaEventCreateWithFlags(&e->evOut[size_t(g)], cudaEventDisableTiming));
         KR_CK(cudaEventCreateWithFlags(&e->evMid[size_t(g)], cudaEventDisableTiming));
+        KR_CK(cudaEventCreateWithFlags(&e->evSolve[size_t(g)], cudaEventDisableTiming));
     }
 }
 
@@ -1498,6 +1502,35 @@ void solve_backward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -
 // accounting.  Pointers address the whole vectors.
 void engine_make_pipeline(kr_engine* e) { make_pipeline(e); }
 
+// End board of each board group: G equal groups (group_count), or groups
+// weighted by KR_GROUP_SIZES ("2,4,8,...": relative sizes, scaled to nb).
+std::vector<int> group_ends(int nb, uint32_t flags) {
+    std::vector<int> ends;
+    const char* env = std::getenv("KR_GROUP_SIZES");
+    if (env && !(flags & KR_FLAG_SINGLE_PART)) {
+        std::vector<double> w;
+        for (const char* p = env; *p;) {
+            char* q = nullptr;
+            const double v = std::strtod(p, &q);
+            if (q == p) break;
+            if (v > 0) w.push_back(v);
+            p = *q == ',' ? q + 1 : q;
+        }
+        double tot = 0, cum = 0;
+        for (double v : w) tot += v;
+        for (double v : w) {
+            cum += v;
+            const int g1 = std::min(nb, int(std::lround(nb * cum / tot)));
+            if (g1 > (ends.empty() ? 0 : ends.back())) ends.push_back(g1);
+        }
+        if (!ends.empty() && ends.back() != nb) ends.back() = nb;
+        if (!ends.empty()) return ends;
+    }
+    const int G = group_count(nb, flags);
+    for (int g = 0; g < G; ++g) ends.push_back(int(int64_t(nb) * (g + 1) / G));
+    return ends;
+}
+
 void engine_chain_setup(kr_engine*) {
     const size_t smem = size_t(kStages) * kChunkRows * 32 * sizeof(double) * 2;
     raise_smem_limit(k_chain_tma<1>, smem);
@@ -1621,37 +1654,58 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
         const size_t a = size_t(oo[size_t(g)]), n = size_t(oo[size_t(g) + 1]) - a;
         KR_CK(cudaMemcpyAsync(hout + a, e->d_out + a, 8 * n, cudaMemcpyDeviceToHost, e->copyOut));
     };
-    for (int g = 0; g < G; ++g) {
-        const size_t a = size_t(io[size_t(g)]), n = size_t(io[size_t(g) + 1]) - a;
-        KR_CK(cudaMemcpyAsync(e->d_in + a, hin + a, 8 * n, cudaMemcpyHostToDevice, e->copyIn));
-        KR_CK(cudaEventRecord(e->evIn[size_t(g)], e->copyIn));
-    }
+    // Input copies run two groups ahead of the kernel enqueue: group g's
+    // kernels are queued before its input lands (enqueueing every copy first
+    // delayed the first kernels by ~30 us of host time), and copy g+2 is
+    // enqueued while copy g+1 (~60 us on the bus) is still running, since a
+    // group's kernels take the host ~40-90 us to enqueue.
+    int nextIn = 0;
+    auto copy_in = [&](int upto) {
+        for (; nextIn < std::min(upto + 1, G); ++nextIn) {
+            const int g = nextIn;
+            const size_t a = size_t(io[size_t(g)]), n = size_t(io[size_t(g) + 1]) - a;
+            KR_CK(cudaMemcpyAsync(e->d_in + a, hin + a, 8 * n, cudaMemcpyHostToDevice, e->copyIn));
+            KR_CK(cudaEventRecord(e->evIn[size_t(g)], e->copyIn));
+        }
+    };
     // Every factor is block diagonal over boards, and so is M's chain solve
     // (chain slices per board, bCh): with chains (or none) a group's whole
-    // product runs as soon as its input has arrived.  Its M solve and last
-    // SpMV run on stage2 while the next group's first SpMV streams on the
-    // main stream (the latency-bound solve hides under it, and each kernel's
-    // tail under the other's); its output copy follows on copyOut.  The
-    // level solve (mkind 2) spans boards, so there it waits for every
-    // group's first stage.
+    // product runs as soon as its input has arrived: its first SpMV on the
+    // main stream, its M solve on stage3 (latency-bound: it hides under the
+    // SpMVs of the groups around it), its last SpMV on stage2 while the next
+    // group's first SpMV streams on the main stream (each kernel's tail under
+    // the other's), its output copy on copyOut.  The level solve (mkind 2)
+    // spans boards, so there it waits for every group's first stage.
     if (e->kron) {
         for (int g = 0; g < G; ++g) {
+            copy_in(g + 1);
             KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
             last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
             copy_out(g, e->stream);
         }
     } else if (e->mkind == 0 ||
                (e->mkind == 1 && int64_t(e->bCh.size()) == int64_t(e->grpBoard.back()) + 1)) {
+        // KR_PIPE_STREAMS=2: the M solve on stage2 ahead of the last SpMV
+        const bool three = e->stage3 != nullptr;
         for (int g = 0; g < G; ++g) {
+            copy_in(g + 1);
             KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
             first_stage(e, dir, e->d_in, e->stream, g);
             KR_CK(cudaEventRecord(e->evMid[size_t(g)], e->stream));
-            KR_CK(cudaStreamWaitEvent(e->stage2, e->evMid[size_t(g)], 0));
-            middle(e, dir, e->stage2, g);
+            if (three) {  // the latency-bound solve on its own stream
+                KR_CK(cudaStreamWaitEvent(e->stage3, e->evMid[size_t(g)], 0));
+                middle(e, dir, e->stage3, g);
+                KR_CK(cudaEventRecord(e->evSolve[size_t(g)], e->stage3));
+                KR_CK(cudaStreamWaitEvent(e->stage2, e->evSolve[size_t(g)], 0));
+            } else {
+                KR_CK(cudaStreamWaitEvent(e->stage2, e->evMid[size_t(g)], 0));
+                middle(e, dir, e->stage2, g);
+            }
             last_stage(e, dir, e->d_in, e->d_out, e->stage2, g);
             copy_out(g, e->stage2);
         }
     } else {
+        copy_in(G - 1);
         for (int g = 0; g < G; ++g) {
             KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
             first_stage(e, dir, e->d_in, e->stream, g);
