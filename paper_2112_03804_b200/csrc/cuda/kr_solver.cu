@@ -1300,6 +1300,10 @@ struct kr_turn_solver {
     void (*exchange)(void*) = nullptr;
     void* user = nullptr;
     bool ownExtra = true;
+    // graph replay (one GPU, no exchange): per-iteration pos/neg/shrink from
+    // a device table indexed by the device iteration counter
+    double* d_fac = nullptr;
+    int* d_cnt = nullptr;
 };
 
 namespace krb {
@@ -1320,7 +1324,9 @@ __global__ void k_turn_gather(const double* __restrict__ root, const int32_t* __
 
 __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, const double* __restrict__ xturn,
                               const int32_t* __restrict__ r2t, int64_t Hr, int nr, int nt, int sigma,
-                              double shrink, int doAvg) {
+                              double shrink, int doAvg, const double* __restrict__ fac = nullptr,
+                              const int* __restrict__ dt = nullptr) {
+    if (fac) shrink = fac[3 * *dt + 2];  // graph replay
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= Hr * nr) return;
     const int64_t r = q / nr;
@@ -1355,26 +1361,28 @@ constexpr int kTurnTeam = 4;
 
 void team_step(kr_turn_solver* s, const kr_turn_solver::TreeDev& T, int64_t H, int mode, const double* g, int negate,
                double* regret, double* x, double* avg, double pos, double neg, double shrink, int noAvg,
-               double* rootOut, const double* extra, cudaStream_t st) {
+               double* rootOut, const double* extra, cudaStream_t st, const double* fac, const int* dt) {
     const int hpb = 256 / kTurnTeam;
     const unsigned grid = unsigned((H + hpb - 1) / hpb);
     if (!grid) return;
     const size_t smem = team_smem(T.n, T.nn, hpb, T.len);
     k_player_team<kTurnTeam><<<grid, 256, smem, st>>>(mode, T.d, T.nn, T.n, T.na, T.len, H, hpb, g, negate, regret, x,
-                                                      avg, pos, neg, shrink, s->rule, nullptr, nullptr, noAvg,
-                                                      rootOut, extra);
+                                                      avg, pos, neg, shrink, s->rule, fac, dt, noAvg, rootOut,
+                                                      extra);
     KR_CK_LAUNCH();
     s->launches++;
 }
 
 // Player p's half-iteration (mode 1) or initial strategy (mode 0).
-void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, double shrink, cudaStream_t st) {
+// fac / dt: graph replay (the factors from the device table, else the scalars).
+void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, double shrink, cudaStream_t st,
+                 const double* fac = nullptr, const int* dt = nullptr) {
     const int nt = s->turnTree[p].n;
     KR_CK(cudaMemsetAsync(s->extra, 0, 8 * size_t(s->m) * nt, st));
     for (int t = 0; t < s->T; ++t) {
         const int64_t o = s->off[p][size_t(t) + 1];
         team_step(s, s->riverTree[p][size_t(t)], s->Hr, mode, s->g + o, p == 1, s->regret[p] + o, s->x[p] + o,
-                  s->avg[p] + o, pos, neg, shrink, 1, mode == 1 ? s->root : nullptr, nullptr, st);
+                  s->avg[p] + o, pos, neg, shrink, 1, mode == 1 ? s->root : nullptr, nullptr, st, fac, dt);
         if (mode == 1) {
             k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root, s->d_t2r, s->d_boff, s->nb, s->m,
                                                                          nt, s->sigma[p][size_t(t)], s->extra);
@@ -1387,13 +1395,14 @@ void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, dou
         s->exchange(s->user);
     }
     team_step(s, s->turnTree[p], s->m, mode, s->g, p == 1, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, 0,
-              nullptr, mode == 1 ? s->extra : nullptr, st);
+              nullptr, mode == 1 ? s->extra : nullptr, st, fac, dt);
     for (int t = 0; t < s->T; ++t) {
         const int64_t o = s->off[p][size_t(t) + 1];
         const int nr = s->riverTree[p][size_t(t)].n;
         const int64_t n = s->Hr * nr;
         k_river_scale<<<unsigned((n + 255) / 256), 256, 0, st>>>(s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr,
-                                                                  nr, nt, s->sigma[p][size_t(t)], shrink, mode == 1);
+                                                                  nr, nt, s->sigma[p][size_t(t)], shrink, mode == 1,
+                                                                  fac, dt);
         KR_CK_LAUNCH();
         s->launches++;
     }
@@ -1455,7 +1464,7 @@ void destroy_turn(kr_turn_solver* s) {
         cudaFree(s->x[p]);
         cudaFree(s->a[p]);
     }
-    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g, s->root, s->handval, s->bval, s->d_one};
+    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g, s->root, s->handval, s->bval, s->d_one, s->d_fac, s->d_cnt};
     for (void* q : ps) cudaFree(q);
     if (s->ownExtra) cudaFree(s->extra);
     delete s;
@@ -1581,13 +1590,61 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         krb::turn_player(s, 1, 0, 0, 0, 0, st);
         double ws = 0;
         r->trace_len = 0;
+        // One GPU (no exchange hook): every iteration replays one captured
+        // graph (tick, both gradients and player steps), its factors read
+        // from a device table filled with the loop's own expressions, so a
+        // replay is bitwise the launched iteration.  Checkpoints stay on the
+        // host path (their values are read back).  KR_NO_GRAPH: launch by launch.
+        cudaGraphExec_t exec = nullptr;
+        int64_t launchDelta = 0;
+        if (!s->exchange && !std::getenv("KR_NO_GRAPH")) {
+            std::vector<double> fac(size_t(3) * (prm->max_iters + 1), 0.0);
+            for (int t = 1; t <= prm->max_iters; ++t) {
+                fac[3 * size_t(t)] = krb::discount_factor(t, prm->alpha);
+                fac[3 * size_t(t) + 1] = krb::discount_factor(t, prm->beta);
+                fac[3 * size_t(t) + 2] = std::pow(double(t) / (t + 1), prm->gamma);
+            }
+            cudaFree(s->d_fac);
+            s->d_fac = nullptr;
+            s->d_fac = krb::dev_alloc<double>(int64_t(fac.size()));
+            if (!s->d_cnt) s->d_cnt = krb::dev_alloc<int>(2);
+            KR_CK(cudaMemcpyAsync(s->d_fac, fac.data(), 8 * fac.size(), cudaMemcpyHostToDevice, st));
+            KR_CK(cudaMemsetAsync(s->d_cnt, 0, 2 * sizeof(int), st));
+            KR_CK(cudaStreamSynchronize(st));
+            const int64_t l0 = s->launches;
+            cudaGraph_t gr;
+            KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 0);
+                KR_CK_LAUNCH();
+                s->launches++;
+                krb::turn_gradient(s, 0, s->x[1], s->g, st);
+                krb::turn_player(s, 0, 1, 0, 0, 0, st, s->d_fac, s->d_cnt);
+                krb::turn_gradient(s, 1, s->x[0], s->g, st);
+                krb::turn_player(s, 1, 1, 0, 0, 0, st, s->d_fac, s->d_cnt);
+            } catch (...) {
+                cudaStreamEndCapture(st, &gr);
+                throw;
+            }
+            KR_CK(cudaStreamEndCapture(st, &gr));
+            const cudaError_t ie = cudaGraphInstantiate(&exec, gr, 0);
+            cudaGraphDestroy(gr);
+            KR_CK(ie);
+            launchDelta = s->launches - l0;
+            s->launches = l0;
+        }
         for (int t = 1; t <= prm->max_iters; ++t) {
             const double pos = krb::discount_factor(t, prm->alpha), neg = krb::discount_factor(t, prm->beta);
             const double shrink = std::pow(double(t) / (t + 1), prm->gamma);
-            krb::turn_gradient(s, 0, s->x[1], s->g, st);        // g1 = A x2
-            krb::turn_player(s, 0, 1, pos, neg, shrink, st);
-            krb::turn_gradient(s, 1, s->x[0], s->g, st);        // A^T x1 (negated in the steps)
-            krb::turn_player(s, 1, 1, pos, neg, shrink, st);
+            if (exec) {
+                KR_CK(cudaGraphLaunch(exec, st));
+                s->launches += launchDelta;
+            } else {
+                krb::turn_gradient(s, 0, s->x[1], s->g, st);    // g1 = A x2
+                krb::turn_player(s, 0, 1, pos, neg, shrink, st);
+                krb::turn_gradient(s, 1, s->x[0], s->g, st);    // A^T x1 (negated in the steps)
+                krb::turn_player(s, 1, 1, pos, neg, shrink, st);
+            }
             ws += 1;
             ws *= shrink;
             if (t % prm->checkpoint_every == 0 || t == prm->max_iters) {
@@ -1614,6 +1671,7 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         }
         KR_CK(cudaEventRecord(ev1, st));
         KR_CK(cudaEventSynchronize(ev1));
+        if (exec) cudaGraphExecDestroy(exec);
         float ms = 0;
         KR_CK(cudaEventElapsedTime(&ms, ev0, ev1));
         r->seconds = ms / 1e3;

@@ -69,6 +69,16 @@ def test_turn_rules_match_checker(game, rule):
     assert e[-1] < 0.25 * e[0] and np.all(np.diff(e) < 0)
 
 
+def test_turn_graph_replay_is_bitwise(game, monkeypatch):
+    """One GPU: iterations replay a captured graph with the factors from a
+    device table; launching them one by one (KR_NO_GRAPH) gives the same bits."""
+    r = TurnSolver(game).run(max_iters=7, checkpoint_every=3, want_avg=True, rule=2)
+    monkeypatch.setenv("KR_NO_GRAPH", "1")
+    q = TurnSolver(game).run(max_iters=7, checkpoint_every=3, want_avg=True, rule=2)
+    for k in ("trace_br1", "trace_br2", "avg1", "avg2"):
+        assert np.array_equal(r[k], q[k]), k
+
+
 def test_turn_dcfr_converges(game):
     r = TurnSolver(game).run(max_iters=300, checkpoint_every=50)
     e = r["trace_expl"]
