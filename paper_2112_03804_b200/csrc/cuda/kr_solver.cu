@@ -1304,6 +1304,15 @@ struct kr_turn_solver {
     // a device table indexed by the device iteration counter
     double* d_fac = nullptr;
     int* d_cnt = nullptr;
+    int32_t* d_sigma = nullptr;                    // [2][T] sigma_p(t), for k_turn_gather_all
+    int64_t* d_roff = nullptr;                     // [2][T+1] river block offsets (from off[p][1])
+    int32_t* d_nr = nullptr;                       // [2][T] river sequences per continuation
+    // the continuations' independent river products and player steps run
+    // side by side: continuation t on side[t], forked from / joined into the
+    // solver stream (KR_TURN_SERIAL=1: all on the solver stream)
+    std::vector<cudaStream_t> side;
+    cudaEvent_t evFork = nullptr;
+    std::vector<cudaEvent_t> evJoin;
 };
 
 namespace krb {
@@ -1322,6 +1331,46 @@ __global__ void k_turn_gather(const double* __restrict__ root, const int32_t* __
     extra[int64_t(h) * nt + sigma - 1] += acc;
 }
 
+// All continuations' river root values summed into the turn hands at once:
+// for t = 0..T-1 in order, extra[h, sigma(t)] += sum over boards b ascending
+// of root[t][boff[b] + t2r[b][h]] (boards holding h skipped) -- the bits of
+// T k_turn_gather launches.  A block stages the (board, hand) values of 32
+// turn hands in shared memory with 8 independent loads per thread, then one
+// thread per hand adds them in board order (a thread walking its 48 boards
+// alone waited out ~96 dependent memory latencies).
+constexpr int kGatherHands = 32;
+__global__ void __launch_bounds__(256) k_turn_gather_all(const double* __restrict__ root, int64_t Hr,
+                                                         const int32_t* __restrict__ t2r,
+                                                         const int64_t* __restrict__ boff, int nb, int m, int nt,
+                                                         const int32_t* __restrict__ sigma, int T,
+                                                         double* __restrict__ extra) {
+    extern __shared__ double gv[];  // [nb][kGatherHands] values, NaN = board holds the hand
+    const int h0 = blockIdx.x * kGatherHands;
+    const int nh = min(kGatherHands, m - h0);
+    for (int t = 0; t < T; ++t) {
+        const double* rt = root + int64_t(t) * Hr;
+        for (int q = threadIdx.x; q < nb * kGatherHands; q += blockDim.x) {
+            const int b = q / kGatherHands, hh = q % kGatherHands;
+            double v = __longlong_as_double(0x7ff8000000000001LL);  // marker: skipped
+            if (hh < nh) {
+                const int r = t2r[int64_t(b) * m + h0 + hh];
+                if (r >= 0) v = rt[boff[b] + r];
+            }
+            gv[q] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < nh) {
+            double acc = 0.0;
+            for (int b = 0; b < nb; ++b) {
+                const double v = gv[b * kGatherHands + threadIdx.x];
+                if (__double_as_longlong(v) != 0x7ff8000000000001LL) acc += v;
+            }
+            extra[int64_t(h0 + threadIdx.x) * nt + sigma[t] - 1] += acc;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, const double* __restrict__ xturn,
                               const int32_t* __restrict__ r2t, int64_t Hr, int nr, int nt, int sigma,
                               double shrink, int doAvg, const double* __restrict__ fac = nullptr,
@@ -1331,6 +1380,25 @@ __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, 
     if (q >= Hr * nr) return;
     const int64_t r = q / nr;
     const double xv = xturn[int64_t(r2t[r]) * nt + sigma - 1] * x[q];
+    x[q] = xv;
+    if (doAvg) avg[q] = (avg[q] + xv) * shrink;  // solver.hpp:382-386
+}
+
+// Every continuation's river blocks of player p in one launch (the bits of T
+// k_river_scale launches): block t holds Hr x nr[t] entries at roff[t].
+__global__ void k_river_scale_all(double* __restrict__ x, double* __restrict__ avg,
+                                  const double* __restrict__ xturn, const int32_t* __restrict__ r2t, int64_t Hr,
+                                  int nt, int T, const int64_t* __restrict__ roff, const int32_t* __restrict__ nrs,
+                                  const int32_t* __restrict__ sigma, double shrink, int doAvg,
+                                  const double* __restrict__ fac, const int* __restrict__ dt) {
+    if (fac) shrink = fac[3 * *dt + 2];  // graph replay
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= roff[T]) return;
+    int t = 0;
+    while (q >= roff[t + 1]) ++t;
+    const int nr = nrs[t];
+    const int64_t r = (q - roff[t]) / nr;
+    const double xv = xturn[int64_t(r2t[r]) * nt + sigma[t] - 1] * x[q];
     x[q] = xv;
     if (doAvg) avg[q] = (avg[q] + xv) * shrink;  // solver.hpp:382-386
 }
@@ -1373,29 +1441,78 @@ void team_step(kr_turn_solver* s, const kr_turn_solver::TreeDev& T, int64_t H, i
     s->launches++;
 }
 
+// Continuation t's stream: side[t] between fork() and join(), else st.
+cudaStream_t cont_stream(kr_turn_solver* s, int t, cudaStream_t st) {
+    return s->side.empty() ? st : s->side[size_t(t)];
+}
+void fork(kr_turn_solver* s, cudaStream_t st) {
+    if (s->side.empty()) return;
+    KR_CK(cudaEventRecord(s->evFork, st));
+    for (cudaStream_t q : s->side) KR_CK(cudaStreamWaitEvent(q, s->evFork, 0));
+}
+void join(kr_turn_solver* s, cudaStream_t st) {
+    for (size_t t = 0; t < s->side.size(); ++t) {
+        KR_CK(cudaEventRecord(s->evJoin[t], s->side[t]));
+        KR_CK(cudaStreamWaitEvent(st, s->evJoin[t], 0));
+    }
+}
+
+// KR_TURN_FUSE=0: one gather and one scale launch per continuation instead
+// of one for all of them (the same bits).
+bool turn_fuse() {
+    const char* env = std::getenv("KR_TURN_FUSE");
+    return !(env && std::atoi(env) == 0);
+}
+
+// The river root values of every continuation into `extra` (one launch).
+void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
+    if (!turn_fuse()) {
+        for (int t = 0; t < s->T; ++t) {
+            k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root + int64_t(t) * s->Hr, s->d_t2r,
+                                                                         s->d_boff, s->nb, s->m, nt,
+                                                                         s->sigma[p][size_t(t)], s->extra);
+            KR_CK_LAUNCH();
+            s->launches++;
+        }
+        return;
+    }
+    const size_t smem = size_t(s->nb) * kGatherHands * sizeof(double);
+    k_turn_gather_all<<<unsigned((s->m + kGatherHands - 1) / kGatherHands), 256, smem, st>>>(
+        s->root, s->Hr, s->d_t2r, s->d_boff, s->nb, s->m, nt, s->d_sigma + p * s->T, s->T, s->extra);
+    KR_CK_LAUNCH();
+    s->launches++;
+}
+
 // Player p's half-iteration (mode 1) or initial strategy (mode 0).
 // fac / dt: graph replay (the factors from the device table, else the scalars).
 void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, double shrink, cudaStream_t st,
                  const double* fac = nullptr, const int* dt = nullptr) {
     const int nt = s->turnTree[p].n;
     KR_CK(cudaMemsetAsync(s->extra, 0, 8 * size_t(s->m) * nt, st));
+    fork(s, st);
     for (int t = 0; t < s->T; ++t) {
         const int64_t o = s->off[p][size_t(t) + 1];
         team_step(s, s->riverTree[p][size_t(t)], s->Hr, mode, s->g + o, p == 1, s->regret[p] + o, s->x[p] + o,
-                  s->avg[p] + o, pos, neg, shrink, 1, mode == 1 ? s->root : nullptr, nullptr, st, fac, dt);
-        if (mode == 1) {
-            k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root, s->d_t2r, s->d_boff, s->nb, s->m,
-                                                                         nt, s->sigma[p][size_t(t)], s->extra);
-            KR_CK_LAUNCH();
-            s->launches++;
-        }
+                  s->avg[p] + o, pos, neg, shrink, 1, mode == 1 ? s->root + int64_t(t) * s->Hr : nullptr, nullptr,
+                  cont_stream(s, t, st), fac, dt);
     }
+    join(s, st);
+    if (mode == 1) gather_all(s, p, nt, st);
     if (mode == 1 && s->exchange) {
         KR_CK(cudaStreamSynchronize(st));
         s->exchange(s->user);
     }
     team_step(s, s->turnTree[p], s->m, mode, s->g, p == 1, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, 0,
               nullptr, mode == 1 ? s->extra : nullptr, st, fac, dt);
+    if (turn_fuse()) {
+        const int64_t o = s->off[p][1], n = s->off[p].back() - o;
+        k_river_scale_all<<<unsigned((n + 255) / 256), 256, 0, st>>>(
+            s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr, nt, s->T, s->d_roff + p * (s->T + 1),
+            s->d_nr + p * s->T, s->d_sigma + p * s->T, shrink, mode == 1, fac, dt);
+        KR_CK_LAUNCH();
+        s->launches++;
+        return;
+    }
     for (int t = 0; t < s->T; ++t) {
         const int64_t o = s->off[p][size_t(t) + 1];
         const int nr = s->riverTree[p][size_t(t)].n;
@@ -1410,14 +1527,16 @@ void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, dou
 
 void turn_gradient(kr_turn_solver* s, int p, const double* opp, double* g, cudaStream_t st) {
     const int q = 1 - p;  // opponent's blocks are the inputs
+    fork(s, st);
     if (p == 0) engine_ax(s->turnEng, opp, g, st);
     else engine_atx(s->turnEng, opp, g, st);
     for (int t = 0; t < s->T; ++t) {
         const double* in = opp + s->off[q][size_t(t) + 1];
         double* out = g + s->off[p][size_t(t) + 1];
-        if (p == 0) engine_ax(s->riverEng[size_t(t)], in, out, st);
-        else engine_atx(s->riverEng[size_t(t)], in, out, st);
+        if (p == 0) engine_ax(s->riverEng[size_t(t)], in, out, cont_stream(s, t, st));
+        else engine_atx(s->riverEng[size_t(t)], in, out, cont_stream(s, t, st));
     }
+    join(s, st);
 }
 
 // bestResponseValue of player p against the device strategy opp.
@@ -1432,13 +1551,10 @@ double turn_br(kr_turn_solver* s, int p, const double* opp, cudaStream_t st) {
         KR_CK_LAUNCH();
         s->launches++;
     };
-    for (int t = 0; t < s->T; ++t) {
-        br(s->riverTree[p][size_t(t)], s->Hr, s->g + s->off[p][size_t(t) + 1], s->root, nullptr);
-        k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root, s->d_t2r, s->d_boff, s->nb, s->m, nt,
-                                                                     s->sigma[p][size_t(t)], s->extra);
-        KR_CK_LAUNCH();
-        s->launches++;
-    }
+    for (int t = 0; t < s->T; ++t)
+        br(s->riverTree[p][size_t(t)], s->Hr, s->g + s->off[p][size_t(t) + 1], s->root + int64_t(t) * s->Hr,
+           nullptr);
+    gather_all(s, p, nt, st);
     if (s->exchange) {
         KR_CK(cudaStreamSynchronize(st));
         s->exchange(s->user);
@@ -1464,9 +1580,13 @@ void destroy_turn(kr_turn_solver* s) {
         cudaFree(s->x[p]);
         cudaFree(s->a[p]);
     }
-    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g, s->root, s->handval, s->bval, s->d_one, s->d_fac, s->d_cnt};
+    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g,     s->root,  s->handval,
+                  s->bval,   s->d_one, s->d_fac, s->d_cnt, s->d_sigma, s->d_roff, s->d_nr};
     for (void* q : ps) cudaFree(q);
     if (s->ownExtra) cudaFree(s->extra);
+    for (cudaStream_t q : s->side) cudaStreamDestroy(q);
+    for (cudaEvent_t ev : s->evJoin) cudaEventDestroy(ev);
+    if (s->evFork) cudaEventDestroy(s->evFork);
     delete s;
 }
 
@@ -1549,7 +1669,33 @@ int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs
                 s->a[p] = krb::dev_alloc<double>(len);
             }
             s->g = krb::dev_alloc<double>(std::max(s->off[0].back(), s->off[1].back()));
-            s->root = krb::dev_alloc<double>(s->Hr);
+            s->root = krb::dev_alloc<double>(s->Hr * T);  // one block of river hands per continuation
+            {
+                std::vector<int32_t> sg;
+                for (int p = 0; p < 2; ++p) sg.insert(sg.end(), s->sigma[p].begin(), s->sigma[p].end());
+                s->d_sigma = krb::dev_alloc<int32_t>(int64_t(sg.size()));
+                KR_CK(cudaMemcpy(s->d_sigma, sg.data(), 4 * sg.size(), cudaMemcpyHostToDevice));
+                std::vector<int64_t> ro;
+                std::vector<int32_t> nr;
+                for (int p = 0; p < 2; ++p) {
+                    for (int t = 0; t <= T; ++t) ro.push_back(s->off[p][size_t(t) + 1] - s->off[p][1]);
+                    for (int t = 0; t < T; ++t) nr.push_back(s->riverTree[p][size_t(t)].n);
+                }
+                s->d_roff = krb::dev_alloc<int64_t>(int64_t(ro.size()));
+                s->d_nr = krb::dev_alloc<int32_t>(int64_t(nr.size()));
+                KR_CK(cudaMemcpy(s->d_roff, ro.data(), 8 * ro.size(), cudaMemcpyHostToDevice));
+                KR_CK(cudaMemcpy(s->d_nr, nr.data(), 4 * nr.size(), cudaMemcpyHostToDevice));
+                krb::raise_smem_limit(krb::k_turn_gather_all, size_t(nb) * krb::kGatherHands * sizeof(double));
+            }
+            if (T > 1 && !std::getenv("KR_TURN_SERIAL")) {
+                s->side.resize(size_t(T));
+                s->evJoin.resize(size_t(T));
+                for (int t = 0; t < T; ++t) {
+                    KR_CK(cudaStreamCreateWithFlags(&s->side[size_t(t)], cudaStreamNonBlocking));
+                    KR_CK(cudaEventCreateWithFlags(&s->evJoin[size_t(t)], cudaEventDisableTiming));
+                }
+                KR_CK(cudaEventCreateWithFlags(&s->evFork, cudaEventDisableTiming));
+            }
             s->extra = krb::dev_alloc<double>(int64_t(m) * std::max(turnTrees[0].n_seq, turnTrees[1].n_seq));
             s->handval = krb::dev_alloc<double>(std::max<int64_t>(m, s->Hr));
             s->bval = krb::dev_alloc<double>(1);

@@ -69,11 +69,15 @@ def test_turn_rules_match_checker(game, rule):
     assert e[-1] < 0.25 * e[0] and np.all(np.diff(e) < 0)
 
 
-def test_turn_graph_replay_is_bitwise(game, monkeypatch):
+@pytest.mark.parametrize("knob", [("KR_NO_GRAPH", "1"), ("KR_TURN_FUSE", "0"), ("KR_TURN_SERIAL", "1")])
+def test_turn_execution_variants_are_bitwise(game, knob, monkeypatch):
     """One GPU: iterations replay a captured graph with the factors from a
-    device table; launching them one by one (KR_NO_GRAPH) gives the same bits."""
+    device table, the continuations' river products and steps run side by
+    side, and one launch gathers / scales every continuation.  Launching one
+    by one (KR_NO_GRAPH), per continuation (KR_TURN_FUSE=0) or on one stream
+    (KR_TURN_SERIAL) gives the same bits."""
     r = TurnSolver(game).run(max_iters=7, checkpoint_every=3, want_avg=True, rule=2)
-    monkeypatch.setenv("KR_NO_GRAPH", "1")
+    monkeypatch.setenv(*knob)
     q = TurnSolver(game).run(max_iters=7, checkpoint_every=3, want_avg=True, rule=2)
     for k in ("trace_br1", "trace_br2", "avg1", "avg2"):
         assert np.array_equal(r[k], q[k]), k
