@@ -73,7 +73,23 @@ struct DevSell {
     // board group (entries relative to the group's first slice)
     int32_t* order_all = nullptr;
     int32_t* order_grp = nullptr;
+    // Compressed slots (SELL-C), same slot layout as col /
+    // val: each row is [segment 0 | segment 1] (the two merged factors, in
+    // storage order); 16-bit columns relative to a per-slice base of each
+    // segment; the coded segment's values as 16-bit codes into its board's
+    // table (exact doubles), the other segment's values in val.
+    bool comp = false;
+    int codedSeg = 0;                // segment whose values are coded (0 or 1)
+    uint16_t* col16 = nullptr;       // padded
+    uint16_t* code16 = nullptr;      // padded
+    int32_t* lane_len0 = nullptr;    // 32 * nslices: entries of segment 0
+    int32_t* base0 = nullptr;        // nslices
+    int32_t* base1 = nullptr;        // nslices
+    int32_t* tbase = nullptr;        // nslices: table offset (board * kCodeSlab)
+    double* table = nullptr;         // nboards * kCodeSlab
 };
+
+constexpr int64_t kCodeSlab = 65536;  // table entries per board (16-bit codes)
 
 template <class T>
 T* dev_alloc(int64_t n) {

@@ -25,6 +25,7 @@
 #include <mutex>
 #include <numeric>
 #include <thread>
+#include <unordered_map>
 
 #include "kr_common.cuh"
 
@@ -83,6 +84,70 @@ __device__ __forceinline__ double gather(const double* __restrict__ xa, const do
     return __ldg(xa + c);
 }
 
+// One long row per warp (the 32 lanes load and multiply a chunk of kChunk
+// entries, lane 0 adds the chunk's products in storage order while the next
+// chunk's loads are in flight).  Shared by the plain and compressed kernels.
+template <bool TWO>
+__device__ __forceinline__ void spmv_long_row(const SellView& A, const double* __restrict__ xa,
+                                              const double* __restrict__ xb, int32_t split, double* __restrict__ y,
+                                              double* P, int lane, int w) {
+    const int64_t r = int64_t(blockIdx.x) * kWarpsPerBlock + w;
+    if (r >= A.nlong) return;
+    const int64_t e0 = A.long_ptr[r], e1 = A.long_ptr[r + 1];
+    double acc = 0.0;
+    constexpr int per = kChunk / 32;
+    double p[per];
+    // chunk 0 products
+    int n = int(lmin(kChunk, e1 - e0));
+    {
+        int32_t c[per];
+        double v[per];
+#pragma unroll
+        for (int u = 0; u < per; ++u)
+            if (u * 32 + lane < n) {
+                c[u] = __ldcs(A.long_col + e0 + u * 32 + lane);
+                v[u] = __ldcs(A.long_val + e0 + u * 32 + lane);
+            }
+#pragma unroll
+        for (int u = 0; u < per; ++u)
+            if (u * 32 + lane < n) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+    }
+    for (int64_t t0 = e0; t0 < e1; t0 += kChunk) {
+#pragma unroll
+        for (int u = 0; u < per; ++u)
+            if (u * 32 + lane < n) P[u * 32 + lane] = p[u];
+        __syncwarp();
+        // issue the next chunk's loads before lane 0 folds this one
+        const int64_t t1 = t0 + kChunk;
+        const int nn = int(lmin(kChunk, e1 - t1));
+        int32_t c[per];
+        double v[per];
+#pragma unroll
+        for (int u = 0; u < per; ++u)
+            if (u * 32 + lane < nn) {
+                c[u] = __ldcs(A.long_col + t1 + u * 32 + lane);
+                v[u] = __ldcs(A.long_val + t1 + u * 32 + lane);
+            }
+        if (lane == 0) {
+            int q = 0;
+            for (; q + 8 <= n; q += 8) {
+                double t[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t[u] = P[q + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc += t[u];
+            }
+            for (; q < n; ++q) acc += P[q];
+        }
+#pragma unroll
+        for (int u = 0; u < per; ++u)
+            if (u * 32 + lane < nn) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+        __syncwarp();
+        n = nn;
+    }
+    if (lane == 0) y[A.long_row[r]] = acc;
+}
+
 // y[row] = sum_j val * src[col] over the row's entries in storage order;
 // src = [xa (split entries) | xb] when TWO.  The first blocks fold one long
 // row per warp (the 32 lanes load and multiply a chunk, lane 0 adds the
@@ -103,61 +168,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
     const int w = threadIdx.x >> 5;
     const int64_t longBlocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blockIdx.x < longBlocks) {
-        const int64_t r = int64_t(blockIdx.x) * kWarpsPerBlock + w;
-        if (r >= A.nlong) return;
-        const int64_t e0 = A.long_ptr[r], e1 = A.long_ptr[r + 1];
-        double acc = 0.0;
-        constexpr int per = kChunk / 32;
-        double p[per];
-        // chunk 0 products
-        int n = int(lmin(kChunk, e1 - e0));
-        {
-            int32_t c[per];
-            double v[per];
-#pragma unroll
-            for (int u = 0; u < per; ++u)
-                if (u * 32 + lane < n) {
-                    c[u] = __ldcs(A.long_col + e0 + u * 32 + lane);
-                    v[u] = __ldcs(A.long_val + e0 + u * 32 + lane);
-                }
-#pragma unroll
-            for (int u = 0; u < per; ++u)
-                if (u * 32 + lane < n) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
-        }
-        for (int64_t t0 = e0; t0 < e1; t0 += kChunk) {
-#pragma unroll
-            for (int u = 0; u < per; ++u)
-                if (u * 32 + lane < n) P[w][u * 32 + lane] = p[u];
-            __syncwarp();
-            // issue the next chunk's loads before lane 0 folds this one
-            const int64_t t1 = t0 + kChunk;
-            const int nn = int(lmin(kChunk, e1 - t1));
-            int32_t c[per];
-            double v[per];
-#pragma unroll
-            for (int u = 0; u < per; ++u)
-                if (u * 32 + lane < nn) {
-                    c[u] = __ldcs(A.long_col + t1 + u * 32 + lane);
-                    v[u] = __ldcs(A.long_val + t1 + u * 32 + lane);
-                }
-            if (lane == 0) {
-                int q = 0;
-                for (; q + 8 <= n; q += 8) {
-                    double t[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) t[u] = P[w][q + u];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) acc += t[u];
-                }
-                for (; q < n; ++q) acc += P[w][q];
-            }
-#pragma unroll
-            for (int u = 0; u < per; ++u)
-                if (u * 32 + lane < nn) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
-            __syncwarp();
-            n = nn;
-        }
-        if (lane == 0) y[A.long_row[r]] = acc;
+        spmv_long_row<TWO>(A, xa, xb, split, y, P[w], lane, w);
         return;
     }
     const int64_t si = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
@@ -215,6 +226,96 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
             v[u] = vn[u];
         }
     }
+    if (row >= 0) y[row] = acc;
+}
+
+struct SellCView {
+    const uint16_t* col16;
+    const uint16_t* code16;
+    const int32_t* len0;
+    const int32_t* base0;
+    const int32_t* base1;
+    const int32_t* tbase;
+    const double* table;
+};
+
+// Entries [j0, j1) of one lane's row, one segment: x = src[cbase + col16],
+// value = the coded table entry or val, accumulated in storage order.  KU
+// entries per stage, the next stage's loads in flight during this one's
+// gathers (as k_spmv).
+template <int KU, bool CODED>
+__device__ __forceinline__ double seg_sum(double acc, const SellView& A, const SellCView& C, int64_t base, int32_t j0,
+                                          int32_t j1, const double* __restrict__ src, int32_t cbase, int32_t tb) {
+    if (j0 >= j1) return acc;
+    uint32_t c[KU], k[KU];
+    double v[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u)
+        if (j0 + u < j1) {
+            const int64_t q = base + int64_t(j0 + u) * 32;
+            c[u] = __ldcs(C.col16 + q);
+            if (CODED) k[u] = __ldcs(C.code16 + q);
+            else v[u] = __ldcs(A.val + q);
+        }
+    for (int32_t j = j0; j < j1; j += KU) {
+        uint32_t cn[KU], kn[KU];
+        double vn[KU], x[KU];
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            const int32_t jj = j + KU + u;
+            if (jj < j1) {
+                const int64_t q = base + int64_t(jj) * 32;
+                cn[u] = __ldcs(C.col16 + q);
+                if (CODED) kn[u] = __ldcs(C.code16 + q);
+                else vn[u] = __ldcs(A.val + q);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < KU; ++u)
+            if (j + u < j1) {
+                x[u] = __ldg(src + cbase + int32_t(c[u]));
+                if (CODED) v[u] = __ldg(C.table + tb + int32_t(k[u]));
+            }
+#pragma unroll
+        for (int u = 0; u < KU; ++u)
+            if (j + u < j1) acc += v[u] * x[u];
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            c[u] = cn[u];
+            if (CODED) k[u] = kn[u];
+            else v[u] = vn[u];
+        }
+    }
+    return acc;
+}
+
+// k_spmv over compressed slots: segment 0 (entries [0, len0), source xa)
+// then segment 1 (entries [len0, len), source xb), one accumulator, so each
+// row's sum is the storage-order sum of k_spmv bit for bit.  CSEG: the coded
+// segment.  Long rows keep the plain CSR path.
+template <bool TWO, int CSEG>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_spmvc(SellView A, SellCView C, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
+            double* __restrict__ y) {
+    __shared__ double P[kWarpsPerBlock][kChunk];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t longBlocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blockIdx.x < longBlocks) {
+        spmv_long_row<TWO>(A, xa, xb, split, y, P[w], lane, w);
+        return;
+    }
+    const int64_t si = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
+    if (si >= A.nslices) return;
+    const int64_t s = A.order ? int64_t(A.order[si]) : si;
+    const int64_t base = A.slice_ptr[s] + lane;
+    const int32_t len = A.lane_len[s * 32 + lane];
+    const int32_t row = A.lane_row[s * 32 + lane];
+    const int32_t len0 = TWO ? C.len0[s * 32 + lane] : len;
+    const int32_t tb = C.tbase[s];
+    double acc = 0.0;
+    acc = seg_sum<kU, CSEG == 0>(acc, A, C, base, 0, len0, xa, C.base0[s], tb);
+    if (TWO) acc = seg_sum<kU, CSEG == 1>(acc, A, C, base, len0, len, xb, C.base1[s], tb);
     if (row >= 0) y[row] = acc;
 }
 
@@ -721,6 +822,119 @@ void upload_sell(const HostSell& h, int64_t sliceBase, int64_t entryBase, int64_
     KR_CK(cudaStreamSynchronize(s));
 }
 
+// SELL-C of one board's slices (DevSell::comp): per lane the number of
+// segment-0 entries (two segments: columns below `split` come first in every
+// merged row), per slice the lowest column of each segment, 16-bit column
+// offsets, and 16-bit codes (first-seen order) for the values of segment
+// `codedSeg`.  ok = false when a slice's segment spans more than 65,536
+// columns or the board has more than 65,536 distinct coded values.
+struct HostComp {
+    std::vector<uint16_t> col16, code16;
+    std::vector<int32_t> len0, base0, base1;
+    std::vector<double> table;
+    bool ok = true;
+};
+
+void compress_sell(const HostSell& h, bool two, int64_t split, int codedSeg, HostComp& c) {
+    const size_t ns = h.sptr.size(), padded = h.col.size();
+    c = HostComp{};
+    c.col16.assign(padded, 0);
+    c.code16.assign(padded, 0);
+    c.len0.assign(32 * ns, 0);
+    c.base0.assign(ns, 0);
+    c.base1.assign(ns, 0);
+    std::unordered_map<uint64_t, uint16_t> codes;
+    for (size_t sl = 0; sl < ns && c.ok; ++sl) {
+        const int64_t at = h.sptr[sl];
+        int64_t lo[2] = {INT64_MAX, INT64_MAX}, hi[2] = {-1, -1};
+        for (int l = 0; l < 32; ++l) {
+            const int32_t len = h.llen[sl * 32 + size_t(l)];
+            int32_t n0 = 0;
+            for (int32_t j = 0; j < len; ++j) {
+                const int64_t col = h.col[size_t(at + 32 * int64_t(j) + l)];
+                const int sg = (two && col >= split) ? 1 : 0;
+                if (sg == 0 && n0 != j) c.ok = false;  // segment 0 must come first
+                if (sg == 0) ++n0;
+                const int64_t cc = sg ? col - split : col;
+                lo[sg] = std::min(lo[sg], cc);
+                hi[sg] = std::max(hi[sg], cc);
+            }
+            c.len0[sl * 32 + size_t(l)] = n0;
+        }
+        for (int sg = 0; sg < 2; ++sg) {
+            if (hi[sg] < 0) lo[sg] = 0;
+            else if (hi[sg] - lo[sg] > 65535) c.ok = false;
+        }
+        c.base0[sl] = int32_t(lo[0]);
+        c.base1[sl] = int32_t(lo[1]);
+        for (int l = 0; l < 32 && c.ok; ++l) {
+            const int32_t len = h.llen[sl * 32 + size_t(l)], n0 = c.len0[sl * 32 + size_t(l)];
+            for (int32_t j = 0; j < len; ++j) {
+                const size_t q = size_t(at + 32 * int64_t(j) + l);
+                const int sg = j < n0 ? 0 : 1;
+                const int64_t col = h.col[q];
+                c.col16[q] = uint16_t(sg ? col - split - lo[1] : col - lo[0]);
+                if (sg == codedSeg) {
+                    uint64_t bits;
+                    std::memcpy(&bits, &h.val[q], 8);
+                    auto it = codes.find(bits);
+                    if (it == codes.end()) {
+                        if (c.table.size() >= size_t(kCodeSlab)) {
+                            c.ok = false;
+                            break;
+                        }
+                        it = codes.emplace(bits, uint16_t(c.table.size())).first;
+                        c.table.push_back(h.val[q]);
+                    }
+                    c.code16[q] = it->second;
+                }
+            }
+        }
+    }
+}
+
+void alloc_comp(krb::DevSell& d, int nb) {
+    d.col16 = dev_alloc<uint16_t>(std::max<int64_t>(d.padded, 1));
+    d.code16 = dev_alloc<uint16_t>(std::max<int64_t>(d.padded, 1));
+    d.lane_len0 = dev_alloc<int32_t>(std::max<int64_t>(32 * d.nslices, 1));
+    d.base0 = dev_alloc<int32_t>(std::max<int64_t>(d.nslices, 1));
+    d.base1 = dev_alloc<int32_t>(std::max<int64_t>(d.nslices, 1));
+    d.tbase = dev_alloc<int32_t>(std::max<int64_t>(d.nslices, 1));
+    d.table = dev_alloc<double>(int64_t(nb) * kCodeSlab);
+}
+
+void upload_comp(const HostComp& c, int b, int64_t sliceBase, int64_t entryBase, krb::DevSell& d, cudaStream_t s) {
+    const size_t ns = c.base0.size();
+    if (ns) {
+        std::vector<int32_t> tb(ns, int32_t(int64_t(b) * kCodeSlab));
+        KR_CK(cudaMemcpyAsync(d.col16 + entryBase, c.col16.data(), 2 * c.col16.size(), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.code16 + entryBase, c.code16.data(), 2 * c.code16.size(), cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.lane_len0 + 32 * sliceBase, c.len0.data(), 4 * c.len0.size(), cudaMemcpyHostToDevice,
+                              s));
+        KR_CK(cudaMemcpyAsync(d.base0 + sliceBase, c.base0.data(), 4 * ns, cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.base1 + sliceBase, c.base1.data(), 4 * ns, cudaMemcpyHostToDevice, s));
+        KR_CK(cudaMemcpyAsync(d.tbase + sliceBase, tb.data(), 4 * ns, cudaMemcpyHostToDevice, s));
+    }
+    if (!c.table.empty())
+        KR_CK(cudaMemcpyAsync(d.table + int64_t(b) * kCodeSlab, c.table.data(), 8 * c.table.size(),
+                              cudaMemcpyHostToDevice, s));
+    KR_CK(cudaStreamSynchronize(s));
+}
+
+void free_comp(krb::DevSell& d) {
+    cudaFree(d.col16);
+    cudaFree(d.code16);
+    cudaFree(d.lane_len0);
+    cudaFree(d.base0);
+    cudaFree(d.base1);
+    cudaFree(d.tbase);
+    cudaFree(d.table);
+    d.col16 = d.code16 = nullptr;
+    d.lane_len0 = d.base0 = d.base1 = d.tbase = nullptr;
+    d.table = nullptr;
+    d.comp = false;
+}
+
 void free_sell(krb::DevSell& d) {
     cudaFree(d.slice_ptr);
     cudaFree(d.lane_row);
@@ -733,6 +947,7 @@ void free_sell(krb::DevSell& d) {
     cudaFree(d.long_val);
     cudaFree(d.order_all);
     cudaFree(d.order_grp);
+    free_comp(d);
     d = krb::DevSell{};
 }
 
@@ -1153,6 +1368,22 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         const int64_t nrowsOf[4] = {Kp, R, Kp, Cc};
         const int64_t nnzOf[4] = {nV, nU + nA, nU, nA + nV};
         for (int w = 0; w < 4; ++w) alloc_sell(*mats[w], nrowsOf[w], tsl[w], nnzOf[w], tpad[w], tnl[w], tnlz[w]);
+        // SELL-C (opt-in, KR_SELL_COMP=1) for VT (all V,
+        // coded), UA ([U coded | Ahat]) and AV ([Ahat^T | V coded]); U^T stays
+        // plain.  Measured: half the bytes, no faster (the SpMVs are bound by
+        // entries in flight and x gathers, not by DRAM bytes).
+        const bool compOn = std::getenv("KR_SELL_COMP") != nullptr;
+        // KR_SELL_CODES=0: 16-bit columns only, every value stays fp64 (codedSeg 2)
+        const char* codesEnv = std::getenv("KR_SELL_CODES");
+        const bool codesOn = !(codesEnv && std::atoi(codesEnv) == 0);
+        const int codedSegOf[4] = {codesOn ? 0 : 2, codesOn ? 0 : 2, -1, codesOn ? 1 : 2};
+        const int64_t splitOf[4] = {0, Kp, 0, R};
+        std::atomic<bool> compFail[4] = {false, false, false, false};
+        for (int w = 0; w < 4; ++w)
+            if (compOn && codedSegOf[w] >= 0) {
+                alloc_comp(*mats[w], nb);
+                mats[w]->codedSeg = codedSegOf[w];
+            }
         e->d_tz = dev_alloc<double>(std::max<int64_t>(Kp, 1));
         e->d_tz2 = dev_alloc<double>(std::max<int64_t>(Kp, 1));
         e->d_xp = dev_alloc<double>(std::max<int64_t>(Cc, 1));
@@ -1175,6 +1406,12 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
                     int64_t(hs.lgrow.size()) != p.nl[w] || int64_t(hs.lcol.size()) != p.nlz[w])
                     throw Fail{KR_CUDA, "internal: SELL sizing mismatch"};
                 upload_sell(hs, p.slOff[w], p.padOff[w], p.nlOff[w], p.nlzOff[w], *mats[w], s);
+                if (mats[w]->col16 && !compFail[w].load()) {
+                    HostComp hc;
+                    compress_sell(hs, w == 1 || w == 3, splitOf[w], codedSegOf[w], hc);
+                    if (hc.ok) upload_comp(hc, b, p.slOff[w], p.padOff[w], *mats[w], s);
+                    else compFail[w] = true;
+                }
                 int32_t ml = 0;
                 for (int32_t l : hs.llen) ml = std::max(ml, l);
                 plan[size_t(b)].maxLen[w] = ml;
@@ -1275,6 +1512,11 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         for (int w = 0; w < 4; ++w)
             for (auto& p : plan) mats[w]->maxLen = std::max(mats[w]->maxLen, p.maxLen[w]);
         for (int w = 0; w < 4; ++w) {
+            if (!mats[w]->col16) continue;
+            if (compFail[w].load()) free_comp(*mats[w]);  // plain slots for this matrix
+            else mats[w]->comp = true;
+        }
+        for (int w = 0; w < 4; ++w) {
             e->bSl[w].clear();
             e->bNl[w].clear();
             for (auto& p : plan) {
@@ -1328,6 +1570,26 @@ void build_orders(kr_engine* e) {
         };
         if (std::getenv("KR_LPT_ALL")) {  // whole-range launches too (measured: -1-2%, off)
             std::vector<int32_t> all = sorted(0, A.nslices);
+            A.order_all = dev_alloc<int32_t>(A.nslices);
+            KR_CK(cudaMemcpy(A.order_all, all.data(), 4 * all.size(), cudaMemcpyHostToDevice));
+        } else if (const char* ord = std::getenv("KR_ORDER"); ord && std::string(ord) == "sm") {
+            // SM-affine: blocks are dealt to SMs round-robin, so launch block
+            // r * nsm + q (likely on SM q) takes block r of SM q's contiguous
+            // region of slices; an SM then works inside one or two boards' x.
+            int nsm = 148;
+            KR_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, e->device));
+            const int64_t full = A.nslices / kWarpsPerBlock;  // whole blocks (a partial one stays last)
+            std::vector<int32_t> all(size_t(A.nslices));
+            std::iota(all.begin(), all.end(), 0);
+            int64_t i = 0, maxReg = (full + nsm - 1) / nsm;
+            for (int64_t r = 0; r < maxReg; ++r)
+                for (int q = 0; q < nsm; ++q) {
+                    const int64_t a = full * q / nsm, b = full * (q + 1) / nsm;
+                    if (a + r >= b) continue;
+                    for (int w = 0; w < kWarpsPerBlock; ++w)
+                        all[size_t(i * kWarpsPerBlock + w)] = int32_t((a + r) * kWarpsPerBlock + w);
+                    ++i;
+                }
             A.order_all = dev_alloc<int32_t>(A.nslices);
             KR_CK(cudaMemcpy(A.order_all, all.data(), 4 * all.size(), cudaMemcpyHostToDevice));
         }
@@ -1413,7 +1675,17 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
         pend.b = pool_event(e);
         KR_CK(cudaEventRecord(pend.a, s));
     }
-    if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
+    if (A.comp) {
+        const SellCView c{A.col16, A.code16, A.lane_len0 + 32 * s0, A.base0 + s0, A.base1 + s0, A.tbase + s0, A.table};
+        if (!xb && A.codedSeg == 2)
+            k_spmvc<false, 2><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, nullptr, 0, y);
+        else if (!xb) k_spmvc<false, 0><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, nullptr, 0, y);
+        else if (A.codedSeg == 2)
+            k_spmvc<true, 2><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, xb, int32_t(split), y);
+        else if (A.codedSeg == 0)
+            k_spmvc<true, 0><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, xb, int32_t(split), y);
+        else k_spmvc<true, 1><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, xb, int32_t(split), y);
+    } else if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
     else if (A.maxLen <= 1 && e->lean)
         k_spmv<false, 1, 8><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
     else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);

@@ -49,9 +49,13 @@ def test_products_bitwise(name, kw, tech, post):
     check_engine(eng, o.sparsify(tech, post), p.rows, p.cols, np.random.default_rng(17))
 
 
+@pytest.mark.parametrize("comp", [False, True], ids=["sell", "sell_c"])
 @pytest.mark.parametrize("board,v", [("Ks7d4c2h9s", 3390846), ("AhKhQh7c7d", 2049828)], ids=["dry", "wet"])
-def test_config2_products_bitwise(board, v):
-    """Config 2 on the dry board and the wet one SURVEY.md §8(d) also names."""
+def test_config2_products_bitwise(board, v, comp, monkeypatch):
+    """Config 2 on the dry board and the wet one SURVEY.md §8(d) also names,
+    with plain and compressed (KR_SELL_COMP) slots."""
+    if comp:
+        monkeypatch.setenv("KR_SELL_COMP", "1")
     p = H.builtin("river_full", seed=1, board=board, tree=3)
     o = po.Instance.builtin("river_full", seed=1, board=board, tree=3)
     eng = CudaEngine(p.sparsify("b", True))
@@ -180,7 +184,8 @@ def test_device_pointer_entry_points():
 
 
 @pytest.mark.parametrize("groups,knob", [("1", None), ("2", None), ("3", None), ("4", None), ("4", ("KR_LPT", "0")),
-                                         ("3", ("KR_LPT_ALL", "1")), ("2", ("KR_PF", "2"))])
+                                         ("3", ("KR_LPT_ALL", "1")), ("2", ("KR_PF", "2")),
+                                         ("3", ("KR_SELL_COMP", "1")), ("4", ("KR_ORDER", "sm"))])
 def test_host_pipeline_groups_bitwise(groups, knob, monkeypatch):
     """kr_engine_ax / kr_engine_atx pipelined over board groups (each group's
     whole product on two streams, widest slices first) give the bits of the
