@@ -192,6 +192,18 @@ struct kr_engine {
     std::vector<int32_t> grpBoard{0};
     cudaStream_t copyIn = nullptr, copyOut = nullptr, stage2 = nullptr, stage3 = nullptr;
     std::vector<cudaEvent_t> evIn, evOut, evMid, evSolve;
+    cudaEvent_t evStart = nullptr, evEnd = nullptr;  // fork from / join into `stream`
+    // captured host-buffer pipelines, keyed by (direction, host input,
+    // host output); pinned buffers only (kr_engine_ax / kr_engine_atx)
+    struct PipeGraph {
+        int dir;
+        const double* in;
+        double* out;
+        cudaGraphExec_t exec;
+        int64_t launches;
+    };
+    std::vector<PipeGraph> pipeGraphs;
+    std::vector<PipeGraph> pipeSeen;  // first calls (exec unused): captured on the second
     // kr_engine_pair_device: A^T y forks onto `side` (created on first use)
     cudaStream_t side = nullptr;
     cudaEvent_t evFork = nullptr, evJoin = nullptr;

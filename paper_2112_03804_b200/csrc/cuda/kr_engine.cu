@@ -1197,6 +1197,9 @@ void destroy_engine(kr_engine* e) {
     if (e->stage3) cudaStreamDestroy(e->stage3);
     for (cudaEvent_t ev : e->evMid) cudaEventDestroy(ev);
     for (cudaEvent_t ev : e->evSolve) cudaEventDestroy(ev);
+    if (e->evStart) cudaEventDestroy(e->evStart);
+    if (e->evEnd) cudaEventDestroy(e->evEnd);
+    for (auto& pg : e->pipeGraphs) cudaGraphExecDestroy(pg.exec);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->evFork) cudaEventDestroy(e->evFork);
     if (e->evJoin) cudaEventDestroy(e->evJoin);
@@ -1615,6 +1618,8 @@ void make_pipeline(kr_engine* e) {
     KR_CK(cudaStreamCreateWithFlags(&e->copyIn, cudaStreamNonBlocking));
     KR_CK(cudaStreamCreateWithFlags(&e->copyOut, cudaStreamNonBlocking));
     KR_CK(cudaStreamCreateWithFlags(&e->stage2, cudaStreamNonBlocking));
+    KR_CK(cudaEventCreateWithFlags(&e->evStart, cudaEventDisableTiming));
+    KR_CK(cudaEventCreateWithFlags(&e->evEnd, cudaEventDisableTiming));
     const char* ps = std::getenv("KR_PIPE_STREAMS");
     if (!(ps && std::atoi(ps) == 2)) KR_CK(cudaStreamCreateWithFlags(&e->stage3, cudaStreamNonBlocking));
     e->evIn.resize(size_t(G));
@@ -1902,6 +1907,8 @@ void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) { engi
 // board groups the input copy of group g overlaps the first-stage kernels of
 // the groups already copied, and the output copy of group g overlaps the
 // last-stage kernels of the groups after it (copyIn / stream / copyOut).
+void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout);
+
 void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double* hout, int64_t nout) {
     const int64_t wantIn = dir == 0 ? e->cols : e->rows, wantOut = dir == 0 ? e->rows : e->cols;
     if (nin != wantIn)
@@ -1918,8 +1925,73 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
         KR_CK(cudaStreamSynchronize(e->stream));
         return;
     }
+    // Pinned buffers (the usual case: a solver loop or a benchmark reuses
+    // them): the second call with the same (direction, input, output)
+    // captures the whole pipeline below into a CUDA graph, and later calls
+    // replay it, so the ~60 launches, copies and event edges are no longer
+    // enqueued by the host one by one.  KR_NO_PIPE_GRAPH: always enqueue.
+    auto pinned = [](const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    };
+    static const bool noGraph = std::getenv("KR_NO_PIPE_GRAPH") != nullptr;
+    if (!noGraph && pinned(hin) && pinned(hout)) {
+        for (auto& pg : e->pipeGraphs)
+            if (pg.dir == dir && pg.in == hin && pg.out == hout) {
+                KR_CK(cudaGraphLaunch(pg.exec, e->stream));
+                KR_CK(cudaStreamSynchronize(e->stream));
+                e->launches += pg.launches;
+                account(e, dir);
+                return;
+            }
+        bool seen = false;
+        for (auto& pg : e->pipeSeen) seen = seen || (pg.dir == dir && pg.in == hin && pg.out == hout);
+        if (seen && e->pipeGraphs.size() < 8) {
+            const int64_t l0 = e->launches;
+            cudaGraph_t gr;
+            KR_CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_pipeline(e, dir, hin, hout);
+            } catch (...) {
+                cudaStreamEndCapture(e->stream, &gr);
+                cudaGetLastError();
+                throw;
+            }
+            KR_CK(cudaStreamEndCapture(e->stream, &gr));
+            cudaGraphExec_t exec;
+            const cudaError_t ie = cudaGraphInstantiate(&exec, gr, 0);
+            cudaGraphDestroy(gr);
+            KR_CK(ie);
+            const int64_t dl = e->launches - l0;
+            e->launches = l0;
+            e->pipeGraphs.push_back({dir, hin, hout, exec, dl});
+            KR_CK(cudaGraphLaunch(exec, e->stream));
+            KR_CK(cudaStreamSynchronize(e->stream));
+            e->launches += dl;
+            account(e, dir);
+            return;
+        }
+        if (!seen && e->pipeSeen.size() < 16) e->pipeSeen.push_back({dir, hin, hout, nullptr, 0});
+    }
+    enqueue_pipeline(e, dir, hin, hout);
+    KR_CK(cudaStreamSynchronize(e->stream));
+    account(e, dir);
+}
+
+// The pipelined host-buffer product (board groups), enqueued from and
+// joined back into e->stream: every stream it uses waits for the work
+// already queued on e->stream, and e->stream waits for all of it.
+void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout) {
+    const int G = e->ngroups();
     const std::vector<int64_t>& io = dir == 0 ? e->grpCol : e->grpRow;
     const std::vector<int64_t>& oo = dir == 0 ? e->grpRow : e->grpCol;
+    KR_CK(cudaEventRecord(e->evStart, e->stream));
+    for (cudaStream_t q : {e->copyIn, e->copyOut, e->stage2, e->stage3})
+        if (q) KR_CK(cudaStreamWaitEvent(q, e->evStart, 0));
     auto copy_out = [&](int g, cudaStream_t from) {
         KR_CK(cudaEventRecord(e->evOut[size_t(g)], from));
         KR_CK(cudaStreamWaitEvent(e->copyOut, e->evOut[size_t(g)], 0));
@@ -1988,8 +2060,8 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
             copy_out(g, e->stream);
         }
     }
-    KR_CK(cudaStreamSynchronize(e->copyOut));
-    account(e, dir);
+    KR_CK(cudaEventRecord(e->evEnd, e->copyOut));
+    KR_CK(cudaStreamWaitEvent(e->stream, e->evEnd, 0));
 }
 
 }  // namespace krb

@@ -229,3 +229,39 @@ def test_pair_device_is_bitwise_ax_then_atx(kind):
         eng.pair_device(x.data_ptr(), ax2.data_ptr(), y.data_ptr(), atx2.data_ptr())
     torch.cuda.ExternalStream(eng.stream).synchronize()
     assert torch.equal(ax, ax2) and torch.equal(atx, atx2)
+
+
+@pytest.mark.parametrize("kind", ["factored", "implicit"])
+def test_pinned_host_calls_replay_a_graph_bitwise(kind):
+    """kr_engine_ax / kr_engine_atx on pinned host buffers: the first call
+    enqueues the pipeline, the second captures it into a CUDA graph, later
+    calls replay it; every call returns the bits of the device-pointer path,
+    also after the input buffer's contents change (the graph reads the
+    buffer, not a snapshot) and with a second pair of buffers."""
+    import ctypes
+
+    import torch
+    from paper_2112_03804_b200 import _native as N
+    boards = H.turn_instances(nboards=3, factors=kind == "factored")
+    eng = CudaEngine([f for _, f in boards]) if kind == "factored" else CudaEngine.kron([i for i, _ in boards])
+    L = N.cuda()
+    nx, ny = eng.cols, eng.rows
+    arr = lambda p, n: np.ctypeslib.as_array((ctypes.c_double * n).from_address(p))  # noqa: E731
+    bufs = [(L.kr_host_alloc(8 * nx), L.kr_host_alloc(8 * ny)) for _ in range(2)]
+    try:
+        rng = np.random.default_rng(21)
+        for call in range(5):
+            px, py = bufs[call % 2 if call >= 3 else 0]
+            x = rng.standard_normal(nx)
+            arr(px, nx)[:] = x
+            N.check(L.kr_engine_ax(eng.handle, px, nx, py, ny))
+            dx = torch.from_numpy(x).cuda()
+            dy = torch.empty(ny, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            eng.ax_device(dx.data_ptr(), dy.data_ptr())
+            torch.cuda.ExternalStream(eng.stream).synchronize()
+            assert bits_equal(arr(py, ny).copy(), dy.cpu().numpy()), call
+    finally:
+        for px, py in bufs:
+            L.kr_host_free(px)
+            L.kr_host_free(py)
