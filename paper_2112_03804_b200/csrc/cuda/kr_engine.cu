@@ -1634,13 +1634,13 @@ void make_pipeline(kr_engine* e) {
     }
 }
 
-// Board groups of the pipelined host-buffer calls: up to six contiguous
+// Board groups of the pipelined host-buffer calls: up to eight contiguous
 // board ranges (KR_FLAG_SINGLE_PART: one; KR_GROUPS overrides the count).
-// Measured at config 3 (profiles/r01l_e2e_pipeline.md): 4 -> 6 groups +2-3%,
-// 8 and more lose to per-launch tails.
+// Measured at config 3 (profiles/r01l_e2e_pipeline.md): with the pipeline
+// replayed as a graph, 8 groups 586 pairs/s, 6 580, 12 568, 16 519.
 int group_count(int nb, uint32_t flags) {
     if (flags & KR_FLAG_SINGLE_PART) return 1;
-    int G = 6;
+    int G = 8;
     if (const char* env = std::getenv("KR_GROUPS")) G = std::atoi(env);
     return std::max(1, std::min(G, nb));
 }

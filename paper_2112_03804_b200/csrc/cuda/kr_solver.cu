@@ -41,6 +41,7 @@ struct kr_solver {
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
     int team = 4;                // lanes per hand in k_player_team (2, 4 or 8)
+    int teamThreads = 256;       // threads per k_player_team block (KR_TEAM_THREADS: 64, 128 or 256)
     // graph replay of whole iterations (kr_solver_run without early stop):
     // per-iteration factors pos/neg/shrink and weightSum as device tables
     // indexed by the device counter d_cnt[0] (iteration), d_cnt[1] = checkpoints
@@ -656,13 +657,13 @@ size_t step_smem(int n, int nt, int nn, int na) {
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
                  cudaStream_t st, bool dev = false) {
     if (s->levelled[p]) {
-        const int team = s->team;
-        const int hpb = 256 / team;
+        const int team = s->team, threads = s->teamThreads;
+        const int hpb = threads / team;
         const unsigned grid = unsigned((s->H[p] + hpb - 1) / hpb);
         if (grid == 0) return;
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
-        kern<<<grid, 256, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
+        kern<<<grid, threads, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
                                       hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule,
                                       dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr);
         KR_CK_LAUNCH();
@@ -838,6 +839,10 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 if (const char* env = std::getenv("KR_TEAM")) {
                     const int tm = std::atoi(env);
                     s->team = tm == 2 || tm == 8 ? tm : 4;
+                }
+                if (const char* env = std::getenv("KR_TEAM_THREADS")) {
+                    const int th = std::atoi(env);
+                    s->teamThreads = th == 64 || th == 128 ? th : 256;
                 }
                 if (s->levelled[p]) {
                     // the team size must fit the smem budget (hands per block = 256 / team)
