@@ -1729,7 +1729,17 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         s->rule = prm->rule;
         KR_CK(cudaSetDevice(s->device));
         cudaStream_t st = s->turnEng->stream;
-        cudaEvent_t ev0, ev1;
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        struct ExecGuard {  // the graph (and the events) go on every exit path
+            cudaGraphExec_t& x;
+            cudaEvent_t &a, &b;
+            ~ExecGuard() {
+                if (x) cudaGraphExecDestroy(x);
+                if (a) cudaEventDestroy(a);
+                if (b) cudaEventDestroy(b);
+            }
+        } guard{exec, ev0, ev1};
         KR_CK(cudaEventCreate(&ev0));
         KR_CK(cudaEventCreate(&ev1));
         KR_CK(cudaEventRecord(ev0, st));
@@ -1746,7 +1756,6 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         // from a device table filled with the loop's own expressions, so a
         // replay is bitwise the launched iteration.  Checkpoints stay on the
         // host path (their values are read back).  KR_NO_GRAPH: launch by launch.
-        cudaGraphExec_t exec = nullptr;
         int64_t launchDelta = 0;
         if (!s->exchange && !std::getenv("KR_NO_GRAPH")) {
             std::vector<double> fac(size_t(3) * (prm->max_iters + 1), 0.0);
@@ -1822,12 +1831,9 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         }
         KR_CK(cudaEventRecord(ev1, st));
         KR_CK(cudaEventSynchronize(ev1));
-        if (exec) cudaGraphExecDestroy(exec);
         float ms = 0;
         KR_CK(cudaEventElapsedTime(&ms, ev0, ev1));
         r->seconds = ms / 1e3;
-        cudaEventDestroy(ev0);
-        cudaEventDestroy(ev1);
         for (int p = 0; p < 2; ++p) {
             double* dst = p == 0 ? r->avg1 : r->avg2;
             if (dst) KR_CK(cudaMemcpy(dst, s->a[p], 8 * size_t(s->off[p].back()), cudaMemcpyDeviceToHost));
