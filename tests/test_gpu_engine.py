@@ -265,3 +265,28 @@ def test_pinned_host_calls_replay_a_graph_bitwise(kind):
         for px, py in bufs:
             L.kr_host_free(px)
             L.kr_host_free(py)
+
+
+def test_host_call_after_async_device_call_is_ordered():
+    """A host-buffer call issued while a device-pointer product is still in
+    flight on the engine stream forks its pipeline streams from that stream
+    (evStart), so neither call sees the other's scratch (d_tz / d_tz2)."""
+    import torch
+    boards = H.turn_instances(nboards=4)
+    eng = CudaEngine([f for _, f in boards])
+    rng = np.random.default_rng(31)
+    x, y = rng.standard_normal(eng.cols), rng.standard_normal(eng.rows)
+    ref_ax, ref_atx = eng.Ax(x), eng.ATx(y)
+    dx = torch.from_numpy(rng.standard_normal(eng.cols)).cuda()
+    dy = torch.from_numpy(rng.standard_normal(eng.rows)).cuda()
+    oax = torch.empty(eng.rows, dtype=torch.float64, device="cuda")
+    oatx = torch.empty(eng.cols, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(3):
+        eng.ax_device(dx.data_ptr(), oax.data_ptr())      # queued, not waited for
+        eng.atx_device(dy.data_ptr(), oatx.data_ptr())
+        got_ax, got_atx = eng.Ax(x), eng.ATx(y)           # host calls right behind
+        assert bits_equal(got_ax, ref_ax) and bits_equal(got_atx, ref_atx)
+    torch.cuda.ExternalStream(eng.stream).synchronize()
+    assert bits_equal(oax.cpu().numpy(), eng.Ax(dx.cpu().numpy()))
+    assert bits_equal(oatx.cpu().numpy(), eng.ATx(dy.cpu().numpy()))
