@@ -146,7 +146,9 @@ int kr_engine_atx_device(kr_engine* e, const double* y_dev, double* x_dev, void*
  * flight together: A^T y runs on an engine-owned side stream forked from
  * `stream` and joined back into it, so the latency-bound stages of each
  * direction (transposes, M solves, short SpMVs) overlap the other direction's
- * bandwidth-bound SpMV.  Results are bitwise those of kr_engine_ax_device /
+ * bandwidth-bound SpMV; above ~8 GB of factors per pair (KR_PAIR_SERIAL_GB),
+ * where each direction is bandwidth-bound alone, the two run one after the
+ * other on `stream`.  Results are bitwise those of kr_engine_ax_device /
  * kr_engine_atx_device (each direction has its own scratch).  x_dev must not
  * alias atx_dev, nor y_dev ax_dev.  No reference counterpart: the reference
  * calls Ax and ATx one after the other (GradientEngine, solver.hpp:21-27). */

@@ -2146,6 +2146,18 @@ int kr_engine_pair_device(kr_engine* e, const double* x, double* ax, const doubl
         if (!e || !x || !ax || !y || !atx) throw Fail{KR_INVALID_INPUT, "null argument"};
         KR_CK(cudaSetDevice(e->device));
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+        // Above ~8 GB of factor traffic per pair (KR_PAIR_SERIAL_GB) both
+        // directions are bandwidth-bound on their own and running them
+        // together measured 3-6% slower (profiles/r01p_sweep.md): one after
+        // the other there.
+        const char* sgb = std::getenv("KR_PAIR_SERIAL_GB");
+        const double serialGB = sgb ? std::atof(sgb) : 8.0;
+        const double pairGB = e->kron ? 0.0 : 12e-9 * 2.0 * double(e->nnzA + e->nnzU + e->nnzV);
+        if (pairGB > serialGB) {
+            krb::engine_ax(e, x, ax, s);
+            krb::engine_atx(e, y, atx, s);
+            return;
+        }
         if (!e->side) {
             // KR_PAIR_PRIORITY (measurement knob): the side stream's priority
             const char* pr = std::getenv("KR_PAIR_PRIORITY");

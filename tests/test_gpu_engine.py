@@ -209,8 +209,9 @@ def test_host_pipeline_groups_bitwise(groups, knob, monkeypatch):
     assert bits_equal(ax, ex) and bits_equal(aty, ey)
 
 
+@pytest.mark.parametrize("serial_gb", [None, "0"], ids=["concurrent", "serial"])
 @pytest.mark.parametrize("kind", ["factored", "implicit"])
-def test_pair_device_is_bitwise_ax_then_atx(kind):
+def test_pair_device_is_bitwise_ax_then_atx(kind, serial_gb, monkeypatch):
     """kr_engine_pair_device (A^T y forked onto a side stream, own scratch)
     gives the bits of kr_engine_ax_device then kr_engine_atx_device, also
     when repeated back to back on the same buffers."""

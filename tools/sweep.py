@@ -49,7 +49,9 @@ POINTS = [
 ]
 
 
-def time_pairs(eng, reps):
+def time_pairs(eng, reps, concurrent=False):
+    """Seconds per pair: Ax then ATy on the engine stream, or both in flight
+    together (kr_engine_pair_device) with concurrent=True."""
     s = torch.cuda.ExternalStream(eng.stream)
     x = torch.randn(eng.cols, dtype=torch.float64, device="cuda")
     y = torch.randn(eng.rows, dtype=torch.float64, device="cuda")
@@ -63,8 +65,11 @@ def time_pairs(eng, reps):
     torch.cuda.synchronize()
     e0.record(s)
     for _ in range(reps):
-        eng.ax_device(x.data_ptr(), ax.data_ptr())
-        eng.atx_device(y.data_ptr(), atx.data_ptr())
+        if concurrent:
+            eng.pair_device(x.data_ptr(), ax.data_ptr(), y.data_ptr(), atx.data_ptr())
+        else:
+            eng.ax_device(x.data_ptr(), ax.data_ptr())
+            eng.atx_device(y.data_ptr(), atx.data_ptr())
     e1.record(s)
     e1.synchronize()
     return e0.elapsed_time(e1) / reps / 1e3
@@ -89,6 +94,7 @@ def main():
         est = pair_bytes / (PEAK * 1e9 * 0.8)
         reps = max(10, min(2000, int(2.0 / max(est, 1e-6))))
         t = time_pairs(eng, reps)
+        tc = time_pairs(eng, reps, concurrent=True)
         gbs = pair_bytes / t / 1e9
         eng.close()
         torch.cuda.empty_cache()
@@ -100,6 +106,7 @@ def main():
         ek.close()
         row = {"point": name, "nnz": nnz, "bytes_per_pair": pair_bytes, "pairs_per_s": 1 / t,
                "us_per_pair": t * 1e6, "gb_per_s": gbs, "frac_of_measured_peak": gbs / PEAK,
+               "concurrent_us_per_pair": tc * 1e6, "concurrent_frac_of_measured_peak": pair_bytes / tc / 1e9 / PEAK,
                "reps": reps, "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2),
                "implicit_us_per_pair": tk * 1e6, "implicit_pairs_per_s": 1 / tk,
                "implicit_create_s": round(kron_create_s, 2)}
@@ -109,12 +116,16 @@ def main():
         torch.cuda.empty_cache()
     lines = [f"# Matvec bandwidth sweep ({tag}), one B200, fp64, Technique B postprocessed", "",
              f"Whole matvec pair (Ax + ATx); algorithmic bytes per BASELINE.md §2; peak {PEAK} GB/s (measured).", "",
-             "The implicit columns time the same pairs through K7 (kr_engine_create_kron), which streams no factors.", "",
-             "| point | stored nnz | MB / pair | us / pair | pairs/s | GB/s | % of peak | K7 us / pair | K7 pairs/s |",
-             "|---|---|---|---|---|---|---|---|---|"]
+             "The concurrent columns put both products of a pair in flight together (kr_engine_pair_device). "
+             "The implicit columns time the same pairs through K7 (kr_engine_create_kron), which streams no factors.",
+             "",
+             "| point | stored nnz | MB / pair | us / pair | pairs/s | GB/s | % of peak | concurrent us / pair "
+             "| concurrent % of peak | K7 us / pair | K7 pairs/s |",
+             "|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append(f"| {r['point']} | {r['nnz']:,} | {r['bytes_per_pair']/1e6:,.1f} | {r['us_per_pair']:,.1f} | "
                      f"{r['pairs_per_s']:,.1f} | {r['gb_per_s']:,.0f} | {100*r['frac_of_measured_peak']:.1f} | "
+                     f"{r['concurrent_us_per_pair']:,.1f} | {100*r['concurrent_frac_of_measured_peak']:.1f} | "
                      f"{r['implicit_us_per_pair']:,.1f} | {r['implicit_pairs_per_s']:,.0f} |")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_sweep.md"), "w") as f:
