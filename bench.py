@@ -212,10 +212,17 @@ def config1_gpu():
     prm = DcfrParams.cfr_plus(max_iters=1000, checkpoint_every=1)
     sv.run(DcfrParams.cfr_plus(max_iters=5, checkpoint_every=1))  # warm
     r = sv.run(prm)
+    # the same solve driven by K7 (within tolerance, not bitwise: DESIGN.md §4.2)
+    sk = solver_for([(inst, f)], implicit=True)
+    sk.run(DcfrParams.cfr_plus(max_iters=5, checkpoint_every=1))
+    rk = sk.run(prm)
     return {"workload": "config1: twenty_card (Leduc role), Technique B post, 1000 CFR+ iterations, "
                         "checkpointEvery=1", "iterations": r.iterations, "exploitability": r.exploitability,
             "device_seconds": r.seconds, "iters_per_s": r.iterations / r.seconds if r.seconds else None,
             "sparsify_s": sparsify_s, "alpha": "+inf", "beta": "-inf", "gamma": 1.0, "rule": "cfr+",
+            "implicit": {"iters_per_s": rk.iterations / rk.seconds if rk.seconds else None,
+                         "exploitability": rk.exploitability,
+                         "rel_diff_vs_factored": abs(rk.exploitability - r.exploitability) / r.exploitability},
             "_trace": r.trace_expl}
 
 

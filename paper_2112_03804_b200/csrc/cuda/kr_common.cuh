@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -91,11 +93,54 @@ struct DevSell {
 
 constexpr int64_t kCodeSlab = 65536;  // table entries per board (16-bit codes)
 
+// Programmatic dependent launch (PDL).  Every engine / solver kernel starts
+// with pdl_entry(): it waits until the grid it depends on has completed (its
+// memory visible) and then lets its own dependents start launching, so a
+// dependent kernel's launch and CTA rasterisation overlap this one instead of
+// following it.  Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// KR_PDL=0: plain stream-ordered launches.  KR_PDL_MAXGRID: only grids of at
+// most this many CTAs are launched early (multi-wave grids launched early
+// measured slower: their waiting CTAs hold SM slots the kernel before them
+// still needs).
+inline bool pdl_enabled(unsigned gridCtas) {
+    static const bool on = [] {
+        const char* env = std::getenv("KR_PDL");
+        return !(env && std::atoi(env) == 0);
+    }();
+    static const unsigned maxGrid = [] {
+        const char* env = std::getenv("KR_PDL_MAXGRID");
+        return env ? unsigned(std::atol(env)) : 2000u;
+    }();
+    return on && gridCtas <= maxGrid;
+}
+
 template <class T>
 T* dev_alloc(int64_t n) {
     T* p = nullptr;
     if (n > 0) KR_CK(cudaMalloc(&p, sizeof(T) * size_t(n)));
     return p;
+}
+
+// kernel<<<grid, block, smem, stream>>>(args...) with the PDL attribute
+// (arguments coerced to the kernel's parameter types, as <<<>>> does).
+template <typename... KArgs, typename... Args>
+void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled(grid.x * grid.y * grid.z) ? 1 : 0;
+    KR_CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
 // Raise (never lower) a kernel's dynamic shared-memory limit: the attribute

@@ -163,6 +163,7 @@ template <bool TWO, int KU = kU, int MINB = 1>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
     k_spmv(SellView A, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
            double* __restrict__ y) {
+    krb::pdl_entry();
     __shared__ double P[kWarpsPerBlock][kChunk];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
@@ -297,6 +298,7 @@ template <bool TWO, int CSEG>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     k_spmvc(SellView A, SellCView C, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
             double* __restrict__ y) {
+    krb::pdl_entry();
     __shared__ double P[kWarpsPerBlock][kChunk];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 // consecutive hands as one 256-byte segment.
 __global__ void __launch_bounds__(256) k_seq_major_tile(const double* __restrict__ x, int64_t M2, int32_t n2,
                                                         double* __restrict__ xp, int64_t J0, int64_t J1) {
+    krb::pdl_entry();
     extern __shared__ double tile[];
     const int64_t j0 = J0 + int64_t(blockIdx.x) * 32;
     const int cnt = int(lmin(32, J1 - j0));
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(256) k_seq_major_tile(const double* __restrict
 // x'[s*M2 + J] = x[J*n2 + s]: the sequence-major copy V^T x gathers from.
 __global__ void k_seq_major(const double* __restrict__ x, int64_t M2, int32_t n2, double* __restrict__ xp,
                             int64_t q0, int64_t q1) {
+    krb::pdl_entry();
     const int64_t q = q0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= q1) return;
     const int64_t J = q / n2;
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(32)
     k_chain_tma(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
                 const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int withMul,
                 double* __restrict__ z, int64_t s0) {
+    krb::pdl_entry();
     extern __shared__ __align__(128) double dsm[];
     __shared__ __align__(8) uint64_t bar[kStages];
     double(*Tb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm);
@@ -551,6 +556,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     k_chain_forward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
                     double* __restrict__ z) {
+    krb::pdl_entry();
     const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
     if (s >= s1) return;
     const int lane = threadIdx.x & 31;
@@ -600,6 +606,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     k_chain_backward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
                      const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
                      double* __restrict__ z) {
+    krb::pdl_entry();
     const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
     if (s >= s1) return;
     const int lane = threadIdx.x & 31;
@@ -653,6 +660,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 __global__ void k_level_forward(const int32_t* __restrict__ rows, int64_t n, const int64_t* __restrict__ ptr,
                                 const int32_t* __restrict__ col, const double* __restrict__ val,
                                 double* __restrict__ z) {
+    krb::pdl_entry();
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= n) return;
     const int32_t r = rows[q];
@@ -668,6 +676,7 @@ __global__ void k_level_forward(const int32_t* __restrict__ rows, int64_t n, con
 __global__ void k_level_backward(const int32_t* __restrict__ cols, int64_t n, const int64_t* __restrict__ ptr,
                                  const int32_t* __restrict__ row, const double* __restrict__ val,
                                  double* __restrict__ z) {
+    krb::pdl_entry();
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= n) return;
     const int32_t j = cols[q];
@@ -1683,17 +1692,17 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
     if (A.comp) {
         const SellCView c{A.col16, A.code16, A.lane_len0 + 32 * s0, A.base0 + s0, A.base1 + s0, A.tbase + s0, A.table};
         if (!xb && A.codedSeg == 2)
-            k_spmvc<false, 2><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, nullptr, 0, y);
-        else if (!xb) k_spmvc<false, 0><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, nullptr, 0, y);
+            krb::launch(k_spmvc<false, 2>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, nullptr, 0, y);
+        else if (!xb) krb::launch(k_spmvc<false, 0>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, nullptr, 0, y);
         else if (A.codedSeg == 2)
-            k_spmvc<true, 2><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, xb, int32_t(split), y);
+            krb::launch(k_spmvc<true, 2>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
         else if (A.codedSeg == 0)
-            k_spmvc<true, 0><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, xb, int32_t(split), y);
-        else k_spmvc<true, 1><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, c, xa, xb, int32_t(split), y);
-    } else if (xb) k_spmv<true><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, xb, int32_t(split), y);
+            krb::launch(k_spmvc<true, 0>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
+        else krb::launch(k_spmvc<true, 1>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
+    } else if (xb) krb::launch(k_spmv<true>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, xb, int32_t(split), y);
     else if (A.maxLen <= 1 && e->lean)
-        k_spmv<false, 1, 8><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
-    else k_spmv<false><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, s>>>(v, xa, nullptr, 0, y);
+        krb::launch(k_spmv<false, 1, 8>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, nullptr, 0, y);
+    else krb::launch(k_spmv<false>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
     if (timed) {
         KR_CK(cudaEventRecord(pend.b, s));
@@ -1727,12 +1736,11 @@ void solve_forward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1
     if (c1 < 0) c1 = e->nchains;
     if (e->mkind == 1 && c1 > c0) {
         if (e->chain_tma) {
-            k_chain_tma<1><<<unsigned(c1 - c0), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
+            krb::launch(k_chain_tma<1>, unsigned(c1 - c0), 32, chain_smem(e), s, e->chain_ptr, e->chain_len, e->chain_mul,
                                                                       e->chain_neg1, e->chain_withmul, e->d_tz, c0);
         } else {
             const int wpb = kWarpsPerBlock;
-            k_chain_forward<<<unsigned((c1 - c0 + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
-                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, c0, c1, e->d_tz);
+            krb::launch(k_chain_forward, unsigned((c1 - c0 + wpb - 1) / wpb), 32 * wpb, 0, s, e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, c0, c1, e->d_tz);
         }
         KR_CK_LAUNCH();
         e->launches++;
@@ -1740,7 +1748,7 @@ void solve_forward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1
         for (size_t l = 0; l + 1 < e->lvl_fwd_ptr.size(); ++l) {
             const int64_t a = e->lvl_fwd_ptr[l], n = e->lvl_fwd_ptr[l + 1] - a;
             if (n == 0) continue;
-            k_level_forward<<<unsigned((n + 127) / 128), 128, 0, s>>>(e->lvl_fwd_rows + a, n, e->mr_ptr, e->mr_col,
+            krb::launch(k_level_forward, unsigned((n + 127) / 128), 128, 0, s, e->lvl_fwd_rows + a, n, e->mr_ptr, e->mr_col,
                                                                       e->mr_val, e->d_tz);
             KR_CK_LAUNCH();
             e->launches++;
@@ -1752,12 +1760,11 @@ void solve_backward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -
     if (c1 < 0) c1 = e->nchains;
     if (e->mkind == 1 && c1 > c0) {
         if (e->chain_tma) {
-            k_chain_tma<-1><<<unsigned(c1 - c0), 32, chain_smem(e), s>>>(e->chain_ptr, e->chain_len, e->chain_mul,
+            krb::launch(k_chain_tma<-1>, unsigned(c1 - c0), 32, chain_smem(e), s, e->chain_ptr, e->chain_len, e->chain_mul,
                                                                        e->chain_neg1, e->chain_withmul, e->d_tz2, c0);
         } else {
             const int wpb = kWarpsPerBlock;
-            k_chain_backward<<<unsigned((c1 - c0 + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
-                e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, c0, c1, e->d_tz2);
+            krb::launch(k_chain_backward, unsigned((c1 - c0 + wpb - 1) / wpb), 32 * wpb, 0, s, e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, c0, c1, e->d_tz2);
         }
         KR_CK_LAUNCH();
         e->launches++;
@@ -1765,7 +1772,7 @@ void solve_backward(kr_engine* e, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -
         for (size_t l = 0; l + 1 < e->lvl_bwd_ptr.size(); ++l) {
             const int64_t a = e->lvl_bwd_ptr[l], n = e->lvl_bwd_ptr[l + 1] - a;
             if (n == 0) continue;
-            k_level_backward<<<unsigned((n + 127) / 128), 128, 0, s>>>(e->lvl_bwd_cols + a, n, e->mc_ptr,
+            krb::launch(k_level_backward, unsigned((n + 127) / 128), 128, 0, s, e->lvl_bwd_cols + a, n, e->mc_ptr,
                                                                        e->mc_row, e->mc_val, e->d_tz2);
             KR_CK_LAUNCH();
             e->launches++;
@@ -1845,12 +1852,12 @@ void seq_major(kr_engine* e, const double* x, int64_t c0, int64_t c1, cudaStream
     const size_t smem = size_t(32) * size_t(e->n2) * sizeof(double);
     if (smem <= 48 * 1024 && c0 % e->n2 == 0 && c1 % e->n2 == 0) {
         const int64_t J0 = c0 / e->n2, J1 = c1 / e->n2;
-        k_seq_major_tile<<<unsigned((J1 - J0 + 31) / 32), 256, smem, s>>>(x, e->M2, e->n2, e->d_xp, J0, J1);
+        krb::launch(k_seq_major_tile, unsigned((J1 - J0 + 31) / 32), 256, smem, s, x, e->M2, e->n2, e->d_xp, J0, J1);
         KR_CK_LAUNCH();
         e->launches++;
         return;
     }
-    k_seq_major<<<unsigned((c1 - c0 + 255) / 256), 256, 0, s>>>(x, e->M2, e->n2, e->d_xp, c0, c1);
+    krb::launch(k_seq_major, unsigned((c1 - c0 + 255) / 256), 256, 0, s, x, e->M2, e->n2, e->d_xp, c0, c1);
     KR_CK_LAUNCH();
     e->launches++;
 }

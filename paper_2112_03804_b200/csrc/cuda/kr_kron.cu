@@ -112,6 +112,7 @@ size_t fused_smem(int maxMS) {
 //                   − (P[p2lt] + P[p2le]) + G[c1] + G[c2],   G[c] = P[B_c] + P[E_c].
 __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
                                                          double* __restrict__ out) {
+    krb::pdl_entry();
     extern __shared__ double sm[];
     __shared__ double warpV[kWarps], warpW[kWarps];
     const int a = blockIdx.x, b = b0 + int(blockIdx.y);
@@ -485,7 +486,7 @@ void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStre
     KronDir& d = k->dir[dir];
     if (b1 < 0) b1 = d.nb;
     if (d.mO * d.nO == 0 || b1 <= b0) return;
-    k_kron_fused<<<dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads, k->smem[dir], s>>>(d, b0, in, out);
+    krb::launch(k_kron_fused, dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads, k->smem[dir], s, d, b0, in, out);
     KR_CK_LAUNCH();
     e->launches++;
 }

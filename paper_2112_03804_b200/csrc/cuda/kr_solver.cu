@@ -135,6 +135,7 @@ __global__ void k_player_step(int mode, const int32_t* __restrict__ treeBuf, int
                               const double* __restrict__ g, int negate, double* __restrict__ regret,
                               double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
                               double shrink) {
+    krb::pdl_entry();
     // Shared memory per hand: its regret row and its seqVal / reach row
     // (strided so consecutive threads hit consecutive banks).  The gradient
     // row is read straight from global memory (each element once); the
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
                                                      const int* __restrict__ dt, int noAvg = 0,
                                                      double* __restrict__ rootOut = nullptr,
                                                      const double* __restrict__ extra = nullptr) {
+    krb::pdl_entry();
     // noAvg: leave avg alone (river blocks of a turn game are averaged after
     // their reach is scaled); rootOut: each hand's root value (the sum of its
     // root nodes' values, descending node order: seqVal[0] of cfrSweep);
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
 }
 
 // Device-side counters of a replayed graph: c[which] += 1.
-__global__ void k_tick(int* c, int which) { c[which] += 1; }
+__global__ void k_tick(int* c, int which) { krb::pdl_entry(); c[which] += 1; }
 
 size_t team_smem(int n, int nn, int hpb, int tlen) {
     return size_t(2 * n + 1 + nn) * size_t(hpb + 1) * 8 + size_t(tlen) * 4 + 16;
@@ -497,6 +499,7 @@ size_t team_smem(int n, int nn, int hpb, int tlen) {
 
 __global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w, double* __restrict__ out,
                             const double* __restrict__ wsArr, const int* __restrict__ dt) {
+    krb::pdl_entry();
     if (wsArr) w = wsArr[*dt];  // graph replay: weightSum of this iteration
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q < n) out[q] = avg[q] / w;  // solver.hpp:390-391
@@ -506,6 +509,7 @@ __global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w,
 __global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
                                 const double* __restrict__ g, int negate, double* __restrict__ handval,
                                 const double* __restrict__ extra = nullptr) {
+    krb::pdl_entry();
     extern __shared__ int32_t Ts[];
     const int tl = 2 * nn + 1;
     for (int q = threadIdx.x; q < tl; q += blockDim.x) Ts[q] = treeBuf[q];
@@ -545,6 +549,7 @@ __global__ void __launch_bounds__(256) k_board_sums(const double* __restrict__ h
                                                     const int64_t* __restrict__ bstart, int nb,
                                                     double* __restrict__ out, const int* __restrict__ slot,
                                                     int64_t slotStride) {
+    krb::pdl_entry();
     __shared__ double buf[kSumChunk];
     if (slot) out += int64_t(*slot) * slotStride;  // graph replay: this checkpoint's slot
     const int b = blockIdx.x;
@@ -574,6 +579,7 @@ __global__ void __launch_bounds__(256) k_board_sums(const double* __restrict__ h
 // 2 = flow conservation violated.
 __global__ void k_validate(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
                            const double* __restrict__ x, double tol, int* __restrict__ flag) {
+    krb::pdl_entry();
     const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (h >= H) return;
     const Tree tr = tree_view(treeBuf, nn);
@@ -663,7 +669,7 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
         if (grid == 0) return;
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
-        kern<<<grid, threads, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
+        krb::launch(kern, grid, threads, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
                                       hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule,
                                       dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr);
         KR_CK_LAUNCH();
@@ -677,7 +683,7 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
     if (grid == 0) return;
     const int na = s->na[p];
     const size_t smem = step_smem(s->n[p], nt, s->nnodes[p], na);
-    k_player_step<<<grid, nt, smem, st>>>(mode, s->d_tree[p], s->nnodes[p], s->n[p], s->H[p], nt, g, negate,
+    krb::launch(k_player_step, grid, nt, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->H[p], nt, g, negate,
                                           s->regret[p], s->x[p], s->avg[p], pos, neg, shrink);
     KR_CK_LAUNCH();
     s->launches++;
@@ -701,12 +707,12 @@ void best_response_to(kr_solver* s, int player, const double* opp, double* dst, 
     const size_t smem = size_t((2 * nn + 1 + na + 2) * 4) + size_t(n + 1) * bt * 8 + 16;
     const unsigned grid = unsigned((s->H[player] + bt - 1) / bt);
     if (grid) {
-        k_best_response<<<grid, bt, smem, st>>>(s->d_tree[player], nn, n, s->H[player], g, player == 1, handval,
+        krb::launch(k_best_response, grid, bt, smem, st, s->d_tree[player], nn, n, s->H[player], g, player == 1, handval,
                                                 nullptr);
         KR_CK_LAUNCH();
         s->launches++;
     }
-    k_board_sums<<<unsigned(s->nboards), 256, 0, st>>>(handval, s->d_bstart[player], s->nboards, dst, slot,
+    krb::launch(k_board_sums, unsigned(s->nboards), 256, 0, st, handval, s->d_bstart[player], s->nboards, dst, slot,
                                                         slotStride);
     KR_CK_LAUNCH();
     s->launches++;
@@ -907,7 +913,7 @@ void normalise_averages(kr_solver* s, cudaStream_t st, bool dev = false) {
     for (int p = 0; p < 2; ++p) {
         const int64_t len = s->H[p] * s->n[p];
         if (len == 0) continue;
-        krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, s->weightSum, s->a[p],
+        krb::launch(krb::k_normalise, unsigned((len + 255) / 256), 256, 0, st, s->avg[p], len, s->weightSum, s->a[p],
                                                                       dev ? s->d_ws : nullptr,
                                                                       dev ? s->d_cnt : nullptr);
         KR_CK_LAUNCH();
@@ -962,7 +968,7 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
         cudaGraph_t g;
         KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
-            krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 0);
+            krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 0);
             KR_CK_LAUNCH();
             s->launches++;
             krb::engine_ax(e, s->x[1], s->g, st);                                    // g1 = A x2
@@ -972,7 +978,7 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
             if (withCk) {
                 normalise_averages(s, st, true);                                     // solver.hpp:390-391
                 krb::best_responses(s, dck, dck + nb, st, s->d_cnt + 1, 2 * nb);
-                krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 1);
+                krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 1);
                 KR_CK_LAUNCH();
                 s->launches++;
             }
@@ -1234,8 +1240,7 @@ int kr_solver_best_response(kr_solver* s, int player, const double* opp, int64_t
         KR_CK(cudaMemcpyAsync(s->a[opp_p], opp, 8 * size_t(len), cudaMemcpyHostToDevice, st));
         KR_CK(cudaMemsetAsync(s->d_flag, 0, 4, st));
         if (s->H[opp_p]) {
-            krb::k_validate<<<unsigned((s->H[opp_p] + 127) / 128), 128, 0, st>>>(
-                s->d_tree[opp_p], s->nnodes[opp_p], s->n[opp_p], s->H[opp_p], s->a[opp_p], 1e-9, s->d_flag);
+            krb::launch(krb::k_validate, unsigned((s->H[opp_p] + 127) / 128), 128, 0, st, s->d_tree[opp_p], s->nnodes[opp_p], s->n[opp_p], s->H[opp_p], s->a[opp_p], 1e-9, s->d_flag);
             KR_CK_LAUNCH();
             s->launches++;
         }
@@ -1326,6 +1331,7 @@ namespace {
 __global__ void k_turn_gather(const double* __restrict__ root, const int32_t* __restrict__ t2r,
                               const int64_t* __restrict__ boff, int nb, int m, int nt, int sigma,
                               double* __restrict__ extra) {
+    krb::pdl_entry();
     const int h = blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= m) return;
     double acc = 0.0;
@@ -1349,6 +1355,7 @@ __global__ void __launch_bounds__(256) k_turn_gather_all(const double* __restric
                                                          const int64_t* __restrict__ boff, int nb, int m, int nt,
                                                          const int32_t* __restrict__ sigma, int T,
                                                          double* __restrict__ extra) {
+    krb::pdl_entry();
     extern __shared__ double gv[];  // [nb][kGatherHands] values, NaN = board holds the hand
     const int h0 = blockIdx.x * kGatherHands;
     const int nh = min(kGatherHands, m - h0);
@@ -1380,6 +1387,7 @@ __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, 
                               const int32_t* __restrict__ r2t, int64_t Hr, int nr, int nt, int sigma,
                               double shrink, int doAvg, const double* __restrict__ fac = nullptr,
                               const int* __restrict__ dt = nullptr) {
+    krb::pdl_entry();
     if (fac) shrink = fac[3 * *dt + 2];  // graph replay
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= Hr * nr) return;
@@ -1396,6 +1404,7 @@ __global__ void k_river_scale_all(double* __restrict__ x, double* __restrict__ a
                                   int nt, int T, const int64_t* __restrict__ roff, const int32_t* __restrict__ nrs,
                                   const int32_t* __restrict__ sigma, double shrink, int doAvg,
                                   const double* __restrict__ fac, const int* __restrict__ dt) {
+    krb::pdl_entry();
     if (fac) shrink = fac[3 * *dt + 2];  // graph replay
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= roff[T]) return;
@@ -1439,7 +1448,7 @@ void team_step(kr_turn_solver* s, const kr_turn_solver::TreeDev& T, int64_t H, i
     const unsigned grid = unsigned((H + hpb - 1) / hpb);
     if (!grid) return;
     const size_t smem = team_smem(T.n, T.nn, hpb, T.len);
-    k_player_team<kTurnTeam><<<grid, 256, smem, st>>>(mode, T.d, T.nn, T.n, T.na, T.len, H, hpb, g, negate, regret, x,
+    krb::launch(k_player_team<kTurnTeam>, grid, 256, smem, st, mode, T.d, T.nn, T.n, T.na, T.len, H, hpb, g, negate, regret, x,
                                                       avg, pos, neg, shrink, s->rule, fac, dt, noAvg, rootOut,
                                                       extra);
     KR_CK_LAUNCH();
@@ -1473,7 +1482,7 @@ bool turn_fuse() {
 void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
     if (!turn_fuse()) {
         for (int t = 0; t < s->T; ++t) {
-            k_turn_gather<<<unsigned((s->m + 127) / 128), 128, 0, st>>>(s->root + int64_t(t) * s->Hr, s->d_t2r,
+            krb::launch(k_turn_gather, unsigned((s->m + 127) / 128), 128, 0, st, s->root + int64_t(t) * s->Hr, s->d_t2r,
                                                                          s->d_boff, s->nb, s->m, nt,
                                                                          s->sigma[p][size_t(t)], s->extra);
             KR_CK_LAUNCH();
@@ -1482,8 +1491,7 @@ void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
         return;
     }
     const size_t smem = size_t(s->nb) * kGatherHands * sizeof(double);
-    k_turn_gather_all<<<unsigned((s->m + kGatherHands - 1) / kGatherHands), 256, smem, st>>>(
-        s->root, s->Hr, s->d_t2r, s->d_boff, s->nb, s->m, nt, s->d_sigma + p * s->T, s->T, s->extra);
+    krb::launch(k_turn_gather_all, unsigned((s->m + kGatherHands - 1) / kGatherHands), 256, smem, st, s->root, s->Hr, s->d_t2r, s->d_boff, s->nb, s->m, nt, s->d_sigma + p * s->T, s->T, s->extra);
     KR_CK_LAUNCH();
     s->launches++;
 }
@@ -1511,8 +1519,7 @@ void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, dou
               nullptr, mode == 1 ? s->extra : nullptr, st, fac, dt);
     if (turn_fuse()) {
         const int64_t o = s->off[p][1], n = s->off[p].back() - o;
-        k_river_scale_all<<<unsigned((n + 255) / 256), 256, 0, st>>>(
-            s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr, nt, s->T, s->d_roff + p * (s->T + 1),
+        krb::launch(k_river_scale_all, unsigned((n + 255) / 256), 256, 0, st, s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr, nt, s->T, s->d_roff + p * (s->T + 1),
             s->d_nr + p * s->T, s->d_sigma + p * s->T, shrink, mode == 1, fac, dt);
         KR_CK_LAUNCH();
         s->launches++;
@@ -1522,7 +1529,7 @@ void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, dou
         const int64_t o = s->off[p][size_t(t) + 1];
         const int nr = s->riverTree[p][size_t(t)].n;
         const int64_t n = s->Hr * nr;
-        k_river_scale<<<unsigned((n + 255) / 256), 256, 0, st>>>(s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr,
+        krb::launch(k_river_scale, unsigned((n + 255) / 256), 256, 0, st, s->x[p] + o, s->avg[p] + o, s->x[p], s->d_r2t, s->Hr,
                                                                   nr, nt, s->sigma[p][size_t(t)], shrink, mode == 1,
                                                                   fac, dt);
         KR_CK_LAUNCH();
@@ -1552,7 +1559,7 @@ double turn_br(kr_turn_solver* s, int p, const double* opp, cudaStream_t st) {
     const int bt = 128;
     auto br = [&](const kr_turn_solver::TreeDev& T, int64_t H, const double* g, double* out, const double* extra) {
         const size_t smem = size_t((2 * T.nn + 1 + T.na + 2) * 4) + size_t(T.n + 1) * bt * 8 + 16;
-        k_best_response<<<unsigned((H + bt - 1) / bt), bt, smem, st>>>(T.d, T.nn, T.n, H, g, p == 1, out, extra);
+        krb::launch(k_best_response, unsigned((H + bt - 1) / bt), bt, smem, st, T.d, T.nn, T.n, H, g, p == 1, out, extra);
         KR_CK_LAUNCH();
         s->launches++;
     };
@@ -1565,7 +1572,7 @@ double turn_br(kr_turn_solver* s, int p, const double* opp, cudaStream_t st) {
         s->exchange(s->user);
     }
     br(s->turnTree[p], s->m, s->g, s->handval, s->extra);
-    k_board_sums<<<1, 256, 0, st>>>(s->handval, s->d_one, 1, s->bval, nullptr, 0);
+    krb::launch(k_board_sums, 1, 256, 0, st, s->handval, s->d_one, 1, s->bval, nullptr, 0);
     KR_CK_LAUNCH();
     s->launches++;
     double v = 0;
@@ -1775,7 +1782,7 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
             cudaGraph_t gr;
             KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             try {
-                krb::k_tick<<<1, 1, 0, st>>>(s->d_cnt, 0);
+                krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 0);
                 KR_CK_LAUNCH();
                 s->launches++;
                 krb::turn_gradient(s, 0, s->x[1], s->g, st);
@@ -1810,7 +1817,7 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
             if (t % prm->checkpoint_every == 0 || t == prm->max_iters) {
                 for (int p = 0; p < 2; ++p) {
                     const int64_t len = s->off[p].back();
-                    krb::k_normalise<<<unsigned((len + 255) / 256), 256, 0, st>>>(s->avg[p], len, ws, s->a[p],
+                    krb::launch(krb::k_normalise, unsigned((len + 255) / 256), 256, 0, st, s->avg[p], len, ws, s->a[p],
                                                                                   nullptr, nullptr);
                     KR_CK_LAUNCH();
                 }
