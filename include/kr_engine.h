@@ -311,6 +311,10 @@ int kr_turn_solver_sizes(const kr_turn_solver* s, int64_t out[4]);
  * [V^T, U|Ahat, U^T, Ahat^T|V], the number of launches, their summed
  * milliseconds and the algorithmic bytes of one launch. */
 int kr_engine_set_timing(kr_engine* e, int enabled);
+/* Which of the four matrices the timing brackets (bit w = matrix w in the
+ * order above; default 0xF).  Timing only the dominant kernel keeps the
+ * events' own cost (~1.5% of a pair for all four) out of a timed region. */
+int kr_engine_set_timing_mask(kr_engine* e, int mask);
 int kr_engine_kernel_times(kr_engine* e, int64_t launches[4], double ms[4], double bytes[4]);
 
 #ifdef __cplusplus

@@ -97,7 +97,7 @@ CUDA_SYMBOLS = [
     "kr_engine_stream", "kr_engine_device", "kr_engine_launches", "kr_host_alloc", "kr_host_free", "kr_last_error",
     "kr_device_count", "kr_solver_create", "kr_solver_destroy", "kr_solver_run", "kr_solver_best_response",
     "kr_solver_launches", "kr_solver_begin", "kr_solver_iterate", "kr_solver_checkpoint", "kr_solver_averages",
-    "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_kernel_times", "kr_engine_create_kron",
+    "kr_solver_iteration", "kr_engine_set_timing", "kr_engine_set_timing_mask", "kr_engine_kernel_times", "kr_engine_create_kron",
     "kr_solver_set_rule", "kr_turn_solver_create", "kr_turn_solver_run", "kr_turn_solver_destroy",
     "kr_turn_solver_launches", "kr_turn_solver_set_exchange", "kr_turn_solver_sizes",
     "kr_factors_build_device", "kr_devfactors_view", "kr_devfactors_seconds", "kr_devfactors_free",
@@ -174,6 +174,7 @@ def cuda():
         L.kr_devfactors_seconds.argtypes = [C.c_void_p]
         L.kr_devfactors_free.argtypes = [C.c_void_p]
         L.kr_engine_set_timing.argtypes = [C.c_void_p, C.c_int]
+        L.kr_engine_set_timing_mask.argtypes = [C.c_void_p, C.c_int]
         L.kr_engine_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _CUDA = L
     return _CUDA

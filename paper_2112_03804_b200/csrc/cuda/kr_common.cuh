@@ -217,6 +217,7 @@ struct kr_engine {
     int64_t flops_per_product = 0;
     // optional per-kernel event timing (kr_engine_set_timing)
     bool timing = false;
+    int timingMask = 0xF;  // matrices bracketed when timing (bit w: VT, UA, UT, AV)
     struct Pending {
         int which;
         cudaEvent_t a, b;

@@ -1682,7 +1682,7 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
     const int32_t* order = b1 < 0 ? A.order_all : A.order_grp ? A.order_grp + s0 : nullptr;
     SellView v{A.slice_ptr + s0, A.lane_row + 32 * s0, A.lane_len + 32 * s0, A.col, A.val, s1 - s0,
                A.long_ptr + l0, A.long_row + l0, A.long_col, A.long_val, l1 - l0, order, e->pf};
-    const bool timed = e->timing && b1 < 0;
+    const bool timed = e->timing && ((e->timingMask >> which) & 1) && b1 < 0;
     kr_engine::Pending pend{which, nullptr, nullptr};
     if (timed) {
         pend.a = pool_event(e);
@@ -2179,6 +2179,13 @@ int kr_engine_pair_device(kr_engine* e, const double* x, double* ax, const doubl
         krb::engine_ax(e, x, ax, s);
         KR_CK(cudaEventRecord(e->evJoin, e->side));
         KR_CK(cudaStreamWaitEvent(s, e->evJoin, 0));
+    });
+}
+
+int kr_engine_set_timing_mask(kr_engine* e, int mask) {
+    return guarded([&] {
+        if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
+        e->timingMask = mask & 0xF;
     });
 }
 

@@ -150,7 +150,10 @@ class CudaEngine:
     # -- per-kernel event timing (kr_engine_set_timing) -------------------
     KERNELS = ("VT", "UA", "UT", "AV")  # V^T x | [U|Ahat][z;x] | U^T y | [Ahat^T|V][y;z]
 
-    def set_timing(self, enabled=True):
+    def set_timing(self, enabled=True, only=None):
+        """Bracket SpMV launches with events; only: names from KERNELS (all if None)."""
+        mask = 0xF if only is None else sum(1 << self.KERNELS.index(k) for k in only)
+        N.check(N.cuda().kr_engine_set_timing_mask(self._h, mask))
         N.check(N.cuda().kr_engine_set_timing(self._h, int(enabled)))
 
     def kernel_times(self):
