@@ -1313,6 +1313,13 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
     bool xseq = n2 > 0;
     for (auto& p : plan)
         if (xseq && (p.f->cols % n2 != 0)) xseq = false;
+    // The sequence-major copy of x (x', k_seq_major_tile before V^T) measured
+    // no faster at config 3 and 2-5% slower on small engines (one more
+    // launch per product): off unless KR_XSEQ=1.
+    {
+        const char* env = std::getenv("KR_XSEQ");
+        xseq = xseq && env && std::atoi(env) != 0;
+    }
 
     kr_engine* e = new kr_engine();
     try {

@@ -185,7 +185,8 @@ def test_device_pointer_entry_points():
 
 @pytest.mark.parametrize("groups,knob", [("1", None), ("2", None), ("3", None), ("4", None), ("4", ("KR_LPT", "0")),
                                          ("3", ("KR_LPT_ALL", "1")), ("2", ("KR_PF", "2")),
-                                         ("3", ("KR_SELL_COMP", "1")), ("4", ("KR_ORDER", "sm"))])
+                                         ("3", ("KR_SELL_COMP", "1")), ("4", ("KR_ORDER", "sm")),
+                                         ("4", ("KR_XSEQ", "1"))])
 def test_host_pipeline_groups_bitwise(groups, knob, monkeypatch):
     """kr_engine_ax / kr_engine_atx pipelined over board groups (each group's
     whole product on two streams, widest slices first) give the bits of the
