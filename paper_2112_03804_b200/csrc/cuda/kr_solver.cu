@@ -505,6 +505,18 @@ __global__ void k_normalise(const double* __restrict__ avg, int64_t n, double w,
     if (q < n) out[q] = avg[q] / w;  // solver.hpp:390-391
 }
 
+// Both players' averages in one launch: elements [0, n0) of avg0, then
+// [0, n1) of avg1 (the same division as k_normalise).
+__global__ void k_normalise2(const double* __restrict__ avg0, int64_t n0, double* __restrict__ out0,
+                             const double* __restrict__ avg1, int64_t n1, double* __restrict__ out1, double w,
+                             const double* __restrict__ wsArr, const int* __restrict__ dt) {
+    krb::pdl_entry();
+    if (wsArr) w = wsArr[*dt];
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q < n0) out0[q] = avg0[q] / w;  // solver.hpp:390-391
+    else if (q < n0 + n1) out1[q - n0] = avg1[q - n0] / w;
+}
+
 // bestResponseValue per hand (solver.hpp:304-318): bottom-up max walk.
 __global__ void k_best_response(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
                                 const double* __restrict__ g, int negate, double* __restrict__ handval,
@@ -910,6 +922,13 @@ int64_t kr_solver_launches(const kr_solver* s) { return s ? s->launches : 0; }
 
 namespace {
 void normalise_averages(kr_solver* s, cudaStream_t st, bool dev = false) {
+    const int64_t n0 = s->H[0] * s->n[0], n1 = s->H[1] * s->n[1];
+    if (n0 > 0 && n1 > 0) {
+        krb::launch(krb::k_normalise2, unsigned((n0 + n1 + 255) / 256), 256, 0, st, s->avg[0], n0, s->a[0], s->avg[1],
+                    n1, s->a[1], s->weightSum, dev ? s->d_ws : nullptr, dev ? s->d_cnt : nullptr);
+        s->launches++;
+        return;
+    }
     for (int p = 0; p < 2; ++p) {
         const int64_t len = s->H[p] * s->n[p];
         if (len == 0) continue;
