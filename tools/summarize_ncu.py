@@ -79,10 +79,14 @@ def main():
             lines.append(f"| {r[kn].split('(')[0].split('::')[-1]} | {val('gpu__time_duration.sum') * 1e6:.1f} | "
                          f"{val('dram__bytes_read.sum') / 1e6:.1f} | {val('dram__bytes_write.sum') / 1e6:.2f} |")
     ks = launches(lcsv)
-    # the first whole-range pair: seq_major, VT, chain, UA, UT, chain^T, AV
-    first = next((i for i in range(len(ks) - 6) if ks[i][0].startswith("k_seq_major")
-                  and ks[i + 6][0].startswith("k_spmv")), max(0, len(ks) - 7))
-    pair = ks[first:first + 7]
+    # the first whole-range pair: [seq_major,] VT, chain, UA, UT, chain^T, AV
+    # (seq_major only with KR_XSEQ=1): from the first kernel to the 4th SpMV
+    first = next((i for i, (n, _) in enumerate(ks) if n.startswith("k_seq_major") or n.startswith("k_spmv")), 0)
+    end, spmvs = first, 0
+    while end < len(ks) and spmvs < 4:
+        spmvs += ks[end][0].startswith("k_spmv")
+        end += 1
+    pair = ks[first:end]
     tot = sum(t for _, t in pair)
     lines += ["", "## One matvec pair, launch list (cold-cache, serialised: compare shares)", "",
               "| kernel | ns | share |", "|---|---|---|"]
