@@ -1313,12 +1313,15 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
     bool xseq = n2 > 0;
     for (auto& p : plan)
         if (xseq && (p.f->cols % n2 != 0)) xseq = false;
-    // The sequence-major copy of x (x', k_seq_major_tile before V^T) measured
-    // no faster at config 3 and 2-5% slower on small engines (one more
-    // launch per product): off unless KR_XSEQ=1.
+    // The sequence-major copy of x (x', k_seq_major_tile before V^T): about
+    // 1% faster sustained at config 3 (2.2M columns), 2-5% slower on small
+    // engines (one more launch per product than its locality saves).  On
+    // from 1M columns of x; KR_XSEQ=0/1 overrides.
     {
+        int64_t cols = 0;
+        for (int b = 0; b < nb; ++b) cols += boards[b].cols;
         const char* env = std::getenv("KR_XSEQ");
-        xseq = xseq && env && std::atoi(env) != 0;
+        xseq = xseq && (env ? std::atoi(env) != 0 : cols >= 1000000);
     }
 
     kr_engine* e = new kr_engine();
