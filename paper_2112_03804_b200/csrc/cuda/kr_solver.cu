@@ -41,7 +41,7 @@ struct kr_solver {
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
     int team = 4;                // lanes per hand in k_player_team (2, 4 or 8)
-    int teamThreads = 256;       // threads per k_player_team block (KR_TEAM_THREADS: 64, 128 or 256)
+    int teamThreads = 128;       // threads per k_player_team block (KR_TEAM_THREADS: 64, 128 or 256)
     // graph replay of whole iterations (kr_solver_run without early stop):
     // per-iteration factors pos/neg/shrink and weightSum as device tables
     // indexed by the device counter d_cnt[0] (iteration), d_cnt[1] = checkpoints
@@ -860,7 +860,7 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 }
                 if (const char* env = std::getenv("KR_TEAM_THREADS")) {
                     const int th = std::atoi(env);
-                    s->teamThreads = th == 64 || th == 128 ? th : 256;
+                    s->teamThreads = th == 64 || th == 256 ? th : 128;
                 }
                 if (s->levelled[p]) {
                     // the team size must fit the smem budget (hands per block = 256 / team)
