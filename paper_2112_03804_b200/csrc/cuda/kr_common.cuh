@@ -108,15 +108,11 @@ __device__ __forceinline__ void pdl_entry() {
 // measured slower: their waiting CTAs hold SM slots the kernel before them
 // still needs).
 inline bool pdl_enabled(unsigned gridCtas) {
-    static const bool on = [] {
-        const char* env = std::getenv("KR_PDL");
-        return !(env && std::atoi(env) == 0);
-    }();
-    static const unsigned maxGrid = [] {
-        const char* env = std::getenv("KR_PDL_MAXGRID");
-        return env ? unsigned(std::atol(env)) : 2000u;
-    }();
-    return on && gridCtas <= maxGrid;
+    // read per launch (tens of ns against a launch), so a process can switch
+    const char* off = std::getenv("KR_PDL");
+    if (off && std::atoi(off) == 0) return false;
+    const char* mg = std::getenv("KR_PDL_MAXGRID");
+    return gridCtas <= (mg ? unsigned(std::atol(mg)) : 2000u);
 }
 
 template <class T>

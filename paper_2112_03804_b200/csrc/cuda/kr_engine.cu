@@ -1955,7 +1955,7 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
         }
         return a.type == cudaMemoryTypeHost;
     };
-    static const bool noGraph = std::getenv("KR_NO_PIPE_GRAPH") != nullptr;
+    const bool noGraph = std::getenv("KR_NO_PIPE_GRAPH") != nullptr;
     if (!noGraph && pinned(hin) && pinned(hout)) {
         for (auto& pg : e->pipeGraphs)
             if (pg.dir == dir && pg.in == hin && pg.out == hout) {

@@ -233,8 +233,9 @@ def test_pair_device_is_bitwise_ax_then_atx(kind, serial_gb, monkeypatch):
     assert torch.equal(ax, ax2) and torch.equal(atx, atx2)
 
 
+@pytest.mark.parametrize("no_graph", [False, True], ids=["graph", "enqueued"])
 @pytest.mark.parametrize("kind", ["factored", "implicit"])
-def test_pinned_host_calls_replay_a_graph_bitwise(kind):
+def test_pinned_host_calls_replay_a_graph_bitwise(kind, no_graph, monkeypatch):
     """kr_engine_ax / kr_engine_atx on pinned host buffers: the first call
     enqueues the pipeline, the second captures it into a CUDA graph, later
     calls replay it; every call returns the bits of the device-pointer path,
@@ -244,6 +245,8 @@ def test_pinned_host_calls_replay_a_graph_bitwise(kind):
 
     import torch
     from paper_2112_03804_b200 import _native as N
+    if no_graph:
+        monkeypatch.setenv("KR_NO_PIPE_GRAPH", "1")
     boards = H.turn_instances(nboards=3, factors=kind == "factored")
     eng = CudaEngine([f for _, f in boards]) if kind == "factored" else CudaEngine.kron([i for i, _ in boards])
     L = N.cuda()
