@@ -186,7 +186,8 @@ def test_device_pointer_entry_points():
 @pytest.mark.parametrize("groups,knob", [("1", None), ("2", None), ("3", None), ("4", None), ("4", ("KR_LPT", "0")),
                                          ("3", ("KR_LPT_ALL", "1")), ("2", ("KR_PF", "2")),
                                          ("3", ("KR_SELL_COMP", "1")), ("4", ("KR_ORDER", "sm")),
-                                         ("4", ("KR_XSEQ", "1"))])
+                                         ("4", ("KR_XSEQ", "1")), ("4", ("KR_PIPE_STREAMS", "2")),
+                                         ("4", ("KR_GROUP_SIZES", "1,2,1"))])
 def test_host_pipeline_groups_bitwise(groups, knob, monkeypatch):
     """kr_engine_ax / kr_engine_atx pipelined over board groups (each group's
     whole product on two streams, widest slices first) give the bits of the
@@ -211,14 +212,19 @@ def test_host_pipeline_groups_bitwise(groups, knob, monkeypatch):
 
 
 @pytest.mark.parametrize("serial_gb", [None, "0"], ids=["concurrent", "serial"])
-@pytest.mark.parametrize("kind", ["factored", "implicit"])
+@pytest.mark.parametrize("kind", ["factored", "implicit", "device_built"])
 def test_pair_device_is_bitwise_ax_then_atx(kind, serial_gb, monkeypatch):
     """kr_engine_pair_device (A^T y forked onto a side stream, own scratch)
     gives the bits of kr_engine_ax_device then kr_engine_atx_device, also
     when repeated back to back on the same buffers."""
     import torch
     boards = H.turn_instances(nboards=3, factors=kind == "factored")
-    eng = CudaEngine([f for _, f in boards]) if kind == "factored" else CudaEngine.kron([i for i, _ in boards])
+    if kind == "factored":
+        eng = CudaEngine([f for _, f in boards])
+    elif kind == "implicit":
+        eng = CudaEngine.kron([i for i, _ in boards])
+    else:
+        eng = CudaEngine.device_built([i for i, _ in boards])
     x = torch.randn(eng.cols, dtype=torch.float64, device="cuda")
     y = torch.randn(eng.rows, dtype=torch.float64, device="cuda")
     ax, atx = torch.empty(eng.rows, dtype=torch.float64, device="cuda"), torch.empty(eng.cols, dtype=torch.float64,
