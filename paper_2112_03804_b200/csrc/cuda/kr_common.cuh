@@ -107,12 +107,31 @@ __device__ __forceinline__ void pdl_entry() {
 // most this many CTAs are launched early (multi-wave grids launched early
 // measured slower: their waiting CTAs hold SM slots the kernel before them
 // still needs).
-inline bool pdl_enabled(unsigned gridCtas) {
+// afterSmall: launches whose early start only pays after a small kernel
+// (the team player step: launched early behind a ~400-CTA SpMV it measured
+// 14% slower for the config-2 factored solver, behind a 43-CTA K7 launch 4%
+// faster): those also need the previous kernel on the stream to have at most
+// KR_PDL_MAXPREV (128) CTAs.
+inline bool pdl_enabled(unsigned gridCtas, unsigned prevCtas, bool afterSmall) {
     // read per launch (tens of ns against a launch), so a process can switch
     const char* off = std::getenv("KR_PDL");
     if (off && std::atoi(off) == 0) return false;
     const char* mg = std::getenv("KR_PDL_MAXGRID");
-    return gridCtas <= (mg ? unsigned(std::atol(mg)) : 2000u);
+    if (gridCtas > (mg ? unsigned(std::atol(mg)) : 2000u)) return false;
+    if (!afterSmall) return true;
+    const char* mp = std::getenv("KR_PDL_MAXPREV");
+    return prevCtas <= (mp ? unsigned(std::atol(mp)) : 128u);
+}
+
+// Grid size of the last kernel this thread launched on each stream (the
+// early launch pays after small, latency-bound kernels).
+inline unsigned& last_grid(cudaStream_t s) {
+    thread_local std::vector<std::pair<cudaStream_t, unsigned>> last;
+    for (auto& e : last)
+        if (e.first == s) return e.second;
+    if (last.size() > 64) last.clear();
+    last.emplace_back(s, 0xffffffffu);
+    return last.back().second;
 }
 
 template <class T>
@@ -125,7 +144,8 @@ T* dev_alloc(int64_t n) {
 // kernel<<<grid, block, smem, stream>>>(args...) with the PDL attribute
 // (arguments coerced to the kernel's parameter types, as <<<>>> does).
 template <typename... KArgs, typename... Args>
-void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+void launch_pdl(bool afterSmall, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -135,8 +155,16 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled(grid.x * grid.y * grid.z) ? 1 : 0;
+    const unsigned ctas = grid.x * grid.y * grid.z;
+    unsigned& prev = last_grid(stream);
+    cfg.numAttrs = pdl_enabled(ctas, prev, afterSmall) ? 1 : 0;
+    prev = ctas;
     KR_CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+template <typename... KArgs, typename... Args>
+void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+    launch_pdl(false, kernel, grid, block, smem, stream, std::forward<Args>(args)...);
 }
 
 // Raise (never lower) a kernel's dynamic shared-memory limit: the attribute

@@ -681,7 +681,7 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
         if (grid == 0) return;
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
-        krb::launch(kern, grid, threads, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
+        krb::launch_pdl(true, kern, grid, threads, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
                                       hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule,
                                       dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr);
         KR_CK_LAUNCH();

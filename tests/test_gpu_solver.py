@@ -161,7 +161,7 @@ def test_cfr_plus_config1_1000_iterations():
 @pytest.mark.parametrize("knob", [("KR_STEP", "thread"), ("KR_TEAM", "2"), ("KR_TEAM", "8"), ("KR_NO_GRAPH", "1"),
                                   ("KR_CHAIN", "reg"), ("KR_NO_LEAN", "1"), ("KR_PF", "2"), ("KR_LPT_ALL", "1"),
                                   ("KR_BR_SERIAL", "1"), ("KR_SELL_COMP", "1"), ("KR_ORDER", "sm"),
-                                  ("KR_TEAM_THREADS", "256"), ("KR_PDL", "0"), ("KR_PDL_MAXGRID", "100000"),
+                                  ("KR_TEAM_THREADS", "256"), ("KR_PDL", "0"), ("KR_PDL_MAXGRID", "100000"), ("KR_PDL_MAXPREV", "100000"),
                                   ("KR_XSEQ", "1")])
 def test_knobs_keep_the_bits(knob, monkeypatch):
     """Every execution variant reproduces the oracle's gap
