@@ -56,12 +56,14 @@ constexpr int kWarps = kThreads / 32;
 // Hands per side per board are at most C(52,2) = 1326, so 3 m < 2^16.
 constexpr int kMaxHands = 1536;            // = kPer * kThreads
 constexpr int kPer = kMaxHands / kThreads; // hands per thread per board
+constexpr bool kKronSeqDefault = false;    // KR_KRON_SEQ, see kron_seq_major
 
 // Device view of one direction (0: A x, 1: Aᵀ y).
 struct KronDir {
     int nO = 0, nS = 0, nb = 0, sign = 1;
     int64_t mO = 0, mS = 0;
     int maxMS = 0;
+    int maxMO = 0;
     int64_t* sumOff = nullptr;    // [nb+1] global summing-hand offsets
     int64_t* outOff = nullptr;    // [nb+1] global output-hand offsets
     double* lamS = nullptr;       // [mS]
@@ -110,6 +112,12 @@ size_t fused_smem(int maxMS) {
 // card c's list in P, the W-weighted part of an output is
 //   lower − upper = (P[lt] + P[le] − TS) − (P[p1lt] + P[p1le])
 //                   − (P[p2lt] + P[p2le]) + G[c1] + G[c2],   G[c] = P[B_c] + P[E_c].
+//
+// SEQ: v and out are sequence-major per board (board b's block of m_b·n
+// values starts where it does hand-major, laid out [seq][hand]), so the
+// gathers of step 1 and the stores of step 3 are coalesced across the CTA;
+// k_board_transpose converts around the kernel.
+template <bool SEQ>
 __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
                                                          double* __restrict__ out) {
     krb::pdl_entry();
@@ -143,21 +151,22 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
         const int64_t* sp = d.sptr + int64_t(b) * (d.nO + 1) + a;
         const int64_t f0 = fp[0], f1 = fp[1], s0 = sp[0], s1 = sp[1];
         const int64_t nS = d.nS;
-        const double* v0 = in + (sBase + tid) * nS;
-        const int64_t step = int64_t(kThreads) * nS;
+        const double* v0 = SEQ ? in + sBase * nS + tid : in + (sBase + tid) * nS;
+        const int64_t step = SEQ ? int64_t(kThreads) : int64_t(kThreads) * nS;
+        const int64_t colMul = SEQ ? int64_t(mSb) : 1;
         double f[kPer], s[kPer];
 #pragma unroll
         for (int q = 0; q < kPer; ++q) f[q] = s[q] = 0.0;
         for (int64_t e = f0; e < f1; ++e) {
             const double val = __ldg(d.fval + e);
-            const double* vc = v0 + __ldg(d.fcol + e);
+            const double* vc = v0 + __ldg(d.fcol + e) * colMul;
 #pragma unroll
             for (int q = 0; q < kPer; ++q)
                 if (tid + q * kThreads < mSb) f[q] += val * __ldg(vc + q * step);
         }
         for (int64_t e = s0; e < s1; ++e) {
             const double val = __ldg(d.sval + e);
-            const double* vc = v0 + __ldg(d.scol + e);
+            const double* vc = v0 + __ldg(d.scol + e) * colMul;
 #pragma unroll
             for (int q = 0; q < kPer; ++q)
                 if (tid + q * kThreads < mSb) s[q] += val * __ldg(vc + q * step);
@@ -262,8 +271,45 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
             double fpart = TF - CF[c1] - CF[c2];
             if (dup >= 0) fpart += W[dup].y;
             const double wsum = (P[lt] + P[le] - TS) - (P[p1lt] + P[p1le]) - (P[p2lt] + P[p2le]) + G[c1] + G[c2];
-            out[(oBase + i) * d.nO + a] = lo[q] * (fpart + sg * wsum);
+            const double r = lo[q] * (fpart + sg * wsum);
+            if (SEQ) out[oBase * d.nO + int64_t(a) * mOb + i] = r;
+            else out[(oBase + i) * d.nO + a] = r;
         }
+    }
+}
+
+// Per-board transpose between hand-major [hand][seq] and sequence-major
+// [seq][hand] (board b's block starts at off[b]·n either way).  32×32 tiles
+// through shared memory, so both the loads and the stores are coalesced.
+// grid = (hand tiles × sequence tiles, boards).
+__global__ void __launch_bounds__(256) k_board_transpose(const double* __restrict__ src, double* __restrict__ dst,
+                                                         const int64_t* __restrict__ off, int n, int b0,
+                                                         int toSeq) {
+    krb::pdl_entry();
+    __shared__ double t[32][33];
+    const int b = b0 + int(blockIdx.y);
+    const int64_t base = off[b] * n;
+    const int m = int(off[b + 1] - off[b]);
+    const int tilesS = (n + 31) >> 5;
+    const int h0 = int(blockIdx.x / unsigned(tilesS)) * 32, s0 = int(blockIdx.x % unsigned(tilesS)) * 32;
+    if (h0 >= m) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    if (toSeq) {  // read rows h (contiguous s), write rows s (contiguous h)
+#pragma unroll
+        for (int r = ty; r < 32; r += 8)
+            if (h0 + r < m && s0 + tx < n) t[r][tx] = src[base + int64_t(h0 + r) * n + s0 + tx];
+        __syncthreads();
+#pragma unroll
+        for (int r = ty; r < 32; r += 8)
+            if (s0 + r < n && h0 + tx < m) dst[base + int64_t(s0 + r) * m + h0 + tx] = t[tx][r];
+    } else {
+#pragma unroll
+        for (int r = ty; r < 32; r += 8)
+            if (s0 + r < n && h0 + tx < m) t[tx][r] = src[base + int64_t(s0 + r) * m + h0 + tx];
+        __syncthreads();
+#pragma unroll
+        for (int r = ty; r < 32; r += 8)
+            if (h0 + r < m && s0 + tx < n) dst[base + int64_t(h0 + r) * n + s0 + tx] = t[r][tx];
     }
 }
 
@@ -351,6 +397,7 @@ void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
         if (mS > kMaxHands || sO.m > kMaxHands)
             throw Fail{KR_INVALID_INPUT, "more than 1536 hands on one side of a board"};
         d.maxMS = std::max(d.maxMS, mS);
+        d.maxMO = std::max(d.maxMO, sO.m);
         sumOff[size_t(b) + 1] = sumOff[size_t(b)] + mS;
         outOff[size_t(b) + 1] = outOff[size_t(b)] + sO.m;
         lamS.insert(lamS.end(), sS.lam, sS.lam + mS);
@@ -472,13 +519,28 @@ void validate_board(const kr_kron_board& B, const kr_kron_board& B0, int b) {
 struct KronState {
     KronDir dir[2];
     size_t smem[2] = {0, 0};
+    // sequence-major copies of each direction's input and output (one pair
+    // per direction: kr_engine_pair_device runs the two concurrently)
+    double* seqIn[2] = {nullptr, nullptr};
+    double* seqOut[2] = {nullptr, nullptr};
 };
 
 void kron_destroy(KronState* k) {
     if (!k) return;
     free_dir(k->dir[0]);
     free_dir(k->dir[1]);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(k->seqIn[i]);
+        cudaFree(k->seqOut[i]);
+    }
     delete k;
+}
+
+// KR_KRON_SEQ=1: the product runs sequence-major (transpose in, K7<SEQ>,
+// transpose out); read per launch so a process can switch.
+bool kron_seq_major() {
+    const char* env = std::getenv("KR_KRON_SEQ");
+    return env ? std::atoi(env) != 0 : kKronSeqDefault;
 }
 
 void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
@@ -486,9 +548,25 @@ void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStre
     KronDir& d = k->dir[dir];
     if (b1 < 0) b1 = d.nb;
     if (d.mO * d.nO == 0 || b1 <= b0) return;
-    krb::launch(k_kron_fused, dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads, k->smem[dir], s, d, b0, in, out);
+    if (!kron_seq_major()) {
+        krb::launch(k_kron_fused<false>, dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads, k->smem[dir], s, d, b0,
+                    in, out);
+        KR_CK_LAUNCH();
+        e->launches++;
+        return;
+    }
+    const unsigned nb = unsigned(b1 - b0);
+    const unsigned tilesS = unsigned((d.nS + 31) / 32), tilesO = unsigned((d.nO + 31) / 32);
+    krb::launch(k_board_transpose, dim3(unsigned((d.maxMS + 31) / 32) * tilesS, nb), 256, 0, s, in, k->seqIn[dir],
+                d.sumOff, d.nS, b0, 1);
     KR_CK_LAUNCH();
-    e->launches++;
+    krb::launch(k_kron_fused<true>, dim3(unsigned(d.nO), nb), kThreads, k->smem[dir], s, d, b0, k->seqIn[dir],
+                k->seqOut[dir]);
+    KR_CK_LAUNCH();
+    krb::launch(k_board_transpose, dim3(unsigned((d.maxMO + 31) / 32) * tilesO, nb), 256, 0, s, k->seqOut[dir], out,
+                d.outOff, d.nO, b0, 0);
+    KR_CK_LAUNCH();
+    e->launches += 3;
 }
 
 int64_t kron_flops(const kr_engine* e, int dir) { return e->kron->dir[dir].flops; }
@@ -527,7 +605,12 @@ kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, u
             smMax = std::max(smMax, e->kron->smem[dir]);
         }
         if (smMax > 227 * 1024) throw Fail{KR_INVALID_INPUT, "board has too many hands for the implicit engine"};
-        raise_smem_limit(k_kron_fused, smMax);
+        raise_smem_limit(k_kron_fused<false>, smMax);
+        raise_smem_limit(k_kron_fused<true>, smMax);
+        for (int dir = 0; dir < 2; ++dir) {
+            e->kron->seqIn[dir] = dev_alloc<double>(dir == 0 ? C : R);
+            e->kron->seqOut[dir] = dev_alloc<double>(dir == 0 ? R : C);
+        }
         e->flops_per_product = e->kron->dir[0].flops;
         e->d_in = dev_alloc<double>(std::max(R, C));
         e->d_out = dev_alloc<double>(std::max(R, C));

@@ -48,13 +48,17 @@ def test_kron_matches_reference_matvec(name, kw):
     assert worst <= TOL, worst
 
 
-def test_kron_launches_and_flops():
+@pytest.mark.parametrize("seq,per_product", [("0", 1), ("1", 3)])
+def test_kron_launches_and_flops(seq, per_product, monkeypatch):
+    # KR_KRON_SEQ=0: one fused kernel per product; =1: transpose, fused
+    # kernel, transpose
+    monkeypatch.setenv("KR_KRON_SEQ", seq)
     p = H.builtin("twenty_card")
     eng = CudaEngine.kron(p)
     l0 = eng.launches()
     eng.Ax(np.ones(p.cols))
     eng.ATx(np.ones(p.rows))
-    assert eng.launches() - l0 == 2  # one fused kernel per product
+    assert eng.launches() - l0 == 2 * per_product
     assert eng.last_flops() > 0 and eng.flops() >= eng.last_flops()
 
 
