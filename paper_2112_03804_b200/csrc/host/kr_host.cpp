@@ -1376,7 +1376,7 @@ Factors readBundle(const std::string& dir) {  // bundle_io.hpp:57-94
 // ==================================================================== C ABI
 struct krh_instance {
     krh::Instance in;
-    std::vector<uint8_t> cards[2];  // card ids per hand, filled by krh_instance_kron_view
+    std::vector<uint8_t> cards[2] = {};  // card ids per hand, filled by krh_instance_kron_view
 };
 struct krh_factors {
     krh::Factors f;
