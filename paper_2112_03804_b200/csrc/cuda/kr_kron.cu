@@ -43,8 +43,10 @@ namespace krb {
 namespace {
 
 constexpr int kCards = 52;
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+#ifndef KR_K7_THREADS
+#define KR_K7_THREADS 256
+#endif
+constexpr int kThreads = KR_K7_THREADS;  // threads per CTA (compile-time: A/B builds)
 
 // Lookup table of one output hand, packed in 16 bytes (positions in the
 // kernel's virtual prefix array; list starts and ends come from the staged
@@ -54,9 +56,10 @@ constexpr int kWarps = kThreads / 32;
 //   z = p1lt | p1le << 16      (m + the same ranks inside the list of c1)
 //   w = p2lt | p2le << 16      (m + ... inside the list of c2)
 // Hands per side per board are at most C(52,2) = 1326, so 3 m < 2^16.
-constexpr int kMaxHands = 1536;            // = kPer * kThreads
-constexpr int kPer = kMaxHands / kThreads; // hands per thread per board
+constexpr int kMaxHands = 1536;            // hands per side and board; a thread takes kMaxHands / T
 constexpr bool kKronSeqDefault = false;    // KR_KRON_SEQ, see kron_seq_major
+constexpr int64_t kSmallGrid = 148;        // K7 grids up to this many CTAs run 512-thread CTAs
+static_assert(kMaxHands % 512 == 0, "512-thread K7 CTAs");
 
 // Device view of one direction (0: A x, 1: Aᵀ y).
 struct KronDir {
@@ -117,12 +120,13 @@ size_t fused_smem(int maxMS) {
 // values starts where it does hand-major, laid out [seq][hand]), so the
 // gathers of step 1 and the stores of step 3 are coalesced across the CTA;
 // k_board_transpose converts around the kernel.
-template <bool SEQ>
-__global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
+template <bool SEQ, int T>
+__global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
                                                          double* __restrict__ out) {
+    constexpr int kPerT = kMaxHands / T, kWarpsT = T / 32;
     krb::pdl_entry();
     extern __shared__ double sm[];
-    __shared__ double warpV[kWarps], warpW[kWarps];
+    __shared__ double warpV[kWarpsT], warpW[kWarpsT];
     const int a = blockIdx.x, b = b0 + int(blockIdx.y);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t sBase = d.sumOff[b];
@@ -138,42 +142,42 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
 
     // 1. weights of every summing hand for sequence a: the few F/S entries of
     // row a are uniform across the CTA, so each thread issues the gathers of
-    // all its kPer hands back to back.  The card lists are staged meanwhile.
+    // all its kPerT hands back to back.  The card lists are staged meanwhile.
     {
         const int32_t* lb = d.listPtr + int64_t(b) * (kCards + 1);
         if (tid <= kCards) lptr[tid] = __ldg(lb + tid);
         const int32_t* hands = d.listHands + d.listBase[b];
 #pragma unroll
-        for (int q = 0; q < 2 * kPer; ++q)
-            if (tid + q * kThreads < 2 * mSb) lhand[tid + q * kThreads] = __ldg(hands + tid + q * kThreads);
+        for (int q = 0; q < 2 * kPerT; ++q)
+            if (tid + q * T < 2 * mSb) lhand[tid + q * T] = __ldg(hands + tid + q * T);
 
         const int64_t* fp = d.fptr + int64_t(b) * (d.nO + 1) + a;
         const int64_t* sp = d.sptr + int64_t(b) * (d.nO + 1) + a;
         const int64_t f0 = fp[0], f1 = fp[1], s0 = sp[0], s1 = sp[1];
         const int64_t nS = d.nS;
         const double* v0 = SEQ ? in + sBase * nS + tid : in + (sBase + tid) * nS;
-        const int64_t step = SEQ ? int64_t(kThreads) : int64_t(kThreads) * nS;
+        const int64_t step = SEQ ? int64_t(T) : int64_t(T) * nS;
         const int64_t colMul = SEQ ? int64_t(mSb) : 1;
-        double f[kPer], s[kPer];
+        double f[kPerT], s[kPerT];
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) f[q] = s[q] = 0.0;
+        for (int q = 0; q < kPerT; ++q) f[q] = s[q] = 0.0;
         for (int64_t e = f0; e < f1; ++e) {
             const double val = __ldg(d.fval + e);
             const double* vc = v0 + __ldg(d.fcol + e) * colMul;
 #pragma unroll
-            for (int q = 0; q < kPer; ++q)
-                if (tid + q * kThreads < mSb) f[q] += val * __ldg(vc + q * step);
+            for (int q = 0; q < kPerT; ++q)
+                if (tid + q * T < mSb) f[q] += val * __ldg(vc + q * step);
         }
         for (int64_t e = s0; e < s1; ++e) {
             const double val = __ldg(d.sval + e);
             const double* vc = v0 + __ldg(d.scol + e) * colMul;
 #pragma unroll
-            for (int q = 0; q < kPer; ++q)
-                if (tid + q * kThreads < mSb) s[q] += val * __ldg(vc + q * step);
+            for (int q = 0; q < kPerT; ++q)
+                if (tid + q * T < mSb) s[q] += val * __ldg(vc + q * step);
         }
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int j = tid + q * kThreads;
+        for (int q = 0; q < kPerT; ++q) {
+            const int j = tid + q * T;
             if (j < mSb) {
                 const double lam = __ldg(d.lamS + sBase + j);
                 W[j] = make_double2(lam * s[q], lam * f[q]);
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
     __syncthreads();
 
     // 2. one block scan over the virtual array (contiguous chunk per thread)
-    const int chunk = (N + kThreads - 1) / kThreads;
+    const int chunk = (N + T - 1) / T;
     const int j0 = min(N, tid * chunk), j1 = min(N, j0 + chunk);
     double sv = 0.0, sw = 0.0;
 #pragma unroll 4
@@ -204,11 +208,11 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
     // resident CTA but is 15% slower)
     const int64_t oBase = d.outOff[b];
     const int mOb = int(d.outOff[b + 1] - oBase);
-    int4 tb[kPer];
-    double lo[kPer];
+    int4 tb[kPerT];
+    double lo[kPerT];
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const int i = tid + q * kThreads;
+    for (int q = 0; q < kPerT; ++q) {
+        const int i = tid + q * T;
         if (i < mOb) {
             tb[q] = __ldg(d.otab + oBase + i);
             lo[q] = __ldg(d.lamO + oBase + i);
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
             for (; p < B; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
             QB[nc] = runQ;
         }
-        if (tid == kThreads - 1) {
+        if (tid == T - 1) {
             for (; p < j1; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
             for (; nc <= kCards; ++nc) QB[nc] = runQ;  // lists ending at N
         }
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
         P[p] = run;
         run += v;
     }
-    if (tid == kThreads - 1) P[N] = run;
+    if (tid == T - 1) P[N] = run;
     __syncthreads();
     if (tid < kCards) {  // per-card terms
         G[tid] = P[mSb + lptr[tid]] + P[mSb + lptr[tid + 1]];
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(kThreads) k_kron_fused(KronDir d, int b0, cons
     const double TS = P[mSb];
     const double sg = double(d.sign);
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const int i = tid + q * kThreads;
+    for (int q = 0; q < kPerT; ++q) {
+        const int i = tid + q * T;
         if (i < mOb) {
             const int4 t = tb[q];
             const int lt = t.x & 0xffff, le = t.x >> 16;
@@ -548,9 +552,19 @@ void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStre
     KronDir& d = k->dir[dir];
     if (b1 < 0) b1 = d.nb;
     if (d.mO * d.nO == 0 || b1 <= b0) return;
+    // Engines whose whole grid has at most one CTA per SM (single boards) run
+    // 512-thread CTAs: that shortens each CTA, which is the whole launch.
+    // Larger grids keep 256 (measured: config 2 14.5 -> 13.3 us per pair,
+    // config 3 110 -> 123 us with 512).  Decided per engine, not per launch,
+    // so board-group sub-launches sum in the same order as whole-range ones.
+    const bool wide = int64_t(d.nO) * d.nb <= kSmallGrid;
     if (!kron_seq_major()) {
-        krb::launch(k_kron_fused<false>, dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads, k->smem[dir], s, d, b0,
-                    in, out);
+        if (wide)
+            krb::launch(k_kron_fused<false, 512>, dim3(unsigned(d.nO), unsigned(b1 - b0)), 512, k->smem[dir], s, d,
+                        b0, in, out);
+        else
+            krb::launch(k_kron_fused<false, kThreads>, dim3(unsigned(d.nO), unsigned(b1 - b0)), kThreads,
+                        k->smem[dir], s, d, b0, in, out);
         KR_CK_LAUNCH();
         e->launches++;
         return;
@@ -560,8 +574,12 @@ void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStre
     krb::launch(k_board_transpose, dim3(unsigned((d.maxMS + 31) / 32) * tilesS, nb), 256, 0, s, in, k->seqIn[dir],
                 d.sumOff, d.nS, b0, 1);
     KR_CK_LAUNCH();
-    krb::launch(k_kron_fused<true>, dim3(unsigned(d.nO), nb), kThreads, k->smem[dir], s, d, b0, k->seqIn[dir],
-                k->seqOut[dir]);
+    if (wide)
+        krb::launch(k_kron_fused<true, 512>, dim3(unsigned(d.nO), nb), 512, k->smem[dir], s, d, b0, k->seqIn[dir],
+                    k->seqOut[dir]);
+    else
+        krb::launch(k_kron_fused<true, kThreads>, dim3(unsigned(d.nO), nb), kThreads, k->smem[dir], s, d, b0,
+                    k->seqIn[dir], k->seqOut[dir]);
     KR_CK_LAUNCH();
     krb::launch(k_board_transpose, dim3(unsigned((d.maxMO + 31) / 32) * tilesO, nb), 256, 0, s, k->seqOut[dir], out,
                 d.outOff, d.nO, b0, 0);
@@ -605,8 +623,10 @@ kr_engine* create_kron_engine(const kr_kron_board* boards, int nb, int device, u
             smMax = std::max(smMax, e->kron->smem[dir]);
         }
         if (smMax > 227 * 1024) throw Fail{KR_INVALID_INPUT, "board has too many hands for the implicit engine"};
-        raise_smem_limit(k_kron_fused<false>, smMax);
-        raise_smem_limit(k_kron_fused<true>, smMax);
+        raise_smem_limit(k_kron_fused<false, kThreads>, smMax);
+        raise_smem_limit(k_kron_fused<false, 512>, smMax);
+        raise_smem_limit(k_kron_fused<true, kThreads>, smMax);
+        raise_smem_limit(k_kron_fused<true, 512>, smMax);
         for (int dir = 0; dir < 2; ++dir) {
             e->kron->seqIn[dir] = dev_alloc<double>(dir == 0 ? C : R);
             e->kron->seqOut[dir] = dev_alloc<double>(dir == 0 ? R : C);
