@@ -854,6 +854,11 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 if (krb::step_smem(t.n_seq, nt, t.n_nodes, na) > 220 * 1024)
                     throw Fail{KR_INVALID_INPUT, "treeplex too large for the on-chip solver step"};
                 s->nt[p] = nt;
+                // single-board engines: eight lanes per hand (their grids are a
+                // few dozen blocks; config 2 measured 19,000 -> 22,500 K7 DCFR
+                // it/s and 6,410 -> 6,850 factored, tools/config2_team_probe.py);
+                // multi-board grids keep four (config 3: 2/4/8 within +-1.2%)
+                s->team = nboards == 1 ? 8 : 4;
                 if (const char* env = std::getenv("KR_TEAM")) {
                     const int tm = std::atoi(env);
                     s->team = tm == 2 || tm == 8 ? tm : 4;
