@@ -112,6 +112,18 @@ void kr_devfactors_free(kr_devfactors* f);
 int kr_engine_create_device_b(const kr_kron_board* boards, int nboards, int device, uint32_t flags,
                               kr_engine** out);
 
+/* The Kronecker-factored engine: Technique B with postprocessing
+ * (sparsify.hpp:246-406) kept as its hand-space factors (lambda1, lambda2, the
+ * blocked-hand lists of Hx, the sparsity of Y = D W) and the tree's F and S,
+ * with every Kronecker product expanded on the fly (a few hundred KB per board
+ * instead of the ~150 MB of expanded factors).  Products are BITWISE those of
+ * kr_engine_create on the host builder's Technique B post factors (same terms,
+ * same order, engine.hpp:58-133); one fused launch per product, one CTA per
+ * (sequence, board).  Boards of at most 2047 hands per side.  Replaces
+ * FactoredEngine(techniqueB + postprocess) (solver.hpp:30-40). */
+int kr_engine_create_kfactored(const kr_kron_board* boards, int nboards, int device, uint32_t flags,
+                               kr_engine** out);
+
 /* Create an engine for one Sparsification on CUDA device `device`.
  * Replaces FactoredEngine(const Sparsification&) (solver.hpp:32); the
  * factors are copied to HBM, so the caller may free them afterwards. */

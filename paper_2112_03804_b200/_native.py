@@ -101,7 +101,7 @@ CUDA_SYMBOLS = [
     "kr_solver_set_rule", "kr_turn_solver_create", "kr_turn_solver_run", "kr_turn_solver_destroy",
     "kr_turn_solver_launches", "kr_turn_solver_set_exchange", "kr_turn_solver_sizes",
     "kr_factors_build_device", "kr_devfactors_view", "kr_devfactors_seconds", "kr_devfactors_free",
-    "kr_engine_create_device_b",
+    "kr_engine_create_device_b", "kr_engine_create_kfactored",
 ]
 
 
@@ -168,6 +168,8 @@ def cuda():
         L.kr_turn_solver_sizes.argtypes = [C.c_void_p, C.c_void_p]
         L.kr_engine_create_device_b.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.c_int, C.c_uint32,
                                                 C.POINTER(C.c_void_p)]
+        L.kr_engine_create_kfactored.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.c_int, C.c_uint32,
+                                                 C.POINTER(C.c_void_p)]
         L.kr_factors_build_device.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.POINTER(C.c_void_p)]
         L.kr_devfactors_view.argtypes = [C.c_void_p, C.POINTER(kr_factors)]
         L.kr_devfactors_seconds.restype = C.c_double

@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2112_03804_b200")
 LIBDIR = os.path.join(PKG, "lib")
-CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu")]
+CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu", "kr_kfengine.cu")]
 HOST_SRC = [os.path.join(PKG, "csrc", "host", f) for f in ("kr_host.cpp",)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # the system g++ links libstdc++ dynamically (a statically linked libstdc++
@@ -48,14 +48,33 @@ def _stale(target, sources):
 
 
 def build_cuda(force=False, verbose=False):
+    """One object per .cu, compiled in parallel, then one shared-library link
+    (no relocatable device code: kernels never cross translation units)."""
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(LIBDIR, exist_ok=True)
     out = os.path.join(LIBDIR, "libkrcuda.so")
     srcs = [s for s in CUDA_SRC if os.path.exists(s)]
-    if force or _stale(out, srcs):
-        cmd = [NVCC, *NVCC_FLAGS, "-o", out, *srcs]
+    if not (force or _stale(out, srcs)):
+        return out
+    objdir = os.path.join(ROOT, "build", "cuda")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in srcs]
+
+    def one(so):
+        s, o = so
+        cmd = [NVCC, *compile_flags, "-c", "-o", o, s]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        list(ex.map(one, zip(srcs, objs)))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", CXX, "-shared", "-cudart", "static",
+           "-o", out, *objs]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
     return out
 
 

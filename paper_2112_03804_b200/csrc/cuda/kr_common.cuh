@@ -185,6 +185,10 @@ int64_t kron_flops(const kr_engine* e, int dir);
 int kron_boards(const kr_engine* e);
 void kron_destroy(KronState* k);
 
+struct KfState;  // Kronecker-factored engine (kr_kfengine.cu)
+void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0 = 0, int b1 = -1);
+void kf_destroy(KfState* k);
+
 }  // namespace krb
 
 // Engine state (opaque to C callers).
@@ -252,6 +256,9 @@ struct kr_engine {
     double tMs[4] = {0, 0, 0, 0};
     // implicit Kronecker mode (kr_engine_create_kron): no factors at all
     krb::KronState* kron = nullptr;
+    // Kronecker-factored mode (kr_engine_create_kfactored): Technique B post
+    // from its hand-space factors, products bitwise the factored engine's
+    krb::KfState* kf = nullptr;
     int pf = 0;  // SELL slice L2 prefetch distance in batches (KR_PF)
     // Board groups.  Host-buffer calls pipeline over them: input copies,
     // per-group kernels and output copies run concurrently (copyIn / stream /

@@ -1213,6 +1213,7 @@ void destroy_engine(kr_engine* e) {
     if (e->evFork) cudaEventDestroy(e->evFork);
     if (e->evJoin) cudaEventDestroy(e->evJoin);
     kron_destroy(e->kron);
+    kf_destroy(e->kf);
     free_sell(e->VT);
     free_sell(e->UA);
     free_sell(e->UT);
@@ -1873,7 +1874,7 @@ void seq_major(kr_engine* e, const double* x, int64_t c0, int64_t c1, cudaStream
 }
 
 void first_stage(kr_engine* e, int dir, const double* in, cudaStream_t s, int g = -1) {
-    if (e->kron) return;
+    if (e->kron || e->kf) return;
     const int b0 = g < 0 ? 0 : e->grpBoard[size_t(g)], b1 = g < 0 ? -1 : e->grpBoard[size_t(g) + 1];
     if (dir == 0) {
         const double* xg = in;
@@ -1888,7 +1889,7 @@ void first_stage(kr_engine* e, int dir, const double* in, cudaStream_t s, int g 
 }
 
 void middle(kr_engine* e, int dir, cudaStream_t s, int g = -1) {
-    if (e->kron) return;
+    if (e->kron || e->kf) return;
     const int64_t c0 = g < 0 ? 0 : e->bCh[size_t(e->grpBoard[size_t(g)])];
     const int64_t c1 = g < 0 ? -1 : e->bCh[size_t(e->grpBoard[size_t(g) + 1])];
     if (dir == 0) solve_forward(e, s, c0, c1);   // z = M^-1 t    engine.hpp:74-78
@@ -1898,6 +1899,7 @@ void middle(kr_engine* e, int dir, cudaStream_t s, int g = -1) {
 void last_stage(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int g = -1) {
     const int b0 = g < 0 ? 0 : e->grpBoard[size_t(g)], b1 = g < 0 ? -1 : e->grpBoard[size_t(g) + 1];
     if (e->kron) return kron_product(e, dir, in, out, s, b0, b1);
+    if (e->kf) return kf_product(e, dir, in, out, s, b0, b1);
     if (dir == 0) launch_sell(e, 1, e->UA, e->d_tz, in, e->kpad, out, s, b0, b1);   // y = U z + Ahat x
     else launch_sell(e, 3, e->AV, in, e->d_tz2, e->rows, out, s, b0, b1);          // x = Ahat^T y + V z
 }
@@ -2037,7 +2039,7 @@ void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout) {
     // group's first SpMV streams on the main stream (each kernel's tail under
     // the other's), its output copy on copyOut.  The level solve (mkind 2)
     // spans boards, so there it waits for every group's first stage.
-    if (e->kron) {
+    if (e->kron || e->kf) {
         for (int g = 0; g < G; ++g) {
             copy_in(g + 1);
             KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
@@ -2169,7 +2171,7 @@ int kr_engine_pair_device(kr_engine* e, const double* x, double* ax, const doubl
         // the other there.
         const char* sgb = std::getenv("KR_PAIR_SERIAL_GB");
         const double serialGB = sgb ? std::atof(sgb) : 8.0;
-        const double pairGB = e->kron ? 0.0 : 12e-9 * 2.0 * double(e->nnzA + e->nnzU + e->nnzV);
+        const double pairGB = (e->kron || e->kf) ? 0.0 : 12e-9 * 2.0 * double(e->nnzA + e->nnzU + e->nnzV);
         if (pairGB > serialGB) {
             krb::engine_ax(e, x, ax, s);
             krb::engine_atx(e, y, atx, s);

@@ -40,7 +40,7 @@ struct kr_solver {
     int32_t na[2] = {0, 0};      // actions (entries of action_seq)
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
-    int team = 4;                // lanes per hand in k_player_team (2, 4 or 8)
+    int team[2] = {4, 4};        // lanes per hand in k_player_team (2, 4 or 8), per player
     int teamThreads = 128;       // threads per k_player_team block (KR_TEAM_THREADS: 64, 128 or 256)
     // graph replay of whole iterations (kr_solver_run without early stop):
     // per-iteration factors pos/neg/shrink and weightSum as device tables
@@ -675,7 +675,7 @@ size_t step_smem(int n, int nt, int nn, int na) {
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
                  cudaStream_t st, bool dev = false) {
     if (s->levelled[p]) {
-        const int team = s->team, threads = s->teamThreads;
+        const int team = s->team[p], threads = s->teamThreads;
         const int hpb = threads / team;
         const unsigned grid = unsigned((s->H[p] + hpb - 1) / hpb);
         if (grid == 0) return;
@@ -807,6 +807,20 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
             s->pot = pot;
             const kr_treeplex* tp[2] = {p1, p2};
             const int32_t* hands[2] = {hands1, hands2};
+            // single-board engines: eight lanes per hand (their grids are a
+            // few dozen blocks; config 2 measured 19,000 -> 22,500 K7 DCFR
+            // it/s and 6,410 -> 6,850 factored, tools/config2_team_probe.py);
+            // multi-board grids keep four (config 3: 2/4/8 within +-1.2%).
+            // Read once, before the per-player fit below.
+            int team0 = nboards == 1 ? 8 : 4;
+            if (const char* env = std::getenv("KR_TEAM")) {
+                const int tm = std::atoi(env);
+                team0 = tm == 2 || tm == 8 ? tm : 4;
+            }
+            if (const char* env = std::getenv("KR_TEAM_THREADS")) {
+                const int th = std::atoi(env);
+                s->teamThreads = th == 64 || th == 256 ? th : 128;
+            }
             for (int p = 0; p < 2; ++p) {
                 const kr_treeplex& t = *tp[p];
                 if (t.n_seq < 1 || t.n_nodes < 1) throw Fail{KR_INVALID_INPUT, "empty treeplex"};
@@ -854,24 +868,15 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 if (krb::step_smem(t.n_seq, nt, t.n_nodes, na) > 220 * 1024)
                     throw Fail{KR_INVALID_INPUT, "treeplex too large for the on-chip solver step"};
                 s->nt[p] = nt;
-                // single-board engines: eight lanes per hand (their grids are a
-                // few dozen blocks; config 2 measured 19,000 -> 22,500 K7 DCFR
-                // it/s and 6,410 -> 6,850 factored, tools/config2_team_probe.py);
-                // multi-board grids keep four (config 3: 2/4/8 within +-1.2%)
-                s->team = nboards == 1 ? 8 : 4;
-                if (const char* env = std::getenv("KR_TEAM")) {
-                    const int tm = std::atoi(env);
-                    s->team = tm == 2 || tm == 8 ? tm : 4;
-                }
-                if (const char* env = std::getenv("KR_TEAM_THREADS")) {
-                    const int th = std::atoi(env);
-                    s->teamThreads = th == 64 || th == 256 ? th : 128;
-                }
+                // lanes per hand: the default (or KR_TEAM) raised, per player, until
+                // that player's block fits the shared-memory budget; sized with the
+                // launch's own hands per block (teamThreads / team)
+                s->team[p] = team0;
                 if (s->levelled[p]) {
-                    // the team size must fit the smem budget (hands per block = 256 / team)
-                    while (s->team < 8 && krb::team_smem(t.n_seq, t.n_nodes, 256 / s->team, s->treeLen[p]) > 200 * 1024)
-                        s->team *= 2;
-                    const size_t tsm = krb::team_smem(t.n_seq, t.n_nodes, 256 / s->team, s->treeLen[p]);
+                    while (s->team[p] < 8 &&
+                           krb::team_smem(t.n_seq, t.n_nodes, s->teamThreads / s->team[p], s->treeLen[p]) > 200 * 1024)
+                        s->team[p] *= 2;
+                    const size_t tsm = krb::team_smem(t.n_seq, t.n_nodes, s->teamThreads / s->team[p], s->treeLen[p]);
                     if (tsm > 220 * 1024) s->levelled[p] = false;
                 }
                 const int64_t len = s->H[p] * s->n[p];
@@ -885,11 +890,12 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                 for (int p = 0; p < 2; ++p)
                     satt = std::max(satt, krb::step_smem(s->n[p], s->nt[p], s->nnodes[p], s->na[p]));
                 krb::raise_smem_limit(krb::k_player_step, satt);
-                // one attribute for both players (the final team size)
+                // one attribute for both players (each with its own team size)
                 size_t att = 48 * 1024;
                 for (int p = 0; p < 2; ++p)
                     if (s->levelled[p])
-                        att = std::max(att, krb::team_smem(s->n[p], s->nnodes[p], 256 / s->team, s->treeLen[p]));
+                        att = std::max(att, krb::team_smem(s->n[p], s->nnodes[p], s->teamThreads / s->team[p],
+                                                           s->treeLen[p]));
                 krb::raise_smem_limit(krb::k_player_team<2>, att);
                 krb::raise_smem_limit(krb::k_player_team<4>, att);
                 krb::raise_smem_limit(krb::k_player_team<8>, att);

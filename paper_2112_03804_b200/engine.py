@@ -80,7 +80,24 @@ class CudaEngine:
         self._attach(h, device, len(insts))
         return self
 
+    @classmethod
+    def kfactored(cls, instances, device=0, flags=0):
+        """Kronecker-factored engine (kr_engine_create_kfactored): Technique B
+        post kept as its hand-space factors and the tree's F and S, every
+        Kronecker product expanded on the fly; products bitwise those of
+        CudaEngine([inst.sparsify("b", True) ...])."""
+        L = N.cuda()
+        insts = instances if isinstance(instances, (list, tuple)) else [instances]
+        arr = (N.kr_kron_board * len(insts))(*[i.kron_view() for i in insts])
+        h = C.c_void_p()
+        N.check(L.kr_engine_create_kfactored(arr, len(insts), device, flags, C.byref(h)))
+        self = cls.__new__(cls)
+        self._attach(h, device, len(insts))
+        self.kfactored_mode = True
+        return self
+
     implicit = False
+    kfactored_mode = False
 
     def _attach(self, h, device, nboards):
         self._h = h

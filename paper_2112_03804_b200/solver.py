@@ -105,6 +105,7 @@ class CudaSolver:
         self._h = h
         self.engine = engine  # keep alive: the solver borrows the engine (solver.hpp:32 ownership rule)
         self.nboards = len(h1)
+        self.pot = float(pot)
         self.rows, self.cols = engine.rows, engine.cols
 
     def close(self):
@@ -173,11 +174,16 @@ class CudaSolver:
         N.check(N.cuda().kr_solver_best_response(self._h, player, N.ptr(opp), len(opp), C.byref(v), N.ptr(bv)))
         return (v.value, bv) if per_board else v.value
 
+    def best_responses(self, x1, x2):
+        """The two best-response values (br1 against x2, br2 against x1),
+        summed over boards; their sum is the saddle-point gap."""
+        return self.best_response(0, x2), self.best_response(1, x1)
+
     def exploitability(self, x1, x2):
-        """exploitability (solver.hpp:325-331) for a single board."""
-        br1 = self.best_response(0, x2)
-        br2 = self.best_response(1, x1)
-        return br1, br2
+        """exploitability (solver.hpp:325-331): (br1 + br2) / 2 / pot, with the
+        chance root's 1/nboards over a multi-board engine (kr_solver_run's rule)."""
+        br1, br2 = self.best_responses(x1, x2)
+        return (br1 + br2) / 2 / self.pot / self.nboards
 
 
 def solver_for(boards, device=0, implicit=False):
