@@ -26,22 +26,32 @@
 //
 // One exact rewrite is used on the Y terms: with Y_ij ∈ {±1, ±2} (an exact
 // power-of-two scale), ((λ2·Y)·S)·x == Y·((λ2·S)·x) in IEEE arithmetic as long
-// as no product is subnormal or overflows.  The per-(j, e) product
-// Q = (λ2_j·S_e)·x[j,col_e] is then formed once per CTA and each Vᵀ term is one
-// fused Y·Q + acc (exact: Y·Q needs no rounding).  The kernels check the
-// premise per CTA (every staged x / z either 0 or within [2^-900, 2^900], every
-// λ2·S within [2^-100, 2^100]) and otherwise evaluate the literal expressions.
+// as no product is subnormal or overflows.  So Aᵀ's per-(j, e) product
+// Q = (λ2_j·S_e)·x[j,col_e] is formed once per CTA in its four signed
+// variants Y·Q, and each Vᵀ term is one load and one add; Aᵀy's V terms scale
+// the chain values the same way.  The kernels check the premise per CTA (every
+// staged x / z either 0 or within [2^-900, 2^900], every λ2·S within
+// [2^-100, 2^100]) and otherwise evaluate the literal expressions.
 //
 // Work decomposes by sequence: y[:, a] depends only on row a of F and S, and
 // Aᵀy[:, b] only on column b.  So one CTA computes one output column of one
 // board end to end — stage the input columns it needs, the Vᵀ (Uᵀ) rows of its
 // chain, the chain solve (one thread; the order is fixed), then the output rows
 // — with every intermediate in shared memory and one launch per product.
+//
+// Lists (Y rows, Y columns, blocked hands) are stored as 16-bit entries that
+// are already shared-memory byte offsets of the value they select (the signed
+// Y·Q / Y·z variant, or the {λ, value} pair of a blocked hand), in a
+// SELL-8x32 layout: rows sorted by length, cut into slices of 32, each lane's
+// entries in 16-byte vectors of 8 (one load per 8 entries, a warp's 32 vectors
+// contiguous).  Padding entries select a zero slot, so every lane of a warp
+// runs to the slice width without branches and the padding adds +0.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <string>
 #include <thread>
 #include <vector>
@@ -52,24 +62,36 @@ namespace krb {
 
 namespace {
 
-constexpr int kKfThreads = 256;
-constexpr int kKfMaxHands = 2047;   // 11-bit hand / alive-rank indices in the packed lists
+constexpr int kKfWarps = 8;         // warps (SELL slices) per row-kernel CTA
 constexpr int kKfMaxSeq = 1024;     // F / S CSR rows and columns
+constexpr int kKfMaxHands = 1364;   // list entries address up to 48 (m + 1) bytes of shared memory (< 64 KB)
+constexpr int kKfDepth = 2;
+constexpr int kKfLong = 256;
+constexpr int kKfFoldThreads = 256;  // fold kernels: staging threads (two of them then fold; 128 measured slower)       // longer list rows take the warp-cooperative path         // 16-byte list vectors in flight per lane
 
-// One list-of-lists in SELL-32 layout: entry k of row r lives at
-// ptr[r / 32] + 32 k + r % 32, so a warp's 32 rows load 64 contiguous bytes
-// per step.  Entries are 16-bit: an index (11 bits) and, for the Y lists,
-// Y + 2 in bits 11-13.
+// One list-of-lists in SELL-8x32 layout: slice s holds 32 rows (perm[32 s + l]
+// = row of lane l, -1 past the end); vector q (8 entries) of lane l is
+// ent[ptr[s] + 32 q + l]; the slice's width in vectors is (ptr[s+1]-ptr[s])/32.
 struct KfList {
-    const int32_t* ptr = nullptr;   // per slice of 32 rows
-    const int32_t* len = nullptr;   // per row
-    const uint16_t* ent = nullptr;
+    const int32_t* ptr = nullptr;
+    const int32_t* perm = nullptr;
+    const uint4* ent = nullptr;
+    int nsl = 0;
+    // rows longer than kKfLong entries (the strongest hands' Y rows: ~1,000
+    // entries against ~100 typical), kept out of the slices: row id, first
+    // vector, vector count, contiguous 16-byte vectors of 8 entries
+    int nlong = 0;
+    const int32_t* lrow = nullptr;
+    const int32_t* lptr = nullptr;
+    const uint4* lent = nullptr;
 };
 
 struct KfBoard {
     int m1, m2, n1, n2;
     int nAlive, fast;                 // fast: every λ2·S in [2^-100, 2^100] (or 0)
+    int maxSa, maxSb;                 // largest S row / S column (shared-memory layout)
     int64_t rowOff, colOff;           // y / x offsets of the board
+    int64_t zOff, zfOff;              // t / z buffer [n1][nAlive] and z_f buffer [n1] offsets
     const double *l1, *l2;
     const int32_t* aliveRows;         // [nAlive]
     const int32_t* aliveEnd;          // [nAlive]: next alive row, or m1 (Uᵀ row range)
@@ -82,15 +104,13 @@ struct KfBoard {
     const double* sval;
     const int32_t *scptr, *scrow;
     const double* scval;
-    const uint8_t* hasF;              // [n1]: F row d is a kept U/V column (fcolOf >= 0)
-    KfList yr;                        // alive r -> (j, Y) with λ2_j·Y ≠ 0, j asc   (Vᵀ rows)
-    KfList yc;                        // j -> (alive r, Y) with λ2_j·Y ≠ 0, r asc   (V rows)
-    KfList b2;                        // i -> blocked j asc                          (Â rows)
-    KfList b1;                        // j -> blocked i asc                          (Âᵀ rows)
+    const uint8_t* hasF;              // [n1]: F row d is a kept U/V column
+    KfList yr;   // A x,  alive r -> (j, Y), j asc: byte offset of QY[v(Y)][j]        (Vᵀ rows)
+    KfList b2;   // A x,  i -> blocked j asc: byte offset of the pair {λ2_j, x_j}      (Â rows)
+    KfList b1;   // Aᵀy, j -> blocked i asc: byte offset of the pair {λ1_i, y_i}     (Âᵀ rows)
+    KfList yc;   // Aᵀy, j -> (alive r, Y), r asc: byte offset of ZY[v(Y)][r]          (V rows)
+                 // (b1 and yc share one row order: an AV row is Âᵀ then V, one sum)
 };
-
-__device__ __forceinline__ int kf_idx(uint16_t e) { return int(e & 0x7FF); }
-__device__ __forceinline__ double kf_y(uint16_t e) { return double(int(e >> 11) - 2); }
 
 // staged value admissible for the Y-factoring rewrite
 __device__ __forceinline__ bool kf_ok(double v) {
@@ -98,20 +118,37 @@ __device__ __forceinline__ bool kf_ok(double v) {
     return a == 0.0 || (a >= 0x1p-900 && a <= 0x1p900);
 }
 
-// Ordered fold of n values (the sum order is fixed: one thread, one chain of
-// dependent adds); loads are issued ahead of the adds.
-__device__ __forceinline__ double kf_fold(const double* v, int n) {
-    double acc = 0.0;
-    int i = 0;
-    for (; i + 8 <= n; i += 8) {
-        double t[8];
+// Y in {-2, -1, +1, +2} is stored as the variant index v in {0, 1, 2, 3}
+__device__ __forceinline__ double kf_yval(int v) { return v < 2 ? double(v - 2) : double(v - 1); }
+
+__device__ __forceinline__ double smd(const char* smb, uint32_t off) {
+    return *reinterpret_cast<const double*>(smb + off);
+}
+__device__ __forceinline__ double2 smd2(const char* smb, uint32_t off) {
+    return *reinterpret_cast<const double2*>(smb + off);
+}
+
+// Stream one lane's vectors of a slice (kKfDepth loads in flight), calling
+// f(entry) for the 8 entries of each vector in order.
+template <class F>
+__device__ __forceinline__ void kf_stream(const uint4* __restrict__ src, int nv, F&& f) {
+    uint4 buf[kKfDepth];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = v[i + u];
+    for (int d = 0; d < kKfDepth; ++d) buf[d] = d < nv ? __ldg(src + 32 * d) : make_uint4(0, 0, 0, 0);
+    for (int q = 0; q < nv; ++q) {
+        const uint4 c = buf[0];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = acc + t[u];
+        for (int d = 0; d + 1 < kKfDepth; ++d) buf[d] = buf[d + 1];
+        buf[kKfDepth - 1] = q + kKfDepth < nv ? __ldg(src + 32 * (q + kKfDepth)) : make_uint4(0, 0, 0, 0);
+        f(c.x & 0xFFFFu);
+        f(c.x >> 16);
+        f(c.y & 0xFFFFu);
+        f(c.y >> 16);
+        f(c.z & 0xFFFFu);
+        f(c.z >> 16);
+        f(c.w & 0xFFFFu);
+        f(c.w >> 16);
     }
-    for (; i < n; ++i) acc = acc + v[i];
-    return acc;
 }
 
 // In-place chain solve with −1 multipliers: z(r) = t(r) + z(r∓1)
@@ -156,314 +193,496 @@ __device__ __forceinline__ void kf_chain(double* tz, int n) {
 }
 
 // ---------------------------------------------------------------------------
-// A x: one CTA per (player-1 sequence a, board).
-// shared: l2[m2] | xF[nFa][m2] | Q[nSa][m2] | fprod[m2 * nFa] | tz[nAlive] | zf
+// Kernels.  Per product direction: the output-row kernels (one warp per SELL
+// slice of 32 rows, all rows of a board's sequence over a few CTAs that stage
+// the columns they gather from in shared memory) and one kernel of ordered
+// folds (the chain solves and the long F rows / columns: one warp per fold).
+//   A x : k_kfa_vt (Vᵀ rows -> t) ; k_kfa_fold (chains t -> z, F rows -> z_f) ;
+//         k_kfa_ua ([U | Â] rows -> y)
+//   Aᵀy : k_kft_fold (Uᵀ rows + backward chains -> z, F columns -> z_f) ;
+//         k_kft_av ([Âᵀ | V] rows -> x)
+// t / z live in a per-board [sequence][alive rank] buffer, z_f in [sequence].
+//
+// Shared-memory layouts (bytes); list entries address the first 64 KB:
+//   k_kfa_vt : QY[maxSa][4][m2+1]  (Y·Q for Y = -2, -1, +1, +2; slot m2 = 0) | long-row buffers
+//   k_kfa_ua : PR[m2+1] {λ2_j, x[j, col(F_a,0)]} | xF[nFa-1][m2]
+//   k_kft_av : PR[m1+1] {λ1_i, y[i, row(F_b,0)]} | ZY[maxSb][4][nA+1] | yF[nFb-1][m1]
 // ---------------------------------------------------------------------------
-template <int T>
-__global__ void __launch_bounds__(T) k_kf_ax(const KfBoard* __restrict__ boards, int b0,
-                                              const double* __restrict__ x, double* __restrict__ y) {
+__host__ __device__ __forceinline__ size_t kf_vt_bytes(int m2, int maxSa, int warps) {
+    const size_t S = size_t(maxSa > 0 ? maxSa : 1);
+    return 32 * (size_t(m2) + 1) * S + 8 * 256 * S * size_t(warps);   // QY | long-row buffers
+}
+__host__ __device__ __forceinline__ size_t kf_ua_bytes(int m2, int maxFa) {
+    return 16 * (size_t(m2) + 1) + 8 * size_t(m2) * size_t(maxFa > 1 ? maxFa - 1 : 0);
+}
+__host__ __device__ __forceinline__ size_t kf_av_bytes(int m1, int nA, int maxSb, int maxFb) {
+    return 16 * (size_t(m1) + 1) + 32 * (size_t(nA) + 1) * size_t(maxSb > 0 ? maxSb : 1) +
+           8 * size_t(m1) * size_t(maxFb > 1 ? maxFb - 1 : 0);
+}
+
+// Ordered left fold of v[0..n) (DESC: v[n-1] down to v[0]) by ONE thread
+// from shared memory: acc = v + acc is the only dependency chain.  Whole
+// batches of 16 are loaded first and added without predicates, which keeps
+// the loop at the DADD latency (tools/fold_bench.cu: 9.8 cycles per element
+// against 26 for a predicated double-buffered loop).  With out != nullptr
+// the running sum after each element is stored there (the chain solves: z in
+// place of t).  Returns the final sum.
+template <bool DESC>
+__device__ __forceinline__ double kf_fold(double* v, int n, double acc, bool store) {
+    int k0 = 0;
+    for (; k0 + 16 <= n; k0 += 16) {
+        double t[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t[u] = v[DESC ? n - 1 - k0 - u : k0 + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            acc = t[u] + acc;
+            if (store) v[DESC ? n - 1 - k0 - u : k0 + u] = acc;
+        }
+    }
+    for (; k0 < n; ++k0) {
+        acc = v[DESC ? n - 1 - k0 : k0] + acc;
+        if (store) v[DESC ? n - 1 - k0 : k0] = acc;
+    }
+    return acc;
+}
+
+// ---- A x -------------------------------------------------------------------
+// One Vᵀ entry's terms added to acc in order (S entries of the row), for rows
+// with several S entries or inputs outside the rewrite's premise (literal
+// expressions of rows_vt); kept out of line so the common path stays lean.
+__device__ __noinline__ double kf_vt_add(const KfBoard& B, const char* smb, const double* xb, uint32_t off, int s0,
+                                         int nSa, int m2p, bool fast, double acc) {
+    if (fast) {
+        for (int e = 0; e < nSa; ++e) acc = acc + smd(smb, off + uint32_t(e) * 32u * uint32_t(m2p));
+        return acc;
+    }
+    const int q = int(off >> 3), v = q / m2p, j = q - v * m2p;
+    if (j >= B.m2) return acc;
+    const double scale = B.l2[j] * kf_yval(v);
+    for (int e = 0; e < nSa; ++e) acc = acc + (scale * B.sval[s0 + e]) * xb[int64_t(j) * B.n2 + B.scol[s0 + e]];
+    return acc;
+}
+// The terms of 8 entries (one vector), in order, into o[8 * nSa].
+__device__ __noinline__ void kf_vt_terms8(const KfBoard& B, const char* smb, const double* xb, uint4 c, int s0, int nSa,
+                                          int m2p, bool fast, double* o) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t off = u & 1 ? w[u >> 1] >> 16 : w[u >> 1] & 0xFFFFu;
+        if (fast) {
+            for (int e = 0; e < nSa; ++e) o[u * nSa + e] = smd(smb, off + uint32_t(e) * 32u * uint32_t(m2p));
+            continue;
+        }
+        const int q = int(off >> 3), v = q / m2p, j = q - v * m2p;
+        if (j >= B.m2) {
+            for (int e = 0; e < nSa; ++e) o[u * nSa + e] = 0.0;
+            continue;
+        }
+        const double scale = B.l2[j] * kf_yval(v);
+        for (int e = 0; e < nSa; ++e)
+            o[u * nSa + e] = (scale * B.sval[s0 + e]) * xb[int64_t(j) * B.n2 + B.scol[s0 + e]];
+    }
+}
+
+// Vᵀ rows of chain a: t(r) = Σ_j↑ Σ_e ((λ2_j·Y)·S_e)·x[j, col_e]  (rows_vt).
+// CTAs g < gs take W slices each (one warp per slice); CTA gs takes the long
+// rows, one warp per row: each round the 32 lanes load 256 entries, produce
+// their terms in order into the warp's buffer, and all lanes add them in
+// order (warp-uniform adds).
+template <int W>
+__global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __restrict__ boards, int b0, int gy, int gs,
+                                                    const double* __restrict__ x, double* __restrict__ tz) {
     pdl_entry();
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
+    const char* smb = reinterpret_cast<const char*>(sm);
     __shared__ int okAll;
-    __shared__ double zf;
     const KfBoard& B = boards[b0 + blockIdx.y];
-    const int a = blockIdx.x;
-    const int m1 = B.m1, m2 = B.m2, n1 = B.n1, n2 = B.n2;
-    const int f0 = B.fptr[a], nFa = B.fptr[a + 1] - f0;
+    const int a = blockIdx.x / gy, g = blockIdx.x - a * gy;
     const int s0 = B.sptr[a], nSa = B.sptr[a + 1] - s0;
-    const bool chain = nSa > 0 && B.nAlive > 0;
-    const bool fA = B.hasF[a] != 0;
-    double* l2s = sm;
-    double* xF = l2s + m2;
-    double* Q = xF + size_t(nFa) * m2;
-    double* fprod = Q + size_t(nSa) * m2;
-    double* tz = fprod + size_t(nFa) * m2;
+    const int nA = B.nAlive, m2 = B.m2, n2 = B.n2, m2p = m2 + 1;
+    const bool longCta = g == gs;
+    if (nSa == 0 || nA == 0 || (longCta ? B.yr.nlong == 0 : g * W >= B.yr.nsl)) return;
     const double* xb = x + B.colOff;
     if (threadIdx.x == 0) okAll = 1;
     __syncthreads();
     int ok = B.fast;
-    for (int j = threadIdx.x; j < m2; j += T) {
-        const double l2 = B.l2[j];
-        l2s[j] = l2;
-        for (int e = 0; e < nFa; ++e) {
-            const double xv = xb[int64_t(j) * n2 + B.fcol[f0 + e]];
-            xF[size_t(e) * m2 + j] = xv;
-            fprod[size_t(j) * nFa + e] = (l2 * B.fval[f0 + e]) * xv;   // Vᵀ F row term (rows_vt)
-        }
-        for (int e = 0; e < nSa; ++e) {
-            const double xv = xb[int64_t(j) * n2 + B.scol[s0 + e]];
-            ok &= kf_ok(xv);
-            Q[size_t(e) * m2 + j] = (l2 * B.sval[s0 + e]) * xv;
+    for (int e = 0; e < nSa; ++e) {
+        double* QY = sm + size_t(e) * 4 * m2p;
+        const int col = B.scol[s0 + e];
+        const double sv = B.sval[s0 + e];
+        for (int j = threadIdx.x; j < m2p; j += 32 * W) {
+            double q = 0.0;
+            if (j < m2) {
+                const double xv = xb[int64_t(j) * n2 + col];
+                ok &= kf_ok(xv);
+                q = (B.l2[j] * sv) * xv;
+            }
+            QY[j] = -2.0 * q;   // exact scalings (premise checked below)
+            QY[m2p + j] = -q;
+            QY[2 * m2p + j] = q;
+            QY[3 * m2p + j] = 2.0 * q;
         }
     }
-    if (!ok) okAll = 0;  // benign race: every writer stores 0
+    if (!ok) okAll = 0;
     __syncthreads();
     const bool fast = okAll != 0;
-    // Vᵀ rows of chain a: t(r) = Σ_j↑ Σ_e ((λ2_j·Y)·S_e)·x[j, col_e]
-    if (chain) {
-        for (int r = threadIdx.x; r < B.nAlive; r += T) {
-            const int len = B.yr.len[r];
-            const uint16_t* p = B.yr.ent + B.yr.ptr[r >> 5] + (r & 31);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (longCta) {
+        double* buf = sm + size_t(4) * m2p * size_t(B.maxSa) + size_t(warp) * 256 * size_t(B.maxSa);
+        for (int L = warp; L < B.yr.nlong; L += W) {
+            const int v0 = B.yr.lptr[L], nvec = B.yr.lptr[L + 1] - v0;
             double acc = 0.0;
-            if (fast) {
-                if (nSa == 1) {
-                    int k = 0;
-                    for (; k + 4 <= len; k += 4) {
-                        uint16_t ee[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) ee[u] = p[32 * (k + u)];
-                        double q[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) q[u] = Q[kf_idx(ee[u])];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) acc = fma(kf_y(ee[u]), q[u], acc);
-                    }
-                    for (; k < len; ++k) {
-                        const uint16_t ee = p[32 * k];
-                        acc = fma(kf_y(ee), Q[kf_idx(ee)], acc);
-                    }
-                } else {
-                    for (int k = 0; k < len; ++k) {
-                        const uint16_t ee = p[32 * k];
-                        const int j = kf_idx(ee);
-                        const double yv = kf_y(ee);
-                        for (int e = 0; e < nSa; ++e) acc = fma(yv, Q[size_t(e) * m2 + j], acc);
+            for (int q0 = 0; q0 < nvec; q0 += 32) {
+                const int cnt = min(32, nvec - q0);
+                __syncwarp();
+                if (lane < cnt) {
+                    const uint4 c = __ldg(B.yr.lent + v0 + q0 + lane);
+                    double* o = buf + size_t(lane) * 8 * nSa;
+                    if (fast && nSa == 1) {
+                        o[0] = smd(smb, c.x & 0xFFFFu);
+                        o[1] = smd(smb, c.x >> 16);
+                        o[2] = smd(smb, c.y & 0xFFFFu);
+                        o[3] = smd(smb, c.y >> 16);
+                        o[4] = smd(smb, c.z & 0xFFFFu);
+                        o[5] = smd(smb, c.z >> 16);
+                        o[6] = smd(smb, c.w & 0xFFFFu);
+                        o[7] = smd(smb, c.w >> 16);
+                    } else {
+                        kf_vt_terms8(B, smb, xb, c, s0, nSa, m2p, fast, o);
                     }
                 }
-            } else {
-                for (int k = 0; k < len; ++k) {
-                    const uint16_t ee = p[32 * k];
-                    const int j = kf_idx(ee);
-                    const double scale = l2s[j] * kf_y(ee);
-                    for (int e = 0; e < nSa; ++e) {
-                        const double v = scale * B.sval[s0 + e];
-                        acc = acc + v * xb[int64_t(j) * n2 + B.scol[s0 + e]];
-                    }
-                }
+                __syncwarp();
+                const int nt = cnt * 8 * nSa;
+                for (int k = 0; k < nt; ++k) acc = acc + buf[k];
             }
-            tz[r] = acc;
+            if (lane == 0) tz[B.zOff + int64_t(a) * nA + B.yr.lrow[L]] = acc;
+        }
+        return;
+    }
+    const int s = g * W + warp;
+    if (s >= B.yr.nsl) return;
+    const int p0 = B.yr.ptr[s], nv = (B.yr.ptr[s + 1] - p0) >> 5;
+    const int r = B.yr.perm[32 * s + lane];
+    const uint4* src = B.yr.ent + p0 + lane;
+    double acc = 0.0;
+    if (fast && nSa == 1) {
+        kf_stream(src, nv, [&](uint32_t off) { acc = acc + smd(smb, off); });
+    } else {
+        kf_stream(src, nv, [&](uint32_t off) { acc = kf_vt_add(B, smb, xb, off, s0, nSa, m2p, fast, acc); });
+    }
+    if (r >= 0) tz[B.zOff + int64_t(a) * nA + r] = acc;
+}
+
+// The ordered folds of A x for player-1 sequence a: all threads stage the
+// fold inputs in shared memory, then thread 0 runs the chain solve
+// (z(r) = t(r) + z(r-1), engine.hpp:31-41) and thread 32 the F row
+// t_f(a) = Σ_j↑ Σ_e (λ2_j·F_e)·x[j, col_e] (rows_vt), side by side.
+// shared: v[nAlive] | f[m2 · nFa]
+__global__ void __launch_bounds__(kKfFoldThreads) k_kfa_fold(const KfBoard* __restrict__ boards, int b0,
+                                                   const double* __restrict__ x, double* __restrict__ tz,
+                                                   double* __restrict__ zf) {
+    pdl_entry();
+    extern __shared__ __align__(16) double sm[];
+    const KfBoard& B = boards[b0 + blockIdx.y];
+    const int a = blockIdx.x;
+    const int nA = B.nAlive, m2 = B.m2, n2 = B.n2;
+    const bool chain = B.sptr[a + 1] > B.sptr[a] && nA > 0;
+    const bool fA = B.hasF[a] != 0;
+    if (!chain && !fA) return;
+    const int f0 = B.fptr[a], nFa = B.fptr[a + 1] - f0;
+    double* v = sm;
+    double* f = sm + nA;
+    double* t = tz + B.zOff + int64_t(a) * nA;
+    const double* xb = x + B.colOff;
+    if (chain)
+        for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) v[r] = t[r];
+    if (fA)
+        for (int k = threadIdx.x; k < m2 * nFa; k += kKfFoldThreads) {
+            const int j = nFa == 1 ? k : k / nFa, e = k - j * nFa;
+            f[k] = (B.l2[j] * B.fval[f0 + e]) * xb[int64_t(j) * n2 + B.fcol[f0 + e]];
+        }
+    __syncthreads();
+    if (threadIdx.x == 0 && chain) kf_fold<false>(v, nA, -0.0, true);
+    if (threadIdx.x == 32 && fA) zf[B.zfOff + a] = kf_fold<false>(f, m2 * nFa, 0.0, false);
+    __syncthreads();
+    if (chain)
+        for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) t[r] = v[r];
+}
+
+// [U | Â] rows (i, a): λ1_i·z(prev alive(i), a) + λ1_i·z_f(a), then the
+// blocked hands j ascending: ((−λ1_i)·λ2_j·F_e)·x[j, col_e]  (rows_ua)
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_kfa_ua(const KfBoard* __restrict__ boards, int b0, int gu,
+                                                    const double* __restrict__ x, const double* __restrict__ tz,
+                                                    const double* __restrict__ zf, double* __restrict__ y) {
+    pdl_entry();
+    extern __shared__ __align__(16) double sm[];
+    const char* smb = reinterpret_cast<const char*>(sm);
+    const KfBoard& B = boards[b0 + blockIdx.y];
+    const int a = blockIdx.x / gu, g = blockIdx.x - a * gu;
+    if (g * W >= B.b2.nsl) return;
+    const int m2 = B.m2, n1 = B.n1, n2 = B.n2, nA = B.nAlive;
+    const int f0 = B.fptr[a], nFa = B.fptr[a + 1] - f0;
+    double2* PR = reinterpret_cast<double2*>(sm);
+    double* xF1 = sm + 2 * (m2 + 1);
+    if (nFa > 0) {
+        const double* xb = x + B.colOff;
+        for (int j = threadIdx.x; j <= m2; j += 32 * W) {
+            if (j == m2) {
+                PR[m2] = make_double2(0.0, 0.0);
+                continue;
+            }
+            PR[j] = make_double2(B.l2[j], xb[int64_t(j) * n2 + B.fcol[f0]]);
+            for (int e = 1; e < nFa; ++e) xF1[size_t(e - 1) * m2 + j] = xb[int64_t(j) * n2 + B.fcol[f0 + e]];
+        }
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, s = g * W + (threadIdx.x >> 5);
+    if (s >= B.b2.nsl) return;
+    const int i = B.b2.perm[32 * s + lane];
+    const bool chain = B.sptr[a + 1] > B.sptr[a] && nA > 0;
+    const double v = i >= 0 ? B.l1[i] : 0.0;
+    double acc = 0.0;
+    if (i >= 0 && v != 0.0) {
+        const int rp = B.rankPrev[i];
+        if (chain && rp >= 0) acc = acc + v * tz[B.zOff + int64_t(a) * nA + rp];
+        if (B.hasF[a]) acc = acc + v * zf[B.zfOff + a];
+    }
+    if (nFa > 0) {
+        const int p0 = B.b2.ptr[s], nv = (B.b2.ptr[s + 1] - p0) >> 5;
+        const uint4* src = B.b2.ent + p0 + lane;
+        const double nv1 = -v;
+        if (nFa == 1) {
+            const double fv = B.fval[f0];
+            kf_stream(src, nv, [&](uint32_t off) {
+                const double2 p = smd2(smb, off);
+                const double w = (nv1 * p.x) * fv;
+                acc = acc + w * p.y;
+            });
+        } else {
+            kf_stream(src, nv, [&](uint32_t off) {
+                const int j = int(off >> 4);
+                if (j >= m2) return;
+                const double scale = nv1 * PR[j].x;
+                for (int e = 0; e < nFa; ++e) {
+                    const double w = scale * B.fval[f0 + e];
+                    acc = acc + w * (e == 0 ? PR[j].y : xF1[size_t(e - 1) * m2 + j]);
+                }
+            });
         }
     }
-    __syncthreads();
-    // the two ordered folds: the chain solve (warp 0) and the F row (warp 1)
-    if (threadIdx.x == 0 && chain) kf_chain<1>(tz, B.nAlive);
-    if (threadIdx.x == 32 && fA) zf = kf_fold(fprod, m2 * nFa);
-    __syncthreads();
-    // [U | Â] rows (i, a): U terms, then the blocked hands in order
-    const double zfa = fA ? zf : 0.0;
-    double* yb = y + B.rowOff;
-    for (int i = threadIdx.x; i < m1; i += T) {
-        const double v = B.l1[i];
-        double acc = 0.0;
-        if (v != 0.0) {
-            const int rp = B.rankPrev[i];
-            if (chain && rp >= 0) acc = acc + v * tz[rp];
-            if (fA) acc = acc + v * zfa;
+    if (i >= 0) y[B.rowOff + int64_t(i) * n1 + a] = acc;
+}
+
+// ---- Aᵀ y ------------------------------------------------------------------
+// The ordered folds of Aᵀy for player-1 sequence d: all threads compute the
+// Uᵀ rows of chain d, s(r) = Σ_{i ∈ [alive r, alive r+1)} λ1_i·y[i, d], and
+// the F-column terms λ1_i·y[i, d] (rows_ut) into shared memory; thread 0 then
+// solves the chain backward (z(r) = s(r) + z(r+1), engine.hpp:44-54) and
+// thread 32 folds the F column Σ_i↑, side by side.
+// shared: v[nAlive] | f[m1]
+__global__ void __launch_bounds__(kKfFoldThreads) k_kft_fold(const KfBoard* __restrict__ boards, int b0,
+                                                   const double* __restrict__ y, double* __restrict__ tz,
+                                                   double* __restrict__ zf) {
+    pdl_entry();
+    extern __shared__ __align__(16) double sm[];
+    const KfBoard& B = boards[b0 + blockIdx.y];
+    const int d = blockIdx.x;
+    const int nA = B.nAlive, m1 = B.m1, n1 = B.n1;
+    const bool chain = B.sptr[d + 1] > B.sptr[d] && nA > 0;
+    const bool fD = B.hasF[d] != 0;
+    if (!chain && !fD) return;
+    const double* yb = y + B.rowOff;
+    double* v = sm;
+    double* f = sm + nA;
+    if (chain)
+        for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) {
+            double acc = 0.0;
+            for (int i = B.aliveRows[r]; i < B.aliveEnd[r]; ++i) acc = acc + B.l1[i] * yb[int64_t(i) * n1 + d];
+            v[r] = acc;
         }
-        if (nFa > 0) {
-            const int len = B.b2.len[i];
-            const uint16_t* p = B.b2.ent + B.b2.ptr[i >> 5] + (i & 31);
-            const double nv = -v;
-            if (nFa == 1) {
-                const double fv = B.fval[f0];
-                int k = 0;
-                for (; k + 4 <= len; k += 4) {
-                    int jj[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) jj[u] = kf_idx(p[32 * (k + u)]);
-                    double l[4], xv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        l[u] = l2s[jj[u]];
-                        xv[u] = xF[jj[u]];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const double w = (nv * l[u]) * fv;
-                        acc = acc + w * xv[u];
-                    }
-                }
-                for (; k < len; ++k) {
-                    const int j = kf_idx(p[32 * k]);
-                    const double w = (nv * l2s[j]) * fv;
-                    acc = acc + w * xF[j];
-                }
-            } else {
-                for (int k = 0; k < len; ++k) {
-                    const int j = kf_idx(p[32 * k]);
-                    const double scale = nv * l2s[j];
-                    for (int e = 0; e < nFa; ++e) {
-                        const double w = scale * B.fval[f0 + e];
-                        acc = acc + w * xF[size_t(e) * m2 + j];
-                    }
-                }
-            }
-        }
-        yb[int64_t(i) * n1 + a] = acc;
+    if (fD)
+        for (int i = threadIdx.x; i < m1; i += kKfFoldThreads) f[i] = B.l1[i] * yb[int64_t(i) * n1 + d];
+    __syncthreads();
+    if (threadIdx.x == 0 && chain) kf_fold<true>(v, nA, -0.0, true);
+    if (threadIdx.x == 32 && fD) zf[B.zfOff + d] = kf_fold<false>(f, m1, 0.0, false);
+    __syncthreads();
+    if (chain) {
+        double* z = tz + B.zOff + int64_t(d) * nA;
+        for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) z[r] = v[r];
     }
 }
 
-// ---------------------------------------------------------------------------
-// Aᵀ y: one CTA per (player-2 sequence b, board).
-// shared: l1[m1] | yF[nFb][m1] | fprod[nFb][m1] | sz[nSb][nAlive] | yS[nSb][m1] | zf[nFb]
-// ---------------------------------------------------------------------------
-template <int T>
-__global__ void __launch_bounds__(T) k_kf_atx(const KfBoard* __restrict__ boards, int b0,
-                                               const double* __restrict__ y, double* __restrict__ x) {
+// [Âᵀ | V] rows (j, b): the blocked hands i ascending, ((−λ1_i)·λ2_j·F_e)·y[i, row_e];
+// then V: alive r ascending, ((λ2_j·Y)·S_e)·z(r, row_e); then λ2_j·F_e·z_f  (rows_av)
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ boards, int b0, int gv,
+                                                    const double* __restrict__ y, const double* __restrict__ tz,
+                                                    const double* __restrict__ zf, double* __restrict__ x) {
     pdl_entry();
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
+    const char* smb = reinterpret_cast<const char*>(sm);
     __shared__ int okAll;
     const KfBoard& B = boards[b0 + blockIdx.y];
-    const int b = blockIdx.x;
-    const int m1 = B.m1, m2 = B.m2, n1 = B.n1, n2 = B.n2;
+    const int b = blockIdx.x / gv, g = blockIdx.x - b * gv;
+    if (g * W >= B.b1.nsl) return;
+    const int m1 = B.m1, n1 = B.n1, n2 = B.n2, nA = B.nAlive;
+    const int m1p = m1 + 1, nAp = nA + 1;
     const int f0 = B.fcptr[b], nFb = B.fcptr[b + 1] - f0;
     const int s0 = B.scptr[b], nSb = B.scptr[b + 1] - s0;
-    const int nA = B.nAlive;
-    double* l1s = sm;
-    double* yF = l1s + m1;
-    double* fprod = yF + size_t(nFb) * m1;
-    double* sz = fprod + size_t(nFb) * m1;
-    double* yS = sz + size_t(nSb) * nA;
-    double* zf = yS + size_t(nSb) * m1;
+    double2* PR = reinterpret_cast<double2*>(sm);
+    double* ZY = sm + 2 * m1p;                                   // [maxSb][4][nAp]
+    double* yF1 = ZY + size_t(4) * nAp * (B.maxSb > 0 ? B.maxSb : 1);
     const double* yb = y + B.rowOff;
     if (threadIdx.x == 0) okAll = 1;
-    for (int i = threadIdx.x; i < m1; i += T) {
-        const double l1 = B.l1[i];
-        l1s[i] = l1;
-        for (int e = 0; e < nFb; ++e) {
-            const double yv = yb[int64_t(i) * n1 + B.fcrow[f0 + e]];
-            yF[size_t(e) * m1 + i] = yv;
-            fprod[size_t(e) * m1 + i] = l1 * yv;   // Uᵀ F-column row terms (rows_ut)
-        }
-        for (int e = 0; e < nSb; ++e) yS[size_t(e) * m1 + i] = yb[int64_t(i) * n1 + B.scrow[s0 + e]];
-    }
     __syncthreads();
-    // Uᵀ rows of each chain d ∈ S column b: s(r) = Σ_{i ∈ [alive r, alive r+1)} λ1_i·y[i, d]
-    int ok = 1;
-    for (int e = 0; e < nSb; ++e)
-        for (int r = threadIdx.x; r < nA; r += T) {
-            double acc = 0.0;
-            for (int i = B.aliveRows[r]; i < B.aliveEnd[r]; ++i) acc = acc + l1s[i] * yS[size_t(e) * m1 + i];
-            sz[size_t(e) * nA + r] = acc;
-        }
-    __syncthreads();
-    {   // ordered folds: the backward chains, then the F-column sums
-        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int task = w; task < nSb + nFb; task += T / 32)
-            if (lane == 0) {
-                if (task < nSb) kf_chain<-1>(sz + size_t(task) * nA, nA);
-                else if (B.hasF[B.fcrow[f0 + task - nSb]]) zf[task - nSb] = kf_fold(fprod + size_t(task - nSb) * m1, m1);
+    if (nFb > 0)
+        for (int i = threadIdx.x; i <= m1; i += 32 * W) {
+            if (i == m1) {
+                PR[m1] = make_double2(0.0, 0.0);
+                continue;
             }
-    }
-    __syncthreads();
-    for (int e = 0; e < nSb; ++e)
-        for (int r = threadIdx.x; r < nA; r += T) ok &= kf_ok(sz[size_t(e) * nA + r]);
+            PR[i] = make_double2(B.l1[i], yb[int64_t(i) * n1 + B.fcrow[f0]]);
+            for (int e = 1; e < nFb; ++e) yF1[size_t(e - 1) * m1 + i] = yb[int64_t(i) * n1 + B.fcrow[f0 + e]];
+        }
+    int ok = B.fast;
+    if (nA > 0)
+        for (int e = 0; e < nSb; ++e) {
+            const double* z = tz + B.zOff + int64_t(B.scrow[s0 + e]) * nA;
+            double* Z = ZY + size_t(e) * 4 * nAp;
+            for (int r = threadIdx.x; r < nAp; r += 32 * W) {
+                const double v = r < nA ? z[r] : 0.0;
+                ok &= kf_ok(v);
+                Z[r] = -2.0 * v;
+                Z[nAp + r] = -v;
+                Z[2 * nAp + r] = v;
+                Z[3 * nAp + r] = 2.0 * v;
+            }
+        }
     if (!ok) okAll = 0;
     __syncthreads();
-    const bool zok = okAll != 0 && B.fast;
-    double* xb = x + B.colOff;
-    for (int j = threadIdx.x; j < m2; j += T) {
-        const double l2 = B.l2[j];
-        double acc = 0.0;
-        if (nFb > 0) {   // Âᵀ: blocked i ascending, F column b
-            const int len = B.b1.len[j];
-            const uint16_t* p = B.b1.ent + B.b1.ptr[j >> 5] + (j & 31);
-            if (nFb == 1) {
-                const double fv = B.fcval[f0];
-                int k = 0;
-                for (; k + 4 <= len; k += 4) {
-                    int ii[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) ii[u] = kf_idx(p[32 * (k + u)]);
-                    double l[4], yv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        l[u] = l1s[ii[u]];
-                        yv[u] = yF[ii[u]];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const double w = (-l[u] * l2) * fv;
-                        acc = acc + w * yv[u];
-                    }
+    const int lane = threadIdx.x & 31, s = g * W + (threadIdx.x >> 5);
+    if (s >= B.b1.nsl) return;
+    const int j = B.b1.perm[32 * s + lane];
+    const double l2 = j >= 0 ? B.l2[j] : 0.0;
+    double acc = 0.0;
+    if (nFb > 0) {   // Âᵀ
+        const int p0 = B.b1.ptr[s], nv = (B.b1.ptr[s + 1] - p0) >> 5;
+        const uint4* src = B.b1.ent + p0 + lane;
+        if (nFb == 1) {
+            const double fv = B.fcval[f0];
+            kf_stream(src, nv, [&](uint32_t off) {
+                const double2 p = smd2(smb, off);
+                const double w = (-p.x * l2) * fv;
+                acc = acc + w * p.y;
+            });
+        } else {
+            kf_stream(src, nv, [&](uint32_t off) {
+                const int i = int(off >> 4);
+                if (i >= m1) return;
+                const double scale = -PR[i].x * l2;
+                for (int e = 0; e < nFb; ++e) {
+                    const double w = scale * B.fcval[f0 + e];
+                    acc = acc + w * (e == 0 ? PR[i].y : yF1[size_t(e - 1) * m1 + i]);
                 }
-                for (; k < len; ++k) {
-                    const int i = kf_idx(p[32 * k]);
-                    const double w = (-l1s[i] * l2) * fv;
-                    acc = acc + w * yF[i];
-                }
-            } else {
-                for (int k = 0; k < len; ++k) {
-                    const int i = kf_idx(p[32 * k]);
-                    const double scale = -l1s[i] * l2;
-                    for (int e = 0; e < nFb; ++e) {
-                        const double w = scale * B.fcval[f0 + e];
-                        acc = acc + w * yF[size_t(e) * m1 + i];
-                    }
-                }
-            }
+            });
         }
-        if (nSb > 0 && nA > 0) {   // V, S columns: alive r ascending, S column b
-            const int len = B.yc.len[j];
-            const uint16_t* p = B.yc.ent + B.yc.ptr[j >> 5] + (j & 31);
-            if (zok && nSb == 1) {
-                const double P = l2 * B.scval[s0];
-                int k = 0;
-                for (; k + 4 <= len; k += 4) {
-                    uint16_t ee[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) ee[u] = p[32 * (k + u)];
-                    double z[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) z[u] = sz[kf_idx(ee[u])];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc = fma(kf_y(ee[u]), P * z[u], acc);
+    }
+    if (nSb > 0 && nA > 0) {   // V, S columns
+        const int p0 = B.yc.ptr[s], nv = (B.yc.ptr[s + 1] - p0) >> 5;
+        const uint4* src = B.yc.ent + p0 + lane;
+        if (okAll && nSb == 1) {
+            // ((λ2·Y)·S)·z == (λ2·S)·(Y·z): one multiply, one add
+            const double P0 = l2 * B.scval[s0];
+            kf_stream(src, nv, [&](uint32_t off) { acc = acc + P0 * smd(smb, off); });
+        } else if (okAll) {
+            kf_stream(src, nv, [&](uint32_t off) {
+                for (int e = 0; e < nSb; ++e)
+                    acc = acc + (l2 * B.scval[s0 + e]) * smd(smb, off + uint32_t(e) * 32u * uint32_t(nAp));
+            });
+        } else {
+            kf_stream(src, nv, [&](uint32_t off) {
+                const int q = int(off >> 3) - 2 * m1p, v = q / nAp, r = q - v * nAp;
+                if (r >= nA) return;
+                const double scale = l2 * kf_yval(v);
+                for (int e = 0; e < nSb; ++e) {
+                    const double w = scale * B.scval[s0 + e];
+                    acc = acc + w * tz[B.zOff + int64_t(B.scrow[s0 + e]) * nA + r];
                 }
-                for (; k < len; ++k) {
-                    const uint16_t ee = p[32 * k];
-                    acc = fma(kf_y(ee), P * sz[kf_idx(ee)], acc);
-                }
-            } else {
-                for (int k = 0; k < len; ++k) {
-                    const uint16_t ee = p[32 * k];
-                    const int r = kf_idx(ee);
-                    const double scale = l2 * kf_y(ee);
-                    for (int e = 0; e < nSb; ++e) {
-                        const double w = scale * B.scval[s0 + e];
-                        acc = acc + w * sz[size_t(e) * nA + r];
-                    }
-                }
-            }
+            });
         }
+    }
+    if (j >= 0) {
         if (l2 != 0.0)   // V, F columns
-            for (int e = 0; e < nFb; ++e)
-                if (B.hasF[B.fcrow[f0 + e]]) acc = acc + (l2 * B.fcval[f0 + e]) * zf[e];
-        xb[int64_t(j) * n2 + b] = acc;
+            for (int e = 0; e < nFb; ++e) {
+                const int d = B.fcrow[f0 + e];
+                if (B.hasF[d]) acc = acc + (l2 * B.fcval[f0 + e]) * zf[B.zfOff + d];
+            }
+        x[B.colOff + int64_t(j) * n2 + b] = acc;
     }
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// SELL-8x32 list (KfList) on the host: rows in `order` (or by length,
+// longest first), slices of 32, each slice padded to a multiple of 8 entries
+// with `pad`.
+// SELL-8x32 list (KfList) on the host: rows in `order` (or by length,
+// longest first), slices of 32, each slice padded to a multiple of 8 entries
+// with `pad`; with longCut > 0, rows longer than longCut go to the long-row
+// list instead (contiguous, padded to whole vectors).
 struct HostList {
-    std::vector<int32_t> ptr, len;
-    std::vector<uint16_t> ent;
-    void build(const std::vector<std::vector<uint16_t>>& rows) {
+    std::vector<int32_t> ptr, perm, lrow, lptr;
+    std::vector<uint16_t> ent, lent;   // 8 per uint4
+    int nsl = 0;
+    void build(const std::vector<std::vector<uint16_t>>& rows, uint16_t pad, const std::vector<int32_t>* order,
+               size_t longCut = 0) {
         const int R = int(rows.size());
-        const int S = (R + 31) / 32;
-        ptr.assign(size_t(S) + 1, 0);
-        len.assign(size_t(R), 0);
-        for (int s = 0; s < S; ++s) {
-            int w = 0;
-            for (int l = 0; l < 32 && 32 * s + l < R; ++l) w = std::max<int>(w, int(rows[size_t(32 * s + l)].size()));
-            ptr[size_t(s) + 1] = ptr[size_t(s)] + 32 * w;
+        std::vector<int32_t> ord;
+        if (order) {
+            ord = *order;
+        } else {
+            ord.resize(size_t(R));
+            std::iota(ord.begin(), ord.end(), 0);
+            std::stable_sort(ord.begin(), ord.end(),
+                             [&](int32_t u, int32_t v) { return rows[size_t(u)].size() > rows[size_t(v)].size(); });
         }
-        ent.assign(size_t(std::max(ptr.back(), 1)), 0);
-        for (int r = 0; r < R; ++r) {
-            len[size_t(r)] = int32_t(rows[size_t(r)].size());
-            for (size_t k = 0; k < rows[size_t(r)].size(); ++k)
-                ent[size_t(ptr[size_t(r / 32)]) + 32 * k + size_t(r % 32)] = rows[size_t(r)][k];
+        std::vector<int32_t> kept;
+        lptr.assign(1, 0);
+        for (int32_t r : ord) {
+            if (longCut > 0 && rows[size_t(r)].size() > longCut) {
+                lrow.push_back(r);
+                const size_t nv = (rows[size_t(r)].size() + 7) / 8;
+                lptr.push_back(lptr.back() + int32_t(nv));
+                for (size_t k = 0; k < nv * 8; ++k) lent.push_back(k < rows[size_t(r)].size() ? rows[size_t(r)][k] : pad);
+            } else {
+                kept.push_back(r);
+            }
         }
+        if (lent.empty()) lent.assign(8, pad);
+        const int K = int(kept.size());
+        nsl = (K + 31) / 32;
+        perm.assign(size_t(std::max(nsl, 1)) * 32, -1);
+        for (int q = 0; q < K; ++q) perm[size_t(q)] = kept[size_t(q)];
+        ptr.assign(size_t(nsl) + 1, 0);
+        for (int sl = 0; sl < nsl; ++sl) {
+            size_t w = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int r = perm[size_t(32 * sl + l)];
+                if (r >= 0) w = std::max(w, rows[size_t(r)].size());
+            }
+            ptr[size_t(sl) + 1] = ptr[size_t(sl)] + int32_t(32 * ((w + 7) / 8));
+        }
+        ent.assign(size_t(std::max(ptr.back(), 1)) * 8, pad);
+        for (int sl = 0; sl < nsl; ++sl)
+            for (int l = 0; l < 32; ++l) {
+                const int r = perm[size_t(32 * sl + l)];
+                if (r < 0) continue;
+                const auto& row = rows[size_t(r)];
+                for (size_t k = 0; k < row.size(); ++k)
+                    ent[(size_t(ptr[size_t(sl)]) + 32 * (k / 8) + size_t(l)) * 8 + k % 8] = row[k];
+            }
     }
 };
 
@@ -515,13 +734,15 @@ void csr_copy(const kr_compressed& A, int rows, int cols, const char* name, int 
 }
 
 // Technique B post in Kronecker form for one board (the closed form the
-// device enumerators of kr_devengine.cu follow; sparsify.hpp:246-406).
+// device enumerators of kr_devengine.cu follow; sparsify.hpp:246-406).  List
+// entries are the kernels' shared-memory byte offsets (kf_ax_bytes /
+// kf_atx_bytes layouts), so they depend on m1, m2 and the alive count.
 void build_host_board(const kr_kron_board& K, int b, HostBoard& H) {
     const std::string at = "board " + std::to_string(b) + ": ";
     const int m1 = K.m1, m2 = K.m2, n1 = K.n1, n2 = K.n2;
     if (m1 < 1 || m2 < 1 || n1 < 1 || n2 < 1) throw Fail{KR_INVALID_INPUT, at + "empty board"};
     if (m1 > kKfMaxHands || m2 > kKfMaxHands)
-        throw Fail{KR_INVALID_INPUT, at + "more than 2047 hands per side (use the factored engine)"};
+        throw Fail{KR_INVALID_INPUT, at + "more than 1364 hands per side (use the factored engine)"};
     if (n1 > kKfMaxSeq || n2 > kKfMaxSeq) throw Fail{KR_INVALID_INPUT, at + "tree too large"};
     if (!K.key1 || !K.key2 || !K.cards1 || !K.cards2 || !K.lambda1 || !K.lambda2)
         throw Fail{KR_INVALID_INPUT, at + "null hand arrays"};
@@ -582,11 +803,14 @@ void build_host_board(const kr_kron_board& K, int b, HostBoard& H) {
     }
     H.aliveEnd.resize(size_t(H.nAlive));
     for (int r = 0; r < H.nAlive; ++r) H.aliveEnd[size_t(r)] = r + 1 < H.nAlive ? H.aliveRows[size_t(r) + 1] : m1;
-    std::vector<std::vector<uint16_t>> yr(static_cast<size_t>(H.nAlive)), yc(static_cast<size_t>(m2));
-    for (int r = 0; r < H.nAlive; ++r) {
-        yr[size_t(r)] = yrows[size_t(H.aliveRows[size_t(r)])];
-        for (uint16_t e : yr[size_t(r)]) yc[size_t(e & 0x7FF)].push_back(uint16_t(r | (e & 0x3800)));
-    }
+    // Y rows (alive r -> j) and columns (j -> alive r), as (index, Y)
+    std::vector<std::vector<std::pair<uint16_t, int8_t>>> yrl(static_cast<size_t>(H.nAlive)), ycl(static_cast<size_t>(m2));
+    for (int r = 0; r < H.nAlive; ++r)
+        for (uint16_t e : yrows[size_t(H.aliveRows[size_t(r)])]) {
+            const int j = e & 0x7FF, yd = int(e >> 11) - 2;
+            yrl[size_t(r)].push_back({uint16_t(j), int8_t(yd)});
+            ycl[size_t(j)].push_back({uint16_t(r), int8_t(yd)});
+        }
     // chains and F columns (kr_devengine.cu pass 0)
     bool anyL2 = false;
     for (double v : H.l2) anyL2 |= v != 0.0;
@@ -600,16 +824,37 @@ void build_host_board(const kr_kron_board& K, int b, HostBoard& H) {
     }
     // blocked lists (H× = 1 - compat)
     std::vector<std::vector<uint16_t>> b2(static_cast<size_t>(m1)), b1(static_cast<size_t>(m2));
+    std::vector<std::vector<int>> b2i(static_cast<size_t>(m1));
     for (int i = 0; i < m1; ++i)
         for (int j = 0; j < m2; ++j)
-            if (!compat(i, j)) {
-                b2[size_t(i)].push_back(uint16_t(j));
-                b1[size_t(j)].push_back(uint16_t(i));
-            }
-    H.yr.build(yr);
-    H.yc.build(yc);
-    H.b2.build(b2);
-    H.b1.build(b1);
+            if (!compat(i, j)) b2i[size_t(i)].push_back(j);
+    // byte offsets into the kernels' shared memory (see kf_ax_bytes / kf_atx_bytes)
+    const int m1p = m1 + 1, m2p = m2 + 1, nAp = H.nAlive + 1;
+    auto vidx = [](int yd) { return yd < 0 ? yd + 2 : yd + 1; };   // Y -> variant 0..3
+    {
+        std::vector<std::vector<uint16_t>> rows(static_cast<size_t>(H.nAlive));
+        for (int r = 0; r < H.nAlive; ++r)
+            for (auto [j, yd] : yrl[size_t(r)]) rows[size_t(r)].push_back(uint16_t((vidx(yd) * m2p + j) * 8));
+        H.yr.build(rows, uint16_t((2 * m2p + m2) * 8), nullptr, kKfLong);
+        for (int i = 0; i < m1; ++i)
+            for (int j : b2i[size_t(i)]) b2[size_t(i)].push_back(uint16_t(16 * j));
+        H.b2.build(b2, uint16_t(16 * m2), nullptr);
+    }
+    {
+        std::vector<std::vector<uint16_t>> yc(static_cast<size_t>(m2));
+        for (int i = 0; i < m1; ++i)
+            for (int j : b2i[size_t(i)]) b1[size_t(j)].push_back(uint16_t(16 * i));
+        for (int j = 0; j < m2; ++j)
+            for (auto [r, yd] : ycl[size_t(j)]) yc[size_t(j)].push_back(uint16_t(16 * m1p + (vidx(yd) * nAp + r) * 8));
+        // one row order for both (an AV row is its Âᵀ part then its V part)
+        std::vector<int32_t> ord(static_cast<size_t>(m2));
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t u, int32_t v) {
+            return b1[size_t(u)].size() + yc[size_t(u)].size() > b1[size_t(v)].size() + yc[size_t(v)].size();
+        });
+        H.b1.build(b1, uint16_t(16 * m1), &ord);
+        H.yc.build(yc, uint16_t(16 * m1p + (2 * nAp + H.nAlive) * 8), &ord);
+    }
     // the products' fast path premise: every λ2·S in [2^-100, 2^100] or 0
     for (int j = 0; j < m2; ++j)
         for (double s : H.sval) {
@@ -627,8 +872,8 @@ void build_host_board(const kr_kron_board& K, int b, HostBoard& H) {
         H.maxSb = std::max(H.maxSb, H.scptr[size_t(c) + 1] - H.scptr[size_t(c)]);
     }
     for (int r = 0; r < H.nAlive; ++r)
-        for (uint16_t e : yr[size_t(r)]) {
-            const double scale = H.l2[size_t(e & 0x7FF)] * double(int(e >> 11) - 2);
+        for (auto [j, yd] : yrl[size_t(r)]) {
+            const double scale = H.l2[size_t(j)] * double(yd);
             for (int d = 0; d < n1; ++d)
                 for (int q = H.sptr[size_t(d)]; q < H.sptr[size_t(d) + 1]; ++q) H.nnzV += scale * H.sval[size_t(q)] != 0.0;
         }
@@ -644,7 +889,7 @@ void build_host_board(const kr_kron_board& K, int b, HostBoard& H) {
                 H.nnzU += (H.sptr[size_t(a) + 1] > H.sptr[size_t(a)] && H.rankPrev[size_t(i)] >= 0) ? 1 : 0;
                 H.nnzU += H.hasF[size_t(a)] ? 1 : 0;
             }
-            for (uint16_t j : b2[size_t(i)]) {
+            for (int j : b2i[size_t(i)]) {
                 const double scale = -v * H.l2[size_t(j)];
                 for (int q = H.fptr[size_t(a)]; q < H.fptr[size_t(a) + 1]; ++q) H.nnzA += scale * H.fval[size_t(q)] != 0.0;
             }
@@ -665,8 +910,19 @@ T* up(std::vector<void*>& keep, const std::vector<T>& v) {
 KfList up_list(std::vector<void*>& keep, const HostList& h) {
     KfList l;
     l.ptr = up(keep, h.ptr);
-    l.len = up(keep, h.len);
-    l.ent = up(keep, h.ent);
+    l.perm = up(keep, h.perm);
+    uint4* e = dev_alloc<uint4>(int64_t(h.ent.size() / 8));
+    keep.push_back(e);
+    KR_CK(cudaMemcpy(e, h.ent.data(), 2 * h.ent.size(), cudaMemcpyHostToDevice));
+    l.ent = e;
+    l.nsl = h.nsl;
+    l.nlong = int(h.lrow.size());
+    l.lrow = up(keep, h.lrow);
+    l.lptr = up(keep, h.lptr);
+    uint4* le = dev_alloc<uint4>(int64_t(h.lent.size() / 8));
+    keep.push_back(le);
+    KR_CK(cudaMemcpy(le, h.lent.data(), 2 * h.lent.size(), cudaMemcpyHostToDevice));
+    l.lent = le;
     return l;
 }
 
@@ -675,8 +931,11 @@ KfList up_list(std::vector<void*>& keep, const HostList& h) {
 struct KfState {
     KfBoard* dBoards = nullptr;    // device array
     std::vector<void*> keep;       // every device table
-    size_t smem[2] = {0, 0};
-    int nb = 0, nSeq[2] = {0, 0};
+    size_t smVT = 0, smUA = 0, smAV = 0, smFA = 0, smFT = 0;
+    int nb = 0, n1 = 0, n2 = 0;
+    int gy = 1, gs = 0, gu = 1, gv = 1;    // row-kernel CTAs per sequence (gs: slice CTAs of the Vᵀ rows)
+    double* tz[2] = {nullptr, nullptr};   // t / z per direction (A x, Aᵀy may run concurrently)
+    double* zf[2] = {nullptr, nullptr};
 };
 
 void kf_destroy(KfState* k) {
@@ -685,17 +944,32 @@ void kf_destroy(KfState* k) {
     delete k;
 }
 
+// Boards [b0, b1) of one product: A x = Vᵀ rows, folds, [U|Â] rows;
+// Aᵀy = folds (Uᵀ rows and chains), [Âᵀ|V] rows.
 void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
     KfState* k = e->kf;
     if (b1 < 0) b1 = k->nb;
-    if (b1 <= b0 || k->nSeq[dir] == 0) return;
-    const dim3 grid(unsigned(k->nSeq[dir]), unsigned(b1 - b0));
-    if (dir == 0)
-        krb::launch(k_kf_ax<kKfThreads>, grid, kKfThreads, k->smem[0], s, k->dBoards, b0, in, out);
-    else
-        krb::launch(k_kf_atx<kKfThreads>, grid, kKfThreads, k->smem[1], s, k->dBoards, b0, in, out);
-    KR_CK_LAUNCH();
-    e->launches++;
+    if (b1 <= b0) return;
+    const unsigned nb = unsigned(b1 - b0);
+    constexpr int T = 32 * kKfWarps;
+    if (dir == 0) {
+        krb::launch(k_kfa_vt<kKfWarps>, dim3(unsigned(k->n1 * k->gy), nb), T, k->smVT, s, k->dBoards, b0, k->gy, k->gs,
+                    in, k->tz[0]);
+        KR_CK_LAUNCH();
+        krb::launch(k_kfa_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFA, s, k->dBoards, b0, in, k->tz[0], k->zf[0]);
+        KR_CK_LAUNCH();
+        krb::launch(k_kfa_ua<kKfWarps>, dim3(unsigned(k->n1 * k->gu), nb), T, k->smUA, s, k->dBoards, b0, k->gu, in,
+                    k->tz[0], k->zf[0], out);
+        KR_CK_LAUNCH();
+        e->launches += 3;
+    } else {
+        krb::launch(k_kft_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFT, s, k->dBoards, b0, in, k->tz[1], k->zf[1]);
+        KR_CK_LAUNCH();
+        krb::launch(k_kft_av<kKfWarps>, dim3(unsigned(k->n2 * k->gv), nb), T, k->smAV, s, k->dBoards, b0, k->gv, in,
+                    k->tz[1], k->zf[1], out);
+        KR_CK_LAUNCH();
+        e->launches += 2;
+    }
 }
 
 kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uint32_t flags) {
@@ -749,11 +1023,12 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
         e->kf = new KfState();
         KfState& k = *e->kf;
         k.nb = nb;
-        k.nSeq[0] = n1;
-        k.nSeq[1] = n2;
+        k.n1 = n1;
+        k.n2 = n2;
         std::vector<KfBoard> db(static_cast<size_t>(nb));
-        int64_t rowOff = 0, colOff = 0, K = 0;
-        size_t sm0 = 0, sm1 = 0;
+        int64_t rowOff = 0, colOff = 0, K = 0, zOff = 0;
+        int slY = 0, slB2 = 0, slB1 = 0;
+        bool anyLong = false;
         for (int b = 0; b < nb; ++b) {
             HostBoard& H = hb[size_t(b)];
             KfBoard& B = db[size_t(b)];
@@ -763,8 +1038,13 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
             B.n2 = n2;
             B.nAlive = H.nAlive;
             B.fast = H.fast;
+            B.maxSa = H.maxSa;
+            B.maxSb = H.maxSb;
             B.rowOff = rowOff;
             B.colOff = colOff;
+            B.zOff = zOff;
+            B.zfOff = int64_t(b) * n1;
+            zOff += int64_t(n1) * H.nAlive;
             rowOff += int64_t(H.m1) * n1;
             colOff += int64_t(H.m2) * n2;
             B.l1 = up(k.keep, H.l1);
@@ -789,9 +1069,15 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
             B.yc = up_list(k.keep, H.yc);
             B.b2 = up_list(k.keep, H.b2);
             B.b1 = up_list(k.keep, H.b1);
-            sm0 = std::max(sm0, 8 * (size_t(H.m2) * (1 + 2 * size_t(H.maxFa) + size_t(H.maxSa)) + size_t(H.nAlive)));
-            sm1 = std::max(sm1, 8 * (size_t(H.m1) * (1 + 2 * size_t(H.maxFb) + size_t(H.maxSb)) +
-                                     size_t(H.maxSb) * size_t(H.nAlive) + size_t(H.maxFb)));
+            k.smVT = std::max(k.smVT, kf_vt_bytes(H.m2, H.maxSa, kKfWarps));
+            anyLong |= H.yr.lrow.size() > 0;
+            k.smUA = std::max(k.smUA, kf_ua_bytes(H.m2, H.maxFa));
+            k.smAV = std::max(k.smAV, kf_av_bytes(H.m1, H.nAlive, H.maxSb, H.maxFb));
+            k.smFA = std::max(k.smFA, 8 * (size_t(H.nAlive) + size_t(H.m2) * size_t(std::max(H.maxFa, 1))));
+            k.smFT = std::max(k.smFT, 8 * (size_t(H.nAlive) + size_t(H.m1)));
+            slY = std::max(slY, H.yr.nsl);
+            slB2 = std::max(slB2, H.b2.nsl);
+            slB1 = std::max(slB1, H.b1.nsl);
             e->nnzA += H.nnzA;
             e->nnzU += H.nnzU;
             e->nnzV += H.nnzV;
@@ -801,12 +1087,24 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
         e->k = K;
         e->flops_per_product = e->nnzV + e->nnzU + e->nnzA + (e->nnzM - K);
         const size_t limit = 227 * 1024 - 1024;
-        if (sm0 > limit || sm1 > limit)
+        if (k.smVT > limit || k.smUA > limit || k.smAV > limit || k.smFA > limit || k.smFT > limit)
             throw Fail{KR_INVALID_INPUT, "board too large for the Kronecker-factored engine's shared memory"};
-        k.smem[0] = sm0;
-        k.smem[1] = sm1;
-        raise_smem_limit(k_kf_ax<kKfThreads>, sm0);
-        raise_smem_limit(k_kf_atx<kKfThreads>, sm1);
+        raise_smem_limit(k_kfa_vt<kKfWarps>, k.smVT);
+        raise_smem_limit(k_kfa_ua<kKfWarps>, k.smUA);
+        raise_smem_limit(k_kft_av<kKfWarps>, k.smAV);
+        raise_smem_limit(k_kfa_fold, k.smFA);
+        raise_smem_limit(k_kft_fold, k.smFT);
+        k.gs = (slY + kKfWarps - 1) / kKfWarps;
+        k.gy = k.gs + (anyLong ? 1 : 0);
+        if (k.gy == 0) k.gy = 1;
+        k.gu = std::max(1, (slB2 + kKfWarps - 1) / kKfWarps);
+        k.gv = std::max(1, (slB1 + kKfWarps - 1) / kKfWarps);
+        for (int d = 0; d < 2; ++d) {
+            k.tz[d] = dev_alloc<double>(std::max<int64_t>(zOff, 1));
+            k.zf[d] = dev_alloc<double>(int64_t(nb) * n1);
+            k.keep.push_back(k.tz[d]);
+            k.keep.push_back(k.zf[d]);
+        }
         k.dBoards = up(k.keep, db);
         e->d_in = dev_alloc<double>(std::max<int64_t>(std::max(R, C), 1));
         e->d_out = dev_alloc<double>(std::max<int64_t>(std::max(R, C), 1));
