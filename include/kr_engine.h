@@ -149,6 +149,18 @@ int kr_engine_ax(kr_engine* e, const double* x, int64_t nx, double* y, int64_t n
 /* GradientEngine::ATx (solver.hpp:25, engine.hpp:96): x[cols] = A^T y[rows]. */
 int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t nx);
 
+/* Both products of one pair on HOST buffers: ax[rows] = A x[cols] and
+ * atx[cols] = A^T y[rows], the two directions' copies on the bus at once
+ * (host->device of x and y, device->host of both results, pipelined over
+ * board groups) and their kernels side by side; returns when both results
+ * are in host memory.  Results are bitwise those of kr_engine_ax then
+ * kr_engine_atx.  Pinned buffers (kr_host_alloc) replay a captured graph from
+ * the second call with the same pointers on.  No reference counterpart: the
+ * reference calls Ax and ATx one after the other (solver.hpp:21-27,
+ * bestResponseValue's two calls at a checkpoint are independent, 299). */
+int kr_engine_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_t nax, const double* y, int64_t ny,
+                   double* atx, int64_t natx);
+
 /* Device-pointer variants, enqueued on `stream` (NULL = the engine's own
  * stream); asynchronous with respect to the host. */
 int kr_engine_ax_device(kr_engine* e, const double* x_dev, double* y_dev, void* stream);

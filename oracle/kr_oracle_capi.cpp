@@ -4,6 +4,7 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <random>
 #include <thread>
 
 #include "kr_oracle.hpp"
@@ -313,17 +314,32 @@ double or_time_pairs(void* sp, const double* x, const double* y, int reps, doubl
 }
 // Same, with `threads` independent sparsifications processed concurrently
 // (one per thread: the multi-board CPU baseline; the reference engine itself
-// is sequential per call).
+// is sequential per call).  Inputs are dense Gaussians from
+// std::mt19937_64(seed + board) as the reference's bench draws them
+// (tools/main.cpp:313-317): the reference skips exact zeros
+// (engine.hpp:38, 105-106, 119-120, 127), so sparse inputs would flatter it.
+// The inputs are drawn before the clock starts.
 double or_time_pairs_multi(void** sps, int count, int threads, int reps, double* sink) {
     std::vector<std::thread> pool;
     std::vector<double> sinks(size_t(threads), 0.0);
+    std::vector<Vec> xs(static_cast<size_t>(count)), ys(static_cast<size_t>(count));
+    for (int b = 0; b < count; ++b) {
+        const auto& s = static_cast<Sp*>(sps[b])->s;
+        std::mt19937_64 rng(1 + uint64_t(b));
+        std::normal_distribution<double> gauss;
+        xs[size_t(b)].resize(size_t(s.cols()));
+        ys[size_t(b)].resize(size_t(s.rows()));
+        for (auto& v : xs[size_t(b)]) v = gauss(rng);
+        for (auto& v : ys[size_t(b)]) v = gauss(rng);
+    }
     auto t0 = std::chrono::steady_clock::now();
     for (int th = 0; th < threads; ++th)
         pool.emplace_back([&, th] {
             for (int b = th; b < count; b += threads) {
                 const auto& s = static_cast<Sp*>(sps[b])->s;
                 GradientWorkspace ws;
-                Vec xv(size_t(s.cols()), 0.5), yv(size_t(s.rows()), 0.25);
+                const Vec& xv = xs[size_t(b)];
+                const Vec& yv = ys[size_t(b)];
                 for (int r = 0; r < reps; ++r) {
                     Vec a = matvec(s, xv, ws);
                     Vec c = matvecTranspose(s, yv, ws);

@@ -191,6 +191,20 @@ void kf_destroy(KfState* k);
 
 }  // namespace krb
 
+namespace krb {
+// Resources of one pipelined host-buffer product (kr_engine_ax / _atx, and
+// each direction of kr_engine_pair): the stream it is forked from and joined
+// into, copy and stage streams, per-group events, device staging buffers.
+struct HostPipe {
+    cudaStream_t main = nullptr, copyIn = nullptr, copyOut = nullptr, stage2 = nullptr, stage3 = nullptr;
+    std::vector<cudaEvent_t> evIn, evOut, evMid, evSolve;
+    cudaEvent_t evStart = nullptr, evEnd = nullptr;
+    double* d_in = nullptr;   // owned by the pipe only for pipe[1]
+    double* d_out = nullptr;
+    bool made = false;
+};
+}  // namespace krb
+
 // Engine state (opaque to C callers).
 struct kr_engine {
     int device = 0;
@@ -267,17 +281,21 @@ struct kr_engine {
     std::vector<int64_t> grpRow{0}, grpCol{0};
     std::vector<int64_t> bSl[4], bNl[4];
     std::vector<int32_t> grpBoard{0};
-    cudaStream_t copyIn = nullptr, copyOut = nullptr, stage2 = nullptr, stage3 = nullptr;
-    std::vector<cudaEvent_t> evIn, evOut, evMid, evSolve;
-    cudaEvent_t evStart = nullptr, evEnd = nullptr;  // fork from / join into `stream`
+    // pipe[0]: the host-buffer products (main = `stream`); pipe[1]: the
+    // second direction of kr_engine_pair (its own streams and staging
+    // buffers, created on first use)
+    krb::HostPipe pipe[2];
     // captured host-buffer pipelines, keyed by (direction, host input,
-    // host output); pinned buffers only (kr_engine_ax / kr_engine_atx)
+    // host output[, second input, second output]); pinned buffers only
+    // (kr_engine_ax / kr_engine_atx: dir 0 / 1; kr_engine_pair: dir 2)
     struct PipeGraph {
         int dir;
         const double* in;
         double* out;
         cudaGraphExec_t exec;
         int64_t launches;
+        const double* in2 = nullptr;
+        double* out2 = nullptr;
     };
     std::vector<PipeGraph> pipeGraphs;
     std::vector<PipeGraph> pipeSeen;  // first calls (exec unused): captured on the second

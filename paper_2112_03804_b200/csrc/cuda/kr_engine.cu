@@ -1198,16 +1198,20 @@ std::vector<int64_t> board_lengths(const BoardPlan& p, int which) {
 void destroy_engine(kr_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
-    for (cudaEvent_t ev : e->evIn) cudaEventDestroy(ev);
-    for (cudaEvent_t ev : e->evOut) cudaEventDestroy(ev);
-    if (e->copyIn) cudaStreamDestroy(e->copyIn);
-    if (e->copyOut) cudaStreamDestroy(e->copyOut);
-    if (e->stage2) cudaStreamDestroy(e->stage2);
-    if (e->stage3) cudaStreamDestroy(e->stage3);
-    for (cudaEvent_t ev : e->evMid) cudaEventDestroy(ev);
-    for (cudaEvent_t ev : e->evSolve) cudaEventDestroy(ev);
-    if (e->evStart) cudaEventDestroy(e->evStart);
-    if (e->evEnd) cudaEventDestroy(e->evEnd);
+    for (int q = 0; q < 2; ++q) {
+        krb::HostPipe& P = e->pipe[q];
+        for (auto* v : {&P.evIn, &P.evOut, &P.evMid, &P.evSolve})
+            for (cudaEvent_t ev : *v) cudaEventDestroy(ev);
+        for (cudaStream_t st : {P.copyIn, P.copyOut, P.stage2, P.stage3})
+            if (st) cudaStreamDestroy(st);
+        if (P.evStart) cudaEventDestroy(P.evStart);
+        if (P.evEnd) cudaEventDestroy(P.evEnd);
+        if (q == 1) {
+            if (P.main) cudaStreamDestroy(P.main);
+            cudaFree(P.d_in);
+            cudaFree(P.d_out);
+        }
+    }
     for (auto& pg : e->pipeGraphs) cudaGraphExecDestroy(pg.exec);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->evFork) cudaEventDestroy(e->evFork);
@@ -1630,28 +1634,31 @@ void build_orders(kr_engine* e) {
     }
 }
 
+// Streams and events of one host pipe (>= 2 board groups).
+void make_host_pipe(kr_engine* e, krb::HostPipe& P) {
+    const int G = e->ngroups();
+    KR_CK(cudaStreamCreateWithFlags(&P.copyIn, cudaStreamNonBlocking));
+    KR_CK(cudaStreamCreateWithFlags(&P.copyOut, cudaStreamNonBlocking));
+    KR_CK(cudaStreamCreateWithFlags(&P.stage2, cudaStreamNonBlocking));
+    KR_CK(cudaEventCreateWithFlags(&P.evStart, cudaEventDisableTiming));
+    KR_CK(cudaEventCreateWithFlags(&P.evEnd, cudaEventDisableTiming));
+    const char* ps = std::getenv("KR_PIPE_STREAMS");
+    if (!(ps && std::atoi(ps) == 2)) KR_CK(cudaStreamCreateWithFlags(&P.stage3, cudaStreamNonBlocking));
+    for (auto* v : {&P.evIn, &P.evOut, &P.evMid, &P.evSolve}) {
+        v->resize(size_t(G));
+        for (auto& ev : *v) KR_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    P.made = true;
+}
+
 void make_pipeline(kr_engine* e) {
     set_carveout();
     build_orders(e);
-    const int G = e->ngroups();
-    if (G < 2) return;
-    KR_CK(cudaStreamCreateWithFlags(&e->copyIn, cudaStreamNonBlocking));
-    KR_CK(cudaStreamCreateWithFlags(&e->copyOut, cudaStreamNonBlocking));
-    KR_CK(cudaStreamCreateWithFlags(&e->stage2, cudaStreamNonBlocking));
-    KR_CK(cudaEventCreateWithFlags(&e->evStart, cudaEventDisableTiming));
-    KR_CK(cudaEventCreateWithFlags(&e->evEnd, cudaEventDisableTiming));
-    const char* ps = std::getenv("KR_PIPE_STREAMS");
-    if (!(ps && std::atoi(ps) == 2)) KR_CK(cudaStreamCreateWithFlags(&e->stage3, cudaStreamNonBlocking));
-    e->evIn.resize(size_t(G));
-    e->evOut.resize(size_t(G));
-    e->evMid.resize(size_t(G));
-    e->evSolve.resize(size_t(G));
-    for (int g = 0; g < G; ++g) {
-        KR_CK(cudaEventCreateWithFlags(&e->evIn[size_t(g)], cudaEventDisableTiming));
-        KR_CK(cudaEventCreateWithFlags(&e->evOut[size_t(g)], cudaEventDisableTiming));
-        KR_CK(cudaEventCreateWithFlags(&e->evMid[size_t(g)], cudaEventDisableTiming));
-        KR_CK(cudaEventCreateWithFlags(&e->evSolve[size_t(g)], cudaEventDisableTiming));
-    }
+    e->pipe[0].main = e->stream;
+    e->pipe[0].d_in = e->d_in;
+    e->pipe[0].d_out = e->d_out;
+    if (e->ngroups() < 2) return;
+    make_host_pipe(e, e->pipe[0]);
 }
 
 // Board groups of the pipelined host-buffer calls: up to eight contiguous
@@ -1926,96 +1933,154 @@ void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) { engi
 // board groups the input copy of group g overlaps the first-stage kernels of
 // the groups already copied, and the output copy of group g overlaps the
 // last-stage kernels of the groups after it (copyIn / stream / copyOut).
-void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout);
+void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout, const HostPipe& P);
 
-void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double* hout, int64_t nout) {
+bool pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void check_sizes(const kr_engine* e, int dir, int64_t nin, int64_t nout) {
     const int64_t wantIn = dir == 0 ? e->cols : e->rows, wantOut = dir == 0 ? e->rows : e->cols;
     if (nin != wantIn)
         throw Fail{KR_INVALID_INPUT,
                    "matvec input has size " + std::to_string(nin) + ", expected " + std::to_string(wantIn)};
     if (nout != wantOut) throw Fail{KR_INVALID_INPUT, "matvec output has the wrong size"};
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    KR_CK(cudaSetDevice(e->device));
-    const int G = e->ngroups();
-    if (G < 2) {
-        KR_CK(cudaMemcpyAsync(e->d_in, hin, 8 * size_t(nin), cudaMemcpyHostToDevice, e->stream));
-        engine_product(e, dir, e->d_in, e->d_out, e->stream);
-        KR_CK(cudaMemcpyAsync(hout, e->d_out, 8 * size_t(nout), cudaMemcpyDeviceToHost, e->stream));
-        KR_CK(cudaStreamSynchronize(e->stream));
+}
+
+// Replay the captured graph of this key, or capture it on the second call
+// with the same pinned buffers (later calls replay it with one launch: the
+// ~60 launches, copies and event edges per direction are no longer enqueued
+// by the host one by one).  Returns true when the work has been launched.
+// KR_NO_PIPE_GRAPH: always enqueue.
+template <class Enqueue>
+bool graph_call(kr_engine* e, int key, const double* in, double* out, const double* in2, double* out2,
+                Enqueue&& enqueue) {
+    if (std::getenv("KR_NO_PIPE_GRAPH")) return false;
+    if (!pinned_host(in) || !pinned_host(out) || (in2 && (!pinned_host(in2) || !pinned_host(out2)))) return false;
+    auto same = [&](const kr_engine::PipeGraph& pg) {
+        return pg.dir == key && pg.in == in && pg.out == out && pg.in2 == in2 && pg.out2 == out2;
+    };
+    for (auto& pg : e->pipeGraphs)
+        if (same(pg)) {
+            KR_CK(cudaGraphLaunch(pg.exec, e->stream));
+            e->launches += pg.launches;
+            return true;
+        }
+    bool seen = false;
+    for (auto& pg : e->pipeSeen) seen = seen || same(pg);
+    if (seen && e->pipeGraphs.size() < 8) {
+        const int64_t l0 = e->launches;
+        cudaGraph_t gr;
+        KR_CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue();
+        } catch (...) {
+            cudaStreamEndCapture(e->stream, &gr);
+            cudaGetLastError();
+            throw;
+        }
+        KR_CK(cudaStreamEndCapture(e->stream, &gr));
+        cudaGraphExec_t exec;
+        const cudaError_t ie = cudaGraphInstantiate(&exec, gr, 0);
+        cudaGraphDestroy(gr);
+        KR_CK(ie);
+        const int64_t dl = e->launches - l0;
+        e->launches = l0;
+        e->pipeGraphs.push_back({key, in, out, exec, dl, in2, out2});
+        KR_CK(cudaGraphLaunch(exec, e->stream));
+        e->launches += dl;
+        return true;
+    }
+    if (!seen && e->pipeSeen.size() < 16) e->pipeSeen.push_back({key, in, out, nullptr, 0, in2, out2});
+    return false;
+}
+
+// One direction's copies and product on pipe P (P.main forked from and
+// joined into e->stream by the caller when P.main != e->stream).
+void enqueue_direction(kr_engine* e, int dir, const double* hin, double* hout, const HostPipe& P) {
+    const int64_t nin = dir == 0 ? e->cols : e->rows, nout = dir == 0 ? e->rows : e->cols;
+    if (e->ngroups() < 2) {
+        KR_CK(cudaMemcpyAsync(P.d_in, hin, 8 * size_t(nin), cudaMemcpyHostToDevice, P.main));
+        first_stage(e, dir, P.d_in, P.main);   // the stages of engine_product; the caller accounts
+        middle(e, dir, P.main);
+        last_stage(e, dir, P.d_in, P.d_out, P.main);
+        KR_CK(cudaMemcpyAsync(hout, P.d_out, 8 * size_t(nout), cudaMemcpyDeviceToHost, P.main));
         return;
     }
-    // Pinned buffers (the usual case: a solver loop or a benchmark reuses
-    // them): the second call with the same (direction, input, output)
-    // captures the whole pipeline below into a CUDA graph, and later calls
-    // replay it, so the ~60 launches, copies and event edges are no longer
-    // enqueued by the host one by one.  KR_NO_PIPE_GRAPH: always enqueue.
-    auto pinned = [](const void* p) {
-        cudaPointerAttributes a{};
-        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        return a.type == cudaMemoryTypeHost;
-    };
-    const bool noGraph = std::getenv("KR_NO_PIPE_GRAPH") != nullptr;
-    if (!noGraph && pinned(hin) && pinned(hout)) {
-        for (auto& pg : e->pipeGraphs)
-            if (pg.dir == dir && pg.in == hin && pg.out == hout) {
-                KR_CK(cudaGraphLaunch(pg.exec, e->stream));
-                KR_CK(cudaStreamSynchronize(e->stream));
-                e->launches += pg.launches;
-                account(e, dir);
-                return;
-            }
-        bool seen = false;
-        for (auto& pg : e->pipeSeen) seen = seen || (pg.dir == dir && pg.in == hin && pg.out == hout);
-        if (seen && e->pipeGraphs.size() < 8) {
-            const int64_t l0 = e->launches;
-            cudaGraph_t gr;
-            KR_CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-            try {
-                enqueue_pipeline(e, dir, hin, hout);
-            } catch (...) {
-                cudaStreamEndCapture(e->stream, &gr);
-                cudaGetLastError();
-                throw;
-            }
-            KR_CK(cudaStreamEndCapture(e->stream, &gr));
-            cudaGraphExec_t exec;
-            const cudaError_t ie = cudaGraphInstantiate(&exec, gr, 0);
-            cudaGraphDestroy(gr);
-            KR_CK(ie);
-            const int64_t dl = e->launches - l0;
-            e->launches = l0;
-            e->pipeGraphs.push_back({dir, hin, hout, exec, dl});
-            KR_CK(cudaGraphLaunch(exec, e->stream));
-            KR_CK(cudaStreamSynchronize(e->stream));
-            e->launches += dl;
-            account(e, dir);
-            return;
-        }
-        if (!seen && e->pipeSeen.size() < 16) e->pipeSeen.push_back({dir, hin, hout, nullptr, 0});
-    }
-    enqueue_pipeline(e, dir, hin, hout);
+    enqueue_pipeline(e, dir, hin, hout, P);
+}
+
+void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double* hout, int64_t nout) {
+    check_sizes(e, dir, nin, nout);
+    KR_CK(cudaSetDevice(e->device));
+    if (!graph_call(e, dir, hin, hout, nullptr, nullptr, [&] { enqueue_direction(e, dir, hin, hout, e->pipe[0]); }))
+        enqueue_direction(e, dir, hin, hout, e->pipe[0]);
     KR_CK(cudaStreamSynchronize(e->stream));
     account(e, dir);
 }
 
+// The second direction's pipe of kr_engine_pair (own streams, events and
+// staging buffers, so the two directions' copies and kernels overlap).
+void ensure_pair_pipe(kr_engine* e) {
+    HostPipe& P = e->pipe[1];
+    if (P.main) return;
+    KR_CK(cudaStreamCreateWithFlags(&P.main, cudaStreamNonBlocking));
+    const int64_t n = std::max<int64_t>(std::max(e->rows, e->cols), 1);
+    P.d_in = dev_alloc<double>(n);
+    P.d_out = dev_alloc<double>(n);
+    if (e->ngroups() >= 2) make_host_pipe(e, P);
+    if (!e->evFork) {
+        KR_CK(cudaEventCreateWithFlags(&e->evFork, cudaEventDisableTiming));
+        KR_CK(cudaEventCreateWithFlags(&e->evJoin, cudaEventDisableTiming));
+    }
+}
+
+// kr_engine_pair: A x on pipe 0 (from e->stream) and A^T y on pipe 1, both
+// directions' copies on the bus at once and their kernels side by side; one
+// synchronisation at the end.  Each direction has its own scratch (d_tz /
+// d_tz2, and the implicit engines' per-direction buffers), so the results are
+// the bits of kr_engine_ax then kr_engine_atx.
+void host_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_t nax, const double* y, int64_t ny,
+               double* atx, int64_t natx) {
+    check_sizes(e, 0, nx, nax);
+    check_sizes(e, 1, ny, natx);
+    KR_CK(cudaSetDevice(e->device));
+    ensure_pair_pipe(e);
+    auto enqueue = [&] {
+        KR_CK(cudaEventRecord(e->evFork, e->stream));
+        KR_CK(cudaStreamWaitEvent(e->pipe[1].main, e->evFork, 0));
+        enqueue_direction(e, 1, y, atx, e->pipe[1]);
+        enqueue_direction(e, 0, x, ax, e->pipe[0]);
+        KR_CK(cudaEventRecord(e->evJoin, e->pipe[1].main));
+        KR_CK(cudaStreamWaitEvent(e->stream, e->evJoin, 0));
+    };
+    if (!graph_call(e, 2, x, ax, y, atx, enqueue)) enqueue();
+    KR_CK(cudaStreamSynchronize(e->stream));
+    account(e, 0);
+    account(e, 1);
+}
+
 // The pipelined host-buffer product (board groups), enqueued from and
-// joined back into e->stream: every stream it uses waits for the work
-// already queued on e->stream, and e->stream waits for all of it.
-void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout) {
+// joined back into P.main: every stream it uses waits for the work already
+// queued on P.main, and P.main waits for all of it.
+void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout, const HostPipe& P) {
     const int G = e->ngroups();
     const std::vector<int64_t>& io = dir == 0 ? e->grpCol : e->grpRow;
     const std::vector<int64_t>& oo = dir == 0 ? e->grpRow : e->grpCol;
-    KR_CK(cudaEventRecord(e->evStart, e->stream));
-    for (cudaStream_t q : {e->copyIn, e->copyOut, e->stage2, e->stage3})
-        if (q) KR_CK(cudaStreamWaitEvent(q, e->evStart, 0));
+    KR_CK(cudaEventRecord(P.evStart, P.main));
+    for (cudaStream_t q : {P.copyIn, P.copyOut, P.stage2, P.stage3})
+        if (q) KR_CK(cudaStreamWaitEvent(q, P.evStart, 0));
     auto copy_out = [&](int g, cudaStream_t from) {
-        KR_CK(cudaEventRecord(e->evOut[size_t(g)], from));
-        KR_CK(cudaStreamWaitEvent(e->copyOut, e->evOut[size_t(g)], 0));
+        KR_CK(cudaEventRecord(P.evOut[size_t(g)], from));
+        KR_CK(cudaStreamWaitEvent(P.copyOut, P.evOut[size_t(g)], 0));
         const size_t a = size_t(oo[size_t(g)]), n = size_t(oo[size_t(g) + 1]) - a;
-        KR_CK(cudaMemcpyAsync(hout + a, e->d_out + a, 8 * n, cudaMemcpyDeviceToHost, e->copyOut));
+        KR_CK(cudaMemcpyAsync(hout + a, P.d_out + a, 8 * n, cudaMemcpyDeviceToHost, P.copyOut));
     };
     // Input copies run two groups ahead of the kernel enqueue: group g's
     // kernels are queued before its input lands (enqueueing every copy first
@@ -2027,8 +2092,8 @@ void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout) {
         for (; nextIn < std::min(upto + 1, G); ++nextIn) {
             const int g = nextIn;
             const size_t a = size_t(io[size_t(g)]), n = size_t(io[size_t(g) + 1]) - a;
-            KR_CK(cudaMemcpyAsync(e->d_in + a, hin + a, 8 * n, cudaMemcpyHostToDevice, e->copyIn));
-            KR_CK(cudaEventRecord(e->evIn[size_t(g)], e->copyIn));
+            KR_CK(cudaMemcpyAsync(P.d_in + a, hin + a, 8 * n, cudaMemcpyHostToDevice, P.copyIn));
+            KR_CK(cudaEventRecord(P.evIn[size_t(g)], P.copyIn));
         }
     };
     // Every factor is block diagonal over boards, and so is M's chain solve
@@ -2042,45 +2107,45 @@ void enqueue_pipeline(kr_engine* e, int dir, const double* hin, double* hout) {
     if (e->kron || e->kf) {
         for (int g = 0; g < G; ++g) {
             copy_in(g + 1);
-            KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
-            last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
-            copy_out(g, e->stream);
+            KR_CK(cudaStreamWaitEvent(P.main, P.evIn[size_t(g)], 0));
+            last_stage(e, dir, P.d_in, P.d_out, P.main, g);
+            copy_out(g, P.main);
         }
     } else if (e->mkind == 0 ||
                (e->mkind == 1 && int64_t(e->bCh.size()) == int64_t(e->grpBoard.back()) + 1)) {
         // KR_PIPE_STREAMS=2: the M solve on stage2 ahead of the last SpMV
-        const bool three = e->stage3 != nullptr;
+        const bool three = P.stage3 != nullptr;
         for (int g = 0; g < G; ++g) {
             copy_in(g + 1);
-            KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
-            first_stage(e, dir, e->d_in, e->stream, g);
-            KR_CK(cudaEventRecord(e->evMid[size_t(g)], e->stream));
+            KR_CK(cudaStreamWaitEvent(P.main, P.evIn[size_t(g)], 0));
+            first_stage(e, dir, P.d_in, P.main, g);
+            KR_CK(cudaEventRecord(P.evMid[size_t(g)], P.main));
             if (three) {  // the latency-bound solve on its own stream
-                KR_CK(cudaStreamWaitEvent(e->stage3, e->evMid[size_t(g)], 0));
-                middle(e, dir, e->stage3, g);
-                KR_CK(cudaEventRecord(e->evSolve[size_t(g)], e->stage3));
-                KR_CK(cudaStreamWaitEvent(e->stage2, e->evSolve[size_t(g)], 0));
+                KR_CK(cudaStreamWaitEvent(P.stage3, P.evMid[size_t(g)], 0));
+                middle(e, dir, P.stage3, g);
+                KR_CK(cudaEventRecord(P.evSolve[size_t(g)], P.stage3));
+                KR_CK(cudaStreamWaitEvent(P.stage2, P.evSolve[size_t(g)], 0));
             } else {
-                KR_CK(cudaStreamWaitEvent(e->stage2, e->evMid[size_t(g)], 0));
-                middle(e, dir, e->stage2, g);
+                KR_CK(cudaStreamWaitEvent(P.stage2, P.evMid[size_t(g)], 0));
+                middle(e, dir, P.stage2, g);
             }
-            last_stage(e, dir, e->d_in, e->d_out, e->stage2, g);
-            copy_out(g, e->stage2);
+            last_stage(e, dir, P.d_in, P.d_out, P.stage2, g);
+            copy_out(g, P.stage2);
         }
     } else {
         copy_in(G - 1);
         for (int g = 0; g < G; ++g) {
-            KR_CK(cudaStreamWaitEvent(e->stream, e->evIn[size_t(g)], 0));
-            first_stage(e, dir, e->d_in, e->stream, g);
+            KR_CK(cudaStreamWaitEvent(P.main, P.evIn[size_t(g)], 0));
+            first_stage(e, dir, P.d_in, P.main, g);
         }
-        middle(e, dir, e->stream);
+        middle(e, dir, P.main);
         for (int g = 0; g < G; ++g) {
-            last_stage(e, dir, e->d_in, e->d_out, e->stream, g);
-            copy_out(g, e->stream);
+            last_stage(e, dir, P.d_in, P.d_out, P.main, g);
+            copy_out(g, P.main);
         }
     }
-    KR_CK(cudaEventRecord(e->evEnd, e->copyOut));
-    KR_CK(cudaStreamWaitEvent(e->stream, e->evEnd, 0));
+    KR_CK(cudaEventRecord(P.evEnd, P.copyOut));
+    KR_CK(cudaStreamWaitEvent(P.main, P.evEnd, 0));
 }
 
 }  // namespace krb
@@ -2141,6 +2206,15 @@ int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t 
     return guarded([&] {
         if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
         krb::host_product(e, 1, y, ny, x, nx);
+    });
+}
+
+int kr_engine_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_t nax, const double* y, int64_t ny,
+                   double* atx, int64_t natx) {
+    return guarded([&] {
+        if (!e || !x || !ax || !y || !atx) throw Fail{KR_INVALID_INPUT, "null argument"};
+        if (x == atx || y == ax) throw Fail{KR_INVALID_INPUT, "pair outputs must not alias the other direction's input"};
+        krb::host_pair(e, x, nx, ax, nax, y, ny, atx, natx);
     });
 }
 

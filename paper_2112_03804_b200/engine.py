@@ -131,6 +131,17 @@ class CudaEngine:
         N.check(N.cuda().kr_engine_ax(self._h, N.ptr(x), len(x), N.ptr(y), len(y)))
         return y
 
+    def pair(self, x2, x1, out=None):
+        """(A x2, Aᵀ x1) through kr_engine_pair: both directions' host<->device
+        copies and kernels in flight together (bitwise Ax then ATx).  `out`:
+        optional (ax, atx) host arrays to fill (pinned ones replay a graph)."""
+        x = np.ascontiguousarray(x2, np.float64)
+        y = np.ascontiguousarray(x1, np.float64)
+        ax, atx = out if out is not None else (np.empty(self.rows), np.empty(self.cols))
+        N.check(N.cuda().kr_engine_pair(self._h, N.ptr(x), len(x), N.ptr(ax), len(ax), N.ptr(y), len(y), N.ptr(atx),
+                                        len(atx)))
+        return ax, atx
+
     def ATx(self, x1):
         y = np.ascontiguousarray(x1, np.float64)
         x = np.empty(self.cols)

@@ -301,3 +301,39 @@ def test_host_call_after_async_device_call_is_ordered():
     torch.cuda.ExternalStream(eng.stream).synchronize()
     assert bits_equal(oax.cpu().numpy(), eng.Ax(dx.cpu().numpy()))
     assert bits_equal(oatx.cpu().numpy(), eng.ATx(dy.cpu().numpy()))
+
+
+@pytest.mark.parametrize("kind,nb", [("factored", 1), ("factored", 4), ("implicit", 4), ("kfactored", 4),
+                                     ("kfactored", 1)])
+def test_host_pair_call_bitwise(kind, nb):
+    """kr_engine_pair (both directions' copies and kernels in flight together)
+    gives the bits of kr_engine_ax then kr_engine_atx, on pageable buffers and
+    on pinned ones (enqueued, captured, then replayed as a graph), also after
+    the inputs change."""
+    import ctypes
+
+    from paper_2112_03804_b200 import _native as N
+    boards = H.turn_instances(nboards=nb, factors=kind == "factored")
+    insts = [i for i, _ in boards]
+    eng = (CudaEngine([f for _, f in boards]) if kind == "factored" else
+           CudaEngine.kron(insts) if kind == "implicit" else CudaEngine.kfactored(insts))
+    rng = np.random.default_rng(41)
+    x, y = rng.standard_normal(eng.cols), rng.standard_normal(eng.rows)
+    ax, atx = eng.pair(x, y)
+    assert bits_equal(ax, eng.Ax(x)) and bits_equal(atx, eng.ATx(y))
+    L = N.cuda()
+    arr = lambda p, n: np.ctypeslib.as_array((ctypes.c_double * n).from_address(p))  # noqa: E731
+    ptrs = [L.kr_host_alloc(8 * n) for n in (eng.cols, eng.rows, eng.rows, eng.cols)]
+    try:
+        px, py, pax, patx = (arr(p, n) for p, n in zip(ptrs, (eng.cols, eng.rows, eng.rows, eng.cols)))
+        for call in range(4):
+            px[:], py[:] = rng.standard_normal(eng.cols), rng.standard_normal(eng.rows)
+            N.check(L.kr_engine_pair(eng.handle, ptrs[0], eng.cols, ptrs[2], eng.rows, ptrs[1], eng.rows, ptrs[3],
+                                     eng.cols))
+            assert bits_equal(pax.copy(), eng.Ax(px.copy())), call
+            assert bits_equal(patx.copy(), eng.ATx(py.copy())), call
+    finally:
+        for p in ptrs:
+            L.kr_host_free(p)
+    with pytest.raises(InvalidInputError):
+        eng.pair(x[:-1], y)

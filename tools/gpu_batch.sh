@@ -1,8 +1,4 @@
 # ad-hoc GPU batch (edited per call)
-T=r02k
-timeout 600 python -m pytest tests/test_gpu_kfengine.py -q -x -p no:cacheprovider > gpurun_out/${T}_pytest_kf.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest_kf.log
-timeout 600 python tools/kf_probe.py > gpurun_out/${T}_kf_probe.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_kf_probe.log
-for c in 3 2; do
-timeout 600 ncu --metrics gpu__time_duration.sum,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum --clock-control none -k "regex:k_kf" --launch-skip 10 --launch-count 10 --csv python tools/kf_probe.py $c > gpurun_out/${T}_list$c.csv 2>&1
-done
-tail -n 3 gpurun_out/${T}_pytest_kf.log; cat gpurun_out/${T}_kf_probe.log
+T=r02l
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider --durations=15 > gpurun_out/${T}_pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest_gpu.log
+tail -n 25 gpurun_out/${T}_pytest_gpu.log
