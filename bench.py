@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--boards", type=int, default=NBOARDS)
     p.add_argument("--solver-iters", type=int, default=100)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-sweep", action="store_true", help="skip the config-5 sweep leg")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the bounded CPU sample")
     return p.parse_args()
 
@@ -308,15 +309,52 @@ def config1_cpu(gpu):
             "exploitability": r["exploitability"], "gpu_trace_bitwise_equal": same}
 
 
-def cpu_baseline(threads, budget_s):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(threads, budget_s, gpu_out=None):
     """The reference engine (restated in oracle/: matvec / matvecTranspose,
     engine.hpp:58-133, sequential per call) over a bounded sample of the
-    boards, one board per host thread; scaled to full-turn pairs/s."""
+    boards, one board per host thread; scaled to full-turn pairs/s.  Inputs
+    are dense Gaussians (mt19937_64, as tools/main.cpp:313-317).  Also: the
+    reference-faithful single-thread per-call time (engine.hpp:11-13 is
+    sequential), and the parity check of the GPU's timed outputs against the
+    oracle on the sampled boards (gpu_out: {engine: (ax, atx)} host arrays of
+    the bench's x, y)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     nb = min(NBOARDS, threads)
     pairs = oracle_boards(range(nb), threads, with_instances=True)
     sps = [sp for _, sp in pairs]
+    # single thread, one board, per call (SURVEY.md §8(d) CPU baseline (i))
+    rng = np.random.default_rng(1)
+    x0, y0 = rng.standard_normal(pairs[0][0].cols), rng.standard_normal(pairs[0][0].rows)
+    s1 = sps[0].time_pairs(x0, y0, 1)
+    reps1 = max(2, int(min(3.0, budget_s / 4) / max(s1, 1e-4)))
+    s1 = sps[0].time_pairs(x0, y0, reps1) / reps1
+    parity = None
+    if gpu_out:
+        parity = {"boards": nb, "inputs": "the bench's own x, y (Gaussian)", "engines": {}}
+        for name, (gax, gatx, x, y) in gpu_out.items():
+            ok = True
+            c0 = r0 = 0
+            for inst, sp in pairs:
+                ok &= bool(np.array_equal(sp.matvec(x[c0:c0 + inst.cols]).view(np.int64),
+                                          gax[r0:r0 + inst.rows].view(np.int64)))
+                ok &= bool(np.array_equal(sp.matvec_t(y[r0:r0 + inst.rows]).view(np.int64),
+                                          gatx[c0:c0 + inst.cols].view(np.int64)))
+                c0 += inst.cols
+                r0 += inst.rows
+            parity["engines"][name] = ok
+        parity["bitwise"] = all(parity["engines"].values())
     t1 = po.time_pairs_multi(sps, threads, 1)  # warm + estimate
     reps = max(1, int(budget_s / max(t1, 1e-3)))
     t = po.time_pairs_multi(sps, threads, reps)
@@ -326,8 +364,13 @@ def cpu_baseline(threads, budget_s):
     iters = max(1, int(0.5 * budget_s / max(d1, 1e-3)))
     d = po.time_dcfr_multi(pairs, threads, iters)
     return {"value": board_pairs_per_s / NBOARDS, "unit": "pairs/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(), "inputs": "dense Gaussian x, y (mt19937_64, tools/main.cpp:313-317)",
             "sample": f"{nb} of {NBOARDS} boards x {reps} matvec pairs each, one board per thread "
                       f"({t:.1f} s); full-turn pairs/s = board-pairs/s / {NBOARDS}",
+            "single_thread": {"ms_per_pair_one_board": 1e3 * s1, "full_turn_pairs_per_s": 1.0 / (s1 * NBOARDS),
+                              "cores": 1, "sample": f"board 0, {reps1} pairs, one thread (the reference engine is "
+                                                    "sequential per call, engine.hpp:11-13)"},
+            "parity": parity,
             "solver_iters_per_s": nb * iters / d / NBOARDS,
             "solver_sample": f"{nb} of {NBOARDS} boards x {iters} DCFR iterations each (default parameters, "
                              f"no checkpoints), one board per thread ({d:.1f} s); full-turn it/s = "
@@ -364,7 +407,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.boards, 1, {"steps_requested": args.steps}),
+            "config": workload_config(args.boards, args.gpus),
+            "steps_requested": args.steps,
             "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
                              "sample": f"all {args.boards} boards per step, one board per thread at a time; "
                                        "reference engine restated in oracle/ (Eigen3 absent: reference "
@@ -432,6 +476,8 @@ def run_product(args):
     t0 = time.time()
     eng = CudaEngine([f for _, f in boards], device=local)
     create_s = time.time() - t0
+    nnz_stored = int(sum(f.size() for _, f in boards))
+    pair_bytes = 2 * eng.bytes_per_product()
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -489,29 +535,9 @@ def run_product(args):
     pairs_per_s = args.steps / (ms / 1e3)
 
     # ---- e2e: the C-ABI host-buffer calls, H2D + D2H inside the region ----
-    from paper_2112_03804_b200 import _native as N
-    L = N.cuda()
+    e2e = e2e_host_pairs(eng, x, y, barrier, max_over_ranks, max(5, min(args.steps, 50)))
+    check_ok = bool(np.array_equal(e2e.pop("_ax"), ax.cpu().numpy()))
     nx, ny = eng.cols, eng.rows
-    px, py = L.kr_host_alloc(8 * nx), L.kr_host_alloc(8 * ny)
-    pax, patx = L.kr_host_alloc(8 * ny), L.kr_host_alloc(8 * nx)
-    as_np = lambda p, n: np.ctypeslib.as_array((__import__("ctypes").c_double * n).from_address(p))  # noqa: E731
-    hx, hy, hax, hatx = as_np(px, nx), as_np(py, ny), as_np(pax, ny), as_np(patx, nx)
-    hx[:] = x.cpu().numpy()
-    hy[:] = y.cpu().numpy()
-    e2e_steps = max(5, min(args.steps, 50))
-    for _ in range(2):
-        N.check(L.kr_engine_ax(eng.handle, px, nx, pax, ny))
-        N.check(L.kr_engine_atx(eng.handle, py, ny, patx, nx))
-    barrier()
-    t_e2e0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        N.check(L.kr_engine_ax(eng.handle, px, nx, pax, ny))
-        N.check(L.kr_engine_atx(eng.handle, py, ny, patx, nx))
-    e2e_s = max_over_ranks(time.perf_counter() - t_e2e0)
-    barrier()
-    check_ok = bool(np.array_equal(hax, ax.cpu().numpy()))
-    for p in (px, py, pax, patx):
-        L.kr_host_free(p)
 
     # ---- solver iterations/s (DCFR, checkpointEvery = 50) ----------------
     i0 = boards[0][0]
@@ -526,12 +552,27 @@ def run_product(args):
     torch.cuda.synchronize(dev)
     solver_s = max_over_ranks(time.perf_counter() - ts)
 
+    # ---- Kronecker-factored engine (bitwise, nothing streamed) -------------
+    kfac = run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, coll_dev, barrier,
+                         max_over_ranks, sum_over_ranks, res)
     # ---- implicit Kronecker engine (K7) -------------
     implicit = run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
                             sum_over_ranks)
     turn = run_turn(rank, world, local, max_over_ranks, dist.group.WORLD if world > 1 else None)
     config1 = config1_gpu() if rank == 0 else None
     config2 = config2_gpu(measured_peak()[0]) if rank == 0 else None
+    gpu_out = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the timed region's last outputs, for the parity check against the oracle
+        eng.ax_device(x.data_ptr(), ax.data_ptr())
+        eng.atx_device(y.data_ptr(), atx.data_ptr())
+        torch.cuda.ExternalStream(eng.stream, device=dev).synchronize()
+        gpu_out = {"factored": (ax.cpu().numpy(), atx.cpu().numpy(), x.cpu().numpy(), y.cpu().numpy())}
+    del boards
+    solver.close()
+    eng.close()
+    torch.cuda.empty_cache()
+    sweep = run_sweep() if rank == 0 and world == 1 and not args.no_sweep else None
 
     if rank != 0:
         return 0
@@ -545,40 +586,230 @@ def run_product(args):
                    "share_of_step": v["ms"] / pre_ms if pre_ms else None} for k, v in pre_times.items()}
     kernels["_source"] = (f"pre-pass of {pre_steps} pairs with every SpMV bracketed by events; the roofline "
                           f"kernel ({dominant}) is timed again over the timed region itself")
-    pair_bytes = 2 * eng.bytes_per_product()
     line = {
         "metric": METRIC, "value": pairs_per_s, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.boards, world, {
-            "nnz_stored": int(sum(f.size() for _, f in boards)) if world == 1 else None,
-            "algorithmic_bytes_per_pair": pair_bytes if world == 1 else None,
-            "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2)}),
+        "config": workload_config(args.boards, world),
+        "workload_detail": {"nnz_stored": nnz_stored if world == 1 else None,
+                            "algorithmic_bytes_per_pair": pair_bytes if world == 1 else None,
+                            "host_build_s": round(build_s, 2), "engine_create_s": round(create_s, 2)},
         "roofline": {"bound": "hbm", "kernel": f"k_spmv[{dominant}]", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
                      "traffic": ncu_traffic(dominant) if world == 1 and args.boards == NBOARDS else None,
                      "whole_pair_gb_per_s": pair_bytes / (ms_local / args.steps / 1e3) / 1e9 if world == 1 else None},
         "kernels": kernels,
-        "e2e": {"value": e2e_steps / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": 8 * (nx + ny),
-                "d2h_bytes_per_step": 8 * (nx + ny), "api": "kr_engine_ax / kr_engine_atx (host pinned buffers)",
-                "steps": e2e_steps, "matches_device_path": check_ok},
+        "e2e": dict(e2e, matches_device_path=check_ok),
         "solver_iters_per_s": args.solver_iters / solver_s,
         "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"],
                    "checkpoint_every": 50},
         "gpu_launches": gpu_launches,
         "clocks": sampler.summary(),
+        "kfactored": kfac,
         "implicit": implicit,
+        "config5_sweep": sweep,
         "config1": {k: v for k, v in config1.items() if not k.startswith("_")},
         "config2": config2,
         "turn": turn,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1, args.cpu_seconds, gpu_out)
+        line["parity"] = line["cpu_baseline"].pop("parity")
         line["cpu_baseline"]["config1"] = config1_cpu(config1)
     print(json.dumps(_finite(line)), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def e2e_host_pairs(eng, x, y, barrier, max_over_ranks, steps):
+    """End to end through the C ABI on pinned host buffers: each step ships x
+    and y to the device and both results back (H2D + D2H inside the timed
+    region).  Headline: kr_engine_pair (both directions' copies and kernels in
+    flight together, graph-replayed); beside it the reference's call pattern,
+    kr_engine_ax then kr_engine_atx."""
+    import ctypes
+
+    from paper_2112_03804_b200 import _native as N
+    L = N.cuda()
+    nx, ny = eng.cols, eng.rows
+    px, py, pax, patx = (L.kr_host_alloc(8 * n) for n in (nx, ny, ny, nx))
+    as_np = lambda p, n: np.ctypeslib.as_array((ctypes.c_double * n).from_address(p))  # noqa: E731
+    as_np(px, nx)[:] = x.cpu().numpy()
+    as_np(py, ny)[:] = y.cpu().numpy()
+
+    def pair():
+        N.check(L.kr_engine_pair(eng.handle, px, nx, pax, ny, py, ny, patx, nx))
+
+    def serial():
+        N.check(L.kr_engine_ax(eng.handle, px, nx, pax, ny))
+        N.check(L.kr_engine_atx(eng.handle, py, ny, patx, nx))
+
+    out = {}
+    for name, fn in (("serial", serial), ("pair", pair)):
+        for _ in range(3):
+            fn()
+        barrier()
+        t = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        out[name] = steps / max_over_ranks(time.perf_counter() - t)
+    res = {"value": out["pair"], "unit": "pairs/s", "h2d_bytes_per_step": 8 * (nx + ny),
+           "d2h_bytes_per_step": 8 * (nx + ny), "steps": steps,
+           "api": "kr_engine_pair (host pinned buffers: x, y in; A x, A^T y out; both directions in flight)",
+           "serial_calls": {"value": out["serial"], "api": "kr_engine_ax then kr_engine_atx (the reference's "
+                                                          "call pattern, solver.hpp:366, 370)"},
+           "_ax": as_np(pax, ny).copy()}
+    for p in (px, py, pax, patx):
+        L.kr_host_free(p)
+    return res
+
+
+def run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
+                  sum_over_ranks, ref_solve):
+    """The same pairs through the Kronecker-factored engine (Technique B post
+    kept as its hand-space factors, every Kronecker product expanded on the
+    fly: kr_kfengine.cu), which is BITWISE the factored engine: device
+    pairs/s, e2e, the bit check against the factored outputs, and DCFR
+    iterations/s with the trace compared bitwise to the factored solve."""
+    import torch
+
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200.dist import DistributedDcfr
+    from paper_2112_03804_b200.solver import CudaSolver
+
+    t0 = time.time()
+    ek = CudaEngine.kfactored([b[0] for b in boards], device=local)
+    create_s = time.time() - t0
+    st = torch.cuda.ExternalStream(ek.stream, device=dev)
+    kax, katx = torch.empty_like(ax), torch.empty_like(atx)
+
+    def serial():
+        ek.ax_device(x.data_ptr(), kax.data_ptr())
+        ek.atx_device(y.data_ptr(), katx.data_ptr())
+
+    def pair():
+        ek.pair_device(x.data_ptr(), kax.data_ptr(), y.data_ptr(), katx.data_ptr())
+
+    res = {}
+    steps = max(args.steps, 50)
+    for name, fn in (("serial", serial), ("pair", pair)):
+        for _ in range(max(args.warmup, 3)):
+            fn()
+        torch.cuda.synchronize(dev)
+        l0 = ek.launches()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        barrier()
+        res[name] = (max_over_ranks(e0.elapsed_time(e1)), int(sum_over_ranks(ek.launches() - l0)))
+    bitwise = bool(torch.equal(kax, ax) and torch.equal(katx, atx))
+    bitwise = max_over_ranks(0.0 if bitwise else 1.0) == 0.0
+    e2e = e2e_host_pairs(ek, x, y, barrier, max_over_ranks, 50)
+    e2e.pop("_ax")
+    i0 = boards[0][0]
+    solver = CudaSolver(ek, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
+                        i0.pot)
+    drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=coll_dev)
+    drv.run(max_iters=5, checkpoint_every=5)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ts = time.perf_counter()
+    r = drv.run(max_iters=args.solver_iters, checkpoint_every=50)
+    torch.cuda.synchronize(dev)
+    solver_s = max_over_ranks(time.perf_counter() - ts)
+    same_trace = bool(np.array_equal(np.asarray(r["trace_expl"]).view(np.int64),
+                                     np.asarray(ref_solve["trace_expl"]).view(np.int64)))
+    out = {"engine": "kr_engine_create_kfactored (Technique B post from its Kronecker factors; "
+                     "k_kfa_vt / k_kfa_fold / k_kfa_ua, k_kft_fold / k_kft_av)",
+           "pairs_per_s": steps / (res["serial"][0] / 1e3), "us_per_pair": 1e3 * res["serial"][0] / steps,
+           "concurrent_pair": {"api": "kr_engine_pair_device", "pairs_per_s": steps / (res["pair"][0] / 1e3),
+                               "us_per_pair": 1e3 * res["pair"][0] / steps},
+           "steps": steps, "gpu_launches": res["serial"][1], "bitwise_equal_to_factored": bitwise,
+           "create_s": round(create_s, 3), "e2e": e2e,
+           "solver_iters_per_s": args.solver_iters / solver_s,
+           "solver": {"iterations": r["iterations"], "exploitability": r["exploitability"],
+                      "trace_bitwise_equal_to_factored_solve": same_trace}}
+    solver.close()
+    ek.close()
+    return out
+
+
+def run_sweep(budget_s=40.0):
+    """Config 5 (BASELINE.json): matvec pairs over synthetic poker instances
+    from ~5e5 to ~1.25e9 stored nonzeros, one B200.  Each point's factored
+    engine is built on the device (kr_engine_create_device_b, bitwise the
+    host-built engine) and timed with CUDA events (whole pair, Ax then ATy);
+    the Kronecker-factored engine (bitwise, nothing streamed) beside it.
+    Algorithmic bytes per BASELINE.md §2."""
+    import torch
+
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200 import host as H
+    peak = measured_peak()[0]
+
+    def river(board, deck=52, tree=3):
+        return [H.builtin("river_full", seed=1, board=board, deck=deck, tree=tree)]
+
+    def turns(ts, tree):
+        out = []
+        for t in ts:
+            out += [i for i, _ in H.turn_instances(turn=t, nboards=NBOARDS, tree=tree, factors=False)]
+        return out
+
+    points = [("config4: 26-card deck, 210 hands, 3-bet", lambda: river("Kc9d7c4d2c", deck=26)),
+              ("config2: river 1081 hands, 3-bet", lambda: river("Ks7d4c2h9s")),
+              ("river 1081 hands, 91-seq tree", lambda: river("Ks7d4c2h9s", tree=91)),
+              ("config3: turn x 48 rivers, 3-bet", lambda: turns([TURN], 3)),
+              ("turn x 48 rivers, 91-seq tree", lambda: turns([TURN], 91)),
+              ("2 turns x 48 rivers, 91-seq tree", lambda: turns([TURN, "Ah8c5d3s"], 91))]
+
+    def timed(e, reps):
+        st = torch.cuda.ExternalStream(e.stream)
+        x = torch.randn(e.cols, dtype=torch.float64, device="cuda")
+        y = torch.randn(e.rows, dtype=torch.float64, device="cuda")
+        a = torch.empty(e.rows, dtype=torch.float64, device="cuda")
+        b = torch.empty(e.cols, dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            e.ax_device(x.data_ptr(), a.data_ptr())
+            e.atx_device(y.data_ptr(), b.data_ptr())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            e.ax_device(x.data_ptr(), a.data_ptr())
+            e.atx_device(y.data_ptr(), b.data_ptr())
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    rows, t_start = [], time.time()
+    for name, make in points:
+        if time.time() - t_start > budget_s:
+            rows.append({"point": name, "skipped": "sweep time budget"})
+            continue
+        insts = make()
+        eng = CudaEngine.device_built(insts)
+        nnz = sum(eng.nnz.values())
+        pair_bytes = 2 * eng.bytes_per_product()
+        reps = max(10, min(500, int(0.3 / max(pair_bytes / (peak * 1e9 * 0.8), 1e-6))))
+        t = timed(eng, reps)
+        eng.close()
+        torch.cuda.empty_cache()
+        ek = CudaEngine.kfactored(insts)
+        tk = timed(ek, max(10, min(500, int(0.3 / max(t / 2, 1e-6)))))
+        ek.close()
+        torch.cuda.empty_cache()
+        rows.append({"point": name, "boards": len(insts), "stored_nnz": int(nnz), "bytes_per_pair": pair_bytes,
+                     "factored": {"us_per_pair": 1e6 * t, "pairs_per_s": 1 / t, "gb_per_s": pair_bytes / t / 1e9,
+                                  "frac_of_measured_peak": pair_bytes / t / 1e9 / peak, "reps": reps},
+                     "kfactored": {"us_per_pair": 1e6 * tk, "pairs_per_s": 1 / tk}})
+    return {"workload": "config5: matvec pairs over synthetic poker instances (Technique B post), one GPU",
+            "peak_gb_per_s": peak, "points": rows}
 
 
 def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
@@ -623,24 +854,8 @@ def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev,
     dif = float((kax - ax).abs().max().item() / (1.0 + ax.abs().max().item()))
     dif = max_over_ranks(dif)
 
-    L = N.cuda()
-    nx, ny = ek.cols, ek.rows
-    px, py, pax, patx = (L.kr_host_alloc(8 * n) for n in (nx, ny, ny, nx))
-    as_np = lambda p, n: np.ctypeslib.as_array((ctypes.c_double * n).from_address(p))  # noqa: E731
-    as_np(px, nx)[:] = x.cpu().numpy()
-    as_np(py, ny)[:] = y.cpu().numpy()
-    for _ in range(2):
-        N.check(L.kr_engine_ax(ek.handle, px, nx, pax, ny))
-        N.check(L.kr_engine_atx(ek.handle, py, ny, patx, nx))
-    e2e_steps = 50
-    barrier()
-    t = time.perf_counter()
-    for _ in range(e2e_steps):
-        N.check(L.kr_engine_ax(ek.handle, px, nx, pax, ny))
-        N.check(L.kr_engine_atx(ek.handle, py, ny, patx, nx))
-    e2e_s = max_over_ranks(time.perf_counter() - t)
-    for p in (px, py, pax, patx):
-        L.kr_host_free(p)
+    e2e = e2e_host_pairs(ek, x, y, barrier, max_over_ranks, 50)
+    e2e.pop("_ax")
 
     i0 = boards[0][0]
     solver = CudaSolver(ek, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
@@ -656,8 +871,7 @@ def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev,
     out = {"engine": "kr_engine_create_kron (k_kron_fused: one CTA per board and sequence)",
            "pairs_per_s": steps / (ms / 1e3), "us_per_pair": 1e3 * ms / steps, "steps": steps,
            "gpu_launches": launches, "normwise_diff_vs_factored": dif, "tolerance": 1e-12,
-           "e2e": {"value": e2e_steps / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": 8 * (nx + ny),
-                   "d2h_bytes_per_step": 8 * (nx + ny), "api": "kr_engine_ax / kr_engine_atx (host pinned buffers)"},
+           "e2e": e2e,
            "solver_iters_per_s": args.solver_iters / solver_s,
            "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"]}}
     solver.close()
