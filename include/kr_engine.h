@@ -320,14 +320,55 @@ int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs
 int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* p, kr_dcfr_result* r);
 int kr_turn_solver_destroy(kr_turn_solver* s);
 int64_t kr_turn_solver_launches(const kr_turn_solver* s);
-/* Board sharding over ranks: each rank's solver holds the turn block and its
- * own boards.  fn(user) is called (stream synchronised) after the river steps
- * of every half-iteration and of every best response, and must sum the turn
- * values buffer `extra` (device, sizes[2] doubles, owned by the caller from
- * now on) over the ranks in place: the one allreduce per half-iteration. */
-int kr_turn_solver_set_exchange(kr_turn_solver* s, void (*fn)(void*), void* user, double* extra);
-/* rows of player 1's vector, of player 2's, turn-values buffer length, river hands */
+/* Board sharding over ranks with a host-driven transport (e.g. a gloo
+ * process group): each rank's solver holds the turn block and its own
+ * boards.  fn(user) is called (stream synchronised) after the river steps of
+ * every half-iteration and of every best response and must all-gather the
+ * device buffer send (sizes[2] * max(boards_per_rank) doubles: this rank's
+ * per-board river values) into the device buffer recv (world times that,
+ * rank-major); both buffers stay the caller's.  The library then folds the
+ * values in global board order, exactly as on one GPU, so the solve is
+ * bitwise the one-GPU solve.  fn = NULL restores the single-rank solver. */
+int kr_turn_solver_set_exchange(kr_turn_solver* s, void (*fn)(void*), void* user, int world, int rank,
+                                const int32_t* boards_per_rank, double* send, double* recv);
+/* rows of player 1's vector, of player 2's, exchanged values per board, river hands */
 int kr_turn_solver_sizes(const kr_turn_solver* s, int64_t out[4]);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU: one rank per GPU, boards sharded contiguously over the ranks
+ * (rank r holds boards [sum boards_per_rank[<r], +boards_per_rank[r])).  The
+ * turn payoff is block diagonal over boards, so products
+ * need no communication; what crosses ranks is all-gathered and folded in
+ * global board order on every rank, the fold of the one-GPU solver, so all
+ * results are bitwise independent of the rank count.
+ * Transport: NCCL over NVLink / NVSwitch, enqueued on the solver stream and
+ * captured into its iteration graphs.
+ * ------------------------------------------------------------------------- */
+#define KR_COMM_ID_BYTES 128
+typedef struct kr_comm kr_comm;
+/* A fresh NCCL unique id (rank 0 creates it and shares it with the others). */
+int kr_comm_unique_id(uint8_t* id);
+/* One rank of an nranks communicator on CUDA device `device` (one process per
+ * GPU): every rank calls it with the same id. */
+int kr_comm_init_rank(const uint8_t* id, int nranks, int rank, int device, kr_comm** out);
+/* ndev ranks in one process, rank r on devices[r]: out[0..ndev). */
+int kr_comm_init_all(int ndev, const int* devices, kr_comm** out);
+int kr_comm_destroy(kr_comm* c);
+int kr_comm_rank(const kr_comm* c);
+int kr_comm_size(const kr_comm* c);
+
+/* The solver's boards are this rank's shard of boards_per_rank (one entry per
+ * rank of c).  From now on kr_solver_run / kr_solver_checkpoint report every
+ * board of every rank in global order (result arrays sized for the total),
+ * the exploitability averages over all boards, and checkpoint values travel
+ * by an in-stream all-gather captured into the iteration graphs.  c = NULL
+ * restores the single-rank solver. */
+int kr_solver_set_comm(kr_solver* s, kr_comm* c, const int32_t* boards_per_rank);
+
+/* Per-iteration exchange of the turn solver (its river values per turn hand,
+ * board by board) over c: all-gathered in-stream, folded in global board
+ * order (graphs stay on). */
+int kr_turn_solver_set_comm(kr_turn_solver* s, kr_comm* c, const int32_t* boards_per_rank);
 
 /* Per-kernel CUDA-event timing of the engine's SpMV launches (off by
  * default).  When enabled every SpMV launch is bracketed by events on the

@@ -102,6 +102,8 @@ CUDA_SYMBOLS = [
     "kr_turn_solver_launches", "kr_turn_solver_set_exchange", "kr_turn_solver_sizes",
     "kr_factors_build_device", "kr_devfactors_view", "kr_devfactors_seconds", "kr_devfactors_free",
     "kr_engine_create_device_b", "kr_engine_create_kfactored", "kr_engine_pair",
+    "kr_comm_unique_id", "kr_comm_init_rank", "kr_comm_init_all", "kr_comm_destroy", "kr_comm_rank", "kr_comm_size",
+    "kr_solver_set_comm", "kr_turn_solver_set_comm",
 ]
 
 
@@ -111,10 +113,26 @@ def cuda_lib_path():
     return os.path.join(_build.LIBDIR, f"libkrcuda_{v}.so" if v else "libkrcuda.so")
 
 
+def _torch_nccl():
+    """PyTorch's bundled NCCL (the copy libtorch binds), if the wheel is here."""
+    try:
+        import nvidia.nccl as m
+        for d in getattr(m, "__path__", []):
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except ImportError:
+        pass
+    return None
+
+
 def cuda():
     """Load libkrcuda.so (building it in-tree if missing)."""
     global _CUDA
     if _CUDA is None:
+        nccl = _torch_nccl()
+        if nccl:  # kr_comm dlopens NCCL on first use: share PyTorch's copy
+            os.environ.setdefault("KR_NCCL_LIB", nccl)
         path = cuda_lib_path()
         if not os.path.exists(path):
             _build.build_cuda()
@@ -166,7 +184,16 @@ def cuda():
         L.kr_turn_solver_destroy.argtypes = [C.c_void_p]
         L.kr_turn_solver_launches.restype = C.c_int64
         L.kr_turn_solver_launches.argtypes = [C.c_void_p]
-        L.kr_turn_solver_set_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kr_turn_solver_set_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p]
+        L.kr_turn_solver_set_comm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kr_solver_set_comm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kr_comm_unique_id.argtypes = [C.c_void_p]
+        L.kr_comm_init_rank.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.kr_comm_init_all.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
+        L.kr_comm_destroy.argtypes = [C.c_void_p]
+        L.kr_comm_rank.argtypes = [C.c_void_p]
+        L.kr_comm_size.argtypes = [C.c_void_p]
         L.kr_turn_solver_sizes.argtypes = [C.c_void_p, C.c_void_p]
         L.kr_engine_create_device_b.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.c_int, C.c_uint32,
                                                 C.POINTER(C.c_void_p)]

@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2112_03804_b200")
 LIBDIR = os.path.join(PKG, "lib")
-CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu", "kr_kfengine.cu")]
+CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu", "kr_kfengine.cu", "kr_comm.cu")]
 HOST_SRC = [os.path.join(PKG, "csrc", "host", f) for f in ("kr_host.cpp",)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # the system g++ links libstdc++ dynamically (a statically linked libstdc++
@@ -70,8 +70,10 @@ def build_cuda(force=False, verbose=False):
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
         list(ex.map(one, zip(srcs, objs)))
+    # NCCL is bound at run time (dlopen in kr_comm.cu), so a process shares
+    # PyTorch's copy
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", CXX, "-shared", "-cudart", "static",
-           "-o", out, *objs]
+           "-o", out, *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

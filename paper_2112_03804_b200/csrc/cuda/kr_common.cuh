@@ -185,6 +185,12 @@ int64_t kron_flops(const kr_engine* e, int dir);
 int kron_boards(const kr_engine* e);
 void kron_destroy(KronState* k);
 
+// NCCL transport (kr_comm.cu)
+void comm_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s);
+int comm_rank(const kr_comm* c);
+int comm_size(const kr_comm* c);
+int comm_device(const kr_comm* c);
+
 struct KfState;  // Kronecker-factored engine (kr_kfengine.cu)
 void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0 = 0, int b1 = -1);
 void kf_destroy(KfState* k);

@@ -59,6 +59,7 @@ constexpr int kThreads = KR_K7_THREADS;  // threads per CTA (compile-time: A/B b
 constexpr int kMaxHands = 1536;            // hands per side and board; a thread takes kMaxHands / T
 constexpr bool kKronSeqDefault = false;    // KR_KRON_SEQ, see kron_seq_major
 constexpr int64_t kSmallGrid = 148;        // K7 grids up to this many CTAs run 512-thread CTAs
+constexpr int kScanT = 256;                // block-scan chunks (fixed: bits independent of the CTA size)
 static_assert(kMaxHands % 512 == 0, "512-thread K7 CTAs");
 
 // Device view of one direction (0: A x, 1: Aᵀ y).
@@ -123,10 +124,11 @@ size_t fused_smem(int maxMS) {
 template <bool SEQ, int T>
 __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const double* __restrict__ in,
                                                          double* __restrict__ out) {
-    constexpr int kPerT = kMaxHands / T, kWarpsT = T / 32;
+    constexpr int kPerT = kMaxHands / T;
+    static_assert(T >= kScanT, "K7 CTAs hold at least the scan's threads");
     krb::pdl_entry();
     extern __shared__ double sm[];
-    __shared__ double warpV[kWarpsT], warpW[kWarpsT];
+    __shared__ double warpV[kScanT / 32], warpW[kScanT / 32];
     const int a = blockIdx.x, b = b0 + int(blockIdx.y);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t sBase = d.sumOff[b];
@@ -186,9 +188,15 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
     }
     __syncthreads();
 
-    // 2. one block scan over the virtual array (contiguous chunk per thread)
-    const int chunk = (N + T - 1) / T;
-    const int j0 = min(N, tid * chunk), j1 = min(N, j0 + chunk);
+    // 2. one block scan over the virtual array, in kScanT contiguous chunks
+    // whatever the CTA size: the summation order (and so the bits) of a
+    // board's product does not depend on the engine's launch shape, which
+    // depends on its board count (a shard of boards on one rank sums exactly
+    // as the whole turn on one GPU).  With T = 512 the upper half idles here.
+    constexpr int kWarpsS = kScanT / 32;
+    const bool scanner = tid < kScanT;
+    const int chunk = (N + kScanT - 1) / kScanT;
+    const int j0 = scanner ? min(N, tid * chunk) : N, j1 = scanner ? min(N, j0 + chunk) : N;
     double sv = 0.0, sw = 0.0;
 #pragma unroll 4
     for (int p = j0; p < j1; ++p) {
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
     }
     const double iv = warp_incl_scan(sv, lane);
     const double iw = warp_incl_scan(sw, lane);
-    if (lane == 31) {
+    if (lane == 31 && warp < kWarpsS) {
         warpV[warp] = iv;
         warpW[warp] = iw;
     }
@@ -219,40 +227,42 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
         }
     }
     __syncthreads();
-    double run = iv - sv, runQ = iw - sw;
-    for (int w = 0; w < warp; ++w) {
-        run += warpV[w];
-        runQ += warpW[w];
-    }
-    {
-        // wf prefix at the list boundaries inside [j0, j1): B_c = mSb + lptr[c]
-        int nc = 0;
+    if (scanner) {
+        double run = iv - sv, runQ = iw - sw;
+        for (int w = 0; w < warp; ++w) {
+            run += warpV[w];
+            runQ += warpW[w];
+        }
         {
-            int hi = kCards + 1;  // first c with mSb + lptr[c] >= j0
-            while (nc < hi) {
-                const int mid = (nc + hi) >> 1;
-                if (mSb + lptr[mid] < j0) nc = mid + 1; else hi = mid;
+            // wf prefix at the list boundaries inside [j0, j1): B_c = mSb + lptr[c]
+            int nc = 0;
+            {
+                int hi = kCards + 1;  // first c with mSb + lptr[c] >= j0
+                while (nc < hi) {
+                    const int mid = (nc + hi) >> 1;
+                    if (mSb + lptr[mid] < j0) nc = mid + 1; else hi = mid;
+                }
+            }
+            int p = j0;
+            for (; nc <= kCards; ++nc) {
+                const int B = mSb + lptr[nc];
+                if (B >= j1) break;
+                for (; p < B; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
+                QB[nc] = runQ;
+            }
+            if (tid == kScanT - 1) {
+                for (; p < j1; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
+                for (; nc <= kCards; ++nc) QB[nc] = runQ;  // lists ending at N
             }
         }
-        int p = j0;
-        for (; nc <= kCards; ++nc) {
-            const int B = mSb + lptr[nc];
-            if (B >= j1) break;
-            for (; p < B; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
-            QB[nc] = runQ;
-        }
-        if (tid == T - 1) {
-            for (; p < j1; ++p) runQ += W[p < mSb ? p : lhand[p - mSb]].y;
-            for (; nc <= kCards; ++nc) QB[nc] = runQ;  // lists ending at N
-        }
-    }
 #pragma unroll 4
-    for (int p = j0; p < j1; ++p) {
-        const double v = P[p];
-        P[p] = run;
-        run += v;
+        for (int p = j0; p < j1; ++p) {
+            const double v = P[p];
+            P[p] = run;
+            run += v;
+        }
+        if (tid == kScanT - 1) P[N] = run;
     }
-    if (tid == T - 1) P[N] = run;
     __syncthreads();
     if (tid < kCards) {  // per-card terms
         G[tid] = P[mSb + lptr[tid]] + P[mSb + lptr[tid + 1]];

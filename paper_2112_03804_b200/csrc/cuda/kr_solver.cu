@@ -73,6 +73,16 @@ struct kr_solver {
     double alpha = 1.5, beta = 0.0, gamma = 2.0;
     int t = 0;                  // iterations completed
     double weightSum = 0;       // solver.hpp:354, 384-387
+    // multi-GPU (kr_solver_set_comm): this rank's boards are
+    // [board0, board0 + nboards) of nbTotal; checkpoint values are
+    // all-gathered (ckSend -> ckRecv, world x 2 x nbMax) and scattered into
+    // global board order (k_ck_scatter), so traces cover every board.
+    kr_comm* comm = nullptr;
+    int world = 1, rank = 0, nbTotal = 0, nbMax = 0;
+    double* ckSend = nullptr;
+    double* ckRecv = nullptr;
+    int32_t* d_bpre = nullptr;  // [world + 1] board prefix over the ranks
+    int totalBoards() const { return comm ? nbTotal : nboards; }
 };
 
 namespace krb {
@@ -587,6 +597,21 @@ __global__ void __launch_bounds__(256) k_board_sums(const double* __restrict__ h
     if (threadIdx.x == 0) out[b] = total;
 }
 
+// The all-gathered checkpoint values (rank r: [2][nbMax], its first
+// bpre[r+1]-bpre[r] entries valid) into global board order:
+// dst[half * nbT + board], at checkpoint slot *slot when given.
+__global__ void k_ck_scatter(const double* __restrict__ recv, int world, int nbMax, const int32_t* __restrict__ bpre,
+                             double* __restrict__ dst, const int* __restrict__ slot, int64_t slotStride) {
+    krb::pdl_entry();
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= world * 2 * nbMax) return;
+    const int r = q / (2 * nbMax), rem = q - r * 2 * nbMax, half = rem / nbMax, b = rem - half * nbMax;
+    if (b >= bpre[r + 1] - bpre[r]) return;
+    const int nbT = bpre[world];
+    if (slot) dst += int64_t(*slot) * slotStride;
+    dst[int64_t(half) * nbT + bpre[r] + b] = recv[q];
+}
+
 // validateSequenceStrategy (solver.hpp:266-286): flag 1 = negative entry,
 // 2 = flow conservation violated.
 __global__ void k_validate(const int32_t* __restrict__ treeBuf, int nn, int n, int64_t H,
@@ -750,6 +775,25 @@ void best_responses(kr_solver* s, double* dst0, double* dst1, cudaStream_t st, c
     KR_CK(cudaStreamWaitEvent(st, s->evJoin, 0));
 }
 
+// One checkpoint's per-board best-response values in global board order,
+// dst[0 .. nbT) = br1 (vs avg2), dst[nbT .. 2 nbT) = br2 (vs avg1), at slot
+// *slot of stride slotStride when given.  With a communicator this rank's
+// values are all-gathered in-stream and scattered into place on every rank.
+void checkpoint_values(kr_solver* s, double* dst, cudaStream_t st, const int* slot = nullptr,
+                       int64_t slotStride = 0) {
+    if (!s->comm) {
+        best_responses(s, dst, dst + s->nboards, st, slot, slotStride);
+        return;
+    }
+    best_responses(s, s->ckSend, s->ckSend + s->nbMax, st);
+    comm_allgather(s->comm, s->ckSend, s->ckRecv, size_t(2) * s->nbMax, st);
+    const int n = s->world * 2 * s->nbMax;
+    krb::launch(k_ck_scatter, unsigned((n + 255) / 256), 256, 0, st, s->ckRecv, s->world, s->nbMax, s->d_bpre, dst,
+                slot, slotStride);
+    KR_CK_LAUNCH();
+    s->launches++;
+}
+
 // The same, copied to the host (synchronises the stream).
 void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<double>& boards, cudaStream_t st) {
     best_response_to(s, player, opp, s->boardval, st);
@@ -781,6 +825,9 @@ void destroy_solver(kr_solver* s) {
     if (s->evFork) cudaEventDestroy(s->evFork);
     if (s->evJoin) cudaEventDestroy(s->evJoin);
     cudaFree(s->d_flag);
+    cudaFree(s->ckSend);
+    cudaFree(s->ckRecv);
+    cudaFree(s->d_bpre);
     delete s;
 }
 
@@ -962,7 +1009,6 @@ namespace {
 // engine's and solver's flop / launch counters advance per replay.
 void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<int>& at, cudaStream_t st) {
     kr_engine* e = s->eng;
-    const int nb = s->nboards;
     const int t0 = s->t;
     std::vector<double> fac(size_t(3) * (maxIters + 1), 0.0), ws(size_t(maxIters) + 1, 0.0);
     double w = s->weightSum;
@@ -1007,7 +1053,7 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
             krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);             // P2
             if (withCk) {
                 normalise_averages(s, st, true);                                     // solver.hpp:390-391
-                krb::best_responses(s, dck, dck + nb, st, s->d_cnt + 1, 2 * nb);
+                krb::checkpoint_values(s, dck, st, s->d_cnt + 1, 2 * int64_t(s->totalBoards()));
                 krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 1);
                 KR_CK_LAUNCH();
                 s->launches++;
@@ -1055,6 +1101,45 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
     s->weightSum = ws[size_t(maxIters)];
 }
 }  // namespace
+
+int kr_solver_set_comm(kr_solver* s, kr_comm* c, const int32_t* boards_per_rank) {
+    return guarded([&] {
+        if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
+        KR_CK(cudaSetDevice(s->device));
+        cudaFree(s->ckSend);
+        cudaFree(s->ckRecv);
+        cudaFree(s->d_bpre);
+        s->ckSend = s->ckRecv = nullptr;
+        s->d_bpre = nullptr;
+        s->comm = nullptr;
+        s->world = 1;
+        s->rank = 0;
+        if (!c) return;
+        if (!boards_per_rank) throw Fail{KR_INVALID_INPUT, "a communicator needs the boards of every rank"};
+        const int world = krb::comm_size(c), rank = krb::comm_rank(c);
+        if (krb::comm_device(c) != s->device) throw Fail{KR_INVALID_INPUT, "communicator and solver on different devices"};
+        if (boards_per_rank[rank] != s->nboards) throw Fail{KR_INVALID_INPUT, "this rank's board count differs"};
+        std::vector<int32_t> pre(size_t(world) + 1, 0);
+        int nbMax = 0;
+        for (int r = 0; r < world; ++r) {
+            if (boards_per_rank[r] < 0) throw Fail{KR_INVALID_INPUT, "negative board count"};
+            pre[size_t(r) + 1] = pre[size_t(r)] + boards_per_rank[r];
+            nbMax = std::max(nbMax, int(boards_per_rank[r]));
+        }
+        s->world = world;
+        s->rank = rank;
+        s->nbTotal = pre[size_t(world)];
+        s->nbMax = nbMax;
+        s->ckSend = krb::dev_alloc<double>(2 * int64_t(nbMax));
+        s->ckRecv = krb::dev_alloc<double>(2 * int64_t(nbMax) * world);
+        s->d_bpre = krb::dev_alloc<int32_t>(world + 1);
+        KR_CK(cudaMemcpy(s->d_bpre, pre.data(), 4 * pre.size(), cudaMemcpyHostToDevice));
+        cudaFree(s->boardval);  // checkpoint values in global order: 2 x nbTotal
+        s->boardval = nullptr;
+        s->boardval = krb::dev_alloc<double>(2 * int64_t(std::max(s->nbTotal, s->nboards)));
+        s->comm = c;
+    });
+}
 
 int kr_solver_set_rule(kr_solver* s, int rule) {
     return guarded([&] {
@@ -1116,9 +1201,9 @@ int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2) {
         KR_CK(cudaSetDevice(s->device));
         cudaStream_t st = s->eng->stream;
         normalise_averages(s, st);                            // solver.hpp:390-391
-        const size_t nb = size_t(s->nboards);
+        const size_t nb = size_t(s->totalBoards());
         // br1 vs avg2, br2 vs avg1 (solver.hpp:327-328), side by side
-        krb::best_responses(s, s->boardval, s->boardval + nb, st);
+        krb::checkpoint_values(s, s->boardval, st);
         std::vector<double> b(2 * nb);
         KR_CK(cudaMemcpyAsync(b.data(), s->boardval, 8 * b.size(), cudaMemcpyDeviceToHost, st));
         KR_CK(cudaStreamSynchronize(st));
@@ -1166,7 +1251,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
         ck(kr_solver_set_rule(s, prm->rule));
         ck(kr_solver_begin(s, prm->alpha, prm->beta, prm->gamma));
         r->trace_len = 0;
-        const int nb = s->nboards;
+        const int nb = s->totalBoards();
         std::vector<double> b1(static_cast<size_t>(nb)), b2(static_cast<size_t>(nb));
         // Record one checkpoint's per-board values (solver.hpp:389-392; the
         // board-order sums are the chance-root average of SURVEY.md 8(d)).
@@ -1224,7 +1309,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
                         ck(kr_solver_iterate(s, next - s->t));
                         double* slot = dck + size_t(at.size()) * 2 * nb;
                         normalise_averages(s, st);                             // solver.hpp:390-391
-                        krb::best_responses(s, slot, slot + nb, st);  // br1 vs avg2, br2 vs avg1
+                        krb::checkpoint_values(s, slot, st);           // br1 vs avg2, br2 vs avg1
                         at.push_back(s->t);
                     }
                 }
@@ -1303,7 +1388,7 @@ int kr_solver_best_response(kr_solver* s, int player, const double* opp, int64_t
 //   1. river team steps per continuation (regrets, mass-1 strategies, each
 //      river hand's root value; no averaging yet);
 //   2. root values summed over the boards in ascending order per turn hand,
-//      added to the turn sequence sigma_p(t) (k_turn_gather);
+//      added to the turn sequence sigma_p(t) (k_turn_contrib, k_turn_fold);
 //   3. the turn team step, whose sweep adds those sums after the children;
 //   4. river strategies scaled by the turn reach of sigma_p(t), then
 //      averaged (k_river_scale).
@@ -1333,18 +1418,25 @@ struct kr_turn_solver {
     double pot = 0;
     int64_t launches = 0;
     int rule = 0;  // KR_RULE_*
-    // board sharding: after the river steps of a half-iteration (and of a
-    // best response) the per-turn-hand river values in `extra` cover this
-    // rank's boards only; exchange(user) must sum them over the ranks in place
-    // (the per-iteration allreduce), the stream having been synchronised.
-    void (*exchange)(void*) = nullptr;
-    void* user = nullptr;
-    bool ownExtra = true;
+    // The river values reach the turn hands board by board: contrib holds
+    // this rank's [T][m][nbMax] values (a marker where a board holds the
+    // hand), gathered every rank's (world x that, rank-major = global board
+    // order), and k_turn_fold adds them per turn hand in board order: the
+    // same fold on one GPU and on any number of ranks.  Transport: comm (NCCL,
+    // in-stream) or xfn (host callback, stream synchronised), else none.
+    kr_comm* comm = nullptr;
+    void (*xfn)(void*) = nullptr;
+    void* xuser = nullptr;
+    int world = 1, rank = 0, nbMax = 0;
+    int32_t* d_bpre = nullptr;                     // [world + 1] board prefix over the ranks
+    double* contrib = nullptr;
+    double* gathered = nullptr;                    // == contrib with one rank
+    bool ownBufs = true;                           // false: the caller's (set_exchange)
     // graph replay (one GPU, no exchange): per-iteration pos/neg/shrink from
     // a device table indexed by the device iteration counter
     double* d_fac = nullptr;
     int* d_cnt = nullptr;
-    int32_t* d_sigma = nullptr;                    // [2][T] sigma_p(t), for k_turn_gather_all
+    int32_t* d_sigma = nullptr;                    // [2][T] sigma_p(t), for k_turn_fold
     int64_t* d_roff = nullptr;                     // [2][T+1] river block offsets (from off[p][1])
     int32_t* d_nr = nullptr;                       // [2][T] river sequences per continuation
     // the continuations' independent river products and player steps run
@@ -1358,58 +1450,50 @@ struct kr_turn_solver {
 namespace krb {
 namespace {
 
-__global__ void k_turn_gather(const double* __restrict__ root, const int32_t* __restrict__ t2r,
-                              const int64_t* __restrict__ boff, int nb, int m, int nt, int sigma,
-                              double* __restrict__ extra) {
+constexpr uint64_t kSkipBits = 0x7ff8000000000001ULL;  // NaN marker: the board holds the hand
+
+// This rank's river root values per (continuation t, turn hand h, local
+// board b): contrib[(t m + h) nbMax + b], the marker where board b holds h
+// (or past this rank's boards).
+__global__ void k_turn_contrib(const double* __restrict__ root, int64_t Hr, const int32_t* __restrict__ t2r,
+                               const int64_t* __restrict__ boff, int nb, int m, int T, int nbMax,
+                               double* __restrict__ contrib) {
+    krb::pdl_entry();
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= int64_t(T) * m * nbMax) return;
+    const int b = int(q % nbMax);
+    const int64_t th = q / nbMax;
+    const int h = int(th % m), t = int(th / m);
+    double v = __longlong_as_double((long long)kSkipBits);
+    if (b < nb) {
+        const int r = t2r[int64_t(b) * m + h];
+        if (r >= 0) v = root[int64_t(t) * Hr + boff[b] + r];
+    }
+    contrib[q] = v;
+}
+
+// Per turn hand h and continuation t in order: extra[h, sigma(t)] += the sum
+// over all boards in global order (rank-major, each rank's boards ascending;
+// boards holding h skipped) -- one left fold, the same on one GPU and on any
+// number of ranks.
+__global__ void k_turn_fold(const double* __restrict__ gathered, int world, int nbMax,
+                            const int32_t* __restrict__ bpre, int T, int m, int nt, const int32_t* __restrict__ sigma,
+                            double* __restrict__ extra) {
     krb::pdl_entry();
     const int h = blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= m) return;
-    double acc = 0.0;
-    for (int b = 0; b < nb; ++b) {
-        const int r = t2r[int64_t(b) * m + h];
-        if (r >= 0) acc += root[boff[b] + r];
-    }
-    extra[int64_t(h) * nt + sigma - 1] += acc;
-}
-
-// All continuations' river root values summed into the turn hands at once:
-// for t = 0..T-1 in order, extra[h, sigma(t)] += sum over boards b ascending
-// of root[t][boff[b] + t2r[b][h]] (boards holding h skipped) -- the bits of
-// T k_turn_gather launches.  A block stages the (board, hand) values of 32
-// turn hands in shared memory with 8 independent loads per thread, then one
-// thread per hand adds them in board order (a thread walking its 48 boards
-// alone waited out ~96 dependent memory latencies).
-constexpr int kGatherHands = 32;
-__global__ void __launch_bounds__(256) k_turn_gather_all(const double* __restrict__ root, int64_t Hr,
-                                                         const int32_t* __restrict__ t2r,
-                                                         const int64_t* __restrict__ boff, int nb, int m, int nt,
-                                                         const int32_t* __restrict__ sigma, int T,
-                                                         double* __restrict__ extra) {
-    krb::pdl_entry();
-    extern __shared__ double gv[];  // [nb][kGatherHands] values, NaN = board holds the hand
-    const int h0 = blockIdx.x * kGatherHands;
-    const int nh = min(kGatherHands, m - h0);
+    const int64_t per = int64_t(T) * m * nbMax;
     for (int t = 0; t < T; ++t) {
-        const double* rt = root + int64_t(t) * Hr;
-        for (int q = threadIdx.x; q < nb * kGatherHands; q += blockDim.x) {
-            const int b = q / kGatherHands, hh = q % kGatherHands;
-            double v = __longlong_as_double(0x7ff8000000000001LL);  // marker: skipped
-            if (hh < nh) {
-                const int r = t2r[int64_t(b) * m + h0 + hh];
-                if (r >= 0) v = rt[boff[b] + r];
+        double acc = 0.0;
+        for (int r = 0; r < world; ++r) {
+            const double* g = gathered + r * per + (int64_t(t) * m + h) * nbMax;
+            const int nbr = bpre[r + 1] - bpre[r];
+            for (int b = 0; b < nbr; ++b) {
+                const double v = g[b];
+                if (uint64_t(__double_as_longlong(v)) != kSkipBits) acc += v;
             }
-            gv[q] = v;
         }
-        __syncthreads();
-        if (threadIdx.x < nh) {
-            double acc = 0.0;
-            for (int b = 0; b < nb; ++b) {
-                const double v = gv[b * kGatherHands + threadIdx.x];
-                if (__double_as_longlong(v) != 0x7ff8000000000001LL) acc += v;
-            }
-            extra[int64_t(h0 + threadIdx.x) * nt + sigma[t] - 1] += acc;
-        }
-        __syncthreads();
+        extra[int64_t(h) * nt + sigma[t] - 1] += acc;
     }
 }
 
@@ -1501,27 +1585,30 @@ void join(kr_turn_solver* s, cudaStream_t st) {
     }
 }
 
-// KR_TURN_FUSE=0: one gather and one scale launch per continuation instead
-// of one for all of them (the same bits).
+// KR_TURN_FUSE=0: one river-scale launch per continuation instead of one for
+// all of them (the same bits).
 bool turn_fuse() {
     const char* env = std::getenv("KR_TURN_FUSE");
     return !(env && std::atoi(env) == 0);
 }
 
-// The river root values of every continuation into `extra` (one launch).
+// The river root values of every continuation into `extra`: this rank's
+// per-board values, exchanged over the ranks (all-gather), folded in global
+// board order.
 void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
-    if (!turn_fuse()) {
-        for (int t = 0; t < s->T; ++t) {
-            krb::launch(k_turn_gather, unsigned((s->m + 127) / 128), 128, 0, st, s->root + int64_t(t) * s->Hr, s->d_t2r,
-                                                                         s->d_boff, s->nb, s->m, nt,
-                                                                         s->sigma[p][size_t(t)], s->extra);
-            KR_CK_LAUNCH();
-            s->launches++;
-        }
-        return;
+    const int64_t count = int64_t(s->T) * s->m * s->nbMax;
+    krb::launch(k_turn_contrib, unsigned((count + 255) / 256), 256, 0, st, s->root, s->Hr, s->d_t2r, s->d_boff, s->nb,
+                s->m, s->T, s->nbMax, s->contrib);
+    KR_CK_LAUNCH();
+    s->launches++;
+    if (s->comm) {
+        comm_allgather(s->comm, s->contrib, s->gathered, size_t(count), st);
+    } else if (s->xfn) {
+        KR_CK(cudaStreamSynchronize(st));
+        s->xfn(s->xuser);  // all-gathers contrib into gathered (the caller's buffers)
     }
-    const size_t smem = size_t(s->nb) * kGatherHands * sizeof(double);
-    krb::launch(k_turn_gather_all, unsigned((s->m + kGatherHands - 1) / kGatherHands), 256, smem, st, s->root, s->Hr, s->d_t2r, s->d_boff, s->nb, s->m, nt, s->d_sigma + p * s->T, s->T, s->extra);
+    krb::launch(k_turn_fold, unsigned((s->m + 127) / 128), 128, 0, st, s->gathered, s->world, s->nbMax, s->d_bpre,
+                s->T, s->m, nt, s->d_sigma + p * s->T, s->extra);
     KR_CK_LAUNCH();
     s->launches++;
 }
@@ -1541,10 +1628,6 @@ void turn_player(kr_turn_solver* s, int p, int mode, double pos, double neg, dou
     }
     join(s, st);
     if (mode == 1) gather_all(s, p, nt, st);
-    if (mode == 1 && s->exchange) {
-        KR_CK(cudaStreamSynchronize(st));
-        s->exchange(s->user);
-    }
     team_step(s, s->turnTree[p], s->m, mode, s->g, p == 1, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, 0,
               nullptr, mode == 1 ? s->extra : nullptr, st, fac, dt);
     if (turn_fuse()) {
@@ -1597,10 +1680,6 @@ double turn_br(kr_turn_solver* s, int p, const double* opp, cudaStream_t st) {
         br(s->riverTree[p][size_t(t)], s->Hr, s->g + s->off[p][size_t(t) + 1], s->root + int64_t(t) * s->Hr,
            nullptr);
     gather_all(s, p, nt, st);
-    if (s->exchange) {
-        KR_CK(cudaStreamSynchronize(st));
-        s->exchange(s->user);
-    }
     br(s->turnTree[p], s->m, s->g, s->handval, s->extra);
     krb::launch(k_board_sums, 1, 256, 0, st, s->handval, s->d_one, 1, s->bval, nullptr, 0);
     KR_CK_LAUNCH();
@@ -1622,10 +1701,13 @@ void destroy_turn(kr_turn_solver* s) {
         cudaFree(s->x[p]);
         cudaFree(s->a[p]);
     }
-    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g,     s->root,  s->handval,
-                  s->bval,   s->d_one, s->d_fac, s->d_cnt, s->d_sigma, s->d_roff, s->d_nr};
+    if (s->ownBufs) {
+        if (s->gathered != s->contrib) cudaFree(s->gathered);
+        cudaFree(s->contrib);
+    }
+    void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g,     s->root,  s->handval, s->bval,
+                  s->d_one,  s->d_fac, s->d_cnt, s->d_sigma, s->d_roff, s->d_nr, s->d_bpre, s->extra};
     for (void* q : ps) cudaFree(q);
-    if (s->ownExtra) cudaFree(s->extra);
     for (cudaStream_t q : s->side) cudaStreamDestroy(q);
     for (cudaEvent_t ev : s->evJoin) cudaEventDestroy(ev);
     if (s->evFork) cudaEventDestroy(s->evFork);
@@ -1727,7 +1809,6 @@ int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs
                 s->d_nr = krb::dev_alloc<int32_t>(int64_t(nr.size()));
                 KR_CK(cudaMemcpy(s->d_roff, ro.data(), 8 * ro.size(), cudaMemcpyHostToDevice));
                 KR_CK(cudaMemcpy(s->d_nr, nr.data(), 4 * nr.size(), cudaMemcpyHostToDevice));
-                krb::raise_smem_limit(krb::k_turn_gather_all, size_t(nb) * krb::kGatherHands * sizeof(double));
             }
             if (T > 1 && !std::getenv("KR_TURN_SERIAL")) {
                 s->side.resize(size_t(T));
@@ -1739,6 +1820,14 @@ int kr_turn_solver_create(kr_engine* turnEng, int T, kr_engine* const* riverEngs
                 KR_CK(cudaEventCreateWithFlags(&s->evFork, cudaEventDisableTiming));
             }
             s->extra = krb::dev_alloc<double>(int64_t(m) * std::max(turnTrees[0].n_seq, turnTrees[1].n_seq));
+            {   // one rank until kr_turn_solver_set_comm / _set_exchange
+                s->nbMax = std::max(nb, 1);
+                s->contrib = krb::dev_alloc<double>(std::max<int64_t>(int64_t(T) * m * s->nbMax, 1));
+                s->gathered = s->contrib;
+                const int32_t pre[2] = {0, nb};
+                s->d_bpre = krb::dev_alloc<int32_t>(2);
+                KR_CK(cudaMemcpy(s->d_bpre, pre, 8, cudaMemcpyHostToDevice));
+            }
             s->handval = krb::dev_alloc<double>(std::max<int64_t>(m, s->Hr));
             s->bval = krb::dev_alloc<double>(1);
             const int64_t one[2] = {0, m};
@@ -1788,13 +1877,14 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         krb::turn_player(s, 1, 0, 0, 0, 0, st);
         double ws = 0;
         r->trace_len = 0;
-        // One GPU (no exchange hook): every iteration replays one captured
-        // graph (tick, both gradients and player steps), its factors read
+        // Without a host exchange (one GPU, or NCCL ranks: the all-gathers are
+        // captured in-stream) every iteration replays one captured graph
+        // (tick, both gradients and player steps), its factors read
         // from a device table filled with the loop's own expressions, so a
         // replay is bitwise the launched iteration.  Checkpoints stay on the
         // host path (their values are read back).  KR_NO_GRAPH: launch by launch.
         int64_t launchDelta = 0;
-        if (!s->exchange && !std::getenv("KR_NO_GRAPH")) {
+        if (!s->xfn && !std::getenv("KR_NO_GRAPH")) {
             std::vector<double> fac(size_t(3) * (prm->max_iters + 1), 0.0);
             for (int t = 1; t <= prm->max_iters; ++t) {
                 fac[3 * size_t(t)] = krb::discount_factor(t, prm->alpha);
@@ -1881,17 +1971,80 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
 
 int64_t kr_turn_solver_launches(const kr_turn_solver* s) { return s ? s->launches : 0; }
 
-int kr_turn_solver_set_exchange(kr_turn_solver* s, void (*fn)(void*), void* user, double* extra) {
+namespace {
+// Shard layout of a turn solver: world ranks, boards_per_rank, the
+// contribution / gathered buffers sized for the largest shard.
+void turn_shards(kr_turn_solver* s, int world, int rank, const int32_t* bpr, double* send = nullptr,
+                 double* recv = nullptr) {
+    if (world < 1 || rank < 0 || rank >= world) throw Fail{KR_INVALID_INPUT, "bad rank / size"};
+    std::vector<int32_t> pre(size_t(world) + 1, 0);
+    int nbMax = 0;
+    for (int r = 0; r < world; ++r) {
+        const int n = bpr ? bpr[r] : s->nb;
+        if (n < 0) throw Fail{KR_INVALID_INPUT, "negative board count"};
+        pre[size_t(r) + 1] = pre[size_t(r)] + n;
+        nbMax = std::max(nbMax, n);
+    }
+    if ((bpr ? bpr[rank] : s->nb) != s->nb) throw Fail{KR_INVALID_INPUT, "this rank's board count differs"};
+    KR_CK(cudaSetDevice(s->device));
+    KR_CK(cudaDeviceSynchronize());
+    if (s->ownBufs) {
+        if (s->gathered != s->contrib) cudaFree(s->gathered);
+        cudaFree(s->contrib);
+    }
+    cudaFree(s->d_bpre);
+    s->contrib = s->gathered = nullptr;
+    s->d_bpre = nullptr;
+    s->world = world;
+    s->rank = rank;
+    s->nbMax = std::max(nbMax, 1);
+    const int64_t count = int64_t(s->T) * s->m * s->nbMax;
+    if (send) {
+        s->contrib = send;
+        s->gathered = recv;
+        s->ownBufs = false;
+    } else {
+        s->contrib = krb::dev_alloc<double>(std::max<int64_t>(count, 1));
+        s->gathered = world == 1 ? s->contrib : krb::dev_alloc<double>(std::max<int64_t>(count * world, 1));
+        s->ownBufs = true;
+    }
+    s->d_bpre = krb::dev_alloc<int32_t>(world + 1);
+    KR_CK(cudaMemcpy(s->d_bpre, pre.data(), 4 * pre.size(), cudaMemcpyHostToDevice));
+}
+}  // namespace
+
+int kr_turn_solver_set_exchange(kr_turn_solver* s, void (*fn)(void*), void* user, int world, int rank,
+                                const int32_t* boards_per_rank, double* send, double* recv) {
     return guarded([&] {
         if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
-        if (fn && !extra) throw Fail{KR_INVALID_INPUT, "an exchange needs the caller's turn-values buffer"};
-        if (extra) {
-            if (s->ownExtra) cudaFree(s->extra);
-            s->extra = extra;
-            s->ownExtra = false;
+        if (fn && (!boards_per_rank || !send || !recv))
+            throw Fail{KR_INVALID_INPUT, "an exchange needs the boards of every rank and its two buffers"};
+        s->comm = nullptr;
+        s->xfn = nullptr;
+        s->xuser = nullptr;
+        if (!fn) {
+            turn_shards(s, 1, 0, nullptr);
+            return;
         }
-        s->exchange = fn;
-        s->user = user;
+        turn_shards(s, world, rank, boards_per_rank, send, recv);
+        s->xfn = fn;
+        s->xuser = user;
+    });
+}
+
+int kr_turn_solver_set_comm(kr_turn_solver* s, kr_comm* c, const int32_t* boards_per_rank) {
+    return guarded([&] {
+        if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
+        s->comm = nullptr;
+        s->xfn = nullptr;
+        if (!c) {
+            turn_shards(s, 1, 0, nullptr);
+            return;
+        }
+        if (!boards_per_rank) throw Fail{KR_INVALID_INPUT, "a communicator needs the boards of every rank"};
+        if (krb::comm_device(c) != s->device) throw Fail{KR_INVALID_INPUT, "communicator and solver on different devices"};
+        turn_shards(s, krb::comm_size(c), krb::comm_rank(c), boards_per_rank);
+        s->comm = c;
     });
 }
 
@@ -1900,7 +2053,7 @@ int kr_turn_solver_sizes(const kr_turn_solver* s, int64_t out[4]) {
         if (!s || !out) throw Fail{KR_INVALID_INPUT, "null argument"};
         out[0] = s->off[0].back();
         out[1] = s->off[1].back();
-        out[2] = int64_t(s->m) * std::max(s->turnTree[0].n, s->turnTree[1].n);  // turn-values buffer
+        out[2] = int64_t(s->T) * s->m;  // exchanged values per board (kr_turn_solver_set_exchange)
         out[3] = s->Hr;
     });
 }

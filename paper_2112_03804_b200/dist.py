@@ -9,8 +9,11 @@ in board order on every rank, so the exploitability trace — and hence the
 early-stop decision — is bitwise identical for any number of ranks (an
 all-reduce would reorder the sum with the world size).
 
-One process per GPU (torchrun); the process group is NCCL on GPUs, gloo in
-the CPU tests (tests/test_dist_gloo.py).
+One process per GPU (torchrun).  On GPUs the transport is the library's own
+NCCL communicator (kr_comm, `Comm` below): the per-board values are
+all-gathered in-stream by libkrcuda and folded there, inside the solver's
+captured iteration graphs.  A host process group (gloo: the CPU tests, and a
+multi-rank smoke on a one-GPU box) drives the same all-gather from Python.
 """
 from __future__ import annotations
 
@@ -25,6 +28,86 @@ def shard(nboards, rank, world):
     base, extra = divmod(nboards, world)
     start = rank * base + min(rank, extra)
     return range(start, start + base + (1 if rank < extra else 0))
+
+
+def boards_per_rank(nboards, world):
+    return np.ascontiguousarray([len(shard(nboards, r, world)) for r in range(world)], np.int32)
+
+
+class Comm:
+    """kr_comm: an NCCL communicator owned by libkrcuda, one rank per GPU
+    (kr_comm_init_rank from a unique id shared over a torch process group,
+    or kr_comm_init_all over a device list in one process)."""
+
+    ID_BYTES = 128
+
+    def __init__(self, handle, device):
+        from . import _native as N
+        self._h = handle
+        self.device = device
+        self.rank = int(N.cuda().kr_comm_rank(handle))
+        self.size = int(N.cuda().kr_comm_size(handle))
+
+    @classmethod
+    def from_process_group(cls, device, group=None):
+        """Every rank of `group` calls this; rank 0's unique id travels over
+        the group (one broadcast), then NCCL takes over."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _native as N
+        L = N.cuda()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_uint8 * cls.ID_BYTES)()
+        if rank == 0:
+            N.check(L.kr_comm_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_uint8 * cls.ID_BYTES).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        N.check(L.kr_comm_init_rank(uid, world, rank, device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def single(cls, device=0):
+        """A one-rank communicator (the NCCL path on one GPU)."""
+        import ctypes as C
+
+        from . import _native as N
+        L = N.cuda()
+        uid = (C.c_uint8 * cls.ID_BYTES)()
+        N.check(L.kr_comm_unique_id(uid))
+        h = C.c_void_p()
+        N.check(L.kr_comm_init_rank(uid, 1, 0, device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def init_all(cls, devices):
+        """One communicator per device, all in this process."""
+        import ctypes as C
+
+        from . import _native as N
+        devs = np.ascontiguousarray(devices, np.int32)
+        hs = (C.c_void_p * len(devs))()
+        N.check(N.cuda().kr_comm_init_all(len(devs), N.ptr(devs), hs))
+        return [cls(C.c_void_p(hs[i]), int(devs[i])) for i in range(len(devs))]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        from . import _native as N
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.cuda().kr_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def gather_boards(local, nboards, world, group=None, device=None):
@@ -69,6 +152,14 @@ class DistributedDcfr:
         if max_iters < 1 or checkpoint_every < 1:
             raise ValueError("iteration budget and checkpoint period must be positive")
         from .solver import CudaSolver, DcfrParams
+        if isinstance(self.local, CudaSolver) and self.local.comm is not None:
+            # the library's NCCL path: kr_solver_run with the checkpoint
+            # all-gathers in-stream, iterations replayed as graphs
+            r = self.local.run(DcfrParams(alpha=alpha, beta=beta, gamma=gamma, max_iters=max_iters,
+                                          target_exploitability=target, checkpoint_every=checkpoint_every,
+                                          rule=rule), want_avg=False)
+            return {"iterations": r.iterations, "exploitability": r.exploitability, "trace_iter": r.trace_iter,
+                    "trace_expl": r.trace_expl, "board_br1": r.board_br1, "board_br2": r.board_br2}
         if isinstance(self.local, CudaSolver):
             self.local.begin(DcfrParams(alpha=alpha, beta=beta, gamma=gamma, rule=rule))
         else:  # the oracle's DcfrBoards (CPU tests)

@@ -105,6 +105,8 @@ class CudaSolver:
         self._h = h
         self.engine = engine  # keep alive: the solver borrows the engine (solver.hpp:32 ownership rule)
         self.nboards = len(h1)
+        self.nb_out = self.nboards   # boards reported per checkpoint (all ranks' with a comm)
+        self.comm = None
         self.pot = float(pot)
         self.rows, self.cols = engine.rows, engine.cols
 
@@ -122,12 +124,22 @@ class CudaSolver:
     def launches(self):
         return int(N.cuda().kr_solver_launches(self._h))
 
+    def set_comm(self, comm, boards_per_rank):
+        """kr_solver_set_comm: this solver's boards are `comm.rank`'s shard of
+        boards_per_rank; runs and checkpoints then report every board in
+        global order, checkpoint values all-gathered over NCCL in-stream."""
+        bpr = np.ascontiguousarray(boards_per_rank, np.int32)
+        N.check(N.cuda().kr_solver_set_comm(self._h, comm.handle if comm else None, N.ptr(bpr) if comm else None))
+        self.comm = comm
+        self.nb_out = int(bpr.sum()) if comm else self.nboards
+
     def run(self, params: DcfrParams = None, want_avg=True) -> DcfrResult:
         p = params or DcfrParams()
         cap = max(p.max_iters, 0) // max(p.checkpoint_every, 1) + 2  # the C ABI validates the params
         ti = np.zeros(cap, np.int32)
         te, b1, b2 = np.zeros(cap), np.zeros(cap), np.zeros(cap)
-        bb1, bb2 = np.zeros(cap * self.nboards), np.zeros(cap * self.nboards)
+        nb = self.nb_out
+        bb1, bb2 = np.zeros(cap * nb), np.zeros(cap * nb)
         a1 = np.zeros(self.rows) if want_avg else None
         a2 = np.zeros(self.cols) if want_avg else None
         prm = N.kr_dcfr_params(p.alpha, p.beta, p.gamma, p.max_iters, p.target_exploitability, p.checkpoint_every,
@@ -138,8 +150,7 @@ class CudaSolver:
         N.check(N.cuda().kr_solver_run(self._h, C.byref(prm), C.byref(res)))
         n = min(res.trace_len, cap)
         return DcfrResult(res.iterations, res.exploitability, res.gradient_flops, ti[:n], te[:n], b1[:n], b2[:n],
-                          bb1[:n * self.nboards].reshape(n, self.nboards),
-                          bb2[:n * self.nboards].reshape(n, self.nboards), a1, a2, res.seconds,
+                          bb1[:n * nb].reshape(n, nb), bb2[:n * nb].reshape(n, nb), a1, a2, res.seconds,
                           self.launches() + self.engine.launches() - launches0)
 
     # -- incremental interface (multi-rank drivers, dist.py) ----------------
@@ -153,7 +164,7 @@ class CudaSolver:
 
     def checkpoint(self):
         """Per-board best-response values (br1, br2) of the current averages."""
-        b1, b2 = np.zeros(self.nboards), np.zeros(self.nboards)
+        b1, b2 = np.zeros(self.nb_out), np.zeros(self.nb_out)
         N.check(N.cuda().kr_solver_checkpoint(self._h, N.ptr(b1), N.ptr(b2)))
         return b1, b2
 

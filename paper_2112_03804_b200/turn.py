@@ -201,11 +201,12 @@ class TurnSolver:
     engines for the turn block and each continuation's river boards, the
     turn treeplex composed with the river treeplexes."""
 
-    def __init__(self, game: TurnGame, device=0, group=None):
-        """group: a torch.distributed process group over the ranks holding the
-        other board shards (each rank builds its TurnGame with boards=shard):
-        the per-turn-hand river values are all-reduced once per
-        half-iteration."""
+    def __init__(self, game: TurnGame, device=0, group=None, comm=None, boards_per_rank=None):
+        """Board sharding (each rank builds its TurnGame with boards=shard):
+        comm, a dist.Comm (NCCL in-stream, graph-captured), or group, a host
+        torch.distributed process group (gloo), carries the per-board river
+        values of every half-iteration; the library folds them in global board
+        order, so the solve is bitwise the one-rank solve (see shard())."""
         import ctypes as C
 
         from . import _native as N
@@ -232,27 +233,62 @@ class TurnSolver:
                                                len(game.rivers), N.ptr(mb), N.ptr(r2t), N.ptr(sig), 2 * game.pot,
                                                C.byref(h)))
         self._h = h
-        if group is not None:
-            import torch
-            import torch.distributed as dist
-            sz = np.zeros(4, np.int64)
-            N.check(N.cuda().kr_turn_solver_sizes(self._h, N.ptr(sz)))
-            self.extra = torch.zeros(int(sz[2]), dtype=torch.float64, device=torch.device("cuda", device))
+        self.comm = None
+        if group is not None or comm is not None:
+            self.shard(group=group, comm=comm, boards_per_rank=boards_per_rank)
 
-            def exchange(_user):
-                dist.all_reduce(self.extra, group=group)
-                torch.cuda.synchronize(self.extra.device)
+    def shard(self, group=None, comm=None, boards_per_rank=None):
+        """Attach the board-sharding transport.  boards_per_rank defaults to
+        this rank's board count gathered over the group."""
+        import ctypes as C
 
-            self._cb = C.CFUNCTYPE(None, C.c_void_p)(exchange)
-            N.check(N.cuda().kr_turn_solver_set_exchange(self._h, C.cast(self._cb, C.c_void_p), None,
-                                                         C.c_void_p(self.extra.data_ptr())))
+        import torch
+
+        from . import _native as N
+        L = N.cuda()
+        nb = len(self.game.rivers)
+        if comm is not None:
+            if boards_per_rank is None:
+                raise ValueError("an NCCL communicator needs boards_per_rank")
+            bpr = np.ascontiguousarray(boards_per_rank, np.int32)
+            N.check(L.kr_turn_solver_set_comm(self._h, comm.handle, N.ptr(bpr)))
+            self.comm = comm
+            return
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if boards_per_rank is None:
+            counts = [None] * world
+            dist.all_gather_object(counts, nb, group=group)
+            boards_per_rank = counts
+        bpr = np.ascontiguousarray(boards_per_rank, np.int32)
+        sz = np.zeros(4, np.int64)
+        N.check(L.kr_turn_solver_sizes(self._h, N.ptr(sz)))
+        count = int(sz[2]) * int(bpr.max())
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.send = torch.zeros(count, dtype=torch.float64, device=dev)
+        self.recv = torch.zeros(world * count, dtype=torch.float64, device=dev)
+        host = dist.get_backend(group) != "nccl"
+
+        def exchange(_user):
+            if host:  # gloo: through host memory
+                src = self.send.cpu()
+                parts = [torch.empty_like(src) for _ in range(world)]
+                dist.all_gather(parts, src, group=group)
+                self.recv.copy_(torch.cat(parts))
+            else:
+                dist.all_gather_into_tensor(self.recv, self.send, group=group)
+            torch.cuda.synchronize(dev)
+
+        self._cb = C.CFUNCTYPE(None, C.c_void_p)(exchange)
+        N.check(L.kr_turn_solver_set_exchange(self._h, C.cast(self._cb, C.c_void_p), None, world, rank, N.ptr(bpr),
+                                              C.c_void_p(self.send.data_ptr()), C.c_void_p(self.recv.data_ptr())))
 
     def close(self):
         from . import _native as N
         if getattr(self, "_h", None) and self._h.value:
             N.cuda().kr_turn_solver_destroy(self._h)
             self._h = None
-        self.extra = None
+        self.send = self.recv = None
 
     def __del__(self):
         try:

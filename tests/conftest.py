@@ -15,6 +15,7 @@ REFERENCE = "/root/reference/proj"
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (runs on the B200 box)")
+    config.addinivalue_line("markers", "multigpu: needs two or more CUDA devices (skips otherwise)")
 
 
 @pytest.fixture(scope="session")

@@ -1,6 +1,4 @@
 # ad-hoc GPU batch (edited per call)
-T=r02m
-timeout 1200 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
-timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${T}_bench_ref.json 2> gpurun_out/${T}_bench_ref.err; echo "ref rc=$?"
-KR_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 20 --warmup 3 > gpurun_out/${T}_bench_n2_gloo.json 2> gpurun_out/${T}_bench_n2_gloo.err; echo "n2 rc=$?"
-tail -c 600 gpurun_out/${T}_bench.err; tail -c 300 gpurun_out/${T}_bench_n2_gloo.err
+T=r02n
+timeout 1500 python -m pytest tests/test_gpu_multigpu.py tests/test_gpu_turn.py tests/test_gpu_kron.py tests/test_gpu_solver.py tests/test_gpu_kron_seq.py -q -x -p no:cacheprovider > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
+tail -n 30 gpurun_out/${T}_pytest.log
