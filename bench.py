@@ -176,16 +176,19 @@ def oracle_boards(indices, threads, with_instances=False):
         return list(ex.map(one, indices))
 
 
-def run_turn(rank, world, local, max_over_ranks, group):
+def run_turn(rank, world, local, max_over_ranks, group, comm=None):
     """Turn endgame: the 52-card turn
     Ks7d4c2h with a betting round (menus {0.5}, no raise) above its 48 river
     boards (menus {0.5, 1.0}, one raise), 1,128 hands per side; boards sharded
     over the ranks, one allreduce of the turn values per half-iteration."""
-    from paper_2112_03804_b200.dist import shard
+    from paper_2112_03804_b200.dist import boards_per_rank, shard
     from paper_2112_03804_b200.turn import TurnGame, TurnSolver
     t0 = time.time()
     g = TurnGame(turn=TURN, deck=52, boards=list(shard(NBOARDS, rank, world)))
-    s = TurnSolver(g, device=local, group=group if world > 1 else None)
+    if comm is not None:  # NCCL in-stream, graph-captured
+        s = TurnSolver(g, device=local, comm=comm, boards_per_rank=boards_per_rank(NBOARDS, world))
+    else:
+        s = TurnSolver(g, device=local, group=group if world > 1 else None)
     setup = time.time() - t0
     s.run(max_iters=3, checkpoint_every=3)  # warm
     r = s.run(max_iters=200, checkpoint_every=50)
@@ -195,8 +198,10 @@ def run_turn(rank, world, local, max_over_ranks, group):
             "sequences_per_player_this_rank": int(g.size[0]),
             "iterations": r["iterations"], "device_seconds": secs, "iters_per_s": r["iterations"] / secs,
             "exploitability": r["exploitability"], "setup_s": round(setup, 2),
-            "collective": "one allreduce (m x n_turn doubles) per half-iteration and per best response"
-            if world > 1 else "none (one GPU)"}
+            "collective": ("one all-gather of the per-board river values (T x m x boards doubles) per "
+                           "half-iteration and per best response, folded in board order "
+                           + ("(libkrcuda NCCL, in-stream, graph-captured)" if comm is not None else
+                              "(host process group)")) if world > 1 else "none (one GPU)"}
 
 
 def config1_gpu():
@@ -450,6 +455,13 @@ def run_product(args):
             dist.init_process_group(backend, rank=rank, world_size=world)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    # The library's own NCCL communicator carries the solvers' exchanges
+    # (checkpoint values, turn river values) in-stream; with a host backend
+    # (KR_DIST_BACKEND=gloo: several ranks on one GPU) the same all-gathers
+    # go through the process group.
+    from paper_2112_03804_b200.dist import Comm, boards_per_rank
+    comm = Comm.from_process_group(local) if world > 1 and backend == "nccl" else None
+    bpr = boards_per_rank(args.boards, world)
 
     def barrier():
         if world > 1:
@@ -543,6 +555,8 @@ def run_product(args):
     i0 = boards[0][0]
     solver = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
                         i0.pot)
+    if comm is not None:
+        solver.set_comm(comm, bpr)
     drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=coll_dev)
     drv.run(max_iters=5, checkpoint_every=5)  # warm
     barrier()
@@ -554,11 +568,11 @@ def run_product(args):
 
     # ---- Kronecker-factored engine (bitwise, nothing streamed) -------------
     kfac = run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, coll_dev, barrier,
-                         max_over_ranks, sum_over_ranks, res)
+                         max_over_ranks, sum_over_ranks, res, comm, bpr)
     # ---- implicit Kronecker engine (K7) -------------
     implicit = run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
-                            sum_over_ranks)
-    turn = run_turn(rank, world, local, max_over_ranks, dist.group.WORLD if world > 1 else None)
+                            sum_over_ranks, comm, bpr)
+    turn = run_turn(rank, world, local, max_over_ranks, dist.group.WORLD if world > 1 else None, comm)
     config1 = config1_gpu() if rank == 0 else None
     config2 = config2_gpu(measured_peak()[0]) if rank == 0 else None
     gpu_out = None
@@ -575,6 +589,8 @@ def run_product(args):
     sweep = run_sweep() if rank == 0 and world == 1 and not args.no_sweep else None
 
     if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
         return 0
     peak, peak_src = measured_peak()
     kd = ktimes[dominant]
@@ -604,6 +620,10 @@ def run_product(args):
         "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"],
                    "checkpoint_every": 50},
         "gpu_launches": gpu_launches,
+        "multi_gpu": {"ranks": world, "boards_per_rank": [int(v) for v in bpr],
+                      "transport": ("libkrcuda kr_comm (NCCL): checkpoint values and turn values all-gathered "
+                                    "in-stream, folded in board order (bitwise N-invariant)") if comm is not None else
+                      ("host process group (" + backend + ")" if world > 1 else "none")},
         "clocks": sampler.summary(),
         "kfactored": kfac,
         "implicit": implicit,
@@ -666,7 +686,7 @@ def e2e_host_pairs(eng, x, y, barrier, max_over_ranks, steps):
 
 
 def run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
-                  sum_over_ranks, ref_solve):
+                  sum_over_ranks, ref_solve, comm=None, bpr=None):
     """The same pairs through the Kronecker-factored engine (Technique B post
     kept as its hand-space factors, every Kronecker product expanded on the
     fly: kr_kfengine.cu), which is BITWISE the factored engine: device
@@ -714,6 +734,8 @@ def run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, col
     i0 = boards[0][0]
     solver = CudaSolver(ek, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
                         i0.pot)
+    if comm is not None:
+        solver.set_comm(comm, bpr)
     drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=coll_dev)
     drv.run(max_iters=5, checkpoint_every=5)
     barrier()
@@ -813,7 +835,7 @@ def run_sweep(budget_s=40.0):
 
 
 def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
-                 sum_over_ranks):
+                 sum_over_ranks, comm=None, bpr=None):
     """The same matvec pairs through the implicit Kronecker engine (nothing
     materialised: strength-order and card-list prefix scans per board and
     sequence, kr_kron.cu), on the same boards and inputs: device pairs/s,
@@ -860,6 +882,8 @@ def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev,
     i0 = boards[0][0]
     solver = CudaSolver(ek, i0.treeplex(0), i0.treeplex(1), [b[0].m1 for b in boards], [b[0].m2 for b in boards],
                         i0.pot)
+    if comm is not None:
+        solver.set_comm(comm, bpr)
     drv = DistributedDcfr(solver, args.boards, i0.pot, rank, world, device=coll_dev)
     drv.run(max_iters=5, checkpoint_every=5)
     barrier()

@@ -64,9 +64,14 @@ public:
     CudaEngine(const std::vector<kr_factors>& boards, int device = 0) {
         check(kr_engine_create_boards(boards.data(), int(boards.size()), device, 0, &e_));
     }
-    // The implicit Kronecker engine over KronPayoff pieces (kr_engine_create_kron).
-    explicit CudaEngine(const std::vector<kr_kron_board>& boards, int device = 0) {
-        check(kr_engine_create_kron(boards.data(), int(boards.size()), device, 0, &e_));
+    // Engines over KronPayoff pieces: the implicit Kronecker engine
+    // (kr_engine_create_kron, products within 1e-12) or the Kronecker-factored
+    // one (kr_engine_create_kfactored: Technique B post from its Kronecker
+    // factors, products bitwise those of the factored engine).
+    enum class Kind { Implicit, KFactored };
+    explicit CudaEngine(const std::vector<kr_kron_board>& boards, int device = 0, Kind kind = Kind::Implicit) {
+        if (kind == Kind::KFactored) check(kr_engine_create_kfactored(boards.data(), int(boards.size()), device, 0, &e_));
+        else check(kr_engine_create_kron(boards.data(), int(boards.size()), device, 0, &e_));
     }
     ~CudaEngine() override {
         if (e_) kr_engine_destroy(e_);
@@ -144,6 +149,12 @@ public:
     }
     CudaSolver(const CudaSolver&) = delete;
     CudaSolver& operator=(const CudaSolver&) = delete;
+
+    // Board sharding (kr_solver_set_comm): this solver holds c's rank's shard
+    // of boardsPerRank; runs then cover every board of every rank.
+    void setComm(kr_comm* c, const std::vector<int32_t>& boardsPerRank) {
+        check(kr_solver_set_comm(s_, c, c ? boardsPerRank.data() : nullptr));
+    }
 
     DcfrResult run(const DcfrParams& p) {  // dcfrSolve (solver.hpp:343-404)
         const int cap = p.maxIters / (p.checkpointEvery > 0 ? p.checkpointEvery : 1) + 2;

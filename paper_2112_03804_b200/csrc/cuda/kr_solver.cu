@@ -1007,8 +1007,56 @@ namespace {
 // the host loop's exact expressions (kr_solver_iterate), so a replayed
 // iteration is bitwise the iteration kr_solver_iterate would launch.  The
 // engine's and solver's flop / launch counters advance per replay.
-void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<int>& at, cudaStream_t st) {
+// Counter deltas of one captured graph (added per replay).
+struct GraphDelta {
+    int64_t flops = 0, elaunch = 0, slaunch = 0;
+};
+
+// Capture one DCFR iteration (counter tick, A x2, step 1, A^T x1, step 2),
+// plus a checkpoint when withCk (normalise, the two best responses into
+// checkpoint slot d_cnt[1] of dck, tick): the scalars come from the device
+// tables d_fac / d_ws indexed by the device counters.
+void capture_iteration(kr_solver* s, bool withCk, double* dck, cudaStream_t st, cudaGraphExec_t& exec,
+                       GraphDelta& d) {
     kr_engine* e = s->eng;
+    const int64_t f0 = e->flops_total, el0 = e->launches, sl0 = s->launches;
+    cudaGraph_t g;
+    KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+        krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 0);
+        KR_CK_LAUNCH();
+        s->launches++;
+        krb::engine_ax(e, s->x[1], s->g, st);                                    // g1 = A x2
+        krb::launch_step(s, 0, 1, s->g, 0, 0.0, 0.0, 0.0, st, true);             // P1
+        krb::engine_atx(e, s->x[0], s->g, st);                                   // A^T x1
+        krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);             // P2
+        if (withCk) {
+            normalise_averages(s, st, true);                                     // solver.hpp:390-391
+            krb::checkpoint_values(s, dck, st, s->d_cnt + 1, 2 * int64_t(s->totalBoards()));
+            krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 1);
+            KR_CK_LAUNCH();
+            s->launches++;
+        }
+    } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        throw;
+    }
+    KR_CK(cudaStreamEndCapture(st, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    KR_CK(ie);
+    d.flops = e->flops_total - f0;
+    d.elaunch = e->launches - el0;
+    d.slaunch = s->launches - sl0;
+    e->flops_total = f0;
+    e->launches = el0;
+    s->launches = sl0;
+}
+
+// The device tables of iterations t = s->t + 1 .. maxIters, filled with the
+// host loop's exact expressions (kr_solver_iterate), and the counters
+// {d_cnt[0], d_cnt[1]} = {s->t, 0}.  Returns weightSum after each iteration.
+std::vector<double> iteration_tables(kr_solver* s, int maxIters, cudaStream_t st) {
     const int t0 = s->t;
     std::vector<double> fac(size_t(3) * (maxIters + 1), 0.0), ws(size_t(maxIters) + 1, 0.0);
     double w = s->weightSum;
@@ -1033,55 +1081,32 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
     const int cnt0[2] = {t0, 0};
     KR_CK(cudaMemcpyAsync(s->d_cnt, cnt0, sizeof(cnt0), cudaMemcpyHostToDevice, st));
     KR_CK(cudaStreamSynchronize(st));
+    return ws;
+}
 
+bool graphs_ok(const kr_solver* s) {
+    return s->graphs && s->levelled[0] && s->levelled[1] && !std::getenv("KR_NO_GRAPH");
+}
+
+// Iterations t = s->t+1 .. maxIters by replaying two captured CUDA graphs:
+// one DCFR iteration and the same plus a checkpoint into dck.  A replayed
+// iteration is bitwise the iteration kr_solver_iterate would launch.  The
+// engine's and solver's flop / launch counters advance per replay.
+void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<int>& at, cudaStream_t st) {
+    kr_engine* e = s->eng;
+    const int t0 = s->t;
+    const std::vector<double> ws = iteration_tables(s, maxIters, st);
     const bool timing = e->timing;
     e->timing = false;
-    struct Delta {
-        int64_t flops = 0, elaunch = 0, slaunch = 0;
-    };
-    auto capture = [&](bool withCk, cudaGraphExec_t& exec, Delta& d) {
-        const int64_t f0 = e->flops_total, el0 = e->launches, sl0 = s->launches;
-        cudaGraph_t g;
-        KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        try {
-            krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 0);
-            KR_CK_LAUNCH();
-            s->launches++;
-            krb::engine_ax(e, s->x[1], s->g, st);                                    // g1 = A x2
-            krb::launch_step(s, 0, 1, s->g, 0, 0.0, 0.0, 0.0, st, true);             // P1
-            krb::engine_atx(e, s->x[0], s->g, st);                                   // A^T x1
-            krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);             // P2
-            if (withCk) {
-                normalise_averages(s, st, true);                                     // solver.hpp:390-391
-                krb::checkpoint_values(s, dck, st, s->d_cnt + 1, 2 * int64_t(s->totalBoards()));
-                krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 1);
-                KR_CK_LAUNCH();
-                s->launches++;
-            }
-        } catch (...) {
-            cudaStreamEndCapture(st, &g);
-            throw;
-        }
-        KR_CK(cudaStreamEndCapture(st, &g));
-        const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
-        cudaGraphDestroy(g);
-        KR_CK(ie);
-        d.flops = e->flops_total - f0;
-        d.elaunch = e->launches - el0;
-        d.slaunch = s->launches - sl0;
-        e->flops_total = f0;
-        e->launches = el0;
-        s->launches = sl0;
-    };
     cudaGraphExec_t gIt = nullptr, gCk = nullptr;
-    Delta dIt, dCk;
+    GraphDelta dIt, dCk;
     try {
-        capture(false, gIt, dIt);
-        capture(true, gCk, dCk);
+        capture_iteration(s, false, dck, st, gIt, dIt);
+        capture_iteration(s, true, dck, st, gCk, dCk);
         for (int t = t0 + 1; t <= maxIters; ++t) {
             const bool isCk = t % every == 0 || t == maxIters;
             KR_CK(cudaGraphLaunch(isCk ? gCk : gIt, st));
-            const Delta& d = isCk ? dCk : dIt;
+            const GraphDelta& d = isCk ? dCk : dIt;
             e->flops_total += d.flops;
             e->launches += d.elaunch;
             s->launches += d.slaunch;
@@ -1099,6 +1124,35 @@ void run_graphs(kr_solver* s, int maxIters, int every, double* dck, std::vector<
     e->timing = timing;
     s->t = maxIters;
     s->weightSum = ws[size_t(maxIters)];
+}
+
+// kr_solver_iterate's n iterations as replays of one captured iteration graph.
+void iterate_graph(kr_solver* s, int n, cudaStream_t st) {
+    kr_engine* e = s->eng;
+    const int t1 = s->t + n;
+    const std::vector<double> ws = iteration_tables(s, t1, st);
+    const bool timing = e->timing;
+    e->timing = false;
+    cudaGraphExec_t g = nullptr;
+    GraphDelta d;
+    try {
+        capture_iteration(s, false, nullptr, st, g, d);
+        for (int q = 0; q < n; ++q) {
+            KR_CK(cudaGraphLaunch(g, st));
+            e->flops_total += d.flops;
+            e->launches += d.elaunch;
+            s->launches += d.slaunch;
+        }
+        e->flops_last = e->kron ? krb::kron_flops(e, 1) : e->flops_per_product;
+    } catch (...) {
+        if (g) cudaGraphExecDestroy(g);
+        e->timing = timing;
+        throw;
+    }
+    cudaGraphExecDestroy(g);
+    e->timing = timing;
+    s->t = t1;
+    s->weightSum = ws[size_t(t1)];
 }
 }  // namespace
 
@@ -1180,6 +1234,10 @@ int kr_solver_iterate(kr_solver* s, int n) {
         KR_CK(cudaSetDevice(s->device));
         kr_engine* e = s->eng;
         cudaStream_t st = e->stream;
+        if (n >= 2 && graphs_ok(s)) {  // one captured iteration, replayed n times
+            iterate_graph(s, n, st);
+            return;
+        }
         for (int q = 0; q < n; ++q) {
             const int t = ++s->t;  // solver.hpp:365-388
             const double pos = krb::discount_factor(t, s->alpha), neg = krb::discount_factor(t, s->beta);
@@ -1300,7 +1358,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
             double* dck = krb::dev_alloc<double>(int64_t(nck) * 2 * nb);
             std::vector<int> at;
             try {
-                if (s->graphs && s->levelled[0] && s->levelled[1] && !std::getenv("KR_NO_GRAPH")) {
+                if (graphs_ok(s)) {
                     run_graphs(s, prm->max_iters, prm->checkpoint_every, dck, at, st);
                 } else {
                     while (s->t < prm->max_iters) {

@@ -80,3 +80,30 @@ def test_solve_implicit_engine_and_cfr_plus(twenty_card):
     r = run("solve", "--instance", inst, "--rule", "cfr+", "--iters", "1000", "--out", str(d / "cfrp"))
     assert r.returncode == 0, r.stderr
     assert r.stdout.startswith("solve: iterations=1000 ") and "rule=cfr+" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["kfactored", "factored", "implicit"])
+def test_solve_turn_matches_the_library_solver(engine):
+    """krb200 solve-turn: config 3's boards sharded over --gpus N (here 1: the
+    box has one GPU) through the C++ driver; the printed trace equals the
+    Python-driven solve of the same boards bit for bit."""
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200 import host as H
+    from paper_2112_03804_b200.solver import CudaSolver, DcfrParams
+    build.build_cli()
+    r = run("solve-turn", "--boards", "4", "--iters", "40", "--checkpoint-every", "20", "--gpus", "1",
+            "--engine", engine)
+    assert r.returncode == 0, r.stderr
+    got = [float(ln.split("exploitability=")[1]) for ln in r.stdout.splitlines() if ln.startswith("checkpoint")]
+    boards = H.turn_instances(nboards=4, factors=engine == "factored")
+    insts = [i for i, _ in boards]
+    eng = (CudaEngine([f for _, f in boards]) if engine == "factored" else
+           CudaEngine.kfactored(insts) if engine == "kfactored" else CudaEngine.kron(insts))
+    i0 = insts[0]
+    ref = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [i.m1 for i in insts], [i.m2 for i in insts],
+                     i0.pot).run(DcfrParams(max_iters=40, checkpoint_every=20))
+    assert got == list(ref.trace_expl)
+    assert "gpus=1" in r.stdout and f"engine={engine}" in r.stdout
+    bad = run("solve-turn", "--gpus", "64")
+    assert bad.returncode == 2 and "INVALID_INPUT" in bad.stderr

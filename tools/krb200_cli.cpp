@@ -6,6 +6,14 @@
 //   krb200 solve    --instance F [--bundle DIR] [--technique a|b] [--iters N]
 //                   [--target-expl X] [--checkpoint-every N] [--out DIR]
 //                   [--engine factored|implicit] [--rule dcfr|cfr+|prm+]
+//   krb200 solve-turn [--turn Ks7d4c2h] [--boards 48] [--gpus N] [--iters N]
+//                   [--checkpoint-every N] [--engine kfactored|factored|implicit]
+//
+// solve-turn: config 3, a turn's river boards under a
+// uniform chance root, boards sharded contiguously over N GPUs of this node
+// (one host thread and one solver per GPU, an NCCL communicator over the
+// device list: kr_comm_init_all); the checkpoint values are all-gathered and
+// folded in board order, so the trace is bitwise the one-GPU trace.
 //
 // --engine implicit applies the payoff without factors (kr_engine_create_kron);
 // --rule selects the update rule (dcfr is the reference's; cfr+ and prm+ are
@@ -16,6 +24,7 @@
 #include <chrono>
 #include <cmath>
 #include <memory>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
@@ -29,8 +38,10 @@ namespace {
 
 struct Options {
     std::string cmd, instance, bundle, technique = "b", out = "out", engine = "factored", rule = "dcfr";
-    int iters = 1000, checkpointEvery = 50;
+    std::string turn = "Ks7d4c2h";
+    int iters = 1000, checkpointEvery = 50, boards = 48, gpus = 1;
     double targetExpl = 0;
+    bool engineSet = false;
 };
 
 void hcheck(int status) {
@@ -48,6 +59,7 @@ struct Instance {
         hcheck(krh_instance_from_json(path.c_str(), &h));
         hcheck(krh_instance_dims(h, d));
     }
+    explicit Instance(krh_instance* owned) : h(owned) { hcheck(krh_instance_dims(h, d)); }
     ~Instance() { krh_instance_free(h); }
     krb200::Treeplex treeplex(int p) const {
         krb200::Treeplex t;
@@ -149,12 +161,104 @@ int runSolve(const Options& o) {
     return 0;
 }
 
+// The river cards under a turn and their belief seeds (config 3: seed 1000 +
+// card id, as paper_2112_03804_b200.host.turn_boards).
+std::vector<std::pair<std::string, uint64_t>> turnBoards(const std::string& turn, int n) {
+    const std::string ranks = "23456789TJQKA", suits = "cdhs";
+    std::vector<std::pair<std::string, uint64_t>> out;
+    for (size_t r = 0; r < ranks.size(); ++r)
+        for (size_t s = 0; s < suits.size(); ++s) {
+            const std::string c = std::string(1, ranks[r]) + suits[s];
+            bool used = false;
+            for (size_t i = 0; i + 1 < turn.size(); i += 2) used = used || turn.substr(i, 2) == c;
+            if (!used && int(out.size()) < n) out.push_back({c, 1000 + uint64_t(r * 4 + s)});
+        }
+    return out;
+}
+
+int runSolveTurn(const Options& o) {
+    const std::string engine = o.engineSet ? o.engine : "kfactored";
+    if (engine != "factored" && engine != "kfactored" && engine != "implicit")
+        throw krb200::Error("INVALID_INPUT", "--engine must be kfactored, factored or implicit");
+    int ndev = kr_device_count();
+    if (o.gpus < 1 || o.gpus > ndev)
+        throw krb200::Error("INVALID_INPUT", "--gpus must be between 1 and the visible device count");
+    const auto specs = turnBoards(o.turn, o.boards);
+    const int nb = int(specs.size()), world = o.gpus;
+    std::vector<int32_t> bpr(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) bpr[size_t(r)] = nb / world + (r < nb % world ? 1 : 0);
+    std::vector<kr_comm*> comms(static_cast<size_t>(world), nullptr);
+    if (world > 1) {
+        std::vector<int> devs(static_cast<size_t>(world));
+        for (int r = 0; r < world; ++r) devs[size_t(r)] = r;
+        krb200::check(kr_comm_init_all(world, devs.data(), comms.data()));
+    }
+    std::vector<krb200::DcfrResult> res(static_cast<size_t>(world));
+    std::vector<std::string> errs(static_cast<size_t>(world));
+    auto rankMain = [&](int r) {
+        try {
+            const int b0 = [&] { int s = 0; for (int q = 0; q < r; ++q) s += bpr[size_t(q)]; return s; }();
+            std::vector<std::unique_ptr<Instance>> insts;
+            std::vector<Factors> fs(static_cast<size_t>(bpr[size_t(r)]));
+            std::vector<kr_kron_board> kb;
+            std::vector<kr_factors> fv;
+            std::vector<int32_t> h1, h2;
+            for (int b = b0; b < b0 + bpr[size_t(r)]; ++b) {
+                const std::string board = o.turn + specs[size_t(b)].first;
+                krh_instance* h = nullptr;
+                hcheck(krh_instance_builtin("river_full", specs[size_t(b)].second, 0, 0, board.c_str(), 52, 3, &h));
+                auto in = std::make_unique<Instance>(h);
+                kr_kron_board k;
+                hcheck(krh_instance_kron_view(in->h, &k));
+                kb.push_back(k);
+                if (engine == "factored") {
+                    hcheck(krh_sparsify(in->h, 1, 1, 1000, &fs[size_t(b - b0)].h));
+                    fv.push_back(fs[size_t(b - b0)].view());
+                }
+                h1.push_back(int32_t(in->d[0]));
+                h2.push_back(int32_t(in->d[1]));
+                insts.push_back(std::move(in));
+            }
+            std::unique_ptr<krb200::CudaEngine> eng;
+            if (engine == "factored") eng = std::make_unique<krb200::CudaEngine>(fv, r);
+            else eng = std::make_unique<krb200::CudaEngine>(kb, r, engine == "kfactored"
+                                                                     ? krb200::CudaEngine::Kind::KFactored
+                                                                     : krb200::CudaEngine::Kind::Implicit);
+            krb200::CudaSolver solver(*eng, insts[0]->treeplex(0), insts[0]->treeplex(1), h1, h2,
+                                      krh_instance_pot(insts[0]->h));
+            if (world > 1) solver.setComm(comms[size_t(r)], bpr);
+            krb200::DcfrParams p;
+            p.maxIters = o.iters;
+            p.checkpointEvery = o.checkpointEvery;
+            res[size_t(r)] = solver.run(p);
+        } catch (const std::exception& e) {
+            errs[size_t(r)] = e.what();
+        }
+    };
+    std::vector<std::thread> th;
+    for (int r = 0; r < world; ++r) th.emplace_back(rankMain, r);
+    for (auto& t : th) t.join();
+    for (kr_comm* c : comms)
+        if (c) kr_comm_destroy(c);
+    for (const auto& e : errs)
+        if (!e.empty()) throw krb200::Error("CUDA", e);
+    const krb200::DcfrResult& r = res[0];
+    double secs = 0;
+    for (const auto& q : res) secs = std::max(secs, q.deviceSeconds);
+    for (const auto& q : r.trace) std::printf("checkpoint iteration=%d exploitability=%.17g\n", q.iteration, q.exploitability);
+    std::printf("solve-turn: turn=%s boards=%d gpus=%d engine=%s iterations=%d exploitability=%.17g "
+                "device_seconds=%.6f iters_per_s=%.1f\n",
+                o.turn.c_str(), nb, world, engine.c_str(), r.iterations, r.exploitability, secs,
+                secs > 0 ? r.iterations / secs : 0.0);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     Options o;
     if (argc < 2) {
-        std::fprintf(stderr, "usage: krb200 {sparsify|solve} --instance F [options]\n");
+        std::fprintf(stderr, "usage: krb200 {sparsify|solve|solve-turn} [options]\n");
         return 1;
     }
     o.cmd = argv[1];
@@ -167,7 +271,12 @@ int main(int argc, char** argv) {
         else if (k == "--iters") o.iters = std::atoi(v.c_str());
         else if (k == "--target-expl") o.targetExpl = std::atof(v.c_str());
         else if (k == "--checkpoint-every") o.checkpointEvery = std::atoi(v.c_str());
-        else if (k == "--engine") o.engine = v;
+        else if (k == "--engine") {
+            o.engine = v;
+            o.engineSet = true;
+        } else if (k == "--turn") o.turn = v;
+        else if (k == "--boards") o.boards = std::atoi(v.c_str());
+        else if (k == "--gpus") o.gpus = std::atoi(v.c_str());
         else if (k == "--rule") o.rule = v;
         else {
             std::fprintf(stderr, "unknown option %s\n", k.c_str());
@@ -177,6 +286,7 @@ int main(int argc, char** argv) {
     try {
         if (o.cmd == "sparsify") return runSparsify(o);
         if (o.cmd == "solve") return runSolve(o);
+        if (o.cmd == "solve-turn") return runSolveTurn(o);
         std::fprintf(stderr, "unknown subcommand %s\n", o.cmd.c_str());
         return 1;
     } catch (const krb200::Error& e) {
