@@ -238,6 +238,41 @@ int or_sparsify(void* h, int technique, int post, int peelIters, void** out) {
         *out = s.release();
     });
 }
+// Technique B with postprocessing (sparsify.hpp:246-406) from raw KronPayoff
+// pieces instead of an instance: strength keys and cards per hand (W_ij =
+// sign(key1_i - key2_j) for disjoint hands, H× = 1 for overlapping ones, as
+// assemble builds them, kron.hpp:134-166), lambda1 / lambda2 as given, F and S
+// as CSR.  The turn checker (turn_oracle.py) uses it to apply each block of a
+// turn game with the reference's factored matvec.
+int or_sparsify_pieces(int m1, int m2, int n1, int n2, const uint32_t* key1, const uint32_t* key2,
+                       const uint8_t* cards1, const uint8_t* cards2, const double* l1, const double* l2,
+                       const int64_t* fptr, const int32_t* fcol, const double* fval, const int64_t* sptr,
+                       const int32_t* scol, const double* sval, void** out) {
+    return guarded([&] {
+        KronPayoff kp;
+        kp.n1 = n1;
+        kp.n2 = n2;
+        kp.hands[0].resize(size_t(m1));
+        kp.hands[1].resize(size_t(m2));
+        kp.lambda1.assign(l1, l1 + m1);
+        kp.lambda2.assign(l2, l2 + m2);
+        kp.W.assign(size_t(m1) * m2, 0.0);
+        kp.Hcross.assign(size_t(m1) * m2, 0.0);
+        for (int i = 0; i < m1; ++i)
+            for (int j = 0; j < m2; ++j) {
+                const int a0 = cards1[2 * i], a1 = cards1[2 * i + 1], b0 = cards2[2 * j], b1 = cards2[2 * j + 1];
+                const bool ok = a0 != b0 && a0 != b1 && a1 != b0 && a1 != b1;
+                kp.Hcross[size_t(i) * m2 + j] = ok ? 0.0 : 1.0;
+                kp.W[size_t(i) * m2 + j] = ok ? (key1[i] > key2[j] ? 1.0 : (key1[i] < key2[j] ? -1.0 : 0.0)) : 0.0;
+            }
+        kp.F = fromArrays(true, n1, n2, fptr, fcol, fval);
+        kp.S = fromArrays(true, n1, n2, sptr, scol, sval);
+        auto sp = std::make_unique<Sp>();
+        sp->s = postprocess(techniqueB(kp));
+        *out = sp.release();
+    });
+}
+
 int or_postprocess(void* sp, void** out) {
     return guarded([&] {
         auto s = std::make_unique<Sp>();

@@ -239,6 +239,36 @@ class Sparsification:
         return {n: self.export(n) for n in self.NAMES}
 
     @classmethod
+    def from_pieces(cls, piece):
+        """Technique B post (sparsify.hpp:246-406) of one Kronecker block from
+        raw pieces: dict(key=[k1, k2], cards=[c1, c2], lam=[l1, l2], F, S)
+        with F, S dense (n1 x n2) arrays (or_sparsify_pieces)."""
+        k1, k2 = [np.ascontiguousarray(k, np.uint32) for k in piece["key"]]
+        c1, c2 = [np.ascontiguousarray(c, np.uint8).reshape(-1) for c in piece["cards"]]
+        l1, l2 = [np.ascontiguousarray(v, np.float64) for v in piece["lam"]]
+
+        def csr(D):
+            D = np.asarray(D, np.float64)
+            ptr, col, val = [0], [], []
+            for r in range(D.shape[0]):
+                nz = np.nonzero(D[r])[0]
+                col += nz.tolist()
+                val += D[r, nz].tolist()
+                ptr.append(len(col))
+            return (np.ascontiguousarray(ptr, np.int64), np.ascontiguousarray(col, np.int32),
+                    np.ascontiguousarray(val, np.float64))
+
+        F, S = csr(piece["F"]), csr(piece["S"])
+        n1, n2 = np.asarray(piece["F"]).shape
+        out = C.c_void_p()
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        _check(lib().or_sparsify_pieces(len(k1), len(k2), n1, n2, p(k1), p(k2), p(c1), p(c2), p(l1), p(l2),
+                                        p(F[0]), p(F[1]), p(F[2]), p(S[0]), p(S[1]), p(S[2]), C.byref(out)))
+        sp = cls(out.value)
+        sp._keep = (k1, k2, c1, c2, l1, l2, F, S)
+        return sp
+
+    @classmethod
     def from_arrays(cls, rows, cols, k, f, technique="b", post=True, validate=True):
         args = []
         for n in cls.NAMES:

@@ -17,8 +17,14 @@ the turn treeplex:
     children (ev = g + (children + river)).  Each river sequence form runs with
     mass 1 and is then scaled by the turn reach of sigma_p(t);
   - bestResponseValue (292-321) composes the same way.
-Products differ from the device's K7 only by summation order, so checks are
-held to tolerances stated in the tests.
+Products: `products="block"` applies each block by the block formula
+(dense numpy); `products="factored"` applies it by the reference's own
+factored matvec / matvecTranspose (engine.hpp:58-133) over Technique B with
+postprocessing built from the block's pieces (the oracle's techniqueB +
+postprocess, or_sparsify_pieces).  The device's Kronecker-factored engine
+reproduces the latter bit for bit, so a turn solve driven by it is checked
+bitwise; the K7 engine differs by summation order and is held to tolerances
+stated in the tests.
 """
 import numpy as np
 
@@ -30,16 +36,25 @@ def _disjoint(c1, c2):
 
 
 class Block:
-    def __init__(self, piece):
+    def __init__(self, piece, products="block"):
+        self.factored = products == "factored"
+        if self.factored:
+            import pyoracle as po
+            self.sp = po.Sparsification.from_pieces(piece)
+            return
         k1, k2 = [np.asarray(k, np.int64) for k in piece["key"]]
         self.P = piece["lam"][0][:, None] * piece["lam"][1][None, :] * _disjoint(*piece["cards"])
         self.PW = self.P * np.sign(k1[:, None] - k2[None, :])
         self.F, self.S = piece["F"], piece["S"]
 
     def ax(self, x):  # x: (m2, n2) -> (m1, n1)
+        if self.factored:
+            return self.sp.matvec(np.ascontiguousarray(x).ravel())
         return self.P @ x @ self.F.T + self.PW @ x @ self.S.T
 
     def atx(self, y):  # y: (m1, n1) -> (m2, n2)
+        if self.factored:
+            return self.sp.matvec_t(np.ascontiguousarray(y).ravel())
         return self.P.T @ y @ self.F + self.PW.T @ y @ self.S
 
 
@@ -131,10 +146,10 @@ def br_walk(tree, g, extra=None):
 
 
 class TurnOracle:
-    def __init__(self, game):
+    def __init__(self, game, products="block"):
         self.g = game
-        self.turn = Block(game.kron_pieces(None)[0])
-        self.river = [[Block(pc) for pc in game.kron_pieces(t)] for t in range(len(game.conts))]
+        self.turn = Block(game.kron_pieces(None)[0], products)
+        self.river = [[Block(pc, products) for pc in game.kron_pieces(t)] for t in range(len(game.conts))]
         self.tt = [Tree(game.tree_turn[p]) for p in range(2)]
         self.tr = [[Tree(game.tree_river[t][p]) for p in range(2)] for t in range(len(game.conts))]
         self.boff = np.concatenate([[0], np.cumsum(game.mb)])

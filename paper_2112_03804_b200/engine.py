@@ -54,16 +54,19 @@ class CudaEngine:
         return cls.from_kron_boards([i.kron_view() for i in insts], device, flags)
 
     @classmethod
-    def from_kron_boards(cls, boards, device=0, flags=0):
-        """Implicit engine from kr_kron_board structs (the caller keeps the
-        arrays they point to alive until this returns: the engine copies)."""
+    def from_kron_boards(cls, boards, device=0, flags=0, kind="implicit"):
+        """Engine from kr_kron_board structs (the caller keeps the arrays they
+        point to alive until this returns: the engine copies): the implicit
+        engine (K7), or kind="kfactored" the Kronecker-factored one."""
         L = N.cuda()
         arr = (N.kr_kron_board * len(boards))(*boards)
         h = C.c_void_p()
-        N.check(L.kr_engine_create_kron(arr, len(boards), device, flags, C.byref(h)))
+        create = L.kr_engine_create_kfactored if kind == "kfactored" else L.kr_engine_create_kron
+        N.check(create(arr, len(boards), device, flags, C.byref(h)))
         self = cls.__new__(cls)
         self._attach(h, device, len(boards))
-        self.implicit = True
+        self.implicit = kind != "kfactored"
+        self.kfactored_mode = kind == "kfactored"
         return self
 
     @classmethod

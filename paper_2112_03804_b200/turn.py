@@ -201,23 +201,27 @@ class TurnSolver:
     engines for the turn block and each continuation's river boards, the
     turn treeplex composed with the river treeplexes."""
 
-    def __init__(self, game: TurnGame, device=0, group=None, comm=None, boards_per_rank=None):
+    def __init__(self, game: TurnGame, device=0, group=None, comm=None, boards_per_rank=None, engine="implicit"):
         """Board sharding (each rank builds its TurnGame with boards=shard):
         comm, a dist.Comm (NCCL in-stream, graph-captured), or group, a host
         torch.distributed process group (gloo), carries the per-board river
         values of every half-iteration; the library folds them in global board
-        order, so the solve is bitwise the one-rank solve (see shard())."""
+        order, so the solve is bitwise the one-rank solve (see shard()).
+        engine: "implicit" (K7, the fastest; products within 1e-12) or
+        "kfactored" (each block as Technique B post from its Kronecker
+        factors: products bitwise the reference's factored matvec, so the
+        whole solve is bitwise its CPU restatement)."""
         import ctypes as C
 
         from . import _native as N
         from .engine import CudaEngine
         self.game = game
         tb, keep = game.turn_board()
-        self.turn_eng = CudaEngine.from_kron_boards([tb], device)
+        self.turn_eng = CudaEngine.from_kron_boards([tb], device, kind=engine)
         self.river_eng = []
         for t in range(len(game.conts)):
             rb, k2 = game.river_boards(t)
-            self.river_eng.append(CudaEngine.from_kron_boards(rb, device))
+            self.river_eng.append(CudaEngine.from_kron_boards(rb, device, kind=engine))
         del keep
         keepalive = []
         tt = (N.kr_treeplex * 2)(*[game.tree_turn[p].struct(keepalive) for p in range(2)])
