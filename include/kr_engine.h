@@ -193,6 +193,22 @@ int kr_engine_device(const kr_engine* e);
 /* Kernel launches issued by this engine since creation (both directions). */
 int64_t kr_engine_launches(const kr_engine* e);
 
+/* SelfCheck mode, the device counterpart of SelfCheckEngine
+ * (solver.hpp:67-99): every `every`-th product of e (calls 0, every,
+ * 2 every, ..., counted over kr_engine_ax / _atx / _pair and the device
+ * variants) is replayed through `reference` (typically the implicit engine
+ * over the same boards: the block formula, kron.hpp:211-254) and compared on
+ * the device; max|got - exp| > tol (1 + max|exp|) makes the next host-buffer
+ * call, kr_solver_run on e, or kr_engine_selfcheck_status return
+ * KR_CONTRACT (the reference throws ContractError).  Solvers on a
+ * self-checked engine run iteration by iteration (no graph replay), so every
+ * product is checked on schedule.  reference = NULL turns it off.  The
+ * reference defaults are every = 500, tol = 1e-8. */
+int kr_engine_set_selfcheck(kr_engine* e, kr_engine* reference, int every, double tol);
+/* Checks made so far, the worst err / (tol (1 + max|exp|)) seen; KR_CONTRACT
+ * if a check has failed. */
+int kr_engine_selfcheck_status(kr_engine* e, int64_t* checks, double* worst);
+
 /* Pinned host memory for the host-buffer entry points. */
 void* kr_host_alloc(int64_t bytes);
 void kr_host_free(void* p);

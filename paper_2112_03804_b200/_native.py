@@ -103,7 +103,7 @@ CUDA_SYMBOLS = [
     "kr_factors_build_device", "kr_devfactors_view", "kr_devfactors_seconds", "kr_devfactors_free",
     "kr_engine_create_device_b", "kr_engine_create_kfactored", "kr_engine_pair",
     "kr_comm_unique_id", "kr_comm_init_rank", "kr_comm_init_all", "kr_comm_destroy", "kr_comm_rank", "kr_comm_size",
-    "kr_solver_set_comm", "kr_turn_solver_set_comm",
+    "kr_solver_set_comm", "kr_turn_solver_set_comm", "kr_engine_set_selfcheck", "kr_engine_selfcheck_status",
 ]
 
 
@@ -194,6 +194,8 @@ def cuda():
         L.kr_comm_destroy.argtypes = [C.c_void_p]
         L.kr_comm_rank.argtypes = [C.c_void_p]
         L.kr_comm_size.argtypes = [C.c_void_p]
+        L.kr_engine_set_selfcheck.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double]
+        L.kr_engine_selfcheck_status.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.kr_turn_solver_sizes.argtypes = [C.c_void_p, C.c_void_p]
         L.kr_engine_create_device_b.argtypes = [C.POINTER(kr_kron_board), C.c_int, C.c_int, C.c_uint32,
                                                 C.POINTER(C.c_void_p)]

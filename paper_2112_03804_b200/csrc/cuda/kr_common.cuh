@@ -305,6 +305,16 @@ struct kr_engine {
     };
     std::vector<PipeGraph> pipeGraphs;
     std::vector<PipeGraph> pipeSeen;  // first calls (exec unused): captured on the second
+    // SelfCheck mode (kr_engine_set_selfcheck, SelfCheckEngine solver.hpp:67-99):
+    // every scEvery-th product is replayed through scRef (the block formula
+    // restated: the implicit engine) and compared normwise on the device;
+    // a violation is sticky (scStat[4] = 1) and surfaces as KR_CONTRACT.
+    kr_engine* scRef = nullptr;
+    int scEvery = 0;
+    double scTol = 0;
+    int64_t scCalls = 0, scChecks = 0;
+    double* scBuf[2] = {nullptr, nullptr};  // expected outputs per direction
+    double* scStat = nullptr;               // [2 dirs][2] (max |got-exp|, max |exp|) bits, [4] flag, [5] worst ratio
     // kr_engine_pair_device: A^T y forks onto `side` (created on first use)
     cudaStream_t side = nullptr;
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
@@ -314,6 +324,11 @@ struct kr_engine {
 namespace krb {
 // Enqueue the products on `s` (device pointers).
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s);
+// SelfCheck: compare out with the reference engine's product of in (every
+// scEvery-th call; no-op when off or while s is being captured); and raise
+// KR_CONTRACT if a check has failed (synchronises the engine's stream).
+void engine_selfcheck(kr_engine* e, int dir, const double* in, const double* out, cudaStream_t s);
+void engine_selfcheck_raise(kr_engine* e);
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s);
 // Copy streams and events for the pipelined host-buffer calls (>= 2 groups).
 void engine_make_pipeline(kr_engine* e);

@@ -1239,6 +1239,9 @@ void destroy_engine(kr_engine* e) {
     cudaFree(e->d_xp);
     cudaFree(e->d_in);
     cudaFree(e->d_out);
+    cudaFree(e->scBuf[0]);
+    cudaFree(e->scBuf[1]);
+    cudaFree(e->scStat);
     for (auto& p : e->pending) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
@@ -1926,6 +1929,63 @@ void engine_product(kr_engine* e, int dir, const double* in, double* out, cudaSt
     account(e, dir);
 }
 
+// SelfCheck reduction: max |got - exp| and max |exp| as the bit patterns of
+// non-negative doubles (unsigned order == numeric order), then one verdict
+// thread: err > tol (1 + max|exp|) sets the sticky flag (solver.hpp:84-91).
+__global__ void k_sc_reduce(const double* __restrict__ got, const double* __restrict__ exp, int64_t n,
+                            unsigned long long* __restrict__ stat) {
+    krb::pdl_entry();
+    double e = 0.0, m = 0.0;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
+        const double x = exp[q];
+        e = fmax(e, fabs(got[q] - x));
+        m = fmax(m, fabs(x));
+        if (got[q] != got[q] || x != x) e = __longlong_as_double(0x7ff0000000000000LL);  // NaN fails the check
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(stat, (unsigned long long)__double_as_longlong(e));
+        atomicMax(stat + 1, (unsigned long long)__double_as_longlong(m));
+    }
+}
+__global__ void k_sc_verdict(const unsigned long long* __restrict__ stat, double tol, double* __restrict__ flags) {
+    krb::pdl_entry();
+    const double err = __longlong_as_double((long long)stat[0]), scale = 1.0 + __longlong_as_double((long long)stat[1]);
+    const double ratio = err / (tol * scale);
+    if (!(err <= tol * scale)) flags[0] = 1.0;
+    flags[1] = fmax(flags[1], ratio);
+}
+
+void engine_selfcheck(kr_engine* e, int dir, const double* in, const double* out, cudaStream_t s) {
+    if (!e->scRef || e->scEvery < 1) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    KR_CK(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return;
+    if (e->scCalls++ % e->scEvery != 0) return;  // SelfCheckEngine: calls_++ % every_ == 0
+    const int64_t n = dir == 0 ? e->rows : e->cols;
+    engine_product(e->scRef, dir, in, e->scBuf[dir], s);
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(e->scStat) + 2 * dir;
+    KR_CK(cudaMemsetAsync(st, 0, 16, s));
+    const unsigned grid = unsigned(std::min<int64_t>((n + 255) / 256, 4 * 148));
+    krb::launch(k_sc_reduce, std::max(grid, 1u), 256, 0, s, out, e->scBuf[dir], n, st);
+    KR_CK_LAUNCH();
+    krb::launch(k_sc_verdict, 1, 1, 0, s, st, e->scTol, e->scStat + 4);
+    KR_CK_LAUNCH();
+    e->scChecks++;
+}
+
+void engine_selfcheck_raise(kr_engine* e) {
+    if (!e->scRef) return;
+    double f[2] = {0, 0};
+    KR_CK(cudaMemcpy(f, e->scStat + 4, 16, cudaMemcpyDeviceToHost));
+    if (f[0] != 0.0)
+        throw Fail{KR_CONTRACT, "self-check: the gradient deviates from the reference engine by " +
+                                    std::to_string(f[1]) + " x tol (1 + max|expect|) (solver.hpp:84-91)"};
+}
+
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) { engine_product(e, 0, x, y, s); }
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) { engine_product(e, 1, y, x, s); }
 
@@ -2021,8 +2081,10 @@ void host_product(kr_engine* e, int dir, const double* hin, int64_t nin, double*
     KR_CK(cudaSetDevice(e->device));
     if (!graph_call(e, dir, hin, hout, nullptr, nullptr, [&] { enqueue_direction(e, dir, hin, hout, e->pipe[0]); }))
         enqueue_direction(e, dir, hin, hout, e->pipe[0]);
+    engine_selfcheck(e, dir, e->pipe[0].d_in, e->pipe[0].d_out, e->stream);
     KR_CK(cudaStreamSynchronize(e->stream));
     account(e, dir);
+    engine_selfcheck_raise(e);
 }
 
 // The second direction's pipe of kr_engine_pair (own streams, events and
@@ -2061,9 +2123,12 @@ void host_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_t na
         KR_CK(cudaStreamWaitEvent(e->stream, e->evJoin, 0));
     };
     if (!graph_call(e, 2, x, ax, y, atx, enqueue)) enqueue();
+    engine_selfcheck(e, 0, e->pipe[0].d_in, e->pipe[0].d_out, e->stream);
+    engine_selfcheck(e, 1, e->pipe[1].d_in, e->pipe[1].d_out, e->stream);
     KR_CK(cudaStreamSynchronize(e->stream));
     account(e, 0);
     account(e, 1);
+    engine_selfcheck_raise(e);
 }
 
 // The pipelined host-buffer product (board groups), enqueued from and
@@ -2222,7 +2287,9 @@ int kr_engine_ax_device(kr_engine* e, const double* x, double* y, void* stream) 
     return guarded([&] {
         if (!e || !x || !y) throw Fail{KR_INVALID_INPUT, "null argument"};
         KR_CK(cudaSetDevice(e->device));
-        krb::engine_ax(e, x, y, stream ? static_cast<cudaStream_t>(stream) : e->stream);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+        krb::engine_ax(e, x, y, s);
+        krb::engine_selfcheck(e, 0, x, y, s);
     });
 }
 
@@ -2230,7 +2297,9 @@ int kr_engine_atx_device(kr_engine* e, const double* y, double* x, void* stream)
     return guarded([&] {
         if (!e || !x || !y) throw Fail{KR_INVALID_INPUT, "null argument"};
         KR_CK(cudaSetDevice(e->device));
-        krb::engine_atx(e, y, x, stream ? static_cast<cudaStream_t>(stream) : e->stream);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+        krb::engine_atx(e, y, x, s);
+        krb::engine_selfcheck(e, 1, y, x, s);
     });
 }
 
@@ -2248,7 +2317,9 @@ int kr_engine_pair_device(kr_engine* e, const double* x, double* ax, const doubl
         const double pairGB = (e->kron || e->kf) ? 0.0 : 12e-9 * 2.0 * double(e->nnzA + e->nnzU + e->nnzV);
         if (pairGB > serialGB) {
             krb::engine_ax(e, x, ax, s);
+            krb::engine_selfcheck(e, 0, x, ax, s);
             krb::engine_atx(e, y, atx, s);
+            krb::engine_selfcheck(e, 1, y, atx, s);
             return;
         }
         if (!e->side) {
@@ -2262,9 +2333,48 @@ int kr_engine_pair_device(kr_engine* e, const double* x, double* ax, const doubl
         KR_CK(cudaEventRecord(e->evFork, s));
         KR_CK(cudaStreamWaitEvent(e->side, e->evFork, 0));
         krb::engine_atx(e, y, atx, e->side);
+        krb::engine_selfcheck(e, 1, y, atx, e->side);
         krb::engine_ax(e, x, ax, s);
+        krb::engine_selfcheck(e, 0, x, ax, s);
         KR_CK(cudaEventRecord(e->evJoin, e->side));
         KR_CK(cudaStreamWaitEvent(s, e->evJoin, 0));
+    });
+}
+
+int kr_engine_set_selfcheck(kr_engine* e, kr_engine* reference, int every, double tol) {
+    return guarded([&] {
+        if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
+        KR_CK(cudaSetDevice(e->device));
+        if (!reference) {
+            e->scRef = nullptr;
+            return;
+        }
+        if (reference == e) throw Fail{KR_INVALID_INPUT, "an engine cannot check itself"};
+        if (reference->device != e->device) throw Fail{KR_INVALID_INPUT, "reference engine on another device"};
+        if (reference->rows != e->rows || reference->cols != e->cols)
+            throw Fail{KR_INVALID_INPUT, "reference engine has other dimensions"};
+        if (every < 1 || !(tol > 0)) throw Fail{KR_INVALID_INPUT, "self-check period and tolerance must be positive"};
+        for (int d = 0; d < 2; ++d)
+            if (!e->scBuf[d]) e->scBuf[d] = krb::dev_alloc<double>(std::max<int64_t>(d == 0 ? e->rows : e->cols, 1));
+        if (!e->scStat) e->scStat = krb::dev_alloc<double>(6);
+        KR_CK(cudaMemset(e->scStat, 0, 6 * sizeof(double)));
+        e->scRef = reference;
+        e->scEvery = every;
+        e->scTol = tol;
+        e->scCalls = e->scChecks = 0;
+    });
+}
+
+int kr_engine_selfcheck_status(kr_engine* e, int64_t* checks, double* worst) {
+    return guarded([&] {
+        if (!e) throw Fail{KR_INVALID_INPUT, "null engine"};
+        KR_CK(cudaSetDevice(e->device));
+        KR_CK(cudaStreamSynchronize(e->stream));
+        double f[2] = {0, 0};
+        if (e->scStat) KR_CK(cudaMemcpy(f, e->scStat + 4, 16, cudaMemcpyDeviceToHost));
+        if (checks) *checks = e->scChecks;
+        if (worst) *worst = f[1];
+        krb::engine_selfcheck_raise(e);
     });
 }
 

@@ -738,6 +738,7 @@ void best_response_to(kr_solver* s, int player, const double* opp, double* dst, 
     if (!handval) handval = s->handval;
     if (player == 0) engine_ax(e, opp, g, st);
     else engine_atx(e, opp, g, st);
+    engine_selfcheck(e, player, opp, g, st);  // bestResponseValue calls eng.Ax / eng.ATx (solver.hpp:299)
     const int nn = s->nnodes[player], n = s->n[player];
     const int bt = 128;
     const int na = s->na[player];
@@ -1085,7 +1086,7 @@ std::vector<double> iteration_tables(kr_solver* s, int maxIters, cudaStream_t st
 }
 
 bool graphs_ok(const kr_solver* s) {
-    return s->graphs && s->levelled[0] && s->levelled[1] && !std::getenv("KR_NO_GRAPH");
+    return s->graphs && s->levelled[0] && s->levelled[1] && !std::getenv("KR_NO_GRAPH") && !s->eng->scRef;
 }
 
 // Iterations t = s->t+1 .. maxIters by replaying two captured CUDA graphs:
@@ -1243,8 +1244,10 @@ int kr_solver_iterate(kr_solver* s, int n) {
             const double pos = krb::discount_factor(t, s->alpha), neg = krb::discount_factor(t, s->beta);
             const double shrink = std::pow(double(t) / (t + 1), s->gamma);
             krb::engine_ax(e, s->x[1], s->g, st);                      // g1 = A x2
+            krb::engine_selfcheck(e, 0, s->x[1], s->g, st);
             krb::launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st);  // P1 sweep/seqform/discount/avg
             krb::engine_atx(e, s->x[0], s->g, st);                     // A^T x1
+            krb::engine_selfcheck(e, 1, s->x[0], s->g, st);
             krb::launch_step(s, 1, 1, s->g, 1, pos, neg, shrink, st);  // P2 with g2 = -A^T x1
             s->weightSum += 1;
             s->weightSum *= shrink;
@@ -1395,6 +1398,7 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
         cudaEventDestroy(ev1);
         if (r->avg1 || r->avg2) ck(kr_solver_averages(s, r->avg1, r->avg2));
         r->gradient_flops = e->flops_total - flops0;
+        krb::engine_selfcheck_raise(e);
     });
 }
 

@@ -102,6 +102,23 @@ class CudaEngine:
     implicit = False
     kfactored_mode = False
 
+    # -- SelfCheckEngine (solver.hpp:67-99) on the device -------------------
+    def set_selfcheck(self, reference, every=500, tol=1e-8):
+        """Replay every `every`-th product through `reference` (an engine over
+        the same boards, typically CudaEngine.kron: the block formula) and
+        compare on the device; a deviation above tol (1 + max|expect|) makes
+        the next host call raise ContractError.  reference=None: off."""
+        N.check(N.cuda().kr_engine_set_selfcheck(self._h, reference.handle if reference else None, int(every),
+                                                 float(tol)))
+        self._sc_ref = reference  # keep the reference engine alive
+
+    def selfcheck_status(self):
+        """(checks made, worst err / (tol (1 + max|expect|))); raises
+        ContractError if a check failed."""
+        n, w = C.c_int64(), C.c_double()
+        N.check(N.cuda().kr_engine_selfcheck_status(self._h, C.byref(n), C.byref(w)))
+        return n.value, w.value
+
     def _attach(self, h, device, nboards):
         self._h = h
         dims = np.zeros(8, np.int64)

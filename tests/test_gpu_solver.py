@@ -168,3 +168,36 @@ def test_knobs_keep_the_bits(knob, monkeypatch):
     trajectory bitwise."""
     monkeypatch.setenv(*knob)
     gap_trajectory_case("golden", {}, "b", 200)
+
+
+def test_selfcheck_mode_passes_and_catches_a_tampered_factor():
+    """SelfCheckEngine (solver.hpp:67-99) on the device: the factored engine's
+    products replayed through the implicit engine (the block formula) pass at
+    the reference's tolerance; a U entry multiplied by 3 (the reference's own
+    fault injection, test_solver.cpp:217-232) fails the first check with
+    ContractError, through the host calls and through a solver run."""
+    from paper_2112_03804_b200 import ContractError, CudaEngine
+    p = H.builtin("twenty_card")
+    f = p.sparsify("b", True)
+    eng, ref = CudaEngine(f), CudaEngine.kron(p)
+    eng.set_selfcheck(ref, every=1, tol=1e-8)
+    x = np.random.default_rng(0).standard_normal(f.cols)
+    eng.Ax(x)
+    eng.ATx(np.ones(f.rows))
+    r = solver_for([(p, f)]).run(DcfrParams(max_iters=5))  # its own engine: unchecked
+    s = solver_for([(p, f)])
+    s.engine.set_selfcheck(ref, every=7, tol=1e-8)
+    r2 = s.run(DcfrParams(max_iters=40, checkpoint_every=10))
+    assert bits_equal(r2.trace_expl, solver_for([(p, f)]).run(DcfrParams(max_iters=40, checkpoint_every=10)).trace_expl)
+    checks, worst = s.engine.selfcheck_status()
+    assert checks == (2 * 40 + 2 * 4 + 6) // 7 and worst < 1e-3
+    # fault injection: one U entry x 3
+    arr = f.factors()
+    uo, ui, uv = arr["u"]
+    uv = uv.copy()
+    uv[len(uv) // 2] *= 3.0
+    bad = CudaEngine(dict(arr, rows=f.rows, cols=f.cols, k=f.k, u=(uo, ui, uv)))
+    bad.set_selfcheck(ref, every=500, tol=1e-8)
+    with pytest.raises(ContractError):
+        bad.Ax(x)   # call 0 is checked (calls_++ % every_ == 0)
+    assert r.iterations == 5
