@@ -65,7 +65,6 @@ namespace {
 constexpr int kKfWarps = 8;         // warps (SELL slices) per row-kernel CTA
 constexpr int kKfMaxSeq = 1024;     // F / S CSR rows and columns
 constexpr int kKfMaxHands = 1364;   // list entries address up to 48 (m + 1) bytes of shared memory (< 64 KB)
-constexpr int kKfDepth = 2;
 constexpr int kKfLong = 256;
 constexpr int kKfFoldThreads = 256;  // fold kernels: staging threads (two of them then fold; 128 measured slower)       // longer list rows take the warp-cooperative path         // 16-byte list vectors in flight per lane
 
@@ -92,6 +91,7 @@ struct KfBoard {
     int maxSa, maxSb;                 // largest S row / S column (shared-memory layout)
     int64_t rowOff, colOff;           // y / x offsets of the board
     int64_t zOff, zfOff;              // t / z buffer [n1][nAlive] and z_f buffer [n1] offsets
+    int64_t h1Off, h2Off;             // first player-1 / player-2 hand over all boards (sequence-major inputs)
     const double *l1, *l2;
     const int32_t* aliveRows;         // [nAlive]
     const int32_t* aliveEnd;          // [nAlive]: next alive row, or m1 (Uᵀ row range)
@@ -128,18 +128,17 @@ __device__ __forceinline__ double2 smd2(const char* smb, uint32_t off) {
     return *reinterpret_cast<const double2*>(smb + off);
 }
 
-// Stream one lane's vectors of a slice (kKfDepth loads in flight), calling
+// Stream one lane's vectors of a slice (two loads in flight), calling
 // f(entry) for the 8 entries of each vector in order.
 template <class F>
 __device__ __forceinline__ void kf_stream(const uint4* __restrict__ src, int nv, F&& f) {
-    uint4 buf[kKfDepth];
-#pragma unroll
-    for (int d = 0; d < kKfDepth; ++d) buf[d] = d < nv ? __ldg(src + 32 * d) : make_uint4(0, 0, 0, 0);
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    uint4 c0 = nv > 0 ? __ldg(src) : z;
+    uint4 c1 = nv > 1 ? __ldg(src + 32) : z;
     for (int q = 0; q < nv; ++q) {
-        const uint4 c = buf[0];
-#pragma unroll
-        for (int d = 0; d + 1 < kKfDepth; ++d) buf[d] = buf[d + 1];
-        buf[kKfDepth - 1] = q + kKfDepth < nv ? __ldg(src + 32 * (q + kKfDepth)) : make_uint4(0, 0, 0, 0);
+        const uint4 c = c0;
+        c0 = c1;
+        c1 = q + 2 < nv ? __ldg(src + 32 * (q + 2)) : z;
         f(c.x & 0xFFFFu);
         f(c.x >> 16);
         f(c.y & 0xFFFFu);
@@ -247,12 +246,40 @@ __device__ __forceinline__ double kf_fold(double* v, int n, double acc, bool sto
     return acc;
 }
 
+// ---- input transpose -------------------------------------------------------
+// The row kernels stage whole input columns (one sequence, every hand of a
+// board); a sequence-major copy of the input, out[s M + J] = in[J n + s] over
+// all boards' hands J (hands [J0, J1) of a board-group launch), makes those
+// loads contiguous.  32 hands per block through shared memory: both the loads
+// (32 n contiguous doubles) and the stores (32 per sequence) are coalesced.
+__global__ void __launch_bounds__(256) k_kf_seqmajor(const double* __restrict__ in, int64_t M, int n, int64_t J0,
+                                                     int64_t J1, double* __restrict__ out) {
+    pdl_entry();
+    extern __shared__ double tile[];  // [32][n]
+    const int64_t h0 = J0 + int64_t(blockIdx.x) * 32;
+    const int nh = int(lmin(32, J1 - h0));
+    if (nh <= 0) return;
+    for (int q = threadIdx.x; q < nh * n; q += blockDim.x) tile[q] = in[h0 * n + q];
+    __syncthreads();
+    for (int q = threadIdx.x; q < n * 32; q += blockDim.x) {
+        const int s = q >> 5, l = q & 31;
+        if (l < nh) out[int64_t(s) * M + h0 + l] = tile[l * n + s];
+    }
+}
+
+// Slices [lo, hi) of CTA g out of gs for a list of nsl slices (balanced).
+__device__ __forceinline__ void kf_range(int g, int gs, int nsl, int& lo, int& hi) {
+    lo = int(int64_t(g) * nsl / gs);
+    hi = int(int64_t(g + 1) * nsl / gs);
+}
+
 // ---- A x -------------------------------------------------------------------
 // One Vᵀ entry's terms added to acc in order (S entries of the row), for rows
 // with several S entries or inputs outside the rewrite's premise (literal
 // expressions of rows_vt); kept out of line so the common path stays lean.
-__device__ __noinline__ double kf_vt_add(const KfBoard& B, const char* smb, const double* xb, uint32_t off, int s0,
-                                         int nSa, int m2p, bool fast, double acc) {
+// xs: the board's sequence-major input, column c at xs + c * M2.
+__device__ __noinline__ double kf_vt_add(const KfBoard& B, const char* smb, const double* xs, int64_t M2,
+                                         uint32_t off, int s0, int nSa, int m2p, bool fast, double acc) {
     if (fast) {
         for (int e = 0; e < nSa; ++e) acc = acc + smd(smb, off + uint32_t(e) * 32u * uint32_t(m2p));
         return acc;
@@ -260,12 +287,12 @@ __device__ __noinline__ double kf_vt_add(const KfBoard& B, const char* smb, cons
     const int q = int(off >> 3), v = q / m2p, j = q - v * m2p;
     if (j >= B.m2) return acc;
     const double scale = B.l2[j] * kf_yval(v);
-    for (int e = 0; e < nSa; ++e) acc = acc + (scale * B.sval[s0 + e]) * xb[int64_t(j) * B.n2 + B.scol[s0 + e]];
+    for (int e = 0; e < nSa; ++e) acc = acc + (scale * B.sval[s0 + e]) * xs[B.scol[s0 + e] * M2 + j];
     return acc;
 }
 // The terms of 8 entries (one vector), in order, into o[8 * nSa].
-__device__ __noinline__ void kf_vt_terms8(const KfBoard& B, const char* smb, const double* xb, uint4 c, int s0, int nSa,
-                                          int m2p, bool fast, double* o) {
+__device__ __noinline__ void kf_vt_terms8(const KfBoard& B, const char* smb, const double* xs, int64_t M2, uint4 c,
+                                          int s0, int nSa, int m2p, bool fast, double* o) {
     const uint32_t w[4] = {c.x, c.y, c.z, c.w};
     for (int u = 0; u < 8; ++u) {
         const uint32_t off = u & 1 ? w[u >> 1] >> 16 : w[u >> 1] & 0xFFFFu;
@@ -279,19 +306,19 @@ __device__ __noinline__ void kf_vt_terms8(const KfBoard& B, const char* smb, con
             continue;
         }
         const double scale = B.l2[j] * kf_yval(v);
-        for (int e = 0; e < nSa; ++e)
-            o[u * nSa + e] = (scale * B.sval[s0 + e]) * xb[int64_t(j) * B.n2 + B.scol[s0 + e]];
+        for (int e = 0; e < nSa; ++e) o[u * nSa + e] = (scale * B.sval[s0 + e]) * xs[B.scol[s0 + e] * M2 + j];
     }
 }
 
 // Vᵀ rows of chain a: t(r) = Σ_j↑ Σ_e ((λ2_j·Y)·S_e)·x[j, col_e]  (rows_vt).
-// CTAs g < gs take W slices each (one warp per slice); CTA gs takes the long
-// rows, one warp per row: each round the 32 lanes load 256 entries, produce
-// their terms in order into the warp's buffer, and all lanes add them in
-// order (warp-uniform adds).
+// CTAs g < gs take a balanced range of slices (warps loop over them); CTA gs
+// takes the long rows, one warp per row: each round the 32 lanes load 256
+// entries, produce their terms in order into the warp's buffer, and all lanes
+// add them in order (warp-uniform adds).  xT: sequence-major input.
 template <int W>
 __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __restrict__ boards, int b0, int gy, int gs,
-                                                    const double* __restrict__ x, double* __restrict__ tz) {
+                                                            const double* __restrict__ xT, int64_t M2,
+                                                            double* __restrict__ tz) {
     pdl_entry();
     extern __shared__ __align__(16) double sm[];
     const char* smb = reinterpret_cast<const char*>(sm);
@@ -299,21 +326,23 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
     const KfBoard& B = boards[b0 + blockIdx.y];
     const int a = blockIdx.x / gy, g = blockIdx.x - a * gy;
     const int s0 = B.sptr[a], nSa = B.sptr[a + 1] - s0;
-    const int nA = B.nAlive, m2 = B.m2, n2 = B.n2, m2p = m2 + 1;
+    const int nA = B.nAlive, m2 = B.m2, m2p = m2 + 1;
     const bool longCta = g == gs;
-    if (nSa == 0 || nA == 0 || (longCta ? B.yr.nlong == 0 : g * W >= B.yr.nsl)) return;
-    const double* xb = x + B.colOff;
+    int lo = 0, hi = 0;
+    if (!longCta) kf_range(g, gs, B.yr.nsl, lo, hi);
+    if (nSa == 0 || nA == 0 || (longCta ? B.yr.nlong == 0 : lo >= hi)) return;
+    const double* xs = xT + B.h2Off;
     if (threadIdx.x == 0) okAll = 1;
     __syncthreads();
     int ok = B.fast;
     for (int e = 0; e < nSa; ++e) {
         double* QY = sm + size_t(e) * 4 * m2p;
-        const int col = B.scol[s0 + e];
+        const double* col = xs + B.scol[s0 + e] * M2;
         const double sv = B.sval[s0 + e];
         for (int j = threadIdx.x; j < m2p; j += 32 * W) {
             double q = 0.0;
             if (j < m2) {
-                const double xv = xb[int64_t(j) * n2 + col];
+                const double xv = col[j];
                 ok &= kf_ok(xv);
                 q = (B.l2[j] * sv) * xv;
             }
@@ -348,7 +377,7 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
                         o[6] = smd(smb, c.w & 0xFFFFu);
                         o[7] = smd(smb, c.w >> 16);
                     } else {
-                        kf_vt_terms8(B, smb, xb, c, s0, nSa, m2p, fast, o);
+                        kf_vt_terms8(B, smb, xs, M2, c, s0, nSa, m2p, fast, o);
                     }
                 }
                 __syncwarp();
@@ -359,18 +388,18 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
         }
         return;
     }
-    const int s = g * W + warp;
-    if (s >= B.yr.nsl) return;
-    const int p0 = B.yr.ptr[s], nv = (B.yr.ptr[s + 1] - p0) >> 5;
-    const int r = B.yr.perm[32 * s + lane];
-    const uint4* src = B.yr.ent + p0 + lane;
-    double acc = 0.0;
-    if (fast && nSa == 1) {
-        kf_stream(src, nv, [&](uint32_t off) { acc = acc + smd(smb, off); });
-    } else {
-        kf_stream(src, nv, [&](uint32_t off) { acc = kf_vt_add(B, smb, xb, off, s0, nSa, m2p, fast, acc); });
+    for (int s = lo + warp; s < hi; s += W) {
+        const int p0 = B.yr.ptr[s], nv = (B.yr.ptr[s + 1] - p0) >> 5;
+        const int r = B.yr.perm[32 * s + lane];
+        const uint4* src = B.yr.ent + p0 + lane;
+        double acc = 0.0;
+        if (fast && nSa == 1) {
+            kf_stream(src, nv, [&](uint32_t off) { acc = acc + smd(smb, off); });
+        } else {
+            kf_stream(src, nv, [&](uint32_t off) { acc = kf_vt_add(B, smb, xs, M2, off, s0, nSa, m2p, fast, acc); });
+        }
+        if (r >= 0) tz[B.zOff + int64_t(a) * nA + r] = acc;
     }
-    if (r >= 0) tz[B.zOff + int64_t(a) * nA + r] = acc;
 }
 
 // The ordered folds of A x for player-1 sequence a: all threads stage the
@@ -379,13 +408,13 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
 // t_f(a) = Σ_j↑ Σ_e (λ2_j·F_e)·x[j, col_e] (rows_vt), side by side.
 // shared: v[nAlive] | f[m2 · nFa]
 __global__ void __launch_bounds__(kKfFoldThreads) k_kfa_fold(const KfBoard* __restrict__ boards, int b0,
-                                                   const double* __restrict__ x, double* __restrict__ tz,
-                                                   double* __restrict__ zf) {
+                                                              const double* __restrict__ xT, int64_t M2,
+                                                              double* __restrict__ tz, double* __restrict__ zf) {
     pdl_entry();
     extern __shared__ __align__(16) double sm[];
     const KfBoard& B = boards[b0 + blockIdx.y];
     const int a = blockIdx.x;
-    const int nA = B.nAlive, m2 = B.m2, n2 = B.n2;
+    const int nA = B.nAlive, m2 = B.m2;
     const bool chain = B.sptr[a + 1] > B.sptr[a] && nA > 0;
     const bool fA = B.hasF[a] != 0;
     if (!chain && !fA) return;
@@ -393,13 +422,13 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kfa_fold(const KfBoard* __re
     double* v = sm;
     double* f = sm + nA;
     double* t = tz + B.zOff + int64_t(a) * nA;
-    const double* xb = x + B.colOff;
+    const double* xs = xT + B.h2Off;
     if (chain)
         for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) v[r] = t[r];
     if (fA)
         for (int k = threadIdx.x; k < m2 * nFa; k += kKfFoldThreads) {
             const int j = nFa == 1 ? k : k / nFa, e = k - j * nFa;
-            f[k] = (B.l2[j] * B.fval[f0 + e]) * xb[int64_t(j) * n2 + B.fcol[f0 + e]];
+            f[k] = (B.l2[j] * B.fval[f0 + e]) * xs[B.fcol[f0 + e] * M2 + j];
         }
     __syncthreads();
     if (threadIdx.x == 0 && chain) kf_fold<false>(v, nA, -0.0, true);
@@ -413,65 +442,72 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kfa_fold(const KfBoard* __re
 // blocked hands j ascending: ((−λ1_i)·λ2_j·F_e)·x[j, col_e]  (rows_ua)
 template <int W>
 __global__ void __launch_bounds__(32 * W) k_kfa_ua(const KfBoard* __restrict__ boards, int b0, int gu,
-                                                    const double* __restrict__ x, const double* __restrict__ tz,
-                                                    const double* __restrict__ zf, double* __restrict__ y) {
+                                                    const double* __restrict__ xT, int64_t M2,
+                                                    const double* __restrict__ tz, const double* __restrict__ zf,
+                                                    double* __restrict__ y) {
     pdl_entry();
     extern __shared__ __align__(16) double sm[];
     const char* smb = reinterpret_cast<const char*>(sm);
     const KfBoard& B = boards[b0 + blockIdx.y];
     const int a = blockIdx.x / gu, g = blockIdx.x - a * gu;
-    if (g * W >= B.b2.nsl) return;
-    const int m2 = B.m2, n1 = B.n1, n2 = B.n2, nA = B.nAlive;
+    int lo, hi;
+    kf_range(g, gu, B.b2.nsl, lo, hi);
+    if (lo >= hi) return;
+    const int m2 = B.m2, n1 = B.n1, nA = B.nAlive;
     const int f0 = B.fptr[a], nFa = B.fptr[a + 1] - f0;
     double2* PR = reinterpret_cast<double2*>(sm);
     double* xF1 = sm + 2 * (m2 + 1);
     if (nFa > 0) {
-        const double* xb = x + B.colOff;
+        const double* xs = xT + B.h2Off;
+        const double* c0 = xs + B.fcol[f0] * M2;
         for (int j = threadIdx.x; j <= m2; j += 32 * W) {
             if (j == m2) {
                 PR[m2] = make_double2(0.0, 0.0);
                 continue;
             }
-            PR[j] = make_double2(B.l2[j], xb[int64_t(j) * n2 + B.fcol[f0]]);
-            for (int e = 1; e < nFa; ++e) xF1[size_t(e - 1) * m2 + j] = xb[int64_t(j) * n2 + B.fcol[f0 + e]];
+            PR[j] = make_double2(B.l2[j], c0[j]);
+            for (int e = 1; e < nFa; ++e) xF1[size_t(e - 1) * m2 + j] = xs[B.fcol[f0 + e] * M2 + j];
         }
         __syncthreads();
     }
-    const int lane = threadIdx.x & 31, s = g * W + (threadIdx.x >> 5);
-    if (s >= B.b2.nsl) return;
-    const int i = B.b2.perm[32 * s + lane];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool chain = B.sptr[a + 1] > B.sptr[a] && nA > 0;
-    const double v = i >= 0 ? B.l1[i] : 0.0;
-    double acc = 0.0;
-    if (i >= 0 && v != 0.0) {
-        const int rp = B.rankPrev[i];
-        if (chain && rp >= 0) acc = acc + v * tz[B.zOff + int64_t(a) * nA + rp];
-        if (B.hasF[a]) acc = acc + v * zf[B.zfOff + a];
-    }
-    if (nFa > 0) {
-        const int p0 = B.b2.ptr[s], nv = (B.b2.ptr[s + 1] - p0) >> 5;
-        const uint4* src = B.b2.ent + p0 + lane;
-        const double nv1 = -v;
-        if (nFa == 1) {
-            const double fv = B.fval[f0];
-            kf_stream(src, nv, [&](uint32_t off) {
-                const double2 p = smd2(smb, off);
-                const double w = (nv1 * p.x) * fv;
-                acc = acc + w * p.y;
-            });
-        } else {
-            kf_stream(src, nv, [&](uint32_t off) {
-                const int j = int(off >> 4);
-                if (j >= m2) return;
-                const double scale = nv1 * PR[j].x;
-                for (int e = 0; e < nFa; ++e) {
-                    const double w = scale * B.fval[f0 + e];
-                    acc = acc + w * (e == 0 ? PR[j].y : xF1[size_t(e - 1) * m2 + j]);
-                }
-            });
+    const bool fA = B.hasF[a] != 0;
+    const double zfa = fA ? zf[B.zfOff + a] : 0.0;
+    const double fv = nFa > 0 ? B.fval[f0] : 0.0;
+    for (int s = lo + warp; s < hi; s += W) {
+        const int i = B.b2.perm[32 * s + lane];
+        const double v = i >= 0 ? B.l1[i] : 0.0;
+        double acc = 0.0;
+        if (i >= 0 && v != 0.0) {
+            const int rp = B.rankPrev[i];
+            if (chain && rp >= 0) acc = acc + v * tz[B.zOff + int64_t(a) * nA + rp];
+            if (fA) acc = acc + v * zfa;
         }
+        if (nFa > 0) {
+            const int p0 = B.b2.ptr[s], nv = (B.b2.ptr[s + 1] - p0) >> 5;
+            const uint4* src = B.b2.ent + p0 + lane;
+            const double nv1 = -v;
+            if (nFa == 1) {
+                kf_stream(src, nv, [&](uint32_t off) {
+                    const double2 p = smd2(smb, off);
+                    const double w = (nv1 * p.x) * fv;
+                    acc = acc + w * p.y;
+                });
+            } else {
+                kf_stream(src, nv, [&](uint32_t off) {
+                    const int j = int(off >> 4);
+                    if (j >= m2) return;
+                    const double scale = nv1 * PR[j].x;
+                    for (int e = 0; e < nFa; ++e) {
+                        const double w = scale * B.fval[f0 + e];
+                        acc = acc + w * (e == 0 ? PR[j].y : xF1[size_t(e - 1) * m2 + j]);
+                    }
+                });
+            }
+        }
+        if (i >= 0) y[B.rowOff + int64_t(i) * n1 + a] = acc;
     }
-    if (i >= 0) y[B.rowOff + int64_t(i) * n1 + a] = acc;
 }
 
 // ---- Aᵀ y ------------------------------------------------------------------
@@ -479,30 +515,30 @@ __global__ void __launch_bounds__(32 * W) k_kfa_ua(const KfBoard* __restrict__ b
 // Uᵀ rows of chain d, s(r) = Σ_{i ∈ [alive r, alive r+1)} λ1_i·y[i, d], and
 // the F-column terms λ1_i·y[i, d] (rows_ut) into shared memory; thread 0 then
 // solves the chain backward (z(r) = s(r) + z(r+1), engine.hpp:44-54) and
-// thread 32 folds the F column Σ_i↑, side by side.
+// thread 32 folds the F column Σ_i↑, side by side.  yT: sequence-major input.
 // shared: v[nAlive] | f[m1]
 __global__ void __launch_bounds__(kKfFoldThreads) k_kft_fold(const KfBoard* __restrict__ boards, int b0,
-                                                   const double* __restrict__ y, double* __restrict__ tz,
-                                                   double* __restrict__ zf) {
+                                                              const double* __restrict__ yT, int64_t M1,
+                                                              double* __restrict__ tz, double* __restrict__ zf) {
     pdl_entry();
     extern __shared__ __align__(16) double sm[];
     const KfBoard& B = boards[b0 + blockIdx.y];
     const int d = blockIdx.x;
-    const int nA = B.nAlive, m1 = B.m1, n1 = B.n1;
+    const int nA = B.nAlive, m1 = B.m1;
     const bool chain = B.sptr[d + 1] > B.sptr[d] && nA > 0;
     const bool fD = B.hasF[d] != 0;
     if (!chain && !fD) return;
-    const double* yb = y + B.rowOff;
+    const double* yd = yT + d * M1 + B.h1Off;
     double* v = sm;
     double* f = sm + nA;
     if (chain)
         for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) {
             double acc = 0.0;
-            for (int i = B.aliveRows[r]; i < B.aliveEnd[r]; ++i) acc = acc + B.l1[i] * yb[int64_t(i) * n1 + d];
+            for (int i = B.aliveRows[r]; i < B.aliveEnd[r]; ++i) acc = acc + B.l1[i] * yd[i];
             v[r] = acc;
         }
     if (fD)
-        for (int i = threadIdx.x; i < m1; i += kKfFoldThreads) f[i] = B.l1[i] * yb[int64_t(i) * n1 + d];
+        for (int i = threadIdx.x; i < m1; i += kKfFoldThreads) f[i] = B.l1[i] * yd[i];
     __syncthreads();
     if (threadIdx.x == 0 && chain) kf_fold<true>(v, nA, -0.0, true);
     if (threadIdx.x == 32 && fD) zf[B.zfOff + d] = kf_fold<false>(f, m1, 0.0, false);
@@ -517,34 +553,39 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kft_fold(const KfBoard* __re
 // then V: alive r ascending, ((λ2_j·Y)·S_e)·z(r, row_e); then λ2_j·F_e·z_f  (rows_av)
 template <int W>
 __global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ boards, int b0, int gv,
-                                                    const double* __restrict__ y, const double* __restrict__ tz,
-                                                    const double* __restrict__ zf, double* __restrict__ x) {
+                                                    const double* __restrict__ yT, int64_t M1,
+                                                    const double* __restrict__ tz, const double* __restrict__ zf,
+                                                    double* __restrict__ x) {
     pdl_entry();
     extern __shared__ __align__(16) double sm[];
     const char* smb = reinterpret_cast<const char*>(sm);
     __shared__ int okAll;
     const KfBoard& B = boards[b0 + blockIdx.y];
     const int b = blockIdx.x / gv, g = blockIdx.x - b * gv;
-    if (g * W >= B.b1.nsl) return;
-    const int m1 = B.m1, n1 = B.n1, n2 = B.n2, nA = B.nAlive;
+    int lo, hi;
+    kf_range(g, gv, B.b1.nsl, lo, hi);
+    if (lo >= hi) return;
+    const int m1 = B.m1, n2 = B.n2, nA = B.nAlive;
     const int m1p = m1 + 1, nAp = nA + 1;
     const int f0 = B.fcptr[b], nFb = B.fcptr[b + 1] - f0;
     const int s0 = B.scptr[b], nSb = B.scptr[b + 1] - s0;
     double2* PR = reinterpret_cast<double2*>(sm);
     double* ZY = sm + 2 * m1p;                                   // [maxSb][4][nAp]
     double* yF1 = ZY + size_t(4) * nAp * (B.maxSb > 0 ? B.maxSb : 1);
-    const double* yb = y + B.rowOff;
+    const double* ys = yT + B.h1Off;
     if (threadIdx.x == 0) okAll = 1;
     __syncthreads();
-    if (nFb > 0)
+    if (nFb > 0) {
+        const double* c0 = ys + B.fcrow[f0] * M1;
         for (int i = threadIdx.x; i <= m1; i += 32 * W) {
             if (i == m1) {
                 PR[m1] = make_double2(0.0, 0.0);
                 continue;
             }
-            PR[i] = make_double2(B.l1[i], yb[int64_t(i) * n1 + B.fcrow[f0]]);
-            for (int e = 1; e < nFb; ++e) yF1[size_t(e - 1) * m1 + i] = yb[int64_t(i) * n1 + B.fcrow[f0 + e]];
+            PR[i] = make_double2(B.l1[i], c0[i]);
+            for (int e = 1; e < nFb; ++e) yF1[size_t(e - 1) * m1 + i] = ys[B.fcrow[f0 + e] * M1 + i];
         }
+    }
     int ok = B.fast;
     if (nA > 0)
         for (int e = 0; e < nSb; ++e) {
@@ -561,64 +602,66 @@ __global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ b
         }
     if (!ok) okAll = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31, s = g * W + (threadIdx.x >> 5);
-    if (s >= B.b1.nsl) return;
-    const int j = B.b1.perm[32 * s + lane];
-    const double l2 = j >= 0 ? B.l2[j] : 0.0;
-    double acc = 0.0;
-    if (nFb > 0) {   // Âᵀ
-        const int p0 = B.b1.ptr[s], nv = (B.b1.ptr[s + 1] - p0) >> 5;
-        const uint4* src = B.b1.ent + p0 + lane;
-        if (nFb == 1) {
-            const double fv = B.fcval[f0];
-            kf_stream(src, nv, [&](uint32_t off) {
-                const double2 p = smd2(smb, off);
-                const double w = (-p.x * l2) * fv;
-                acc = acc + w * p.y;
-            });
-        } else {
-            kf_stream(src, nv, [&](uint32_t off) {
-                const int i = int(off >> 4);
-                if (i >= m1) return;
-                const double scale = -PR[i].x * l2;
-                for (int e = 0; e < nFb; ++e) {
-                    const double w = scale * B.fcval[f0 + e];
-                    acc = acc + w * (e == 0 ? PR[i].y : yF1[size_t(e - 1) * m1 + i]);
-                }
-            });
-        }
-    }
-    if (nSb > 0 && nA > 0) {   // V, S columns
-        const int p0 = B.yc.ptr[s], nv = (B.yc.ptr[s + 1] - p0) >> 5;
-        const uint4* src = B.yc.ent + p0 + lane;
-        if (okAll && nSb == 1) {
-            // ((λ2·Y)·S)·z == (λ2·S)·(Y·z): one multiply, one add
-            const double P0 = l2 * B.scval[s0];
-            kf_stream(src, nv, [&](uint32_t off) { acc = acc + P0 * smd(smb, off); });
-        } else if (okAll) {
-            kf_stream(src, nv, [&](uint32_t off) {
-                for (int e = 0; e < nSb; ++e)
-                    acc = acc + (l2 * B.scval[s0 + e]) * smd(smb, off + uint32_t(e) * 32u * uint32_t(nAp));
-            });
-        } else {
-            kf_stream(src, nv, [&](uint32_t off) {
-                const int q = int(off >> 3) - 2 * m1p, v = q / nAp, r = q - v * nAp;
-                if (r >= nA) return;
-                const double scale = l2 * kf_yval(v);
-                for (int e = 0; e < nSb; ++e) {
-                    const double w = scale * B.scval[s0 + e];
-                    acc = acc + w * tz[B.zOff + int64_t(B.scrow[s0 + e]) * nA + r];
-                }
-            });
-        }
-    }
-    if (j >= 0) {
-        if (l2 != 0.0)   // V, F columns
-            for (int e = 0; e < nFb; ++e) {
-                const int d = B.fcrow[f0 + e];
-                if (B.hasF[d]) acc = acc + (l2 * B.fcval[f0 + e]) * zf[B.zfOff + d];
+    const bool zok = okAll != 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double fv = nFb > 0 ? B.fcval[f0] : 0.0;
+    for (int s = lo + warp; s < hi; s += W) {
+        const int j = B.b1.perm[32 * s + lane];
+        const double l2 = j >= 0 ? B.l2[j] : 0.0;
+        double acc = 0.0;
+        if (nFb > 0) {   // Âᵀ
+            const int p0 = B.b1.ptr[s], nv = (B.b1.ptr[s + 1] - p0) >> 5;
+            const uint4* src = B.b1.ent + p0 + lane;
+            if (nFb == 1) {
+                kf_stream(src, nv, [&](uint32_t off) {
+                    const double2 p = smd2(smb, off);
+                    const double w = (-p.x * l2) * fv;
+                    acc = acc + w * p.y;
+                });
+            } else {
+                kf_stream(src, nv, [&](uint32_t off) {
+                    const int i = int(off >> 4);
+                    if (i >= m1) return;
+                    const double scale = -PR[i].x * l2;
+                    for (int e = 0; e < nFb; ++e) {
+                        const double w = scale * B.fcval[f0 + e];
+                        acc = acc + w * (e == 0 ? PR[i].y : yF1[size_t(e - 1) * m1 + i]);
+                    }
+                });
             }
-        x[B.colOff + int64_t(j) * n2 + b] = acc;
+        }
+        if (nSb > 0 && nA > 0) {   // V, S columns
+            const int p0 = B.yc.ptr[s], nv = (B.yc.ptr[s + 1] - p0) >> 5;
+            const uint4* src = B.yc.ent + p0 + lane;
+            if (zok && nSb == 1) {
+                // ((λ2·Y)·S)·z == (λ2·S)·(Y·z): one multiply, one add
+                const double P0 = l2 * B.scval[s0];
+                kf_stream(src, nv, [&](uint32_t off) { acc = acc + P0 * smd(smb, off); });
+            } else if (zok) {
+                kf_stream(src, nv, [&](uint32_t off) {
+                    for (int e = 0; e < nSb; ++e)
+                        acc = acc + (l2 * B.scval[s0 + e]) * smd(smb, off + uint32_t(e) * 32u * uint32_t(nAp));
+                });
+            } else {
+                kf_stream(src, nv, [&](uint32_t off) {
+                    const int q = int(off >> 3) - 2 * m1p, v = q / nAp, r = q - v * nAp;
+                    if (r >= nA) return;
+                    const double scale = l2 * kf_yval(v);
+                    for (int e = 0; e < nSb; ++e) {
+                        const double w = scale * B.scval[s0 + e];
+                        acc = acc + w * tz[B.zOff + int64_t(B.scrow[s0 + e]) * nA + r];
+                    }
+                });
+            }
+        }
+        if (j >= 0) {
+            if (l2 != 0.0)   // V, F columns
+                for (int e = 0; e < nFb; ++e) {
+                    const int d = B.fcrow[f0 + e];
+                    if (B.hasF[d]) acc = acc + (l2 * B.fcval[f0 + e]) * zf[B.zfOff + d];
+                }
+            x[B.colOff + int64_t(j) * n2 + b] = acc;
+        }
     }
 }
 
@@ -936,6 +979,9 @@ struct KfState {
     int gy = 1, gs = 0, gu = 1, gv = 1;    // row-kernel CTAs per sequence (gs: slice CTAs of the Vᵀ rows)
     double* tz[2] = {nullptr, nullptr};   // t / z per direction (A x, Aᵀy may run concurrently)
     double* zf[2] = {nullptr, nullptr};
+    double* inT[2] = {nullptr, nullptr};  // sequence-major input per direction
+    int64_t M1 = 0, M2 = 0;               // hands of each player over all boards
+    std::vector<int64_t> hOff1, hOff2;    // per board (+ total)
 };
 
 void kf_destroy(KfState* k) {
@@ -944,31 +990,40 @@ void kf_destroy(KfState* k) {
     delete k;
 }
 
-// Boards [b0, b1) of one product: A x = Vᵀ rows, folds, [U|Â] rows;
-// Aᵀy = folds (Uᵀ rows and chains), [Âᵀ|V] rows.
+// Boards [b0, b1) of one product: the input made sequence-major, then
+// A x = Vᵀ rows, folds, [U|Â] rows; Aᵀy = folds (Uᵀ rows and chains), [Âᵀ|V] rows.
 void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
     KfState* k = e->kf;
     if (b1 < 0) b1 = k->nb;
     if (b1 <= b0) return;
     const unsigned nb = unsigned(b1 - b0);
     constexpr int T = 32 * kKfWarps;
+    const int64_t M = dir == 0 ? k->M2 : k->M1;
+    const int n = dir == 0 ? k->n2 : k->n1;
+    const int64_t J0 = (dir == 0 ? k->hOff2 : k->hOff1)[size_t(b0)], J1 = (dir == 0 ? k->hOff2 : k->hOff1)[size_t(b1)];
+    double* inT = k->inT[dir];
+    krb::launch(k_kf_seqmajor, unsigned((J1 - J0 + 31) / 32), 256, size_t(32) * n * sizeof(double), s, in, M, n, J0, J1,
+                inT);
+    KR_CK_LAUNCH();
     if (dir == 0) {
         krb::launch(k_kfa_vt<kKfWarps>, dim3(unsigned(k->n1 * k->gy), nb), T, k->smVT, s, k->dBoards, b0, k->gy, k->gs,
-                    in, k->tz[0]);
+                    inT, M, k->tz[0]);
         KR_CK_LAUNCH();
-        krb::launch(k_kfa_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFA, s, k->dBoards, b0, in, k->tz[0], k->zf[0]);
+        krb::launch(k_kfa_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFA, s, k->dBoards, b0, inT, M, k->tz[0],
+                    k->zf[0]);
         KR_CK_LAUNCH();
-        krb::launch(k_kfa_ua<kKfWarps>, dim3(unsigned(k->n1 * k->gu), nb), T, k->smUA, s, k->dBoards, b0, k->gu, in,
-                    k->tz[0], k->zf[0], out);
+        krb::launch(k_kfa_ua<kKfWarps>, dim3(unsigned(k->n1 * k->gu), nb), T, k->smUA, s, k->dBoards, b0, k->gu, inT,
+                    M, k->tz[0], k->zf[0], out);
+        KR_CK_LAUNCH();
+        e->launches += 4;
+    } else {
+        krb::launch(k_kft_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFT, s, k->dBoards, b0, inT, M, k->tz[1],
+                    k->zf[1]);
+        KR_CK_LAUNCH();
+        krb::launch(k_kft_av<kKfWarps>, dim3(unsigned(k->n2 * k->gv), nb), T, k->smAV, s, k->dBoards, b0, k->gv, inT,
+                    M, k->tz[1], k->zf[1], out);
         KR_CK_LAUNCH();
         e->launches += 3;
-    } else {
-        krb::launch(k_kft_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFT, s, k->dBoards, b0, in, k->tz[1], k->zf[1]);
-        KR_CK_LAUNCH();
-        krb::launch(k_kft_av<kKfWarps>, dim3(unsigned(k->n2 * k->gv), nb), T, k->smAV, s, k->dBoards, b0, k->gv, in,
-                    k->tz[1], k->zf[1], out);
-        KR_CK_LAUNCH();
-        e->launches += 2;
     }
 }
 
@@ -1042,6 +1097,12 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
             B.maxSb = H.maxSb;
             B.rowOff = rowOff;
             B.colOff = colOff;
+            B.h1Off = k.M1;
+            B.h2Off = k.M2;
+            k.hOff1.push_back(k.M1);
+            k.hOff2.push_back(k.M2);
+            k.M1 += H.m1;
+            k.M2 += H.m2;
             B.zOff = zOff;
             B.zfOff = int64_t(b) * n1;
             zOff += int64_t(n1) * H.nAlive;
@@ -1094,12 +1155,26 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
         raise_smem_limit(k_kft_av<kKfWarps>, k.smAV);
         raise_smem_limit(k_kfa_fold, k.smFA);
         raise_smem_limit(k_kft_fold, k.smFT);
-        k.gs = (slY + kKfWarps - 1) / kKfWarps;
+        raise_smem_limit(k_kf_seqmajor, size_t(32) * std::max(n1, n2) * sizeof(double));
+        k.hOff1.push_back(k.M1);
+        k.hOff2.push_back(k.M2);
+        // CTAs per sequence: one slice per warp, or up to four rounds of
+        // slices per CTA when the grid would exceed ~6 waves (fewer CTAs
+        // stage the same input columns); slices spread evenly (kf_range)
+        auto ctas = [&](int slices, int seqs) {
+            const int base = (slices + kKfWarps - 1) / kKfWarps;
+            const int64_t total = int64_t(base) * seqs * nb;
+            const int rounds = int(std::min<int64_t>(4, std::max<int64_t>(1, total / (6 * 148))));
+            return std::max(1, (slices + kKfWarps * rounds - 1) / (kKfWarps * rounds));
+        };
+        k.gs = slY > 0 ? ctas(slY, n1) : 0;
         k.gy = k.gs + (anyLong ? 1 : 0);
         if (k.gy == 0) k.gy = 1;
-        k.gu = std::max(1, (slB2 + kKfWarps - 1) / kKfWarps);
-        k.gv = std::max(1, (slB1 + kKfWarps - 1) / kKfWarps);
+        k.gu = ctas(slB2, n1);
+        k.gv = ctas(slB1, n2);
         for (int d = 0; d < 2; ++d) {
+            k.inT[d] = dev_alloc<double>(std::max<int64_t>(d == 0 ? C : R, 1));
+            k.keep.push_back(k.inT[d]);
             k.tz[d] = dev_alloc<double>(std::max<int64_t>(zOff, 1));
             k.zf[d] = dev_alloc<double>(int64_t(nb) * n1);
             k.keep.push_back(k.tz[d]);
