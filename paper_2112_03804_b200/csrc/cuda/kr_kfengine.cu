@@ -65,8 +65,11 @@ namespace {
 constexpr int kKfWarps = 8;         // warps (SELL slices) per row-kernel CTA
 constexpr int kKfMaxSeq = 1024;     // F / S CSR rows and columns
 constexpr int kKfMaxHands = 1364;   // list entries address up to 48 (m + 1) bytes of shared memory (< 64 KB)
-constexpr int kKfLong = 256;
-constexpr int kKfFoldThreads = 256;  // fold kernels: staging threads (two of them then fold; 128 measured slower)       // longer list rows take the warp-cooperative path         // 16-byte list vectors in flight per lane
+constexpr int kKfLong = 256;        // longer list rows take the warp-cooperative path
+// fold kernels: one CTA per sequence, all threads stage, two fold (a
+// warp-per-fold layout with 4 folds per CTA measured slower: its staging is
+// latency-bound, profiles/r02/kf_launches_r02t.txt)
+constexpr int kKfFoldThreads = 256;
 
 // One list-of-lists in SELL-8x32 layout: slice s holds 32 rows (perm[32 s + l]
 // = row of lane l, -1 past the end); vector q (8 entries) of lane l is

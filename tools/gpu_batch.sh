@@ -1,5 +1,5 @@
 # ad-hoc GPU batch (edited per call)
-T=r02r
+T=r02t
 timeout 900 python -m pytest tests/test_gpu_kfengine.py tests/test_gpu_headline.py -q -x -p no:cacheprovider > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
 timeout 600 python tools/kf_probe.py > gpurun_out/${T}_kf_probe.log 2>&1
 for c in 3 2; do
