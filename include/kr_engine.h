@@ -161,6 +161,19 @@ int kr_engine_atx(kr_engine* e, const double* y, int64_t ny, double* x, int64_t 
 int kr_engine_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_t nax, const double* y, int64_t ny,
                    double* atx, int64_t natx);
 
+/* A queue of `count` independent pairs on HOST buffers: axs[i] = A xs[i] and
+ * atxs[i] = A^T ys[i] for i < count (arrays of buffer pointers; the same
+ * buffer may appear in several entries).  Each result is bitwise that of
+ * kr_engine_pair on the same pair.  The input copies of pair i + 1 and the
+ * output copies of pair i - 1 overlap pair i's kernels (two device slots per
+ * direction), so with pinned buffers the bus runs inputs and outputs at once,
+ * back to back.  Inputs are read at unspecified times during the call: no
+ * output buffer may alias any input buffer of the queue.  Returns when every
+ * result is in host memory.  The reference's counterpart is its benchmark
+ * loop of independent products (tools/main.cpp:313-323). */
+int kr_engine_pair_queue(kr_engine* e, int64_t count, const double* const* xs, int64_t nx, double* const* axs,
+                         int64_t nax, const double* const* ys, int64_t ny, double* const* atxs, int64_t natx);
+
 /* Device-pointer variants, enqueued on `stream` (NULL = the engine's own
  * stream); asynchronous with respect to the host. */
 int kr_engine_ax_device(kr_engine* e, const double* x_dev, double* y_dev, void* stream);

@@ -80,6 +80,33 @@ def build_cuda(force=False, verbose=False):
     return out
 
 
+def build_cuda_variant(name, defines=(), replace=None, verbose=False):
+    """lib/libkrcuda_<name>.so: the same sources with extra -D flags and / or
+    some translation units swapped for other files (`replace` maps a source
+    basename to a path).  Loaded with KR_CUDA_LIB_VARIANT=<name>: A/B timing of
+    a kernel change on one box, and the bounds-checked build (KR_CHECKED)."""
+    from concurrent.futures import ThreadPoolExecutor
+    replace = replace or {}
+    out = os.path.join(LIBDIR, f"libkrcuda_{name}.so")
+    objdir = os.path.join(ROOT, "build", f"cuda_{name}")
+    os.makedirs(objdir, exist_ok=True)
+    srcs = [replace.get(os.path.basename(s), s) for s in CUDA_SRC]
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
+    objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in srcs]
+
+    def one(so):
+        cmd = [NVCC, *flags, "-c", "-o", so[1], so[0]]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        list(ex.map(one, zip(srcs, objs)))
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", CXX, "-shared", "-cudart", "static",
+                    "-o", out, *objs, "-ldl"], check=True)
+    return out
+
+
 def build_host(force=False, verbose=False):
     os.makedirs(LIBDIR, exist_ok=True)
     out = os.path.join(LIBDIR, "libkrhost.so")

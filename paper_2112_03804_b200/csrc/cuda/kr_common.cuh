@@ -209,6 +209,21 @@ struct HostPipe {
     double* d_out = nullptr;
     bool made = false;
 };
+
+// kr_engine_pair_queue: a queue of independent pairs.  Each direction has two
+// device slots (input, output); pair i uses slot i % 2, so the input copy of
+// pair i + 1 and the output copy of pair i - 1 run while pair i computes.
+// One H2D stream and one D2H stream carry both directions (one whole-vector
+// copy each: the bus runs at its duplex rate, profiles/r02/zc_probe_r02z.log),
+// one compute stream per direction.
+struct QueuePipe {
+    cudaStream_t cin = nullptr, cout = nullptr, comp[2] = {nullptr, nullptr};
+    cudaEvent_t evIn[2][2] = {}, evDone[2][2] = {}, evOut[2][2] = {};  // [dir][slot]
+    cudaEvent_t evStart = nullptr, evEnd[4] = {};
+    double* in[2][2] = {};
+    double* out[2][2] = {};
+    bool made = false;
+};
 }  // namespace krb
 
 // Engine state (opaque to C callers).
@@ -291,6 +306,7 @@ struct kr_engine {
     // second direction of kr_engine_pair (its own streams and staging
     // buffers, created on first use)
     krb::HostPipe pipe[2];
+    krb::QueuePipe queue;
     // captured host-buffer pipelines, keyed by (direction, host input,
     // host output[, second input, second output]); pinned buffers only
     // (kr_engine_ax / kr_engine_atx: dir 0 / 1; kr_engine_pair: dir 2)

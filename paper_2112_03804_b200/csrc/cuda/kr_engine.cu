@@ -1212,6 +1212,21 @@ void destroy_engine(kr_engine* e) {
             cudaFree(P.d_out);
         }
     }
+    {
+        krb::QueuePipe& Q = e->queue;
+        for (cudaStream_t st : {Q.cin, Q.cout, Q.comp[0], Q.comp[1]})
+            if (st) cudaStreamDestroy(st);
+        for (int d = 0; d < 2; ++d)
+            for (int k = 0; k < 2; ++k) {
+                for (cudaEvent_t ev : {Q.evIn[d][k], Q.evDone[d][k], Q.evOut[d][k]})
+                    if (ev) cudaEventDestroy(ev);
+                cudaFree(Q.in[d][k]);
+                cudaFree(Q.out[d][k]);
+            }
+        for (cudaEvent_t ev : Q.evEnd)
+            if (ev) cudaEventDestroy(ev);
+        if (Q.evStart) cudaEventDestroy(Q.evStart);
+    }
     for (auto& pg : e->pipeGraphs) cudaGraphExecDestroy(pg.exec);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->evFork) cudaEventDestroy(e->evFork);
@@ -2131,6 +2146,78 @@ void host_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_t na
     engine_selfcheck_raise(e);
 }
 
+void ensure_queue(kr_engine* e) {
+    QueuePipe& Q = e->queue;
+    if (Q.made) return;
+    for (cudaStream_t* st : {&Q.cin, &Q.cout, &Q.comp[0], &Q.comp[1]})
+        KR_CK(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (int d = 0; d < 2; ++d)
+        for (int k = 0; k < 2; ++k) {
+            for (cudaEvent_t* ev : {&Q.evIn[d][k], &Q.evDone[d][k], &Q.evOut[d][k]})
+                KR_CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+            Q.in[d][k] = dev_alloc<double>(std::max<int64_t>(d == 0 ? e->cols : e->rows, 1));
+            Q.out[d][k] = dev_alloc<double>(std::max<int64_t>(d == 0 ? e->rows : e->cols, 1));
+        }
+    for (cudaEvent_t& ev : Q.evEnd) KR_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    KR_CK(cudaEventCreateWithFlags(&Q.evStart, cudaEventDisableTiming));
+    Q.made = true;
+}
+
+// kr_engine_pair_queue: `count` independent pairs (x_i, y_i) -> (A x_i,
+// A^T y_i), each result the bits of kr_engine_pair on that pair.  Pair i's
+// products run whole (no board groups) on the direction's compute stream from
+// slot i % 2; the copy of pair i + 1's inputs waits only for pair i - 1's
+// products to have consumed that slot, the products of pair i only for pair
+// i - 2's output copy to have drained theirs.  In steady state the bus carries
+// inputs and outputs at once, back to back, and the kernels hide under them.
+void host_pair_queue(kr_engine* e, int64_t count, const double* const* xs, int64_t nx, double* const* axs,
+                     int64_t nax, const double* const* ys, int64_t ny, double* const* atxs, int64_t natx) {
+    check_sizes(e, 0, nx, nax);
+    check_sizes(e, 1, ny, natx);
+    if (count <= 0) return;
+    for (int64_t i = 0; i < count; ++i)
+        if (!xs[i] || !axs[i] || !ys[i] || !atxs[i]) throw Fail{KR_INVALID_INPUT, "null buffer in the pair queue"};
+    KR_CK(cudaSetDevice(e->device));
+    if (e->scRef) {  // SelfCheck compares every N-th product: pair by pair
+        for (int64_t i = 0; i < count; ++i) host_pair(e, xs[i], nx, axs[i], nax, ys[i], ny, atxs[i], natx);
+        return;
+    }
+    ensure_queue(e);
+    QueuePipe& Q = e->queue;
+    KR_CK(cudaEventRecord(Q.evStart, e->stream));
+    for (cudaStream_t st : {Q.cin, Q.cout, Q.comp[0], Q.comp[1]}) KR_CK(cudaStreamWaitEvent(st, Q.evStart, 0));
+    for (int64_t i = 0; i < count; ++i) {
+        const int k = int(i & 1);
+        for (int d : {1, 0}) {  // A^T y first, as kr_engine_pair
+            const double* hin = d == 0 ? xs[i] : ys[i];
+            double* hout = d == 0 ? axs[i] : atxs[i];
+            const int64_t nin = d == 0 ? nx : ny, nout = d == 0 ? nax : natx;
+            if (i >= 2) KR_CK(cudaStreamWaitEvent(Q.cin, Q.evDone[d][k], 0));
+            KR_CK(cudaMemcpyAsync(Q.in[d][k], hin, 8 * size_t(nin), cudaMemcpyHostToDevice, Q.cin));
+            KR_CK(cudaEventRecord(Q.evIn[d][k], Q.cin));
+            KR_CK(cudaStreamWaitEvent(Q.comp[d], Q.evIn[d][k], 0));
+            if (i >= 2) KR_CK(cudaStreamWaitEvent(Q.comp[d], Q.evOut[d][k], 0));
+            first_stage(e, d, Q.in[d][k], Q.comp[d]);
+            middle(e, d, Q.comp[d]);
+            last_stage(e, d, Q.in[d][k], Q.out[d][k], Q.comp[d]);
+            KR_CK(cudaEventRecord(Q.evDone[d][k], Q.comp[d]));
+            KR_CK(cudaStreamWaitEvent(Q.cout, Q.evDone[d][k], 0));
+            KR_CK(cudaMemcpyAsync(hout, Q.out[d][k], 8 * size_t(nout), cudaMemcpyDeviceToHost, Q.cout));
+            KR_CK(cudaEventRecord(Q.evOut[d][k], Q.cout));
+        }
+    }
+    int j = 0;
+    for (cudaStream_t st : {Q.cin, Q.cout, Q.comp[0], Q.comp[1]}) {
+        KR_CK(cudaEventRecord(Q.evEnd[j], st));
+        KR_CK(cudaStreamWaitEvent(e->stream, Q.evEnd[j++], 0));
+    }
+    KR_CK(cudaStreamSynchronize(e->stream));
+    for (int64_t i = 0; i < count; ++i) {
+        account(e, 0);
+        account(e, 1);
+    }
+}
+
 // The pipelined host-buffer product (board groups), enqueued from and
 // joined back into P.main: every stream it uses waits for the work already
 // queued on P.main, and P.main waits for all of it.
@@ -2280,6 +2367,18 @@ int kr_engine_pair(kr_engine* e, const double* x, int64_t nx, double* ax, int64_
         if (!e || !x || !ax || !y || !atx) throw Fail{KR_INVALID_INPUT, "null argument"};
         if (x == atx || y == ax) throw Fail{KR_INVALID_INPUT, "pair outputs must not alias the other direction's input"};
         krb::host_pair(e, x, nx, ax, nax, y, ny, atx, natx);
+    });
+}
+
+int kr_engine_pair_queue(kr_engine* e, int64_t count, const double* const* xs, int64_t nx, double* const* axs,
+                         int64_t nax, const double* const* ys, int64_t ny, double* const* atxs, int64_t natx) {
+    return guarded([&] {
+        if (!e || (count > 0 && (!xs || !axs || !ys || !atxs))) throw Fail{KR_INVALID_INPUT, "null argument"};
+        if (count < 0) throw Fail{KR_INVALID_INPUT, "negative pair count"};
+        for (int64_t i = 0; i < count; ++i)
+            if (xs[i] == atxs[i] || ys[i] == axs[i])
+                throw Fail{KR_INVALID_INPUT, "pair outputs must not alias the other direction's input"};
+        krb::host_pair_queue(e, count, xs, nx, axs, nax, ys, ny, atxs, natx);
     });
 }
 

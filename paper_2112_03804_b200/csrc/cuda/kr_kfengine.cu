@@ -68,7 +68,7 @@ constexpr int kKfMaxHands = 1364;   // list entries address up to 48 (m + 1) byt
 constexpr int kKfLong = 256;        // longer list rows take the warp-cooperative path
 // fold kernels: one CTA per sequence, all threads stage, two fold (a
 // warp-per-fold layout with 4 folds per CTA measured slower: its staging is
-// latency-bound, profiles/r02/kf_launches_r02t.txt)
+// latency-bound, profiles/r02/kf_launches_r02t_warp_folds_rejected.txt)
 constexpr int kKfFoldThreads = 256;
 
 // One list-of-lists in SELL-8x32 layout: slice s holds 32 rows (perm[32 s + l]
@@ -318,19 +318,19 @@ __device__ __noinline__ void kf_vt_terms8(const KfBoard& B, const char* smb, con
 // takes the long rows, one warp per row: each round the 32 lanes load 256
 // entries, produce their terms in order into the warp's buffer, and all lanes
 // add them in order (warp-uniform adds).  xT: sequence-major input.
-template <int W, bool LONG>
-__global__ void __launch_bounds__(32 * W, LONG ? 2 : 32 / W) k_kfa_vt(const KfBoard* __restrict__ boards, int b0,
-                                                                       int gs, const double* __restrict__ xT,
-                                                                       int64_t M2, double* __restrict__ tz) {
+template <int W>
+__global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __restrict__ boards, int b0, int gy, int gs,
+                                                            const double* __restrict__ xT, int64_t M2,
+                                                            double* __restrict__ tz) {
     pdl_entry();
     extern __shared__ __align__(16) double sm[];
     const char* smb = reinterpret_cast<const char*>(sm);
     __shared__ int okAll;
     const KfBoard& B = boards[b0 + blockIdx.y];
-    const int a = LONG ? blockIdx.x : blockIdx.x / gs, g = LONG ? 0 : blockIdx.x - a * gs;
+    const int a = blockIdx.x / gy, g = blockIdx.x - a * gy;
     const int s0 = B.sptr[a], nSa = B.sptr[a + 1] - s0;
     const int nA = B.nAlive, m2 = B.m2, m2p = m2 + 1;
-    constexpr bool longCta = LONG;
+    const bool longCta = g == gs;
     int lo = 0, hi = 0;
     if (!longCta) kf_range(g, gs, B.yr.nsl, lo, hi);
     if (nSa == 0 || nA == 0 || (longCta ? B.yr.nlong == 0 : lo >= hi)) return;
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kfa_fold(const KfBoard* __re
 // [U | Â] rows (i, a): λ1_i·z(prev alive(i), a) + λ1_i·z_f(a), then the
 // blocked hands j ascending: ((−λ1_i)·λ2_j·F_e)·x[j, col_e]  (rows_ua)
 template <int W>
-__global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_ua(const KfBoard* __restrict__ boards, int b0, int gu,
+__global__ void __launch_bounds__(32 * W) k_kfa_ua(const KfBoard* __restrict__ boards, int b0, int gu,
                                                     const double* __restrict__ xT, int64_t M2,
                                                     const double* __restrict__ tz, const double* __restrict__ zf,
                                                     double* __restrict__ y) {
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kft_fold(const KfBoard* __re
 // [Âᵀ | V] rows (j, b): the blocked hands i ascending, ((−λ1_i)·λ2_j·F_e)·y[i, row_e];
 // then V: alive r ascending, ((λ2_j·Y)·S_e)·z(r, row_e); then λ2_j·F_e·z_f  (rows_av)
 template <int W>
-__global__ void __launch_bounds__(32 * W, 40 / W) k_kft_av(const KfBoard* __restrict__ boards, int b0, int gv,
+__global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ boards, int b0, int gv,
                                                     const double* __restrict__ yT, int64_t M1,
                                                     const double* __restrict__ tz, const double* __restrict__ zf,
                                                     double* __restrict__ x) {
@@ -979,9 +979,7 @@ struct KfState {
     std::vector<void*> keep;       // every device table
     size_t smVT = 0, smUA = 0, smAV = 0, smFA = 0, smFT = 0;
     int nb = 0, n1 = 0, n2 = 0;
-    int gs = 0, gu = 1, gv = 1;    // row-kernel CTAs per sequence (gs: slice CTAs of the Vᵀ rows)
-    bool anyLong = false;          // some board has Y rows in the long-row list
-    size_t smVTL = 0;              // the long-row launch: QY + per-warp buffers
+    int gy = 1, gs = 0, gu = 1, gv = 1;    // row-kernel CTAs per sequence (gs: slice CTAs of the Vᵀ rows)
     double* tz[2] = {nullptr, nullptr};   // t / z per direction (A x, Aᵀy may run concurrently)
     double* zf[2] = {nullptr, nullptr};
     double* inT[2] = {nullptr, nullptr};  // sequence-major input per direction
@@ -1011,25 +1009,16 @@ void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream
                 inT);
     KR_CK_LAUNCH();
     if (dir == 0) {
-        if (k->gs > 0) {
-            krb::launch(k_kfa_vt<kKfWarps, false>, dim3(unsigned(k->n1 * k->gs), nb), T, k->smVT, s, k->dBoards, b0,
-                        k->gs, inT, M, k->tz[0]);
-            KR_CK_LAUNCH();
-            e->launches++;
-        }
-        if (k->anyLong) {  // the few very long Y rows, one warp each
-            krb::launch(k_kfa_vt<kKfWarps, true>, dim3(unsigned(k->n1), nb), T, k->smVTL, s, k->dBoards, b0, 1, inT,
-                        M, k->tz[0]);
-            KR_CK_LAUNCH();
-            e->launches++;
-        }
+        krb::launch(k_kfa_vt<kKfWarps>, dim3(unsigned(k->n1 * k->gy), nb), T, k->smVT, s, k->dBoards, b0, k->gy, k->gs,
+                    inT, M, k->tz[0]);
+        KR_CK_LAUNCH();
         krb::launch(k_kfa_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFA, s, k->dBoards, b0, inT, M, k->tz[0],
                     k->zf[0]);
         KR_CK_LAUNCH();
         krb::launch(k_kfa_ua<kKfWarps>, dim3(unsigned(k->n1 * k->gu), nb), T, k->smUA, s, k->dBoards, b0, k->gu, inT,
                     M, k->tz[0], k->zf[0], out);
         KR_CK_LAUNCH();
-        e->launches += 3;
+        e->launches += 4;
     } else {
         krb::launch(k_kft_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFT, s, k->dBoards, b0, inT, M, k->tz[1],
                     k->zf[1]);
@@ -1144,8 +1133,7 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
             B.yc = up_list(k.keep, H.yc);
             B.b2 = up_list(k.keep, H.b2);
             B.b1 = up_list(k.keep, H.b1);
-            k.smVT = std::max(k.smVT, kf_vt_bytes(H.m2, H.maxSa, 0));
-            k.smVTL = std::max(k.smVTL, kf_vt_bytes(H.m2, H.maxSa, kKfWarps));
+            k.smVT = std::max(k.smVT, kf_vt_bytes(H.m2, H.maxSa, kKfWarps));
             anyLong |= H.yr.lrow.size() > 0;
             k.smUA = std::max(k.smUA, kf_ua_bytes(H.m2, H.maxFa));
             k.smAV = std::max(k.smAV, kf_av_bytes(H.m1, H.nAlive, H.maxSb, H.maxFb));
@@ -1163,10 +1151,9 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
         e->k = K;
         e->flops_per_product = e->nnzV + e->nnzU + e->nnzA + (e->nnzM - K);
         const size_t limit = 227 * 1024 - 1024;
-        if (k.smVT > limit || k.smVTL > limit || k.smUA > limit || k.smAV > limit || k.smFA > limit || k.smFT > limit)
+        if (k.smVT > limit || k.smUA > limit || k.smAV > limit || k.smFA > limit || k.smFT > limit)
             throw Fail{KR_INVALID_INPUT, "board too large for the Kronecker-factored engine's shared memory"};
-        raise_smem_limit(k_kfa_vt<kKfWarps, false>, k.smVT);
-        raise_smem_limit(k_kfa_vt<kKfWarps, true>, k.smVTL);
+        raise_smem_limit(k_kfa_vt<kKfWarps>, k.smVT);
         raise_smem_limit(k_kfa_ua<kKfWarps>, k.smUA);
         raise_smem_limit(k_kft_av<kKfWarps>, k.smAV);
         raise_smem_limit(k_kfa_fold, k.smFA);
@@ -1184,7 +1171,8 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
             return std::max(1, (slices + kKfWarps * rounds - 1) / (kKfWarps * rounds));
         };
         k.gs = slY > 0 ? ctas(slY, n1) : 0;
-        k.anyLong = anyLong;
+        k.gy = k.gs + (anyLong ? 1 : 0);
+        if (k.gy == 0) k.gy = 1;
         k.gu = ctas(slB2, n1);
         k.gv = ctas(slB1, n2);
         for (int d = 0; d < 2; ++d) {

@@ -162,6 +162,28 @@ class CudaEngine:
                                         len(atx)))
         return ax, atx
 
+    def pair_queue(self, xs, ys, out=None):
+        """A queue of independent pairs through kr_engine_pair_queue: returns
+        ([A x for x in xs], [Aᵀ y for y in ys]), each the bits of `pair`.  The
+        input copies of the next pair and the output copies of the previous
+        one overlap each pair's kernels.  `out`: optional (axs, atxs) lists
+        of host arrays to fill (pinned ones keep the bus at its duplex rate)."""
+        if len(xs) != len(ys):
+            raise ValueError("xs and ys must have the same length")
+        xs = [np.ascontiguousarray(x, np.float64) for x in xs]
+        ys = [np.ascontiguousarray(y, np.float64) for y in ys]
+        axs, atxs = out if out is not None else ([np.empty(self.rows) for _ in xs], [np.empty(self.cols) for _ in ys])
+        P = C.c_void_p * max(len(xs), 1)
+        px, py = P(*[N.ptr(a) for a in xs]), P(*[N.ptr(a) for a in ys])
+        pax, patx = P(*[N.ptr(a) for a in axs]), P(*[N.ptr(a) for a in atxs])
+        nx = len(xs[0]) if xs else self.cols
+        ny = len(ys[0]) if ys else self.rows
+        if any(len(a) != nx for a in xs) or any(len(a) != ny for a in ys):
+            raise N.InvalidInputError("queued inputs must all have the same length")
+        N.check(N.cuda().kr_engine_pair_queue(self._h, len(xs), px, nx, pax, len(axs[0]) if axs else self.rows, py, ny,
+                                              patx, len(atxs[0]) if atxs else self.cols))
+        return axs, atxs
+
     def ATx(self, x1):
         y = np.ascontiguousarray(x1, np.float64)
         x = np.empty(self.cols)

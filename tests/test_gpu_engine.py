@@ -337,3 +337,49 @@ def test_host_pair_call_bitwise(kind, nb):
             L.kr_host_free(p)
     with pytest.raises(InvalidInputError):
         eng.pair(x[:-1], y)
+
+
+@pytest.mark.parametrize("kind,nb", [("factored", 1), ("factored", 4), ("implicit", 4), ("kfactored", 4)])
+def test_pair_queue_bitwise(kind, nb):
+    """kr_engine_pair_queue: every queued pair's results are the bits of
+    kr_engine_pair on it — on pageable and pinned buffers, with a buffer
+    shared by several queue entries, for queues of 1, 2 and 5 pairs (slot
+    reuse from the third pair on)."""
+    import ctypes
+
+    from paper_2112_03804_b200 import _native as N
+    boards = H.turn_instances(nboards=nb, factors=kind == "factored")
+    insts = [i for i, _ in boards]
+    eng = (CudaEngine([f for _, f in boards]) if kind == "factored" else
+           CudaEngine.kron(insts) if kind == "implicit" else CudaEngine.kfactored(insts))
+    rng = np.random.default_rng(43)
+    for q in (1, 2, 5):
+        xs = [rng.standard_normal(eng.cols) for _ in range(q)]
+        ys = [rng.standard_normal(eng.rows) for _ in range(q)]
+        axs, atxs = eng.pair_queue(xs, ys)
+        for i in range(q):
+            ax, atx = eng.pair(xs[i], ys[i])
+            assert bits_equal(axs[i], ax) and bits_equal(atxs[i], atx), (q, i)
+    L = N.cuda()
+    arr = lambda p, n: np.ctypeslib.as_array((ctypes.c_double * n).from_address(p))  # noqa: E731
+    sizes = (eng.cols, eng.rows, eng.rows, eng.cols)
+    bufs = [[L.kr_host_alloc(8 * n) for n in sizes] for _ in range(3)]
+    try:
+        for b in bufs:
+            arr(b[0], eng.cols)[:] = rng.standard_normal(eng.cols)
+            arr(b[1], eng.rows)[:] = rng.standard_normal(eng.rows)
+        order = [0, 1, 2, 0, 1, 2, 2]   # entries share buffers; the last writer of an output is its last entry
+        P = ctypes.c_void_p * len(order)
+        col = lambda j: P(*[bufs[o][j] for o in order])  # noqa: E731
+        N.check(L.kr_engine_pair_queue(eng.handle, len(order), col(0), eng.cols, col(2), eng.rows, col(1), eng.rows,
+                                       col(3), eng.cols))
+        for b in bufs:
+            ax, atx = eng.pair(arr(b[0], eng.cols).copy(), arr(b[1], eng.rows).copy())
+            assert bits_equal(arr(b[2], eng.rows).copy(), ax) and bits_equal(arr(b[3], eng.cols).copy(), atx)
+    finally:
+        for b in bufs:
+            for p in b:
+                L.kr_host_free(p)
+    with pytest.raises(InvalidInputError):
+        eng.pair_queue([rng.standard_normal(eng.cols + 1)], [rng.standard_normal(eng.rows)])
+    assert eng.pair_queue([], []) == ([], [])
