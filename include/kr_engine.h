@@ -232,6 +232,19 @@ const char* kr_last_error(int* code);
 /* Number of CUDA devices visible (0 on a machine without a GPU). */
 int kr_device_count(void);
 
+/* The bounds-checked build (KR_CHECKED; lib/libkrcuda_checked.so): the number
+ * of device allocations whose guard zones were found overwritten (live ones
+ * now, freed ones when they were freed), 0 when all are intact; -1 in the
+ * normal build.  Synchronises the device.  No reference counterpart (the
+ * reference's sanitizer builds). */
+int64_t kr_checked_verify(void);
+
+/* The checked build's own test (-1 in the normal build): mode 0 writes one
+ * double past a 100-double allocation and returns the number of corrupted
+ * guard zones found (1); mode 1 does it behind a failing device index check,
+ * which traps (returns minus the CUDA error; the context is lost). */
+int64_t kr_checked_selftest(int mode);
+
 /* ---------------------------------------------------------------------------
  * Solver step on the device: DCFR with alternating updates
  * (solver.hpp:343-404), regret matching (166-194), sequence form (197-218),

@@ -30,6 +30,28 @@ void set_error(int code, const std::string& msg);
 
 #define KR_CK_LAUNCH() KR_CK(cudaGetLastError())
 
+#ifdef KR_CHECKED
+#include <cstdio>
+__device__ __forceinline__ uint32_t kr_dyn_smem() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+#define KR_DCHECK(c)                                                                                       \
+    do {                                                                                                   \
+        if (!(c)) {                                                                                        \
+            printf("KR_CHECKED %s:%d: %s (block %d,%d thread %d)\n", __FILE__, __LINE__, #c, int(blockIdx.x), \
+                   int(blockIdx.y), int(threadIdx.x));                                                     \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+// [off, off + bytes) inside the launch's dynamic shared memory
+#define KR_SMEM_CHECK(off, bytes) KR_DCHECK(uint64_t(off) + uint64_t(bytes) <= uint64_t(kr_dyn_smem()))
+#else
+#define KR_DCHECK(c) ((void)0)
+#define KR_SMEM_CHECK(off, bytes) ((void)0)
+#endif
+
 template <class F>
 int guarded(F&& f) {
     try {
@@ -134,11 +156,36 @@ inline unsigned& last_grid(cudaStream_t s) {
     return last.back().second;
 }
 
+// KR_CHECKED: the bounds-checked build (build.build_cuda_variant("checked",
+// ["KR_CHECKED"]), loaded with KR_CUDA_LIB_VARIANT=checked; the pool's GPUs
+// take no compute-sanitizer runs).  Every device allocation gets 4 KB guard
+// zones on both sides and its whole extent filled with a poison byte (reads
+// of uninitialised or out-of-range data turn into huge / negative values that
+// break the bitwise tests or trip an index check); the guards are verified
+// when the allocation is freed and by kr_checked_verify().  KR_DCHECK traps
+// on a failed device-side index check, printing where.
+#ifdef KR_CHECKED
+void* checked_alloc(size_t bytes);
+void checked_free(void* p);
+#endif
+
 template <class T>
 T* dev_alloc(int64_t n) {
     T* p = nullptr;
+#ifdef KR_CHECKED
+    if (n > 0) p = static_cast<T*>(checked_alloc(sizeof(T) * size_t(n)));
+#else
     if (n > 0) KR_CK(cudaMalloc(&p, sizeof(T) * size_t(n)));
+#endif
     return p;
+}
+
+inline void dev_free(void* p) {
+#ifdef KR_CHECKED
+    checked_free(p);
+#else
+    cudaFree(p);
+#endif
 }
 
 // kernel<<<grid, block, smem, stream>>>(args...) with the PDL attribute

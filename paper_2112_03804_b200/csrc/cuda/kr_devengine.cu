@@ -740,11 +740,11 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
         engine_make_pipeline(e);
         KR_CK(cudaDeviceSynchronize());
     } catch (...) {
-        for (void* p : keep) cudaFree(p);
+        for (void* p : keep) krb::dev_free(p);
         kr_engine_destroy(e);
         throw;
     }
-    for (void* p : keep) cudaFree(p);
+    for (void* p : keep) krb::dev_free(p);
     return e;
 }
 

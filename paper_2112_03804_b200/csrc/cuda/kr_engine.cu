@@ -29,6 +29,68 @@
 
 #include "kr_common.cuh"
 
+#ifdef KR_CHECKED
+namespace krb {
+namespace {
+constexpr size_t kGuard = 4096;
+constexpr unsigned char kPoison = 0xF7;  // double -1.4e270-ish, int32 < 0, uint16 0xF7F7
+struct CheckedAlloc {
+    char* base;
+    size_t bytes, total;
+};
+std::mutex g_checked_mu;
+std::unordered_map<void*, CheckedAlloc>& checked_allocs() {
+    static std::unordered_map<void*, CheckedAlloc> m;
+    return m;
+}
+int64_t g_checked_bad = 0;
+
+// the two guard zones and the rounding tail after the caller's bytes
+bool guards_intact(void* p, const CheckedAlloc& a) {
+    const size_t lo = kGuard, tail = a.total - kGuard - a.bytes;
+    std::vector<unsigned char> h(std::max(lo, tail));
+    auto all_poison = [&](const char* d, size_t n) {
+        if (cudaMemcpy(h.data(), d, n, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+        for (size_t i = 0; i < n; ++i)
+            if (h[i] != kPoison) return false;
+        return true;
+    };
+    const bool ok = all_poison(a.base, lo) && all_poison(static_cast<char*>(p) + a.bytes, tail);
+    if (!ok)
+        std::fprintf(stderr, "KR_CHECKED: guard zone of a %zu-byte device allocation was overwritten\n", a.bytes);
+    return ok;
+}
+}  // namespace
+
+void* checked_alloc(size_t bytes) {
+    const size_t total = ((bytes + 255) & ~size_t(255)) + 2 * kGuard;
+    char* base = nullptr;
+    KR_CK(cudaMalloc(&base, total));
+    KR_CK(cudaMemset(base, kPoison, total));
+    KR_CK(cudaDeviceSynchronize());
+    void* p = base + kGuard;
+    std::lock_guard<std::mutex> g(g_checked_mu);
+    checked_allocs()[p] = {base, bytes, total};
+    return p;
+}
+
+void checked_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_checked_mu);
+    auto it = checked_allocs().find(p);
+    if (it == checked_allocs().end()) {
+        std::fprintf(stderr, "KR_CHECKED: free of a pointer the library did not allocate\n");
+        ++g_checked_bad;
+        return;
+    }
+    cudaDeviceSynchronize();
+    if (!guards_intact(p, it->second)) ++g_checked_bad;
+    cudaFree(it->second.base);
+    checked_allocs().erase(it);
+}
+}  // namespace krb
+#endif
+
 namespace krb {
 
 namespace {
@@ -64,6 +126,7 @@ struct SellView {
     int64_t nlong;
     const int32_t* order;  // slice dispatch order (nullptr: storage order)
     int32_t pf;            // L2 prefetch distance of the slice rows, in batches of KU (0: none)
+    int64_t nsrc, ndst;    // gather-index and output-row bounds (checked build)
 };
 
 // One bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16).
@@ -80,6 +143,7 @@ constexpr int kU = KR_KU;  // entries per lane per pipeline stage
 template <bool TWO>
 __device__ __forceinline__ double gather(const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
                                          int32_t c) {
+    KR_DCHECK(c >= 0);
     if (TWO) return c < split ? __ldg(xa + c) : __ldg(xb + (c - split));
     return __ldg(xa + c);
 }
@@ -110,7 +174,10 @@ __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* _
             }
 #pragma unroll
         for (int u = 0; u < per; ++u)
-            if (u * 32 + lane < n) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+            if (u * 32 + lane < n) {
+                KR_DCHECK(c[u] < A.nsrc);
+                p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+            }
     }
     for (int64_t t0 = e0; t0 < e1; t0 += kChunk) {
 #pragma unroll
@@ -141,10 +208,14 @@ __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* _
         }
 #pragma unroll
         for (int u = 0; u < per; ++u)
-            if (u * 32 + lane < nn) p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+            if (u * 32 + lane < nn) {
+                KR_DCHECK(c[u] < A.nsrc);
+                p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+            }
         __syncwarp();
         n = nn;
     }
+    KR_DCHECK(A.long_row[r] >= 0 && A.long_row[r] < A.ndst);
     if (lane == 0) y[A.long_row[r]] = acc;
 }
 
@@ -217,7 +288,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
         }
 #pragma unroll
         for (int u = 0; u < KU; ++u)
-            if (j + u < len) x[u] = gather<TWO>(xa, xb, split, c[u]);
+            if (j + u < len) {
+                KR_DCHECK(c[u] < A.nsrc);
+                x[u] = gather<TWO>(xa, xb, split, c[u]);
+            }
 #pragma unroll
         for (int u = 0; u < KU; ++u)
             if (j + u < len) acc += v[u] * x[u];
@@ -227,6 +301,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
             v[u] = vn[u];
         }
     }
+    KR_DCHECK(row < A.ndst);
     if (row >= 0) y[row] = acc;
 }
 
@@ -274,6 +349,7 @@ __device__ __forceinline__ double seg_sum(double acc, const SellView& A, const S
 #pragma unroll
         for (int u = 0; u < KU; ++u)
             if (j + u < j1) {
+                KR_DCHECK(int64_t(cbase) + int64_t(c[u]) < A.nsrc && cbase >= 0);
                 x[u] = __ldg(src + cbase + int32_t(c[u]));
                 if (CODED) v[u] = __ldg(C.table + tb + int32_t(k[u]));
             }
@@ -318,6 +394,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     double acc = 0.0;
     acc = seg_sum<kU, CSEG == 0>(acc, A, C, base, 0, len0, xa, C.base0[s], tb);
     if (TWO) acc = seg_sum<kU, CSEG == 1>(acc, A, C, base, len0, len, xb, C.base1[s], tb);
+    KR_DCHECK(row < A.ndst && len0 <= len);
     if (row >= 0) y[row] = acc;
 }
 
@@ -409,6 +486,8 @@ __global__ void __launch_bounds__(32)
     const bool allneg = neg1[s * 32 + lane] != 0;
     const bool needMul = withMul && __any_sync(0xffffffffu, !allneg);
     const int nChunks = (width + kChunkRows - 1) / kChunkRows;
+    KR_DCHECK(len >= 0 && len <= width && (sbase[s + 1] - b0) % 32 == 0);
+    KR_SMEM_CHECK(0, size_t(kStages) * kChunkRows * 32 * 8 * (needMul ? 2 : 1));
     if (lane == 0)
         for (int q = 0; q < kStages; ++q) mbar_init(&bar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -430,6 +509,7 @@ __global__ void __launch_bounds__(32)
             chunk_rows(c, r0, n);
             const int st = c % kStages;
             const uint32_t bytes = uint32_t(n) * 32 * 8;
+            KR_DCHECK(n > 0 && n <= kChunkRows && r0 >= 0 && r0 + n <= width);
             mbar_expect_tx(&bar[st], needMul ? 2 * bytes : bytes);
             bulk_g2s(Tb[st], z + b0 + int64_t(r0) * 32, bytes, &bar[st]);
             if (needMul) bulk_g2s(Mb[st], cmul + b0 + int64_t(r0) * 32, bytes, &bar[st]);
@@ -931,13 +1011,13 @@ void upload_comp(const HostComp& c, int b, int64_t sliceBase, int64_t entryBase,
 }
 
 void free_comp(krb::DevSell& d) {
-    cudaFree(d.col16);
-    cudaFree(d.code16);
-    cudaFree(d.lane_len0);
-    cudaFree(d.base0);
-    cudaFree(d.base1);
-    cudaFree(d.tbase);
-    cudaFree(d.table);
+    krb::dev_free(d.col16);
+    krb::dev_free(d.code16);
+    krb::dev_free(d.lane_len0);
+    krb::dev_free(d.base0);
+    krb::dev_free(d.base1);
+    krb::dev_free(d.tbase);
+    krb::dev_free(d.table);
     d.col16 = d.code16 = nullptr;
     d.lane_len0 = d.base0 = d.base1 = d.tbase = nullptr;
     d.table = nullptr;
@@ -945,17 +1025,17 @@ void free_comp(krb::DevSell& d) {
 }
 
 void free_sell(krb::DevSell& d) {
-    cudaFree(d.slice_ptr);
-    cudaFree(d.lane_row);
-    cudaFree(d.lane_len);
-    cudaFree(d.col);
-    cudaFree(d.val);
-    cudaFree(d.long_ptr);
-    cudaFree(d.long_row);
-    cudaFree(d.long_col);
-    cudaFree(d.long_val);
-    cudaFree(d.order_all);
-    cudaFree(d.order_grp);
+    krb::dev_free(d.slice_ptr);
+    krb::dev_free(d.lane_row);
+    krb::dev_free(d.lane_len);
+    krb::dev_free(d.col);
+    krb::dev_free(d.val);
+    krb::dev_free(d.long_ptr);
+    krb::dev_free(d.long_row);
+    krb::dev_free(d.long_col);
+    krb::dev_free(d.long_val);
+    krb::dev_free(d.order_all);
+    krb::dev_free(d.order_grp);
     free_comp(d);
     d = krb::DevSell{};
 }
@@ -1208,8 +1288,8 @@ void destroy_engine(kr_engine* e) {
         if (P.evEnd) cudaEventDestroy(P.evEnd);
         if (q == 1) {
             if (P.main) cudaStreamDestroy(P.main);
-            cudaFree(P.d_in);
-            cudaFree(P.d_out);
+            krb::dev_free(P.d_in);
+            krb::dev_free(P.d_out);
         }
     }
     {
@@ -1220,8 +1300,8 @@ void destroy_engine(kr_engine* e) {
             for (int k = 0; k < 2; ++k) {
                 for (cudaEvent_t ev : {Q.evIn[d][k], Q.evDone[d][k], Q.evOut[d][k]})
                     if (ev) cudaEventDestroy(ev);
-                cudaFree(Q.in[d][k]);
-                cudaFree(Q.out[d][k]);
+                krb::dev_free(Q.in[d][k]);
+                krb::dev_free(Q.out[d][k]);
             }
         for (cudaEvent_t ev : Q.evEnd)
             if (ev) cudaEventDestroy(ev);
@@ -1237,26 +1317,26 @@ void destroy_engine(kr_engine* e) {
     free_sell(e->UA);
     free_sell(e->UT);
     free_sell(e->AV);
-    cudaFree(e->chain_ptr);
-    cudaFree(e->chain_len);
-    cudaFree(e->chain_mul);
-    cudaFree(e->chain_neg1);
-    cudaFree(e->lvl_fwd_rows);
-    cudaFree(e->lvl_bwd_cols);
-    cudaFree(e->mr_ptr);
-    cudaFree(e->mr_col);
-    cudaFree(e->mr_val);
-    cudaFree(e->mc_ptr);
-    cudaFree(e->mc_row);
-    cudaFree(e->mc_val);
-    cudaFree(e->d_tz);
-    cudaFree(e->d_tz2);
-    cudaFree(e->d_xp);
-    cudaFree(e->d_in);
-    cudaFree(e->d_out);
-    cudaFree(e->scBuf[0]);
-    cudaFree(e->scBuf[1]);
-    cudaFree(e->scStat);
+    krb::dev_free(e->chain_ptr);
+    krb::dev_free(e->chain_len);
+    krb::dev_free(e->chain_mul);
+    krb::dev_free(e->chain_neg1);
+    krb::dev_free(e->lvl_fwd_rows);
+    krb::dev_free(e->lvl_bwd_cols);
+    krb::dev_free(e->mr_ptr);
+    krb::dev_free(e->mr_col);
+    krb::dev_free(e->mr_val);
+    krb::dev_free(e->mc_ptr);
+    krb::dev_free(e->mc_row);
+    krb::dev_free(e->mc_val);
+    krb::dev_free(e->d_tz);
+    krb::dev_free(e->d_tz2);
+    krb::dev_free(e->d_xp);
+    krb::dev_free(e->d_in);
+    krb::dev_free(e->d_out);
+    krb::dev_free(e->scBuf[0]);
+    krb::dev_free(e->scBuf[1]);
+    krb::dev_free(e->scStat);
     for (auto& p : e->pending) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
@@ -1716,8 +1796,13 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
                            (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return;
     const int32_t* order = b1 < 0 ? A.order_all : A.order_grp ? A.order_grp + s0 : nullptr;
+    // gather sources and outputs: V^T x (x or x': cols -> k), [U | Ahat] ([tz | x] -> rows),
+    // U^T y (y: rows -> k), [Ahat^T | V] ([y | tz2] -> cols)
+    const int64_t nsrc = which == 0 ? e->cols : which == 1 ? e->kpad + e->cols : which == 2 ? e->rows
+                                                                                               : e->rows + e->kpad;
+    const int64_t ndst = which == 0 || which == 2 ? e->kpad : which == 1 ? e->rows : e->cols;
     SellView v{A.slice_ptr + s0, A.lane_row + 32 * s0, A.lane_len + 32 * s0, A.col, A.val, s1 - s0,
-               A.long_ptr + l0, A.long_row + l0, A.long_col, A.long_val, l1 - l0, order, e->pf};
+               A.long_ptr + l0, A.long_row + l0, A.long_col, A.long_val, l1 - l0, order, e->pf, nsrc, ndst};
     const bool timed = e->timing && ((e->timingMask >> which) & 1) && b1 < 0;
     kr_engine::Pending pend{which, nullptr, nullptr};
     if (timed) {
@@ -2310,6 +2395,52 @@ extern "C" {
 const char* kr_last_error(int* code) {
     if (code) *code = krb::g_code;
     return krb::g_msg.c_str();
+}
+
+int64_t kr_checked_verify(void) {
+#ifdef KR_CHECKED
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> g(krb::g_checked_mu);
+    int64_t bad = krb::g_checked_bad;
+    for (auto& [p, a] : krb::checked_allocs()) bad += krb::guards_intact(p, a) ? 0 : 1;
+    return bad;
+#else
+    return -1;
+#endif
+}
+
+#ifdef KR_CHECKED
+namespace {
+__global__ void k_checked_poke(double* p, int64_t i, int checkIndex, int64_t n) {
+    if (checkIndex) KR_DCHECK(i < n);
+    p[i] = 1.0;
+}
+}  // namespace
+#endif
+
+int64_t kr_checked_selftest(int mode) {
+#ifdef KR_CHECKED
+    // mode 0: write one element past a 100-double allocation and report how
+    // many corrupted guard zones kr_checked_verify finds (1), leaving the
+    // global count as it was; mode 1: the same write behind a failing
+    // KR_DCHECK (traps: the context is lost, run it in a child process)
+    double* p = krb::dev_alloc<double>(100);
+    k_checked_poke<<<1, 1>>>(p, 100, mode == 1, 100);
+    const cudaError_t err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) return -int64_t(err);
+    int64_t found = 0;
+    {
+        std::lock_guard<std::mutex> g(krb::g_checked_mu);
+        auto it = krb::checked_allocs().find(p);
+        found = krb::guards_intact(p, it->second) ? 0 : 1;
+        cudaFree(it->second.base);
+        krb::checked_allocs().erase(it);
+    }
+    return found;
+#else
+    (void)mode;
+    return -1;
+#endif
 }
 
 int kr_device_count(void) {

@@ -300,7 +300,7 @@ struct DevBuf {
         return p;
     }
     ~DevBuf() {
-        for (void* p : ptrs) cudaFree(p);
+        for (void* p : ptrs) krb::dev_free(p);
     }
 };
 

@@ -125,9 +125,11 @@ __device__ __forceinline__ bool kf_ok(double v) {
 __device__ __forceinline__ double kf_yval(int v) { return v < 2 ? double(v - 2) : double(v - 1); }
 
 __device__ __forceinline__ double smd(const char* smb, uint32_t off) {
+    KR_SMEM_CHECK(off, 8);
     return *reinterpret_cast<const double*>(smb + off);
 }
 __device__ __forceinline__ double2 smd2(const char* smb, uint32_t off) {
+    KR_SMEM_CHECK(off, 16);
     return *reinterpret_cast<const double2*>(smb + off);
 }
 
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(256) k_kf_seqmajor(const double* __restrict__ 
     const int64_t h0 = J0 + int64_t(blockIdx.x) * 32;
     const int nh = int(lmin(32, J1 - h0));
     if (nh <= 0) return;
+    KR_SMEM_CHECK(0, size_t(8) * 32 * n);
     for (int q = threadIdx.x; q < nh * n; q += blockDim.x) tile[q] = in[h0 * n + q];
     __syncthreads();
     for (int q = threadIdx.x; q < n * 32; q += blockDim.x) {
@@ -338,7 +341,10 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
     if (threadIdx.x == 0) okAll = 1;
     __syncthreads();
     int ok = B.fast;
+    KR_DCHECK(nSa <= B.maxSa && m2 <= M2);
+    KR_SMEM_CHECK(0, size_t(32) * m2p * nSa);
     for (int e = 0; e < nSa; ++e) {
+        KR_DCHECK(unsigned(B.scol[s0 + e]) < unsigned(B.n2));
         double* QY = sm + size_t(e) * 4 * m2p;
         const double* col = xs + B.scol[s0 + e] * M2;
         const double sv = B.sval[s0 + e];
@@ -361,6 +367,7 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (longCta) {
         double* buf = sm + size_t(4) * m2p * size_t(B.maxSa) + size_t(warp) * 256 * size_t(B.maxSa);
+        KR_SMEM_CHECK(8 * (size_t(4) * m2p * B.maxSa + (size_t(warp) + 1) * 256 * B.maxSa), 0);
         for (int L = warp; L < B.yr.nlong; L += W) {
             const int v0 = B.yr.lptr[L], nvec = B.yr.lptr[L + 1] - v0;
             double acc = 0.0;
@@ -387,6 +394,7 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
                 const int nt = cnt * 8 * nSa;
                 for (int k = 0; k < nt; ++k) acc = acc + buf[k];
             }
+            KR_DCHECK(unsigned(B.yr.lrow[L]) < unsigned(nA));
             if (lane == 0) tz[B.zOff + int64_t(a) * nA + B.yr.lrow[L]] = acc;
         }
         return;
@@ -401,6 +409,7 @@ __global__ void __launch_bounds__(32 * W, 32 / W) k_kfa_vt(const KfBoard* __rest
         } else {
             kf_stream(src, nv, [&](uint32_t off) { acc = kf_vt_add(B, smb, xs, M2, off, s0, nSa, m2p, fast, acc); });
         }
+        KR_DCHECK(r < nA);
         if (r >= 0) tz[B.zOff + int64_t(a) * nA + r] = acc;
     }
 }
@@ -426,11 +435,13 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kfa_fold(const KfBoard* __re
     double* f = sm + nA;
     double* t = tz + B.zOff + int64_t(a) * nA;
     const double* xs = xT + B.h2Off;
+    KR_SMEM_CHECK(0, 8 * (size_t(nA) + size_t(fA ? m2 : 0) * nFa));
     if (chain)
         for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) v[r] = t[r];
     if (fA)
         for (int k = threadIdx.x; k < m2 * nFa; k += kKfFoldThreads) {
             const int j = nFa == 1 ? k : k / nFa, e = k - j * nFa;
+            KR_DCHECK(unsigned(B.fcol[f0 + e]) < unsigned(B.n2));
             f[k] = (B.l2[j] * B.fval[f0 + e]) * xs[B.fcol[f0 + e] * M2 + j];
         }
     __syncthreads();
@@ -460,6 +471,7 @@ __global__ void __launch_bounds__(32 * W) k_kfa_ua(const KfBoard* __restrict__ b
     const int f0 = B.fptr[a], nFa = B.fptr[a + 1] - f0;
     double2* PR = reinterpret_cast<double2*>(sm);
     double* xF1 = sm + 2 * (m2 + 1);
+    KR_SMEM_CHECK(0, 8 * (2 * (size_t(m2) + 1) + size_t(nFa > 1 ? nFa - 1 : 0) * m2));
     if (nFa > 0) {
         const double* xs = xT + B.h2Off;
         const double* c0 = xs + B.fcol[f0] * M2;
@@ -480,10 +492,12 @@ __global__ void __launch_bounds__(32 * W) k_kfa_ua(const KfBoard* __restrict__ b
     const double fv = nFa > 0 ? B.fval[f0] : 0.0;
     for (int s = lo + warp; s < hi; s += W) {
         const int i = B.b2.perm[32 * s + lane];
+        KR_DCHECK(i < B.m1);
         const double v = i >= 0 ? B.l1[i] : 0.0;
         double acc = 0.0;
         if (i >= 0 && v != 0.0) {
             const int rp = B.rankPrev[i];
+            KR_DCHECK(rp < nA);
             if (chain && rp >= 0) acc = acc + v * tz[B.zOff + int64_t(a) * nA + rp];
             if (fA) acc = acc + v * zfa;
         }
@@ -534,8 +548,10 @@ __global__ void __launch_bounds__(kKfFoldThreads) k_kft_fold(const KfBoard* __re
     const double* yd = yT + d * M1 + B.h1Off;
     double* v = sm;
     double* f = sm + nA;
+    KR_SMEM_CHECK(0, 8 * (size_t(nA) + (fD ? m1 : 0)));
     if (chain)
         for (int r = threadIdx.x; r < nA; r += kKfFoldThreads) {
+            KR_DCHECK(B.aliveRows[r] >= 0 && B.aliveEnd[r] <= m1);
             double acc = 0.0;
             for (int i = B.aliveRows[r]; i < B.aliveEnd[r]; ++i) acc = acc + B.l1[i] * yd[i];
             v[r] = acc;
@@ -576,6 +592,9 @@ __global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ b
     double* ZY = sm + 2 * m1p;                                   // [maxSb][4][nAp]
     double* yF1 = ZY + size_t(4) * nAp * (B.maxSb > 0 ? B.maxSb : 1);
     const double* ys = yT + B.h1Off;
+    KR_DCHECK(nSb <= (B.maxSb > 0 ? B.maxSb : 1) || nA == 0);
+    KR_SMEM_CHECK(0, 8 * (2 * size_t(m1p) + size_t(4) * nAp * (B.maxSb > 0 ? B.maxSb : 1) +
+                          size_t(nFb > 1 ? nFb - 1 : 0) * m1));
     if (threadIdx.x == 0) okAll = 1;
     __syncthreads();
     if (nFb > 0) {
@@ -592,6 +611,7 @@ __global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ b
     int ok = B.fast;
     if (nA > 0)
         for (int e = 0; e < nSb; ++e) {
+            KR_DCHECK(unsigned(B.scrow[s0 + e]) < unsigned(B.n1));
             const double* z = tz + B.zOff + int64_t(B.scrow[s0 + e]) * nA;
             double* Z = ZY + size_t(e) * 4 * nAp;
             for (int r = threadIdx.x; r < nAp; r += 32 * W) {
@@ -610,6 +630,7 @@ __global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ b
     const double fv = nFb > 0 ? B.fcval[f0] : 0.0;
     for (int s = lo + warp; s < hi; s += W) {
         const int j = B.b1.perm[32 * s + lane];
+        KR_DCHECK(j < B.m2);
         const double l2 = j >= 0 ? B.l2[j] : 0.0;
         double acc = 0.0;
         if (nFb > 0) {   // Âᵀ
@@ -671,9 +692,6 @@ __global__ void __launch_bounds__(32 * W) k_kft_av(const KfBoard* __restrict__ b
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-// SELL-8x32 list (KfList) on the host: rows in `order` (or by length,
-// longest first), slices of 32, each slice padded to a multiple of 8 entries
-// with `pad`.
 // SELL-8x32 list (KfList) on the host: rows in `order` (or by length,
 // longest first), slices of 32, each slice padded to a multiple of 8 entries
 // with `pad`; with longCut > 0, rows longer than longCut go to the long-row
@@ -989,7 +1007,7 @@ struct KfState {
 
 void kf_destroy(KfState* k) {
     if (!k) return;
-    for (void* p : k->keep) cudaFree(p);
+    for (void* p : k->keep) krb::dev_free(p);
     delete k;
 }
 

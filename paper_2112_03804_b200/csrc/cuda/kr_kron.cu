@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
     double* CF = G + 56;                          // [52]
     int32_t* lhand = reinterpret_cast<int32_t*>(CF + 56);  // [2 mSb]
     int32_t* lptr = lhand + 2 * mSb;                       // [53]
+    KR_SMEM_CHECK(0, sizeof(double) * (5 * size_t(mSb) + 1 + 3 * 56) + sizeof(int32_t) * (2 * size_t(mSb) + 56));
+    KR_DCHECK(mSb <= d.maxMS && mSb <= kMaxHands);
 
     // 1. weights of every summing hand for sequence a: the few F/S entries of
     // row a are uniform across the CTA, so each thread issues the gathers of
@@ -151,7 +153,11 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
         const int32_t* hands = d.listHands + d.listBase[b];
 #pragma unroll
         for (int q = 0; q < 2 * kPerT; ++q)
-            if (tid + q * T < 2 * mSb) lhand[tid + q * T] = __ldg(hands + tid + q * T);
+            if (tid + q * T < 2 * mSb) {
+                lhand[tid + q * T] = __ldg(hands + tid + q * T);
+                KR_DCHECK(unsigned(lhand[tid + q * T]) < unsigned(mSb));
+            }
+        KR_DCHECK(tid > kCards || (lptr[tid] >= 0 && lptr[tid] <= 2 * mSb));
 
         const int64_t* fp = d.fptr + int64_t(b) * (d.nO + 1) + a;
         const int64_t* sp = d.sptr + int64_t(b) * (d.nO + 1) + a;
@@ -165,6 +171,7 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
         for (int q = 0; q < kPerT; ++q) f[q] = s[q] = 0.0;
         for (int64_t e = f0; e < f1; ++e) {
             const double val = __ldg(d.fval + e);
+            KR_DCHECK(unsigned(__ldg(d.fcol + e)) < unsigned(nS));
             const double* vc = v0 + __ldg(d.fcol + e) * colMul;
 #pragma unroll
             for (int q = 0; q < kPerT; ++q)
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
         }
         for (int64_t e = s0; e < s1; ++e) {
             const double val = __ldg(d.sval + e);
+            KR_DCHECK(unsigned(__ldg(d.scol + e)) < unsigned(nS));
             const double* vc = v0 + __ldg(d.scol + e) * colMul;
 #pragma unroll
             for (int q = 0; q < kPerT; ++q)
@@ -282,6 +290,8 @@ __global__ void __launch_bounds__(T) k_kron_fused(KronDir d, int b0, const doubl
             const int lt = t.x & 0xffff, le = t.x >> 16;
             const int dup = (t.y & 0xffff) - 1, c1 = (t.y >> 16) & 0xff, c2 = t.y >> 24;
             const int p1lt = t.z & 0xffff, p1le = t.z >> 16, p2lt = t.w & 0xffff, p2le = t.w >> 16;
+            KR_DCHECK(lt <= N && le <= N && p1lt <= N && p1le <= N && p2lt <= N && p2le <= N);
+            KR_DCHECK(dup < mSb && c1 < kCards && c2 < kCards);
             double fpart = TF - CF[c1] - CF[c2];
             if (dup >= 0) fpart += W[dup].y;
             const double wsum = (P[lt] + P[le] - TS) - (P[p1lt] + P[p1le]) - (P[p2lt] + P[p2le]) + G[c1] + G[c2];
@@ -504,7 +514,7 @@ void build_dir(KronDir& d, const kr_kron_board* boards, int nb, int dir) {
 void free_dir(KronDir& d) {
     void* ps[] = {d.sumOff, d.outOff, d.lamS, d.lamO, d.fptr, d.fcol, d.fval, d.sptr, d.scol, d.sval,
                   d.listPtr, d.listBase, d.listHands, d.otab};
-    for (void* p : ps) cudaFree(p);
+    for (void* p : ps) krb::dev_free(p);
     d = KronDir{};
 }
 
@@ -544,8 +554,8 @@ void kron_destroy(KronState* k) {
     free_dir(k->dir[0]);
     free_dir(k->dir[1]);
     for (int i = 0; i < 2; ++i) {
-        cudaFree(k->seqIn[i]);
-        cudaFree(k->seqOut[i]);
+        krb::dev_free(k->seqIn[i]);
+        krb::dev_free(k->seqOut[i]);
     }
     delete k;
 }

@@ -320,6 +320,8 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
     double* V = Rg + n * stride;          // (n+1) x stride  gradient -> values -> probabilities -> reach
     double* NV = V + (n + 1) * stride;    // nn x stride     node values
     int32_t* T = reinterpret_cast<int32_t*>(NV + nn * stride);
+    KR_SMEM_CHECK(0, sizeof(double) * size_t(2 * n + 1 + nn) * stride + sizeof(int32_t) * size_t(tlen));
+    KR_DCHECK(int(blockDim.x) / kTeam >= hpb);
     for (int q = threadIdx.x; q < tlen; q += blockDim.x) T[q] = treeBuf[q];
     const int64_t h0 = int64_t(blockIdx.x) * hpb;
     const int nh = int(lmin(hpb, H - h0));
@@ -379,8 +381,10 @@ __global__ void __launch_bounds__(256) k_player_team(int mode, const int32_t* __
             if (valid)
                 for (int k = levPtr[l] + lane; k < levPtr[l + 1]; k += kTeam) {
                     const int v = levNodes[k];
+                    KR_DCHECK(v >= 0 && v < nn);
                     const int a0 = tr.aptr[v], cnt = tr.aptr[v + 1] - a0;
                     const int32_t* seqs = tr.aseq + a0;
+                    KR_DCHECK(cnt >= 1 && seqs[0] >= 1 && seqs[cnt - 1] <= n);
                     const RmStats st = rm_stats(R, stride, seqs, cnt);
                     double nodeVal = 0;
                     for (int a = 0; a < cnt; ++a) {
@@ -807,28 +811,28 @@ void destroy_solver(kr_solver* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     for (int p = 0; p < 2; ++p) {
-        cudaFree(s->d_tree[p]);
-        cudaFree(s->d_bstart[p]);
-        cudaFree(s->regret[p]);
-        cudaFree(s->avg[p]);
-        cudaFree(s->x[p]);
-        cudaFree(s->a[p]);
+        krb::dev_free(s->d_tree[p]);
+        krb::dev_free(s->d_bstart[p]);
+        krb::dev_free(s->regret[p]);
+        krb::dev_free(s->avg[p]);
+        krb::dev_free(s->x[p]);
+        krb::dev_free(s->a[p]);
     }
-    cudaFree(s->d_fac);
-    cudaFree(s->d_ws);
-    cudaFree(s->d_cnt);
-    cudaFree(s->g);
-    cudaFree(s->handval);
-    cudaFree(s->boardval);
-    cudaFree(s->g2);
-    cudaFree(s->handval2);
+    krb::dev_free(s->d_fac);
+    krb::dev_free(s->d_ws);
+    krb::dev_free(s->d_cnt);
+    krb::dev_free(s->g);
+    krb::dev_free(s->handval);
+    krb::dev_free(s->boardval);
+    krb::dev_free(s->g2);
+    krb::dev_free(s->handval2);
     if (s->side) cudaStreamDestroy(s->side);
     if (s->evFork) cudaEventDestroy(s->evFork);
     if (s->evJoin) cudaEventDestroy(s->evJoin);
-    cudaFree(s->d_flag);
-    cudaFree(s->ckSend);
-    cudaFree(s->ckRecv);
-    cudaFree(s->d_bpre);
+    krb::dev_free(s->d_flag);
+    krb::dev_free(s->ckSend);
+    krb::dev_free(s->ckRecv);
+    krb::dev_free(s->d_bpre);
     delete s;
 }
 
@@ -1071,8 +1075,8 @@ std::vector<double> iteration_tables(kr_solver* s, int maxIters, cudaStream_t st
         w *= shrink;
         ws[size_t(t)] = w;
     }
-    cudaFree(s->d_fac);
-    cudaFree(s->d_ws);
+    krb::dev_free(s->d_fac);
+    krb::dev_free(s->d_ws);
     s->d_fac = s->d_ws = nullptr;
     s->d_fac = krb::dev_alloc<double>(int64_t(fac.size()));
     s->d_ws = krb::dev_alloc<double>(int64_t(ws.size()));
@@ -1161,9 +1165,9 @@ int kr_solver_set_comm(kr_solver* s, kr_comm* c, const int32_t* boards_per_rank)
     return guarded([&] {
         if (!s) throw Fail{KR_INVALID_INPUT, "null solver"};
         KR_CK(cudaSetDevice(s->device));
-        cudaFree(s->ckSend);
-        cudaFree(s->ckRecv);
-        cudaFree(s->d_bpre);
+        krb::dev_free(s->ckSend);
+        krb::dev_free(s->ckRecv);
+        krb::dev_free(s->d_bpre);
         s->ckSend = s->ckRecv = nullptr;
         s->d_bpre = nullptr;
         s->comm = nullptr;
@@ -1189,7 +1193,7 @@ int kr_solver_set_comm(kr_solver* s, kr_comm* c, const int32_t* boards_per_rank)
         s->ckRecv = krb::dev_alloc<double>(2 * int64_t(nbMax) * world);
         s->d_bpre = krb::dev_alloc<int32_t>(world + 1);
         KR_CK(cudaMemcpy(s->d_bpre, pre.data(), 4 * pre.size(), cudaMemcpyHostToDevice));
-        cudaFree(s->boardval);  // checkpoint values in global order: 2 x nbTotal
+        krb::dev_free(s->boardval);  // checkpoint values in global order: 2 x nbTotal
         s->boardval = nullptr;
         s->boardval = krb::dev_alloc<double>(2 * int64_t(std::max(s->nbTotal, s->nboards)));
         s->comm = c;
@@ -1384,10 +1388,10 @@ int kr_solver_run(kr_solver* s, const kr_dcfr_params* prm, kr_dcfr_result* r) {
                 }
                 s->t = tEnd;
             } catch (...) {
-                cudaFree(dck);
+                krb::dev_free(dck);
                 throw;
             }
-            cudaFree(dck);
+            krb::dev_free(dck);
         }
         KR_CK(cudaEventRecord(ev1, st));
         KR_CK(cudaEventSynchronize(ev1));
@@ -1756,20 +1760,20 @@ void destroy_turn(kr_turn_solver* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     for (int p = 0; p < 2; ++p) {
-        cudaFree(s->turnTree[p].d);
-        for (auto& t : s->riverTree[p]) cudaFree(t.d);
-        cudaFree(s->regret[p]);
-        cudaFree(s->avg[p]);
-        cudaFree(s->x[p]);
-        cudaFree(s->a[p]);
+        krb::dev_free(s->turnTree[p].d);
+        for (auto& t : s->riverTree[p]) krb::dev_free(t.d);
+        krb::dev_free(s->regret[p]);
+        krb::dev_free(s->avg[p]);
+        krb::dev_free(s->x[p]);
+        krb::dev_free(s->a[p]);
     }
     if (s->ownBufs) {
-        if (s->gathered != s->contrib) cudaFree(s->gathered);
-        cudaFree(s->contrib);
+        if (s->gathered != s->contrib) krb::dev_free(s->gathered);
+        krb::dev_free(s->contrib);
     }
     void* ps[] = {s->d_boff, s->d_r2t, s->d_t2r, s->g,     s->root,  s->handval, s->bval,
                   s->d_one,  s->d_fac, s->d_cnt, s->d_sigma, s->d_roff, s->d_nr, s->d_bpre, s->extra};
-    for (void* q : ps) cudaFree(q);
+    for (void* q : ps) krb::dev_free(q);
     for (cudaStream_t q : s->side) cudaStreamDestroy(q);
     for (cudaEvent_t ev : s->evJoin) cudaEventDestroy(ev);
     if (s->evFork) cudaEventDestroy(s->evFork);
@@ -1953,7 +1957,7 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
                 fac[3 * size_t(t) + 1] = krb::discount_factor(t, prm->beta);
                 fac[3 * size_t(t) + 2] = std::pow(double(t) / (t + 1), prm->gamma);
             }
-            cudaFree(s->d_fac);
+            krb::dev_free(s->d_fac);
             s->d_fac = nullptr;
             s->d_fac = krb::dev_alloc<double>(int64_t(fac.size()));
             if (!s->d_cnt) s->d_cnt = krb::dev_alloc<int>(2);
@@ -2051,10 +2055,10 @@ void turn_shards(kr_turn_solver* s, int world, int rank, const int32_t* bpr, dou
     KR_CK(cudaSetDevice(s->device));
     KR_CK(cudaDeviceSynchronize());
     if (s->ownBufs) {
-        if (s->gathered != s->contrib) cudaFree(s->gathered);
-        cudaFree(s->contrib);
+        if (s->gathered != s->contrib) krb::dev_free(s->gathered);
+        krb::dev_free(s->contrib);
     }
-    cudaFree(s->d_bpre);
+    krb::dev_free(s->d_bpre);
     s->contrib = s->gathered = nullptr;
     s->d_bpre = nullptr;
     s->world = world;

@@ -45,3 +45,18 @@ def factors_equal(fa, fb):
             if not bits_equal(x, y):
                 return False
     return True
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_guards(request):
+    """Under the bounds-checked build (KR_CUDA_LIB_VARIANT=checked), every GPU
+    test ends with the guard zones of all device allocations intact."""
+    yield
+    if os.environ.get("KR_CUDA_LIB_VARIANT") != "checked" or request.node.get_closest_marker("gpu") is None:
+        return
+    import gc
+
+    from paper_2112_03804_b200 import _native as N
+    gc.collect()  # engines / solvers freed now have their guards checked too
+    bad = N.cuda().kr_checked_verify()
+    assert bad == 0, f"{bad} device allocation(s) had a guard zone overwritten"
