@@ -340,6 +340,18 @@ int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma);
  * than DCFR need a treeplex whose parent sequences belong to earlier nodes
  * (every reference skeleton), else KR_INVALID_INPUT. */
 int kr_solver_set_rule(kr_solver* s, int rule);
+/* Which kernel runs `player`'s DCFR step (0 or 1): 2 = compiled for the
+ * player's treeplex at solver creation (NVRTC, kr_jit.cu: one thread per
+ * hand, regrets in registers), 1 = the generic team kernel, 0 = the generic
+ * one-thread-per-hand kernel; -1 for a bad argument.  `why` (optional)
+ * receives the reason the compiled step is not used (empty when it is).
+ * All three give bitwise-identical results. */
+int kr_solver_step_kind(const kr_solver* s, int player, const char** why);
+/* The CUDA C the compiled step is generated from, for treeplex t and update
+ * rule (KR_RULE_*): copies up to cap bytes (NUL-terminated) into buf when buf
+ * is non-NULL and returns the source length, or -1 when the treeplex is not
+ * level-ordered.  Needs no device (inspection and compile tests). */
+int64_t kr_jit_step_source(const kr_treeplex* t, int rule, char* buf, int64_t cap);
 int kr_solver_iterate(kr_solver* s, int n);
 int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2);
 int kr_solver_averages(kr_solver* s, double* avg1, double* avg2);

@@ -101,7 +101,7 @@ CUDA_SYMBOLS = [
     "kr_solver_set_rule", "kr_turn_solver_create", "kr_turn_solver_run", "kr_turn_solver_destroy",
     "kr_turn_solver_launches", "kr_turn_solver_set_exchange", "kr_turn_solver_sizes",
     "kr_factors_build_device", "kr_devfactors_view", "kr_devfactors_seconds", "kr_devfactors_free",
-    "kr_engine_create_device_b", "kr_engine_create_kfactored", "kr_engine_pair", "kr_engine_pair_queue", "kr_checked_verify", "kr_checked_selftest",
+    "kr_engine_create_device_b", "kr_engine_create_kfactored", "kr_engine_pair", "kr_engine_pair_queue", "kr_checked_verify", "kr_checked_selftest", "kr_solver_step_kind", "kr_jit_step_source",
     "kr_comm_unique_id", "kr_comm_init_rank", "kr_comm_init_all", "kr_comm_destroy", "kr_comm_rank", "kr_comm_size",
     "kr_solver_set_comm", "kr_turn_solver_set_comm", "kr_engine_set_selfcheck", "kr_engine_selfcheck_status",
 ]
@@ -134,11 +134,10 @@ def cuda():
         if nccl:  # kr_comm dlopens NCCL on first use: share PyTorch's copy
             os.environ.setdefault("KR_NCCL_LIB", nccl)
         path = cuda_lib_path()
-        if not os.path.exists(path):
-            if os.environ.get("KR_CUDA_LIB_VARIANT") == "checked":
-                _build.build_cuda_variant("checked", ["KR_CHECKED"])
-            else:
-                _build.build_cuda()
+        if os.environ.get("KR_CUDA_LIB_VARIANT") == "checked":
+            _build.build_cuda_variant("checked", ["KR_CHECKED"])   # no-op when current
+        elif not os.path.exists(path):
+            _build.build_cuda()
         L = C.CDLL(path)
         L.kr_last_error.restype = C.c_char_p
         L.kr_last_error.argtypes = [C.POINTER(C.c_int)]
@@ -159,6 +158,9 @@ def cuda():
         L.kr_engine_pair_device.argtypes = [C.c_void_p] * 6
         L.kr_engine_pair.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                      C.c_void_p, C.c_int64]
+        L.kr_jit_step_source.restype = C.c_int64
+        L.kr_jit_step_source.argtypes = [C.POINTER(kr_treeplex), C.c_int, C.c_char_p, C.c_int64]
+        L.kr_solver_step_kind.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_char_p)]
         L.kr_checked_verify.restype = C.c_int64
         L.kr_checked_verify.argtypes = []
         L.kr_checked_selftest.restype = C.c_int64

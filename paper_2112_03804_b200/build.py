@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2112_03804_b200")
 LIBDIR = os.path.join(PKG, "lib")
-CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu", "kr_kfengine.cu", "kr_comm.cu")]
+CUDA_SRC = [os.path.join(PKG, "csrc", "cuda", f) for f in ("kr_engine.cu", "kr_solver.cu", "kr_kron.cu", "kr_factors_dev.cu", "kr_devengine.cu", "kr_kfengine.cu", "kr_comm.cu", "kr_jit.cu")]
 HOST_SRC = [os.path.join(PKG, "csrc", "host", f) for f in ("kr_host.cpp",)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # the system g++ links libstdc++ dynamically (a statically linked libstdc++
@@ -88,6 +88,8 @@ def build_cuda_variant(name, defines=(), replace=None, verbose=False):
     from concurrent.futures import ThreadPoolExecutor
     replace = replace or {}
     out = os.path.join(LIBDIR, f"libkrcuda_{name}.so")
+    if not replace and not _stale(out, CUDA_SRC):
+        return out
     objdir = os.path.join(ROOT, "build", f"cuda_{name}")
     os.makedirs(objdir, exist_ok=True)
     srcs = [replace.get(os.path.basename(s), s) for s in CUDA_SRC]
@@ -138,6 +140,8 @@ def build_cli(force=False, verbose=False):
 def build_all(force=False, verbose=False):
     out = build_host(force, verbose), build_cuda(force, verbose)
     build_cli(force, verbose)
+    # the bounds-checked build (KR_CUDA_LIB_VARIANT=checked), kept current
+    build_cuda_variant("checked", ["KR_CHECKED"], verbose=verbose)
     return out
 
 

@@ -1,0 +1,37 @@
+// kr_jit.cuh — the DCFR player step compiled for a treeplex (kr_jit.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "kr_engine.h"
+
+namespace krb {
+
+constexpr int kJitHands = 32;    // granule of the hands per CTA (one warp)
+constexpr int kJitMaxSeq = 96;   // regrets live in registers: larger trees keep the generic kernels
+
+struct JitStep {
+    cudaKernel_t kern = nullptr;
+    int n = 0;
+    int hands = 128;   // hands (threads) per CTA
+    size_t smem = 0;   // one hands x n tile
+    std::string log;   // NVRTC / ptxas log (registers, spills)
+};
+
+// Compile (or fetch from the process cache) the step kernel for tree t and
+// update rule (KR_RULE_*).  False, with the reason in `why`, when NVRTC is
+// absent, the tree is not level-ordered or too large, or KR_STEP names
+// another kernel.
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why);
+
+// k_player_team's mode-1 arguments (the sweep, sequence form, discount and
+// average of one player over H hands).
+void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, int negate, double* regret,
+                     double* xout, double* avg, double pos, double neg, double shrink, const double* fac,
+                     const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st);
+
+// The generated source (for inspection and tests).
+std::string jit_step_source(const kr_treeplex& t, int rule);
+
+}  // namespace krb

@@ -24,6 +24,7 @@
 #include <cstring>
 
 #include "kr_common.cuh"
+#include "kr_jit.cuh"
 
 struct kr_solver {
     kr_engine* eng = nullptr;
@@ -41,6 +42,12 @@ struct kr_solver {
     bool levelled[2] = {false, false};  // level tables appended (team step kernel)
     int nlev[2] = {0, 0};
     int team[2] = {4, 4};        // lanes per hand in k_player_team (2, 4 or 8), per player
+    // the step compiled for each player's tree (kr_jit.cu), for update rule
+    // jitRule[p]; host copies of the trees to recompile on kr_solver_set_rule
+    krb::JitStep jit[2];
+    int jitRule[2] = {-1, -1};
+    std::string jitWhy[2];
+    std::vector<int32_t> tPar[2], tPtr[2], tSeq[2];
     int teamThreads = 128;       // threads per k_player_team block (KR_TEAM_THREADS: 64, 128 or 256)
     // graph replay of whole iterations (kr_solver_run without early stop):
     // per-iteration factors pos/neg/shrink and weightSum as device tables
@@ -701,8 +708,42 @@ size_t step_smem(int n, int nt, int nn, int na) {
     return size_t(2 * n + 1) * size_t(nt + 1) * 8 + size_t(2 * nn + 1 + na) * 4 + 16;
 }
 
+// Compile each player's step for the current update rule when it pays:
+// grids of at least two CTAs per SM (smaller ones, single boards, keep the
+// team kernel, whose lanes spread a few hundred hands over more threads);
+// KR_STEP=jit forces it, KR_STEP=team / thread forbids it.
+void jit_prepare(kr_solver* s) {
+    const char* env = std::getenv("KR_STEP");
+    const bool force = env && std::string(env) == "jit";
+    for (int p = 0; p < 2; ++p) {
+        if (!s->levelled[p] || s->jitRule[p] == s->rule) continue;
+        s->jit[p] = JitStep{};
+        s->jitRule[p] = -1;
+        if (!force && s->H[p] < int64_t(2) * 148 * kJitHands) {
+            s->jitWhy[p] = "grid below two CTAs per SM";
+            continue;
+        }
+        kr_treeplex t{};
+        t.n_nodes = s->nnodes[p];
+        t.n_seq = s->n[p];
+        t.node_parent_seq = s->tPar[p].data();
+        t.node_action_ptr = s->tPtr[p].data();
+        t.action_seq = s->tSeq[p].data();
+        if (jit_step_compile(t, s->rule, s->jit[p], s->jitWhy[p])) {
+            s->jitRule[p] = s->rule;
+            s->jitWhy[p].clear();
+        }
+    }
+}
+
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
                  cudaStream_t st, bool dev = false) {
+    if (mode == 1 && s->jit[p].kern && s->jitRule[p] == s->rule) {
+        jit_step_launch(s->jit[p], s->device, s->H[p], g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink,
+                        dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st);
+        s->launches++;
+        return;
+    }
     if (s->levelled[p]) {
         const int team = s->team[p], threads = s->teamThreads;
         const int hpb = threads / team;
@@ -894,6 +935,9 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
                     if (sq < 1 || sq > t.n_seq || seen[size_t(sq)]) throw Fail{KR_INVALID_INPUT, "bad action sequence id"};
                     seen[size_t(sq)] = 1;
                 }
+                s->tPar[p].assign(t.node_parent_seq, t.node_parent_seq + t.n_nodes);
+                s->tPtr[p].assign(t.node_action_ptr, t.node_action_ptr + t.n_nodes + 1);
+                s->tSeq[p].assign(t.action_seq, t.action_seq + na);
                 std::vector<int32_t> buf;
                 buf.insert(buf.end(), t.node_parent_seq, t.node_parent_seq + t.n_nodes);
                 buf.insert(buf.end(), t.node_action_ptr, t.node_action_ptr + t.n_nodes + 1);
@@ -969,6 +1013,7 @@ int kr_solver_create(kr_engine* e, const kr_treeplex* p1, const kr_treeplex* p2,
             const int bsm0 = int((2 * s->nnodes[0] + 1 + s->treeLen[0] + 4) * 4 + (s->n[0] + 1) * 128 * 8 + 16);
             const int bsm1 = int((2 * s->nnodes[1] + 1 + s->treeLen[1] + 4) * 4 + (s->n[1] + 1) * 128 * 8 + 16);
             krb::raise_smem_limit(krb::k_best_response, size_t(std::max(bsm0, bsm1)));
+            krb::jit_prepare(s);
         } catch (...) {
             krb::destroy_solver(s);
             throw;
@@ -1207,7 +1252,28 @@ int kr_solver_set_rule(kr_solver* s, int rule) {
         if (rule != 0 && !(s->levelled[0] && s->levelled[1]))
             throw Fail{KR_INVALID_INPUT, "update rule needs a reference-ordered treeplex"};
         s->rule = rule;
+        KR_CK(cudaSetDevice(s->device));
+        krb::jit_prepare(s);
     });
+}
+
+int64_t kr_jit_step_source(const kr_treeplex* t, int rule, char* buf, int64_t cap) {
+    if (!t) return -1;
+    const std::string src = krb::jit_step_source(*t, rule);
+    if (src.empty()) return -1;
+    if (buf && cap > 0) {
+        const size_t n = std::min(src.size(), size_t(cap - 1));
+        std::memcpy(buf, src.data(), n);
+        buf[n] = 0;
+    }
+    return int64_t(src.size());
+}
+
+int kr_solver_step_kind(const kr_solver* s, int player, const char** why) {
+    if (!s || player < 0 || player > 1) return -1;
+    if (why) *why = s->jitWhy[player].c_str();
+    if (s->jit[player].kern && s->jitRule[player] == s->rule) return 2;
+    return s->levelled[player] ? 1 : 0;
 }
 
 int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma) {
@@ -1469,6 +1535,10 @@ struct kr_turn_solver {
     struct TreeDev {
         int32_t* d = nullptr;
         int len = 0, na = 0, nn = 0, n = 0;
+        // the step compiled for this tree (kr_jit.cu) and its host copy
+        krb::JitStep jit;
+        int jitRule = -1;
+        std::vector<int32_t> par, ptr, seq;
     };
     TreeDev turnTree[2];
     std::vector<TreeDev> riverTree[2];             // [p][t]
@@ -1610,6 +1680,9 @@ kr_turn_solver::TreeDev make_tree(const kr_treeplex& t) {
     append_levels(t, buf, ok, nlev);
     if (!ok) throw Fail{KR_INVALID_INPUT, "turn solver needs reference-ordered treeplexes"};
     kr_turn_solver::TreeDev d;
+    d.par.assign(t.node_parent_seq, t.node_parent_seq + t.n_nodes);
+    d.ptr.assign(t.node_action_ptr, t.node_action_ptr + t.n_nodes + 1);
+    d.seq.assign(t.action_seq, t.action_seq + na);
     d.len = int(buf.size());
     d.na = na;
     d.nn = t.n_nodes;
@@ -1621,9 +1694,40 @@ kr_turn_solver::TreeDev make_tree(const kr_treeplex& t) {
 
 constexpr int kTurnTeam = 4;
 
+// Compile the river trees' steps (and the turn tree's when its hands fill
+// the GPU) for the current rule, as jit_prepare does for kr_solver.
+void turn_jit_prepare(kr_turn_solver* s) {
+    const char* env = std::getenv("KR_STEP");
+    const bool force = env && std::string(env) == "jit";
+    auto prep = [&](kr_turn_solver::TreeDev& T, int64_t H) {
+        if (T.jitRule == s->rule) return;
+        T.jit = JitStep{};
+        T.jitRule = -1;
+        if (!force && H < int64_t(2) * 148 * kJitHands) return;
+        kr_treeplex t{};
+        t.n_nodes = T.nn;
+        t.n_seq = T.n;
+        t.node_parent_seq = T.par.data();
+        t.node_action_ptr = T.ptr.data();
+        t.action_seq = T.seq.data();
+        std::string why;
+        if (jit_step_compile(t, s->rule, T.jit, why)) T.jitRule = s->rule;
+    };
+    for (int p = 0; p < 2; ++p) {
+        prep(s->turnTree[p], s->m);
+        for (auto& T : s->riverTree[p]) prep(T, s->Hr);
+    }
+}
+
 void team_step(kr_turn_solver* s, const kr_turn_solver::TreeDev& T, int64_t H, int mode, const double* g, int negate,
                double* regret, double* x, double* avg, double pos, double neg, double shrink, int noAvg,
                double* rootOut, const double* extra, cudaStream_t st, const double* fac, const int* dt) {
+    if (mode == 1 && T.jit.kern && T.jitRule == s->rule) {
+        jit_step_launch(T.jit, s->device, H, g, negate, regret, x, avg, pos, neg, shrink, fac, dt, noAvg, rootOut,
+                        extra, st);
+        s->launches++;
+        return;
+    }
     const int hpb = 256 / kTurnTeam;
     const unsigned grid = unsigned((H + hpb - 1) / hpb);
     if (!grid) return;
@@ -1920,6 +2024,7 @@ int kr_turn_solver_run(kr_turn_solver* s, const kr_dcfr_params* prm, kr_dcfr_res
         if (prm->rule < KR_RULE_DCFR || prm->rule > KR_RULE_PRMP) throw Fail{KR_INVALID_INPUT, "unknown update rule"};
         s->rule = prm->rule;
         KR_CK(cudaSetDevice(s->device));
+        krb::turn_jit_prepare(s);
         cudaStream_t st = s->turnEng->stream;
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         cudaGraphExec_t exec = nullptr;

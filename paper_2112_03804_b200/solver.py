@@ -44,6 +44,19 @@ class Treeplex:
         return N.kr_treeplex(self.n_seq, len(self.parent), *(N.ptr(a) for a in arrs))
 
 
+def jit_step_source(tree: Treeplex, rule=0):
+    """The CUDA C of the player step compiled for `tree` (kr_jit_step_source)."""
+    keep = []
+    t = tree.struct(keep)
+    L = N.cuda()
+    n = L.kr_jit_step_source(C.byref(t), int(rule), None, 0)
+    if n < 0:
+        raise N.InvalidInputError(1, "treeplex is not level-ordered")
+    buf = C.create_string_buffer(int(n) + 1)
+    L.kr_jit_step_source(C.byref(t), int(rule), buf, int(n) + 1)
+    return buf.value.decode()
+
+
 RULE_DCFR, RULE_CFRP, RULE_PRMP = 0, 1, 2
 
 
@@ -109,6 +122,14 @@ class CudaSolver:
         self.comm = None
         self.pot = float(pot)
         self.rows, self.cols = engine.rows, engine.cols
+
+    def step_kind(self, player):
+        """(kind, why): 2 = the step compiled for this player's treeplex
+        (NVRTC), 1 = the generic team kernel, 0 = the generic per-hand kernel;
+        `why` says why the compiled step is not used."""
+        why = C.c_char_p()
+        k = N.cuda().kr_solver_step_kind(self._h, int(player), C.byref(why))
+        return int(k), (why.value or b"").decode()
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

@@ -1,0 +1,91 @@
+"""The DCFR player step compiled for the instance's treeplex (kr_jit.cu).
+
+The compiled step performs the reference's per-node operations in the
+reference's order, like the generic team kernel, so every result must be
+BITWISE the team kernel's and the oracle's:
+* the oracle's gap trajectories (checkpointEvery = 1) on the corpus trees
+  with the compiled step forced (KR_STEP=jit: small instances end in partial
+  32-hand tiles, `bench` with 60 hands has a full TMA tile and a partial one);
+* a 12-board turn (12,972 hands per player: the compiled step is the default
+  there) against KR_STEP=team for DCFR, CFR+ and PRM+, through the graph-
+  replayed run and the incremental iterate path."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from conftest import bits_equal
+from paper_2112_03804_b200 import host as H
+from paper_2112_03804_b200.solver import DcfrParams, dcfr_solve, jit_step_source, solver_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,kw,tech,iters", [
+    ("twenty_card", {}, "b", 300),
+    ("golden", {}, "b", 300),
+    ("bluffing", {}, "b", 300),
+    ("all_tie", {}, "b", 100),
+    ("random_small", dict(seed=1), "b", 200),
+    ("bench", dict(seed=7, hands=60), "b", 200),
+])
+def test_forced_jit_gap_trajectory_bitwise(name, kw, tech, iters, monkeypatch):
+    monkeypatch.setenv("KR_STEP", "jit")
+    p, o = H.builtin(name, **kw), po.Instance.builtin(name, **kw)
+    s = solver_for([(p, p.sparsify(tech, True))])
+    assert s.step_kind(0)[0] == 2 and s.step_kind(1)[0] == 2, s.step_kind(0)
+    r = s.run(DcfrParams(max_iters=iters, checkpoint_every=1))
+    ro = po.dcfr(o, o.sparsify(tech, True), max_iters=iters, checkpoint_every=1)
+    assert bits_equal(r.trace_br1, ro["trace_br1"]) and bits_equal(r.trace_br2, ro["trace_br2"])
+    assert bits_equal(r.avg1, ro["avg1"]) and bits_equal(r.avg2, ro["avg2"])
+
+
+@pytest.fixture(scope="module")
+def turn12():
+    return H.turn_instances(nboards=12, factors=False)
+
+
+def run_turn(boards, params, step, monkeypatch, incremental=False):
+    if step == "default":
+        monkeypatch.delenv("KR_STEP", raising=False)
+    else:
+        monkeypatch.setenv("KR_STEP", step)
+    s = solver_for(boards, implicit=True)
+    kinds = (s.step_kind(0)[0], s.step_kind(1)[0])
+    if incremental:
+        s.begin(params)
+        s.iterate(params.max_iters)
+        return kinds, s.averages()
+    return kinds, s.run(params)
+
+
+@pytest.mark.parametrize("preset", ["dcfr", "cfr_plus", "prm_plus"])
+def test_turn12_jit_equals_team(turn12, preset, monkeypatch):
+    prm = DcfrParams(max_iters=40, checkpoint_every=10) if preset == "dcfr" else \
+        getattr(DcfrParams, preset)(max_iters=40, checkpoint_every=10)
+    kinds, rj = run_turn(turn12, prm, "default", monkeypatch)
+    assert kinds == (2, 2)
+    kt, rt = run_turn(turn12, prm, "team", monkeypatch)
+    assert kt == (1, 1)
+    assert bits_equal(rj.trace_br1, rt.trace_br1) and bits_equal(rj.trace_br2, rt.trace_br2)
+    assert bits_equal(rj.avg1, rt.avg1) and bits_equal(rj.avg2, rt.avg2)
+
+
+def test_turn12_incremental_jit_equals_team(turn12, monkeypatch):
+    prm = DcfrParams(max_iters=25)
+    kj, aj = run_turn(turn12, prm, "default", monkeypatch, incremental=True)
+    kt, at = run_turn(turn12, prm, "team", monkeypatch, incremental=True)
+    assert kj == (2, 2) and kt == (1, 1)
+    assert bits_equal(aj[0], at[0]) and bits_equal(aj[1], at[1])
+
+
+def test_step_kind_reports_why(monkeypatch):
+    p = H.builtin("twenty_card")
+    monkeypatch.setenv("KR_STEP", "team")
+    s = solver_for([(p, p.sparsify("b", True))])
+    k, why = s.step_kind(0)
+    assert k == 1 and why   # the team kernel, with the reason
+    monkeypatch.delenv("KR_STEP")
+    s = solver_for([(p, p.sparsify("b", True))])
+    k, why = s.step_kind(0)
+    assert k == 1 and "two CTAs per SM" in why   # 105 hands: the team kernel pays there
+    assert "kr_step" in jit_step_source(p.treeplex(0))
