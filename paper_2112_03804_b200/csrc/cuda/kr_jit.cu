@@ -30,6 +30,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -172,6 +173,60 @@ std::string prob(const std::string& p, const std::string& v) {
 std::string reg(int sq) { return "r" + std::to_string(sq - 1); }       // regret of sequence sq
 std::string val(int sq) { return "Gh[" + std::to_string(sq - 1) + "]"; }  // value / probability / reach of sq
 
+// One decision node of the sweep (k_player_team mode 1, per node): regret
+// matching on the pre-update regrets, the node value, the regret update, the
+// rule's discount, the post-update strategy into the value slots.  child(c)
+// is the expression holding child node c's value.
+template <class Child>
+void emit_node(std::ostringstream& o, const Levels& L, int v, int rule, Child&& child) {
+    const int a0 = L.aptr[size_t(v)], cnt = L.aptr[size_t(v) + 1] - a0;
+    std::vector<int> seqs(L.aseq.begin() + a0, L.aseq.begin() + a0 + cnt);
+    const std::string p = "s" + std::to_string(v) + "_";
+    o << "  {\n";
+    std::vector<std::string> rv;
+    for (int sq : seqs) rv.push_back(reg(sq));
+    emit_stats(o, p, rv);
+    o << "  double nodeVal = 0;\n";
+    for (int a = 0; a < cnt; ++a) {
+        const int sq = seqs[size_t(a)];
+        o << "  double ev" << a << ";\n  { double cs = 0.0;";
+        for (int c : L.children[size_t(sq)]) o << " cs += " << child(c) << ";";
+        o << " if (ex) cs += ex[" << sq - 1 << "];";
+        o << " const double gr = " << val(sq) << "; const double gv = negate ? -gr : gr; ev" << a
+          << " = gv + cs; nodeVal += " << prob(p, reg(sq)) << " * ev" << a << "; }\n";
+    }
+    for (int a = 0; a < cnt; ++a) {
+        const int sq = seqs[size_t(a)];
+        o << "  const double d" << a << " = ev" << a << " - nodeVal; " << reg(sq) << " += d" << a << ";\n";
+    }
+    o << "  nv" << v << " = nodeVal;\n";
+    if (rule != 0)
+        for (int sq : seqs) o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
+    const std::string q = "t" + std::to_string(v) + "_";
+    if (rule == 2) {  // PRM+: match R + d
+        std::vector<std::string> w;
+        for (int a = 0; a < cnt; ++a) {
+            o << "  const double w" << a << " = " << reg(seqs[size_t(a)]) << " + d" << a << ";\n";
+            w.push_back("w" + std::to_string(a));
+        }
+        emit_stats(o, q, w);
+        for (int a = 0; a < cnt; ++a) o << "  " << val(seqs[size_t(a)]) << " = " << prob(q, w[size_t(a)]) << ";\n";
+    } else {
+        emit_stats(o, q, rv);
+        for (int sq : seqs) o << "  " << val(sq) << " = " << prob(q, reg(sq)) << ";\n";
+    }
+    o << "  }\n";
+}
+
+// sequenceForm for node v's actions: reach = mass * prob (V[0] = 1.0)
+void emit_reach(std::ostringstream& o, const Levels& L, int v) {
+    const int ps = L.parentSeq[size_t(v)];
+    for (int a = L.aptr[size_t(v)]; a < L.aptr[size_t(v) + 1]; ++a) {
+        const int sq = L.aseq[size_t(a)];
+        o << "  " << val(sq) << " = " << (ps == 0 ? std::string("1.0") : val(ps)) << " * " << val(sq) << ";\n";
+    }
+}
+
 // The kernel source for one player's tree and update rule (mode 1 of
 // k_player_team: sweep, sequence form, discount, average).
 std::string generate(const Levels& L, int rule, int minBlocks, int hands) {
@@ -229,61 +284,17 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands) {
   if (lane < nh) {
     const double* ex = extra ? extra + (h0 + lane) * N : nullptr;
 )";
+    for (int v = 0; v < L.nn; ++v) o << "  double nv" << v << ";\n";
     // cfrSweep, deepest level first (k_player_team mode 1)
     for (int l = L.nlev - 1; l >= 0; --l)
-        for (int v : L.levNodes[size_t(l)]) {
-            const int a0 = L.aptr[size_t(v)], cnt = L.aptr[size_t(v) + 1] - a0;
-            std::vector<int> seqs(L.aseq.begin() + a0, L.aseq.begin() + a0 + cnt);
-            const std::string p = "s" + std::to_string(v) + "_";
-            o << "  double nv" << v << ";\n  {\n";
-            std::vector<std::string> rv;
-            for (int sq : seqs) rv.push_back(reg(sq));
-            emit_stats(o, p, rv);
-            o << "  double nodeVal = 0;\n";
-            for (int a = 0; a < cnt; ++a) {
-                const int sq = seqs[size_t(a)];
-                o << "  double ev" << a << ";\n  { double cs = 0.0;";
-                for (int c : L.children[size_t(sq)]) o << " cs += nv" << c << ";";
-                o << " if (ex) cs += ex[" << sq - 1 << "];";
-                o << " const double gr = " << val(sq) << "; const double gv = negate ? -gr : gr; ev" << a
-                  << " = gv + cs; nodeVal += " << prob(p, reg(sq)) << " * ev" << a << "; }\n";
-            }
-            for (int a = 0; a < cnt; ++a) {
-                const int sq = seqs[size_t(a)];
-                o << "  const double d" << a << " = ev" << a << " - nodeVal; " << reg(sq) << " += d" << a << ";\n";
-            }
-            o << "  nv" << v << " = nodeVal;\n";
-            if (rule != 0)
-                for (int sq : seqs)
-                    o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
-            const std::string q = "t" + std::to_string(v) + "_";
-            if (rule == 2) {  // PRM+: match R + d
-                std::vector<std::string> w;
-                for (int a = 0; a < cnt; ++a) {
-                    o << "  const double w" << a << " = " << reg(seqs[size_t(a)]) << " + d" << a << ";\n";
-                    w.push_back("w" + std::to_string(a));
-                }
-                emit_stats(o, q, w);
-                for (int a = 0; a < cnt; ++a) o << "  " << val(seqs[size_t(a)]) << " = " << prob(q, w[size_t(a)]) << ";\n";
-            } else {
-                emit_stats(o, q, rv);
-                for (int sq : seqs) o << "  " << val(sq) << " = " << prob(q, reg(sq)) << ";\n";
-            }
-            o << "  }\n";
-        }
+        for (int v : L.levNodes[size_t(l)]) emit_node(o, L, v, rule, [](int c) { return "nv" + std::to_string(c); });
     // seqVal[0]: root nodes, descending
     o << "  if (rootOut) { double acc = 0.0;";
     for (auto it = L.levNodes[0].rbegin(); it != L.levNodes[0].rend(); ++it) o << " acc += nv" << *it << ";";
     o << " rootOut[h0 + lane] = acc; }\n";
     // sequenceForm: reach = mass * prob, root level first
     for (int l = 0; l < L.nlev; ++l)
-        for (int v : L.levNodes[size_t(l)]) {
-            const int ps = L.parentSeq[size_t(v)];
-            for (int a = L.aptr[size_t(v)]; a < L.aptr[size_t(v) + 1]; ++a) {
-                const int sq = L.aseq[size_t(a)];
-                o << "  " << val(sq) << " = " << (ps == 0 ? std::string("1.0") : val(ps)) << " * " << val(sq) << ";\n";
-            }
-        }
+        for (int v : L.levNodes[size_t(l)]) emit_reach(o, L, v);
     if (rule == 0)  // discount (solver.hpp:262-264)
         for (int sq = 1; sq <= N; ++sq)
             o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
@@ -332,9 +343,227 @@ int jit_hands() {
     return 128;
 }
 
+// Two-group kernels: resident 64-thread units per SM they are compiled for
+// (KR_JIT_PAIR_MINB overrides; 11 caps registers at ~93).
+int jit_pair_min_blocks() {
+    if (const char* e = std::getenv("KR_JIT_PAIR_MINB")) return std::max(1, std::atoi(e));
+    return 11;
+}
+
 int jit_min_blocks() {
     if (const char* e = std::getenv("KR_JIT_MINB")) return std::max(1, std::atoi(e));
     return 12;
+}
+
+// Two warp groups per hand set: group 0 owns the level-0 (root) nodes and
+// part of the subtrees below them, group 1 the other subtrees, balanced by
+// action count.  Each thread holds only its group's regrets (about half), so
+// twice the warps fit an SM.  Group 1 hands its subtree roots' node values to
+// group 0 through shared memory; group 0 hands the root sequences' reach back.
+// Returns false when the tree has no level-1 node to give group 1.
+struct Split {
+    std::vector<int> grp;     // per node: 0 or 1
+    std::vector<int> slot;    // per node: exchange slot (group-1 level-1 nodes), else -1
+    int nx = 0;
+};
+
+bool split_tree(const Levels& L, Split& S) {
+    if (L.nlev < 2) return false;
+    std::vector<int> owner(size_t(L.n) + 1, -1);
+    for (int v = 0; v < L.nn; ++v)
+        for (int a = L.aptr[size_t(v)]; a < L.aptr[size_t(v) + 1]; ++a) owner[size_t(L.aseq[size_t(a)])] = v;
+    std::vector<int> sub(size_t(L.nn), -1), weight(size_t(L.nn), 0);
+    int w0 = 0;
+    for (int v = 0; v < L.nn; ++v) {
+        const int acts = L.aptr[size_t(v) + 1] - L.aptr[size_t(v)];
+        if (L.lev[size_t(v)] == 0) {
+            w0 += acts;
+            continue;
+        }
+        int u = v;
+        while (L.lev[size_t(u)] > 1) u = owner[size_t(L.parentSeq[size_t(u)])];
+        sub[size_t(v)] = u;
+        weight[size_t(u)] += acts;
+    }
+    std::vector<int> roots(L.levNodes[1]);
+    std::sort(roots.begin(), roots.end(), [&](int a, int b) {
+        return weight[size_t(a)] != weight[size_t(b)] ? weight[size_t(a)] > weight[size_t(b)] : a < b;
+    });
+    std::vector<int> rootGrp(size_t(L.nn), 0);
+    int w1 = 0;
+    for (int u : roots) {
+        if (w1 <= w0) {
+            rootGrp[size_t(u)] = 1;
+            w1 += weight[size_t(u)];
+        } else {
+            w0 += weight[size_t(u)];
+        }
+    }
+    if (w1 == 0) return false;
+    S.grp.assign(size_t(L.nn), 0);
+    S.slot.assign(size_t(L.nn), -1);
+    for (int v = 0; v < L.nn; ++v)
+        if (L.lev[size_t(v)] > 0) S.grp[size_t(v)] = rootGrp[size_t(sub[size_t(v)])];
+    for (int v : L.levNodes[1])
+        if (S.grp[size_t(v)] == 1) S.slot[size_t(v)] = S.nx++;
+    return true;
+}
+
+std::string generate_pair(const Levels& L, const Split& S, int rule, int minBlocks, int hands) {
+    std::ostringstream o;
+    const int N = L.n;
+    o << kPreamble;
+    o << "#define N " << N << "\n#define HB " << hands << "\n#define NT (2 * HB)\n#define NX " << S.nx << "\n";
+    o << "#define MINB " << minBlocks << "\n";
+    o << R"(__device__ __forceinline__ void bar_all() { asm volatile("barrier.sync 1, %0;" :: "n"(NT) : "memory"); }
+extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __restrict__ g, int negate,
+    double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
+    double shrink, const double* __restrict__ fac, const int* __restrict__ dt, int noAvg,
+    double* __restrict__ rootOut, const double* __restrict__ extra, long long H) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(128) double G[];  // tile: regrets in, then gradients -> values -> probabilities -> x
+  double* X = G + HB * N;                        // group 1 -> group 0: subtree roots' node values
+  __shared__ __align__(8) u64 bar;
+  if (fac) { const int t = *dt; pos = fac[3 * t]; neg = fac[3 * t + 1]; shrink = fac[3 * t + 2]; }
+  const int tid = threadIdx.x, grp = tid / HB, hand = tid - grp * HB;
+  const long long h0 = (long long)blockIdx.x * HB;
+  const int nh = (int)(H - h0 < HB ? H - h0 : HB);
+  const long long e0 = h0 * N;
+  const int ne = nh * N;
+  const unsigned bytes = HB * N * 8;
+  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (unsigned long long)(g + e0) |
+                                   (unsigned long long)(xout + e0) | (noAvg ? 0ull : (unsigned long long)(avg + e0))) &
+                                  15ull) == 0;
+  if (full) {
+    if (tid == 0) {
+      bar_init(&bar);
+      bar_expect(&bar, bytes);
+      g2s(G, regret + e0, bytes, &bar);
+      l2_prefetch(g + e0, bytes);
+      if (!noAvg) l2_prefetch(avg + e0, bytes);
+    }
+    bar_all();
+    bar_wait(&bar, 0);
+  } else {
+    for (int q = tid; q < ne; q += NT) G[q] = regret[e0 + q];
+    bar_all();
+  }
+  double* Gh = G + hand * N;
+  double* Xh = X + hand * NX;
+  const bool valid = hand < nh;
+  const double* ex = (extra && valid) ? extra + (h0 + hand) * N : nullptr;
+)";
+    // the part both groups run between their own sections (same barrier sequence)
+    const std::string loadG = R"(  bar_all();
+  if (full) {
+    if (tid == 0) { fence_async(); bar_expect(&bar, bytes); g2s(G, g + e0, bytes, &bar); }
+    bar_wait(&bar, 1);
+  } else {
+    for (int q = tid; q < ne; q += NT) G[q] = g[e0 + q];
+  }
+  bar_all();
+)";
+    const std::string outX = R"(  bar_all();
+  if (full) {
+    fence_async();
+    bar_all();
+    if (tid == 0) { s2g(xout + e0, G, bytes); bulk_commit(); }
+  } else {
+    for (int q = tid; q < ne; q += NT) xout[e0 + q] = G[q];
+  }
+  if (!noAvg) {
+#pragma unroll 8
+    for (int q = tid; q < ne; q += NT) avg[e0 + q] = (avg[e0 + q] + G[q]) * shrink;
+  }
+  if (full && tid == 0) bulk_wait_read();
+  bar_all();
+)";
+    const std::string outR = R"(  if (full) {
+    fence_async();
+    bar_all();
+    if (tid == 0) { s2g(regret + e0, G, bytes); bulk_commit(); bulk_wait_all(); }
+  } else {
+    bar_all();
+    for (int q = tid; q < ne; q += NT) regret[e0 + q] = G[q];
+  }
+)";
+    for (int gi = 0; gi < 2; ++gi) {
+        std::vector<int> mine;   // sequences of this group's nodes
+        for (int v = 0; v < L.nn; ++v)
+            if (S.grp[size_t(v)] == gi)
+                for (int a = L.aptr[size_t(v)]; a < L.aptr[size_t(v) + 1]; ++a) mine.push_back(L.aseq[size_t(a)]);
+        std::sort(mine.begin(), mine.end());
+        o << (gi == 0 ? "  if (grp == 0) {\n" : "  } else {\n");
+        for (int sq : mine) o << "  double " << reg(sq) << " = " << val(sq) << ";\n";
+        for (int v = 0; v < L.nn; ++v)
+            if (S.grp[size_t(v)] == gi) o << "  double nv" << v << " = 0.0;\n";
+        o << loadG;
+        // the group's nodes below level 0, deepest level first
+        o << "  if (valid) {\n";
+        for (int l = L.nlev - 1; l >= 1; --l)
+            for (int v : L.levNodes[size_t(l)])
+                if (S.grp[size_t(v)] == gi) emit_node(o, L, v, rule, [](int c) { return "nv" + std::to_string(c); });
+        if (gi == 1)
+            for (int v : L.levNodes[1])
+                if (S.grp[size_t(v)] == 1) o << "  Xh[" << S.slot[size_t(v)] << "] = nv" << v << ";\n";
+        o << "  }\n  bar_all();\n";   // B: group 1's subtree values are in X
+        if (gi == 0) {
+            o << "  if (valid) {\n";
+            for (int v : L.levNodes[0])
+                emit_node(o, L, v, rule, [&](int c) {
+                    return S.grp[size_t(c)] == 1 ? "Xh[" + std::to_string(S.slot[size_t(c)]) + "]"
+                                                 : "nv" + std::to_string(c);
+                });
+            o << "  if (rootOut) { double acc = 0.0;";
+            for (auto it = L.levNodes[0].rbegin(); it != L.levNodes[0].rend(); ++it) o << " acc += nv" << *it << ";";
+            o << " rootOut[h0 + hand] = acc; }\n";
+            for (int v : L.levNodes[0]) emit_reach(o, L, v);
+            o << "  }\n";
+        }
+        o << "  bar_all();\n";   // C: the root sequences' reach is in G
+        o << "  if (valid) {\n";
+        for (int l = 1; l < L.nlev; ++l)
+            for (int v : L.levNodes[size_t(l)])
+                if (S.grp[size_t(v)] == gi) emit_reach(o, L, v);
+        if (rule == 0)
+            for (int sq : mine) o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
+        o << "  }\n";
+        o << outX;
+        for (int sq : mine) o << "  " << val(sq) << " = " << reg(sq) << ";\n";
+        o << outR;
+    }
+    o << "  }\n}\n";
+    return o.str();
+}
+
+// The source for the tree: one thread per hand, compiled for the resident
+// CTAs per SM that one round of config 3's hands needs; KR_JIT_SPLIT=1: two
+// warp groups per hand set when the tree splits (80 registers, twice the
+// warps, but the groups wait on each other: within 1-2% of the one-thread
+// kernel at config 3, profiles/r02/jit_step_probe_r02z.log).
+struct Gen {
+    std::string src;
+    int hands = 0, threads = 0;   // hands and threads per CTA
+    size_t smem = 0;              // dynamic shared memory per CTA
+};
+
+Gen jit_source(const Levels& L, int rule, int hands) {
+    Gen r;
+    Split S;
+    const char* e = std::getenv("KR_JIT_SPLIT");
+    if (e && std::atoi(e) == 1 && split_tree(L, S)) {
+        const int hb = std::max(32, hands / 2);   // hands per CTA; 2 x hb threads
+        r.src = generate_pair(L, S, rule, std::max(1, jit_pair_min_blocks() * 64 / (2 * hb)), hb);
+        r.hands = hb;
+        r.threads = 2 * hb;
+        r.smem = size_t(hb) * size_t(L.n + S.nx) * sizeof(double);
+        return r;
+    }
+    r.src = generate(L, rule, std::max(1, jit_min_blocks() * 32 / hands), hands);
+    r.hands = r.threads = hands;
+    r.smem = size_t(hands) * size_t(L.n) * sizeof(double);
+    return r;
 }
 
 struct Compiled {
@@ -373,8 +602,8 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         why = "NVRTC not available";
         return false;
     }
-    const int hands = jit_hands();
-    const std::string src = generate(L, rule, jit_min_blocks() * 32 / hands, hands);
+    const Gen gen = jit_source(L, rule, jit_hands());
+    const std::string& src = gen.src;
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = jit_cache().find(src);
     if (it == jit_cache().end()) {
@@ -411,8 +640,9 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
     }
     out.kern = it->second.kern;
     out.n = t.n_seq;
-    out.hands = hands;
-    out.smem = size_t(hands) * size_t(t.n_seq) * sizeof(double);
+    out.hands = gen.hands;
+    out.threads = gen.threads;
+    out.smem = gen.smem;
     out.log = it->second.log;
     return true;
 }
@@ -432,7 +662,7 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
     void* args[] = {&g, &negate, &regret, &xout, &avg, &pos, &neg, &shrink, &fac, &dt, &noAvg, &rootOut, &extra, &Hl};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(unsigned(j.hands));
+    cfg.blockDim = dim3(unsigned(j.threads));
     cfg.dynamicSmemBytes = j.smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -448,7 +678,7 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
 std::string jit_step_source(const kr_treeplex& t, int rule) {
     Levels L;
     if (!levels_of(t, L)) return "";
-    return generate(L, rule, jit_min_blocks() * 32 / jit_hands(), jit_hands());
+    return jit_source(L, rule, jit_hands()).src;
 }
 
 }  // namespace krb

@@ -14,8 +14,9 @@ constexpr int kJitMaxSeq = 96;   // regrets live in registers: larger trees keep
 struct JitStep {
     cudaKernel_t kern = nullptr;
     int n = 0;
-    int hands = 128;   // hands (threads) per CTA
-    size_t smem = 0;   // one hands x n tile
+    int hands = 128;   // hands per CTA
+    int threads = 128; // threads per CTA (two per hand in the two-group kernels)
+    size_t smem = 0;   // one hands x n tile (+ the two-group exchange slots)
     std::string log;   // NVRTC / ptxas log (registers, spills)
 };
 

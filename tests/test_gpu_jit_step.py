@@ -58,8 +58,10 @@ def run_turn(boards, params, step, monkeypatch, incremental=False):
     return kinds, s.run(params)
 
 
+@pytest.mark.parametrize("split", ["0", "1"], ids=["one-thread", "two-groups"])
 @pytest.mark.parametrize("preset", ["dcfr", "cfr_plus", "prm_plus"])
-def test_turn12_jit_equals_team(turn12, preset, monkeypatch):
+def test_turn12_jit_equals_team(turn12, preset, split, monkeypatch):
+    monkeypatch.setenv("KR_JIT_SPLIT", split)
     prm = DcfrParams(max_iters=40, checkpoint_every=10) if preset == "dcfr" else \
         getattr(DcfrParams, preset)(max_iters=40, checkpoint_every=10)
     kinds, rj = run_turn(turn12, prm, "default", monkeypatch)

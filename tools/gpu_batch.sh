@@ -1,4 +1,4 @@
 # ad-hoc GPU batch (edited per call)
 T=r02z
-timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${T}_pytest_jit_all.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest_jit_all.log
-tail -5 gpurun_out/${T}_pytest_jit_all.log
+KR_JIT_HANDS=64 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"kr_step" -s 10 -c 1 -o gpurun_out/${T}_jit_pair -f python tools/solver_probe.py kron 20 > gpurun_out/${T}_ncu_jit.log 2>&1
+tail -1 gpurun_out/${T}_ncu_jit.log
