@@ -387,6 +387,13 @@ struct kr_engine {
 namespace krb {
 // Enqueue the products on `s` (device pointers).
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s);
+// Boards [b0, b1) of one product (direction dir), for the board-block
+// engines (implicit, Kronecker-factored); no flop accounting (the caller
+// accounts the whole product once with engine_account).  False for engines
+// whose products do not split by board range (the factored engine).
+bool engine_product_boards(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1);
+void engine_account(kr_engine* e, int dir);
+int engine_boards(const kr_engine* e);
 // SelfCheck: compare out with the reference engine's product of in (every
 // scEvery-th call; no-op when off or while s is being captured); and raise
 // KR_CONTRACT if a check has failed (synchronises the engine's stream).

@@ -2086,6 +2086,15 @@ void engine_selfcheck_raise(kr_engine* e) {
                                     std::to_string(f[1]) + " x tol (1 + max|expect|) (solver.hpp:84-91)"};
 }
 
+bool engine_product_boards(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
+    if (e->kron) kron_product(e, dir, in, out, s, b0, b1);
+    else if (e->kf) kf_product(e, dir, in, out, s, b0, b1);
+    else return false;
+    return true;
+}
+void engine_account(kr_engine* e, int dir) { account(e, dir); }
+int engine_boards(const kr_engine* e) { return e->grpBoard.empty() ? 1 : e->grpBoard.back(); }
+
 void engine_ax(kr_engine* e, const double* x, double* y, cudaStream_t s) { engine_product(e, 0, x, y, s); }
 void engine_atx(kr_engine* e, const double* y, double* x, cudaStream_t s) { engine_product(e, 1, y, x, s); }
 

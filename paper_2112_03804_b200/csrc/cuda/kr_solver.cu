@@ -48,6 +48,12 @@ struct kr_solver {
     int jitRule[2] = {-1, -1};
     std::string jitWhy[2];
     std::vector<int32_t> tPar[2], tPtr[2], tSeq[2];
+    // board-half pipelining of the captured iteration (overlap_ok): the
+    // steps run on ovSide beside the next half's product; gB holds g2 so the
+    // two players' gradients never share a buffer while both are in flight
+    cudaStream_t ovSide = nullptr;
+    cudaEvent_t ovEv[8] = {};
+    double* gB = nullptr;
     int teamThreads = 128;       // threads per k_player_team block (KR_TEAM_THREADS: 64, 128 or 256)
     // graph replay of whole iterations (kr_solver_run without early stop):
     // per-iteration factors pos/neg/shrink and weightSum as device tables
@@ -736,10 +742,15 @@ void jit_prepare(kr_solver* s) {
     }
 }
 
+// Player p's step over hands [hoff, hoff + hcnt) (all hands: hcnt < 0); g
+// is the gradient of those hands' rows.
 void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, double pos, double neg, double shrink,
-                 cudaStream_t st, bool dev = false) {
+                 cudaStream_t st, bool dev = false, int64_t hoff = 0, int64_t hcnt = -1) {
+    const int64_t H = hcnt < 0 ? s->H[p] : hcnt;
+    const int64_t o = hoff * s->n[p];
+    double *regret = s->regret[p] + o, *x = s->x[p] + o, *avg = s->avg[p] + o;
     if (mode == 1 && s->jit[p].kern && s->jitRule[p] == s->rule) {
-        jit_step_launch(s->jit[p], s->device, s->H[p], g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink,
+        jit_step_launch(s->jit[p], s->device, H, g, negate, regret, x, avg, pos, neg, shrink,
                         dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st);
         s->launches++;
         return;
@@ -747,13 +758,13 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
     if (s->levelled[p]) {
         const int team = s->team[p], threads = s->teamThreads;
         const int hpb = threads / team;
-        const unsigned grid = unsigned((s->H[p] + hpb - 1) / hpb);
+        const unsigned grid = unsigned((H + hpb - 1) / hpb);
         if (grid == 0) return;
         const size_t smem = team_smem(s->n[p], s->nnodes[p], hpb, s->treeLen[p]);
         auto kern = team == 2 ? k_player_team<2> : team == 4 ? k_player_team<4> : k_player_team<8>;
-        krb::launch_pdl(true, kern, grid, threads, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p], s->treeLen[p], s->H[p],
-                                      hpb, g, negate, s->regret[p], s->x[p], s->avg[p], pos, neg, shrink, s->rule,
-                                      dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr);
+        krb::launch_pdl(true, kern, grid, threads, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->na[p],
+                        s->treeLen[p], H, hpb, g, negate, regret, x, avg, pos, neg, shrink, s->rule,
+                        dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr);
         KR_CK_LAUNCH();
         s->launches++;
         return;
@@ -761,12 +772,12 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
     if (s->rule != 0) throw Fail{KR_INVALID_INPUT, "update rule needs a reference-ordered treeplex"};
     if (dev) throw Fail{KR_CUDA, "internal: graph replay needs the team step kernel"};
     const int nt = s->nt[p];
-    const unsigned grid = unsigned((s->H[p] + nt - 1) / nt);
+    const unsigned grid = unsigned((H + nt - 1) / nt);
     if (grid == 0) return;
     const int na = s->na[p];
     const size_t smem = step_smem(s->n[p], nt, s->nnodes[p], na);
-    krb::launch(k_player_step, grid, nt, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], s->H[p], nt, g, negate,
-                                          s->regret[p], s->x[p], s->avg[p], pos, neg, shrink);
+    krb::launch(k_player_step, grid, nt, smem, st, mode, s->d_tree[p], s->nnodes[p], s->n[p], H, nt, g, negate,
+                regret, x, avg, pos, neg, shrink);
     KR_CK_LAUNCH();
     s->launches++;
 }
@@ -851,6 +862,10 @@ void best_response_dev(kr_solver* s, int player, const double* opp, std::vector<
 void destroy_solver(kr_solver* s) {
     if (!s) return;
     cudaSetDevice(s->device);
+    if (s->ovSide) cudaStreamDestroy(s->ovSide);
+    for (cudaEvent_t ev : s->ovEv)
+        if (ev) cudaEventDestroy(ev);
+    krb::dev_free(s->gB);
     for (int p = 0; p < 2; ++p) {
         krb::dev_free(s->d_tree[p]);
         krb::dev_free(s->d_bstart[p]);
@@ -1066,9 +1081,62 @@ struct GraphDelta {
 // plus a checkpoint when withCk (normalise, the two best responses into
 // checkpoint slot d_cnt[1] of dck, tick): the scalars come from the device
 // tables d_fac / d_ws indexed by the device counters.
+// Board-half pipelining: every board is an independent block of A (the
+// products and both players' steps are board-local), so the iteration runs
+// as A x2 [half 0], A x2 [half 1] beside P1 [half 0], A^T x1 [half 0] beside
+// P1 [half 1], ... : each step overlaps the other half's product (the
+// products are shared-memory bound, the steps latency-bound).  Every board
+// computes exactly what it computes in the serial order.  Multi-board
+// implicit and Kronecker-factored engines, opt-in (KR_OVERLAP=1): measured
+// slower at config 3 (K7 DCFR 5,055 -> 4,147 it/s, Kronecker-factored
+// 1,323 -> 1,178): half-size product grids lose more to their tails than the
+// steps gain beside them (profiles/r02/jit_step_probe_r02z.log).
+bool overlap_ok(const kr_solver* s) {
+    const char* env = std::getenv("KR_OVERLAP");
+    if (!(env && std::atoi(env) == 1)) return false;
+    return s->nboards >= 2 && (s->eng->kron || s->eng->kf) && krb::engine_boards(s->eng) == s->nboards;
+}
+
+void ensure_overlap(kr_solver* s) {
+    if (s->ovSide) return;
+    KR_CK(cudaStreamCreateWithFlags(&s->ovSide, cudaStreamNonBlocking));
+    for (auto& ev : s->ovEv) KR_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    s->gB = krb::dev_alloc<double>(std::max<int64_t>(s->eng->cols, 1));
+}
+
+// One iteration's products and steps, board halves pipelined (graph capture).
+void overlapped_iteration(kr_solver* s, cudaStream_t st) {
+    kr_engine* e = s->eng;
+    cudaStream_t T = s->ovSide;
+    const int nb = s->nboards, bm = nb / 2;
+    const int b[3] = {0, bm, nb};
+    cudaEvent_t* ev = s->ovEv;
+    KR_CK(cudaEventRecord(ev[0], st));
+    KR_CK(cudaStreamWaitEvent(T, ev[0], 0));
+    for (int p = 0; p < 2; ++p) {
+        const double* in = s->x[1 - p];
+        double* g = p == 0 ? s->g : s->gB;
+        for (int h = 0; h < 2; ++h) {
+            if (p == 1) KR_CK(cudaStreamWaitEvent(st, ev[2 + h], 0));   // x1 of this half is final
+            if (!krb::engine_product_boards(e, p, in, g, st, b[h], b[h + 1]))
+                throw Fail{KR_CUDA, "internal: board-range product on a factored engine"};
+            KR_CK(cudaEventRecord(ev[4 + h], st));
+            KR_CK(cudaStreamWaitEvent(T, ev[4 + h], 0));
+            const int64_t h0 = s->boardStart[p][size_t(b[h])], h1 = s->boardStart[p][size_t(b[h + 1])];
+            krb::launch_step(s, p, 1, g + h0 * s->n[p], p, 0.0, 0.0, 0.0, T, true, h0, h1 - h0);
+            if (p == 0) KR_CK(cudaEventRecord(ev[2 + h], T));
+        }
+        krb::engine_account(e, p);
+    }
+    KR_CK(cudaEventRecord(ev[6], T));
+    KR_CK(cudaStreamWaitEvent(st, ev[6], 0));
+}
+
 void capture_iteration(kr_solver* s, bool withCk, double* dck, cudaStream_t st, cudaGraphExec_t& exec,
                        GraphDelta& d) {
     kr_engine* e = s->eng;
+    const bool ov = overlap_ok(s);
+    if (ov) ensure_overlap(s);
     const int64_t f0 = e->flops_total, el0 = e->launches, sl0 = s->launches;
     cudaGraph_t g;
     KR_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -1076,10 +1144,14 @@ void capture_iteration(kr_solver* s, bool withCk, double* dck, cudaStream_t st, 
         krb::launch(krb::k_tick, 1, 1, 0, st, s->d_cnt, 0);
         KR_CK_LAUNCH();
         s->launches++;
-        krb::engine_ax(e, s->x[1], s->g, st);                                    // g1 = A x2
-        krb::launch_step(s, 0, 1, s->g, 0, 0.0, 0.0, 0.0, st, true);             // P1
-        krb::engine_atx(e, s->x[0], s->g, st);                                   // A^T x1
-        krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);             // P2
+        if (ov) {
+            overlapped_iteration(s, st);
+        } else {
+            krb::engine_ax(e, s->x[1], s->g, st);                                // g1 = A x2
+            krb::launch_step(s, 0, 1, s->g, 0, 0.0, 0.0, 0.0, st, true);         // P1
+            krb::engine_atx(e, s->x[0], s->g, st);                               // A^T x1
+            krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);         // P2
+        }
         if (withCk) {
             normalise_averages(s, st, true);                                     // solver.hpp:390-391
             krb::checkpoint_values(s, dck, st, s->d_cnt + 1, 2 * int64_t(s->totalBoards()));

@@ -91,3 +91,25 @@ def test_step_kind_reports_why(monkeypatch):
     k, why = s.step_kind(0)
     assert k == 1 and "two CTAs per SM" in why   # 105 hands: the team kernel pays there
     assert "kr_step" in jit_step_source(p.treeplex(0))
+
+
+@pytest.mark.parametrize("kind", ["implicit", "kfactored"])
+def test_board_half_pipelining_bitwise(turn12, kind, monkeypatch):
+    """The captured iteration with its board halves pipelined (each step
+    beside the other half's product, kr_solver.cu overlapped_iteration)
+    against the serial order (KR_OVERLAP=0): same bits."""
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200.solver import CudaSolver
+
+    def solve(overlap):
+        monkeypatch.setenv("KR_OVERLAP", overlap)
+        insts = [i for i, _ in turn12] if isinstance(turn12[0], tuple) else list(turn12)
+        eng = CudaEngine.kron(insts) if kind == "implicit" else CudaEngine.kfactored(insts)
+        i0 = insts[0]
+        s = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [i.m1 for i in insts], [i.m2 for i in insts], i0.pot)
+        return s.run(DcfrParams(max_iters=30, checkpoint_every=10))  # KR_OVERLAP=1 opts in
+
+    a, b = solve("1"), solve("0")
+    assert bits_equal(a.trace_br1, b.trace_br1) and bits_equal(a.trace_br2, b.trace_br2)
+    assert bits_equal(a.avg1, b.avg1) and bits_equal(a.avg2, b.avg2)
+    assert a.gradient_flops == b.gradient_flops

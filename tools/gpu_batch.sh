@@ -1,4 +1,8 @@
 # ad-hoc GPU batch (edited per call)
 T=r02z
-KR_JIT_HANDS=64 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"kr_step" -s 10 -c 1 -o gpurun_out/${T}_jit_pair -f python tools/solver_probe.py kron 20 > gpurun_out/${T}_ncu_jit.log 2>&1
-tail -1 gpurun_out/${T}_ncu_jit.log
+timeout 900 python -m pytest tests/test_gpu_jit_step.py -q -x -p no:cacheprovider > gpurun_out/${T}_ov_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_ov_pytest.log
+tail -3 gpurun_out/${T}_ov_pytest.log
+for ov in 0 1; do
+  KR_OVERLAP=$ov timeout 300 python tools/solver_probe.py kron 400 2>&1 | sed "s/^/[overlap $ov] /"
+  KR_OVERLAP=$ov timeout 300 python tools/solver_probe.py kfactored 200 2>&1 | sed "s/^/[overlap $ov] /"
+done
