@@ -299,20 +299,32 @@ def config2_gpu(peak):
         sv.run(DcfrParams(max_iters=10, checkpoint_every=10))
         r = sv.run(DcfrParams(max_iters=400, checkpoint_every=50), want_avg=False)
         solver[name] = {"iters_per_s": 400 / r.seconds, "exploitability": r.exploitability}
+    # the headline: the fastest pair whose bits are the factored engine's
+    # (the oracle's, tests/test_gpu_kfengine.py)
+    cands = [("factored", "kr_engine_ax_device + kr_engine_atx_device", us_serial, True),
+             ("factored", "kr_engine_pair_device", us_pair, bitwise),
+             ("kfactored", "kr_engine_ax_device + kr_engine_atx_device", us_kf, kf_bitwise),
+             ("kfactored", "kr_engine_pair_device", us_kf_pair, kf_bitwise)]
+    best = min((c for c in cands if c[3]), key=lambda c: c[2])
     return {"workload": "config2: river Ks7d4c2h9s, 1,081 hands per side, 3-bet tree (n=43), B-post",
             "nnz_stored": int(f.size()), "algorithmic_bytes_per_pair": pair_bytes,
-            "us_per_pair": us_serial, "pairs_per_s": 1e6 / us_serial,
-            "whole_pair_frac_of_peak": pair_bytes / (us_serial / 1e6) / 1e9 / peak,
-            "concurrent_pair": {"api": "kr_engine_pair_device", "us_per_pair": us_pair,
-                                "pairs_per_s": 1e6 / us_pair, "bitwise_equal_to_serial": bitwise},
+            "us_per_pair": best[2], "pairs_per_s": 1e6 / best[2], "engine": best[0], "api": best[1],
+            "bitwise_equal": True,
+            "whole_pair_frac_of_peak": pair_bytes / (best[2] / 1e6) / 1e9 / peak,
+            "frac_note": "algorithmic bytes of the materialised factors (SURVEY 8(d)) over the pair time; the "
+                         "Kronecker-factored engine computes the same products bit for bit without streaming "
+                         "those bytes (an effective rate)" if best[0] == "kfactored" else
+                         "algorithmic bytes over the pair time",
+            "factored": {"us_per_pair": us_serial, "pairs_per_s": 1e6 / us_serial,
+                         "whole_pair_frac_of_peak": pair_bytes / (us_serial / 1e6) / 1e9 / peak,
+                         "concurrent_pair": {"api": "kr_engine_pair_device", "us_per_pair": us_pair,
+                                             "pairs_per_s": 1e6 / us_pair, "bitwise_equal_to_serial": bitwise}},
             "implicit": {"us_per_pair": us_k7, "pairs_per_s": 1e6 / us_k7, "normwise_diff_vs_factored": k7_diff,
                          "tolerance": 1e-12},
             "kfactored": {"api": "kr_engine_create_kfactored", "us_per_pair": us_kf, "pairs_per_s": 1e6 / us_kf,
                           "concurrent_us_per_pair": us_kf_pair, "concurrent_pairs_per_s": 1e6 / us_kf_pair,
                           "bitwise_equal_to_factored": kf_bitwise,
-                          "effective_frac_of_peak": pair_bytes / (min(us_kf, us_kf_pair) / 1e6) / 1e9 / peak,
-                          "note": "algorithmic bytes of the materialised factors over the time of an engine that "
-                                  "streams none of them (same arithmetic, same bits)"},
+                          "effective_frac_of_peak": pair_bytes / (min(us_kf, us_kf_pair) / 1e6) / 1e9 / peak},
             "solver_checkpoint_every_50": solver}
 
 
