@@ -160,9 +160,13 @@ void emit_stats(std::ostringstream& o, const std::string& p, const std::vector<s
     o << "  const bool " << p << "pos = " << p << "best > " << p << "tol;\n";
     o << "  const double " << p << "cut = " << p << "best - " << p << "tol;\n";
     o << "  double " << p << "uni = 0;\n";
+    // 1.0 / ties for ties in 1..cnt: the correctly rounded constants the
+    // division produces (the compiler folds 1.0 / k exactly), no runtime divide
     o << "  if (!" << p << "pos) { int ties_ = 0;";
     for (const auto& v : vals) o << " if (" << v << " >= " << p << "cut) ++ties_;";
-    o << " " << p << "uni = 1.0 / ties_; }\n";
+    o << " " << p << "uni = ties_ == 0 ? __longlong_as_double(0x7ff0000000000000ll) : ";   // 1.0 / 0
+    for (size_t k = 1; k < vals.size(); ++k) o << "ties_ == " << k << " ? 1.0 / " << k << ".0 : ";
+    o << "1.0 / " << vals.size() << ".0; }\n";
 }
 
 std::string prob(const std::string& p, const std::string& v) {
