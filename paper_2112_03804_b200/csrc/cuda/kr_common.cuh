@@ -229,6 +229,11 @@ struct KronState;  // implicit Kronecker engine (kr_kron.cu)
 // Boards [b0, b1) of direction dir (0: A x, 1: Aᵀ y); b1 < 0 = all boards.
 void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0 = 0, int b1 = -1);
 int64_t kron_flops(const kr_engine* e, int dir);
+// Sequence-major (per board [seq][hand]) product and layout conversions of
+// the implicit engine (kr_kron.cu).
+void kron_product_seq(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s);
+void kron_transpose(kr_engine* e, int dir, int side, const double* src, double* dst, bool toSeq, cudaStream_t s);
+bool kron_seq_major();
 int kron_boards(const kr_engine* e);
 void kron_destroy(KronState* k);
 

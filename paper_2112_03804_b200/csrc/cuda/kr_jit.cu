@@ -233,16 +233,17 @@ void emit_reach(std::ostringstream& o, const Levels& L, int v) {
 
 // The kernel source for one player's tree and update rule (mode 1 of
 // k_player_team: sweep, sequence form, discount, average).
-std::string generate(const Levels& L, int rule, int minBlocks, int hands) {
+std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool seq) {
     std::ostringstream o;
     const int N = L.n;
     o << kPreamble;
     o << "#define N " << N << "\n#define HB " << hands << "\n";
-    o << "#define MINB " << minBlocks << "\n";
+    o << "#define MINB " << minBlocks << "\n#define SEQ " << (seq ? 1 : 0) << "\n";
     o << R"(extern "C" __global__ void __launch_bounds__(HB, MINB) kr_step(const double* __restrict__ g, int negate,
     double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
     double shrink, const double* __restrict__ fac, const int* __restrict__ dt, int noAvg,
-    double* __restrict__ rootOut, const double* __restrict__ extra, long long H) {
+    double* __restrict__ rootOut, const double* __restrict__ extra, long long H,
+    const long long* __restrict__ bstart, int nb) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) double G[];  // tile: regrets in, then gradients -> values -> probabilities -> x
@@ -256,15 +257,15 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands) {
   const unsigned bytes = HB * N * 8;
   // whole tiles move by TMA when every tile address is 16-byte aligned (the
   // turn solver's per-continuation blocks start at arbitrary offsets)
-  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (unsigned long long)(g + e0) |
-                                   (unsigned long long)(xout + e0) | (noAvg ? 0ull : (unsigned long long)(avg + e0))) &
-                                  15ull) == 0;
+  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (SEQ ? 0ull : (unsigned long long)(g + e0)) |
+                                   (SEQ ? 0ull : (unsigned long long)(xout + e0)) |
+                                   (noAvg ? 0ull : (unsigned long long)(avg + e0))) & 15ull) == 0;
   if (full) {
     if (lane == 0) {
       bar_init(&bar);
       bar_expect(&bar, bytes);
       g2s(G, regret + e0, bytes, &bar);
-      l2_prefetch(g + e0, bytes);                 // the next tile in, and the averages
+      if (!SEQ) l2_prefetch(g + e0, bytes);       // the next tile in, and the averages
       if (!noAvg) l2_prefetch(avg + e0, bytes);   // streamed at the end, wait in L2
     }
     __syncthreads();
@@ -277,7 +278,22 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands) {
 )";
     for (int i = 0; i < N; ++i) o << "  double r" << i << " = Gh[" << i << "];\n";
     o << R"(  __syncthreads();
-  if (full) {
+  // SEQ: gradients and strategies sequence-major per board (the implicit
+  // engine's coalesced layout, [seq][hand] from the board's first hand
+  // times N): lane h reads and writes its own hand's N values, m apart
+  long long gb = 0, gm = 1;
+  if (SEQ) {
+    if (lane < nh) {
+      const long long hg = h0 + lane;
+      int lo = 0, hi = nb;
+      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (bstart[mid] <= hg) lo = mid; else hi = mid; }
+      gb = bstart[lo] * N + (hg - bstart[lo]);
+      gm = bstart[lo + 1] - bstart[lo];
+#pragma unroll
+      for (int q = 0; q < N; ++q) Gh[q] = g[gb + q * gm];
+    }
+    __syncthreads();
+  } else if (full) {
     if (lane == 0) { fence_async(); bar_expect(&bar, bytes); g2s(G, g + e0, bytes, &bar); }
     __syncthreads();
     bar_wait(&bar, 1);
@@ -304,7 +320,12 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands) {
             o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
     o << R"(  }
   __syncthreads();
-  if (full) {  // x out by TMA while the lanes stream the averages (solver.hpp:382-386)
+  if (SEQ) {
+    if (lane < nh) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) xout[gb + q * gm] = Gh[q];
+    }
+  } else if (full) {  // x out by TMA while the lanes stream the averages (solver.hpp:382-386)
     fence_async();
     __syncthreads();
     if (lane == 0) { s2g(xout + e0, G, bytes); bulk_commit(); }
@@ -423,7 +444,8 @@ std::string generate_pair(const Levels& L, const Split& S, int rule, int minBloc
 extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __restrict__ g, int negate,
     double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
     double shrink, const double* __restrict__ fac, const int* __restrict__ dt, int noAvg,
-    double* __restrict__ rootOut, const double* __restrict__ extra, long long H) {
+    double* __restrict__ rootOut, const double* __restrict__ extra, long long H,
+    const long long* __restrict__ bstart, int nb) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) double G[];  // tile: regrets in, then gradients -> values -> probabilities -> x
@@ -552,11 +574,11 @@ struct Gen {
     size_t smem = 0;              // dynamic shared memory per CTA
 };
 
-Gen jit_source(const Levels& L, int rule, int hands) {
+Gen jit_source(const Levels& L, int rule, int hands, bool seq) {
     Gen r;
     Split S;
     const char* e = std::getenv("KR_JIT_SPLIT");
-    if (e && std::atoi(e) == 1 && split_tree(L, S)) {
+    if (!seq && e && std::atoi(e) == 1 && split_tree(L, S)) {
         const int hb = std::max(32, hands / 2);   // hands per CTA; 2 x hb threads
         r.src = generate_pair(L, S, rule, std::max(1, jit_pair_min_blocks() * 64 / (2 * hb)), hb);
         r.hands = hb;
@@ -564,7 +586,7 @@ Gen jit_source(const Levels& L, int rule, int hands) {
         r.smem = size_t(hb) * size_t(L.n + S.nx) * sizeof(double);
         return r;
     }
-    r.src = generate(L, rule, std::max(1, jit_min_blocks() * 32 / hands), hands);
+    r.src = generate(L, rule, std::max(1, jit_min_blocks() * 32 / hands), hands, seq);
     r.hands = r.threads = hands;
     r.smem = size_t(hands) * size_t(L.n) * sizeof(double);
     return r;
@@ -584,7 +606,7 @@ std::map<std::string, Compiled>& jit_cache() {
 
 }  // namespace
 
-bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why) {
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq) {
     out = JitStep{};
     if (const char* env = std::getenv("KR_STEP"))
         if (std::string(env) != "jit") {
@@ -606,7 +628,7 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         why = "NVRTC not available";
         return false;
     }
-    const Gen gen = jit_source(L, rule, jit_hands());
+    const Gen gen = jit_source(L, rule, jit_hands(), seq);
     const std::string& src = gen.src;
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = jit_cache().find(src);
@@ -643,6 +665,7 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         it = jit_cache().emplace(src, std::move(c)).first;
     }
     out.kern = it->second.kern;
+    out.seq = seq;
     out.n = t.n_seq;
     out.hands = gen.hands;
     out.threads = gen.threads;
@@ -653,7 +676,8 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
 
 void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, int negate, double* regret,
                      double* xout, double* avg, double pos, double neg, double shrink, const double* fac,
-                     const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st) {
+                     const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st,
+                     const int64_t* bstart, int nb) {
     const unsigned grid = unsigned((H + j.hands - 1) / j.hands);
     if (grid == 0) return;
     if (j.smem > 48 * 1024) {
@@ -663,7 +687,8 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
                                               device));
     }
     long long Hl = H;
-    void* args[] = {&g, &negate, &regret, &xout, &avg, &pos, &neg, &shrink, &fac, &dt, &noAvg, &rootOut, &extra, &Hl};
+    void* args[] = {&g,     &negate,  &regret, &xout, &avg, &pos, &neg, &shrink,
+                    &fac,   &dt,      &noAvg,  &rootOut, &extra, &Hl, &bstart, &nb};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(unsigned(j.threads));
@@ -679,10 +704,10 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
     KR_CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(j.kern), args));
 }
 
-std::string jit_step_source(const kr_treeplex& t, int rule) {
+std::string jit_step_source(const kr_treeplex& t, int rule, bool seq) {
     Levels L;
     if (!levels_of(t, L)) return "";
-    return jit_source(L, rule, jit_hands()).src;
+    return jit_source(L, rule, jit_hands(), seq).src;
 }
 
 }  // namespace krb

@@ -16,6 +16,7 @@ struct JitStep {
     int n = 0;
     int hands = 128;   // hands per CTA
     int threads = 128; // threads per CTA (two per hand in the two-group kernels)
+    bool seq = false;  // sequence-major gradients / strategies
     size_t smem = 0;   // one hands x n tile (+ the two-group exchange slots)
     std::string log;   // NVRTC / ptxas log (registers, spills)
 };
@@ -24,15 +25,18 @@ struct JitStep {
 // update rule (KR_RULE_*).  False, with the reason in `why`, when NVRTC is
 // absent, the tree is not level-ordered or too large, or KR_STEP names
 // another kernel.
-bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why);
+// seq: gradients read and strategies written sequence-major per board (the
+// implicit engine's kron_product_seq layout; bstart / nb at launch).
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq = false);
 
 // k_player_team's mode-1 arguments (the sweep, sequence form, discount and
 // average of one player over H hands).
 void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, int negate, double* regret,
                      double* xout, double* avg, double pos, double neg, double shrink, const double* fac,
-                     const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st);
+                     const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st,
+                     const int64_t* bstart = nullptr, int nb = 0);
 
 // The generated source (for inspection and tests).
-std::string jit_step_source(const kr_treeplex& t, int rule);
+std::string jit_step_source(const kr_treeplex& t, int rule, bool seq = false);
 
 }  // namespace krb

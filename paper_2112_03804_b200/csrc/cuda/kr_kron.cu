@@ -567,6 +567,40 @@ bool kron_seq_major() {
     return env ? std::atoi(env) != 0 : kKronSeqDefault;
 }
 
+// The product on sequence-major vectors (per board [seq][hand]) with no
+// transposes: the DCFR solver keeps the strategies and gradients of a K7
+// engine sequence-major (kr_solver.cu, k7seq), so the coalesced kernel runs
+// alone.  Same bits as kron_product (the layout changes only addresses).
+void kron_product_seq(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
+    KronState* k = e->kron;
+    KronDir& d = k->dir[dir];
+    if (d.mO * d.nO == 0) return;
+    const bool wide = int64_t(d.nO) * d.nb <= kSmallGrid;
+    if (wide)
+        krb::launch(k_kron_fused<true, 512>, dim3(unsigned(d.nO), unsigned(d.nb)), 512, k->smem[dir], s, d, 0, in,
+                    out);
+    else
+        krb::launch(k_kron_fused<true, kThreads>, dim3(unsigned(d.nO), unsigned(d.nb)), kThreads, k->smem[dir], s, d,
+                    0, in, out);
+    KR_CK_LAUNCH();
+    e->launches++;
+}
+
+// Hand-major <-> sequence-major per board for direction dir's input side
+// (side 0: the summing hands, n = nS) or output side (side 1: n = nO).
+void kron_transpose(kr_engine* e, int dir, int side, const double* src, double* dst, bool toSeq, cudaStream_t s) {
+    KronState* k = e->kron;
+    KronDir& d = k->dir[dir];
+    const int n = side == 0 ? d.nS : d.nO;
+    const int maxM = side == 0 ? d.maxMS : d.maxMO;
+    if (n == 0 || d.nb == 0) return;
+    const unsigned tiles = unsigned((maxM + 31) / 32) * unsigned((n + 31) / 32);
+    krb::launch(k_board_transpose, dim3(tiles, unsigned(d.nb)), 256, 0, s, src, dst, side == 0 ? d.sumOff : d.outOff, n,
+                0, toSeq ? 1 : 0);
+    KR_CK_LAUNCH();
+    e->launches++;
+}
+
 void kron_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
     KronState* k = e->kron;
     KronDir& d = k->dir[dir];

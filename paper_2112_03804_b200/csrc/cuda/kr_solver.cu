@@ -51,6 +51,13 @@ struct kr_solver {
     // board-half pipelining of the captured iteration (overlap_ok): the
     // steps run on ovSide beside the next half's product; gB holds g2 so the
     // two players' gradients never share a buffer while both are in flight
+    // implicit-engine solves keep x and the gradients sequence-major per
+    // board (k7seq): kron_product_seq runs without transposes and the
+    // compiled step reads / writes that layout (jitSeq)
+    bool k7seq = false;
+    krb::JitStep jitSeq[2];
+    int jitSeqRule[2] = {-1, -1};
+    double* xs[2] = {nullptr, nullptr};
     cudaStream_t ovSide = nullptr;
     cudaEvent_t ovEv[8] = {};
     double* gB = nullptr;
@@ -738,9 +745,40 @@ void jit_prepare(kr_solver* s) {
         if (jit_step_compile(t, s->rule, s->jit[p], s->jitWhy[p])) {
             s->jitRule[p] = s->rule;
             s->jitWhy[p].clear();
+            std::string why;
+            s->jitSeq[p] = JitStep{};
+            s->jitSeqRule[p] = -1;
+            if (s->eng->kron && jit_step_compile(t, s->rule, s->jitSeq[p], why, true)) s->jitSeqRule[p] = s->rule;
         }
     }
 }
+
+// Sequence-major solves on the implicit engine (KR_K7SEQ=0 disables): both
+// players' compiled steps in their sequence-major form, no SelfCheck (it
+// compares hand-major products).
+bool k7seq_ok(const kr_solver* s) {
+    if (const char* env = std::getenv("KR_K7SEQ"))
+        if (std::atoi(env) == 0) return false;
+    return s->eng->kron && !s->eng->scRef && s->jitSeqRule[0] == s->rule && s->jitSeqRule[1] == s->rule &&
+           s->jitSeq[0].kern && s->jitSeq[1].kern;
+}
+
+// x (hand-major, from the initial strategy) -> xs: player 1's x feeds A^T
+// (direction 1's summing side), player 2's feeds A (direction 0's)
+void enter_seq(kr_solver* s, cudaStream_t st) {
+    for (int p = 0; p < 2; ++p) {
+        if (!s->xs[p]) s->xs[p] = dev_alloc<double>(std::max<int64_t>(s->H[p] * s->n[p], 1));
+        kron_transpose(s->eng, p == 0 ? 1 : 0, 0, s->x[p], s->xs[p], true, st);
+    }
+    s->k7seq = true;
+}
+
+void leave_seq(kr_solver* s, cudaStream_t st) {
+    if (!s->k7seq) return;
+    for (int p = 0; p < 2; ++p) kron_transpose(s->eng, p == 0 ? 1 : 0, 0, s->xs[p], s->x[p], false, st);
+    s->k7seq = false;
+}
+
 
 // Player p's step over hands [hoff, hoff + hcnt) (all hands: hcnt < 0); g
 // is the gradient of those hands' rows.
@@ -780,6 +818,29 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
                 regret, x, avg, pos, neg, shrink);
     KR_CK_LAUNCH();
     s->launches++;
+}
+
+// One DCFR iteration's products and steps (solver.hpp:365-388); dev: the
+// scalars from the device tables (graph replay).
+void iteration_body(kr_solver* s, cudaStream_t st, double pos, double neg, double shrink, bool dev) {
+    kr_engine* e = s->eng;
+    if (s->k7seq) {
+        for (int p = 0; p < 2; ++p) {
+            kron_product_seq(e, p, s->xs[1 - p], s->g, st);                     // g1 = A x2, A^T x1
+            engine_account(e, p);
+            jit_step_launch(s->jitSeq[p], s->device, s->H[p], s->g, p, s->regret[p], s->xs[p], s->avg[p], pos, neg,
+                            shrink, dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st,
+                            s->d_bstart[p], s->nboards);
+            s->launches++;
+        }
+        return;
+    }
+    engine_ax(e, s->x[1], s->g, st);                               // g1 = A x2
+    if (!dev) engine_selfcheck(e, 0, s->x[1], s->g, st);
+    launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st, dev);      // P1 sweep/seqform/discount/avg
+    engine_atx(e, s->x[0], s->g, st);                              // A^T x1
+    if (!dev) engine_selfcheck(e, 1, s->x[0], s->g, st);
+    launch_step(s, 1, 1, s->g, 1, pos, neg, shrink, st, dev);      // P2 with g2 = -A^T x1
 }
 
 // Best-response totals of `player` against device strategy `opp`; fills
@@ -863,6 +924,8 @@ void destroy_solver(kr_solver* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     if (s->ovSide) cudaStreamDestroy(s->ovSide);
+    krb::dev_free(s->xs[0]);
+    krb::dev_free(s->xs[1]);
     for (cudaEvent_t ev : s->ovEv)
         if (ev) cudaEventDestroy(ev);
     krb::dev_free(s->gB);
@@ -1147,10 +1210,7 @@ void capture_iteration(kr_solver* s, bool withCk, double* dck, cudaStream_t st, 
         if (ov) {
             overlapped_iteration(s, st);
         } else {
-            krb::engine_ax(e, s->x[1], s->g, st);                                // g1 = A x2
-            krb::launch_step(s, 0, 1, s->g, 0, 0.0, 0.0, 0.0, st, true);         // P1
-            krb::engine_atx(e, s->x[0], s->g, st);                               // A^T x1
-            krb::launch_step(s, 1, 1, s->g, 1, 0.0, 0.0, 0.0, st, true);         // P2
+            krb::iteration_body(s, st, 0.0, 0.0, 0.0, true);
         }
         if (withCk) {
             normalise_averages(s, st, true);                                     // solver.hpp:390-391
@@ -1361,6 +1421,8 @@ int kr_solver_begin(kr_solver* s, double alpha, double beta, double gamma) {
         // x1, x2 = sequenceForm of zero regrets (solver.hpp:363-364)
         krb::launch_step(s, 0, 0, nullptr, 0, 0, 0, 0, st);
         krb::launch_step(s, 1, 0, nullptr, 0, 0, 0, 0, st);
+        s->k7seq = false;
+        if (krb::k7seq_ok(s)) krb::enter_seq(s, st);
         s->alpha = alpha;
         s->beta = beta;
         s->gamma = gamma;
@@ -1377,6 +1439,7 @@ int kr_solver_iterate(kr_solver* s, int n) {
         KR_CK(cudaSetDevice(s->device));
         kr_engine* e = s->eng;
         cudaStream_t st = e->stream;
+        if (s->k7seq && !krb::k7seq_ok(s)) krb::leave_seq(s, st);
         if (n >= 2 && graphs_ok(s)) {  // one captured iteration, replayed n times
             iterate_graph(s, n, st);
             return;
@@ -1385,12 +1448,7 @@ int kr_solver_iterate(kr_solver* s, int n) {
             const int t = ++s->t;  // solver.hpp:365-388
             const double pos = krb::discount_factor(t, s->alpha), neg = krb::discount_factor(t, s->beta);
             const double shrink = std::pow(double(t) / (t + 1), s->gamma);
-            krb::engine_ax(e, s->x[1], s->g, st);                      // g1 = A x2
-            krb::engine_selfcheck(e, 0, s->x[1], s->g, st);
-            krb::launch_step(s, 0, 1, s->g, 0, pos, neg, shrink, st);  // P1 sweep/seqform/discount/avg
-            krb::engine_atx(e, s->x[0], s->g, st);                     // A^T x1
-            krb::engine_selfcheck(e, 1, s->x[0], s->g, st);
-            krb::launch_step(s, 1, 1, s->g, 1, pos, neg, shrink, st);  // P2 with g2 = -A^T x1
+            krb::iteration_body(s, st, pos, neg, shrink, false);
             s->weightSum += 1;
             s->weightSum *= shrink;
         }

@@ -113,3 +113,31 @@ def test_board_half_pipelining_bitwise(turn12, kind, monkeypatch):
     assert bits_equal(a.trace_br1, b.trace_br1) and bits_equal(a.trace_br2, b.trace_br2)
     assert bits_equal(a.avg1, b.avg1) and bits_equal(a.avg2, b.avg2)
     assert a.gradient_flops == b.gradient_flops
+
+
+@pytest.mark.parametrize("preset", ["dcfr", "cfr_plus", "prm_plus"])
+def test_k7_sequence_major_solve_bitwise(turn12, preset, monkeypatch):
+    """Implicit-engine solves keep x and the gradients sequence-major per
+    board (no transposes around the coalesced K7 kernel, the compiled step
+    reads and writes that layout): the same bits as the hand-major solve
+    (KR_K7SEQ=0), through the graph-replayed run and iterate(1) steps."""
+    prm = DcfrParams(max_iters=30, checkpoint_every=10) if preset == "dcfr" else \
+        getattr(DcfrParams, preset)(max_iters=30, checkpoint_every=10)
+
+    def solve(seq, incremental):
+        monkeypatch.setenv("KR_K7SEQ", seq)
+        s = solver_for(turn12, implicit=True)
+        if incremental:
+            s.begin(prm)
+            for _ in range(12):
+                s.iterate(1)
+            s.iterate(5)
+            return s.checkpoint(), s.averages()
+        r = s.run(prm)
+        return (r.trace_br1, r.trace_br2), (r.avg1, r.avg2)
+
+    for incremental in (False, True):
+        (b1, b2), (a1, a2) = solve("1", incremental)
+        (c1, c2), (d1, d2) = solve("0", incremental)
+        assert bits_equal(b1, c1) and bits_equal(b2, c2), incremental
+        assert bits_equal(a1, d1) and bits_equal(a2, d2), incremental
