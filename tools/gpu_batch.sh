@@ -1,5 +1,4 @@
 # ad-hoc GPU batch (edited per call)
 T=r02z
-timeout 900 python -m pytest tests/test_gpu_jit_step.py -q -x -p no:cacheprovider > gpurun_out/${T}_seq_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_seq_pytest.log
-tail -15 gpurun_out/${T}_seq_pytest.log
-for v in 0 1; do KR_K7SEQ=$v timeout 300 python tools/solver_probe.py kron 400 2>&1 | sed "s/^/[k7seq $v] /"; done
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"kr_step" -s 10 -c 1 -o gpurun_out/${T}_jit_seq -f python tools/solver_probe.py kron 20 > gpurun_out/${T}_ncu_jit.log 2>&1
+tail -1 gpurun_out/${T}_ncu_jit.log
