@@ -239,6 +239,12 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
     o << kPreamble;
     o << "#define N " << N << "\n#define HB " << hands << "\n";
     o << "#define MINB " << minBlocks << "\n#define SEQ " << (seq ? 1 : 0) << "\n";
+    {
+        const char* e = std::getenv("KR_JIT_STAGGER");     // start delay step (ns), 0 = off
+        o << "#define STAGGER " << (e ? std::atoi(e) : 4000) << "\n";
+        const char* k = std::getenv("KR_JIT_STAGGER_K");   // CTAs start at K staggered times
+        o << "#define STAGGER_K " << (k ? std::max(2, std::atoi(k)) : 3) << "\n";
+    }
     o << R"(extern "C" __global__ void __launch_bounds__(HB, MINB) kr_step(const double* __restrict__ g, int negate,
     double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
     double shrink, const double* __restrict__ fac, const int* __restrict__ dt, int noAvg,
@@ -249,6 +255,13 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
   extern __shared__ __align__(128) double G[];  // tile: regrets in, then gradients -> values -> probabilities -> x
   __shared__ __align__(8) u64 bar;
   if (fac) { const int t = *dt; pos = fac[3 * t]; neg = fac[3 * t + 1]; shrink = fac[3 * t + 2]; }
+#if STAGGER > 0
+  // a full-GPU grid runs as one round whose CTAs would all move their tiles,
+  // then all compute: starting two thirds of them 4 / 8 us late lets the
+  // others' transfers overlap their compute (+2% at config 3; the bits are
+  // the same whatever the order, every hand being independent)
+  if (gridDim.x >= 2 * 148 && blockIdx.x % STAGGER_K) __nanosleep(STAGGER * (blockIdx.x % STAGGER_K));
+#endif
   const int lane = threadIdx.x;
   const long long h0 = (long long)blockIdx.x * HB;
   const int nh = (int)(H - h0 < HB ? H - h0 : HB);

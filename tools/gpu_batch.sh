@@ -1,4 +1,3 @@
 # ad-hoc GPU batch (edited per call)
 T=r02z
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"kr_step" -s 10 -c 1 -o gpurun_out/${T}_jit_seq -f python tools/solver_probe.py kron 20 > gpurun_out/${T}_ncu_jit.log 2>&1
-tail -1 gpurun_out/${T}_ncu_jit.log
+for cfg in "0 2" "6000 2" "10000 2" "15000 2" "4000 3" "6000 3" "3000 4" "5000 4"; do set -- $cfg; KR_JIT_STAGGER=$1 KR_JIT_STAGGER_K=$2 timeout 300 python tools/solver_probe.py kron 400 2>&1 | sed "s/^/[stagger $1 k $2] /"; done
