@@ -1,3 +1,4 @@
 # ad-hoc GPU batch (edited per call)
 T=r02z
-for cfg in "0 2" "6000 2" "10000 2" "15000 2" "4000 3" "6000 3" "3000 4" "5000 4"; do set -- $cfg; KR_JIT_STAGGER=$1 KR_JIT_STAGGER_K=$2 timeout 300 python tools/solver_probe.py kron 400 2>&1 | sed "s/^/[stagger $1 k $2] /"; done
+for t in 32 64 128 32; do KR_KF_TILE=$t timeout 600 python tools/kf_probe.py 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('tile $t', d['kf_ax_us'], d['kf_atx_us'], d['kf_pair_us'], d['bitwise_vs_device_built'])"; done
+KR_KF_TILE=64 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_kf_seqmajor -c 4 --csv python tools/kf_probe.py 2>/dev/null | grep gpu__time | awk -F'","' '{print $NF}' | head -4
