@@ -595,6 +595,7 @@ def run_product(args):
     res = drv.run(max_iters=args.solver_iters, checkpoint_every=50)
     torch.cuda.synchronize(dev)
     solver_s = max_over_ranks(time.perf_counter() - ts)
+    factored_steps = step_kinds(solver)
 
     # ---- Kronecker-factored engine (bitwise, nothing streamed) -------------
     kfac = run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, coll_dev, barrier,
@@ -648,7 +649,7 @@ def run_product(args):
         "e2e": dict(e2e, matches_device_path=check_ok),
         "solver_iters_per_s": args.solver_iters / solver_s,
         "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"],
-                   "checkpoint_every": 50},
+                   "checkpoint_every": 50, "player_step": factored_steps},
         "gpu_launches": gpu_launches,
         "multi_gpu": {"ranks": world, "boards_per_rank": [int(v) for v in bpr],
                       "transport": ("libkrcuda kr_comm (NCCL): checkpoint values and turn values all-gathered "
@@ -744,6 +745,16 @@ def e2e_host_pairs(eng, x, y, barrier, max_over_ranks, steps, ring=4):
     return res
 
 
+def step_kinds(solver):
+    """Which kernel ran each player's step (kr_solver_step_kind)."""
+    names = {2: "compiled for the treeplex (NVRTC, kr_jit.cu)", 1: "generic team kernel", 0: "generic per-hand kernel"}
+    out = {}
+    for p in (0, 1):
+        k, why = solver.step_kind(p)
+        out[f"player{p + 1}"] = names.get(k, "?") + (f" ({why})" if why and k != 2 else "")
+    return out
+
+
 def run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, coll_dev, barrier, max_over_ranks,
                   sum_over_ranks, ref_solve, comm=None, bpr=None):
     """The same pairs through the Kronecker-factored engine (Technique B post
@@ -814,7 +825,7 @@ def run_kfactored(args, boards, eng, x, y, ax, atx, dev, local, rank, world, col
            "create_s": round(create_s, 3), "e2e": e2e,
            "solver_iters_per_s": args.solver_iters / solver_s,
            "solver": {"iterations": r["iterations"], "exploitability": r["exploitability"],
-                      "trace_bitwise_equal_to_factored_solve": same_trace}}
+                      "trace_bitwise_equal_to_factored_solve": same_trace, "player_step": step_kinds(solver)}}
     solver.close()
     ek.close()
     return out
@@ -956,7 +967,10 @@ def run_implicit(args, boards, eng, x, y, ax, dev, local, rank, world, coll_dev,
            "gpu_launches": launches, "normwise_diff_vs_factored": dif, "tolerance": 1e-12,
            "e2e": e2e,
            "solver_iters_per_s": args.solver_iters / solver_s,
-           "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"]}}
+           "solver": {"iterations": res["iterations"], "exploitability": res["exploitability"],
+                      "player_step": step_kinds(solver),
+                      "layout": "sequence-major x and gradients (kron_product_seq)" if os.environ.get("KR_K7SEQ") != "0"
+                                else "hand-major"}}
     solver.close()
     ek.close()
     return out
