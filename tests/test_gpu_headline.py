@@ -96,6 +96,9 @@ def test_config3_dcfr_trace_bitwise_per_board(config3, kind):
     i0 = boards[0][0]
     eng = CudaEngine([f for _, f in boards]) if kind == "factored" else CudaEngine.kfactored([i for i, _ in boards])
     s = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [i.m1 for i, _ in boards], [i.m2 for i, _ in boards], i0.pot)
+    # the player step runs compiled for the treeplex here (kr_jit.cu); the
+    # per-board comparison below is against the oracle's own walk
+    assert s.step_kind(0)[0] == 2 and s.step_kind(1)[0] == 2, (s.step_kind(0), s.step_kind(1))
     r = s.run(DcfrParams(max_iters=100, checkpoint_every=50))
     assert r.iterations == 100 and len(r.trace_iter) == 2
 
