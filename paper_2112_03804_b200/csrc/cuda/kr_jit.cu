@@ -240,8 +240,6 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
     o << "#define N " << N << "\n#define HB " << hands << "\n";
     o << "#define MINB " << minBlocks << "\n#define SEQ " << (seq ? 1 : 0) << "\n";
     {
-        const char* e = std::getenv("KR_JIT_STAGGER");     // start delay step (ns), 0 = off
-        o << "#define STAGGER " << (e ? std::atoi(e) : 4000) << "\n";
         const char* k = std::getenv("KR_JIT_STAGGER_K");   // CTAs start at K staggered times
         o << "#define STAGGER_K " << (k ? std::max(2, std::atoi(k)) : 3) << "\n";
     }
@@ -249,19 +247,19 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
     double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
     double shrink, const double* __restrict__ fac, const int* __restrict__ dt, int noAvg,
     double* __restrict__ rootOut, const double* __restrict__ extra, long long H,
-    const long long* __restrict__ bstart, int nb) {
+    const long long* __restrict__ bstart, int nb, int stagger) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) double G[];  // tile: regrets in, then gradients -> values -> probabilities -> x
   __shared__ __align__(8) u64 bar;
   if (fac) { const int t = *dt; pos = fac[3 * t]; neg = fac[3 * t + 1]; shrink = fac[3 * t + 2]; }
-#if STAGGER > 0
-  // a full-GPU grid runs as one round whose CTAs would all move their tiles,
-  // then all compute: starting two thirds of them 4 / 8 us late lets the
-  // others' transfers overlap their compute (+2% at config 3; the bits are
-  // the same whatever the order, every hand being independent)
-  if (gridDim.x >= 2 * 148 && blockIdx.x % STAGGER_K) __nanosleep(STAGGER * (blockIdx.x % STAGGER_K));
-#endif
+  // stagger (ns): a full-GPU grid runs as one round whose CTAs would all
+  // move their tiles, then all compute; starting two thirds of them stagger /
+  // 2 x stagger late lets the others' transfers overlap their compute (+2% at
+  // config 3; the bits are the same whatever the order, every hand being
+  // independent).  0 where other kernels share the GPU (turn continuations).
+  if (stagger > 0 && gridDim.x >= 2 * 148 && blockIdx.x % STAGGER_K)
+    __nanosleep(unsigned(stagger) * (blockIdx.x % STAGGER_K));
   const int lane = threadIdx.x;
   const long long h0 = (long long)blockIdx.x * HB;
   const int nh = (int)(H - h0 < HB ? H - h0 : HB);
@@ -458,7 +456,7 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
     double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
     double shrink, const double* __restrict__ fac, const int* __restrict__ dt, int noAvg,
     double* __restrict__ rootOut, const double* __restrict__ extra, long long H,
-    const long long* __restrict__ bstart, int nb) {
+    const long long* __restrict__ bstart, int nb, int stagger) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) double G[];  // tile: regrets in, then gradients -> values -> probabilities -> x
@@ -687,10 +685,15 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
     return true;
 }
 
+int jit_stagger_ns() {
+    if (const char* e = std::getenv("KR_JIT_STAGGER")) return std::max(0, std::atoi(e));
+    return 4000;
+}
+
 void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, int negate, double* regret,
                      double* xout, double* avg, double pos, double neg, double shrink, const double* fac,
                      const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st,
-                     const int64_t* bstart, int nb) {
+                     const int64_t* bstart, int nb, int stagger) {
     const unsigned grid = unsigned((H + j.hands - 1) / j.hands);
     if (grid == 0) return;
     if (j.smem > 48 * 1024) {
@@ -700,8 +703,8 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
                                               device));
     }
     long long Hl = H;
-    void* args[] = {&g,     &negate,  &regret, &xout, &avg, &pos, &neg, &shrink,
-                    &fac,   &dt,      &noAvg,  &rootOut, &extra, &Hl, &bstart, &nb};
+    void* args[] = {&g,   &negate, &regret,  &xout,  &avg, &pos,    &neg, &shrink, &fac,
+                    &dt,  &noAvg,  &rootOut, &extra, &Hl,  &bstart, &nb,  &stagger};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(unsigned(j.threads));

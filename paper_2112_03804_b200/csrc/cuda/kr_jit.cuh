@@ -34,7 +34,10 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
 void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, int negate, double* regret,
                      double* xout, double* avg, double pos, double neg, double shrink, const double* fac,
                      const int* dt, int noAvg, double* rootOut, const double* extra, cudaStream_t st,
-                     const int64_t* bstart = nullptr, int nb = 0);
+                     const int64_t* bstart = nullptr, int nb = 0, int stagger = 0);
+
+// Start stagger (ns) of the DCFR solver's full-GPU step grids (KR_JIT_STAGGER).
+int jit_stagger_ns();
 
 // The generated source (for inspection and tests).
 std::string jit_step_source(const kr_treeplex& t, int rule, bool seq = false);

@@ -789,7 +789,8 @@ void launch_step(kr_solver* s, int p, int mode, const double* g, int negate, dou
     double *regret = s->regret[p] + o, *x = s->x[p] + o, *avg = s->avg[p] + o;
     if (mode == 1 && s->jit[p].kern && s->jitRule[p] == s->rule) {
         jit_step_launch(s->jit[p], s->device, H, g, negate, regret, x, avg, pos, neg, shrink,
-                        dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st);
+                        dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st, nullptr, 0,
+                        hcnt < 0 ? jit_stagger_ns() : 0);
         s->launches++;
         return;
     }
@@ -830,7 +831,7 @@ void iteration_body(kr_solver* s, cudaStream_t st, double pos, double neg, doubl
             engine_account(e, p);
             jit_step_launch(s->jitSeq[p], s->device, s->H[p], s->g, p, s->regret[p], s->xs[p], s->avg[p], pos, neg,
                             shrink, dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st,
-                            s->d_bstart[p], s->nboards);
+                            s->d_bstart[p], s->nboards, jit_stagger_ns());
             s->launches++;
         }
         return;
