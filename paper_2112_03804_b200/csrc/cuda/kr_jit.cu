@@ -398,22 +398,25 @@ int jit_min_blocks() {
 // group 0 through shared memory; group 0 hands the root sequences' reach back.
 // Returns false when the tree has no level-1 node to give group 1.
 struct Split {
-    std::vector<int> grp;     // per node: 0 or 1
-    std::vector<int> slot;    // per node: exchange slot (group-1 level-1 nodes), else -1
+    int groups = 1;
+    std::vector<int> grp;     // per node: its group
+    std::vector<int> slot;    // per node: exchange slot (level-1 nodes of groups > 0), else -1
     int nx = 0;
 };
 
-bool split_tree(const Levels& L, Split& S) {
-    if (L.nlev < 2) return false;
+// Up to `want` groups: the level-1 subtrees dealt greedily (heaviest first,
+// by action count) to the lightest group, group 0 also holding the roots.
+bool split_tree(const Levels& L, Split& S, int want = 2) {
+    if (L.nlev < 2 || want < 2) return false;
     std::vector<int> owner(size_t(L.n) + 1, -1);
     for (int v = 0; v < L.nn; ++v)
         for (int a = L.aptr[size_t(v)]; a < L.aptr[size_t(v) + 1]; ++a) owner[size_t(L.aseq[size_t(a)])] = v;
     std::vector<int> sub(size_t(L.nn), -1), weight(size_t(L.nn), 0);
-    int w0 = 0;
+    std::vector<int> w(size_t(want), 0);
     for (int v = 0; v < L.nn; ++v) {
         const int acts = L.aptr[size_t(v) + 1] - L.aptr[size_t(v)];
         if (L.lev[size_t(v)] == 0) {
-            w0 += acts;
+            w[0] += acts;
             continue;
         }
         int u = v;
@@ -422,26 +425,30 @@ bool split_tree(const Levels& L, Split& S) {
         weight[size_t(u)] += acts;
     }
     std::vector<int> roots(L.levNodes[1]);
-    std::sort(roots.begin(), roots.end(), [&](int a, int b) {
-        return weight[size_t(a)] != weight[size_t(b)] ? weight[size_t(a)] > weight[size_t(b)] : a < b;
+    std::sort(roots.begin(), roots.end(), [&](int x, int y) {
+        return weight[size_t(x)] != weight[size_t(y)] ? weight[size_t(x)] > weight[size_t(y)] : x < y;
     });
     std::vector<int> rootGrp(size_t(L.nn), 0);
-    int w1 = 0;
     for (int u : roots) {
-        if (w1 <= w0) {
-            rootGrp[size_t(u)] = 1;
-            w1 += weight[size_t(u)];
-        } else {
-            w0 += weight[size_t(u)];
-        }
+        int best = 0;   // the lightest group, preferring groups other than 0 on ties
+        for (int q = 1; q < want; ++q)
+            if (w[size_t(q)] <= w[size_t(best)]) best = q;
+        rootGrp[size_t(u)] = best;
+        w[size_t(best)] += weight[size_t(u)];
     }
-    if (w1 == 0) return false;
+    int used = 1;
+    for (int q = 1; q < want; ++q)
+        if (w[size_t(q)] > 0) used = q + 1;
+    if (used < 2) return false;
+    for (int q = 1; q < used; ++q)
+        if (w[size_t(q)] == 0) return false;   // keep the groups contiguous
+    S.groups = used;
     S.grp.assign(size_t(L.nn), 0);
     S.slot.assign(size_t(L.nn), -1);
     for (int v = 0; v < L.nn; ++v)
         if (L.lev[size_t(v)] > 0) S.grp[size_t(v)] = rootGrp[size_t(sub[size_t(v)])];
     for (int v : L.levNodes[1])
-        if (S.grp[size_t(v)] == 1) S.slot[size_t(v)] = S.nx++;
+        if (S.grp[size_t(v)] > 0) S.slot[size_t(v)] = S.nx++;
     return true;
 }
 
@@ -449,7 +456,8 @@ std::string generate_pair(const Levels& L, const Split& S, int rule, int minBloc
     std::ostringstream o;
     const int N = L.n;
     o << kPreamble;
-    o << "#define N " << N << "\n#define HB " << hands << "\n#define NT (2 * HB)\n#define NX " << S.nx << "\n";
+    o << "#define N " << N << "\n#define HB " << hands << "\n#define NT (" << S.groups << " * HB)\n#define NX "
+      << std::max(S.nx, 1) << "\n";
     o << "#define MINB " << minBlocks << "\n";
     o << R"(__device__ __forceinline__ void bar_all() { asm volatile("barrier.sync 1, %0;" :: "n"(NT) : "memory"); }
 extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __restrict__ g, int negate,
@@ -525,13 +533,13 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
     for (int q = tid; q < ne; q += NT) regret[e0 + q] = G[q];
   }
 )";
-    for (int gi = 0; gi < 2; ++gi) {
+    for (int gi = 0; gi < S.groups; ++gi) {
         std::vector<int> mine;   // sequences of this group's nodes
         for (int v = 0; v < L.nn; ++v)
             if (S.grp[size_t(v)] == gi)
                 for (int a = L.aptr[size_t(v)]; a < L.aptr[size_t(v) + 1]; ++a) mine.push_back(L.aseq[size_t(a)]);
         std::sort(mine.begin(), mine.end());
-        o << (gi == 0 ? "  if (grp == 0) {\n" : "  } else {\n");
+        o << (gi == 0 ? "  if (grp == 0) {\n" : "  } else if (grp == " + std::to_string(gi) + ") {\n");
         for (int sq : mine) o << "  double " << reg(sq) << " = " << val(sq) << ";\n";
         for (int v = 0; v < L.nn; ++v)
             if (S.grp[size_t(v)] == gi) o << "  double nv" << v << " = 0.0;\n";
@@ -541,16 +549,16 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
         for (int l = L.nlev - 1; l >= 1; --l)
             for (int v : L.levNodes[size_t(l)])
                 if (S.grp[size_t(v)] == gi) emit_node(o, L, v, rule, [](int c) { return "nv" + std::to_string(c); });
-        if (gi == 1)
+        if (gi > 0)
             for (int v : L.levNodes[1])
-                if (S.grp[size_t(v)] == 1) o << "  Xh[" << S.slot[size_t(v)] << "] = nv" << v << ";\n";
+                if (S.grp[size_t(v)] == gi) o << "  Xh[" << S.slot[size_t(v)] << "] = nv" << v << ";\n";
         o << "  }\n  bar_all();\n";   // B: group 1's subtree values are in X
         if (gi == 0) {
             o << "  if (valid) {\n";
             for (int v : L.levNodes[0])
                 emit_node(o, L, v, rule, [&](int c) {
-                    return S.grp[size_t(c)] == 1 ? "Xh[" + std::to_string(S.slot[size_t(c)]) + "]"
-                                                 : "nv" + std::to_string(c);
+                    return S.grp[size_t(c)] > 0 ? "Xh[" + std::to_string(S.slot[size_t(c)]) + "]"
+                                                : "nv" + std::to_string(c);
                 });
             o << "  if (rootOut) { double acc = 0.0;";
             for (auto it = L.levNodes[0].rbegin(); it != L.levNodes[0].rend(); ++it) o << " acc += nv" << *it << ";";
@@ -585,10 +593,21 @@ struct Gen {
     size_t smem = 0;              // dynamic shared memory per CTA
 };
 
-Gen jit_source(const Levels& L, int rule, int hands, bool seq) {
+// groups > 1: the hand set's tree split over that many warp groups (small
+// grids: single boards, where one thread per hand leaves most SMs idle), 32
+// hands per CTA; empty source when the tree does not split that way.
+Gen jit_source(const Levels& L, int rule, int hands, bool seq, int groups) {
     Gen r;
     Split S;
     const char* e = std::getenv("KR_JIT_SPLIT");
+    if (groups > 1) {
+        if (seq || !split_tree(L, S, groups)) return r;
+        r.src = generate_pair(L, S, rule, 1, 32);
+        r.hands = 32;
+        r.threads = 32 * S.groups;
+        r.smem = size_t(32) * size_t(L.n + std::max(S.nx, 1)) * sizeof(double);
+        return r;
+    }
     if (!seq && e && std::atoi(e) == 1 && split_tree(L, S)) {
         const int hb = std::max(32, hands / 2);   // hands per CTA; 2 x hb threads
         r.src = generate_pair(L, S, rule, std::max(1, jit_pair_min_blocks() * 64 / (2 * hb)), hb);
@@ -617,7 +636,7 @@ std::map<std::string, Compiled>& jit_cache() {
 
 }  // namespace
 
-bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq) {
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq, int groups) {
     out = JitStep{};
     if (const char* env = std::getenv("KR_STEP"))
         if (std::string(env) != "jit") {
@@ -639,8 +658,12 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         why = "NVRTC not available";
         return false;
     }
-    const Gen gen = jit_source(L, rule, jit_hands(), seq);
+    const Gen gen = jit_source(L, rule, jit_hands(), seq, groups);
     const std::string& src = gen.src;
+    if (src.empty()) {
+        why = "treeplex does not split into " + std::to_string(groups) + " warp groups";
+        return false;
+    }
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = jit_cache().find(src);
     if (it == jit_cache().end()) {
@@ -720,10 +743,10 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
     KR_CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(j.kern), args));
 }
 
-std::string jit_step_source(const kr_treeplex& t, int rule, bool seq) {
+std::string jit_step_source(const kr_treeplex& t, int rule, bool seq, int groups) {
     Levels L;
     if (!levels_of(t, L)) return "";
-    return jit_source(L, rule, jit_hands(), seq).src;
+    return jit_source(L, rule, jit_hands(), seq, groups).src;
 }
 
 }  // namespace krb

@@ -27,7 +27,10 @@ struct JitStep {
 // another kernel.
 // seq: gradients read and strategies written sequence-major per board (the
 // implicit engine's kron_product_seq layout; bstart / nb at launch).
-bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq = false);
+// groups > 1: the tree split over that many warp groups per 32-hand set (for
+// grids too small to fill the GPU with one thread per hand).
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq = false,
+                      int groups = 1);
 
 // k_player_team's mode-1 arguments (the sweep, sequence form, discount and
 // average of one player over H hands).
@@ -40,6 +43,6 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
 int jit_stagger_ns();
 
 // The generated source (for inspection and tests).
-std::string jit_step_source(const kr_treeplex& t, int rule, bool seq = false);
+std::string jit_step_source(const kr_treeplex& t, int rule, bool seq = false, int groups = 1);
 
 }  // namespace krb

@@ -732,23 +732,32 @@ void jit_prepare(kr_solver* s) {
         if (!s->levelled[p] || s->jitRule[p] == s->rule) continue;
         s->jit[p] = JitStep{};
         s->jitRule[p] = -1;
-        if (!force && s->H[p] < int64_t(2) * 148 * kJitHands) {
-            s->jitWhy[p] = "grid below two CTAs per SM";
-            continue;
-        }
         kr_treeplex t{};
         t.n_nodes = s->nnodes[p];
         t.n_seq = s->n[p];
         t.node_parent_seq = s->tPar[p].data();
         t.node_action_ptr = s->tPtr[p].data();
         t.action_seq = s->tSeq[p].data();
-        if (jit_step_compile(t, s->rule, s->jit[p], s->jitWhy[p])) {
+        // below two one-thread-per-hand CTAs per SM (single boards): the tree
+        // split over warp groups (KR_JIT_GROUPS, 0 = the team kernel there)
+        const bool small = !force && s->H[p] < int64_t(2) * 148 * kJitHands;
+        int groups = 1;
+        if (small) {
+            const char* ge = std::getenv("KR_JIT_GROUPS");
+            groups = ge ? std::atoi(ge) : 4;
+            if (groups < 2) {
+                s->jitWhy[p] = "grid below two CTAs per SM";
+                continue;
+            }
+        }
+        if (jit_step_compile(t, s->rule, s->jit[p], s->jitWhy[p], false, groups)) {
             s->jitRule[p] = s->rule;
             s->jitWhy[p].clear();
             std::string why;
             s->jitSeq[p] = JitStep{};
             s->jitSeqRule[p] = -1;
-            if (s->eng->kron && jit_step_compile(t, s->rule, s->jitSeq[p], why, true)) s->jitSeqRule[p] = s->rule;
+            if (!small && s->eng->kron && jit_step_compile(t, s->rule, s->jitSeq[p], why, true))
+                s->jitSeqRule[p] = s->rule;
         }
     }
 }
@@ -1392,7 +1401,8 @@ int kr_solver_set_rule(kr_solver* s, int rule) {
 
 int64_t kr_jit_step_source(const kr_treeplex* t, int rule, char* buf, int64_t cap) {
     if (!t) return -1;
-    const std::string src = krb::jit_step_source(*t, rule);
+    const char* ge = std::getenv("KR_JIT_SOURCE_GROUPS");   // inspect the warp-group form
+    const std::string src = krb::jit_step_source(*t, rule, false, ge ? std::atoi(ge) : 1);
     if (src.empty()) return -1;
     if (buf && cap > 0) {
         const size_t n = std::min(src.size(), size_t(cap - 1));

@@ -87,9 +87,13 @@ def test_step_kind_reports_why(monkeypatch):
     k, why = s.step_kind(0)
     assert k == 1 and why   # the team kernel, with the reason
     monkeypatch.delenv("KR_STEP")
+    monkeypatch.setenv("KR_JIT_GROUPS", "0")
     s = solver_for([(p, p.sparsify("b", True))])
     k, why = s.step_kind(0)
-    assert k == 1 and "two CTAs per SM" in why   # 105 hands: the team kernel pays there
+    assert k == 1 and "two CTAs per SM" in why   # 105 hands, warp groups off: the team kernel
+    monkeypatch.delenv("KR_JIT_GROUPS")
+    s = solver_for([(p, p.sparsify("b", True))])
+    assert s.step_kind(0)[0] == 2                # the tree split over warp groups
     assert "kr_step" in jit_step_source(p.treeplex(0))
 
 
