@@ -246,6 +246,11 @@ int comm_device(const kr_comm* c);
 struct KfState;  // Kronecker-factored engine (kr_kfengine.cu)
 void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0 = 0, int b1 = -1);
 void kf_destroy(KfState* k);
+// The Kronecker-factored products on an input already in the engine's
+// staging layout (sequence-major over all of the direction's hands), and the
+// conversion into that layout.
+void kf_product_staged(kr_engine* e, int dir, const double* inT, double* out, cudaStream_t s);
+void kf_stage_all(kr_engine* e, int dir, const double* in, double* inT, cudaStream_t s);
 
 }  // namespace krb
 

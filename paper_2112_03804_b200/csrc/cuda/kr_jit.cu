@@ -233,12 +233,16 @@ void emit_reach(std::ostringstream& o, const Levels& L, int v) {
 
 // The kernel source for one player's tree and update rule (mode 1 of
 // k_player_team: sweep, sequence form, discount, average).
-std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool seq) {
+// layout: 0 hand-major; 1 gradients and strategies sequence-major per board
+// (implicit engine); 2 strategies sequence-major over all hands (Kronecker-
+// factored engine), gradients hand-major.
+std::string generate(const Levels& L, int rule, int minBlocks, int hands, int layout) {
     std::ostringstream o;
     const int N = L.n;
     o << kPreamble;
     o << "#define N " << N << "\n#define HB " << hands << "\n";
-    o << "#define MINB " << minBlocks << "\n#define SEQ " << (seq ? 1 : 0) << "\n";
+    o << "#define MINB " << minBlocks << "\n#define GSEQ " << (layout == 1 ? 1 : 0) << "\n#define XSEQ " << layout
+      << "\n";
     {
         const char* k = std::getenv("KR_JIT_STAGGER_K");   // CTAs start at K staggered times
         o << "#define STAGGER_K " << (k ? std::max(2, std::atoi(k)) : 3) << "\n";
@@ -268,15 +272,15 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
   const unsigned bytes = HB * N * 8;
   // whole tiles move by TMA when every tile address is 16-byte aligned (the
   // turn solver's per-continuation blocks start at arbitrary offsets)
-  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (SEQ ? 0ull : (unsigned long long)(g + e0)) |
-                                   (SEQ ? 0ull : (unsigned long long)(xout + e0)) |
+  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (GSEQ ? 0ull : (unsigned long long)(g + e0)) |
+                                   (XSEQ ? 0ull : (unsigned long long)(xout + e0)) |
                                    (noAvg ? 0ull : (unsigned long long)(avg + e0))) & 15ull) == 0;
   if (full) {
     if (lane == 0) {
       bar_init(&bar);
       bar_expect(&bar, bytes);
       g2s(G, regret + e0, bytes, &bar);
-      if (!SEQ) l2_prefetch(g + e0, bytes);       // the next tile in, and the averages
+      if (!GSEQ) l2_prefetch(g + e0, bytes);      // the next tile in, and the averages
       if (!noAvg) l2_prefetch(avg + e0, bytes);   // streamed at the end, wait in L2
     }
     __syncthreads();
@@ -289,17 +293,22 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
 )";
     for (int i = 0; i < N; ++i) o << "  double r" << i << " = Gh[" << i << "];\n";
     o << R"(  __syncthreads();
-  // SEQ: gradients and strategies sequence-major per board (the implicit
-  // engine's coalesced layout, [seq][hand] from the board's first hand
-  // times N): lane h reads and writes its own hand's N values, m apart
+  // GSEQ / XSEQ == 1: gradients / strategies sequence-major per board (the
+  // implicit engine's coalesced layout, [seq][hand] from the board's first
+  // hand times N): lane h reads / writes its own hand's N values, m apart.
+  // XSEQ == 2: strategies sequence-major over all hands, [seq][hand] (the
+  // Kronecker-factored engine's staging layout), H apart.
   long long gb = 0, gm = 1;
-  if (SEQ) {
+  if ((GSEQ || XSEQ == 1) && lane < nh) {
+    const long long hg = h0 + lane;
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (bstart[mid] <= hg) lo = mid; else hi = mid; }
+    gb = bstart[lo] * N + (hg - bstart[lo]);
+    gm = bstart[lo + 1] - bstart[lo];
+  }
+  if (XSEQ == 2) { gb = h0 + lane; gm = H; }
+  if (GSEQ) {
     if (lane < nh) {
-      const long long hg = h0 + lane;
-      int lo = 0, hi = nb;
-      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (bstart[mid] <= hg) lo = mid; else hi = mid; }
-      gb = bstart[lo] * N + (hg - bstart[lo]);
-      gm = bstart[lo + 1] - bstart[lo];
 #pragma unroll
       for (int q = 0; q < N; ++q) Gh[q] = g[gb + q * gm];
     }
@@ -331,7 +340,7 @@ std::string generate(const Levels& L, int rule, int minBlocks, int hands, bool s
             o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
     o << R"(  }
   __syncthreads();
-  if (SEQ) {
+  if (XSEQ) {
     if (lane < nh) {
 #pragma unroll
       for (int q = 0; q < N; ++q) xout[gb + q * gm] = Gh[q];
@@ -596,19 +605,19 @@ struct Gen {
 // groups > 1: the hand set's tree split over that many warp groups (small
 // grids: single boards, where one thread per hand leaves most SMs idle), 32
 // hands per CTA; empty source when the tree does not split that way.
-Gen jit_source(const Levels& L, int rule, int hands, bool seq, int groups) {
+Gen jit_source(const Levels& L, int rule, int hands, int layout, int groups) {
     Gen r;
     Split S;
     const char* e = std::getenv("KR_JIT_SPLIT");
     if (groups > 1) {
-        if (seq || !split_tree(L, S, groups)) return r;
+        if (layout || !split_tree(L, S, groups)) return r;
         r.src = generate_pair(L, S, rule, 1, 32);
         r.hands = 32;
         r.threads = 32 * S.groups;
         r.smem = size_t(32) * size_t(L.n + std::max(S.nx, 1)) * sizeof(double);
         return r;
     }
-    if (!seq && e && std::atoi(e) == 1 && split_tree(L, S)) {
+    if (!layout && e && std::atoi(e) == 1 && split_tree(L, S)) {
         const int hb = std::max(32, hands / 2);   // hands per CTA; 2 x hb threads
         r.src = generate_pair(L, S, rule, std::max(1, jit_pair_min_blocks() * 64 / (2 * hb)), hb);
         r.hands = hb;
@@ -616,7 +625,7 @@ Gen jit_source(const Levels& L, int rule, int hands, bool seq, int groups) {
         r.smem = size_t(hb) * size_t(L.n + S.nx) * sizeof(double);
         return r;
     }
-    r.src = generate(L, rule, std::max(1, jit_min_blocks() * 32 / hands), hands, seq);
+    r.src = generate(L, rule, std::max(1, jit_min_blocks() * 32 / hands), hands, layout);
     r.hands = r.threads = hands;
     r.smem = size_t(hands) * size_t(L.n) * sizeof(double);
     return r;
@@ -636,7 +645,7 @@ std::map<std::string, Compiled>& jit_cache() {
 
 }  // namespace
 
-bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq, int groups) {
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, int layout, int groups) {
     out = JitStep{};
     if (const char* env = std::getenv("KR_STEP"))
         if (std::string(env) != "jit") {
@@ -658,7 +667,7 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         why = "NVRTC not available";
         return false;
     }
-    const Gen gen = jit_source(L, rule, jit_hands(), seq, groups);
+    const Gen gen = jit_source(L, rule, jit_hands(), layout, groups);
     const std::string& src = gen.src;
     if (src.empty()) {
         why = "treeplex does not split into " + std::to_string(groups) + " warp groups";
@@ -699,7 +708,7 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         it = jit_cache().emplace(src, std::move(c)).first;
     }
     out.kern = it->second.kern;
-    out.seq = seq;
+    out.layout = layout;
     out.n = t.n_seq;
     out.hands = gen.hands;
     out.threads = gen.threads;
@@ -743,10 +752,10 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
     KR_CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(j.kern), args));
 }
 
-std::string jit_step_source(const kr_treeplex& t, int rule, bool seq, int groups) {
+std::string jit_step_source(const kr_treeplex& t, int rule, int layout, int groups) {
     Levels L;
     if (!levels_of(t, L)) return "";
-    return jit_source(L, rule, jit_hands(), seq, groups).src;
+    return jit_source(L, rule, jit_hands(), layout, groups).src;
 }
 
 }  // namespace krb

@@ -16,7 +16,7 @@ struct JitStep {
     int n = 0;
     int hands = 128;   // hands per CTA
     int threads = 128; // threads per CTA (two per hand in the two-group kernels)
-    bool seq = false;  // sequence-major gradients / strategies
+    int layout = 0;    // 0 hand-major, 1 per-board sequence-major, 2 global sequence-major x
     size_t smem = 0;   // one hands x n tile (+ the two-group exchange slots)
     std::string log;   // NVRTC / ptxas log (registers, spills)
 };
@@ -25,11 +25,13 @@ struct JitStep {
 // update rule (KR_RULE_*).  False, with the reason in `why`, when NVRTC is
 // absent, the tree is not level-ordered or too large, or KR_STEP names
 // another kernel.
-// seq: gradients read and strategies written sequence-major per board (the
-// implicit engine's kron_product_seq layout; bstart / nb at launch).
+// layout 1: gradients read and strategies written sequence-major per board
+// (the implicit engine's kron_product_seq layout; bstart / nb at launch);
+// layout 2: strategies written sequence-major over all hands (the
+// Kronecker-factored engine's staging layout), gradients hand-major.
 // groups > 1: the tree split over that many warp groups per 32-hand set (for
 // grids too small to fill the GPU with one thread per hand).
-bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, bool seq = false,
+bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string& why, int layout = 0,
                       int groups = 1);
 
 // k_player_team's mode-1 arguments (the sweep, sequence form, discount and
@@ -43,6 +45,6 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
 int jit_stagger_ns();
 
 // The generated source (for inspection and tests).
-std::string jit_step_source(const kr_treeplex& t, int rule, bool seq = false, int groups = 1);
+std::string jit_step_source(const kr_treeplex& t, int rule, int layout = 0, int groups = 1);
 
 }  // namespace krb

@@ -1013,19 +1013,46 @@ void kf_destroy(KfState* k) {
 
 // Boards [b0, b1) of one product: the input made sequence-major, then
 // A x = Vᵀ rows, folds, [U|Â] rows; Aᵀy = folds (Uᵀ rows and chains), [Âᵀ|V] rows.
+// The engine's staging layout: the input sequence-major over all of the
+// direction's hands, out[s M + J] = in[J n + s] (hands [J0, J1)).
+void kf_stage(kr_engine* e, int dir, const double* in, double* inT, int64_t J0, int64_t J1, cudaStream_t s) {
+    KfState* k = e->kf;
+    const int64_t M = dir == 0 ? k->M2 : k->M1;
+    const int n = dir == 0 ? k->n2 : k->n1;
+    if (J1 <= J0) return;
+    krb::launch(k_kf_seqmajor, unsigned((J1 - J0 + 31) / 32), 256, size_t(32) * n * sizeof(double), s, in, M, n, J0, J1,
+                inT);
+    KR_CK_LAUNCH();
+    e->launches++;
+}
+
+void kf_kernels(kr_engine* e, int dir, const double* inT, double* out, cudaStream_t s, int b0, int b1);
+
 void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s, int b0, int b1) {
     KfState* k = e->kf;
     if (b1 < 0) b1 = k->nb;
     if (b1 <= b0) return;
+    const int64_t J0 = (dir == 0 ? k->hOff2 : k->hOff1)[size_t(b0)], J1 = (dir == 0 ? k->hOff2 : k->hOff1)[size_t(b1)];
+    kf_stage(e, dir, in, k->inT[dir], J0, J1, s);
+    kf_kernels(e, dir, k->inT[dir], out, s, b0, b1);
+}
+
+// The products on an input already in the staging layout (the DCFR solver
+// writes its strategies that way: no transpose per product).
+void kf_product_staged(kr_engine* e, int dir, const double* inT, double* out, cudaStream_t s) {
+    kf_kernels(e, dir, inT, out, s, 0, e->kf->nb);
+}
+
+void kf_stage_all(kr_engine* e, int dir, const double* in, double* inT, cudaStream_t s) {
+    KfState* k = e->kf;
+    kf_stage(e, dir, in, inT, 0, (dir == 0 ? k->hOff2 : k->hOff1)[size_t(k->nb)], s);
+}
+
+void kf_kernels(kr_engine* e, int dir, const double* inT, double* out, cudaStream_t s, int b0, int b1) {
+    KfState* k = e->kf;
     const unsigned nb = unsigned(b1 - b0);
     constexpr int T = 32 * kKfWarps;
     const int64_t M = dir == 0 ? k->M2 : k->M1;
-    const int n = dir == 0 ? k->n2 : k->n1;
-    const int64_t J0 = (dir == 0 ? k->hOff2 : k->hOff1)[size_t(b0)], J1 = (dir == 0 ? k->hOff2 : k->hOff1)[size_t(b1)];
-    double* inT = k->inT[dir];
-    krb::launch(k_kf_seqmajor, unsigned((J1 - J0 + 31) / 32), 256, size_t(32) * n * sizeof(double), s, in, M, n, J0, J1,
-                inT);
-    KR_CK_LAUNCH();
     if (dir == 0) {
         krb::launch(k_kfa_vt<kKfWarps>, dim3(unsigned(k->n1 * k->gy), nb), T, k->smVT, s, k->dBoards, b0, k->gy, k->gs,
                     inT, M, k->tz[0]);
@@ -1036,7 +1063,7 @@ void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream
         krb::launch(k_kfa_ua<kKfWarps>, dim3(unsigned(k->n1 * k->gu), nb), T, k->smUA, s, k->dBoards, b0, k->gu, inT,
                     M, k->tz[0], k->zf[0], out);
         KR_CK_LAUNCH();
-        e->launches += 4;
+        e->launches += 3;
     } else {
         krb::launch(k_kft_fold, dim3(unsigned(k->n1), nb), kKfFoldThreads, k->smFT, s, k->dBoards, b0, inT, M, k->tz[1],
                     k->zf[1]);
@@ -1044,7 +1071,7 @@ void kf_product(kr_engine* e, int dir, const double* in, double* out, cudaStream
         krb::launch(k_kft_av<kKfWarps>, dim3(unsigned(k->n2 * k->gv), nb), T, k->smAV, s, k->dBoards, b0, k->gv, inT,
                     M, k->tz[1], k->zf[1], out);
         KR_CK_LAUNCH();
-        e->launches += 3;
+        e->launches += 2;
     }
 }
 

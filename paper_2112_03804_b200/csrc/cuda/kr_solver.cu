@@ -54,7 +54,8 @@ struct kr_solver {
     // implicit-engine solves keep x and the gradients sequence-major per
     // board (k7seq): kron_product_seq runs without transposes and the
     // compiled step reads / writes that layout (jitSeq)
-    bool k7seq = false;
+    bool k7seq = false;          // a sequence-major solve is running (seqMode 1: implicit, 2: Kronecker-factored)
+    int seqMode = 0;
     krb::JitStep jitSeq[2];
     int jitSeqRule[2] = {-1, -1};
     double* xs[2] = {nullptr, nullptr};
@@ -750,42 +751,76 @@ void jit_prepare(kr_solver* s) {
                 continue;
             }
         }
-        if (jit_step_compile(t, s->rule, s->jit[p], s->jitWhy[p], false, groups)) {
+        if (jit_step_compile(t, s->rule, s->jit[p], s->jitWhy[p], 0, groups)) {
             s->jitRule[p] = s->rule;
             s->jitWhy[p].clear();
             std::string why;
             s->jitSeq[p] = JitStep{};
             s->jitSeqRule[p] = -1;
-            if (!small && s->eng->kron && jit_step_compile(t, s->rule, s->jitSeq[p], why, true))
-                s->jitSeqRule[p] = s->rule;
+            const int lay = s->eng->kron ? 1 : s->eng->kf ? 2 : 0;
+            if (!small && lay && jit_step_compile(t, s->rule, s->jitSeq[p], why, lay)) s->jitSeqRule[p] = s->rule;
         }
     }
 }
 
-// Sequence-major solves on the implicit engine (KR_K7SEQ=0 disables): both
-// players' compiled steps in their sequence-major form, no SelfCheck (it
+// Sequence-major solves: the implicit engine keeps x and the gradients
+// [seq][hand] per board (kron_product_seq, no transposes; KR_K7SEQ=0
+// disables), the Kronecker-factored engine keeps x in its staging layout
+// (kf_product_staged skips the per-product transpose; KR_KFSEQ=0 disables).
+// Both players' compiled steps in the matching form; no SelfCheck (it
 // compares hand-major products).
-bool k7seq_ok(const kr_solver* s) {
-    if (const char* env = std::getenv("KR_K7SEQ"))
-        if (std::atoi(env) == 0) return false;
-    return s->eng->kron && !s->eng->scRef && s->jitSeqRule[0] == s->rule && s->jitSeqRule[1] == s->rule &&
-           s->jitSeq[0].kern && s->jitSeq[1].kern;
+int seq_mode_for(const kr_solver* s) {
+    const int mode = s->eng->kron ? 1 : s->eng->kf ? 2 : 0;
+    if (!mode) return 0;
+    if (const char* env = std::getenv(mode == 1 ? "KR_K7SEQ" : "KR_KFSEQ"))
+        if (std::atoi(env) == 0) return 0;
+    if (s->eng->scRef) return 0;
+    for (int p = 0; p < 2; ++p)
+        if (s->jitSeqRule[p] != s->rule || !s->jitSeq[p].kern || s->jitSeq[p].layout != mode) return 0;
+    return mode;
 }
+bool k7seq_ok(const kr_solver* s) { return seq_mode_for(s) != 0; }
 
-// x (hand-major, from the initial strategy) -> xs: player 1's x feeds A^T
-// (direction 1's summing side), player 2's feeds A (direction 0's)
+// player p's x as the input of the product that consumes it: player 1's
+// feeds A^T (direction 1), player 2's feeds A (direction 0)
 void enter_seq(kr_solver* s, cudaStream_t st) {
+    const int mode = seq_mode_for(s);
     for (int p = 0; p < 2; ++p) {
         if (!s->xs[p]) s->xs[p] = dev_alloc<double>(std::max<int64_t>(s->H[p] * s->n[p], 1));
-        kron_transpose(s->eng, p == 0 ? 1 : 0, 0, s->x[p], s->xs[p], true, st);
+        const int dir = p == 0 ? 1 : 0;
+        if (mode == 1) kron_transpose(s->eng, dir, 0, s->x[p], s->xs[p], true, st);
+        else kf_stage_all(s->eng, dir, s->x[p], s->xs[p], st);
     }
     s->k7seq = true;
+    s->seqMode = mode;
+}
+
+// the staging layout back to hand-major: out[h n + q] = in[q H + h]
+__global__ void k_unstage(const double* __restrict__ in, double* __restrict__ out, int64_t H, int n) {
+    pdl_entry();
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= H * n) return;
+    const int64_t h = i / n;
+    const int q = int(i - h * n);
+    out[i] = in[int64_t(q) * H + h];
 }
 
 void leave_seq(kr_solver* s, cudaStream_t st) {
     if (!s->k7seq) return;
-    for (int p = 0; p < 2; ++p) kron_transpose(s->eng, p == 0 ? 1 : 0, 0, s->xs[p], s->x[p], false, st);
+    for (int p = 0; p < 2; ++p) {
+        if (s->seqMode == 1) {
+            kron_transpose(s->eng, p == 0 ? 1 : 0, 0, s->xs[p], s->x[p], false, st);
+        } else {
+            const int64_t len = s->H[p] * s->n[p];
+            if (len > 0) {
+                krb::launch(k_unstage, unsigned((len + 255) / 256), 256, 0, st, s->xs[p], s->x[p], s->H[p], s->n[p]);
+                KR_CK_LAUNCH();
+                s->launches++;
+            }
+        }
+    }
     s->k7seq = false;
+    s->seqMode = 0;
 }
 
 
@@ -836,7 +871,8 @@ void iteration_body(kr_solver* s, cudaStream_t st, double pos, double neg, doubl
     kr_engine* e = s->eng;
     if (s->k7seq) {
         for (int p = 0; p < 2; ++p) {
-            kron_product_seq(e, p, s->xs[1 - p], s->g, st);                     // g1 = A x2, A^T x1
+            if (s->seqMode == 1) kron_product_seq(e, p, s->xs[1 - p], s->g, st);   // g1 = A x2, A^T x1
+            else kf_product_staged(e, p, s->xs[1 - p], s->g, st);
             engine_account(e, p);
             jit_step_launch(s->jitSeq[p], s->device, s->H[p], s->g, p, s->regret[p], s->xs[p], s->avg[p], pos, neg,
                             shrink, dev ? s->d_fac : nullptr, dev ? s->d_cnt : nullptr, 0, nullptr, nullptr, st,
@@ -1402,7 +1438,7 @@ int kr_solver_set_rule(kr_solver* s, int rule) {
 int64_t kr_jit_step_source(const kr_treeplex* t, int rule, char* buf, int64_t cap) {
     if (!t) return -1;
     const char* ge = std::getenv("KR_JIT_SOURCE_GROUPS");   // inspect the warp-group form
-    const std::string src = krb::jit_step_source(*t, rule, false, ge ? std::atoi(ge) : 1);
+    const std::string src = krb::jit_step_source(*t, rule, 0, ge ? std::atoi(ge) : 1);
     if (src.empty()) return -1;
     if (buf && cap > 0) {
         const size_t n = std::min(src.size(), size_t(cap - 1));

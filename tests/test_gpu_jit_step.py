@@ -145,3 +145,35 @@ def test_k7_sequence_major_solve_bitwise(turn12, preset, monkeypatch):
         (c1, c2), (d1, d2) = solve("0", incremental)
         assert bits_equal(b1, c1) and bits_equal(b2, c2), incremental
         assert bits_equal(a1, d1) and bits_equal(a2, d2), incremental
+
+
+@pytest.mark.parametrize("preset", ["dcfr", "prm_plus"])
+def test_kf_staged_solve_bitwise(turn12, preset, monkeypatch):
+    """Kronecker-factored solves keep x in the engine's staging layout (the
+    compiled step writes it, kf_product_staged skips the per-product
+    transpose): the same bits as the hand-major solve (KR_KFSEQ=0)."""
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200.solver import CudaSolver
+    prm = DcfrParams(max_iters=25, checkpoint_every=5) if preset == "dcfr" else \
+        DcfrParams.prm_plus(max_iters=25, checkpoint_every=5)
+
+    def solve(flag, incremental):
+        monkeypatch.setenv("KR_KFSEQ", flag)
+        insts = [i for i, _ in turn12]
+        eng = CudaEngine.kfactored(insts)
+        i0 = insts[0]
+        s = CudaSolver(eng, i0.treeplex(0), i0.treeplex(1), [i.m1 for i in insts], [i.m2 for i in insts], i0.pot)
+        if incremental:
+            s.begin(prm)
+            for _ in range(7):
+                s.iterate(1)
+            s.iterate(4)
+            return s.checkpoint(), s.averages()
+        r = s.run(prm)
+        return (r.trace_br1, r.trace_br2), (r.avg1, r.avg2)
+
+    for incremental in (False, True):
+        (b1, b2), (a1, a2) = solve("1", incremental)
+        (c1, c2), (d1, d2) = solve("0", incremental)
+        assert bits_equal(b1, c1) and bits_equal(b2, c2), incremental
+        assert bits_equal(a1, d1) and bits_equal(a2, d2), incremental
