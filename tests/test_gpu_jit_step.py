@@ -26,13 +26,24 @@ pytestmark = pytest.mark.gpu
     ("bluffing", {}, "b", 300),
     ("all_tie", {}, "b", 100),
     ("random_small", dict(seed=1), "b", 200),
+    ("random_small", dict(seed=5), "a", 150),
+    ("random_small", dict(seed=9), "b", 150),
     ("bench", dict(seed=7, hands=60), "b", 200),
+    ("bench", dict(seed=11, hands=97), "b", 120),
 ])
-def test_forced_jit_gap_trajectory_bitwise(name, kw, tech, iters, monkeypatch):
-    monkeypatch.setenv("KR_STEP", "jit")
+@pytest.mark.parametrize("groups", ["1", "4"], ids=["one-thread", "four-groups"])
+def test_forced_jit_gap_trajectory_bitwise(name, kw, tech, iters, groups, monkeypatch):
+    """Every corpus tree through the compiled step, one thread per hand
+    (KR_STEP=jit) and split over four warp groups (the single-board default),
+    against the oracle's gap trajectory."""
+    if groups == "1":
+        monkeypatch.setenv("KR_STEP", "jit")
+    else:
+        monkeypatch.setenv("KR_JIT_GROUPS", "4")
     p, o = H.builtin(name, **kw), po.Instance.builtin(name, **kw)
     s = solver_for([(p, p.sparsify(tech, True))])
-    assert s.step_kind(0)[0] == 2 and s.step_kind(1)[0] == 2, s.step_kind(0)
+    if groups == "1":
+        assert s.step_kind(0)[0] == 2 and s.step_kind(1)[0] == 2, s.step_kind(0)
     r = s.run(DcfrParams(max_iters=iters, checkpoint_every=1))
     ro = po.dcfr(o, o.sparsify(tech, True), max_iters=iters, checkpoint_every=1)
     assert bits_equal(r.trace_br1, ro["trace_br1"]) and bits_equal(r.trace_br2, ro["trace_br2"])
