@@ -1203,7 +1203,7 @@ struct GraphDelta {
 bool overlap_ok(const kr_solver* s) {
     const char* env = std::getenv("KR_OVERLAP");
     if (!(env && std::atoi(env) == 1)) return false;
-    return s->nboards >= 2 && (s->eng->kron || s->eng->kf) && krb::engine_boards(s->eng) == s->nboards;
+    return !s->k7seq && s->nboards >= 2 && (s->eng->kron || s->eng->kf) && krb::engine_boards(s->eng) == s->nboards;
 }
 
 void ensure_overlap(kr_solver* s) {

@@ -118,6 +118,8 @@ def test_board_half_pipelining_bitwise(turn12, kind, monkeypatch):
 
     def solve(overlap):
         monkeypatch.setenv("KR_OVERLAP", overlap)
+        monkeypatch.setenv("KR_K7SEQ", "0")   # the pipelined form runs on hand-major solves
+        monkeypatch.setenv("KR_KFSEQ", "0")
         insts = [i for i, _ in turn12] if isinstance(turn12[0], tuple) else list(turn12)
         eng = CudaEngine.kron(insts) if kind == "implicit" else CudaEngine.kfactored(insts)
         i0 = insts[0]
