@@ -561,7 +561,7 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
         if (gi > 0)
             for (int v : L.levNodes[1])
                 if (S.grp[size_t(v)] == gi) o << "  Xh[" << S.slot[size_t(v)] << "] = nv" << v << ";\n";
-        o << "  }\n  bar_all();\n";   // B: group 1's subtree values are in X
+        o << "  }\n  bar_all();\n";   // B: the other groups' subtree values are in X
         if (gi == 0) {
             o << "  if (valid) {\n";
             for (int v : L.levNodes[0])
@@ -591,20 +591,20 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
     return o.str();
 }
 
-// The source for the tree: one thread per hand, compiled for the resident
-// CTAs per SM that one round of config 3's hands needs; KR_JIT_SPLIT=1: two
-// warp groups per hand set when the tree splits (80 registers, twice the
-// warps, but the groups wait on each other: within 1-2% of the one-thread
-// kernel at config 3, profiles/r02/jit_step_probe_r02z.log).
 struct Gen {
     std::string src;
     int hands = 0, threads = 0;   // hands and threads per CTA
     size_t smem = 0;              // dynamic shared memory per CTA
 };
 
-// groups > 1: the hand set's tree split over that many warp groups (small
-// grids: single boards, where one thread per hand leaves most SMs idle), 32
-// hands per CTA; empty source when the tree does not split that way.
+// The source for the tree.  groups > 1: the hand set's tree split over that
+// many warp groups (small grids: single boards, where one thread per hand
+// leaves most SMs idle), 32 hands per CTA; empty when the tree does not split
+// that way.  Otherwise one thread per hand, compiled for the resident CTAs
+// per SM that one round of config 3's hands needs; KR_JIT_SPLIT=1: two warp
+// groups per hand set (80 registers, twice the warps, but the groups wait on
+// each other: within 1-2% of the one-thread kernel at config 3,
+// profiles/r02/jit_step_probe_r02z.log).
 Gen jit_source(const Levels& L, int rule, int hands, int layout, int groups) {
     Gen r;
     Split S;
@@ -728,11 +728,16 @@ void jit_step_launch(const JitStep& j, int device, int64_t H, const double* g, i
                      const int64_t* bstart, int nb, int stagger) {
     const unsigned grid = unsigned((H + j.hands - 1) / j.hands);
     if (grid == 0) return;
-    if (j.smem > 48 * 1024) {
+    if (j.smem > 48 * 1024) {   // once per kernel and device
         static std::mutex mu;
+        static std::map<std::pair<cudaKernel_t, int>, size_t> done;
         std::lock_guard<std::mutex> lk(mu);
-        KR_CK(cudaKernelSetAttributeForDevice(j.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(j.smem),
-                                              device));
+        size_t& have = done[{j.kern, device}];
+        if (have < j.smem) {
+            KR_CK(cudaKernelSetAttributeForDevice(j.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(j.smem),
+                                                  device));
+            have = j.smem;
+        }
     }
     long long Hl = H;
     void* args[] = {&g,   &negate, &regret,  &xout,  &avg, &pos,    &neg, &shrink, &fac,
