@@ -328,6 +328,62 @@ def config2_gpu(peak):
             "solver_checkpoint_every_50": solver}
 
 
+def config4_gpu(peak):
+    """BASELINE configs[3] (config 4): the large-rank variant, 26-card deck
+    (13 ranks x 2 suits), board Kc9d7c4d2c, all 210 hands per side, 3-bet tree.
+    Technique A exercises the low-rank U V^T term (rank 1,000 = the peel cap)
+    and the A-hat SpMV; Technique B beside it.  Pairs/s (device pointers,
+    CUDA events), the fraction of the HBM peak, DCFR iterations/s, and the
+    implicit engine on the same payoff."""
+    import torch
+
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200 import host as H
+    from paper_2112_03804_b200.solver import DcfrParams, solver_for
+    inst = H.builtin("river_full", seed=1, board="Kc9d7c4d2c", deck=26, tree=3)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = {"workload": "config4: 26-card deck (13 ranks x 2 suits), board Kc9d7c4d2c, 210 hands per side, 3-bet tree"}
+
+    def timed(e, reps=500):
+        st = torch.cuda.ExternalStream(e.stream)
+        g = torch.Generator(device="cpu").manual_seed(4)
+        x = torch.randn(e.cols, dtype=torch.float64, generator=g).to(dev)
+        y = torch.randn(e.rows, dtype=torch.float64, generator=g).to(dev)
+        a = torch.empty(e.rows, dtype=torch.float64, device=dev)
+        b = torch.empty(e.cols, dtype=torch.float64, device=dev)
+        for _ in range(5):
+            e.pair_device(x.data_ptr(), a.data_ptr(), y.data_ptr(), b.data_ptr())
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            e.pair_device(x.data_ptr(), a.data_ptr(), y.data_ptr(), b.data_ptr())
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3
+
+    for tech in ("a", "b"):
+        f = inst.sparsify(tech, True)
+        eng = CudaEngine(f)
+        us = timed(eng)
+        pair_bytes = 2 * eng.bytes_per_product()
+        sv = solver_for([(inst, f)])
+        sv.run(DcfrParams(max_iters=10, checkpoint_every=10))
+        r = sv.run(DcfrParams(max_iters=1000, checkpoint_every=50), want_avg=False)
+        out[f"technique_{tech}"] = {"nnz": {k: int(v) for k, v in eng.nnz.items()}, "k": int(eng.k),
+                                    "us_per_pair": us, "pairs_per_s": 1e6 / us,
+                                    "whole_pair_frac_of_peak": pair_bytes / (us / 1e6) / 1e9 / peak,
+                                    "api": "kr_engine_pair_device",
+                                    "solver_iters_per_s": 1000 / r.seconds, "exploitability": r.exploitability}
+        sv.close()
+        eng.close()
+    ek = CudaEngine.kron([inst])
+    us = timed(ek)
+    out["implicit"] = {"us_per_pair": us, "pairs_per_s": 1e6 / us}
+    ek.close()
+    return out
+
+
 def config1_cpu(gpu):
     """The same 1000 CFR+ iterations on the oracle (CPU, one thread) and the
     bitwise cross-check of the GPU trace against it."""
@@ -606,6 +662,7 @@ def run_product(args):
     turn = run_turn(rank, world, local, max_over_ranks, dist.group.WORLD if world > 1 else None, comm)
     config1 = config1_gpu() if rank == 0 else None
     config2 = config2_gpu(measured_peak()[0]) if rank == 0 else None
+    config4 = config4_gpu(measured_peak()[0]) if rank == 0 else None
     gpu_out = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the timed region's last outputs, for the parity check against the oracle
@@ -661,6 +718,7 @@ def run_product(args):
         "config5_sweep": sweep,
         "config1": {k: v for k, v in config1.items() if not k.startswith("_")},
         "config2": config2,
+        "config4": config4,
         "turn": turn,
     }
     if world == 1 and not args.no_cpu_baseline:
