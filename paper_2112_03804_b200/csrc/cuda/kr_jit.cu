@@ -707,6 +707,23 @@ bool jit_step_compile(const kr_treeplex& t, int rule, JitStep& out, std::string&
         }
         it = jit_cache().emplace(src, std::move(c)).first;
     }
+    // ptxas' spills of the compiled step (its -v report): a tree whose
+    // regrets overflow the register budget runs slower than the generic team
+    // kernel (the 91-sequence tree: 1,265 against 1,804 it/s), so heavy
+    // spilling keeps the generic kernel
+    {
+        const std::string& lg = it->second.log;
+        const size_t at = lg.find(" bytes spill stores");
+        if (at != std::string::npos) {
+            size_t b = lg.rfind(' ', at - 1);
+            const long spills = std::strtol(lg.c_str() + (b == std::string::npos ? 0 : b + 1), nullptr, 10);
+            const char* lim = std::getenv("KR_JIT_MAX_SPILL");
+            if (spills > (lim ? std::atol(lim) : 1024)) {
+                why = "compiled step spills " + std::to_string(spills) + " bytes per thread";
+                return false;
+            }
+        }
+    }
     out.kern = it->second.kern;
     out.layout = layout;
     out.n = t.n_seq;

@@ -190,3 +190,14 @@ def test_kf_staged_solve_bitwise(turn12, preset, monkeypatch):
         (c1, c2), (d1, d2) = solve("0", incremental)
         assert bits_equal(b1, c1) and bits_equal(b2, c2), incremental
         assert bits_equal(a1, d1) and bits_equal(a2, d2), incremental
+
+
+def test_spilling_tree_keeps_the_team_kernel(monkeypatch):
+    """A tree whose regrets overflow the compiled step's register budget (the
+    91-sequence tree: ~2 KB of spills per thread) keeps the generic team
+    kernel, which is faster there; the reason says so."""
+    monkeypatch.setenv("KR_STEP", "jit")   # one thread per hand, any size
+    p = H.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=91)
+    s = solver_for([(p, p.sparsify("b", True))])
+    k, why = s.step_kind(0)
+    assert k == 1 and "spills" in why, (k, why)
