@@ -461,13 +461,14 @@ bool split_tree(const Levels& L, Split& S, int want = 2) {
     return true;
 }
 
-std::string generate_pair(const Levels& L, const Split& S, int rule, int minBlocks, int hands) {
+std::string generate_pair(const Levels& L, const Split& S, int rule, int minBlocks, int hands, int layout = 0) {
     std::ostringstream o;
     const int N = L.n;
     o << kPreamble;
     o << "#define N " << N << "\n#define HB " << hands << "\n#define NT (" << S.groups << " * HB)\n#define NX "
       << std::max(S.nx, 1) << "\n";
-    o << "#define MINB " << minBlocks << "\n";
+    o << "#define MINB " << minBlocks << "\n#define GSEQ " << (layout == 1 ? 1 : 0) << "\n#define XSEQ " << layout
+      << "\n";
     o << R"(__device__ __forceinline__ void bar_all() { asm volatile("barrier.sync 1, %0;" :: "n"(NT) : "memory"); }
 extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __restrict__ g, int negate,
     double* __restrict__ regret, double* __restrict__ xout, double* __restrict__ avg, double pos, double neg,
@@ -486,15 +487,15 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
   const long long e0 = h0 * N;
   const int ne = nh * N;
   const unsigned bytes = HB * N * 8;
-  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (unsigned long long)(g + e0) |
-                                   (unsigned long long)(xout + e0) | (noAvg ? 0ull : (unsigned long long)(avg + e0))) &
-                                  15ull) == 0;
+  const bool full = nh == HB && (((unsigned long long)(regret + e0) | (GSEQ ? 0ull : (unsigned long long)(g + e0)) |
+                                   (XSEQ ? 0ull : (unsigned long long)(xout + e0)) |
+                                   (noAvg ? 0ull : (unsigned long long)(avg + e0))) & 15ull) == 0;
   if (full) {
     if (tid == 0) {
       bar_init(&bar);
       bar_expect(&bar, bytes);
       g2s(G, regret + e0, bytes, &bar);
-      l2_prefetch(g + e0, bytes);
+      if (!GSEQ) l2_prefetch(g + e0, bytes);
       if (!noAvg) l2_prefetch(avg + e0, bytes);
     }
     bar_all();
@@ -507,9 +508,20 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
   double* Xh = X + hand * NX;
   const bool valid = hand < nh;
   const double* ex = (extra && valid) ? extra + (h0 + hand) * N : nullptr;
+  // sequence-major layouts (as the one-thread kernel): this hand's N values
+  // m apart from gb (per board, XSEQ / GSEQ 1) or H apart (XSEQ 2)
+  long long gb = 0, gm = 1;
+  if ((GSEQ || XSEQ == 1) && valid) {
+    const long long hg = h0 + hand;
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (bstart[mid] <= hg) lo = mid; else hi = mid; }
+    gb = bstart[lo] * N + (hg - bstart[lo]);
+    gm = bstart[lo + 1] - bstart[lo];
+  }
+  if (XSEQ == 2) { gb = h0 + hand; gm = H; }
 )";
     // the part both groups run between their own sections (same barrier sequence)
-    const std::string loadG = R"(  bar_all();
+    const std::string loadTile = R"(  bar_all();
   if (full) {
     if (tid == 0) { fence_async(); bar_expect(&bar, bytes); g2s(G, g + e0, bytes, &bar); }
     bar_wait(&bar, 1);
@@ -518,7 +530,7 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
   }
   bar_all();
 )";
-    const std::string outX = R"(  bar_all();
+    const std::string outTile = R"(  bar_all();
   if (full) {
     fence_async();
     bar_all();
@@ -526,7 +538,8 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
   } else {
     for (int q = tid; q < ne; q += NT) xout[e0 + q] = G[q];
   }
-  if (!noAvg) {
+)";
+    const std::string outAvg = R"(  if (!noAvg) {
 #pragma unroll 8
     for (int q = tid; q < ne; q += NT) avg[e0 + q] = (avg[e0 + q] + G[q]) * shrink;
   }
@@ -552,7 +565,13 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
         for (int sq : mine) o << "  double " << reg(sq) << " = " << val(sq) << ";\n";
         for (int v = 0; v < L.nn; ++v)
             if (S.grp[size_t(v)] == gi) o << "  double nv" << v << " = 0.0;\n";
-        o << loadG;
+        if (layout == 1) {   // each group gathers its own sequences' gradients
+            o << "  bar_all();\n  if (valid) {\n";
+            for (int sq : mine) o << "    " << val(sq) << " = g[gb + " << sq - 1 << " * gm];\n";
+            o << "  }\n  bar_all();\n";
+        } else {
+            o << loadTile;
+        }
         // the group's nodes below level 0, deepest level first
         o << "  if (valid) {\n";
         for (int l = L.nlev - 1; l >= 1; --l)
@@ -583,7 +602,14 @@ extern "C" __global__ void __launch_bounds__(NT, MINB) kr_step(const double* __r
         if (rule == 0)
             for (int sq : mine) o << "  " << reg(sq) << " = " << reg(sq) << " * (" << reg(sq) << " > 0 ? pos : neg);\n";
         o << "  }\n";
-        o << outX;
+        if (layout) {   // each group writes its own sequences' strategies
+            o << "  bar_all();\n  if (valid) {\n";
+            for (int sq : mine) o << "    xout[gb + " << sq - 1 << " * gm] = " << val(sq) << ";\n";
+            o << "  }\n";
+        } else {
+            o << outTile;
+        }
+        o << outAvg;
         for (int sq : mine) o << "  " << val(sq) << " = " << reg(sq) << ";\n";
         o << outR;
     }
@@ -610,8 +636,8 @@ Gen jit_source(const Levels& L, int rule, int hands, int layout, int groups) {
     Split S;
     const char* e = std::getenv("KR_JIT_SPLIT");
     if (groups > 1) {
-        if (layout || !split_tree(L, S, groups)) return r;
-        r.src = generate_pair(L, S, rule, 1, 32);
+        if (!split_tree(L, S, groups)) return r;
+        r.src = generate_pair(L, S, rule, 1, 32, layout);
         r.hands = 32;
         r.threads = 32 * S.groups;
         r.smem = size_t(32) * size_t(L.n + std::max(S.nx, 1)) * sizeof(double);

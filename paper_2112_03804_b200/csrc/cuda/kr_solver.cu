@@ -757,8 +757,12 @@ void jit_prepare(kr_solver* s) {
             std::string why;
             s->jitSeq[p] = JitStep{};
             s->jitSeqRule[p] = -1;
-            const int lay = s->eng->kron ? 1 : s->eng->kf ? 2 : 0;
-            if (!small && lay && jit_step_compile(t, s->rule, s->jitSeq[p], why, lay)) s->jitSeqRule[p] = s->rule;
+            // implicit engines: sequence-major on full-GPU grids only (single
+            // boards measured no gain: 26,523 -> 26,380 it/s at config 2);
+            // Kronecker-factored: the staging layout at every size (config 2
+            // 10,908 -> 11,708)
+            const int lay = s->eng->kron ? (small ? 0 : 1) : s->eng->kf ? 2 : 0;
+            if (lay && jit_step_compile(t, s->rule, s->jitSeq[p], why, lay, groups)) s->jitSeqRule[p] = s->rule;
         }
     }
 }

@@ -201,3 +201,26 @@ def test_spilling_tree_keeps_the_team_kernel(monkeypatch):
     s = solver_for([(p, p.sparsify("b", True))])
     k, why = s.step_kind(0)
     assert k == 1 and "spills" in why, (k, why)
+
+
+@pytest.mark.parametrize("kind", ["kfactored"])
+@pytest.mark.parametrize("board,deck", [("Kc9d7c4d2c", 26), ("Ks7d4c2h9s", 52)], ids=["config4", "config2"])
+def test_single_board_sequence_major_solve_bitwise(kind, board, deck, monkeypatch):
+    """Single boards (the warp-group step) in the Kronecker-factored staging
+    layout against the hand-major solve: same bits.  (The implicit engine
+    keeps hand-major vectors on single boards; its sequence-major warp-group
+    form was measured no faster and is covered by the generator's layout
+    switch.)"""
+    from paper_2112_03804_b200 import CudaEngine
+    from paper_2112_03804_b200.solver import CudaSolver
+    p = H.builtin("river_full", seed=1, board=board, deck=deck, tree=3)
+
+    def solve(flag):
+        monkeypatch.setenv("KR_K7SEQ" if kind == "implicit" else "KR_KFSEQ", flag)
+        eng = CudaEngine.kron([p]) if kind == "implicit" else CudaEngine.kfactored([p])
+        s = CudaSolver(eng, p.treeplex(0), p.treeplex(1), [p.m1], [p.m2], p.pot)
+        return s.run(DcfrParams(max_iters=40, checkpoint_every=10))
+
+    a, b = solve("1"), solve("0")
+    assert bits_equal(a.trace_br1, b.trace_br1) and bits_equal(a.trace_br2, b.trace_br2)
+    assert bits_equal(a.avg1, b.avg1) and bits_equal(a.avg2, b.avg2)
