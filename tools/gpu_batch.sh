@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_jit_step.py -q -p no:cacheprovider -k "single_board or sequence_major or staged" 2>&1 | tail -3
-for v in 0 1; do KR_K7SEQ=$v BOARDS=1 timeout 300 python tools/solver_probe.py kron 2000 2>&1 | tail -1 | sed "s/^/[config2 k7seq $v] /"; KR_KFSEQ=$v BOARDS=1 timeout 300 python tools/solver_probe.py kfactored 2000 2>&1 | tail -1 | sed "s/^/[config2 kfseq $v] /"; done
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r02z_pytest_all5.log 2>&1; echo "rc=$?" >> gpurun_out/r02z_pytest_all5.log
+tail -3 gpurun_out/r02z_pytest_all5.log
