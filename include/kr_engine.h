@@ -350,7 +350,9 @@ int kr_solver_step_kind(const kr_solver* s, int player, const char** why);
 /* The CUDA C the compiled step is generated from, for treeplex t and update
  * rule (KR_RULE_*): copies up to cap bytes (NUL-terminated) into buf when buf
  * is non-NULL and returns the source length, or -1 when the treeplex is not
- * level-ordered.  Needs no device (inspection and compile tests). */
+ * level-ordered (or, with KR_JIT_SOURCE_GROUPS=g, does not split into g warp
+ * groups: the single-board form).  Needs no device (inspection and compile
+ * tests). */
 int64_t kr_jit_step_source(const kr_treeplex* t, int rule, char* buf, int64_t cap);
 int kr_solver_iterate(kr_solver* s, int n);
 int kr_solver_checkpoint(kr_solver* s, double* board_br1, double* board_br2);
