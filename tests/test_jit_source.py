@@ -52,3 +52,22 @@ def test_compiles_for_sm100a_without_local_arrays(config3_tree, tmp_path, rule):
     assert r.returncode == 0, r.stderr
     regs = int(re.search(r"Used (\d+) registers", r.stderr).group(1))
     assert regs <= 168   # three 128-hand CTAs per SM
+
+
+@pytest.mark.skipif(not os.path.exists(NVCC) and not shutil.which("nvcc"), reason="nvcc absent")
+def test_warp_group_form_compiles(config3_tree, tmp_path, monkeypatch):
+    """The single-board form (the tree split over four warp groups, node
+    values exchanged through shared memory) compiles for sm_100a without
+    spills, and every group section ends on the same barrier sequence."""
+    monkeypatch.setenv("KR_JIT_SOURCE_GROUPS", "4")
+    src = jit_step_source(config3_tree, 0)
+    assert "#define NT (4 * HB)" in src
+    sections = src.split("if (grp == ")
+    counts = {sec.count("bar_all();") for sec in sections[1:]}
+    assert len(sections) == 5 and len(counts) == 1, counts   # groups 0..3, same barrier count each
+    f = tmp_path / "kr_step_g4.cu"
+    f.write_text(src)
+    r = subprocess.run([NVCC, "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false", "-Xptxas", "-v",
+                        "-o", str(tmp_path / "g4.cubin"), str(f)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert " 0 bytes spill stores" in r.stderr
