@@ -1792,25 +1792,39 @@ __global__ void k_turn_contrib(const double* __restrict__ root, int64_t Hr, cons
 // Per turn hand h and continuation t in order: extra[h, sigma(t)] += the sum
 // over all boards in global order (rank-major, each rank's boards ascending;
 // boards holding h skipped) -- one left fold, the same on one GPU and on any
-// number of ranks.
-__global__ void k_turn_fold(const double* __restrict__ gathered, int world, int nbMax,
-                            const int32_t* __restrict__ bpre, int T, int m, int nt, const int32_t* __restrict__ sigma,
-                            double* __restrict__ extra) {
+// number of ranks.  One warp per turn hand: the lanes stage a continuation's
+// per-board values in shared memory (coalesced), lane 0 folds them in board
+// order (one thread per hand, 9 CTAs, took ~20 us per half-iteration).
+constexpr int kFoldWarps = 4;
+__global__ void __launch_bounds__(32 * kFoldWarps) k_turn_fold(const double* __restrict__ gathered, int world,
+                                                               int nbMax, const int32_t* __restrict__ bpre, int T,
+                                                               int m, int nt, const int32_t* __restrict__ sigma,
+                                                               double* __restrict__ extra) {
     krb::pdl_entry();
-    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    extern __shared__ double fs[];   // [kFoldWarps][world * nbMax]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int h = blockIdx.x * kFoldWarps + w;
     if (h >= m) return;
     const int64_t per = int64_t(T) * m * nbMax;
+    double* v = fs + size_t(w) * size_t(world) * nbMax;
     for (int t = 0; t < T; ++t) {
-        double acc = 0.0;
+        int n = 0;
         for (int r = 0; r < world; ++r) {
             const double* g = gathered + r * per + (int64_t(t) * m + h) * nbMax;
             const int nbr = bpre[r + 1] - bpre[r];
-            for (int b = 0; b < nbr; ++b) {
-                const double v = g[b];
-                if (uint64_t(__double_as_longlong(v)) != kSkipBits) acc += v;
-            }
+            for (int b = lane; b < nbr; b += 32) v[n + b] = g[b];
+            n += nbr;
         }
-        extra[int64_t(h) * nt + sigma[t] - 1] += acc;
+        __syncwarp();
+        if (lane == 0) {
+            double acc = 0.0;
+            for (int q = 0; q < n; ++q) {
+                const double x = v[q];
+                if (uint64_t(__double_as_longlong(x)) != kSkipBits) acc += x;
+            }
+            extra[int64_t(h) * nt + sigma[t] - 1] += acc;
+        }
+        __syncwarp();
     }
 }
 
@@ -1822,7 +1836,7 @@ __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, 
     if (fac) shrink = fac[3 * *dt + 2];  // graph replay
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= Hr * nr) return;
-    const int64_t r = q / nr;
+    const int64_t r = q < (int64_t(1) << 32) ? int64_t(uint32_t(q) / uint32_t(nr)) : q / nr;
     const double xv = xturn[int64_t(r2t[r]) * nt + sigma - 1] * x[q];
     x[q] = xv;
     if (doAvg) avg[q] = (avg[q] + xv) * shrink;  // solver.hpp:382-386
@@ -1842,7 +1856,10 @@ __global__ void k_river_scale_all(double* __restrict__ x, double* __restrict__ a
     int t = 0;
     while (q >= roff[t + 1]) ++t;
     const int nr = nrs[t];
-    const int64_t r = (q - roff[t]) / nr;
+    const int64_t off = q - roff[t];
+    // a continuation block holds Hr x nr < 2^32 values: 32-bit division (the
+    // 64-bit one is a long software sequence per element)
+    const int64_t r = off < (int64_t(1) << 32) ? int64_t(uint32_t(off) / uint32_t(nr)) : off / nr;
     const double xv = xturn[int64_t(r2t[r]) * nt + sigma[t] - 1] * x[q];
     x[q] = xv;
     if (doAvg) avg[q] = (avg[q] + xv) * shrink;  // solver.hpp:382-386
@@ -1884,7 +1901,7 @@ void turn_jit_prepare(kr_turn_solver* s) {
         if (T.jitRule == s->rule) return;
         T.jit = JitStep{};
         T.jitRule = -1;
-        if (!force && H < int64_t(2) * 148 * kJitHands) return;
+        if (!force && H < int64_t(2) * 148 * kJitHands) return;   // (the 1,128-hand turn tree: no gain compiled)
         kr_treeplex t{};
         t.n_nodes = T.nn;
         t.n_seq = T.n;
@@ -1958,7 +1975,9 @@ void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
         KR_CK(cudaStreamSynchronize(st));
         s->xfn(s->xuser);  // all-gathers contrib into gathered (the caller's buffers)
     }
-    krb::launch(k_turn_fold, unsigned((s->m + 127) / 128), 128, 0, st, s->gathered, s->world, s->nbMax, s->d_bpre,
+    krb::launch(k_turn_fold, unsigned((s->m + kFoldWarps - 1) / kFoldWarps), 32 * kFoldWarps,
+                size_t(kFoldWarps) * size_t(s->world) * size_t(s->nbMax) * sizeof(double), st, s->gathered, s->world,
+                s->nbMax, s->d_bpre,
                 s->T, s->m, nt, s->d_sigma + p * s->T, s->extra);
     KR_CK_LAUNCH();
     s->launches++;
