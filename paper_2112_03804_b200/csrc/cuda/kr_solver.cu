@@ -1828,6 +1828,39 @@ __global__ void __launch_bounds__(32 * kFoldWarps) k_turn_fold(const double* __r
     }
 }
 
+// One rank, no exchange: the same fold straight from the river root values
+// (k_turn_contrib + k_turn_fold without the staging array): board b's value
+// for turn hand h is root[t Hr + boff[b] + t2r[b m + h]], boards holding h
+// skipped, added in board order.
+__global__ void __launch_bounds__(32 * kFoldWarps) k_turn_fold_direct(const double* __restrict__ root, int64_t Hr,
+                                                                      const int32_t* __restrict__ t2r,
+                                                                      const int64_t* __restrict__ boff, int nb, int T,
+                                                                      int m, int nt, const int32_t* __restrict__ sigma,
+                                                                      double* __restrict__ extra) {
+    krb::pdl_entry();
+    extern __shared__ double fs[];   // [kFoldWarps][nb]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int h = blockIdx.x * kFoldWarps + w;
+    if (h >= m) return;
+    double* v = fs + size_t(w) * nb;
+    for (int t = 0; t < T; ++t) {
+        for (int b = lane; b < nb; b += 32) {
+            const int r = t2r[int64_t(b) * m + h];
+            v[b] = r >= 0 ? root[int64_t(t) * Hr + boff[b] + r] : __longlong_as_double((long long)kSkipBits);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double acc = 0.0;
+            for (int b = 0; b < nb; ++b) {
+                const double x = v[b];
+                if (uint64_t(__double_as_longlong(x)) != kSkipBits) acc += x;
+            }
+            extra[int64_t(h) * nt + sigma[t] - 1] += acc;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, const double* __restrict__ xturn,
                               const int32_t* __restrict__ r2t, int64_t Hr, int nr, int nt, int sigma,
                               double shrink, int doAvg, const double* __restrict__ fac = nullptr,
@@ -1964,6 +1997,14 @@ bool turn_fuse() {
 // per-board values, exchanged over the ranks (all-gather), folded in global
 // board order.
 void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
+    if (!s->comm && !s->xfn) {   // one rank: fold straight from the root values
+        krb::launch(k_turn_fold_direct, unsigned((s->m + kFoldWarps - 1) / kFoldWarps), 32 * kFoldWarps,
+                    size_t(kFoldWarps) * size_t(s->nb) * sizeof(double), st, s->root, s->Hr, s->d_t2r, s->d_boff,
+                    s->nb, s->T, s->m, nt, s->d_sigma + p * s->T, s->extra);
+        KR_CK_LAUNCH();
+        s->launches++;
+        return;
+    }
     const int64_t count = int64_t(s->T) * s->m * s->nbMax;
     krb::launch(k_turn_contrib, unsigned((count + 255) / 256), 256, 0, st, s->root, s->Hr, s->d_t2r, s->d_boff, s->nb,
                 s->m, s->T, s->nbMax, s->contrib);
