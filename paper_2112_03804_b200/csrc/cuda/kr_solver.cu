@@ -1838,27 +1838,28 @@ __global__ void __launch_bounds__(32 * kFoldWarps) k_turn_fold_direct(const doub
                                                                       int m, int nt, const int32_t* __restrict__ sigma,
                                                                       double* __restrict__ extra) {
     krb::pdl_entry();
-    extern __shared__ double fs[];   // [kFoldWarps][nb]
+    extern __shared__ double fs[];   // [kFoldWarps][T][nb]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int h = blockIdx.x * kFoldWarps + w;
     if (h >= m) return;
-    double* v = fs + size_t(w) * nb;
-    for (int t = 0; t < T; ++t) {
-        for (int b = lane; b < nb; b += 32) {
-            const int r = t2r[int64_t(b) * m + h];
-            v[b] = r >= 0 ? root[int64_t(t) * Hr + boff[b] + r] : __longlong_as_double((long long)kSkipBits);
-        }
-        __syncwarp();
-        if (lane == 0) {
+    double* v = fs + size_t(w) * size_t(T) * nb;
+    // every continuation's values staged at once (one load latency), then
+    // folded continuation by continuation in order
+    for (int b = lane; b < nb; b += 32) {
+        const int r = t2r[int64_t(b) * m + h];
+        for (int t = 0; t < T; ++t)
+            v[t * nb + b] = r >= 0 ? root[int64_t(t) * Hr + boff[b] + r] : __longlong_as_double((long long)kSkipBits);
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (int t = 0; t < T; ++t) {
             double acc = 0.0;
             for (int b = 0; b < nb; ++b) {
-                const double x = v[b];
+                const double x = v[t * nb + b];
                 if (uint64_t(__double_as_longlong(x)) != kSkipBits) acc += x;
             }
             extra[int64_t(h) * nt + sigma[t] - 1] += acc;
         }
-        __syncwarp();
-    }
 }
 
 __global__ void k_river_scale(double* __restrict__ x, double* __restrict__ avg, const double* __restrict__ xturn,
@@ -1999,7 +2000,8 @@ bool turn_fuse() {
 void gather_all(kr_turn_solver* s, int p, int nt, cudaStream_t st) {
     if (!s->comm && !s->xfn) {   // one rank: fold straight from the root values
         krb::launch(k_turn_fold_direct, unsigned((s->m + kFoldWarps - 1) / kFoldWarps), 32 * kFoldWarps,
-                    size_t(kFoldWarps) * size_t(s->nb) * sizeof(double), st, s->root, s->Hr, s->d_t2r, s->d_boff,
+                    size_t(kFoldWarps) * size_t(s->T) * size_t(s->nb) * sizeof(double), st, s->root, s->Hr, s->d_t2r,
+                    s->d_boff,
                     s->nb, s->T, s->m, nt, s->d_sigma + p * s->T, s->extra);
         KR_CK_LAUNCH();
         s->launches++;
