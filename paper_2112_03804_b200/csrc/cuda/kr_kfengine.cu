@@ -1206,20 +1206,25 @@ kr_engine* create_kf_engine(const kr_kron_board* boards, int nb, int device, uin
         raise_smem_limit(k_kf_seqmajor, size_t(32) * std::max(n1, n2) * sizeof(double));
         k.hOff1.push_back(k.M1);
         k.hOff2.push_back(k.M2);
-        // CTAs per sequence: one slice per warp, or up to four rounds of
-        // slices per CTA when the grid would exceed ~6 waves (fewer CTAs
-        // stage the same input columns); slices spread evenly (kf_range)
-        auto ctas = [&](int slices, int seqs) {
+        // CTAs per sequence: one slice per warp, or several rounds of slices
+        // per CTA when the grid would exceed ~6 waves (fewer CTAs stage the
+        // same input columns); slices spread evenly (kf_range).  Rounds
+        // capped at 8 for the A x row kernels and 2 for A^T y's (config 3,
+        // one box: A x 310 -> 306 us from 4 to 8, A^T y 351 -> 347 from 4 to
+        // 2; KR_KF_ROUNDS_A / KR_KF_ROUNDS_T override)
+        auto ctas = [&](int slices, int seqs, const char* env, int capDefault) {
             const int base = (slices + kKfWarps - 1) / kKfWarps;
             const int64_t total = int64_t(base) * seqs * nb;
-            const int rounds = int(std::min<int64_t>(4, std::max<int64_t>(1, total / (6 * 148))));
+            const char* re = std::getenv(env);
+            const int64_t cap = re ? std::max(1, std::atoi(re)) : capDefault;
+            const int rounds = int(std::min<int64_t>(cap, std::max<int64_t>(1, total / (6 * 148))));
             return std::max(1, (slices + kKfWarps * rounds - 1) / (kKfWarps * rounds));
         };
-        k.gs = slY > 0 ? ctas(slY, n1) : 0;
+        k.gs = slY > 0 ? ctas(slY, n1, "KR_KF_ROUNDS_A", 8) : 0;
         k.gy = k.gs + (anyLong ? 1 : 0);
         if (k.gy == 0) k.gy = 1;
-        k.gu = ctas(slB2, n1);
-        k.gv = ctas(slB1, n2);
+        k.gu = ctas(slB2, n1, "KR_KF_ROUNDS_A", 8);
+        k.gv = ctas(slB1, n2, "KR_KF_ROUNDS_T", 2);
         for (int d = 0; d < 2; ++d) {
             k.inT[d] = dev_alloc<double>(std::max<int64_t>(d == 0 ? C : R, 1));
             k.keep.push_back(k.inT[d]);

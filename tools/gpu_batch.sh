@@ -1,1 +1,3 @@
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 100 --csv python tools/_c1_probe.py 2>/dev/null | grep -E "gpu__time" | awk -F'","' '{print $5, $NF}' | sed 's/(.*)//; s/"//g' | awk '{n=split($0,a," "); v=a[n]; k=""; for(i=1;i<n;i++) k=k" "a[i]; s[k]+=v; c[k]++} END {for (k in s) printf "%8.1f us  %3d  %s\n", s[k]/1000, c[k], k}' | sort -rn | head -16
+timeout 900 python -m pytest tests/test_gpu_kfengine.py -q -p no:cacheprovider 2>&1 | tail -1
+for cfg in "KR_KF_ROUNDS_A=4 KR_KF_ROUNDS_T=4" "X=1" "KR_KF_ROUNDS_A=4 KR_KF_ROUNDS_T=4" "X=1"; do env $cfg timeout 600 python tools/kf_probe.py 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$cfg config3', d['kf_ax_us'], d['kf_atx_us'], d['kf_pair_us'])"; done
+for cfg in "KR_KF_ROUNDS_A=4 KR_KF_ROUNDS_T=4" "X=1"; do env $cfg timeout 300 python tools/solver_probe.py kfactored 300 2>&1 | tail -1 | sed "s/^/[$cfg] /"; done
