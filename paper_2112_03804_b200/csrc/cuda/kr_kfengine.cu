@@ -62,7 +62,10 @@ namespace krb {
 
 namespace {
 
-constexpr int kKfWarps = 8;         // warps (SELL slices) per row-kernel CTA
+#ifndef KR_KF_WARPS
+#define KR_KF_WARPS 8
+#endif
+constexpr int kKfWarps = KR_KF_WARPS;   // warps (SELL slices) per row-kernel CTA
 constexpr int kKfMaxSeq = 1024;     // F / S CSR rows and columns
 constexpr int kKfMaxHands = 1364;   // list entries address up to 48 (m + 1) bytes of shared memory (< 64 KB)
 constexpr int kKfLong = 256;        // longer list rows take the warp-cooperative path
