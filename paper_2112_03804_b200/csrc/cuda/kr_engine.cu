@@ -27,7 +27,11 @@
 #include <thread>
 #include <unordered_map>
 
+#include <cooperative_groups.h>
+
 #include "kr_common.cuh"
+
+namespace cg = cooperative_groups;
 
 #ifdef KR_CHECKED
 namespace krb {
@@ -140,10 +144,16 @@ constexpr int kChunk = 256;  // long-row entries staged per warp
 #endif
 constexpr int kU = KR_KU;  // entries per lane per pipeline stage
 
-template <bool TWO>
+// COH: the source was written earlier in the same kernel (the fused small-
+// engine product): coherent L2 loads instead of the read-only path.
+template <bool TWO, bool COH = false>
 __device__ __forceinline__ double gather(const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
                                          int32_t c) {
     KR_DCHECK(c >= 0);
+    if (COH) {
+        if (TWO) return c < split ? __ldcg(xa + c) : __ldcg(xb + (c - split));
+        return __ldcg(xa + c);
+    }
     if (TWO) return c < split ? __ldg(xa + c) : __ldg(xb + (c - split));
     return __ldg(xa + c);
 }
@@ -151,12 +161,22 @@ __device__ __forceinline__ double gather(const double* __restrict__ xa, const do
 // One long row per warp (the 32 lanes load and multiply a chunk of kChunk
 // entries, lane 0 adds the chunk's products in storage order while the next
 // chunk's loads are in flight).  Shared by the plain and compressed kernels.
+template <bool TWO, bool COH = false>
+__device__ __forceinline__ void spmv_long_row_at(const SellView& A, const double* __restrict__ xa,
+                                                 const double* __restrict__ xb, int32_t split, double* __restrict__ y,
+                                                 double* P, int lane, int64_t r);
 template <bool TWO>
 __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* __restrict__ xa,
                                               const double* __restrict__ xb, int32_t split, double* __restrict__ y,
                                               double* P, int lane, int w) {
     const int64_t r = int64_t(blockIdx.x) * kWarpsPerBlock + w;
     if (r >= A.nlong) return;
+    spmv_long_row_at<TWO>(A, xa, xb, split, y, P, lane, r);
+}
+template <bool TWO, bool COH>
+__device__ __forceinline__ void spmv_long_row_at(const SellView& A, const double* __restrict__ xa,
+                                                 const double* __restrict__ xb, int32_t split, double* __restrict__ y,
+                                                 double* P, int lane, int64_t r) {
     const int64_t e0 = A.long_ptr[r], e1 = A.long_ptr[r + 1];
     double acc = 0.0;
     constexpr int per = kChunk / 32;
@@ -176,7 +196,7 @@ __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* _
         for (int u = 0; u < per; ++u)
             if (u * 32 + lane < n) {
                 KR_DCHECK(c[u] < A.nsrc);
-                p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+                p[u] = v[u] * gather<TWO, COH>(xa, xb, split, c[u]);
             }
     }
     for (int64_t t0 = e0; t0 < e1; t0 += kChunk) {
@@ -210,7 +230,7 @@ __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* _
         for (int u = 0; u < per; ++u)
             if (u * 32 + lane < nn) {
                 KR_DCHECK(c[u] < A.nsrc);
-                p[u] = v[u] * gather<TWO>(xa, xb, split, c[u]);
+                p[u] = v[u] * gather<TWO, COH>(xa, xb, split, c[u]);
             }
         __syncwarp();
         n = nn;
@@ -230,6 +250,11 @@ __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* _
 // blocks; matrices whose SELL rows hold at most one entry (U^T of Technique
 // B: one entry per k position) use <1, 8>, a lean variant with twice
 // the resident warps, since their cost is the per-row load latency.
+template <bool TWO, int KU, bool COH = false>
+__device__ __forceinline__ void spmv_slice(const SellView& A, const double* __restrict__ xa,
+                                           const double* __restrict__ xb, int32_t split, double* __restrict__ y,
+                                           int64_t si, int lane);
+
 template <bool TWO, int KU = kU, int MINB = 1>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
     k_spmv(SellView A, const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
@@ -245,6 +270,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
     }
     const int64_t si = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
     if (si >= A.nslices) return;
+    spmv_slice<TWO, KU>(A, xa, xb, split, y, si, lane);
+}
+
+// One SELL slice (32 rows) by one warp: each lane's row summed in storage
+// order, KU entries per pipeline stage.
+template <bool TWO, int KU, bool COH>
+__device__ __forceinline__ void spmv_slice(const SellView& A, const double* __restrict__ xa,
+                                           const double* __restrict__ xb, int32_t split, double* __restrict__ y,
+                                           int64_t si, int lane) {
     // widest slices first: a slice's latency grows with its width, so the
     // widest ones must not be the last dispatched (they would set the tail)
     const int64_t s = A.order ? int64_t(A.order[si]) : si;
@@ -290,7 +324,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
         for (int u = 0; u < KU; ++u)
             if (j + u < len) {
                 KR_DCHECK(c[u] < A.nsrc);
-                x[u] = gather<TWO>(xa, xb, split, c[u]);
+                x[u] = gather<TWO, COH>(xa, xb, split, c[u]);
             }
 #pragma unroll
         for (int u = 0; u < KU; ++u)
@@ -468,18 +502,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // the register kernels above.
 // Dynamic shared memory: kStages chunks of t (and of the multipliers when
 // the engine has any chain whose multipliers are not all -1: withMul).
-template <int DIR>
-__global__ void __launch_bounds__(32)
-    k_chain_tma(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
-                const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int withMul,
-                double* __restrict__ z, int64_t s0) {
-    krb::pdl_entry();
-    extern __shared__ __align__(128) double dsm[];
-    __shared__ __align__(8) uint64_t bar[kStages];
-    double(*Tb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm);
-    double(*Mb)[kChunkRows * 32] = reinterpret_cast<double(*)[kChunkRows * 32]>(dsm + kStages * kChunkRows * 32);
-    const int lane = threadIdx.x;
-    const int64_t s = s0 + blockIdx.x;
+// One chain slice by one warp: ROWS rows per chunk, a STAGES-deep ring
+// (Tb / Mb: STAGES chunks each, bar: STAGES mbarriers initialised with count
+// 1).  ring: the warp's running chunk count, so a warp can run several slices
+// through one ring without re-initialising its barriers.
+template <int DIR, int ROWS, int STAGES>
+__device__ __forceinline__ void chain_tma_slice(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                                                const double* __restrict__ cmul, const uint8_t* __restrict__ neg1,
+                                                int withMul, double* __restrict__ z, int64_t s, int lane,
+                                                double (*Tb)[ROWS * 32], double (*Mb)[ROWS * 32], uint64_t* bar,
+                                                uint32_t& ring) {
+    constexpr int kChunkRows = ROWS, kStages = STAGES;
     const int64_t b0 = sbase[s];
     const int32_t width = int32_t((sbase[s + 1] - b0) / 32);
     const int32_t len = slen[s * 32 + lane];
@@ -487,11 +520,6 @@ __global__ void __launch_bounds__(32)
     const bool needMul = withMul && __any_sync(0xffffffffu, !allneg);
     const int nChunks = (width + kChunkRows - 1) / kChunkRows;
     KR_DCHECK(len >= 0 && len <= width && (sbase[s + 1] - b0) % 32 == 0);
-    KR_SMEM_CHECK(0, size_t(kStages) * kChunkRows * 32 * 8 * (needMul ? 2 : 1));
-    if (lane == 0)
-        for (int q = 0; q < kStages; ++q) mbar_init(&bar[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
     // chunk c covers rows [r0, r0 + n); forward chunks ascend, backward descend
     auto chunk_rows = [&](int c, int32_t& r0, int32_t& n) {
         if (DIR > 0) {
@@ -507,7 +535,7 @@ __global__ void __launch_bounds__(32)
         if (lane == 0 && c < nChunks) {
             int32_t r0, n;
             chunk_rows(c, r0, n);
-            const int st = c % kStages;
+            const int st = (ring + uint32_t(c)) % kStages;
             const uint32_t bytes = uint32_t(n) * 32 * 8;
             KR_DCHECK(n > 0 && n <= kChunkRows && r0 >= 0 && r0 + n <= width);
             mbar_expect_tx(&bar[st], needMul ? 2 * bytes : bytes);
@@ -519,8 +547,9 @@ __global__ void __launch_bounds__(32)
     double carry = needMul ? 0.0 : -0.0, mulNext = 0.0;
     for (int c = 0; c < nChunks; ++c) {
         issue(c + kStages - 1);
-        const int st = c % kStages;
-        mbar_wait(&bar[st], uint32_t((c / kStages) & 1));
+        const uint32_t gc = ring + uint32_t(c);
+        const int st = gc % kStages;
+        mbar_wait(&bar[st], (gc / kStages) & 1);
         int32_t r0, n;
         chunk_rows(c, r0, n);
         const double* T = Tb[st];
@@ -622,6 +651,28 @@ __global__ void __launch_bounds__(32)
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    ring += uint32_t(nChunks);
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(32)
+    k_chain_tma(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int withMul,
+                double* __restrict__ z, int64_t s0) {
+    krb::pdl_entry();
+    extern __shared__ __align__(128) double dsm[];
+    __shared__ __align__(8) uint64_t bar[kStages];
+    KR_SMEM_CHECK(0, size_t(kStages) * kChunkRows * 32 * 8 * (withMul ? 2 : 1));
+    const int lane = threadIdx.x;
+    if (lane == 0)
+        for (int q = 0; q < kStages; ++q) mbar_init(&bar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t ring = 0;
+    chain_tma_slice<DIR, kChunkRows, kStages>(
+        sbase, slen, cmul, neg1, withMul, z, s0 + blockIdx.x, lane,
+        reinterpret_cast<double(*)[kChunkRows * 32]>(dsm),
+        reinterpret_cast<double(*)[kChunkRows * 32]>(dsm + kStages * kChunkRows * 32), bar, ring);
 }
 
 // Forward solve M z = t along chains (engine.hpp:31-41 restricted to <=1
@@ -632,14 +683,9 @@ __global__ void __launch_bounds__(32)
 //   z_p = (z_{p-1} != 0) ? t_p - M(p,p-1) z_{p-1} : t_p
 // (for M(p,p-1) == -1 this is bitwise t_p + z_{p-1}: one dependent add).
 // The next stage's loads are issued before the current stage's adds.
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    k_chain_forward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
-                    const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
-                    double* __restrict__ z) {
-    krb::pdl_entry();
-    const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (s >= s1) return;
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void chain_forward_slice(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                                                    const double* __restrict__ cmul, const uint8_t* __restrict__ neg1,
+                                                    int64_t s, double* __restrict__ z, int lane) {
     const int32_t len = slen[s * 32 + lane];
     const bool allneg = neg1[s * 32 + lane] != 0;
     double* zc = z + sbase[s] + lane;
@@ -682,14 +728,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 
 // Backward solve M^T z = s along chains (engine.hpp:44-54), same layout,
 // each lane walking its chain in reverse: z_p = s_p - (0 + M(p+1,p) z_{p+1}).
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    k_chain_backward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
-                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
-                     double* __restrict__ z) {
-    krb::pdl_entry();
-    const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (s >= s1) return;
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void chain_backward_slice(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                                                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1,
+                                                     int64_t s, double* __restrict__ z, int lane) {
     const int32_t len = slen[s * 32 + lane];
     const bool allneg = neg1[s * 32 + lane] != 0;
     double* zc = z + sbase[s] + lane;
@@ -732,6 +773,92 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
             t[u] = tn[u];
             m[u] = mn[u];
         }
+    }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_chain_forward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                    const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
+                    double* __restrict__ z) {
+    krb::pdl_entry();
+    const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s < s1) chain_forward_slice(sbase, slen, cmul, neg1, s, z, threadIdx.x & 31);
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_chain_backward(const int64_t* __restrict__ sbase, const int32_t* __restrict__ slen,
+                     const double* __restrict__ cmul, const uint8_t* __restrict__ neg1, int64_t s0, int64_t s1,
+                     double* __restrict__ z) {
+    krb::pdl_entry();
+    const int64_t s = s0 + int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (s < s1) chain_backward_slice(sbase, slen, cmul, neg1, s, z, threadIdx.x & 31);
+}
+
+// The whole product of a small engine in one launch: a
+// cluster of CTAs runs the three stages the separate launches run -- the
+// input-side SpMV (V^T x or U^T y) into tz, the M solve along the chains in
+// place, the output-side SpMV ([U | Ahat] or [Ahat^T | V]) -- with a cluster
+// barrier (release / acquire) between stages, each warp taking rows, slices
+// and chain slices strided over the cluster's warps.  Every row, slice and
+// chain runs the same device code as the separate kernels, so the result is
+// bitwise theirs; the last stage reads tz through coherent L2 loads (it was
+// written inside this launch).  For engines whose three launches are
+// latency-bound (a few us of work each), this takes two launch gaps and two
+// grid drains off every product.
+constexpr int kTinyWarps = 8;
+struct TinyChains {
+    const int64_t* sbase;
+    const int32_t* slen;
+    const double* cmul;
+    const uint8_t* neg1;
+    int64_t n;    // chain slices (0: M = I)
+    int withMul;  // some chain has a multiplier other than -1
+};
+// chain stage: each warp streams its slices through a TMA ring of
+// kTinyStages chunks of kTinyRows rows (t, and the multipliers withMul)
+constexpr int kTinyRows = 16, kTinyStages = 3;
+constexpr size_t kTinyRing = size_t(kTinyStages) * kTinyRows * 32;  // doubles per array per warp
+template <int DIR>
+__global__ void __launch_bounds__(32 * kTinyWarps, 1)
+    k_tiny_product(SellView A1, SellView A2, TinyChains C, const double* __restrict__ in, double* __restrict__ tz,
+                   int32_t split, double* __restrict__ out) {
+    krb::pdl_entry();
+    __shared__ double P[kTinyWarps][kChunk];
+    __shared__ __align__(8) uint64_t bar[kTinyWarps][kTinyStages];
+    extern __shared__ __align__(128) double ring[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0)
+        for (int q = 0; q < kTinyStages; ++q) mbar_init(&bar[w][q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const int64_t nw = int64_t(cl.num_blocks()) * kTinyWarps;
+    const int64_t gw = int64_t(cl.block_rank()) * kTinyWarps + w;
+    for (int64_t i = gw; i < A1.nlong + A1.nslices; i += nw) {
+        if (i < A1.nlong) spmv_long_row_at<false>(A1, in, nullptr, 0, tz, P[w], lane, i);
+        else spmv_slice<false, kU>(A1, in, nullptr, 0, tz, i - A1.nlong, lane);
+    }
+    cl.sync();
+    if (C.n) {
+        // stage 1's stores (ordered before this point by the cluster
+        // barrier) before the bulk copies read them through the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        KR_SMEM_CHECK(0, kTinyWarps * kTinyRing * 8 * (C.withMul ? 2 : 1));
+        double* Tb = ring + size_t(w) * kTinyRing * (C.withMul ? 2 : 1);
+        uint32_t used = 0;
+        for (int64_t i = gw; i < C.n; i += nw)
+            chain_tma_slice<DIR == 0 ? 1 : -1, kTinyRows, kTinyStages>(
+                C.sbase, C.slen, C.cmul, C.neg1, C.withMul, tz, i, lane,
+                reinterpret_cast<double(*)[kTinyRows * 32]>(Tb),
+                reinterpret_cast<double(*)[kTinyRows * 32]>(Tb + kTinyRing), bar[w], used);
+        cl.sync();
+    }
+    // [U | Ahat] over [tz | x]; [Ahat^T | V] over [y | tz]
+    const double* xa = DIR == 0 ? tz : in;
+    const double* xb = DIR == 0 ? in : tz;
+    for (int64_t i = gw; i < A2.nlong + A2.nslices; i += nw) {
+        if (i < A2.nlong) spmv_long_row_at<true, true>(A2, xa, xb, split, out, P[w], lane, i);
+        else spmv_slice<true, kU, true>(A2, xa, xb, split, out, i - A2.nlong, lane);
     }
 }
 
@@ -2014,6 +2141,93 @@ void last_stage(kr_engine* e, int dir, const double* in, double* out, cudaStream
     else launch_sell(e, 3, e->AV, in, e->d_tz2, e->rows, out, s, b0, b1);          // x = Ahat^T y + V z
 }
 
+// Cluster size of the fused small-engine product (k_tiny_product), 0 = the
+// three launches.  Measured (profiles/r02/tiny_product_r02z.log): a product
+// launched on a stream runs ~1.5-2x faster fused on the smallest engines (its
+// three launches are each a launch latency), but inside a CUDA graph the
+// three kernel nodes with programmatic dependent launch cost the same or less
+// (twenty_card: 14.0 us three nodes, 16.5 us fused), so captured products --
+// the solver's iterations, the host API's replayed graphs -- keep the three
+// launches.  KR_TINY: the largest product (stored entries of the two SpMV
+// stages + the chain positions) launched fused, everywhere including
+// captures (0 = never; default 16384, outside captures only);
+// KR_TINY_CLUSTER: CTAs per cluster (1 to 16, default 8).  Engines with
+// per-stage timing, a sequence-major x, compressed slots or level-scheduled
+// M keep the separate launches.
+int tiny_cluster(const kr_engine* e, int dir, cudaStream_t s) {
+    if (e->kron || e->kf || e->xseq || e->mkind > 1 || e->timing) return 0;
+    const krb::DevSell& A1 = dir == 0 ? e->VT : e->UT;
+    const krb::DevSell& A2 = dir == 0 ? e->UA : e->AV;
+    if (A1.comp || A2.comp) return 0;
+    // read per product (tens of ns against a launch), so a process can switch
+    const char* env = std::getenv("KR_TINY");
+    const int64_t lim = env ? std::atoll(env) : int64_t(16384);
+    const int64_t nnz = e->nnzA + e->nnzU + e->nnzV + (e->mkind == 1 ? e->kpad : 0);
+    if (nnz > lim) return 0;
+    if (!env) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        KR_CK(cudaStreamIsCapturing(s, &cs));
+        if (cs != cudaStreamCaptureStatusNone) return 0;
+    }
+    env = std::getenv("KR_TINY_CLUSTER");
+    return env ? std::max(1, std::min(16, std::atoi(env))) : 8;
+}
+
+template <int DIR>
+void launch_tiny(kr_engine* e, int cl, const double* in, double* out, cudaStream_t s) {
+    const krb::DevSell& A1 = DIR == 0 ? e->VT : e->UT;
+    const krb::DevSell& A2 = DIR == 0 ? e->UA : e->AV;
+    const int64_t n1 = DIR == 0 ? e->cols : e->rows, n2 = DIR == 0 ? e->rows : e->cols;
+    const int64_t src2 = DIR == 0 ? e->kpad + e->cols : e->rows + e->kpad;
+    SellView v1{A1.slice_ptr, A1.lane_row, A1.lane_len, A1.col, A1.val, A1.nslices, A1.long_ptr, A1.long_row,
+                A1.long_col, A1.long_val, A1.nlong, A1.order_all, e->pf, n1, e->kpad};
+    SellView v2{A2.slice_ptr, A2.lane_row, A2.lane_len, A2.col, A2.val, A2.nslices, A2.long_ptr, A2.long_row,
+                A2.long_col, A2.long_val, A2.nlong, A2.order_all, e->pf, src2, n2};
+    const TinyChains C{e->chain_ptr, e->chain_len, e->chain_mul, e->chain_neg1, e->mkind == 1 ? e->nchains : 0,
+                       e->chain_withmul};
+    const size_t smem = C.n ? size_t(kTinyWarps) * kTinyRing * 8 * (C.withMul ? 2 : 1) : 0;
+    double* tz = DIR == 0 ? e->d_tz : e->d_tz2;
+    const int32_t split = int32_t(DIR == 0 ? e->kpad : e->rows);
+    static bool attr = [] {
+        KR_CK(cudaFuncSetAttribute(k_tiny_product<DIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        krb::raise_smem_limit(k_tiny_product<DIR>, size_t(kTinyWarps) * kTinyRing * 8 * 2);
+        return true;
+    }();
+    (void)attr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(cl));
+    cfg.blockDim = dim3(32 * kTinyWarps);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(cl);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    unsigned& prev = krb::last_grid(s);
+    cfg.numAttrs = krb::pdl_enabled(unsigned(cl), prev, false) ? 2 : 1;
+    prev = unsigned(cl);
+    KR_CK(cudaLaunchKernelEx(&cfg, k_tiny_product<DIR>, v1, v2, C, in, tz, split, out));
+    KR_CK_LAUNCH();
+    e->launches++;
+}
+
+// The whole product, fused when the engine is small (tiny_cluster), else the
+// three stages.
+void product_stages(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
+    if (const int cl = tiny_cluster(e, dir, s)) {
+        if (dir == 0) launch_tiny<0>(e, cl, in, out, s);
+        else launch_tiny<1>(e, cl, in, out, s);
+        return;
+    }
+    first_stage(e, dir, in, s);
+    middle(e, dir, s);
+    last_stage(e, dir, in, out, s);
+}
+
 void account(kr_engine* e, int dir) {
     e->flops_last = e->kron ? kron_flops(e, dir) : e->flops_per_product;
     e->flops_total += e->flops_last;
@@ -2023,9 +2237,7 @@ void account(kr_engine* e, int dir) {
 
 void engine_product(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
     if (e->mkind == 3) throw Fail{KR_CONTRACT, e->mfail};
-    first_stage(e, dir, in, s);
-    middle(e, dir, s);
-    last_stage(e, dir, in, out, s);
+    product_stages(e, dir, in, out, s);
     account(e, dir);
 }
 
@@ -2176,9 +2388,7 @@ void enqueue_direction(kr_engine* e, int dir, const double* hin, double* hout, c
     const int64_t nin = dir == 0 ? e->cols : e->rows, nout = dir == 0 ? e->rows : e->cols;
     if (e->ngroups() < 2) {
         KR_CK(cudaMemcpyAsync(P.d_in, hin, 8 * size_t(nin), cudaMemcpyHostToDevice, P.main));
-        first_stage(e, dir, P.d_in, P.main);   // the stages of engine_product; the caller accounts
-        middle(e, dir, P.main);
-        last_stage(e, dir, P.d_in, P.d_out, P.main);
+        product_stages(e, dir, P.d_in, P.d_out, P.main);   // engine_product's; the caller accounts
         KR_CK(cudaMemcpyAsync(hout, P.d_out, 8 * size_t(nout), cudaMemcpyDeviceToHost, P.main));
         return;
     }
