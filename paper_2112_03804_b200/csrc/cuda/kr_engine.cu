@@ -1910,6 +1910,23 @@ cudaEvent_t pool_event(kr_engine* e) {
 
 // Boards [b0, b1) only when b1 >= 0 (a board's slices and long rows are
 // contiguous: SELL windows never straddle boards); untimed.
+// Deep batches (2 kU entries per lane per pipeline stage) for a launch of
+// `blocks` CTAs over rows of up to maxLen entries.  In a small grid every
+// SELL lane's row is a chain of dependent gather batches (each waits on L2),
+// so fewer, wider batches shorten it; large grids are bandwidth-bound and keep
+// kU (the registers buy residency).  Measured (profiles/r02/deep_batches_r02z.log):
+// config-1 CFR+ 13,984 -> 15,100 it/s, config-2 factored DCFR 7,171 -> 7,712,
+// config-4 DCFR 14,037 -> 15,357; 12 or 24 entries measured no better, 32
+// spills.  KR_DEEP_KU=0: off; KR_DEEP_BLOCKS: the largest grid (default 8
+// CTAs per SM).  Read per launch, so a process can switch.
+bool deep_batches(int64_t blocks, int32_t maxLen) {
+    const char* env = std::getenv("KR_DEEP_KU");
+    if (env && std::atoi(env) == 0) return false;
+    if (maxLen <= kU) return false;
+    env = std::getenv("KR_DEEP_BLOCKS");
+    return blocks <= (env ? std::atoll(env) : int64_t(1184));
+}
+
 void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* xa, const double* xb, int64_t split,
                  double* y, cudaStream_t s, int b0 = 0, int b1 = -1) {
     int64_t s0 = 0, s1 = A.nslices, l0 = 0, l1 = A.nlong;
@@ -1947,9 +1964,14 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
         else if (A.codedSeg == 0)
             krb::launch(k_spmvc<true, 0>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
         else krb::launch(k_spmvc<true, 1>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
-    } else if (xb) krb::launch(k_spmv<true>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, xb, int32_t(split), y);
-    else if (A.maxLen <= 1 && e->lean)
+    } else if (A.maxLen <= 1 && e->lean && !xb)
         krb::launch(k_spmv<false, 1, 8>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, nullptr, 0, y);
+    else if (deep_batches(blocks, A.maxLen)) {
+        // small grids: each lane's row is a chain of dependent gather
+        // batches, so twice the entries per batch halves it (same order)
+        if (xb) krb::launch(k_spmv<true, 2 * kU>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, xb, int32_t(split), y);
+        else krb::launch(k_spmv<false, 2 * kU>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, nullptr, 0, y);
+    } else if (xb) krb::launch(k_spmv<true>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, xb, int32_t(split), y);
     else krb::launch(k_spmv<false>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, nullptr, 0, y);
     KR_CK_LAUNCH();
     if (timed) {

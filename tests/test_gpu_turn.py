@@ -47,10 +47,10 @@ def test_turn_dcfr_matches_checker(game):
     assert r["iterations"] == 6
     ob1 = np.array([b for _, b, _, _ in trace])
     ob2 = np.array([b for _, _, b, _ in trace])
-    np.testing.assert_allclose(r["trace_br1"], ob1, rtol=1e-9)
-    np.testing.assert_allclose(r["trace_br2"], ob2, rtol=1e-9)
-    np.testing.assert_allclose(r["trace_expl"], [e for *_, e in trace], rtol=1e-9)
-    assert normwise(r["avg1"], a1) <= 1e-9 and normwise(r["avg2"], a2) <= 1e-9
+    np.testing.assert_allclose(r["trace_br1"], ob1, rtol=1e-12)
+    np.testing.assert_allclose(r["trace_br2"], ob2, rtol=1e-12)
+    np.testing.assert_allclose(r["trace_expl"], [e for *_, e in trace], rtol=1e-12)
+    assert normwise(r["avg1"], a1) <= 1e-12 and normwise(r["avg2"], a2) <= 1e-12
 
 
 @pytest.mark.parametrize("rule", [1, 2], ids=["cfr+", "prm+"])
@@ -63,9 +63,9 @@ def test_turn_rules_match_checker(game, rule):
     trace, (a1, a2) = o.dcfr(6, alpha=inf, beta=-inf, gamma=1.0, checkpoint_every=1, rule=rule)
     r = TurnSolver(game).run(max_iters=6, checkpoint_every=1, alpha=inf, beta=-inf, gamma=1.0,
                              want_avg=True, rule=rule)
-    np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-9)
-    np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-9)
-    assert normwise(r["avg1"], a1) <= 1e-9 and normwise(r["avg2"], a2) <= 1e-9
+    np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-12)
+    np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-12)
+    assert normwise(r["avg1"], a1) <= 1e-12 and normwise(r["avg2"], a2) <= 1e-12
     long = TurnSolver(game).run(max_iters=200, checkpoint_every=50, alpha=inf, beta=-inf, gamma=1.0, rule=rule)
     e = long["trace_expl"]  # CFR+ / PRM+ on this game: ~13% of the start after 200
     assert e[-1] < 0.25 * e[0] and np.all(np.diff(e) < 0)
@@ -135,8 +135,8 @@ def test_turn_with_raises_and_all_in():
     o = TO.TurnOracle(g)
     trace, _ = o.dcfr(4, checkpoint_every=1)
     r = TurnSolver(g).run(max_iters=4, checkpoint_every=1)
-    np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-9)
-    np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-9)
+    np.testing.assert_allclose(r["trace_br1"], [b for _, b, _, _ in trace], rtol=1e-12)
+    np.testing.assert_allclose(r["trace_br2"], [b for _, _, b, _ in trace], rtol=1e-12)
 
 
 def test_52_card_turn_blocks_match_checker():

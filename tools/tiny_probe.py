@@ -1,6 +1,8 @@
-"""The fused small-engine product (k_tiny_product) against the three launches:
-config-1 CFR+ iterations/s (twenty_card, checkpointEvery = 1), config-4 and
-a few corpus engines' pair times, per KR_TINY / KR_TINY_CLUSTER setting.
+"""Small-engine product settings (the fused product k_tiny_product, the
+deep-batch SELL kernels): config-1 CFR+ iterations/s (twenty_card,
+checkpointEvery = 1), config-2 / config-4 and a few corpus engines' pair and
+product times and DCFR it/s, per environment setting (default: the KR_TINY /
+KR_TINY_CLUSTER sweep; argv[1]: a JSON list of [label, env] pairs).
 Each setting runs in its own process (the engine reads the knobs per
 product, but the solver's captured graph keeps the launches it captured)."""
 import json
@@ -82,6 +84,14 @@ for name, kw in [("twenty_card", {}), ("bench", dict(seed=2, hands=100)), ("gold
         sv.run(DcfrParams(max_iters=5, checkpoint_every=1))
         r = sv.run(DcfrParams(max_iters=1000, checkpoint_every=1))
         out[name + "_dcfr_its_ck1"] = r.iterations / r.seconds
+inst2 = H.builtin("river_full", seed=1, board="Ks7d4c2h9s", tree=3)
+e2 = CudaEngine(inst2.sparsify("b", True))
+out["config2_factored_pair_us"] = pair_us(e2, reps=500)
+out["config2_factored_ax_atx_us"] = dir_us(e2, reps=500)
+s2 = solver_for([(inst2, inst2.sparsify("b", True))])
+s2.run(DcfrParams(max_iters=5, checkpoint_every=50))
+r = s2.run(DcfrParams(max_iters=400, checkpoint_every=50))
+out["config2_factored_dcfr_its"] = r.iterations / r.seconds
 inst4 = H.builtin("river_full", seed=1, board="Kc9d7c4d2c", deck=26, tree=3)
 s4 = solver_for([(inst4, inst4.sparsify("b", True))])
 s4.run(DcfrParams(max_iters=5, checkpoint_every=50))
@@ -102,6 +112,10 @@ def run(env):
 
 
 def main():
+    if len(sys.argv) > 1:   # JSON list of [label, env] pairs
+        for label, env in json.loads(sys.argv[1]):
+            print(json.dumps({"setting": label, "env": env, **run(env)}), flush=True)
+        return
     settings = [("three launches", {"KR_TINY": "0"}),
                 ("fused, default size", {}),
                 ("fused, all engines, default size", {"KR_TINY": "1000000000"})]
