@@ -2195,8 +2195,10 @@ int tiny_cluster(const kr_engine* e, int dir, cudaStream_t s) {
     return env ? std::max(1, std::min(16, std::atoi(env))) : 8;
 }
 
+// false when the device cannot co-schedule a cluster of that shape (a
+// partitioned GPU, too few SMs per GPC): the caller keeps the three launches.
 template <int DIR>
-void launch_tiny(kr_engine* e, int cl, const double* in, double* out, cudaStream_t s) {
+bool launch_tiny(kr_engine* e, int cl, const double* in, double* out, cudaStream_t s) {
     const krb::DevSell& A1 = DIR == 0 ? e->VT : e->UT;
     const krb::DevSell& A2 = DIR == 0 ? e->UA : e->AV;
     const int64_t n1 = DIR == 0 ? e->cols : e->rows, n2 = DIR == 0 ? e->rows : e->cols;
@@ -2229,22 +2231,35 @@ void launch_tiny(kr_engine* e, int cl, const double* in, double* out, cudaStream
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
+    {
+        static std::mutex mu;
+        static std::unordered_map<int64_t, bool> fits;  // (device, cluster, smem) -> schedulable
+        const int64_t key = (int64_t(e->device) << 40) | (int64_t(cl) << 32) | int64_t(smem);
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = fits.find(key);
+        if (it == fits.end()) {
+            cfg.numAttrs = 1;
+            int n = 0;
+            const bool ok = cudaOccupancyMaxActiveClusters(&n, k_tiny_product<DIR>, &cfg) == cudaSuccess && n > 0;
+            (void)cudaGetLastError();
+            it = fits.emplace(key, ok).first;
+        }
+        if (!it->second) return false;
+    }
     unsigned& prev = krb::last_grid(s);
     cfg.numAttrs = krb::pdl_enabled(unsigned(cl), prev, false) ? 2 : 1;
     prev = unsigned(cl);
     KR_CK(cudaLaunchKernelEx(&cfg, k_tiny_product<DIR>, v1, v2, C, in, tz, split, out));
     KR_CK_LAUNCH();
     e->launches++;
+    return true;
 }
 
 // The whole product, fused when the engine is small (tiny_cluster), else the
 // three stages.
 void product_stages(kr_engine* e, int dir, const double* in, double* out, cudaStream_t s) {
-    if (const int cl = tiny_cluster(e, dir, s)) {
-        if (dir == 0) launch_tiny<0>(e, cl, in, out, s);
-        else launch_tiny<1>(e, cl, in, out, s);
-        return;
-    }
+    if (const int cl = tiny_cluster(e, dir, s))
+        if (dir == 0 ? launch_tiny<0>(e, cl, in, out, s) : launch_tiny<1>(e, cl, in, out, s)) return;
     first_stage(e, dir, in, s);
     middle(e, dir, s);
     last_stage(e, dir, in, out, s);

@@ -383,3 +383,23 @@ def test_pair_queue_bitwise(kind, nb):
     with pytest.raises(InvalidInputError):
         eng.pair_queue([rng.standard_normal(eng.cols + 1)], [rng.standard_normal(eng.rows)])
     assert eng.pair_queue([], []) == ([], [])
+
+
+@pytest.mark.parametrize("name,kw", [("twenty_card", {}), ("bench", dict(seed=2, hands=100)),
+                                     ("river_full", dict(seed=1, board="Kc9d7c4d2c", deck=26, tree=3))])
+@pytest.mark.parametrize("tech", ["a", "b"])
+def test_deep_batches_bitwise(name, kw, tech, monkeypatch):
+    """Small grids run the SELL kernels with 16 entries per lane per batch
+    (kr_engine.cu deep_batches): the same storage-order sums as the 8-entry
+    kernels (KR_DEEP_KU=0), bit for bit, on both directions."""
+    p = H.builtin(name, **kw)
+    sp = p.sparsify(tech, True)
+    rng = np.random.default_rng(23)
+    x, y = rng.standard_normal(p.cols), rng.standard_normal(p.rows)
+    monkeypatch.setenv("KR_TINY", "0")
+    deep = CudaEngine(sp)
+    a1, b1 = deep.Ax(x), deep.ATx(y)
+    monkeypatch.setenv("KR_DEEP_KU", "0")
+    plain = CudaEngine(sp)
+    a0, b0 = plain.Ax(x), plain.ATx(y)
+    assert bits_equal(a1, a0) and bits_equal(b1, b0)
