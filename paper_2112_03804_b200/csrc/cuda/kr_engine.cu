@@ -144,24 +144,25 @@ constexpr int kChunk = 256;  // long-row entries staged per warp
 #endif
 constexpr int kU = KR_KU;  // entries per lane per pipeline stage
 
-// COH: the source was written earlier in the same kernel (the fused small-
-// engine product): coherent L2 loads instead of the read-only path.
-template <bool TWO, bool COH = false>
+// COH bit 0 / bit 1: xa / xb was written earlier in the same kernel (the
+// fused small-engine product, behind a cluster barrier's acquire): plain
+// coherent loads (ld.global.ca) instead of the read-only path.
+template <int COH>
+__device__ __forceinline__ double src_load(const double* p) {
+    return COH ? __ldca(p) : __ldg(p);
+}
+template <bool TWO, int COH = 0>
 __device__ __forceinline__ double gather(const double* __restrict__ xa, const double* __restrict__ xb, int32_t split,
                                          int32_t c) {
     KR_DCHECK(c >= 0);
-    if (COH) {
-        if (TWO) return c < split ? __ldcg(xa + c) : __ldcg(xb + (c - split));
-        return __ldcg(xa + c);
-    }
-    if (TWO) return c < split ? __ldg(xa + c) : __ldg(xb + (c - split));
-    return __ldg(xa + c);
+    if (TWO) return c < split ? src_load<COH & 1>(xa + c) : src_load<COH & 2>(xb + (c - split));
+    return src_load<COH & 1>(xa + c);
 }
 
 // One long row per warp (the 32 lanes load and multiply a chunk of kChunk
 // entries, lane 0 adds the chunk's products in storage order while the next
 // chunk's loads are in flight).  Shared by the plain and compressed kernels.
-template <bool TWO, bool COH = false>
+template <bool TWO, int COH = 0>
 __device__ __forceinline__ void spmv_long_row_at(const SellView& A, const double* __restrict__ xa,
                                                  const double* __restrict__ xb, int32_t split, double* __restrict__ y,
                                                  double* P, int lane, int64_t r);
@@ -173,7 +174,7 @@ __device__ __forceinline__ void spmv_long_row(const SellView& A, const double* _
     if (r >= A.nlong) return;
     spmv_long_row_at<TWO>(A, xa, xb, split, y, P, lane, r);
 }
-template <bool TWO, bool COH>
+template <bool TWO, int COH>
 __device__ __forceinline__ void spmv_long_row_at(const SellView& A, const double* __restrict__ xa,
                                                  const double* __restrict__ xb, int32_t split, double* __restrict__ y,
                                                  double* P, int lane, int64_t r) {
@@ -250,7 +251,7 @@ __device__ __forceinline__ void spmv_long_row_at(const SellView& A, const double
 // blocks; matrices whose SELL rows hold at most one entry (U^T of Technique
 // B: one entry per k position) use <1, 8>, a lean variant with twice
 // the resident warps, since their cost is the per-row load latency.
-template <bool TWO, int KU, bool COH = false>
+template <bool TWO, int KU, int COH = 0>
 __device__ __forceinline__ void spmv_slice(const SellView& A, const double* __restrict__ xa,
                                            const double* __restrict__ xb, int32_t split, double* __restrict__ y,
                                            int64_t si, int lane);
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
 
 // One SELL slice (32 rows) by one warp: each lane's row summed in storage
 // order, KU entries per pipeline stage.
-template <bool TWO, int KU, bool COH>
+template <bool TWO, int KU, int COH>
 __device__ __forceinline__ void spmv_slice(const SellView& A, const double* __restrict__ xa,
                                            const double* __restrict__ xb, int32_t split, double* __restrict__ y,
                                            int64_t si, int lane) {
@@ -801,7 +802,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 // barrier (release / acquire) between stages, each warp taking rows, slices
 // and chain slices strided over the cluster's warps.  Every row, slice and
 // chain runs the same device code as the separate kernels, so the result is
-// bitwise theirs; the last stage reads tz through coherent L2 loads (it was
+// bitwise theirs; the last stage reads tz through coherent loads (it was
 // written inside this launch).  For engines whose three launches are
 // latency-bound (a few us of work each), this takes two launch gaps and two
 // grid drains off every product.
@@ -853,12 +854,14 @@ __global__ void __launch_bounds__(32 * kTinyWarps, 1)
                 reinterpret_cast<double(*)[kTinyRows * 32]>(Tb + kTinyRing), bar[w], used);
         cl.sync();
     }
-    // [U | Ahat] over [tz | x]; [Ahat^T | V] over [y | tz]
+    // [U | Ahat] over [tz | x]; [Ahat^T | V] over [y | tz]: tz (written
+    // above) through coherent loads, the input through the read-only path
     const double* xa = DIR == 0 ? tz : in;
     const double* xb = DIR == 0 ? in : tz;
+    constexpr int coh = DIR == 0 ? 1 : 2;
     for (int64_t i = gw; i < A2.nlong + A2.nslices; i += nw) {
-        if (i < A2.nlong) spmv_long_row_at<true, true>(A2, xa, xb, split, out, P[w], lane, i);
-        else spmv_slice<true, kU, true>(A2, xa, xb, split, out, i - A2.nlong, lane);
+        if (i < A2.nlong) spmv_long_row_at<true, coh>(A2, xa, xb, split, out, P[w], lane, i);
+        else spmv_slice<true, kU, coh>(A2, xa, xb, split, out, i - A2.nlong, lane);
     }
 }
 
