@@ -136,25 +136,31 @@ __device__ __forceinline__ double2 smd2(const char* smb, uint32_t off) {
     return *reinterpret_cast<const double2*>(smb + off);
 }
 
-// Stream one lane's vectors of a slice (two loads in flight), calling
-// f(entry) for the 8 entries of each vector in order.
+// Stream one lane's vectors of a slice (KR_KF_DEPTH loads in flight),
+// calling f(entry) for the 8 entries of each vector in order.
+#ifndef KR_KF_DEPTH
+#define KR_KF_DEPTH 2
+#endif
 template <class F>
 __device__ __forceinline__ void kf_stream(const uint4* __restrict__ src, int nv, F&& f) {
+    constexpr int D = KR_KF_DEPTH;
     const uint4 z = make_uint4(0, 0, 0, 0);
-    uint4 c0 = nv > 0 ? __ldg(src) : z;
-    uint4 c1 = nv > 1 ? __ldg(src + 32) : z;
+    uint4 c[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) c[d] = nv > d ? __ldg(src + 32 * d) : z;
     for (int q = 0; q < nv; ++q) {
-        const uint4 c = c0;
-        c0 = c1;
-        c1 = q + 2 < nv ? __ldg(src + 32 * (q + 2)) : z;
-        f(c.x & 0xFFFFu);
-        f(c.x >> 16);
-        f(c.y & 0xFFFFu);
-        f(c.y >> 16);
-        f(c.z & 0xFFFFu);
-        f(c.z >> 16);
-        f(c.w & 0xFFFFu);
-        f(c.w >> 16);
+        const uint4 cur = c[0];
+#pragma unroll
+        for (int d = 0; d + 1 < D; ++d) c[d] = c[d + 1];
+        c[D - 1] = q + D < nv ? __ldg(src + 32 * (q + D)) : z;
+        f(cur.x & 0xFFFFu);
+        f(cur.x >> 16);
+        f(cur.y & 0xFFFFu);
+        f(cur.y >> 16);
+        f(cur.z & 0xFFFFu);
+        f(cur.z >> 16);
+        f(cur.w & 0xFFFFu);
+        f(cur.w >> 16);
     }
 }
 

@@ -1,5 +1,11 @@
 #!/bin/bash
 # scratch batch for one gpurun call (edited per call)
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_tiny_product.py tests/test_gpu_engine.py -x -q -p no:cacheprovider > gpurun_out/tiny3.log 2>&1; echo "rc=$?" >> gpurun_out/tiny3.log
-KR_CUDA_LIB_VARIANT=checked timeout 600 python -m pytest tests/test_gpu_tiny_product.py -x -q -p no:cacheprovider >> gpurun_out/tiny3.log 2>&1; echo "rc=$?" >> gpurun_out/tiny3.log
+{
+for rep in 1 2; do
+for v in "" kfd3 kfd4; do
+  echo "variant=${v:-default} rep=$rep"
+  KR_CUDA_LIB_VARIANT=$v timeout 300 python tools/kf_probe.py 2 3
+done
+done
+} > gpurun_out/kf_depth.log 2>&1
