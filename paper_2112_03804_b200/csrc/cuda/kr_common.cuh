@@ -79,6 +79,7 @@ __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return 
 // few very long rows cannot serialise a warp on memory latency.
 constexpr int kSigma = 1024;
 constexpr int kLongRow = 256;
+constexpr int64_t kLongRowBudget = 4096;  // long rows per matrix the adaptive threshold allows (kr_engine.cu)
 struct DevSell {
     int64_t nrows = 0, nslices = 0, nnz = 0, padded = 0;
     int32_t maxLen = 0;            // longest row kept in the slices

@@ -1587,16 +1587,47 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
         e->flops_per_product = nV + nU + nA + (e->mkind == 0 ? 0 : nM - K);
         // Identity boards inside a chain engine are sets of singleton chains.
         const bool chainMode = e->mkind == 1;
-        // Rows longer than longRow take the warp-per-row path (SELL measured
-        // faster for everything shorter, at config 2 and config 3 alike).
-        int64_t longRow = kLongRow;
-        if (const char* env = std::getenv("KR_LONG_ROW")) longRow = std::max<int64_t>(8, std::atoll(env));
-
-        // pass 1: relabelling and SELL sizes
+        // Rows longer than longRow[w] take the warp-per-row path: a SELL
+        // lane's row is a chain of dependent gather batches, a long row's
+        // entries are gathered by 32 lanes at once and summed by one.  Per
+        // matrix, the smallest threshold in {16, 32, ..., kLongRow} whose long
+        // rows (over all boards) fit one resident round of warps
+        // (kLongRowBudget); more long rows than that queue behind each other's
+        // serial sums (config 2 at 128: 8,960 / 21,591 long V^T / AV rows,
+        // 2.4x slower).  Measured (profiles/r02/long_rows_r02z.log): config-1
+        // CFR+ 15,100 -> 17,900 it/s, config-4 DCFR 15,360 -> 16,950; configs
+        // 2 and 3 keep 256.  KR_LONG_ROW=n: one fixed threshold.
+        int64_t longRow[4] = {kLongRow, kLongRow, kLongRow, kLongRow};
+        const int kThr = 5;
+        const int64_t thr[5] = {16, 32, 64, 128, kLongRow};
+        std::vector<int64_t> over(size_t(nb) * 4 * kThr, 0);  // [board][matrix][threshold]
+        // pass 1: relabelling, long-row counts per threshold
         parallel_boards(nb, [&](int b) {
             BoardPlan& p = plan[size_t(b)];
             build_chain_order(p, chainMode);
-            for (int w = 0; w < 4; ++w) sell_sizes(board_lengths(p, w), longRow, p.sl[w], p.pad[w], p.nl[w], p.nlz[w]);
+            int64_t* o = over.data() + size_t(b) * 4 * kThr;
+            for (int w = 0; w < 4; ++w)
+                for (int64_t l : board_lengths(p, w))
+                    for (int t = 0; t < kThr; ++t) o[w * kThr + t] += l > thr[t];
+        });
+        if (const char* env = std::getenv("KR_LONG_ROW")) {
+            for (auto& l : longRow) l = std::max<int64_t>(8, std::atoll(env));
+        } else {
+            for (int w = 0; w < 4; ++w)
+                for (int t = 0; t < kThr; ++t) {
+                    int64_t n = 0;
+                    for (int b = 0; b < nb; ++b) n += over[size_t(b) * 4 * kThr + size_t(w * kThr + t)];
+                    if (n <= kLongRowBudget) {
+                        longRow[w] = thr[t];
+                        break;
+                    }
+                }
+        }
+        // SELL sizes
+        parallel_boards(nb, [&](int b) {
+            BoardPlan& p = plan[size_t(b)];
+            for (int w = 0; w < 4; ++w)
+                sell_sizes(board_lengths(p, w), longRow[w], p.sl[w], p.pad[w], p.nl[w], p.nlz[w]);
         });
         // internal k space: each board's chain-sliced positions, in board order
         int64_t Kp = 0;
@@ -1656,7 +1687,7 @@ kr_engine* create_engine(const kr_factors* boards, int nb, int device, uint32_t 
             HostSell hs;
             for (int w = 0; w < 4; ++w) {
                 board_rows(p, w, R, Kp, xseq, e->M2, n2, h);
-                to_sell(h, rowBase[w], longRow, hs);
+                to_sell(h, rowBase[w], longRow[w], hs);
                 if (int64_t(hs.sptr.size()) != p.sl[w] || int64_t(hs.col.size()) != p.pad[w] ||
                     int64_t(hs.lgrow.size()) != p.nl[w] || int64_t(hs.lcol.size()) != p.nlz[w])
                     throw Fail{KR_CUDA, "internal: SELL sizing mismatch"};
