@@ -397,6 +397,7 @@ struct BoardHost {
     int32_t* wcount[4] = {nullptr, nullptr, nullptr, nullptr};
     int32_t* lcount[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<int64_t> wslice[4], wlong[4];
+    std::vector<int32_t> hlen[4];  // row lengths (host copy)
     int64_t slices[4] = {0, 0, 0, 0}, nlong[4] = {0, 0, 0, 0};
     int64_t slOff[4] = {0, 0, 0, 0}, nlOff[4] = {0, 0, 0, 0};
     int64_t nnz[4] = {0, 0, 0, 0};
@@ -565,6 +566,33 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
                 else if (w == 2) k_len<2><<<g, 128>>>(B, R, H.len[w]);
                 else k_len<3><<<g, 128>>>(B, R, H.len[w]);
                 KR_CK_LAUNCH();
+                H.hlen[w] = down(H.len[w], R);
+            }
+        }
+        // the long-row threshold per matrix, as the host-built engine picks it
+        // (kr_engine.cu): the smallest of 16 .. kLongRow whose long rows over
+        // all boards number at most kLongRowBudget (KR_LONG_ROW: fixed)
+        int longRowW[4] = {longRow, longRow, longRow, longRow};
+        if (!std::getenv("KR_LONG_ROW")) {
+            const int thr[5] = {16, 32, 64, 128, kLongRow};
+            for (int w = 0; w < 4; ++w)
+                for (int t : thr) {
+                    int64_t n = 0;
+                    for (int b = 0; b < nb; ++b)
+                        for (int32_t v : bh[size_t(b)].hlen[w]) n += v > t;
+                    if (n <= kLongRowBudget) {
+                        longRowW[w] = t;
+                        break;
+                    }
+                }
+        }
+        for (int b = 0; b < nb; ++b) {
+            BoardHost& H = bh[size_t(b)];
+            for (int w = 0; w < 4; ++w) {
+                const int64_t R = H.R[w];
+                const int longRow = longRowW[w];
+                const int64_t nw = (R + kWin - 1) / kWin;
+                if (R == 0) continue;
                 k_window_sort<<<unsigned(nw), kWin / 2>>>(H.len[w], R, longRow, H.perm[w], H.wcount[w], H.lcount[w]);
                 KR_CK_LAUNCH();
                 const auto wc = down(H.wcount[w], nw), lc = down(H.lcount[w], nw);
@@ -576,11 +604,11 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
                 }
                 H.slices[w] = H.wslice[w].back();
                 H.nlong[w] = H.wlong[w].back();
-                const auto L = down(H.len[w], R);
-                for (int32_t v : L) {
+                for (int32_t v : H.hlen[w]) {
                     H.nnz[w] += v;
                     if (v <= longRow) H.maxLen[w] = std::max(H.maxLen[w], v);
                 }
+                std::vector<int32_t>().swap(H.hlen[w]);
             }
             for (int w = 0; w < 4; ++w) {
                 H.slOff[w] = tsl[w];
@@ -626,7 +654,7 @@ kr_engine* create_engine_device_b(const kr_kron_board* boards, int nb, int devic
                         keep.push_back(vtB);
                         KR_CK(cudaMemcpy(vtB, &H.dev, sizeof(BoardDev), cudaMemcpyHostToDevice));
                     }
-                    k_slots<<<unsigned(nw), 256>>>(H.len[w], H.perm[w], H.wcount[w], dws, dwl, R, longRow,
+                    k_slots<<<unsigned(nw), 256>>>(H.len[w], H.perm[w], H.wcount[w], dws, dwl, R, longRowW[w],
                                                   w == 1 ? H.dev.rowOff : (w == 3 ? H.dev.colOff : H.dev.kOff),
                                                   H.slOff[w], H.nlOff[w], slot, S.lane_row, S.lane_len, wd,
                                                   S.long_row, ll, vtB);
