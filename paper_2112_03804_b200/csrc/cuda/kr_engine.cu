@@ -248,9 +248,9 @@ __device__ __forceinline__ void spmv_long_row_at(const SellView& A, const double
 // register pipeline (loads of stage g+1 in flight while stage g gathers and
 // accumulates).
 // KU / MINB: entries per lane per pipeline stage and minimum resident
-// blocks; matrices whose SELL rows hold at most one entry (U^T of Technique
-// B: one entry per k position) use <1, 8>, a lean variant with twice
-// the resident warps, since their cost is the per-row load latency.
+// blocks.  Matrices whose SELL rows hold at most one entry (U^T of Technique
+// B: one entry per k position) take k_spmv_lean instead: their cost is the
+// per-row load latency.
 template <bool TWO, int KU, int COH = 0>
 __device__ __forceinline__ void spmv_slice(const SellView& A, const double* __restrict__ xa,
                                            const double* __restrict__ xb, int32_t split, double* __restrict__ y,
@@ -272,6 +272,63 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB)
     const int64_t si = (int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w;
     if (si >= A.nslices) return;
     spmv_slice<TWO, KU>(A, xa, xb, split, y, si, lane);
+}
+
+// Matrices whose SELL rows hold at most one entry (U^T of Technique B): no
+// pipeline, one load round per lane (row metadata, the entry, the gather),
+// y[row] = 0.0 + val * x[col] (0.0 for an empty row): k_spmv's sum for one
+// entry, bit for bit.  Long rows as in k_spmv.  KR_LEAN_SLICES: slices per
+// warp, all in flight together (config 3 U^T: 37.8 us at 1, 43.5 at 4,
+// 43.9 at 8; the <1, 8> k_spmv instance it replaces: 41-43, k_spmv<false>:
+// 49; profiles/r02/lean_ut_r02z.log).
+#ifndef KR_LEAN_SLICES
+#define KR_LEAN_SLICES 1
+#endif
+constexpr int kLeanSlices = KR_LEAN_SLICES;
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 8)
+    k_spmv_lean(SellView A, const double* __restrict__ xa, double* __restrict__ y) {
+    krb::pdl_entry();
+    __shared__ double P[kWarpsPerBlock][kChunk];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t longBlocks = (A.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blockIdx.x < longBlocks) {
+        spmv_long_row<false>(A, xa, nullptr, 0, y, P[w], lane, w);
+        return;
+    }
+    const int64_t si0 = ((int64_t(blockIdx.x) - longBlocks) * kWarpsPerBlock + w) * kLeanSlices;
+    int32_t row[kLeanSlices], len[kLeanSlices], c[kLeanSlices];
+    int64_t base[kLeanSlices];
+    double v[kLeanSlices], x[kLeanSlices];
+#pragma unroll
+    for (int u = 0; u < kLeanSlices; ++u) {
+        row[u] = -1;
+        len[u] = 0;
+        const int64_t si = si0 + u;
+        if (si < A.nslices) {
+            const int64_t sl = A.order ? int64_t(A.order[si]) : si;
+            base[u] = A.slice_ptr[sl] + lane;
+            len[u] = A.lane_len[sl * 32 + lane];
+            row[u] = A.lane_row[sl * 32 + lane];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kLeanSlices; ++u)
+        if (len[u] > 0) {
+            c[u] = __ldcs(A.col + base[u]);
+            v[u] = __ldcs(A.val + base[u]);
+        }
+#pragma unroll
+    for (int u = 0; u < kLeanSlices; ++u)
+        if (len[u] > 0) {
+            KR_DCHECK(len[u] == 1 && c[u] < A.nsrc);
+            x[u] = gather<false>(xa, nullptr, 0, c[u]);
+        }
+#pragma unroll
+    for (int u = 0; u < kLeanSlices; ++u) {
+        KR_DCHECK(row[u] < A.ndst);
+        if (row[u] >= 0) y[row[u]] = len[u] > 0 ? 0.0 + v[u] * x[u] : 0.0;
+    }
 }
 
 // One SELL slice (32 rows) by one warp: each lane's row summed in storage
@@ -1998,8 +2055,11 @@ void launch_sell(kr_engine* e, int which, const krb::DevSell& A, const double* x
         else if (A.codedSeg == 0)
             krb::launch(k_spmvc<true, 0>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
         else krb::launch(k_spmvc<true, 1>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, c, xa, xb, int32_t(split), y);
-    } else if (A.maxLen <= 1 && e->lean && !xb)
-        krb::launch(k_spmv<false, 1, 8>, unsigned(blocks), 32 * kWarpsPerBlock, 0, s, v, xa, nullptr, 0, y);
+    } else if (A.maxLen <= 1 && e->lean && !xb) {
+        const int64_t lb = (l1 - l0 + kWarpsPerBlock - 1) / kWarpsPerBlock +
+                           (s1 - s0 + kWarpsPerBlock * kLeanSlices - 1) / (kWarpsPerBlock * kLeanSlices);
+        krb::launch(k_spmv_lean, unsigned(lb), 32 * kWarpsPerBlock, 0, s, v, xa, y);
+    }
     else if (deep_batches(blocks, A.maxLen)) {
         // small grids: each lane's row is a chain of dependent gather
         // batches, so twice the entries per batch halves it (same order)
@@ -2139,7 +2199,7 @@ void set_carveout() {
     auto set = [](const void* f) { KR_CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct)); };
     set(reinterpret_cast<const void*>(k_spmv<true>));
     set(reinterpret_cast<const void*>(k_spmv<false>));
-    set(reinterpret_cast<const void*>(k_spmv<false, 1, 8>));
+    set(reinterpret_cast<const void*>(k_spmv_lean));
     set(reinterpret_cast<const void*>(k_seq_major_tile));
     set(reinterpret_cast<const void*>(k_seq_major));
     set(reinterpret_cast<const void*>(k_chain_tma<1>));
