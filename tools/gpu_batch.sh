@@ -1,6 +1,10 @@
 #!/bin/bash
 # scratch batch for one gpurun call (edited per call)
 mkdir -p gpurun_out
-timeout 300 python tools/small_engine_ncu.py > gpurun_out/se_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_spmv|k_tiny|k_chain" --launch-count 14 -o gpurun_out/small_engines -f python tools/small_engine_ncu.py > gpurun_out/se_ncu.log 2>&1
-echo "rc=$?" >> gpurun_out/se_ncu.log
+{
+for rep in 1 2; do
+echo "default rep=$rep"; timeout 300 python tools/pair_probe.py
+echo "deep-all rep=$rep"; KR_DEEP_BLOCKS=1000000000 timeout 300 python tools/pair_probe.py
+echo "nodeep rep=$rep"; KR_DEEP_KU=0 timeout 300 python tools/pair_probe.py
+done
+} > gpurun_out/deep_c3.log 2>&1
