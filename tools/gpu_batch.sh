@@ -3,8 +3,6 @@
 mkdir -p gpurun_out
 {
 for rep in 1 2; do
-echo "default rep=$rep"; timeout 300 python tools/pair_probe.py
-echo "deep-all rep=$rep"; KR_DEEP_BLOCKS=1000000000 timeout 300 python tools/pair_probe.py
-echo "nodeep rep=$rep"; KR_DEEP_KU=0 timeout 300 python tools/pair_probe.py
+for v in "" ku6 ku10 ku12; do echo "variant=${v:-ku8} rep=$rep"; KR_CUDA_LIB_VARIANT=$v timeout 300 python tools/pair_probe.py; done
 done
-} > gpurun_out/deep_c3.log 2>&1
+} > gpurun_out/ku_c3.log 2>&1
